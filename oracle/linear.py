@@ -1,0 +1,138 @@
+"""The compensated quantized linear and its compositions (oracle; test infrastructure only).
+
+Definition (north_star; §4.1 "Y = XŴ + XΔW ≈ XŴ + (XA_r)B_r"
+"(X·A)·B, evaluated in that association order"):
+
+    y* = Ŵ·x + U[:, :r] · (V[:r, :] · x)            (float64, associated as (V·x) then U)
+
+with Ŵ = s·(q − z) (oracle.quant.dequant) and every bf16 input upcast exactly.
+
+Windows (App. A.1.3): members sharing one input are evaluated on the
+same x and their outputs concatenated in member order (QKV = q,k,v; UPGATE = up,gate).
+
+Stack (reading R9, attention is out of scope and
+replaced by the identity on the q-part): per layer
+    qkv = QKV(h); a = bf16(q-part); h1 = bf16(h + O(a));
+    gu = UPGATE(h1); m = bf16(silu(gate) ⊙ up); h2 = bf16(h1 + DOWN(m)).
+MoE ("Y_MoE = Σ_e g_e E_e(X)"): per activated expert e over its
+routed tokens: m_e = bf16(silu(gate_e) ⊙ up_e), y[t] += g_{t,e} · DOWN_e(m_e)[t].
+bf16 rounding points are part of the definition (the activations a model passes
+between linears are bf16); both the oracle and the kernels round there (RNE).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .packing import unpack_codes, bf16_to_f64
+from .quant import dequant_abi
+
+
+def deq_weight(codes, scales, zeros, K: int, bits: int, group: int) -> np.ndarray:
+    """Ŵ in float64 from the canonical C-ABI formats."""
+    q = unpack_codes(codes, K, bits)
+    return dequant_abi(q, scales, zeros, group)
+
+
+def compensated_product(W_hat: np.ndarray, U: np.ndarray, V: np.ndarray, r: int,
+                        x: np.ndarray) -> np.ndarray:
+    """y*[b, :] = Ŵ·x_b + U[:, :r]·(V[:r, :]·x_b); x is float64 [B, K]; returns [B, N]."""
+    x = np.asarray(x, dtype=np.float64)
+    y = x @ W_hat.T                                   # Ŵ·x for every row b
+    if r > 0:
+        t = x @ V[:r, :].T                            # t = V[:r,:]·x   -> [B, r]
+        y = y + t @ U[:, :r].T                        # + U[:, :r]·t    -> [B, N]
+    return y
+
+
+def compensated_linear(case: dict, r: int, x_bits=None, rows=None) -> np.ndarray:
+    """Oracle for one matrix given a synth.linear_case-style dict (ABI formats).
+
+    ``rows`` (optional index array) restricts the output rows (sampled checks at full size).
+    """
+    K, bits, group = case["K"], case["bits"], case["group"]
+    codes, scales, zeros, U = case["codes"], case["scales"], case["zeros"], case["U"]
+    if rows is not None:
+        codes, scales, zeros, U = codes[rows], scales[rows], zeros[rows], U[rows]
+    W_hat = deq_weight(codes, scales, zeros, K, bits, group)
+    x = bf16_to_f64(case["x"] if x_bits is None else x_bits)
+    return compensated_product(W_hat, bf16_to_f64(U), bf16_to_f64(case["V"]), r, x)
+
+
+def window_linear(members: list, ranks: list, x_bits) -> np.ndarray:
+    """Members sharing x (one compensation window): concatenate outputs in member order."""
+    return np.concatenate([compensated_linear(m, r, x_bits=x_bits) for m, r in zip(members, ranks)],
+                          axis=1)
+
+
+def _round_bf16(a: np.ndarray) -> np.ndarray:
+    """float64 -> nearest bf16 value (round half to even on the float64 value), as float64.
+
+    v = m·2^e with 0.5 <= |m| < 1; bf16 keeps 8 significant bits, so the value is
+    round_half_even(m·256)/256·2^e.  (Normal range only; the activations here are
+    far from bf16 under/overflow.)"""
+    a = np.asarray(a, dtype=np.float64)
+    m, e = np.frexp(a)
+    sm = m * 256.0
+    fl = np.floor(sm)
+    d = sm - fl
+    odd = np.mod(fl, 2.0) != 0.0
+    up = (d > 0.5) | ((d == 0.5) & odd)
+    out = np.ldexp((fl + up) / 256.0, e)
+    return np.where((a == 0.0) | ~np.isfinite(a), a, out)
+
+
+def round_bf16(a: np.ndarray) -> np.ndarray:
+    return _round_bf16(a)
+
+
+def silu(v: np.ndarray) -> np.ndarray:
+    v = np.asarray(v, dtype=np.float64)
+    return v / (1.0 + np.exp(-v))
+
+
+def stack_forward(layers: list, ranks: list, x_bits) -> np.ndarray:
+    """Oracle for the decode stack (C2/C5).
+
+    layers[l] = dict(qkv=[q, k, v], o=[o], upgate=[up, gate], down=[down]) of linear_case dicts;
+    ranks[l] = dict with the same keys holding per-member ranks.
+    Returns the final hidden state h (float64 [B, d], bf16-valued).
+    """
+    h = bf16_to_f64(x_bits)
+    for L, R in zip(layers, ranks):
+        qkv = np.concatenate([_lin(m, r, h) for m, r in zip(L["qkv"], R["qkv"])], axis=1)
+        d = L["o"][0]["K"]
+        a = round_bf16(qkv[:, :d])
+        h1 = round_bf16(h + _lin(L["o"][0], R["o"][0], a))
+        up = _lin(L["upgate"][0], R["upgate"][0], h1)
+        gate = _lin(L["upgate"][1], R["upgate"][1], h1)
+        m = round_bf16(silu(gate) * up)
+        h = round_bf16(h1 + _lin(L["down"][0], R["down"][0], m))
+    return h
+
+
+def _lin(case: dict, r: int, x_f64: np.ndarray) -> np.ndarray:
+    W_hat = deq_weight(case["codes"], case["scales"], case["zeros"], case["K"], case["bits"], case["group"])
+    return compensated_product(W_hat, bf16_to_f64(case["U"]), bf16_to_f64(case["V"]), r, x_f64)
+
+
+def moe_forward(experts: list, ranks: list, x_bits, topk_idx, topk_gate) -> np.ndarray:
+    """Oracle for the grouped MoE expert path (C3).
+
+    experts[e] = dict(up=case, gate=case, down=case); ranks[e] = dict(up=r, gate=r, down=r).
+    x_bits [T, d] bf16; topk_idx int [T, k]; topk_gate float32 [T, k] (used as given, as fp32 values).
+    y[t] = Σ_{j} g[t, j] · DOWN_e(bf16(silu(GATE_e(x_t)) ⊙ UP_e(x_t))),  e = topk_idx[t, j].
+    """
+    x = bf16_to_f64(x_bits)
+    T = x.shape[0]
+    d = experts[0]["down"]["N"]
+    y = np.zeros((T, d), dtype=np.float64)
+    for e in sorted(set(int(v) for v in np.asarray(topk_idx).reshape(-1))):
+        toks, slots = np.nonzero(np.asarray(topk_idx) == e)
+        xe = x[toks]
+        up = _lin(experts[e]["up"], ranks[e]["up"], xe)
+        gate = _lin(experts[e]["gate"], ranks[e]["gate"], xe)
+        m = round_bf16(silu(gate) * up)
+        de = _lin(experts[e]["down"], ranks[e]["down"], m)
+        g = np.asarray(topk_gate, dtype=np.float32)[toks, slots].astype(np.float64)
+        y[toks] += g[:, None] * de
+    return y

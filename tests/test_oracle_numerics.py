@@ -1,0 +1,220 @@
+"""Pins for oracle.packing / oracle.quant / oracle.factors / oracle.linear.
+
+Each test pins the oracle to something other than itself: hand-packed words, the
+SPEC's printed worked examples (tests/golden), closed forms (Eckart–Young), exact
+identities (rank 0, full rank), or an independent brute-force construction.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import packing, quant, factors, linear
+
+
+# ------------------------------------------------------------------ unpack (c1)
+def _pack_bigint(q, bits):
+    """Independent construction of the canonical stream: Python big int Σ q_k << (b·k)."""
+    N, K = q.shape
+    words = K * bits // 32
+    out = np.zeros((N, words), dtype=np.uint32)
+    for n in range(N):
+        v = 0
+        for k in range(K):
+            v |= int(q[n, k]) << (bits * k)
+        for w in range(words):
+            out[n, w] = (v >> (32 * w)) & 0xFFFFFFFF
+    return out
+
+
+def test_unpack_hand_words_4bit():
+    w = np.array([[0x76543210, 0xFEDCBA98]], dtype=np.uint32)
+    assert packing.unpack_codes(w, 16, 4).tolist() == [list(range(16))]
+
+
+def test_unpack_hand_words_2bit():
+    # 0xE4 = 0b11_10_01_00 -> 0,1,2,3 then zeros
+    w = np.array([[0x000000E4]], dtype=np.uint32)
+    assert packing.unpack_codes(w, 16, 2).tolist() == [[0, 1, 2, 3] + [0] * 12]
+
+
+def test_unpack_hand_words_3bit_straddle():
+    # q[0] = 1 (bits 0-2); q[10] = 5 = 0b101 occupies bits 30,31,32: bit30=1, bit31=0, bit32=1
+    w = np.array([[0x40000001, 0x00000001, 0x00000000]], dtype=np.uint32)
+    q = packing.unpack_codes(w, 32, 3)[0]
+    exp = [0] * 32
+    exp[0], exp[10] = 1, 5
+    assert q.tolist() == exp
+
+
+@pytest.mark.parametrize("bits", [2, 3, 4, 8])
+def test_unpack_inverts_bigint_pack(bits):
+    g = synth.rng(bits)
+    q = g.integers(0, 1 << bits, size=(5, 256))
+    assert np.array_equal(packing.unpack_codes(_pack_bigint(q, bits), 256, bits), q)
+
+
+def test_bf16_decode_exact():
+    assert packing.bf16_to_f64(np.array([0x3F80, 0xC000, 0x3DCD], dtype=np.uint16)).tolist() == \
+        [1.0, -2.0, float(np.float32(np.uint32(0x3DCD0000).view(np.float32)))]
+
+
+# ------------------------------------------------------------------ quantiser / dequant (c2, c3)
+def test_rtn_spec_examples(golden):
+    e4 = golden["rtn_4bit"]
+    c, s = quant.rtn_quantize(np.array([e4["w"]]), 4, 2)
+    assert c.tolist() == [e4["codes"]] and abs(s[0, 0] - e4["scale"]) < 1e-15
+    assert np.allclose(quant.rtn_dequantize(c, s, 2), [e4["deq"]], atol=1e-15)
+    e3 = golden["rtn_3bit"]
+    c, s = quant.rtn_quantize(np.array([e3["w"]]), 3, 2)
+    assert c.tolist() == [e3["codes"]] and abs(s[0, 0] - e3["scale"]) < 1e-15
+    res = np.array([e3["w"]]) - quant.rtn_dequantize(c, s, 2)
+    assert np.allclose(res, [e3["residual"]], atol=e3["residual_tol"])
+
+
+def test_rtn_zero_group_and_rounding():
+    c, s = quant.rtn_quantize(np.zeros((2, 4)), 4, 4)
+    assert (c == 0).all() and (s == 1.0).all()
+    assert quant.round_half_away(np.array([2.5, -2.5, 0.5, 1.49])).tolist() == [3.0, -3.0, 1.0, 1.0]
+
+
+@pytest.mark.parametrize("bits", [2, 3, 4])
+def test_half_step_bound_tight(bits):
+    # |W - Ŵ| <= scale/2 elementwise; tight (ratio -> 1) on random weights
+    w = synth.rng(10 + bits).standard_normal((64, 256)) * 0.02
+    c, s = quant.rtn_quantize(w, bits, 128)
+    res = np.abs(w - quant.rtn_dequantize(c, s, 128))
+    half = np.repeat(s, 128, axis=1) / 2
+    ratio = (res / half).max()
+    assert ratio <= 1.0 + 1e-12 and ratio > 0.98
+    # S:149 idempotence of quantize∘dequantize on codes
+    c2, _ = quant.rtn_quantize(quant.rtn_dequantize(c, s, 128), bits, 128)
+    assert np.array_equal(c, c2)
+
+
+def test_dequant_hand_group():
+    q = np.arange(16)[None, :]
+    W = quant.dequant(q, np.array([[0.5, 2.0]]), np.array([[8, 3]]), 8)
+    exp = [0.5 * (k - 8) for k in range(8)] + [2.0 * (k - 3) for k in range(8, 16)]
+    assert W[0].tolist() == exp
+
+
+# ------------------------------------------------------------------ factors (c4)
+def test_eckart_young_diag(golden):
+    for key in ("eckart_young_r1", "eckart_young_r2"):
+        e = golden[key]
+        M = np.diag(np.array(e["diag"], dtype=np.float64))
+        U, V, _ = factors.svd_factors(M, e["r"])
+        assert abs(factors.frobenius_sq(M - U @ V) - e["err_sq"]) < 1e-12
+
+
+def test_eckart_young_random_and_monotone():
+    # SPEC acceptance 1: ||ΔW - U_r V_r||² = Σ_{j>r} σ_j², and monotone in r
+    for seed in range(10):
+        M = synth.rng(100 + seed).standard_normal((64, 64))
+        prev = np.inf
+        for r in (0, 8, 16, 32, 64):
+            U, V, sig = factors.svd_factors(M, r)
+            err = factors.frobenius_sq(M - U @ V)
+            tail = float(np.sum(sig[r:] ** 2))
+            assert abs(err - tail) <= 1e-9 * max(1.0, factors.frobenius_sq(M))
+            assert err <= prev + 1e-12
+            prev = err
+
+
+@pytest.mark.parametrize("bits", [2, 3, 4])
+def test_full_rank_reconstructs_W(bits):
+    # north_star: "exact reconstruction of W when the error SVD is kept at full rank"
+    W = synth.rng(7).standard_normal((96, 128)) * 0.02
+    c, s = quant.rtn_quantize(W, bits, 128)
+    W_hat = quant.rtn_dequantize(c, s, 128)
+    U, V, _ = factors.svd_factors(W - W_hat, 96)
+    assert np.abs(W_hat + U @ V - W).max() <= 1e-14 * 96
+
+
+def test_rank_prefix_and_sign_convention():
+    M = synth.rng(3).standard_normal((40, 30))
+    U30, V30, _ = factors.svd_factors(M, 30)
+    U8, V8, _ = factors.svd_factors(M, 8)
+    assert np.array_equal(U30[:, :8], U8) and np.array_equal(V30[:8], V8)
+    for j in range(8):
+        nz = np.flatnonzero(U8[:, j])
+        assert U8[nz[0], j] > 0
+    with pytest.raises(ValueError):
+        factors.svd_factors(M, 31)
+
+
+# ------------------------------------------------------------------ compensated product (c5)
+def _brute_linear(case, r):
+    """Element-by-element construction from the definition, independent of the
+    vectorised oracle: per (b, n) a Python loop over k, extracting each code from a
+    Python big-int stream."""
+    N, K, bits, g = case["N"], case["K"], case["bits"], case["group"]
+    f = lambda u16: float(np.uint32(int(u16) << 16).view(np.float32))
+    out = np.zeros((case["B"], N))
+    for n in range(N):
+        stream = 0
+        for w in range(K * bits // 32):
+            stream |= int(case["codes"][n, w]) << (32 * w)
+        for b in range(case["B"]):
+            acc = 0.0
+            for k in range(K):
+                q = (stream >> (bits * k)) & ((1 << bits) - 1)
+                acc += f(case["scales"][n, k // g]) * (q - int(case["zeros"][n, k // g])) * f(case["x"][b, k])
+            t = [sum(f(case["V"][j, k]) * f(case["x"][b, k]) for k in range(K)) for j in range(r)]
+            acc += sum(f(case["U"][n, j]) * t[j] for j in range(r))
+            out[b, n] = acc
+    return out
+
+
+@pytest.mark.parametrize("bits,zeros", [(4, "sym"), (3, "asym"), (2, "asym")])
+def test_compensated_linear_matches_brute_force(bits, zeros):
+    case = synth.linear_case(5, N=6, K=256, bits=bits, group=128, r_stored=16, B=2, zeros=zeros)
+    for r in (0, 8, 16):
+        y = linear.compensated_linear(case, r)
+        yb = _brute_linear(case, r)
+        assert np.abs(y - yb).max() <= 1e-12 * max(1.0, np.abs(yb).max())
+
+
+def test_rank0_equals_plain_quantized_product():
+    # S:226 / S:730: rank 0 equals the plain quantised product exactly
+    case = synth.linear_case(1, N=64, K=256, bits=4, r_stored=16, B=3)
+    W_hat = linear.deq_weight(case["codes"], case["scales"], case["zeros"], 256, 4, 128)
+    x = packing.bf16_to_f64(case["x"])
+    assert np.array_equal(linear.compensated_linear(case, 0), x @ W_hat.T)
+
+
+def test_full_rank_factors_give_W_x_and_association():
+    # full-rank factors -> X·ΔW;  S:231: (Vx)U == x(UV) (association equivalence)
+    W = synth.rng(11).standard_normal((48, 128)) * 0.02
+    c, s = quant.rtn_quantize(W, 3, 128)
+    W_hat = quant.rtn_dequantize(c, s, 128)
+    U, V, _ = factors.svd_factors(W - W_hat, 48)
+    x = synth.rng(12).standard_normal((4, 128))
+    y = linear.compensated_product(W_hat, U, V, 48, x)
+    assert np.abs(y - x @ W.T).max() <= 1e-12
+    assert np.abs(linear.compensated_product(W_hat, U, V, 16, x) - x @ (W_hat + U[:, :16] @ V[:16]).T).max() <= 1e-12
+
+
+def test_round_bf16_matches_fp32_route():
+    # bf16 RNE of float64 values that are exactly float32-representable equals the
+    # classic fp32 bit trick (independent construction)
+    a = synth.rng(2).standard_normal(10000).astype(np.float32).astype(np.float64)
+    r = linear.round_bf16(a)
+    bits = packing.f64_to_bf16_bits_rne(a)
+    assert np.array_equal(r, packing.bf16_to_f64(bits))
+    assert linear.round_bf16(np.array([1.0 + 2.0 ** -8]))[0] == 1.0          # tie -> even
+    assert linear.round_bf16(np.array([1.0 + 3 * 2.0 ** -8]))[0] == 1.0 + 2.0 ** -6
+
+
+def test_moe_single_expert_equals_dense():
+    # SPEC toymodel example: MoE with one expert, g = 1 == dense FFN
+    d, f = 128, 128
+    up = synth.linear_case(20, f, d, 3, 128, 16, 1, "asym")
+    gate = synth.linear_case(21, f, d, 3, 128, 16, 1, "asym")
+    down = synth.linear_case(22, d, f, 3, 128, 16, 1, "asym")
+    x = synth.activations(23, 5, d)
+    y = linear.moe_forward([dict(up=up, gate=gate, down=down)], [dict(up=8, gate=0, down=16)],
+                           x, np.zeros((5, 1), np.int32), np.ones((5, 1), np.float32))
+    xf = packing.bf16_to_f64(x)
+    m = linear.round_bf16(linear.silu(linear._lin(gate, 0, xf)) * linear._lin(up, 8, xf))
+    assert np.array_equal(y, linear._lin(down, 16, m))
