@@ -1,0 +1,161 @@
+/* hcinfer.h — C-ABI of the B200-native HCInfer compensated quantized linear.
+ *
+ * The library evaluates, per weight matrix, the error-compensated quantized linear of
+ * HCInfer (arXiv 2605.05819), §4.1:
+ *
+ *     y = deq(W_q)·x + U[:, :r]·(V[:r, :]·x),     deq(W_q)[n,k] = s[n,k/g]·(q[n,k] − z[n,k/g])
+ *
+ * at the rank r chosen by the sensitivity-aware dynamic rank allocation of §4.3 /
+ * Appendix B.1.  Matrices that share an input run as one
+ * "compensation window" launch (App. A.1.3): QKV, O, UPGATE, DOWN.
+ *
+ * Conventions (all entry points):
+ *   - Every function returns an hc_status; no C++ exception crosses the ABI.  On error
+ *     hc_last_error() returns a thread-local, NUL-terminated message (valid until the
+ *     next call on that thread).  Status codes mirror SPEC S:713 exit codes.
+ *   - "device" pointers are CUDA global-memory pointers on the context's device.
+ *     "stream" is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Layouts are row-major, little-endian.  bf16 values travel as uint16 bit patterns.
+ *   - There is no CPU fallback: every compute entry point runs hand-written sm_100a
+ *     kernels and fails with HC_ERR_RUNTIME when no suitable GPU is present.
+ */
+#ifndef HCINFER_H
+#define HCINFER_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HC_OK = 0,
+  HC_ERR_CONFIG = 2,   /* invalid argument / shape / bit width / rank */
+  HC_ERR_STATE = 3,    /* unknown layer/window, use before load, missing communicator    */
+  HC_ERR_NUMERIC = 4,  /* non-finite or negative sensitivity, non-normalised gates */
+  HC_ERR_RUNTIME = 5   /* CUDA / NCCL failure, no sm_100 device                            */
+} hc_status;
+
+typedef enum { HC_WIN_QKV = 0, HC_WIN_O = 1, HC_WIN_UPGATE = 2, HC_WIN_DOWN = 3 } hc_window_kind;
+typedef enum { HC_OUT_F32 = 0, HC_OUT_BF16 = 1 } hc_out_dtype;
+
+const char* hc_version(void);
+const char* hc_last_error(void);
+
+/* =====================================================================================
+ * Rank allocation (host only, pure, deterministic, re-entrant).  PAPER.md App. B.1.
+ * ===================================================================================== */
+
+/* One weight matrix's allocation inputs.  Windows are keyed by (layer, window_kind);
+ * sums over a window run over its members in the order they appear in the array. */
+typedef struct {
+  int32_t layer;          /* 0 <= layer < budget->n_layers                                 */
+  int32_t window_kind;    /* hc_window_kind                                                */
+  int32_t slot;           /* member slot inside the window (q,k,v | o | up,gate | down)     */
+  int32_t expert;         /* MoE expert id, -1 for dense                                   */
+  int32_t n_sigma;        /* length of sigma, or 0                                         */
+  const double* sigma;    /* singular values of ΔW, non-increasing; NULL -> use phi */
+  double phi;             /* salience φ_i when sigma == NULL                               */
+  int32_t n_salient;      /* |S_i| when sigma == NULL (two_stage_mode 1 only)              */
+  int32_t n_total;        /* |S_i| + |R_i| when sigma == NULL                              */
+  double D_matrix;        /* D_i = KL(P || Q_i) >= 0, an input                 */
+  double gate;            /* routing weight g_e of this expert (MoE), else ignored         */
+} hc_sens;
+
+typedef struct {
+  int32_t n_layers;
+  const double* D_layer;  /* [n_layers], D_ℓ >= 0                             */
+  int32_t top_k_layers;   /* K of the top-K layer set 𝒯, 1 <= K <= n_layers       */
+  double tau;             /* salience threshold τ (0.01)                            */
+  int32_t k0;             /* minimum non-zero rank 2^k0 (8 => k0 = 3)           */
+  double r_std[4];        /* per-window-kind standard rank r_std, the budget  */
+  int32_t two_stage_mode; /* 0: per-matrix reading; 1: pooled literal reading      */
+  int32_t moe_k;          /* activated experts per MoE window (𝒢 = k·g_e); 0 = dense */
+} hc_budget;
+
+/* φ -> 𝒱 = Norm_W(φ) -> 𝒮_i = Norm_W(D) -> 𝒮_ℓ
+ * -> 𝒫 = 𝒢·Norm_W(𝒱𝒮)·𝒮_ℓ -> r̃ = 𝒫·r_std -> two-stage
+ * -> Align to {0} ∪ {2^k : k >= k0}, nearest, ties up
+ * -> cap: largest level <= caps[i] (R15)
+ * -> enforce Σ_W r <= r_std by demoting the lowest-𝒫 member one level (R16).
+ * caps[n]: per-matrix maximum rank (min(N, K, r_stored) typically).
+ * ranks_out[n]: result.  priority_out[n] (nullable): 𝒫_i.
+ * Errors: HC_ERR_CONFIG (bad layer/window/K/k0/n), HC_ERR_NUMERIC (non-finite or
+ * negative D, gates of a slot not summing to 1 within 1e-9).  Bit-exact with oracle/allocate.py. */
+hc_status hc_allocate_ranks(const hc_sens* recs, int32_t n, const hc_budget* budget,
+                            const int32_t* caps, int32_t* ranks_out, double* priority_out);
+
+/* =====================================================================================
+ * Context and weights
+ * ===================================================================================== */
+typedef struct hc_ctx hc_ctx;
+
+/* Create a context on CUDA device `device` (must be sm_100).  *out receives the handle. */
+hc_status hc_create(hc_ctx** out, int32_t device);
+hc_status hc_destroy(hc_ctx* ctx);
+
+/* One weight matrix in canonical formats (device or host pointers; read during the call only).
+ *   codes  uint32 [N][K*bits/32]: row n is a little-endian bitstream, element k at bits
+ *          [bits*k, bits*k+bits) — unsigned codes q in [0, 2^bits)            (R1)
+ *   scales bf16   [N][K/group]                                                 (R2: groups run along K)
+ *   zeros  uint8  [N][K/group], 0 <= z < 2^bits (symmetric RTN: z = 2^(bits-1)) (R3)
+ *   U      bf16   [N][r_stored]   (U[:, :r] is the rank-r slice; NULL iff r_stored == 0)
+ *   V      bf16   [r_stored][K]   (V[:r, :] is the rank-r slice; absorbs Σ)
+ * bits in {2, 3, 4}; group == 128; K % 128 == 0; N % 16 == 0; r_stored % 16 == 0, <= 256;
+ * r_alloc in {0} ∪ {8, 16, 32, ...}, r_alloc <= min(r_stored, N, K).
+ * row_begin/row_end: the rows [row_begin, row_end) this context keeps (column sharding of
+ * the output across GPUs); use 0 / N for an unsharded matrix.
+ * (row_end - row_begin) % 16 == 0. */
+typedef struct {
+  int32_t layer, window_kind, slot, expert;
+  int32_t N, K, bits, group;
+  const uint32_t* codes;
+  const uint16_t* scales;
+  const uint8_t* zeros;
+  const uint16_t* U;
+  const uint16_t* V;
+  int32_t r_stored, r_alloc;
+  int32_t row_begin, row_end;
+} hc_matrix_desc;
+
+/* Copy + repack matrices into context-owned device memory (synchronous w.r.t. its inputs:
+ * the caller may free them on return).  Matrices with equal (layer, window_kind, expert)
+ * form one window; members are ordered by `slot`.  Loading a slot again replaces it.
+ * Errors: HC_ERR_CONFIG on any shape/bit-width/rank violation. */
+hc_status hc_load_layer(hc_ctx* ctx, const hc_matrix_desc* mats, int32_t n_mats, void* stream);
+
+/* Change the allocated rank of one loaded matrix (0 disables its compensation; the
+ * r = 0 launch reads no U/V bytes).  HC_ERR_CONFIG if not admissible or > its cap. */
+hc_status hc_set_rank(hc_ctx* ctx, int32_t layer, int32_t window_kind, int32_t slot,
+                      int32_t expert, int32_t r_alloc);
+
+/* Sum of window output widths (Σ local rows of its members), or -1 if unknown. */
+int64_t hc_window_rows(hc_ctx* ctx, int32_t layer, int32_t window_kind, int32_t expert);
+
+/* =====================================================================================
+ * Execution (asynchronous on `stream`; caller keeps x / y alive until the stream is done)
+ * ===================================================================================== */
+
+/* y[b, :] = concat over the window's members of  deq(W_m)·x_b + U_m[:, :r_m]·(V_m[:r_m, :]·x_b)
+ *   x: bf16 [B][K];  y: [B][rows] (fp32 if y_dtype == HC_OUT_F32, else bf16 = RNE of the fp32
+ *   value); rows = hc_window_rows(...).  1 <= B <= 16 runs the fused decode kernel.
+ *   x and y may be host pointers (pinned or pageable): they are then staged through
+ *   context-owned device buffers inside the call (stream-ordered, the call synchronises
+ *   the stream before returning). */
+hc_status hc_compensated_linear(hc_ctx* ctx, int32_t layer, int32_t window_kind, int32_t expert,
+                                const void* x, int32_t B, void* y, int32_t y_dtype, void* stream);
+
+/* Debug/test exports (host only, no GPU needed): the load-time repack and its inverse. */
+size_t hc_repacked_bytes(int32_t N, int32_t K, int32_t bits);
+hc_status hc_repack_host(const uint32_t* codes, const uint16_t* scales, const uint8_t* zeros,
+                         int32_t N, int32_t K, int32_t bits, uint8_t* out);
+/* Decode a repacked buffer back to unsigned codes q[N][K], scales bf16 [N][K/128], zeros [N][K/128]
+ * through the kernel's own fragment/slot mapping. */
+hc_status hc_unpack_repacked_host(const uint8_t* packed, int32_t N, int32_t K, int32_t bits,
+                                  uint8_t* q_out, uint16_t* scales_out, uint8_t* zeros_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HCINFER_H */

@@ -1,0 +1,150 @@
+"""B200-native HCInfer compensated quantized linear (arXiv 2605.05819).
+
+Thin Python binding over the C-ABI library ``libhcinfer.so`` (include/hcinfer.h).  Names
+follow the C entry points: ``allocate_ranks``, ``Context.load_layer``, ``Context.set_rank``,
+``Context.compensated_linear``.  This module only marshals arguments (numpy arrays or torch
+tensors -> raw pointers, the current torch CUDA stream -> cudaStream_t); PyTorch is used for
+device memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import (HCError, HC_OK, HC_ERR_CONFIG, HC_ERR_STATE, HC_ERR_NUMERIC, HC_ERR_RUNTIME,
+                   QKV, O, UPGATE, DOWN, OUT_F32, OUT_BF16, check, lib)
+
+__all__ = ["allocate_ranks", "Context", "HCError", "QKV", "O", "UPGATE", "DOWN", "OUT_F32", "OUT_BF16",
+           "repack_host", "unpack_repacked_host", "lib"]
+
+
+def _ptr(a):
+    """Raw address of a numpy array or torch tensor (None -> NULL)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        assert a.flags["C_CONTIGUOUS"], "arrays must be C-contiguous"
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        assert a.is_contiguous(), "tensors must be contiguous"
+        return a.data_ptr()
+    raise TypeError(type(a))
+
+
+def _stream(stream):
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return torch.cuda.current_stream().cuda_stream
+        except Exception:
+            pass
+        return None
+    return getattr(stream, "cuda_stream", stream)
+
+
+# ------------------------------------------------------------------ allocation (host)
+def allocate_ranks(records, D_layer, top_k_layers, r_std, caps, tau=0.01, k0=3, two_stage_mode=0, moe_k=0):
+    """hc_allocate_ranks.  records: iterable of dicts with keys layer, window, slot, expert,
+    sigma (array or None), phi, n_sal, n_all, D, gate.  Returns (ranks int32, priority float64)."""
+    recs = list(records)
+    n = len(recs)
+    arr = (_lib.hc_sens * max(n, 1))()
+    keep = []
+    for i, r in enumerate(recs):
+        s = arr[i]
+        s.layer, s.window_kind, s.slot = int(r["layer"]), int(r["window"]), int(r["slot"])
+        s.expert = int(r.get("expert", -1))
+        sig = r.get("sigma")
+        if sig is not None:
+            sig = np.ascontiguousarray(sig, dtype=np.float64)
+            keep.append(sig)
+            s.n_sigma, s.sigma = sig.size, sig.ctypes.data_as(C.POINTER(C.c_double))
+        else:
+            s.n_sigma, s.sigma = 0, None
+        s.phi = float(r.get("phi", 1.0))
+        s.n_salient, s.n_total = int(r.get("n_sal", 0)), int(r.get("n_all", 0))
+        s.D_matrix, s.gate = float(r["D"]), float(r.get("gate", 1.0))
+    dl = np.ascontiguousarray(D_layer, dtype=np.float64)
+    b = _lib.hc_budget()
+    b.n_layers, b.D_layer = dl.size, dl.ctypes.data_as(C.POINTER(C.c_double))
+    b.top_k_layers, b.tau, b.k0 = int(top_k_layers), float(tau), int(k0)
+    for k in range(4):
+        b.r_std[k] = float(r_std[k])
+    b.two_stage_mode, b.moe_k = int(two_stage_mode), int(moe_k)
+    capv = np.ascontiguousarray(caps, dtype=np.int32)
+    ranks = np.zeros(max(n, 1), dtype=np.int32)
+    prio = np.zeros(max(n, 1), dtype=np.float64)
+    check(lib().hc_allocate_ranks(arr, n, C.byref(b), capv.ctypes.data_as(C.POINTER(C.c_int32)),
+                                  ranks.ctypes.data_as(C.POINTER(C.c_int32)),
+                                  prio.ctypes.data_as(C.POINTER(C.c_double))))
+    return ranks[:n], prio[:n]
+
+
+# ------------------------------------------------------------------ layout test exports (host)
+def repack_host(codes, scales, zeros, N, K, bits):
+    out = np.zeros(lib().hc_repacked_bytes(N, K, bits), dtype=np.uint8)
+    check(lib().hc_repack_host(_ptr(codes), _ptr(scales), _ptr(zeros), N, K, bits, _ptr(out)))
+    return out
+
+
+def unpack_repacked_host(packed, N, K, bits):
+    q = np.zeros((N, K), dtype=np.uint8)
+    s = np.zeros((N, K // 128), dtype=np.uint16)
+    z = np.zeros((N, K // 128), dtype=np.uint8)
+    check(lib().hc_unpack_repacked_host(_ptr(packed), N, K, bits, _ptr(q), _ptr(s), _ptr(z)))
+    return q, s, z
+
+
+# ------------------------------------------------------------------ device context
+class Context:
+    """hc_ctx: owns the repacked weights of loaded windows on one CUDA device."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib().hc_create(C.byref(h), int(device)))
+        self._h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hc_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def load_layer(self, mats, stream=None):
+        """mats: list of dicts with layer, window, slot, expert(-1), N, K, bits, group(128),
+        codes, scales, zeros, U, V (numpy or torch), r_stored, r_alloc, row_begin(0), row_end(N)."""
+        arr = (_lib.hc_matrix_desc * len(mats))()
+        for i, m in enumerate(mats):
+            d = arr[i]
+            d.layer, d.window_kind, d.slot = int(m["layer"]), int(m["window"]), int(m["slot"])
+            d.expert = int(m.get("expert", -1))
+            d.N, d.K, d.bits, d.group = int(m["N"]), int(m["K"]), int(m["bits"]), int(m.get("group", 128))
+            d.codes, d.scales, d.zeros = _ptr(m["codes"]), _ptr(m["scales"]), _ptr(m["zeros"])
+            d.U, d.V = _ptr(m.get("U")), _ptr(m.get("V"))
+            d.r_stored, d.r_alloc = int(m.get("r_stored", 0)), int(m.get("r_alloc", 0))
+            d.row_begin, d.row_end = int(m.get("row_begin", 0)), int(m.get("row_end", m["N"]))
+        check(lib().hc_load_layer(self._h, arr, len(mats), _stream(stream)))
+
+    def set_rank(self, layer, window, slot, r, expert=-1):
+        check(lib().hc_set_rank(self._h, layer, window, slot, expert, r))
+
+    def window_rows(self, layer, window, expert=-1) -> int:
+        return int(lib().hc_window_rows(self._h, layer, window, expert))
+
+    def compensated_linear(self, layer, window, x, y, B=None, expert=-1, out_dtype=OUT_F32, stream=None):
+        """y[b, :] = concat_m ( deq(W_m)·x_b + U_m[:, :r_m]·(V_m[:r_m, :]·x_b) ).
+        x: bf16 [B, K] (torch bf16 / uint16 bits, device or host); y: [B, rows] fp32 or bf16."""
+        if B is None:
+            B = x.shape[0]
+        check(lib().hc_compensated_linear(self._h, layer, window, expert, _ptr(x), int(B), _ptr(y),
+                                          int(out_dtype), _stream(stream)))
+        return y

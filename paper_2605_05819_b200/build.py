@@ -1,0 +1,71 @@
+"""Build libhcinfer.so in-tree: nvcc for sm_100a (-gencode arch=compute_100a,code=sm_100a).
+
+The allocator (alloc.cpp) is compiled by g++ with -ffp-contract=off (no FMA contraction,
+no fast-math) so that its float64 arithmetic is bit-identical to the oracle's.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INC = os.path.join(ROOT, "include")
+LIB = os.path.join(PKG, "libhcinfer.so")
+BUILD = os.path.join(PKG, "_build")
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CU_SOURCES = ["api.cu", "decode.cu", "repack.cu"]
+CPP_SOURCES = ["alloc.cpp"]
+
+
+def _run(cmd):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        raise RuntimeError(f"build step failed: {cmd[0]} {cmd[-1]}")
+    return r.stdout + r.stderr
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(verbose: bool = False, force: bool = False) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
+    headers.append(os.path.join(INC, "hcinfer.h"))
+    objs = []
+    log = []
+    for src in CU_SOURCES:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(BUILD, src + ".o")
+        objs.append(o)
+        if force or _stale(o, [s] + headers):
+            log.append(_run([NVCC, "-c", s, "-o", o, "-std=c++17", "-O3", "-lineinfo", *ARCH,
+                             "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
+                             "-I", INC, "-I", CSRC]))
+    for src in CPP_SOURCES:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(BUILD, src + ".o")
+        objs.append(o)
+        if force or _stale(o, [s] + headers):
+            log.append(_run(["g++", "-c", s, "-o", o, "-std=c++17", "-O2", "-fPIC", "-ffp-contract=off",
+                             "-fno-fast-math", "-I", INC, "-I", CSRC]))
+    if force or _stale(LIB, objs):
+        log.append(_run([NVCC, "-shared", "-o", LIB, *objs, *ARCH, "-lcudart"]))
+    out = "\n".join(x for x in log if x)
+    if verbose and out:
+        print(out)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(verbose=True, force="--force" in sys.argv)
+    print(LIB)

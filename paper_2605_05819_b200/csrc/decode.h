@@ -1,0 +1,48 @@
+// Fused decode kernel interface (one compensation window per launch).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hc {
+
+constexpr int kMaxMembers = 4;
+constexpr int kDecodeWarps = 8;          // consumer warps per CTA
+constexpr int kRing = 4;                 // bulk-copy ring slots per warp
+constexpr int kSlotBytes = 1088;         // >= rec_bytes(4) = 1072, >= 1 KB V piece
+
+struct DMember {
+  const uint8_t* rec;   // [n_rb][G][rec_bytes]          (layout.h)
+  const uint4* U;       // [n_rb][r_stored/16][32]       (bf16 A-fragments of U)
+  const uint4* V;       // [r_stored/16][G][8][32]       (bf16 A-fragments of V)
+  int n_rb;             // local rows / 16
+  int rb_begin;         // first window-global rb index
+  int row_off;          // output column offset of this member inside y rows
+  int r;                // allocated rank (0 = no compensation, no U/V reads)
+  int r_stored;
+  int chunk_begin;      // first window-global rank chunk (16 ranks) of this member
+};
+
+struct DArgs {
+  DMember m[kMaxMembers];
+  int n_members;
+  int K, G, B;
+  const uint16_t* x;    // bf16 [B][K]
+  void* y;              // [B][ldy] fp32 or bf16
+  int ldy, y_bf16;
+  const uint16_t* resid;  // optional bf16 [B][ld_resid] added before the output rounding
+  int ld_resid;
+  int glue;             // 0 none; 1 SiLU(gate)*up with interleaved up/gate rows (see api)
+  int n_rb;             // Σ members
+  int n_chunks;         // Σ ceil(r_m / 16)
+  int vks;              // K-slices per V chunk
+  float* vpart;         // [n_chunks * vks][32][8]
+  float* t;             // [n_chunks][16 batch][16 ranks]
+  unsigned* cnt;        // [n_chunks] chunk counters, [n_chunks] t_done, [n_chunks+1] w_done
+};
+
+// Launch the fused window kernel; bits in {2,3,4}; 1 <= B <= 16.
+cudaError_t launch_decode(const DArgs& a, int bits, int grid, cudaStream_t st);
+// Max co-resident CTAs of the decode kernel on this device (persistent grid size).
+int decode_max_ctas(int bits, int B);
+
+}  // namespace hc

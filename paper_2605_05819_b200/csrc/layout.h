@@ -1,0 +1,97 @@
+// Kernel-side HBM layout of one compensated linear (product code; NOT shared with oracle/).
+//
+// The C-ABI takes canonical formats (include/hcinfer.h); hc_load_layer repacks them
+// once into the layout below, chosen so that the decode kernel
+//   * streams every weight byte exactly once with 16-byte-aligned bulk (TMA) copies,
+//   * turns each 32-bit code word into mma.sync A-fragment registers with only
+//     shift + lop3 (the bf16 "magic number" trick: 0x4300 | bits = 128 + bits),
+//   * never materialises W.
+//
+// Row block (rb) = 16 output rows (the mma M dimension).  Group = 128 input
+// elements (the quantisation group).  A lane of a warp owns,
+// per (rb, group), the A-fragments of all eight k16 steps of the group:
+//     lane = 4*gid + tig;  register (j, i), step j in 0..7, reg i in 0..3 holds
+//     row  = gid + 8*(i&1)
+//     k_lo = 32*tig + 4*j + 2*(i>>1),  k_hi = k_lo + 1     (k within the group)
+// The k permutation is legal because the per-group partial sum is order-free;
+// it makes each lane's x values contiguous (x[32*tig + 4j .. +3] per step).
+//
+// Record for (rb, group) = [codes: 32 lanes x 2*bits words][scales 8 x u32][zeros u64][pad 8]
+//   codes word w of lane l at byte  (w/4)*512 + l*16 + (w%4)*4   for w < 4*(2b/4)
+//                                   512*(2b/4) + l*8 + (w%4)*4    for the 2-word tail (b = 3)
+//   scales word gid = bf16 s[row gid] | bf16 s[row gid+8] << 16
+//   zeros  u64: row r's zero in bits [4r, 4r+4)
+//
+// Register extraction ("slots"): register (j, i) = 0x43004300 | field bits, where a
+// field is up to 3 "parts" (word, shift, pos, nbits) taken from the lo 16-bit half
+// (and the same bits +16 from the hi half).  The register then holds
+// 128 + q*2^fp in both halves (exact in bf16), fp in {0, 2, 3}.  The B operand
+// (x) of the two registers sharing a column pair is pre-scaled by 2^-fp (exact).
+#pragma once
+#include <stdint.h>
+
+#ifdef __CUDACC__
+#define HC_HD __host__ __device__ __forceinline__
+#else
+#define HC_HD inline
+#endif
+
+namespace hc {
+
+constexpr int kRows = 16;
+constexpr int kGroup = 128;
+constexpr uint32_t kMagic = 0x43004300u;   // bf16x2(128, 128)
+
+HC_HD constexpr int code_words(int bits) { return 2 * bits; }            // per lane per group
+HC_HD constexpr int code_bytes(int bits) { return 256 * bits; }          // per (rb, group)
+HC_HD constexpr int rec_bytes(int bits) { return 256 * bits + 48; }      // + scales/zeros/pad
+HC_HD constexpr int scales_off(int bits) { return 256 * bits; }
+HC_HD constexpr int zeros_off(int bits) { return 256 * bits + 32; }
+
+HC_HD constexpr int word_offset(int bits, int w, int lane) {
+  return (w < 4 * ((2 * bits) / 4))
+             ? (w / 4) * 512 + lane * 16 + (w % 4) * 4
+             : 512 * ((2 * bits) / 4) + lane * 8 + (w % 4) * 4;
+}
+
+struct Part { int word, shift, pos, nbits; };
+struct Slot { int nparts; int fp; Part p[3]; };
+
+// Slot table for register (j, i) at a given bit width.  See the header comment.
+HC_HD constexpr Slot slot(int bits, int j, int i) {
+  if (bits == 4) {
+    return Slot{1, 0, {Part{j, 4 * i, 0, 4}, Part{0, 0, 0, 0}, Part{0, 0, 0, 0}}};
+  }
+  if (bits == 2) {
+    const int fp = 2 * (i >> 1);
+    return Slot{1, fp, {Part{j / 2, 8 * (j & 1) + 4 * (i & 1), fp, 2}, Part{0, 0, 0, 0}, Part{0, 0, 0, 0}}};
+  }
+  // bits == 3: 20 weight-1 slots (18 plain + 2 gathered from bit 15 of each word),
+  // 12 weight-8 slots; steps 0..5 pair (w1, w8), steps 6..7 pair (w1, w1).
+  const int pair = i >> 1, mem = i & 1;
+  int w1 = -1, w8 = -1;
+  if (j < 6) { if (pair == 0) w1 = 2 * j + mem; else w8 = 2 * j + mem; }
+  else       { w1 = 12 + 4 * (j - 6) + 2 * pair + mem; }
+  if (w8 >= 0) {
+    return Slot{1, 3, {Part{w8 / 2, 6 * (w8 % 2), 3, 3}, Part{0, 0, 0, 0}, Part{0, 0, 0, 0}}};
+  }
+  if (w1 < 18) {
+    return Slot{1, 0, {Part{w1 / 3, 6 * (w1 % 3), 0, 3}, Part{0, 0, 0, 0}, Part{0, 0, 0, 0}}};
+  }
+  const int base = (w1 == 18) ? 0 : 3;   // gather bit 15 of words base..base+2
+  return Slot{3, 0, {Part{base, 15, 0, 1}, Part{base + 1, 14, 1, 1}, Part{base + 2, 13, 2, 1}}};
+}
+
+// x pre-scale exponent for the B register of step j: pair 0 (b0, cols 2tig..) or pair 1 (b1).
+HC_HD constexpr int step_fp(int bits, int j, int pair) { return slot(bits, j, 2 * pair).fp; }
+
+// Fragment element -> (row within rb, k within group)
+HC_HD constexpr int frag_row(int lane, int i) { return (lane >> 2) + 8 * (i & 1); }
+HC_HD constexpr int frag_k(int lane, int j, int i, int hi) { return 32 * (lane & 3) + 4 * j + 2 * (i >> 1) + hi; }
+
+// Compensation factor tiles (bf16, no quantisation):
+//  U: [rb][chunk c = rank/16][lane][uint4]; reg i of lane: row gid + 8(i&1), ranks 16c + 2tig + 8(i>>1) + {0,1}
+//  V: [chunk c][group g][step j][lane][uint4]; reg i: rank 16c + gid + 8(i&1), k = frag_k(lane, j, i, {0,1})
+HC_HD constexpr int u_rank(int lane, int i, int hi) { return 2 * (lane & 3) + 8 * (i >> 1) + hi; }
+
+}  // namespace hc

@@ -1,0 +1,162 @@
+// Load-time repack (hc_load_layer) and its host test exports.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <vector>
+
+#include "hcinfer.h"
+#include "repack.cuh"
+#include "repack_kernels.h"
+#include "status.h"
+
+namespace hc {
+
+// one thread per (rb, g, lane)
+__global__ void repack_codes_kernel(const uint32_t* __restrict__ codes, const uint16_t* __restrict__ scales,
+                                    const uint8_t* __restrict__ zeros, int n_rb, int K, int bits,
+                                    int row0, uint8_t* __restrict__ out) {
+  const int G = K / kGroup;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long total = (long long)n_rb * G * 32;
+  if (tid >= total) return;
+  const int lane = (int)(tid & 31);
+  const long long rg = tid >> 5;
+  const int g = (int)(rg % G), rb = (int)(rg / G);
+  const int wpr = K * bits / 32;
+  const uint32_t* src = codes + (size_t)row0 * wpr;    // shard rows start at row0
+  uint32_t words[8];
+  pack_lane_words(src, wpr, rb, g, lane, bits, words);
+  uint8_t* rec = out + (size_t)rg * rec_bytes(bits);
+  for (int w = 0; w < 2 * bits; ++w) *reinterpret_cast<uint32_t*>(rec + word_offset(bits, w, lane)) = words[w];
+  const int ng = G;
+  if (lane < 8) {
+    const size_t r0 = (size_t)(row0 + rb * kRows + lane), r1 = r0 + 8;
+    const uint32_t sw = (uint32_t)scales[r0 * ng + g] | ((uint32_t)scales[r1 * ng + g] << 16);
+    *reinterpret_cast<uint32_t*>(rec + scales_off(bits) + 4 * lane) = sw;
+  }
+  if (lane == 8) {
+    uint64_t zw = 0;
+    for (int r = 0; r < kRows; ++r)
+      zw |= (uint64_t)(zeros[(size_t)(row0 + rb * kRows + r) * ng + g] & 0xF) << (4 * r);
+    *reinterpret_cast<uint64_t*>(rec + zeros_off(bits)) = zw;
+    *reinterpret_cast<uint64_t*>(rec + zeros_off(bits) + 8) = 0ull;
+  }
+}
+
+// U: [rb][c][lane][4 regs]; one thread per (rb, c, lane)
+__global__ void repack_u_kernel(const uint16_t* __restrict__ U, int n_rb, int r_stored, int row0,
+                                uint32_t* __restrict__ out) {
+  const int nc = r_stored / 16;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= (long long)n_rb * nc * 32) return;
+  const int lane = (int)(tid & 31);
+  const int c = (int)((tid >> 5) % nc), rb = (int)((tid >> 5) / nc);
+  for (int i = 0; i < 4; ++i) {
+    const size_t row = (size_t)(row0 + rb * kRows + frag_row(lane, i));
+    const uint32_t lo = U[row * r_stored + 16 * c + u_rank(lane, i, 0)];
+    const uint32_t hi = U[row * r_stored + 16 * c + u_rank(lane, i, 1)];
+    out[tid * 4 + i] = lo | (hi << 16);
+  }
+}
+
+// V: [c][g][j][lane][4 regs]; one thread per (c, g, j, lane)
+__global__ void repack_v_kernel(const uint16_t* __restrict__ V, int K, int r_stored, uint32_t* __restrict__ out) {
+  const int G = K / kGroup, nc = r_stored / 16;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= (long long)nc * G * 8 * 32) return;
+  const int lane = (int)(tid & 31);
+  const int j = (int)((tid >> 5) & 7);
+  const long long cg = tid >> 8;
+  const int g = (int)(cg % G), c = (int)(cg / G);
+  for (int i = 0; i < 4; ++i) {
+    const size_t rank = (size_t)(16 * c + frag_row(lane, i));
+    const uint32_t lo = V[rank * K + g * kGroup + frag_k(lane, j, i, 0)];
+    const uint32_t hi = V[rank * K + g * kGroup + frag_k(lane, j, i, 1)];
+    out[tid * 4 + i] = lo | (hi << 16);
+  }
+}
+
+cudaError_t launch_repack(const uint32_t* codes, const uint16_t* scales, const uint8_t* zeros,
+                          const uint16_t* U, const uint16_t* V, int K, int bits, int r_stored,
+                          int row0, int n_rows, uint8_t* rec_out, uint32_t* u_out, uint32_t* v_out,
+                          cudaStream_t st) {
+  const int n_rb = n_rows / kRows, G = K / kGroup;
+  long long n = (long long)n_rb * G * 32;
+  repack_codes_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(codes, scales, zeros, n_rb, K, bits, row0, rec_out);
+  if (r_stored > 0) {
+    n = (long long)n_rb * (r_stored / 16) * 32;
+    repack_u_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(U, n_rb, r_stored, row0, u_out);
+    n = (long long)(r_stored / 16) * G * 8 * 32;
+    repack_v_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(V, K, r_stored, v_out);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace hc
+
+// ------------------------------------------------------------------ host test exports
+extern "C" size_t hc_repacked_bytes(int32_t N, int32_t K, int32_t bits) {
+  if (N <= 0 || K <= 0 || N % hc::kRows || K % hc::kGroup) return 0;
+  return (size_t)(N / hc::kRows) * (K / hc::kGroup) * hc::rec_bytes(bits);
+}
+
+static bool bits_ok(int b) { return b == 2 || b == 3 || b == 4; }
+
+extern "C" hc_status hc_repack_host(const uint32_t* codes, const uint16_t* scales, const uint8_t* zeros,
+                                    int32_t N, int32_t K, int32_t bits, uint8_t* out) {
+  using namespace hc;
+  if (!codes || !scales || !zeros || !out) return fail(HC_ERR_CONFIG, "hc_repack_host: null pointer");
+  if (!bits_ok(bits) || N <= 0 || N % kRows || K <= 0 || K % kGroup)
+    return fail(HC_ERR_CONFIG, "hc_repack_host: bad shape N=%d K=%d bits=%d", N, K, bits);
+  const int G = K / kGroup, wpr = K * bits / 32;
+  for (int rb = 0; rb < N / kRows; ++rb)
+    for (int g = 0; g < G; ++g) {
+      uint8_t* rec = out + ((size_t)rb * G + g) * rec_bytes(bits);
+      std::memset(rec, 0, rec_bytes(bits));
+      for (int lane = 0; lane < 32; ++lane) {
+        uint32_t words[8];
+        pack_lane_words(codes, wpr, rb, g, lane, bits, words);
+        for (int w = 0; w < 2 * bits; ++w) std::memcpy(rec + word_offset(bits, w, lane), &words[w], 4);
+      }
+      for (int gid = 0; gid < 8; ++gid) {
+        const size_t r0 = (size_t)rb * kRows + gid;
+        const uint32_t sw = (uint32_t)scales[r0 * G + g] | ((uint32_t)scales[(r0 + 8) * G + g] << 16);
+        std::memcpy(rec + scales_off(bits) + 4 * gid, &sw, 4);
+      }
+      uint64_t zw = 0;
+      for (int r = 0; r < kRows; ++r) zw |= (uint64_t)(zeros[((size_t)rb * kRows + r) * G + g] & 0xF) << (4 * r);
+      std::memcpy(rec + zeros_off(bits), &zw, 8);
+    }
+  return HC_OK;
+}
+
+extern "C" hc_status hc_unpack_repacked_host(const uint8_t* packed, int32_t N, int32_t K, int32_t bits,
+                                             uint8_t* q_out, uint16_t* scales_out, uint8_t* zeros_out) {
+  using namespace hc;
+  if (!packed || !q_out) return fail(HC_ERR_CONFIG, "hc_unpack_repacked_host: null pointer");
+  if (!bits_ok(bits) || N <= 0 || N % kRows || K <= 0 || K % kGroup)
+    return fail(HC_ERR_CONFIG, "hc_unpack_repacked_host: bad shape");
+  const int G = K / kGroup;
+  for (int rb = 0; rb < N / kRows; ++rb)
+    for (int g = 0; g < G; ++g) {
+      const uint8_t* rec = packed + ((size_t)rb * G + g) * rec_bytes(bits);
+      for (int lane = 0; lane < 32; ++lane) {
+        uint32_t words[8];
+        for (int w = 0; w < 2 * bits; ++w) std::memcpy(&words[w], rec + word_offset(bits, w, lane), 4);
+        unpack_lane_words(words, lane, bits, g, rb, q_out, K);
+      }
+      if (scales_out)
+        for (int gid = 0; gid < 8; ++gid) {
+          uint32_t sw;
+          std::memcpy(&sw, rec + scales_off(bits) + 4 * gid, 4);
+          scales_out[((size_t)rb * kRows + gid) * G + g] = (uint16_t)(sw & 0xFFFF);
+          scales_out[((size_t)rb * kRows + gid + 8) * G + g] = (uint16_t)(sw >> 16);
+        }
+      if (zeros_out) {
+        uint64_t zw;
+        std::memcpy(&zw, rec + zeros_off(bits), 8);
+        for (int r = 0; r < kRows; ++r) zeros_out[((size_t)rb * kRows + r) * G + g] = (uint8_t)((zw >> (4 * r)) & 0xF);
+      }
+    }
+  return HC_OK;
+}

@@ -1,0 +1,150 @@
+"""GPU parity of the fused decode kernel (through the C-ABI) against the float64 oracle.
+
+Bar (BASELINE.json north_star): max|y − y*| / max|y*| <= 2e-3 on fp32 output; bf16 output
+bit-equal to RNE(fp32 output); r = 0 bit-identical to the uncompensated product; results
+deterministic and identical across repeated launches (self-resetting counters)."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import linear
+from oracle.packing import bf16_to_f64, f64_to_bf16_bits_rne
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-3
+
+
+@pytest.fixture(scope="module")
+def hc():
+    import paper_2605_05819_b200 as m
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    return m
+
+
+@pytest.fixture(scope="module")
+def ctx(hc):
+    return hc.Context(0)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def load(ctx, case, layer, window=0, slot=0, r=0, expert=-1):
+    ctx.load_layer([dict(layer=layer, window=window, slot=slot, expert=expert, N=case["N"], K=case["K"],
+                         bits=case["bits"], codes=dev(case["codes"]), scales=dev(case["scales"]),
+                         zeros=dev(case["zeros"]), U=dev(case["U"]) if case["r_stored"] else None,
+                         V=dev(case["V"]) if case["r_stored"] else None, r_stored=case["r_stored"], r_alloc=r)])
+
+
+def run(hc, ctx, layer, x_bits, rows, window=0, out=0):
+    B = x_bits.shape[0]
+    y = torch.empty((B, rows), dtype=torch.float32 if out == 0 else torch.int16, device="cuda")
+    ctx.compensated_linear(layer, window, dev(x_bits), y, out_dtype=out)
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+def rel_err(y, ref):
+    return np.abs(y - ref).max() / np.abs(ref).max()
+
+
+_layer = [100]
+
+
+def next_layer():
+    _layer[0] += 1
+    return _layer[0]
+
+
+@pytest.mark.parametrize("bits,zeros", [(4, "sym"), (4, "asym"), (3, "asym"), (3, "sym"), (2, "asym")])
+@pytest.mark.parametrize("B", [1, 3, 8, 9, 16])
+def test_single_matrix_parity(hc, ctx, bits, zeros, B):
+    # 17 row blocks, 11 groups (uneven split over 8 warps), several V slices
+    case = synth.linear_case(bits * 31 + B, N=272, K=1408, bits=bits, r_stored=64, B=B, zeros=zeros)
+    L = next_layer()
+    for r in (0, 8, 32, 64):
+        load(ctx, case, L, r=r)
+        y = run(hc, ctx, L, case["x"], 272)
+        ref = linear.compensated_linear(case, r)
+        assert rel_err(y, ref) <= TOL, (r, rel_err(y, ref))
+        assert rel_err(y, ref) <= 1e-5      # exact-integer dequant: far inside the bar
+
+
+def test_rank0_bit_identical_to_zero_compensation(hc, ctx):
+    # r = 0 launch (no U/V reads) == r = 64 launch with U = 0 (compensation exactly 0)
+    case = synth.linear_case(5, N=512, K=1024, bits=4, r_stored=64, B=4, zeros="asym")
+    L = next_layer()
+    load(ctx, case, L, r=0)
+    y0 = run(hc, ctx, L, case["x"], 512)
+    case0 = dict(case, U=np.zeros_like(case["U"]))
+    load(ctx, case0, L, r=64)
+    y64 = run(hc, ctx, L, case["x"], 512)
+    assert np.array_equal(y0, y64)
+    ref = linear.compensated_linear(case, 0)
+    assert rel_err(y0, ref) <= 1e-5
+
+
+def test_bf16_output_is_rne_of_fp32(hc, ctx):
+    case = synth.linear_case(6, N=256, K=2048, bits=4, r_stored=32, B=5)
+    L = next_layer()
+    load(ctx, case, L, r=32)
+    y32 = run(hc, ctx, L, case["x"], 256, out=0)
+    y16 = run(hc, ctx, L, case["x"], 256, out=1).view(np.uint16)
+    assert np.array_equal(y16, f64_to_bf16_bits_rne(y32))
+
+
+def test_window_three_members_and_determinism(hc, ctx):
+    L = next_layer()
+    K = 1024
+    cases = [synth.linear_case(40 + i, N=n, K=K, bits=4, r_stored=64, B=2, zeros="asym")
+             for i, n in enumerate((512, 128, 128))]
+    ranks = (64, 0, 16)
+    for slot, (c, r) in enumerate(zip(cases, ranks)):
+        load(ctx, c, L, window=0, slot=slot, r=r)
+    assert ctx.window_rows(L, 0) == 768
+    x = cases[0]["x"]
+    y1 = run(hc, ctx, L, x, 768)
+    y2 = run(hc, ctx, L, x, 768)
+    y3 = run(hc, ctx, L, x, 768)
+    assert np.array_equal(y1, y2) and np.array_equal(y2, y3)      # deterministic, counters reset
+    ref = linear.window_linear(cases, list(ranks), x)
+    assert rel_err(y1, ref) <= 1e-5
+
+
+def test_host_buffers_path_equals_device_path(hc, ctx):
+    case = synth.linear_case(8, N=256, K=1024, bits=3, r_stored=32, B=3, zeros="asym")
+    L = next_layer()
+    load(ctx, case, L, r=32)
+    yd = run(hc, ctx, L, case["x"], 256)
+    yh = np.zeros((3, 256), np.float32)
+    ctx.compensated_linear(L, 0, np.ascontiguousarray(case["x"]), yh)     # host numpy in/out
+    assert np.array_equal(yd, yh)
+
+
+def test_c1_full_size_parity(hc, ctx):
+    # BASELINE C1: 4096 x 4096, 4-bit g128, rank 64, batch 1 — the bench launch configuration
+    for zeros in ("sym", "asym"):
+        case = synth.linear_case(0, N=4096, K=4096, bits=4, r_stored=64, B=1, zeros=zeros)
+        L = next_layer()
+        load(ctx, case, L, r=64)
+        y = run(hc, ctx, L, case["x"], 4096)
+        ref = linear.compensated_linear(case, 64)
+        assert rel_err(y, ref) <= 1e-5
+
+
+def test_errors(hc, ctx):
+    case = synth.linear_case(9, N=128, K=256, bits=4, r_stored=16, B=1)
+    with pytest.raises(hc.HCError) as ei:
+        ctx.load_layer([dict(layer=0, window=0, slot=0, N=120, K=256, bits=4, codes=dev(case["codes"]),
+                             scales=dev(case["scales"]), zeros=dev(case["zeros"]))])
+    assert ei.value.code == hc.HC_ERR_CONFIG
+    with pytest.raises(hc.HCError) as ei:
+        load(ctx, case, 999, r=24)                       # not admissible
+    assert ei.value.code == hc.HC_ERR_CONFIG
+    with pytest.raises(hc.HCError) as ei:
+        ctx.compensated_linear(12345, 0, dev(case["x"]), torch.empty(1, 128, device="cuda"))
+    assert ei.value.code == hc.HC_ERR_STATE
