@@ -130,17 +130,18 @@ def run_c1_ours(args, rank, world, device):
     torch.cuda.synchronize()
     reps = max(1, (args.steps + ncopy - 1) // ncopy)
     warm = max(1, (args.warmup + ncopy - 1) // ncopy)
-    for _ in range(warm):
-        graph.replay()
+    with torch.cuda.stream(st):
+        for _ in range(warm):
+            graph.replay()
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(device) as clk:
+    with Clocks(device) as clk, torch.cuda.stream(st):
         e0.record(st)
         for _ in range(reps):
-            graph.replay()
+            graph.replay()                               # replays on the current stream = st
         e1.record(st)
         torch.cuda.synchronize()
     if world > 1:

@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -42,7 +43,7 @@ struct Member {
 struct Window {
   int layer = 0, kind = 0, expert = -1;
   std::vector<Member> members;        // sorted by slot
-  DevBuf vpart, t, cnt;               // launch workspace (self-resetting counters)
+  DevBuf vpart, cnt;                  // launch workspace (self-resetting counters)
   int ws_chunks = -1;
 };
 
@@ -63,7 +64,7 @@ struct hc_ctx {
   int device = 0;
   int sms = 0;
   std::map<Key, Window> windows;
-  std::map<int, int> max_ctas;        // key: bits*2 + (B > 8)
+  std::map<std::tuple<int, int, int, int, int>, int> max_ctas;   // (bits, B, K, chunks, vks) -> co-resident CTAs
   DevBuf stage_x, stage_y;
 };
 
@@ -239,24 +240,25 @@ hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int B, void* y, int
   a.ldy = row;
   a.n_rb = rb;
   a.n_chunks = chunks;
-  a.vks = std::max(1, std::min(a.G, 16 / m0.bits));
+  a.vks = std::max(1, std::min(4, a.G / 8));   // ~8 groups (32 KB of V) per rank-projection item
   if (w.ws_chunks < max_chunks) {
     const int mc = std::max(max_chunks, 1);
-    CUDA_TRY(w.vpart.alloc((size_t)mc * 8 * 32 * 8 * sizeof(float)));
-    CUDA_TRY(w.t.alloc((size_t)mc * 256 * sizeof(float)));
-    CUDA_TRY(w.cnt.alloc((size_t)(mc + 2) * sizeof(unsigned)));
+    CUDA_TRY(w.vpart.alloc((size_t)mc * kMaxVks * 256 * sizeof(float)));
+    CUDA_TRY(w.cnt.alloc(2 * sizeof(unsigned)));
     CUDA_TRY(cudaMemset(w.cnt.p, 0, w.cnt.bytes));
-    CUDA_TRY(cudaMemset(w.t.p, 0, w.t.bytes));
     w.ws_chunks = max_chunks;
   }
+  if (a.n_chunks > kMaxChunks) return fail(HC_ERR_CONFIG, "window ranks need %d chunks > %d", a.n_chunks, kMaxChunks);
   a.vpart = (float*)w.vpart.p;
-  a.t = (float*)w.t.p;
   a.cnt = (unsigned*)w.cnt.p;
-  const int key = m0.bits * 2 + (B > 8);
+  const auto key = std::make_tuple(m0.bits, B, a.K, a.n_chunks, a.vks);
   auto it = ctx->max_ctas.find(key);
-  if (it == ctx->max_ctas.end()) it = ctx->max_ctas.emplace(key, decode_max_ctas(m0.bits, B)).first;
+  if (it == ctx->max_ctas.end())
+    it = ctx->max_ctas.emplace(key, decode_max_ctas(m0.bits, B, a.K, a.n_chunks, a.vks)).first;
   const int n_items = a.n_chunks * a.vks + a.n_rb;
-  grid = std::max(1, std::min(n_items, it->second));
+  static const int per_sm = [] { const char* e = getenv("HC_DECODE_CTAS_PER_SM"); return e ? atoi(e) : 0; }();
+  const int cap = per_sm > 0 ? std::min(it->second, per_sm * ctx->sms) : it->second;
+  grid = std::max(1, std::min(n_items, cap));
   if (it->second <= 0) return fail(HC_ERR_RUNTIME, "decode kernel cannot be resident on this device");
   return HC_OK;
 }

@@ -4,20 +4,27 @@
 //     t[b, j] = Σ_k V[j,k] · x[b,k]                                      (north_star)
 //
 // Design (DESIGN.md §"Decode kernel"):
-//  * persistent grid, 8 warps per CTA; CTA work items are (a) rank-projection items
-//    (16 ranks × a K-slice of V) and then (b) row-block items (16 output rows × all K);
-//  * each warp streams its tiles (one (row-block, group) record or one 1 KB V piece) from
-//    HBM with cp.async.bulk (TMA engine) into a private 4-slot shared-memory ring guarded by
-//    mbarriers, L2 evict-first; W is never materialised;
-//  * codes -> bf16 A-fragments with shift/lop3 and the 0x4300 magic (exact integers), minus
-//    the per-group zero (exact), contracted with bf16 x on mma.sync m16n8k16 (fp32 accumulate),
-//    per-group partial sums scaled by the fp32 group scale afterwards (no bf16 rounding of W);
-//  * the 8 warps' partial sums are reduced in shared memory; the CTA's epilogue warp adds
-//    U[:, :r]·t with t split into bf16 hi + lo (fp32-accurate) on the same mma, then writes y
-//    once (fp32, or bf16 = RNE of the fp32 value), optionally adding a bf16 residual;
-//  * t is produced inside the same launch: rank-projection items publish per-slice partials,
-//    the last arriver per chunk reduces them in a fixed order (deterministic) and bumps a
-//    release counter that row-block epilogues acquire.  Counters self-reset at the end.
+//  * one CTA work item is either a rank-projection item (16 ranks of V × a 4-group K-slice) or a
+//    row-block item (16 output rows × all of K); rank-projection items come first so that t is
+//    ready long before the row-block epilogues need it; the grid is one resident wave
+//    (persistent loop beyond that);
+//  * each warp streams its tiles — a (row-block, group) record or a 1 KB V piece — from HBM with
+//    cp.async.bulk (TMA engine, L2 evict-first) into a private 4-slot shared-memory ring guarded
+//    by mbarriers; W is never materialised;
+//  * PDL: weight tiles (and U fragments) are requested before griddepcontrol.wait, i.e. while the
+//    previous kernel in the stream is still finishing; x, t, y and the counters are touched only
+//    after it;
+//  * x is staged once per CTA in shared memory (rows padded so 128-bit fragment loads are
+//    bank-conflict-free), or read through L1 when it does not fit;
+//  * codes -> bf16 A-fragments with shift/lop3 and the 0x4300 magic (exact integers), minus the
+//    per-group zero (exact), on mma.sync m16n8k16 with fp32 accumulation, two independent
+//    accumulator chains, per-group partials scaled by the fp32 group scale afterwards;
+//  * the 8 warps' partial sums are reduced in shared memory in a fixed order; the CTA's epilogue
+//    warp adds U[:, :r]·t with t split into bf16 hi + lo (fp32-accurate) on the same mma and
+//    writes y once (fp32, or bf16 = RNE of the fp32 value), optionally adding a bf16 residual;
+//  * t is produced inside the launch: rank-projection items publish per-slice partials and bump a
+//    release counter; each row-block epilogue acquires it and sums the slices of its member's
+//    chunks in slice order (deterministic).  The counters self-reset before the kernel exits.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -46,10 +53,13 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                          uint64_t policy) {
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
+}
+
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                          uint64_t policy) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
           "r"(smem_u32(dst)),
@@ -62,10 +72,15 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t evict_last_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
   unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 
@@ -90,9 +105,7 @@ __device__ __forceinline__ uint32_t f32_to_bf16_rn(float f) {
   __nv_bfloat16 b = __float2bfloat16_rn(f);
   return (uint32_t)(*reinterpret_cast<uint16_t*>(&b));
 }
-
-// 2^-fp as a bf16x2 constant
-__device__ __forceinline__ constexpr uint32_t pow2neg_bf16x2(int fp) {
+__device__ __forceinline__ constexpr uint32_t pow2neg_bf16x2(int fp) {   // bf16x2(2^-fp)
   return (uint32_t)(0x3F80 - (fp << 7)) * 0x00010001u;
 }
 
@@ -111,22 +124,11 @@ __device__ __forceinline__ uint32_t extract(const uint32_t (&w)[2 * BITS], int j
   return acc;
 }
 
-struct Tiles {   // a warp's share of one CTA work item
-  int n;         // number of tiles
-  int g0;        // first group
+// A warp's share of one CTA work item: n tiles at base + t*tb (tb bytes each).
+struct Share {
+  const uint8_t* base;
+  int n, tb, g0, member, is_v;
 };
-
-__device__ __forceinline__ Tiles warp_tiles(const DArgs& a, int item, int warp) {
-  const int nV = a.n_chunks * a.vks;
-  if (item < nV) {
-    const int vs = item % a.vks;
-    const int lo = vs * a.G / a.vks, hi = (vs + 1) * a.G / a.vks;
-    const int g0 = lo + warp * (hi - lo) / kDecodeWarps, g1 = lo + (warp + 1) * (hi - lo) / kDecodeWarps;
-    return Tiles{4 * (g1 - g0), g0};
-  }
-  const int g0 = warp * a.G / kDecodeWarps, g1 = (warp + 1) * a.G / kDecodeWarps;
-  return Tiles{g1 - g0, g0};
-}
 
 __device__ __forceinline__ int member_of_rb(const DArgs& a, int rb) {
   int m = 0;
@@ -144,45 +146,59 @@ __device__ __forceinline__ int member_of_chunk(const DArgs& a, int cc) {
 }
 
 template <int BITS>
-__device__ __forceinline__ const void* tile_src(const DArgs& a, int item, int g0, int t, uint32_t& bytes) {
+__device__ __forceinline__ Share warp_share(const DArgs& a, int item, int warp) {
+  Share s;
   const int nV = a.n_chunks * a.vks;
-  if (item < nV) {
-    const int cc = item / a.vks;
-    const DMember& m = a.m[member_of_chunk(a, cc)];
-    const int c = cc - m.chunk_begin, g = g0 + (t >> 2), p = t & 3;
-    bytes = 1024;
-    return m.V + ((size_t)(c * a.G + g) * 8 + 2 * p) * 32;
+  if (item < nV) {   // V pieces of (chunk, slice), split evenly over the warps at piece granularity
+    const int cc = item / a.vks, vs = item - cc * a.vks;
+    s.member = member_of_chunk(a, cc);
+    const DMember& m = a.m[s.member];
+    const int lo = vs * a.G / a.vks, hi = (vs + 1) * a.G / a.vks;
+    const int np = 4 * (hi - lo);
+    const int p0 = warp * np / kDecodeWarps, p1 = (warp + 1) * np / kDecodeWarps;
+    s.n = p1 - p0;
+    s.g0 = 4 * lo + p0;   // absolute piece index inside the chunk (4 pieces of 1 KB per group)
+    s.base = reinterpret_cast<const uint8_t*>(m.V + (size_t)(cc - m.chunk_begin) * a.G * 256) + (size_t)s.g0 * 1024;
+    s.tb = 1024;
+    s.is_v = 1;
+  } else {           // all of K of one row block, contiguous group ranges per warp
+    const int rb = item - nV;
+    s.member = member_of_rb(a, rb);
+    const DMember& m = a.m[s.member];
+    const int g0 = warp * a.G / kDecodeWarps, g1 = (warp + 1) * a.G / kDecodeWarps;
+    s.n = g1 - g0;
+    s.g0 = g0;
+    s.base = m.rec + ((size_t)(rb - m.rb_begin) * a.G + g0) * rec_bytes(BITS);
+    s.tb = rec_bytes(BITS);
+    s.is_v = 0;
   }
-  const int rb = item - nV;
-  const DMember& m = a.m[member_of_rb(a, rb)];
-  bytes = rec_bytes(BITS);
-  return m.rec + ((size_t)(rb - m.rb_begin) * a.G + (g0 + t)) * rec_bytes(BITS);
+  return s;
 }
 
-// x fragments of group g for the lane: xr[nb][16] (bf16x2), step j uses xr[nb][2j], xr[nb][2j+1]
+// Row of x used by mma column `col` (batch index).  Columns >= B read a valid row; their
+// outputs are never stored, so no zeroing is needed.
+__device__ __forceinline__ int xrow(const DArgs& a, int col) { return col < a.B ? col : a.B - 1; }
+
+// x fragments of group g from global memory (L1-cached): xr[nb][4q + e] = x[b][g*128 + 32q + 8tig .. +7]
 template <int NB8>
-__device__ __forceinline__ void load_x(const DArgs& a, int g, int lane, uint32_t (&xr)[NB8][16]) {
+__device__ __forceinline__ void load_x_global(const DArgs& a, int g, int lane, uint32_t (&xr)[NB8][16]) {
 #pragma unroll
   for (int nb = 0; nb < NB8; ++nb) {
-    const int b = (lane >> 2) + 8 * nb;
-    if (b < a.B) {
-      const uint4* p = reinterpret_cast<const uint4*>(a.x + (size_t)b * a.K + g * kGroup + 32 * (lane & 3));
+    const uint4* p = reinterpret_cast<const uint4*>(a.x + (size_t)xrow(a, (lane >> 2) + 8 * nb) * a.K +
+                                                    g * kGroup + 8 * (lane & 3));
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint4 v = __ldg(p + q);
-        xr[nb][4 * q + 0] = v.x; xr[nb][4 * q + 1] = v.y; xr[nb][4 * q + 2] = v.z; xr[nb][4 * q + 3] = v.w;
-      }
-    } else {
-#pragma unroll
-      for (int q = 0; q < 16; ++q) xr[nb][q] = 0u;
+    for (int q = 0; q < 4; ++q) {
+      const uint4 v = __ldg(p + 4 * q);
+      xr[nb][4 * q + 0] = v.x; xr[nb][4 * q + 1] = v.y; xr[nb][4 * q + 2] = v.z; xr[nb][4 * q + 3] = v.w;
     }
   }
 }
 
-// One (row-block, group) record: tot[nb][e] += s_row · Σ_k (q − z)·x
-template <int BITS, int NB8>
-__device__ __forceinline__ void w_tile(const uint8_t* rec, int lane, const uint32_t (&xr)[NB8][16],
-                                       float (&tot)[NB8][4]) {
+// One (row-block, group) record: tot[nb][e] += s_row · Σ_k (q − z)·x.
+// XS: x fragments come from shared memory (xrow_s[nb] = this lane's run start for the group).
+template <int BITS, int NB8, bool XS>
+__device__ __forceinline__ void w_tile(const uint8_t* rec, int lane, const uint4* const (&xrow_s)[NB8],
+                                       const uint32_t (&xr)[NB8][16], float (&tot)[NB8][4]) {
   uint32_t w[2 * BITS];
 #pragma unroll
   for (int q = 0; q < (2 * BITS) / 4; ++q) {
@@ -195,312 +211,447 @@ __device__ __forceinline__ void w_tile(const uint8_t* rec, int lane, const uint3
   }
   const int gid = lane >> 2;
   const uint32_t sw = *reinterpret_cast<const uint32_t*>(rec + scales_off(BITS) + 4 * gid);
-  const uint64_t zw = *reinterpret_cast<const uint64_t*>(rec + zeros_off(BITS));
-  const float s0 = bf16_bits_to_f32(sw & 0xFFFFu), s1 = bf16_bits_to_f32(sw >> 16);
-  const uint32_t z[2] = {(uint32_t)(zw >> (4 * gid)) & 15u, (uint32_t)(zw >> (4 * gid + 32)) & 15u};
-  float acc[NB8][4];
+  const uint32_t z0 = *reinterpret_cast<const uint32_t*>(rec + zeros_off(BITS));       // rows 0..7
+  const uint32_t z1 = *reinterpret_cast<const uint32_t*>(rec + zeros_off(BITS) + 4);   // rows 8..15
+  const uint32_t zr[2] = {(z0 >> (4 * gid)) & 15u, (z1 >> (4 * gid)) & 15u};
+  constexpr int kFpHi = BITS == 2 ? 2 : (BITS == 3 ? 3 : 0);   // the non-zero field weight exponent
+  uint32_t zc[2][2];                                            // [row parity][fp == 0 ? 0 : 1]
 #pragma unroll
-  for (int nb = 0; nb < NB8; ++nb)
+  for (int rp = 0; rp < 2; ++rp) {
+    zc[rp][0] = (0x4300u + zr[rp]) * 0x00010001u;               // bf16x2(128 + z), exact
+    zc[rp][1] = (0x4300u + (zr[rp] << kFpHi)) * 0x00010001u;    // bf16x2(128 + z·2^fp), exact
+  }
+  float acc[2][NB8][4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) acc[nb][e] = 0.f;
+  for (int h = 0; h < 2; ++h)
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    uint32_t af[4];
+    for (int nb = 0; nb < NB8; ++nb)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int fp = slot(BITS, j, i).fp;
-      const uint32_t zc = (0x4300u + (z[i & 1] << fp)) * 0x00010001u;   // bf16x2(128 + z·2^fp), exact
-      af[i] = bf2_sub(extract<BITS>(w, j, i), zc);                       // 2^fp·(q − z), exact
-    }
-    const int fp0 = step_fp(BITS, j, 0), fp1 = step_fp(BITS, j, 1);
+      for (int e = 0; e < 4; ++e) acc[h][nb][e] = 0.f;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t xq[NB8][4];
 #pragma unroll
     for (int nb = 0; nb < NB8; ++nb) {
-      uint32_t b0 = xr[nb][2 * j], b1 = xr[nb][2 * j + 1];
-      if (fp0) b0 = bf2_mul(b0, pow2neg_bf16x2(fp0));
-      if (fp1) b1 = bf2_mul(b1, pow2neg_bf16x2(fp1));
-      mma16816(acc[nb], af, b0, b1);
+      if constexpr (XS) {
+        const uint4 v = xrow_s[nb][4 * q];
+        xq[nb][0] = v.x; xq[nb][1] = v.y; xq[nb][2] = v.z; xq[nb][3] = v.w;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) xq[nb][e] = xr[nb][4 * q + e];
+      }
+    }
+#pragma unroll
+    for (int jj = 0; jj < 2; ++jj) {
+      const int j = 2 * q + jj;
+      uint32_t af[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        af[i] = bf2_sub(extract<BITS>(w, j, i), zc[i & 1][slot(BITS, j, i).fp ? 1 : 0]);   // 2^fp·(q − z)
+      const int fp0 = step_fp(BITS, j, 0), fp1 = step_fp(BITS, j, 1);
+#pragma unroll
+      for (int nb = 0; nb < NB8; ++nb) {
+        uint32_t b0 = xq[nb][2 * jj], b1 = xq[nb][2 * jj + 1];
+        if (fp0) b0 = bf2_mul(b0, pow2neg_bf16x2(fp0));
+        if (fp1) b1 = bf2_mul(b1, pow2neg_bf16x2(fp1));
+        mma16816(acc[jj][nb], af, b0, b1);
+      }
     }
   }
+  const float s0 = bf16_bits_to_f32(sw & 0xFFFFu), s1 = bf16_bits_to_f32(sw >> 16);
 #pragma unroll
   for (int nb = 0; nb < NB8; ++nb) {
-    tot[nb][0] = fmaf(s0, acc[nb][0], tot[nb][0]);
-    tot[nb][1] = fmaf(s0, acc[nb][1], tot[nb][1]);
-    tot[nb][2] = fmaf(s1, acc[nb][2], tot[nb][2]);
-    tot[nb][3] = fmaf(s1, acc[nb][3], tot[nb][3]);
+    tot[nb][0] = fmaf(s0, acc[0][nb][0] + acc[1][nb][0], tot[nb][0]);
+    tot[nb][1] = fmaf(s0, acc[0][nb][1] + acc[1][nb][1], tot[nb][1]);
+    tot[nb][2] = fmaf(s1, acc[0][nb][2] + acc[1][nb][2], tot[nb][2]);
+    tot[nb][3] = fmaf(s1, acc[0][nb][3] + acc[1][nb][3], tot[nb][3]);
   }
 }
 
-// One 1 KB V piece = steps 2p, 2p+1 of a (chunk, group) tile
+// One 1 KB V piece = steps 2p, 2p+1 of a (chunk, group) tile; xv = the lane's 16 B x run.
 template <int NB8>
-__device__ __forceinline__ void v_tile(const uint8_t* piece, int p, int lane, const uint32_t (&xr)[NB8][16],
-                                       float (&tot)[NB8][4]) {
+__device__ __forceinline__ void v_tile(const uint8_t* piece, int lane, const uint4 (&xv)[NB8], float (&tot)[NB8][4]) {
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
     const uint4 v = *reinterpret_cast<const uint4*>(piece + s * 512 + lane * 16);
     const uint32_t af[4] = {v.x, v.y, v.z, v.w};
-    const int j = 2 * p + s;
 #pragma unroll
     for (int nb = 0; nb < NB8; ++nb) {
-      // j is not a compile-time constant here (p is runtime): index the pair explicitly
-      uint32_t b0, b1;
-      switch (j) {
-        case 0: b0 = xr[nb][0]; b1 = xr[nb][1]; break;
-        case 1: b0 = xr[nb][2]; b1 = xr[nb][3]; break;
-        case 2: b0 = xr[nb][4]; b1 = xr[nb][5]; break;
-        case 3: b0 = xr[nb][6]; b1 = xr[nb][7]; break;
-        case 4: b0 = xr[nb][8]; b1 = xr[nb][9]; break;
-        case 5: b0 = xr[nb][10]; b1 = xr[nb][11]; break;
-        case 6: b0 = xr[nb][12]; b1 = xr[nb][13]; break;
-        default: b0 = xr[nb][14]; b1 = xr[nb][15]; break;
-      }
-      mma16816(tot[nb], af, b0, b1);
+      if (s == 0) mma16816(tot[nb], af, xv[nb].x, xv[nb].y);
+      else        mma16816(tot[nb], af, xv[nb].z, xv[nb].w);
     }
   }
 }
 
 }  // namespace
 
-template <int BITS, int NB8>
-__global__ void __launch_bounds__(kDecodeWarps * 32) decode_kernel(const __grid_constant__ DArgs a) {
+// Warp roles: warps 0..7 stream and contract tiles; warp 8 is the epilogue warp (reduction of the
+// 8 partial sums, rank-projection publication, U·t, output).  Named barriers hand the shared
+// reduction buffer red[p] (p = item parity) between them:
+//   FULL[p]  (id 1+p): 256 tile threads arrive, the epilogue warp syncs
+//   EMPTY[p] (id 3+p): the epilogue warp arrives after reading red[p], the tile warps sync before
+//                      writing red[p] again two items later.
+template <int BITS, int NB8, bool XS>
+__global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_constant__ DArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* ring = smem + (size_t)warp * kRing * kSlotBytes;
-  float* red = reinterpret_cast<float*>(smem + (size_t)kDecodeWarps * kRing * kSlotBytes);   // [2][8][32][8]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 2 * kDecodeWarps * 32 * 8) + warp * kRing;
+  const int gid = lane >> 2, tig = lane & 3;
+  constexpr int kBlk = kTPB * kTileMax;
+  constexpr int kEpi = kDecodeWarps;          // epilogue warp index
+  float* red = reinterpret_cast<float*>(smem + (size_t)kDecodeWarps * kNBuf * kBlk);        // [2][8][32][8]
+  uint4* ubuf = reinterpret_cast<uint4*>(red + 2 * kDecodeWarps * 32 * 8);                   // [2][kUPre][32]
+  uint64_t* bars_all = reinterpret_cast<uint64_t*>(ubuf + 2 * kUPre * 32);
+  uint64_t* ubar = bars_all + kDecodeWarps * kNBuf;       // [2]
+  uint64_t* xbar = ubar + 2;
+  uint64_t* pbar = xbar + 1;
+  float4* tsm = reinterpret_cast<float4*>(xbar + 2);      // [n_chunks][NB8][32] t fragments (hi/lo source)
+  float* pstage = reinterpret_cast<float*>(tsm + (size_t)a.n_chunks * NB8 * 32);   // [nV][NB8][128]
+  uint16_t* xs = reinterpret_cast<uint16_t*>(pstage + (size_t)a.n_chunks * a.vks * NB8 * 128);
+  const int xs_ld = a.K + 32;   // +64 B per row: consecutive batch rows fall in disjoint banks
 
   if (lane == 0) {
+    if (warp < kDecodeWarps) {
 #pragma unroll
-    for (int s = 0; s < kRing; ++s) mbar_init(&bars[s], 1);
+      for (int s = 0; s < kNBuf; ++s) mbar_init(&bars_all[warp * kNBuf + s], 1);
+    } else {
+      mbar_init(&ubar[0], 1); mbar_init(&ubar[1], 1); mbar_init(xbar, 1); mbar_init(pbar, 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
-  __syncwarp();
-  const uint64_t policy = evict_first_policy();
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   const int nV = a.n_chunks * a.vks;
   const int n_items = nV + a.n_rb;
 
-  // producer cursor (tiles issued) — warp-uniform state, lane 0 issues
-  int p_item = blockIdx.x, p_t = 0;
-  Tiles p_tl = p_item < n_items ? warp_tiles(a, p_item, warp) : Tiles{0, 0};
-  unsigned issued = 0, consumed = 0;
-  auto issue = [&]() {
-    while (issued - consumed < (unsigned)kRing && p_item < n_items) {
-      if (p_t < p_tl.n) {
-        uint32_t bytes;
-        const void* src = tile_src<BITS>(a, p_item, p_tl.g0, p_t, bytes);
-        const int s = issued % kRing;
-        if (lane == 0) bulk_load(ring + s * kSlotBytes, src, bytes, &bars[s], policy);
-        ++issued;
-        ++p_t;
-      } else {
-        p_item += gridDim.x;
-        p_t = 0;
-        p_tl = p_item < n_items ? warp_tiles(a, p_item, warp) : Tiles{0, 0};
+  if (warp == kEpi) {
+    // ======================= epilogue warp =======================
+    auto prefetch_u = [&](int item, int par) {   // U fragments of a row-block item -> ubuf[par]
+      if (item < nV || item >= n_items) return;
+      const DMember& m = a.m[member_of_rb(a, item - nV)];
+      const int nck = min((m.r + 15) >> 4, kUPre);
+      if (nck == 0) return;
+      if (lane == 0) {
+        const uint32_t bytes = (uint32_t)nck * 512u;
+        mbar_expect_tx(&ubar[par], bytes);
+        bulk_copy(ubuf + par * kUPre * 32, m.U + (size_t)(item - nV - m.rb_begin) * (m.r_stored >> 4) * 32, bytes,
+                  &ubar[par], evict_first_policy());
+      }
+    };
+    prefetch_u(blockIdx.x, 0);                           // weights: before the PDL wait
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if constexpr (XS) {
+      if (lane == 0) {
+        mbar_expect_tx(xbar, (uint32_t)(a.B * a.K * 2));
+        for (int b = 0; b < a.B; ++b)
+          bulk_copy(xs + (size_t)b * xs_ld, a.x + (size_t)b * a.K, (uint32_t)(a.K * 2), xbar, evict_last_policy());
       }
     }
-  };
-  issue();
+    unsigned u_phase = 0;   // bit p = phase of ubar[p]
+    bool t_ready = false;
+    int my_rb = 0;
+    int k = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++k) {
+      const int par = k & 1;
+      if (!t_ready && item >= nV && a.m[member_of_rb(a, item - nV)].r > 0) {
+        // once per CTA, while the tile warps still stream this item: acquire the rank-projection
+        // partials, bring all of them into smem with one round of bulk copies, and sum them per
+        // chunk in slice order (deterministic t) into t fragments
+        if (lane == 0)
+          while (ld_relaxed(&a.cnt[0]) < (unsigned)nV) __nanosleep(20);
+        __syncwarp();
+        __threadfence();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        constexpr uint32_t kPB = NB8 * 512;               // bytes of one partial this CTA needs
+        if (lane == 0) mbar_expect_tx(pbar, (uint32_t)nV * kPB);
+        __syncwarp();
+        for (int i = lane; i < nV; i += 32)
+          bulk_copy(pstage + (size_t)i * (kPB / 4), a.vpart + (size_t)i * 256, kPB, pbar, evict_last_policy());
+        while (!mbar_try_wait(pbar, 0)) {}
+        for (int cc = 0; cc < a.n_chunks; ++cc) {
+#pragma unroll
+          for (int nb = 0; nb < NB8; ++nb) {
+            float4 ts = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int vs = 0; vs < a.vks; ++vs) {
+              const float4 v = *reinterpret_cast<const float4*>(
+                  pstage + ((size_t)(cc * a.vks + vs) * NB8 + nb) * 128 + gid * 16 + tig * 4);
+              ts.x += v.x; ts.y += v.y; ts.z += v.z; ts.w += v.w;
+            }
+            tsm[((size_t)cc * NB8 + nb) * 32 + lane] = ts;
+          }
+        }
+        __syncwarp();
+        t_ready = true;
+      }
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + par), "n"(kDecodeThreads) : "memory");   // FULL[par]
+      float fin[NB8][4];
+#pragma unroll
+      for (int nb = 0; nb < NB8; ++nb)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) fin[nb][e] = 0.f;
+#pragma unroll
+      for (int w = 0; w < kDecodeWarps; ++w) {            // fixed order: deterministic
+        const float* src = red + ((size_t)(par * kDecodeWarps + w) * 32 + lane) * 8;
+#pragma unroll
+        for (int nb = 0; nb < NB8; ++nb) {
+          const float4 v = *reinterpret_cast<const float4*>(src + 4 * nb);
+          fin[nb][0] += v.x; fin[nb][1] += v.y; fin[nb][2] += v.z; fin[nb][3] += v.w;
+        }
+      }
+      if (item + 2 * (int)gridDim.x < n_items)
+        asm volatile("bar.arrive %0, %1;" ::"r"(3 + par), "n"(kDecodeThreads) : "memory");   // EMPTY[par]
+      prefetch_u(item + gridDim.x, par ^ 1);
 
-  int parity = 0;
-  for (int item = blockIdx.x; item < n_items; item += gridDim.x, parity ^= 1) {
-    const Tiles tl = warp_tiles(a, item, warp);
-    const bool is_v = item < nV;
+      if (item < nV) {
+        // ---- rank-projection partial in "t layout" [b][tig][4]; publish with a release counter
+        float* vp = a.vpart + (size_t)item * 256;
+#pragma unroll
+        for (int nb = 0; nb < NB8; ++nb)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int rank = gid + 8 * (e >> 1), bl = 2 * tig + (e & 1);   // batch column nb*8 + bl
+            __stcg(vp + nb * 128 + bl * 16 + ((rank & 7) >> 1) * 4 + (rank >> 3) * 2 + (rank & 1), fin[nb][e]);
+          }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(&a.cnt[0], 1u);
+        continue;
+      }
+      // ---- row-block epilogue: + U[:, :r]·t, residual, output
+      const int rb = item - nV;
+      const DMember& m = a.m[member_of_rb(a, rb)];
+      const int rbl = rb - m.rb_begin;
+      float comp[NB8][4];
+#pragma unroll
+      for (int nb = 0; nb < NB8; ++nb)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) comp[nb][e] = 0.f;
+      if (m.r > 0) {
+        const int nck = (m.r + 15) >> 4;
+        while (!mbar_try_wait(&ubar[par], (u_phase >> par) & 1u)) {}
+        u_phase ^= 1u << par;
+        for (int c = 0; c < nck; ++c) {
+          const uint4 u = (c < kUPre) ? ubuf[(par * kUPre + c) * 32 + lane]
+                                      : __ldg(m.U + ((size_t)rbl * (m.r_stored >> 4) + c) * 32 + lane);
+          const uint32_t af[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int nb = 0; nb < NB8; ++nb) {
+            const float4 t4 = tsm[((size_t)(m.chunk_begin + c) * NB8 + nb) * 32 + lane];
+            const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
+            uint32_t hi[2], lo[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int rank0 = 16 * c + 2 * tig + 8 * h;
+              const float ta = (rank0 < m.r) ? tv[2 * h] : 0.f;
+              const float tb = (rank0 + 1 < m.r) ? tv[2 * h + 1] : 0.f;
+              const uint32_t ha = f32_to_bf16_rn(ta), hb = f32_to_bf16_rn(tb);
+              hi[h] = ha | (hb << 16);
+              lo[h] = f32_to_bf16_rn(ta - bf16_bits_to_f32(ha)) | (f32_to_bf16_rn(tb - bf16_bits_to_f32(hb)) << 16);
+            }
+            mma16816(comp[nb], af, hi[0], hi[1]);
+            mma16816(comp[nb], af, lo[0], lo[1]);
+          }
+        }
+      }
+#pragma unroll
+      for (int nb = 0; nb < NB8; ++nb)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int b = 2 * tig + (e & 1) + 8 * nb;
+          if (b >= a.B) continue;
+          const int n = m.row_off + rbl * kRows + gid + 8 * (e >> 1);
+          float v = fin[nb][e] + comp[nb][e];
+          if (a.resid) v += bf16_bits_to_f32(a.resid[(size_t)b * a.ld_resid + n]);
+          if (a.y_bf16)
+            reinterpret_cast<uint16_t*>(a.y)[(size_t)b * a.ldy + n] = (uint16_t)f32_to_bf16_rn(v);
+          else
+            reinterpret_cast<float*>(a.y)[(size_t)b * a.ldy + n] = v;
+        }
+      ++my_rb;
+    }
+    // one counter update per CTA: the CTA that completes the last row block resets the counters
+    // (every v_done reader has finished by then: they are row-block epilogues)
+    __syncwarp();
+    if (lane == 0 && my_rb > 0) {
+      __threadfence();
+      const unsigned old = atomicAdd(&a.cnt[1], (unsigned)my_rb);
+      if (old + (unsigned)my_rb == (unsigned)a.n_rb) {
+        a.cnt[0] = 0u;
+        a.cnt[1] = 0u;
+      }
+    }
+    return;
+  }
+
+  // ======================= tile warps =======================
+  uint8_t* bufs = smem + (size_t)warp * kNBuf * kBlk;    // [kNBuf][kBlk]
+  uint64_t* bars = bars_all + warp * kNBuf;
+  const uint64_t pol_w = evict_first_policy();
+  // producer: blocks of up to kTPB consecutive tiles of a share, one bulk copy each,
+  // double-buffered per warp.  State is warp-uniform; lane 0 issues.
+  int p_item = blockIdx.x, p_t = 0;
+  Share p_sh = p_item < n_items ? warp_share<BITS>(a, p_item, warp) : Share{nullptr, 0, 1024, 0, 0, 0};
+  unsigned blk_issued = 0;
+  auto issue_block = [&]() {   // issue the next non-empty block, if any
+    while (p_item < n_items && p_t >= p_sh.n) {
+      p_item += gridDim.x;
+      p_t = 0;
+      if (p_item < n_items) p_sh = warp_share<BITS>(a, p_item, warp);
+    }
+    if (p_item >= n_items) return;
+    const int nt = min(kTPB, p_sh.n - p_t);
+    const int s = blk_issued % kNBuf;
+    if (lane == 0) {
+      const uint32_t bytes = (uint32_t)(nt * p_sh.tb);
+      mbar_expect_tx(&bars[s], bytes);
+      bulk_copy(bufs + s * kBlk, p_sh.base + (size_t)p_t * p_sh.tb, bytes, &bars[s], pol_w);
+    }
+    p_t += nt;
+    ++blk_issued;
+  };
+#pragma unroll
+  for (int s = 0; s < kNBuf; ++s) issue_block();   // weights: before the PDL wait
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if constexpr (XS) {
+    while (!mbar_try_wait(xbar, 0)) {}
+  }
+  const uint16_t* xs_row[NB8];
+#pragma unroll
+  for (int nb = 0; nb < NB8; ++nb) xs_row[nb] = xs + (size_t)xrow(a, gid + 8 * nb) * xs_ld + 8 * tig;
+
+  unsigned blk_done = 0;
+  int k = 0;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++k) {
+    const int par = k & 1;
+    const Share sh = warp_share<BITS>(a, item, warp);
     float tot[NB8][4];
 #pragma unroll
     for (int nb = 0; nb < NB8; ++nb)
 #pragma unroll
       for (int e = 0; e < 4; ++e) tot[nb][e] = 0.f;
-    uint32_t xr[NB8][16];
-    int xg = -1;
-    for (int t = 0; t < tl.n; ++t) {
-      const int s = consumed % kRing;
-      const uint32_t ph = (consumed / kRing) & 1u;
-      const int g = is_v ? tl.g0 + (t >> 2) : tl.g0 + t;
-      if (g != xg) { load_x<NB8>(a, g, lane, xr); xg = g; }
-      while (!mbar_try_wait(&bars[s], ph)) {}
-      if (is_v) v_tile<NB8>(ring + s * kSlotBytes, t & 3, lane, xr, tot);
-      else      w_tile<BITS, NB8>(ring + s * kSlotBytes, lane, xr, tot);
+    for (int t0 = 0; t0 < sh.n; t0 += kTPB) {
+      const int s = blk_done % kNBuf;
+      const uint32_t ph = (blk_done / kNBuf) & 1u;
+      const int nt = min(kTPB, sh.n - t0);
+      const uint8_t* blk = bufs + s * kBlk;
+      if (sh.is_v) {
+        uint4 xv[kTPB][NB8];
+#pragma unroll
+        for (int t = 0; t < kTPB; ++t) {
+          const int piece = sh.g0 + t0 + min(t, nt - 1);
+#pragma unroll
+          for (int nb = 0; nb < NB8; ++nb) {
+            const uint4* p = reinterpret_cast<const uint4*>(
+                (XS ? xs_row[nb] : a.x + (size_t)xrow(a, gid + 8 * nb) * a.K + 8 * tig) +
+                (piece >> 2) * kGroup + 32 * (piece & 3));
+            xv[t][nb] = XS ? *p : __ldg(p);
+          }
+        }
+        while (!mbar_try_wait(&bars[s], ph)) {}
+#pragma unroll
+        for (int t = 0; t < kTPB; ++t)
+          if (t < nt) v_tile<NB8>(blk + t * 1024, lane, xv[t], tot);
+      } else {
+        while (!mbar_try_wait(&bars[s], ph)) {}
+        for (int t = 0; t < nt; ++t) {
+          const int g = sh.g0 + t0 + t;
+          uint32_t xr[NB8][16];
+          const uint4* xrs[NB8];
+#pragma unroll
+          for (int nb = 0; nb < NB8; ++nb) xrs[nb] = reinterpret_cast<const uint4*>(xs_row[nb] + g * kGroup);
+          if constexpr (!XS) load_x_global<NB8>(a, g, lane, xr);
+          w_tile<BITS, NB8, XS>(blk + t * rec_bytes(BITS), lane, xrs, xr, tot);
+        }
+      }
       __syncwarp();
-      ++consumed;
-      issue();
+      ++blk_done;
+      issue_block();
     }
-    // ---- CTA reduction of the 8 warps' partial sums (fixed order)
-    float* rb_ = red + ((size_t)(parity * kDecodeWarps + warp) * 32 + lane) * 8;
+    // ---- hand the partial sums to the epilogue warp
+    if (k >= 2) asm volatile("bar.sync %0, %1;" ::"r"(3 + par), "n"(kDecodeThreads) : "memory");   // EMPTY[par]
+    float* rb_ = red + ((size_t)(par * kDecodeWarps + warp) * 32 + lane) * 8;
 #pragma unroll
     for (int nb = 0; nb < NB8; ++nb)
       *reinterpret_cast<float4*>(rb_ + 4 * nb) = make_float4(tot[nb][0], tot[nb][1], tot[nb][2], tot[nb][3]);
-    asm volatile("bar.sync 1, %0;" ::"n"(kDecodeWarps * 32) : "memory");
-    if (warp != 0) continue;
-
-    float fin[NB8][4];
-#pragma unroll
-    for (int nb = 0; nb < NB8; ++nb)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) fin[nb][e] = 0.f;
-    for (int w = 0; w < kDecodeWarps; ++w) {
-      const float* src = red + ((size_t)(parity * kDecodeWarps + w) * 32 + lane) * 8;
-#pragma unroll
-      for (int nb = 0; nb < NB8; ++nb) {
-        const float4 v = *reinterpret_cast<const float4*>(src + 4 * nb);
-        fin[nb][0] += v.x; fin[nb][1] += v.y; fin[nb][2] += v.z; fin[nb][3] += v.w;
-      }
-    }
-    const int gid = lane >> 2, tig = lane & 3;
-    if (is_v) {
-      // ---- rank projection partial -> last arriver per chunk reduces in slice order
-      const int cc = item / a.vks;
-      float* vp = a.vpart + ((size_t)item * 32 + lane) * 8;
-#pragma unroll
-      for (int nb = 0; nb < NB8; ++nb)
-        *reinterpret_cast<float4*>(vp + 4 * nb) = make_float4(fin[nb][0], fin[nb][1], fin[nb][2], fin[nb][3]);
-      __threadfence();
-      __syncwarp();
-      unsigned old = 0;
-      if (lane == 0) old = atomicAdd(&a.cnt[cc], 1u);
-      old = __shfl_sync(0xffffffffu, old, 0);
-      if (old == (unsigned)a.vks - 1) {
-        __threadfence();
-        float sum[NB8][4];
-#pragma unroll
-        for (int nb = 0; nb < NB8; ++nb)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) sum[nb][e] = 0.f;
-        for (int vs = 0; vs < a.vks; ++vs) {
-          const float* src = a.vpart + ((size_t)(cc * a.vks + vs) * 32 + lane) * 8;
-#pragma unroll
-          for (int nb = 0; nb < NB8; ++nb) {
-            const float4 v = __ldcg(reinterpret_cast<const float4*>(src + 4 * nb));
-            sum[nb][0] += v.x; sum[nb][1] += v.y; sum[nb][2] += v.z; sum[nb][3] += v.w;
-          }
-        }
-        // fragment: rows = ranks (gid, gid+8), cols = batch (2tig, 2tig+1) + 8nb;  t[cc][b][rank]
-        float* tc = a.t + (size_t)cc * 256;
-#pragma unroll
-        for (int nb = 0; nb < NB8; ++nb)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) tc[(2 * tig + (e & 1) + 8 * nb) * 16 + gid + 8 * (e >> 1)] = sum[nb][e];
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) {
-          a.cnt[cc] = 0u;                       // self-reset for the next launch
-          atomicAdd(&a.cnt[a.n_chunks], 1u);    // t_done (release via the fence above)
-        }
-      }
-      continue;
-    }
-    // ---- row-block epilogue: + U[:, :r]·t, residual, output
-    const int rb = item - nV;
-    const DMember& m = a.m[member_of_rb(a, rb)];
-    const int rbl = rb - m.rb_begin;
-    float comp[NB8][4];
-#pragma unroll
-    for (int nb = 0; nb < NB8; ++nb)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) comp[nb][e] = 0.f;
-    if (m.r > 0) {
-      if (lane == 0)
-        while (ld_acquire(&a.cnt[a.n_chunks]) < (unsigned)a.n_chunks) __nanosleep(64);
-      __syncwarp();
-      const int nck = (m.r + 15) >> 4;
-      for (int c = 0; c < nck; ++c) {
-        const uint4 u = __ldg(m.U + ((size_t)rbl * (m.r_stored >> 4) + c) * 32 + lane);
-        const uint32_t af[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-        for (int nb = 0; nb < NB8; ++nb) {
-          const int b = gid + 8 * nb;
-          const float* tp = a.t + ((size_t)(m.chunk_begin + c) * 16 + b) * 16;
-          float tv[4];
-          const float2 v01 = __ldcg(reinterpret_cast<const float2*>(tp + 2 * tig));
-          const float2 v89 = __ldcg(reinterpret_cast<const float2*>(tp + 2 * tig + 8));
-          tv[0] = v01.x; tv[1] = v01.y; tv[2] = v89.x; tv[3] = v89.y;
-          uint32_t hi[2], lo[2];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int rank0 = 16 * c + 2 * tig + 8 * h;
-            const float ta = (rank0 < m.r) ? tv[2 * h] : 0.f;
-            const float tb = (rank0 + 1 < m.r) ? tv[2 * h + 1] : 0.f;
-            const uint32_t ha = f32_to_bf16_rn(ta), hb = f32_to_bf16_rn(tb);
-            hi[h] = ha | (hb << 16);
-            lo[h] = f32_to_bf16_rn(ta - bf16_bits_to_f32(ha)) | (f32_to_bf16_rn(tb - bf16_bits_to_f32(hb)) << 16);
-          }
-          mma16816(comp[nb], af, hi[0], hi[1]);
-          mma16816(comp[nb], af, lo[0], lo[1]);
-        }
-      }
-    }
-#pragma unroll
-    for (int nb = 0; nb < NB8; ++nb)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int b = 2 * tig + (e & 1) + 8 * nb;
-        if (b >= a.B) continue;
-        const int n = m.row_off + rbl * kRows + gid + 8 * (e >> 1);
-        float v = fin[nb][e] + comp[nb][e];
-        if (a.resid) v += bf16_bits_to_f32(a.resid[(size_t)b * a.ld_resid + n]);
-        if (a.y_bf16)
-          reinterpret_cast<uint16_t*>(a.y)[(size_t)b * a.ldy + n] = (uint16_t)f32_to_bf16_rn(v);
-        else
-          reinterpret_cast<float*>(a.y)[(size_t)b * a.ldy + n] = v;
-      }
-    __syncwarp();
-    if (lane == 0) {
-      const unsigned old = atomicAdd(&a.cnt[a.n_chunks + 1], 1u);
-      if (old == (unsigned)a.n_rb - 1) {       // last row block of the launch: reset counters
-        a.cnt[a.n_chunks] = 0u;
-        a.cnt[a.n_chunks + 1] = 0u;
-      }
-    }
+    asm volatile("bar.arrive %0, %1;" ::"r"(1 + par), "n"(kDecodeThreads) : "memory");            // FULL[par]
   }
 }
 
-static size_t decode_smem_bytes() {
-  return (size_t)kDecodeWarps * kRing * kSlotBytes + 2 * kDecodeWarps * 32 * 8 * sizeof(float) +
-         kDecodeWarps * kRing * sizeof(uint64_t);
+static size_t decode_smem_bytes(bool xs, int B, int K, int n_chunks, int vks) {
+  const int nb8 = B > 8 ? 2 : 1;
+  size_t s = (size_t)kDecodeWarps * kNBuf * kTPB * kTileMax + 2 * kDecodeWarps * 32 * 8 * sizeof(float) +
+             2 * kUPre * 32 * 16 + (kDecodeWarps * kNBuf + 4) * sizeof(uint64_t) +
+             (size_t)n_chunks * nb8 * 32 * 16 + (size_t)n_chunks * vks * nb8 * 512;
+  if (xs) s += (size_t)B * (K + 32) * 2;
+  return s;
 }
 
-template <int BITS, int NB8>
+constexpr size_t kXsMax = 48 * 1024;
+constexpr size_t kSmemOptin = 227 * 1024;   // x staged in smem when B*(K+32)*2 fits this
+
+static bool use_xs(int B, int K) { return B <= 8 && (size_t)B * (K + 32) * 2 <= kXsMax; }
+
+template <int BITS, int NB8, bool XS>
 static cudaError_t launch_t(const DArgs& a, int grid, cudaStream_t st) {
-  const size_t smem = decode_smem_bytes();
+  const size_t smem = decode_smem_bytes(XS, a.B, a.K, a.n_chunks, a.vks);
+  if (smem > kSmemOptin) return cudaErrorInvalidConfiguration;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(decode_kernel<BITS, NB8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(decode_kernel<BITS, NB8, XS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kSmemOptin);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  decode_kernel<BITS, NB8><<<grid, kDecodeWarps * 32, smem, st>>>(a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kDecodeThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, decode_kernel<BITS, NB8, XS>, a);
 }
 
-template <int BITS, int NB8>
-static int max_ctas_t() {
-  const size_t smem = decode_smem_bytes();
-  cudaFuncSetAttribute(decode_kernel<BITS, NB8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <int BITS, int NB8, bool XS>
+static int max_ctas_t(int B, int K, int n_chunks, int vks) {
+  const size_t smem = decode_smem_bytes(XS, B, K, n_chunks, vks);
+  cudaFuncSetAttribute(decode_kernel<BITS, NB8, XS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kSmemOptin);
   int per_sm = 0, dev = 0, sms = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<BITS, NB8>, kDecodeWarps * 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<BITS, NB8, XS>, kDecodeThreads, smem);
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   return per_sm * sms;
 }
 
+#define HC_DISPATCH(FN, ...)                                                       \
+  do {                                                                             \
+    const bool two = a_B > 8, xs = use_xs(a_B, a_K);                               \
+    switch (bits) {                                                                \
+      case 2: return two ? FN<2, 2, false>(__VA_ARGS__)                            \
+                         : (xs ? FN<2, 1, true>(__VA_ARGS__) : FN<2, 1, false>(__VA_ARGS__)); \
+      case 3: return two ? FN<3, 2, false>(__VA_ARGS__)                            \
+                         : (xs ? FN<3, 1, true>(__VA_ARGS__) : FN<3, 1, false>(__VA_ARGS__)); \
+      case 4: return two ? FN<4, 2, false>(__VA_ARGS__)                            \
+                         : (xs ? FN<4, 1, true>(__VA_ARGS__) : FN<4, 1, false>(__VA_ARGS__)); \
+      default: break;                                                              \
+    }                                                                              \
+  } while (0)
+
 cudaError_t launch_decode(const DArgs& a, int bits, int grid, cudaStream_t st) {
-  const bool two = a.B > 8;
-  switch (bits) {
-    case 2: return two ? launch_t<2, 2>(a, grid, st) : launch_t<2, 1>(a, grid, st);
-    case 3: return two ? launch_t<3, 2>(a, grid, st) : launch_t<3, 1>(a, grid, st);
-    case 4: return two ? launch_t<4, 2>(a, grid, st) : launch_t<4, 1>(a, grid, st);
-    default: return cudaErrorInvalidValue;
-  }
+  const int a_B = a.B, a_K = a.K;
+  HC_DISPATCH(launch_t, a, grid, st);
+  return cudaErrorInvalidValue;
 }
 
-int decode_max_ctas(int bits, int B) {
-  const bool two = B > 8;
-  switch (bits) {
-    case 2: return two ? max_ctas_t<2, 2>() : max_ctas_t<2, 1>();
-    case 3: return two ? max_ctas_t<3, 2>() : max_ctas_t<3, 1>();
-    case 4: return two ? max_ctas_t<4, 2>() : max_ctas_t<4, 1>();
-    default: return 0;
-  }
+int decode_max_ctas(int bits, int B, int K, int n_chunks, int vks) {
+  const int a_B = B, a_K = K;
+  HC_DISPATCH(max_ctas_t, B, K, n_chunks, vks);
+  return 0;
 }
 
 }  // namespace hc

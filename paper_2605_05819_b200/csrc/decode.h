@@ -6,9 +6,14 @@
 namespace hc {
 
 constexpr int kMaxMembers = 4;
-constexpr int kDecodeWarps = 8;          // consumer warps per CTA
-constexpr int kRing = 4;                 // bulk-copy ring slots per warp
-constexpr int kSlotBytes = 1088;         // >= rec_bytes(4) = 1072, >= 1 KB V piece
+constexpr int kDecodeWarps = 8;          // tile (streaming + contraction) warps per CTA
+constexpr int kDecodeThreads = (kDecodeWarps + 1) * 32;   // + one epilogue warp
+constexpr int kMaxChunks = 32;           // Σ ceil(r_m/16) over a window's members
+constexpr int kTPB = 4;                  // tiles per bulk-copy block
+constexpr int kNBuf = 2;                 // block buffers per warp (double buffering)
+constexpr int kTileMax = 1088;           // >= rec_bytes(4) = 1072, >= 1 KB V piece
+constexpr int kUPre = 4;                 // U chunks (16 ranks each) staged in smem per item
+constexpr int kMaxVks = 16;
 
 struct DMember {
   const uint8_t* rec;   // [n_rb][G][rec_bytes]          (layout.h)
@@ -34,15 +39,14 @@ struct DArgs {
   int glue;             // 0 none; 1 SiLU(gate)*up with interleaved up/gate rows (see api)
   int n_rb;             // Σ members
   int n_chunks;         // Σ ceil(r_m / 16)
-  int vks;              // K-slices per V chunk
-  float* vpart;         // [n_chunks * vks][32][8]
-  float* t;             // [n_chunks][16 batch][16 ranks]
-  unsigned* cnt;        // [n_chunks] chunk counters, [n_chunks] t_done, [n_chunks+1] w_done
+  int vks;              // K-slices per V chunk (<= kMaxVks)
+  float* vpart;         // [n_chunks * vks][16 batch][4 tig][4]  rank-projection partials
+  unsigned* cnt;        // [0] v_done, [1] w_done (self-resetting)
 };
 
 // Launch the fused window kernel; bits in {2,3,4}; 1 <= B <= 16.
 cudaError_t launch_decode(const DArgs& a, int bits, int grid, cudaStream_t st);
 // Max co-resident CTAs of the decode kernel on this device (persistent grid size).
-int decode_max_ctas(int bits, int B);
+int decode_max_ctas(int bits, int B, int K, int n_chunks, int vks);
 
 }  // namespace hc

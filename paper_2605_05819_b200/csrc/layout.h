@@ -12,9 +12,9 @@
 // per (rb, group), the A-fragments of all eight k16 steps of the group:
 //     lane = 4*gid + tig;  register (j, i), step j in 0..7, reg i in 0..3 holds
 //     row  = gid + 8*(i&1)
-//     k_lo = 32*tig + 4*j + 2*(i>>1),  k_hi = k_lo + 1     (k within the group)
-// The k permutation is legal because the per-group partial sum is order-free;
-// it makes each lane's x values contiguous (x[32*tig + 4j .. +3] per step).
+//     k_lo = 32*(j>>1) + 8*tig + 4*(j&1) + 2*(i>>1),  k_hi = k_lo + 1   (k within the group)
+// The k permutation is legal because the per-group partial sum is order-free; it makes
+// lane tig's x values for steps (2q, 2q+1) one 16-byte run x[32q + 8tig .. +7].
 //
 // Record for (rb, group) = [codes: 32 lanes x 2*bits words][scales 8 x u32][zeros u64][pad 8]
 //   codes word w of lane l at byte  (w/4)*512 + l*16 + (w%4)*4   for w < 4*(2b/4)
@@ -87,7 +87,12 @@ HC_HD constexpr int step_fp(int bits, int j, int pair) { return slot(bits, j, 2 
 
 // Fragment element -> (row within rb, k within group)
 HC_HD constexpr int frag_row(int lane, int i) { return (lane >> 2) + 8 * (i & 1); }
-HC_HD constexpr int frag_k(int lane, int j, int i, int hi) { return 32 * (lane & 3) + 4 * j + 2 * (i >> 1) + hi; }
+// k within the group: 32*(j>>1) + 8*tig + 4*(j&1) + 2*(i>>1) + hi.  For a fixed pair of steps
+// (2q, 2q+1) the four tig lanes of a row read one contiguous 64 B run of x (16 B each), so
+// 128-bit x loads are conflict-free in shared memory and fully coalesced in global memory.
+HC_HD constexpr int frag_k(int lane, int j, int i, int hi) {
+  return 32 * (j >> 1) + 8 * (lane & 3) + 4 * (j & 1) + 2 * (i >> 1) + hi;
+}
 
 // Compensation factor tiles (bf16, no quantisation):
 //  U: [rb][chunk c = rank/16][lane][uint4]; reg i of lane: row gid + 8(i&1), ranks 16c + 2tig + 8(i>>1) + {0,1}
