@@ -249,6 +249,8 @@ hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int B, void* y, int
     w.ws_chunks = max_chunks;
   }
   if (a.n_chunks > kMaxChunks) return fail(HC_ERR_CONFIG, "window ranks need %d chunks > %d", a.n_chunks, kMaxChunks);
+  static const int dbg = [] { const char* e = getenv("HC_DECODE_DEBUG"); return e ? atoi(e) : 0; }();
+  a.dbg = dbg;
   a.vpart = (float*)w.vpart.p;
   a.cnt = (unsigned*)w.cnt.p;
   const auto key = std::make_tuple(m0.bits, B, a.K, a.n_chunks, a.vks);

@@ -109,6 +109,19 @@ __device__ __forceinline__ constexpr uint32_t pow2neg_bf16x2(int fp) {   // bf16
   return (uint32_t)(0x3F80 - (fp << 7)) * 0x00010001u;
 }
 
+// (a & b) | c in one LOP3 (nvcc otherwise emits two)
+__device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// w >> s; shifts of 8 or more run as IMAD.HI on the FMA pipe to balance it against the ALU pipe
+// (which carries the LOP3s)
+__device__ __forceinline__ uint32_t shr(uint32_t w, int s) {
+  return s == 0 ? w : (s >= 8 ? __umulhi(w, 1u << (32 - s)) : (w >> s));
+}
+
 template <int BITS>
 __device__ __forceinline__ uint32_t extract(const uint32_t (&w)[2 * BITS], int j, int i) {
   const Slot s = slot(BITS, j, i);
@@ -118,7 +131,7 @@ __device__ __forceinline__ uint32_t extract(const uint32_t (&w)[2 * BITS], int j
     if (p < s.nparts) {
       uint32_t m = ((1u << s.p[p].nbits) - 1u) << s.p[p].pos;
       m |= m << 16;
-      acc |= (w[s.p[p].word] >> s.p[p].shift) & m;
+      acc = and_or(shr(w[s.p[p].word], s.p[p].shift), m, acc);
     }
   }
   return acc;
@@ -246,8 +259,9 @@ __device__ __forceinline__ void w_tile(const uint8_t* rec, int lane, const uint4
       const int j = 2 * q + jj;
       uint32_t af[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        af[i] = bf2_sub(extract<BITS>(w, j, i), zc[i & 1][slot(BITS, j, i).fp ? 1 : 0]);   // 2^fp·(q − z)
+      for (int i = 0; i < 4; ++i) {
+        af[i] = bf2_sub(extract<BITS>(w, j, i), zc[i & 1][slot(BITS, j, i).fp ? 1 : 0]);   // 2^fp·(q − z), exact
+      }
       const int fp0 = step_fp(BITS, j, 0), fp1 = step_fp(BITS, j, 1);
 #pragma unroll
       for (int nb = 0; nb < NB8; ++nb) {
@@ -494,6 +508,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_
   Share p_sh = p_item < n_items ? warp_share<BITS>(a, p_item, warp) : Share{nullptr, 0, 1024, 0, 0, 0};
   unsigned blk_issued = 0;
   auto issue_block = [&]() {   // issue the next non-empty block, if any
+    if (a.dbg == 2 && blk_issued >= kNBuf) return;   // dev knob: compute on stale tiles, no streaming
     while (p_item < n_items && p_t >= p_sh.n) {
       p_item += gridDim.x;
       p_t = 0;
@@ -553,13 +568,14 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_
         for (int t = 0; t < kTPB; ++t)
           if (t < nt) v_tile<NB8>(blk + t * 1024, lane, xv[t], tot);
       } else {
-        while (!mbar_try_wait(&bars[s], ph)) {}
+        if (a.dbg != 2 || blk_done < kNBuf) { while (!mbar_try_wait(&bars[s], ph)) {} }
         for (int t = 0; t < nt; ++t) {
           const int g = sh.g0 + t0 + t;
           uint32_t xr[NB8][16];
           const uint4* xrs[NB8];
 #pragma unroll
           for (int nb = 0; nb < NB8; ++nb) xrs[nb] = reinterpret_cast<const uint4*>(xs_row[nb] + g * kGroup);
+          if (a.dbg == 1) { tot[0][0] += (float)blk[t * rec_bytes(BITS) + lane]; continue; }
           if constexpr (!XS) load_x_global<NB8>(a, g, lane, xr);
           w_tile<BITS, NB8, XS>(blk + t * rec_bytes(BITS), lane, xrs, xr, tot);
         }

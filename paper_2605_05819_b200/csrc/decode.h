@@ -9,8 +9,8 @@ constexpr int kMaxMembers = 4;
 constexpr int kDecodeWarps = 8;          // tile (streaming + contraction) warps per CTA
 constexpr int kDecodeThreads = (kDecodeWarps + 1) * 32;   // + one epilogue warp
 constexpr int kMaxChunks = 32;           // Σ ceil(r_m/16) over a window's members
-constexpr int kTPB = 4;                  // tiles per bulk-copy block
-constexpr int kNBuf = 2;                 // block buffers per warp (double buffering)
+constexpr int kTPB = 2;                  // tiles per bulk-copy block
+constexpr int kNBuf = 4;                 // block buffers per warp (3 blocks in flight while one computes)
 constexpr int kTileMax = 1088;           // >= rec_bytes(4) = 1072, >= 1 KB V piece
 constexpr int kUPre = 4;                 // U chunks (16 ranks each) staged in smem per item
 constexpr int kMaxVks = 16;
@@ -42,6 +42,7 @@ struct DArgs {
   int vks;              // K-slices per V chunk (<= kMaxVks)
   float* vpart;         // [n_chunks * vks][16 batch][4 tig][4]  rank-projection partials
   unsigned* cnt;        // [0] v_done, [1] w_done (self-resetting)
+  int dbg;              // development knob (HC_DECODE_DEBUG): 1 = stream tiles without contracting them
 };
 
 // Launch the fused window kernel; bits in {2,3,4}; 1 <= B <= 16.
