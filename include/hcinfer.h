@@ -39,6 +39,7 @@ typedef enum {
 
 typedef enum { HC_WIN_QKV = 0, HC_WIN_O = 1, HC_WIN_UPGATE = 2, HC_WIN_DOWN = 3 } hc_window_kind;
 typedef enum { HC_OUT_F32 = 0, HC_OUT_BF16 = 1 } hc_out_dtype;
+typedef enum { HC_GLUE_NONE = 0, HC_GLUE_SILU_MUL = 1 } hc_glue;
 
 const char* hc_version(void);
 const char* hc_last_error(void);
@@ -106,7 +107,12 @@ hc_status hc_destroy(hc_ctx* ctx);
  * r_alloc in {0} ∪ {8, 16, 32, ...}, r_alloc <= min(r_stored, N, K).
  * row_begin/row_end: the rows [row_begin, row_end) this context keeps (column sharding of
  * the output across GPUs); use 0 / N for an unsharded matrix.
- * (row_end - row_begin) % 16 == 0. */
+ * (row_end - row_begin) % 16 == 0.
+ * glue: HC_GLUE_SILU_MUL fuses the FFN gate (App. A.1.3, "h = σ(W_gate X) ⊙ W_up X", σ = SiLU)
+ * into an UPGATE window: slot 0 = up and slot 1 = gate, same shape, loaded in the SAME call, both
+ * flagged; their rows are interleaved at load time (8 up + 8 gate rows per row block) so the
+ * window outputs m = silu(gate·x) ⊙ (up·x) (each product compensated at its own rank), width N.
+ * Otherwise HC_GLUE_NONE. */
 typedef struct {
   int32_t layer, window_kind, slot, expert;
   int32_t N, K, bits, group;
@@ -117,6 +123,7 @@ typedef struct {
   const uint16_t* V;
   int32_t r_stored, r_alloc;
   int32_t row_begin, row_end;
+  int32_t glue;
 } hc_matrix_desc;
 
 /* Copy + repack matrices into context-owned device memory (synchronous w.r.t. its inputs:
@@ -145,6 +152,18 @@ int64_t hc_window_rows(hc_ctx* ctx, int32_t layer, int32_t window_kind, int32_t 
  *   the stream before returning). */
 hc_status hc_compensated_linear(hc_ctx* ctx, int32_t layer, int32_t window_kind, int32_t expert,
                                 const void* x, int32_t B, void* y, int32_t y_dtype, void* stream);
+
+/* Decode step through every loaded dense layer 0..L-1 (R9):
+ *   a  = q-part of QKV(h)          (attention is out of scope: identity stand-in on q)
+ *   h1 = bf16(h + O(a))            (residual fused into the O epilogue)
+ *   m  = bf16(silu(gate) ⊙ up)     (UPGATE loaded with HC_GLUE_SILU_MUL)
+ *   h' = bf16(h1 + DOWN(m))        (residual fused into the DOWN epilogue)
+ * x: bf16 [B][d] (input hidden state), y: bf16 [B][d] (output of the last layer), 1 <= B <= 16.
+ * Every window is one fused decode launch (4 per layer) with programmatic dependent launch; the
+ * whole stack is captured once per (B, x, y) into a CUDA graph owned by the context and replayed
+ * (re-captured after hc_load_layer / hc_set_rank).  Host x / y are staged like hc_compensated_linear.
+ * HC_ERR_STATE if a layer lacks a window or its UPGATE window is not SiLU-fused. */
+hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, void* y, void* stream);
 
 /* Debug/test exports (host only, no GPU needed): the load-time repack and its inverse. */
 size_t hc_repacked_bytes(int32_t N, int32_t K, int32_t bits);

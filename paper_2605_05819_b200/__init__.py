@@ -14,9 +14,10 @@ import numpy as np
 
 from . import _lib
 from ._lib import (HCError, HC_OK, HC_ERR_CONFIG, HC_ERR_STATE, HC_ERR_NUMERIC, HC_ERR_RUNTIME,
-                   QKV, O, UPGATE, DOWN, OUT_F32, OUT_BF16, check, lib)
+                   QKV, O, UPGATE, DOWN, OUT_F32, OUT_BF16, GLUE_NONE, GLUE_SILU_MUL, check, lib)
 
 __all__ = ["allocate_ranks", "Context", "HCError", "QKV", "O", "UPGATE", "DOWN", "OUT_F32", "OUT_BF16",
+           "GLUE_NONE", "GLUE_SILU_MUL",
            "repack_host", "unpack_repacked_host", "lib"]
 
 
@@ -132,6 +133,7 @@ class Context:
             d.U, d.V = _ptr(m.get("U")), _ptr(m.get("V"))
             d.r_stored, d.r_alloc = int(m.get("r_stored", 0)), int(m.get("r_alloc", 0))
             d.row_begin, d.row_end = int(m.get("row_begin", 0)), int(m.get("row_end", m["N"]))
+            d.glue = int(m.get("glue", 0))
         check(lib().hc_load_layer(self._h, arr, len(mats), _stream(stream)))
 
     def set_rank(self, layer, window, slot, r, expert=-1):
@@ -139,6 +141,13 @@ class Context:
 
     def window_rows(self, layer, window, expert=-1) -> int:
         return int(lib().hc_window_rows(self._h, layer, window, expert))
+
+    def stack_forward(self, x, y, B=None, stream=None):
+        """hc_stack_forward: one decode step through all loaded layers (bf16 in, bf16 out)."""
+        if B is None:
+            B = x.shape[0]
+        check(lib().hc_stack_forward(self._h, _ptr(x), int(B), _ptr(y), _stream(stream)))
+        return y
 
     def compensated_linear(self, layer, window, x, y, B=None, expert=-1, out_dtype=OUT_F32, stream=None):
         """y[b, :] = concat_m ( deq(W_m)·x_b + U_m[:, :r_m]·(V_m[:r_m, :]·x_b) ).

@@ -12,6 +12,7 @@ LIB_PATH = os.path.join(_PKG, "libhcinfer.so")
 HC_OK, HC_ERR_CONFIG, HC_ERR_STATE, HC_ERR_NUMERIC, HC_ERR_RUNTIME = 0, 2, 3, 4, 5
 QKV, O, UPGATE, DOWN = 0, 1, 2, 3
 OUT_F32, OUT_BF16 = 0, 1
+GLUE_NONE, GLUE_SILU_MUL = 0, 1
 
 
 class HCError(RuntimeError):
@@ -37,7 +38,8 @@ class hc_matrix_desc(C.Structure):
                 ("N", C.c_int32), ("K", C.c_int32), ("bits", C.c_int32), ("group", C.c_int32),
                 ("codes", C.c_void_p), ("scales", C.c_void_p), ("zeros", C.c_void_p),
                 ("U", C.c_void_p), ("V", C.c_void_p),
-                ("r_stored", C.c_int32), ("r_alloc", C.c_int32), ("row_begin", C.c_int32), ("row_end", C.c_int32)]
+                ("r_stored", C.c_int32), ("r_alloc", C.c_int32), ("row_begin", C.c_int32), ("row_end", C.c_int32),
+                ("glue", C.c_int32)]
 
 
 # (name, restype, argtypes) — every symbol include/hcinfer.h declares
@@ -53,6 +55,7 @@ SIGNATURES = [
     ("hc_window_rows", C.c_int64, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32]),
     ("hc_compensated_linear", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_int32,
                                         C.c_void_p, C.c_int32, C.c_void_p]),
+    ("hc_stack_forward", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     ("hc_repacked_bytes", C.c_size_t, [C.c_int32, C.c_int32, C.c_int32]),
     ("hc_repack_host", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
     ("hc_unpack_repacked_host", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,

@@ -1,7 +1,8 @@
-// C-ABI: context, load_layer (copy + repack), set_rank, compensated_linear (hcinfer.h).
+// C-ABI: context, load_layer (copy + repack), set_rank, compensated_linear, stack_forward (hcinfer.h).
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -35,16 +36,23 @@ struct DevBuf {
 
 struct Member {
   int slot = 0, N = 0, K = 0, bits = 0, r_stored = 0, r_alloc = 0, row_begin = 0, row_end = 0;
-  std::shared_ptr<DevBuf> rec, U, V;
+  std::shared_ptr<DevBuf> rec, U, V;   // rec/U empty for the gate member of a fused SiLU window
   int rows() const { return row_end - row_begin; }
   int cap() const { return std::min(std::min(r_stored, N), K); }
 };
 
 struct Window {
   int layer = 0, kind = 0, expert = -1;
+  int glue = HC_GLUE_NONE;            // SILU_MUL: members[0] = up (interleaved records), [1] = gate
   std::vector<Member> members;        // sorted by slot
   DevBuf vpart, cnt;                  // launch workspace (self-resetting counters)
   int ws_chunks = -1;
+  int64_t out_rows() const {
+    if (glue == HC_GLUE_SILU_MUL) return members.front().rows();
+    int64_t n = 0;
+    for (const Member& m : members) n += m.rows();
+    return n;
+  }
 };
 
 using Key = std::tuple<int, int, int>;
@@ -58,6 +66,11 @@ bool is_device_ptr(const void* p) {
 
 bool admissible_rank(int r) { return r == 0 || (r >= 8 && (r & (r - 1)) == 0); }
 
+struct StackGraph {
+  cudaGraphExec_t exec = nullptr;
+  ~StackGraph() { if (exec) cudaGraphExecDestroy(exec); }
+};
+
 }  // namespace
 
 struct hc_ctx {
@@ -66,6 +79,11 @@ struct hc_ctx {
   std::map<Key, Window> windows;
   std::map<std::tuple<int, int, int, int, int>, int> max_ctas;   // (bits, B, K, chunks, vks) -> co-resident CTAs
   DevBuf stage_x, stage_y;
+  // decode stack (hc_stack_forward)
+  DevBuf s_h, s_h1, s_qkv, s_m;
+  std::map<std::tuple<int, const void*, void*>, std::unique_ptr<StackGraph>> graphs;
+  cudaStream_t cap_stream = nullptr;
+  void invalidate_graphs() { graphs.clear(); }
 };
 
 #define CUDA_TRY(expr)                                                                       \
@@ -74,7 +92,7 @@ struct hc_ctx {
     if (_e != cudaSuccess) return fail(HC_ERR_RUNTIME, "%s: %s", #expr, cudaGetErrorString(_e)); \
   } while (0)
 
-extern "C" const char* hc_version(void) { return "hcinfer-b200 0.1 (sm_100a)"; }
+extern "C" const char* hc_version(void) { return "hcinfer-b200 0.2 (sm_100a)"; }
 extern "C" const char* hc_last_error(void) { return hc::last_error_buf(); }
 
 extern "C" hc_status hc_create(hc_ctx** out, int32_t device) {
@@ -92,6 +110,10 @@ extern "C" hc_status hc_create(hc_ctx** out, int32_t device) {
   hc_ctx* c = new hc_ctx();
   c->device = device;
   c->sms = prop.multiProcessorCount;
+  if (cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return fail(HC_ERR_RUNTIME, "hc_create: stream creation failed");
+  }
   *out = c;
   return HC_OK;
 }
@@ -100,6 +122,8 @@ extern "C" hc_status hc_destroy(hc_ctx* ctx) {
   if (!ctx) return HC_OK;
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
+  ctx->graphs.clear();
+  if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   delete ctx;
   return HC_OK;
 }
@@ -117,10 +141,21 @@ static hc_status validate_desc(const hc_matrix_desc& d, int i) {
     return fail(HC_ERR_CONFIG, "mat %d: r_alloc %d not admissible or > cap", i, d.r_alloc);
   if (!d.codes || !d.scales || !d.zeros) return fail(HC_ERR_CONFIG, "mat %d: null codes/scales/zeros", i);
   if (d.r_stored > 0 && (!d.U || !d.V)) return fail(HC_ERR_CONFIG, "mat %d: r_stored > 0 needs U and V", i);
+  if (d.glue != HC_GLUE_NONE && d.glue != HC_GLUE_SILU_MUL) return fail(HC_ERR_CONFIG, "mat %d: glue %d", i, d.glue);
+  if (d.glue == HC_GLUE_SILU_MUL && (d.window_kind != HC_WIN_UPGATE || (d.slot != 0 && d.slot != 1)))
+    return fail(HC_ERR_CONFIG, "mat %d: SiLU glue needs an UPGATE window with slots 0 (up) and 1 (gate)", i);
   return HC_OK;
 }
 
-// copy a host or device source to a device temporary (or return the device pointer)
+// Canonical (host or device) inputs of one matrix, resident on the device for the repack.
+struct Staged {
+  DevBuf tc, ts, tz, tu, tv;
+  const uint32_t* codes = nullptr;
+  const uint16_t* scales = nullptr;
+  const uint8_t* zeros = nullptr;
+  const uint16_t *U = nullptr, *V = nullptr;
+};
+
 static const void* to_device(const void* src, size_t bytes, DevBuf& tmp, cudaStream_t st, cudaError_t& err) {
   err = cudaSuccess;
   if (is_device_ptr(src)) return src;
@@ -128,6 +163,34 @@ static const void* to_device(const void* src, size_t bytes, DevBuf& tmp, cudaStr
   if (err != cudaSuccess) return nullptr;
   err = cudaMemcpyAsync(tmp.p, src, bytes, cudaMemcpyHostToDevice, st);
   return tmp.p;
+}
+
+static hc_status stage(const hc_matrix_desc& d, Staged& s, cudaStream_t st) {
+  const int G = d.K / hc::kGroup;
+  cudaError_t e;
+  s.codes = (const uint32_t*)to_device(d.codes, (size_t)d.N * d.K * d.bits / 8, s.tc, st, e);
+  CUDA_TRY(e);
+  s.scales = (const uint16_t*)to_device(d.scales, (size_t)d.N * G * 2, s.ts, st, e);
+  CUDA_TRY(e);
+  s.zeros = (const uint8_t*)to_device(d.zeros, (size_t)d.N * G, s.tz, st, e);
+  CUDA_TRY(e);
+  if (d.r_stored > 0) {
+    s.U = (const uint16_t*)to_device(d.U, (size_t)d.N * d.r_stored * 2, s.tu, st, e);
+    CUDA_TRY(e);
+    s.V = (const uint16_t*)to_device(d.V, (size_t)d.r_stored * d.K * 2, s.tv, st, e);
+    CUDA_TRY(e);
+  }
+  return HC_OK;
+}
+
+static Member make_member(const hc_matrix_desc& d) {
+  Member m;
+  m.slot = d.slot; m.N = d.N; m.K = d.K; m.bits = d.bits; m.r_stored = d.r_stored; m.r_alloc = d.r_alloc;
+  m.row_begin = d.row_begin; m.row_end = d.row_end;
+  m.rec = std::make_shared<DevBuf>();
+  m.U = std::make_shared<DevBuf>();
+  m.V = std::make_shared<DevBuf>();
+  return m;
 }
 
 extern "C" hc_status hc_load_layer(hc_ctx* ctx, const hc_matrix_desc* mats, int32_t n_mats, void* stream) {
@@ -139,49 +202,97 @@ extern "C" hc_status hc_load_layer(hc_ctx* ctx, const hc_matrix_desc* mats, int3
     hc_status s = validate_desc(mats[i], i);
     if (s != HC_OK) return s;
   }
+  ctx->invalidate_graphs();
+  std::vector<char> done(n_mats, 0);
   for (int i = 0; i < n_mats; ++i) {
+    if (done[i]) continue;
     const hc_matrix_desc& d = mats[i];
     Key key{d.layer, d.window_kind, d.expert};
     Window& w = ctx->windows[key];
     w.layer = d.layer; w.kind = d.window_kind; w.expert = d.expert;
+    const int G = d.K / hc::kGroup;
+
+    if (d.glue == HC_GLUE_SILU_MUL) {
+      // ---- fused SiLU(gate)·up window: find the partner in this call, interleave rows 8 + 8
+      int j = -1;
+      for (int k = 0; k < n_mats; ++k)
+        if (k != i && !done[k] && mats[k].glue == HC_GLUE_SILU_MUL && mats[k].layer == d.layer &&
+            mats[k].window_kind == d.window_kind && mats[k].expert == d.expert && mats[k].slot != d.slot)
+          j = k;
+      if (j < 0) return fail(HC_ERR_CONFIG, "mat %d: SiLU glue needs up and gate in the same hc_load_layer call", i);
+      const hc_matrix_desc& up = d.slot == 0 ? d : mats[j];
+      const hc_matrix_desc& gate = d.slot == 0 ? mats[j] : d;
+      if (up.N != gate.N || up.K != gate.K || up.bits != gate.bits || up.r_stored != gate.r_stored ||
+          up.row_begin != gate.row_begin || up.row_end != gate.row_end)
+        return fail(HC_ERR_CONFIG, "SiLU glue: up and gate must have identical shape, bits, r_stored and shard");
+      Member mu = make_member(up), mg = make_member(gate);
+      const int rows = mu.rows();
+      Staged su, sg;
+      hc_status s = stage(up, su, st);
+      if (s != HC_OK) return s;
+      s = stage(gate, sg, st);
+      if (s != HC_OK) return s;
+      CUDA_TRY(mu.rec->alloc((size_t)(rows / 8) * G * hc::rec_bytes(up.bits)));
+      if (up.r_stored > 0) {
+        CUDA_TRY(mu.U->alloc((size_t)2 * rows * up.r_stored * 2));
+        CUDA_TRY(mu.V->alloc((size_t)up.r_stored * up.K * 2));
+        CUDA_TRY(mg.V->alloc((size_t)gate.r_stored * gate.K * 2));
+      }
+      const int wpr = up.K * up.bits / 32;
+      hc::RepackSrc src;
+      src.codes[0] = su.codes + (size_t)up.row_begin * wpr;  src.codes[1] = sg.codes + (size_t)up.row_begin * wpr;
+      src.scales[0] = su.scales + (size_t)up.row_begin * G;  src.scales[1] = sg.scales + (size_t)up.row_begin * G;
+      src.zeros[0] = su.zeros + (size_t)up.row_begin * G;    src.zeros[1] = sg.zeros + (size_t)up.row_begin * G;
+      src.U[0] = su.U ? su.U + (size_t)up.row_begin * up.r_stored : nullptr;
+      src.U[1] = sg.U ? sg.U + (size_t)up.row_begin * up.r_stored : nullptr;
+      src.rstride = 8;
+      CUDA_TRY(hc::launch_repack_records(src, up.K, up.bits, up.r_stored, rows / 8, (uint8_t*)mu.rec->p,
+                                         (uint32_t*)mu.U->p, st));
+      CUDA_TRY(hc::launch_repack_v(su.V, up.K, up.r_stored, (uint32_t*)mu.V->p, st));
+      CUDA_TRY(hc::launch_repack_v(sg.V, gate.K, gate.r_stored, (uint32_t*)mg.V->p, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      w.members.clear();
+      w.members.push_back(mu);
+      w.members.push_back(mg);
+      w.glue = HC_GLUE_SILU_MUL;
+      w.ws_chunks = -1;
+      done[i] = done[j] = 1;
+      continue;
+    }
+
+    // ---- plain member
+    if (w.glue != HC_GLUE_NONE) { w.members.clear(); w.glue = HC_GLUE_NONE; }
     for (const Member& o : w.members)
       if (o.slot != d.slot && (o.K != d.K || o.bits != d.bits))
         return fail(HC_ERR_CONFIG, "mat %d: window members must share K and bits", i);
-    Member m;
-    m.slot = d.slot; m.N = d.N; m.K = d.K; m.bits = d.bits; m.r_stored = d.r_stored; m.r_alloc = d.r_alloc;
-    m.row_begin = d.row_begin; m.row_end = d.row_end;
-    const int rows = m.rows(), G = d.K / hc::kGroup;
-    m.rec = std::make_shared<DevBuf>();
+    Member m = make_member(d);
+    const int rows = m.rows();
     CUDA_TRY(m.rec->alloc((size_t)(rows / hc::kRows) * G * hc::rec_bytes(d.bits)));
-    m.U = std::make_shared<DevBuf>();
-    m.V = std::make_shared<DevBuf>();
     if (d.r_stored > 0) {
       CUDA_TRY(m.U->alloc((size_t)rows * d.r_stored * 2));
       CUDA_TRY(m.V->alloc((size_t)d.r_stored * d.K * 2));
     }
-    DevBuf tc, ts, tz, tu, tv;
-    cudaError_t e;
-    const uint32_t* codes = (const uint32_t*)to_device(d.codes, (size_t)d.N * d.K * d.bits / 8, tc, st, e);
-    CUDA_TRY(e);
-    const uint16_t* scales = (const uint16_t*)to_device(d.scales, (size_t)d.N * G * 2, ts, st, e);
-    CUDA_TRY(e);
-    const uint8_t* zeros = (const uint8_t*)to_device(d.zeros, (size_t)d.N * G, tz, st, e);
-    CUDA_TRY(e);
-    const uint16_t *U = nullptr, *V = nullptr;
-    if (d.r_stored > 0) {
-      U = (const uint16_t*)to_device(d.U, (size_t)d.N * d.r_stored * 2, tu, st, e);
-      CUDA_TRY(e);
-      V = (const uint16_t*)to_device(d.V, (size_t)d.r_stored * d.K * 2, tv, st, e);
-      CUDA_TRY(e);
-    }
-    CUDA_TRY(hc::launch_repack(codes, scales, zeros, U, V, d.K, d.bits, d.r_stored, d.row_begin, rows,
-                               (uint8_t*)m.rec->p, (uint32_t*)m.U->p, (uint32_t*)m.V->p, st));
-    CUDA_TRY(cudaStreamSynchronize(st));   // temporaries die at scope end
+    Staged sd;
+    hc_status s = stage(d, sd, st);
+    if (s != HC_OK) return s;
+    const int wpr = d.K * d.bits / 32;
+    hc::RepackSrc src;
+    src.codes[0] = sd.codes + (size_t)d.row_begin * wpr;  src.codes[1] = src.codes[0] + (size_t)8 * wpr;
+    src.scales[0] = sd.scales + (size_t)d.row_begin * G;  src.scales[1] = src.scales[0] + (size_t)8 * G;
+    src.zeros[0] = sd.zeros + (size_t)d.row_begin * G;    src.zeros[1] = src.zeros[0] + (size_t)8 * G;
+    src.U[0] = sd.U ? sd.U + (size_t)d.row_begin * d.r_stored : nullptr;
+    src.U[1] = sd.U ? src.U[0] + (size_t)8 * d.r_stored : nullptr;
+    src.rstride = hc::kRows;
+    CUDA_TRY(hc::launch_repack_records(src, d.K, d.bits, d.r_stored, rows / hc::kRows, (uint8_t*)m.rec->p,
+                                       (uint32_t*)m.U->p, st));
+    CUDA_TRY(hc::launch_repack_v(sd.V, d.K, d.r_stored, (uint32_t*)m.V->p, st));
+    CUDA_TRY(cudaStreamSynchronize(st));   // staged temporaries die at scope end
     auto it = std::find_if(w.members.begin(), w.members.end(), [&](const Member& o) { return o.slot == d.slot; });
     if (it != w.members.end()) *it = m; else w.members.push_back(m);
     std::sort(w.members.begin(), w.members.end(), [](const Member& a, const Member& b) { return a.slot < b.slot; });
     if ((int)w.members.size() > hc::kMaxMembers) return fail(HC_ERR_CONFIG, "window has more than %d members", hc::kMaxMembers);
     w.ws_chunks = -1;
+    done[i] = 1;
   }
   return HC_OK;
 }
@@ -194,6 +305,7 @@ extern "C" hc_status hc_set_rank(hc_ctx* ctx, int32_t layer, int32_t kind, int32
     if (m.slot == slot) {
       if (!admissible_rank(r) || r > m.cap()) return fail(HC_ERR_CONFIG, "hc_set_rank: rank %d not admissible or > cap %d", r, m.cap());
       m.r_alloc = r;
+      ctx->invalidate_graphs();
       return HC_OK;
     }
   return fail(HC_ERR_STATE, "hc_set_rank: slot %d not loaded", slot);
@@ -203,44 +315,62 @@ extern "C" int64_t hc_window_rows(hc_ctx* ctx, int32_t layer, int32_t kind, int3
   if (!ctx) return -1;
   auto it = ctx->windows.find(Key{layer, kind, expert});
   if (it == ctx->windows.end()) return -1;
-  int64_t n = 0;
-  for (const Member& m : it->second.members) n += m.rows();
-  return n;
+  return it->second.out_rows();
 }
 
 namespace hc {
 
-// Build the launch arguments of one window (also used by the stack / MoE drivers).
-hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int B, void* y, int y_bf16, const void* resid,
-                      int ld_resid, DArgs& a, int& grid) {
+// Launch arguments of one window (also used by the stack driver).
+static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int B, void* y, int y_bf16,
+                             const void* resid, int ld_resid, DArgs& a, int& grid) {
   std::memset(&a, 0, sizeof(a));
   const Member& m0 = w.members.front();
   a.K = m0.K; a.G = m0.K / kGroup; a.B = B;
-  a.x = (const uint16_t*)x; a.y = y; a.y_bf16 = y_bf16;
+  a.x = (const uint16_t*)x; a.ldx = ldx; a.y = y; a.y_bf16 = y_bf16;
   a.resid = (const uint16_t*)resid; a.ld_resid = ld_resid;
-  int rb = 0, row = 0, chunks = 0, max_chunks = 0;
+  int max_chunks = 0;
   a.n_members = (int)w.members.size();
-  for (int i = 0; i < a.n_members; ++i) {
-    const Member& m = w.members[i];
-    DMember& d = a.m[i];
-    d.rec = (const uint8_t*)m.rec->p;
-    d.U = (const uint4*)m.U->p;
-    d.V = (const uint4*)m.V->p;
-    d.n_rb = m.rows() / kRows;
-    d.rb_begin = rb;
-    d.row_off = row;
-    d.r = m.r_alloc;
-    d.r_stored = m.r_stored;
-    d.chunk_begin = chunks;
-    rb += d.n_rb;
-    row += m.rows();
-    chunks += (m.r_alloc + 15) / 16;
-    max_chunks += m.r_stored / 16;
+  if (w.glue == HC_GLUE_SILU_MUL) {
+    const Member& up = w.members[0];
+    const Member& gate = w.members[1];
+    a.glue = 1;
+    DMember& d0 = a.m[0];
+    d0.rec = (const uint8_t*)up.rec->p; d0.U = (const uint4*)up.U->p; d0.V = (const uint4*)up.V->p;
+    d0.n_rb = up.rows() / 8; d0.rb_begin = 0; d0.row_off = 0; d0.r = up.r_alloc; d0.r_stored = up.r_stored;
+    d0.chunk_begin = 0;
+    DMember& d1 = a.m[1];
+    d1.rec = nullptr; d1.U = nullptr; d1.V = (const uint4*)gate.V->p;
+    d1.n_rb = 0; d1.rb_begin = INT_MAX; d1.row_off = 0; d1.r = gate.r_alloc; d1.r_stored = gate.r_stored;
+    d1.chunk_begin = (up.r_alloc + 15) / 16;
+    a.n_rb = d0.n_rb;
+    a.ldy = up.rows();
+    a.n_chunks = d1.chunk_begin + (gate.r_alloc + 15) / 16;
+    max_chunks = (up.r_stored + gate.r_stored) / 16;
+  } else {
+    int rb = 0, row = 0, chunks = 0;
+    for (int i = 0; i < a.n_members; ++i) {
+      const Member& m = w.members[i];
+      DMember& d = a.m[i];
+      d.rec = (const uint8_t*)m.rec->p;
+      d.U = (const uint4*)m.U->p;
+      d.V = (const uint4*)m.V->p;
+      d.n_rb = m.rows() / kRows;
+      d.rb_begin = rb;
+      d.row_off = row;
+      d.r = m.r_alloc;
+      d.r_stored = m.r_stored;
+      d.chunk_begin = chunks;
+      rb += d.n_rb;
+      row += m.rows();
+      chunks += (m.r_alloc + 15) / 16;
+      max_chunks += m.r_stored / 16;
+    }
+    a.ldy = row;
+    a.n_rb = rb;
+    a.n_chunks = chunks;
   }
-  a.ldy = row;
-  a.n_rb = rb;
-  a.n_chunks = chunks;
   a.vks = std::max(1, std::min(4, a.G / 8));   // ~8 groups (32 KB of V) per rank-projection item
+  if (a.n_chunks > kMaxChunks) return fail(HC_ERR_CONFIG, "window ranks need %d chunks > %d", a.n_chunks, kMaxChunks);
   if (w.ws_chunks < max_chunks) {
     const int mc = std::max(max_chunks, 1);
     CUDA_TRY(w.vpart.alloc((size_t)mc * kMaxVks * 256 * sizeof(float)));
@@ -248,7 +378,6 @@ hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int B, void* y, int
     CUDA_TRY(cudaMemset(w.cnt.p, 0, w.cnt.bytes));
     w.ws_chunks = max_chunks;
   }
-  if (a.n_chunks > kMaxChunks) return fail(HC_ERR_CONFIG, "window ranks need %d chunks > %d", a.n_chunks, kMaxChunks);
   static const int dbg = [] { const char* e = getenv("HC_DECODE_DEBUG"); return e ? atoi(e) : 0; }();
   a.dbg = dbg;
   a.vpart = (float*)w.vpart.p;
@@ -257,11 +386,21 @@ hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int B, void* y, int
   auto it = ctx->max_ctas.find(key);
   if (it == ctx->max_ctas.end())
     it = ctx->max_ctas.emplace(key, decode_max_ctas(m0.bits, B, a.K, a.n_chunks, a.vks)).first;
+  if (it->second <= 0) return fail(HC_ERR_RUNTIME, "decode kernel cannot be resident on this device");
   const int n_items = a.n_chunks * a.vks + a.n_rb;
   static const int per_sm = [] { const char* e = getenv("HC_DECODE_CTAS_PER_SM"); return e ? atoi(e) : 0; }();
   const int cap = per_sm > 0 ? std::min(it->second, per_sm * ctx->sms) : it->second;
   grid = std::max(1, std::min(n_items, cap));
-  if (it->second <= 0) return fail(HC_ERR_RUNTIME, "decode kernel cannot be resident on this device");
+  return HC_OK;
+}
+
+static hc_status launch_window(hc_ctx* ctx, Window& w, const void* x, int ldx, int B, void* y, int y_bf16,
+                               const void* resid, int ld_resid, cudaStream_t st) {
+  DArgs a;
+  int grid = 0;
+  hc_status s = window_args(ctx, w, x, ldx, B, y, y_bf16, resid, ld_resid, a, grid);
+  if (s != HC_OK) return s;
+  CUDA_TRY(launch_decode(a, w.members.front().bits, grid, st));
   return HC_OK;
 }
 
@@ -280,7 +419,7 @@ extern "C" hc_status hc_compensated_linear(hc_ctx* ctx, int32_t layer, int32_t k
   cudaStream_t st = (cudaStream_t)stream;
   Window& w = it->second;
   const int K = w.members.front().K;
-  const int64_t rows = hc_window_rows(ctx, layer, kind, expert);
+  const int64_t rows = w.out_rows();
   const size_t xb = (size_t)B * K * 2, yb = (size_t)B * rows * (y_dtype == HC_OUT_F32 ? 4 : 2);
   const bool hx = !is_device_ptr(x), hy = !is_device_ptr(y);
   const void* dx = x;
@@ -294,14 +433,124 @@ extern "C" hc_status hc_compensated_linear(hc_ctx* ctx, int32_t layer, int32_t k
     if (ctx->stage_y.bytes < yb) CUDA_TRY(ctx->stage_y.alloc(yb));
     dy = ctx->stage_y.p;
   }
-  hc::DArgs a;
-  int grid = 0;
-  hc_status s = hc::window_args(ctx, w, dx, B, dy, y_dtype == HC_OUT_BF16, nullptr, 0, a, grid);
+  hc_status s = hc::launch_window(ctx, w, dx, K, B, dy, y_dtype == HC_OUT_BF16, nullptr, 0, st);
   if (s != HC_OK) return s;
-  CUDA_TRY(hc::launch_decode(a, w.members.front().bits, grid, st));
-  if (hy) {
-    CUDA_TRY(cudaMemcpyAsync(y, dy, yb, cudaMemcpyDeviceToHost, st));
+  if (hy) CUDA_TRY(cudaMemcpyAsync(y, dy, yb, cudaMemcpyDeviceToHost, st));
+  if (hx || hy) CUDA_TRY(cudaStreamSynchronize(st));
+  return HC_OK;
+}
+
+// ------------------------------------------------------------------ decode stack
+namespace {
+
+struct LayerPlan {
+  Window *qkv, *o, *ug, *down;
+};
+
+hc_status stack_plan(hc_ctx* ctx, std::vector<LayerPlan>& plan, int& d, int& nqkv, int& f) {
+  plan.clear();
+  for (int l = 0;; ++l) {
+    auto f0 = ctx->windows.find(Key{l, HC_WIN_QKV, -1});
+    if (f0 == ctx->windows.end()) break;
+    auto f1 = ctx->windows.find(Key{l, HC_WIN_O, -1});
+    auto f2 = ctx->windows.find(Key{l, HC_WIN_UPGATE, -1});
+    auto f3 = ctx->windows.find(Key{l, HC_WIN_DOWN, -1});
+    if (f1 == ctx->windows.end() || f2 == ctx->windows.end() || f3 == ctx->windows.end())
+      return fail(HC_ERR_STATE, "hc_stack_forward: layer %d lacks a window", l);
+    if (f2->second.glue != HC_GLUE_SILU_MUL)
+      return fail(HC_ERR_STATE, "hc_stack_forward: layer %d UPGATE window is not loaded with HC_GLUE_SILU_MUL", l);
+    plan.push_back(LayerPlan{&f0->second, &f1->second, &f2->second, &f3->second});
   }
+  if (plan.empty()) return fail(HC_ERR_STATE, "hc_stack_forward: no layer 0 QKV window loaded");
+  const LayerPlan& p0 = plan.front();
+  d = p0.qkv->members.front().K;
+  nqkv = (int)p0.qkv->out_rows();
+  f = (int)p0.ug->out_rows();
+  for (size_t l = 0; l < plan.size(); ++l) {
+    const LayerPlan& p = plan[l];
+    const int q_rows = p.qkv->members.front().rows();
+    if (p.qkv->members.front().K != d || p.qkv->out_rows() != nqkv || q_rows != d || p.o->members.front().K != d ||
+        p.o->out_rows() != d || p.ug->members.front().K != d || p.ug->out_rows() != f ||
+        p.down->members.front().K != f || p.down->out_rows() != d)
+      return fail(HC_ERR_CONFIG, "hc_stack_forward: layer %zu shapes inconsistent (need q rows = hidden = O/DOWN rows)", l);
+  }
+  return HC_OK;
+}
+
+}  // namespace
+
+extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, void* y, void* stream) {
+  if (!ctx) return fail(HC_ERR_STATE, "hc_stack_forward: null context");
+  if (B < 1 || B > 16) return fail(HC_ERR_CONFIG, "hc_stack_forward: B = %d outside [1, 16]", B);
+  if (!x || !y) return fail(HC_ERR_CONFIG, "hc_stack_forward: null x or y");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<LayerPlan> plan;
+  int d = 0, nqkv = 0, f = 0;
+  hc_status s = stack_plan(ctx, plan, d, nqkv, f);
+  if (s != HC_OK) return s;
+  const size_t hb = (size_t)B * d * 2;
+  const bool hx = !is_device_ptr(x), hy = !is_device_ptr(y);
+  const void* dx = x;
+  void* dy = y;
+  if (hx) {
+    if (ctx->stage_x.bytes < hb) CUDA_TRY(ctx->stage_x.alloc(hb));
+    CUDA_TRY(cudaMemcpyAsync(ctx->stage_x.p, x, hb, cudaMemcpyHostToDevice, st));
+    dx = ctx->stage_x.p;
+  }
+  if (hy) {
+    if (ctx->stage_y.bytes < hb) CUDA_TRY(ctx->stage_y.alloc(hb));
+    dy = ctx->stage_y.p;
+  }
+  if (ctx->s_h.bytes < (size_t)16 * d * 2) {
+    ctx->invalidate_graphs();
+    CUDA_TRY(ctx->s_h.alloc((size_t)16 * d * 2));
+    CUDA_TRY(ctx->s_h1.alloc((size_t)16 * d * 2));
+  }
+  if (ctx->s_qkv.bytes < (size_t)16 * nqkv * 2) { ctx->invalidate_graphs(); CUDA_TRY(ctx->s_qkv.alloc((size_t)16 * nqkv * 2)); }
+  if (ctx->s_m.bytes < (size_t)16 * f * 2) { ctx->invalidate_graphs(); CUDA_TRY(ctx->s_m.alloc((size_t)16 * f * 2)); }
+
+  auto key = std::make_tuple((int)B, dx, dy);
+  auto git = ctx->graphs.find(key);
+  if (git == ctx->graphs.end()) {
+    // first use: make sure every window's workspace exists (allocation is not capturable), then
+    // capture the 4·L launches into one graph
+    for (LayerPlan& p : plan)
+      for (Window* w : {p.qkv, p.o, p.ug, p.down}) {
+        hc::DArgs a;
+        int grid;
+        s = hc::window_args(ctx, *w, dx, d, B, dy, 1, nullptr, 0, a, grid);
+        if (s != HC_OK) return s;
+      }
+    cudaStream_t cs = ctx->cap_stream;
+    CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    hc_status cap = HC_OK;
+    const uint16_t* hin = (const uint16_t*)dx;
+    uint16_t* h = (uint16_t*)ctx->s_h.p;
+    uint16_t* h1 = (uint16_t*)ctx->s_h1.p;
+    uint16_t* qkv = (uint16_t*)ctx->s_qkv.p;
+    uint16_t* mm = (uint16_t*)ctx->s_m.p;
+    for (size_t l = 0; l < plan.size() && cap == HC_OK; ++l) {
+      LayerPlan& p = plan[l];
+      uint16_t* hout = (l + 1 == plan.size()) ? (uint16_t*)dy : h;
+      cap = hc::launch_window(ctx, *p.qkv, hin, d, B, qkv, 1, nullptr, 0, cs);                 // q | k | v
+      if (cap == HC_OK) cap = hc::launch_window(ctx, *p.o, qkv, nqkv, B, h1, 1, hin, d, cs);   // h1 = h + O(q)
+      if (cap == HC_OK) cap = hc::launch_window(ctx, *p.ug, h1, d, B, mm, 1, nullptr, 0, cs);  // m = silu(g)·u
+      if (cap == HC_OK) cap = hc::launch_window(ctx, *p.down, mm, f, B, hout, 1, h1, d, cs);   // h' = h1 + DOWN(m)
+      hin = hout;
+    }
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(cs, &g);
+    if (cap != HC_OK) { if (g) cudaGraphDestroy(g); return cap; }
+    CUDA_TRY(e);
+    std::unique_ptr<StackGraph> sg(new StackGraph());
+    e = cudaGraphInstantiate(&sg->exec, g, 0);
+    cudaGraphDestroy(g);
+    CUDA_TRY(e);
+    git = ctx->graphs.emplace(key, std::move(sg)).first;
+  }
+  CUDA_TRY(cudaGraphLaunch(git->second->exec, st));
+  if (hy) CUDA_TRY(cudaMemcpyAsync(y, dy, hb, cudaMemcpyDeviceToHost, st));
   if (hx || hy) CUDA_TRY(cudaStreamSynchronize(st));
   return HC_OK;
 }

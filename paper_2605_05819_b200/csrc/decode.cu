@@ -197,7 +197,7 @@ template <int NB8>
 __device__ __forceinline__ void load_x_global(const DArgs& a, int g, int lane, uint32_t (&xr)[NB8][16]) {
 #pragma unroll
   for (int nb = 0; nb < NB8; ++nb) {
-    const uint4* p = reinterpret_cast<const uint4*>(a.x + (size_t)xrow(a, (lane >> 2) + 8 * nb) * a.K +
+    const uint4* p = reinterpret_cast<const uint4*>(a.x + (size_t)xrow(a, (lane >> 2) + 8 * nb) * a.ldx +
                                                     g * kGroup + 8 * (lane & 3));
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -344,7 +344,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_
     auto prefetch_u = [&](int item, int par) {   // U fragments of a row-block item -> ubuf[par]
       if (item < nV || item >= n_items) return;
       const DMember& m = a.m[member_of_rb(a, item - nV)];
-      const int nck = min((m.r + 15) >> 4, kUPre);
+      const int r_eff = a.glue ? max(a.m[0].r, a.m[1].r) : m.r;
+      const int nck = min((r_eff + 15) >> 4, kUPre);
       if (nck == 0) return;
       if (lane == 0) {
         const uint32_t bytes = (uint32_t)nck * 512u;
@@ -359,7 +360,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_
       if (lane == 0) {
         mbar_expect_tx(xbar, (uint32_t)(a.B * a.K * 2));
         for (int b = 0; b < a.B; ++b)
-          bulk_copy(xs + (size_t)b * xs_ld, a.x + (size_t)b * a.K, (uint32_t)(a.K * 2), xbar, evict_last_policy());
+          bulk_copy(xs + (size_t)b * xs_ld, a.x + (size_t)b * a.ldx, (uint32_t)(a.K * 2), xbar, evict_last_policy());
       }
     }
     unsigned u_phase = 0;   // bit p = phase of ubar[p]
@@ -368,7 +369,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_
     int k = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++k) {
       const int par = k & 1;
-      if (!t_ready && item >= nV && a.m[member_of_rb(a, item - nV)].r > 0) {
+      if (!t_ready && item >= nV && (a.m[member_of_rb(a, item - nV)].r > 0 || (a.glue && a.m[1].r > 0))) {
         // once per CTA, while the tile warps still stream this item: acquire the rank-projection
         // partials, bring all of them into smem with one round of bulk copies, and sum them per
         // chunk in slice order (deterministic t) into t fragments
@@ -436,13 +437,18 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_
       const int rb = item - nV;
       const DMember& m = a.m[member_of_rb(a, rb)];
       const int rbl = rb - m.rb_begin;
-      float comp[NB8][4];
+      // U·t: plain windows use the member's own chunks for all 16 rows; a fused SiLU window runs
+      // the up chunks (rows 0-7 = up rows) and the gate chunks (rows 8-15 = gate rows) separately
+      float comp[2][NB8][4];
 #pragma unroll
-      for (int nb = 0; nb < NB8; ++nb)
+      for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) comp[nb][e] = 0.f;
-      if (m.r > 0) {
-        const int nck = (m.r + 15) >> 4;
+        for (int nb = 0; nb < NB8; ++nb)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) comp[h][nb][e] = 0.f;
+      const int r_eff = a.glue ? max(a.m[0].r, a.m[1].r) : m.r;
+      if (r_eff > 0) {
+        const int nck = (r_eff + 15) >> 4;
         while (!mbar_try_wait(&ubar[par], (u_phase >> par) & 1u)) {}
         u_phase ^= 1u << par;
         for (int c = 0; c < nck; ++c) {
@@ -450,38 +456,63 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_
                                       : __ldg(m.U + ((size_t)rbl * (m.r_stored >> 4) + c) * 32 + lane);
           const uint32_t af[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-          for (int nb = 0; nb < NB8; ++nb) {
-            const float4 t4 = tsm[((size_t)(m.chunk_begin + c) * NB8 + nb) * 32 + lane];
-            const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
-            uint32_t hi[2], lo[2];
+          for (int h = 0; h < 2; ++h) {
+            if (h == 1 && !a.glue) break;
+            const DMember& mt = a.glue ? a.m[h] : m;      // whose rank space / t
+            if (16 * c >= mt.r) continue;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int rank0 = 16 * c + 2 * tig + 8 * h;
-              const float ta = (rank0 < m.r) ? tv[2 * h] : 0.f;
-              const float tb = (rank0 + 1 < m.r) ? tv[2 * h + 1] : 0.f;
-              const uint32_t ha = f32_to_bf16_rn(ta), hb = f32_to_bf16_rn(tb);
-              hi[h] = ha | (hb << 16);
-              lo[h] = f32_to_bf16_rn(ta - bf16_bits_to_f32(ha)) | (f32_to_bf16_rn(tb - bf16_bits_to_f32(hb)) << 16);
+            for (int nb = 0; nb < NB8; ++nb) {
+              const float4 t4 = tsm[((size_t)(mt.chunk_begin + c) * NB8 + nb) * 32 + lane];
+              const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
+              uint32_t hi[2], lo[2];
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                const int rank0 = 16 * c + 2 * tig + 8 * hh;
+                const float ta = (rank0 < mt.r) ? tv[2 * hh] : 0.f;
+                const float tb = (rank0 + 1 < mt.r) ? tv[2 * hh + 1] : 0.f;
+                const uint32_t ha = f32_to_bf16_rn(ta), hb = f32_to_bf16_rn(tb);
+                hi[hh] = ha | (hb << 16);
+                lo[hh] = f32_to_bf16_rn(ta - bf16_bits_to_f32(ha)) | (f32_to_bf16_rn(tb - bf16_bits_to_f32(hb)) << 16);
+              }
+              mma16816(comp[h][nb], af, hi[0], hi[1]);
+              mma16816(comp[h][nb], af, lo[0], lo[1]);
             }
-            mma16816(comp[nb], af, hi[0], hi[1]);
-            mma16816(comp[nb], af, lo[0], lo[1]);
           }
         }
       }
+      if (a.glue) {
+        // m[b][8·rbl + gid] = silu(gate) · up, gate = row gid+8 (c2, c3), up = row gid (c0, c1)
 #pragma unroll
-      for (int nb = 0; nb < NB8; ++nb)
+        for (int nb = 0; nb < NB8; ++nb)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int b = 2 * tig + (e & 1) + 8 * nb;
-          if (b >= a.B) continue;
-          const int n = m.row_off + rbl * kRows + gid + 8 * (e >> 1);
-          float v = fin[nb][e] + comp[nb][e];
-          if (a.resid) v += bf16_bits_to_f32(a.resid[(size_t)b * a.ld_resid + n]);
-          if (a.y_bf16)
-            reinterpret_cast<uint16_t*>(a.y)[(size_t)b * a.ldy + n] = (uint16_t)f32_to_bf16_rn(v);
-          else
-            reinterpret_cast<float*>(a.y)[(size_t)b * a.ldy + n] = v;
-        }
+          for (int e = 0; e < 2; ++e) {
+            const int b = 2 * tig + e + 8 * nb;
+            if (b >= a.B) continue;
+            const float up = fin[nb][e] + comp[0][nb][e];
+            const float gt = fin[nb][e + 2] + comp[1][nb][e + 2];
+            const float v = up * (gt / (1.f + __expf(-gt)));
+            const int n = m.row_off + rbl * 8 + gid;
+            if (a.y_bf16)
+              reinterpret_cast<uint16_t*>(a.y)[(size_t)b * a.ldy + n] = (uint16_t)f32_to_bf16_rn(v);
+            else
+              reinterpret_cast<float*>(a.y)[(size_t)b * a.ldy + n] = v;
+          }
+      } else {
+#pragma unroll
+        for (int nb = 0; nb < NB8; ++nb)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int b = 2 * tig + (e & 1) + 8 * nb;
+            if (b >= a.B) continue;
+            const int n = m.row_off + rbl * kRows + gid + 8 * (e >> 1);
+            float v = fin[nb][e] + comp[0][nb][e];
+            if (a.resid) v += bf16_bits_to_f32(a.resid[(size_t)b * a.ld_resid + n]);
+            if (a.y_bf16)
+              reinterpret_cast<uint16_t*>(a.y)[(size_t)b * a.ldy + n] = (uint16_t)f32_to_bf16_rn(v);
+            else
+              reinterpret_cast<float*>(a.y)[(size_t)b * a.ldy + n] = v;
+          }
+      }
       ++my_rb;
     }
     // one counter update per CTA: the CTA that completes the last row block resets the counters
@@ -558,7 +589,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_
 #pragma unroll
           for (int nb = 0; nb < NB8; ++nb) {
             const uint4* p = reinterpret_cast<const uint4*>(
-                (XS ? xs_row[nb] : a.x + (size_t)xrow(a, gid + 8 * nb) * a.K + 8 * tig) +
+                (XS ? xs_row[nb] : a.x + (size_t)xrow(a, gid + 8 * nb) * a.ldx + 8 * tig) +
                 (piece >> 2) * kGroup + 32 * (piece & 3));
             xv[t][nb] = XS ? *p : __ldg(p);
           }

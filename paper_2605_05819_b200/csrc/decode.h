@@ -31,12 +31,14 @@ struct DArgs {
   DMember m[kMaxMembers];
   int n_members;
   int K, G, B;
-  const uint16_t* x;    // bf16 [B][K]
+  const uint16_t* x;    // bf16 [B][ldx]
+  int ldx;              // row stride of x in elements (multiple of 8)
   void* y;              // [B][ldy] fp32 or bf16
   int ldy, y_bf16;
   const uint16_t* resid;  // optional bf16 [B][ld_resid] added before the output rounding
   int ld_resid;
-  int glue;             // 0 none; 1 SiLU(gate)*up with interleaved up/gate rows (see api)
+  int glue;             // 0 none; 1 fused SiLU(gate)*up: m[0] = up (holds the interleaved records and U),
+                        //   m[1] = gate (V / rank only); row block = 8 up rows + 8 gate rows
   int n_rb;             // Σ members
   int n_chunks;         // Σ ceil(r_m / 16)
   int vks;              // K-slices per V chunk (<= kMaxVks)

@@ -12,9 +12,7 @@
 namespace hc {
 
 // one thread per (rb, g, lane)
-__global__ void repack_codes_kernel(const uint32_t* __restrict__ codes, const uint16_t* __restrict__ scales,
-                                    const uint8_t* __restrict__ zeros, int n_rb, int K, int bits,
-                                    int row0, uint8_t* __restrict__ out) {
+__global__ void repack_codes_kernel(RepackSrc src, int n_rb, int K, int bits, uint8_t* __restrict__ out) {
   const int G = K / kGroup;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long total = (long long)n_rb * G * 32;
@@ -23,38 +21,35 @@ __global__ void repack_codes_kernel(const uint32_t* __restrict__ codes, const ui
   const long long rg = tid >> 5;
   const int g = (int)(rg % G), rb = (int)(rg / G);
   const int wpr = K * bits / 32;
-  const uint32_t* src = codes + (size_t)row0 * wpr;    // shard rows start at row0
   uint32_t words[8];
-  pack_lane_words(src, wpr, rb, g, lane, bits, words);
+  pack_lane_words(src.codes[0], src.codes[1], src.rstride, wpr, rb, g, lane, bits, words);
   uint8_t* rec = out + (size_t)rg * rec_bytes(bits);
   for (int w = 0; w < 2 * bits; ++w) *reinterpret_cast<uint32_t*>(rec + word_offset(bits, w, lane)) = words[w];
-  const int ng = G;
   if (lane < 8) {
-    const size_t r0 = (size_t)(row0 + rb * kRows + lane), r1 = r0 + 8;
-    const uint32_t sw = (uint32_t)scales[r0 * ng + g] | ((uint32_t)scales[r1 * ng + g] << 16);
-    *reinterpret_cast<uint32_t*>(rec + scales_off(bits) + 4 * lane) = sw;
+    const uint16_t s0 = row_ptr(src.scales[0], src.scales[1], src.rstride, (size_t)G, rb, lane)[g];
+    const uint16_t s1 = row_ptr(src.scales[0], src.scales[1], src.rstride, (size_t)G, rb, lane + 8)[g];
+    *reinterpret_cast<uint32_t*>(rec + scales_off(bits) + 4 * lane) = (uint32_t)s0 | ((uint32_t)s1 << 16);
   }
   if (lane == 8) {
     uint64_t zw = 0;
     for (int r = 0; r < kRows; ++r)
-      zw |= (uint64_t)(zeros[(size_t)(row0 + rb * kRows + r) * ng + g] & 0xF) << (4 * r);
+      zw |= (uint64_t)(row_ptr(src.zeros[0], src.zeros[1], src.rstride, (size_t)G, rb, r)[g] & 0xF) << (4 * r);
     *reinterpret_cast<uint64_t*>(rec + zeros_off(bits)) = zw;
     *reinterpret_cast<uint64_t*>(rec + zeros_off(bits) + 8) = 0ull;
   }
 }
 
 // U: [rb][c][lane][4 regs]; one thread per (rb, c, lane)
-__global__ void repack_u_kernel(const uint16_t* __restrict__ U, int n_rb, int r_stored, int row0,
-                                uint32_t* __restrict__ out) {
+__global__ void repack_u_kernel(RepackSrc src, int n_rb, int r_stored, uint32_t* __restrict__ out) {
   const int nc = r_stored / 16;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= (long long)n_rb * nc * 32) return;
   const int lane = (int)(tid & 31);
   const int c = (int)((tid >> 5) % nc), rb = (int)((tid >> 5) / nc);
   for (int i = 0; i < 4; ++i) {
-    const size_t row = (size_t)(row0 + rb * kRows + frag_row(lane, i));
-    const uint32_t lo = U[row * r_stored + 16 * c + u_rank(lane, i, 0)];
-    const uint32_t hi = U[row * r_stored + 16 * c + u_rank(lane, i, 1)];
+    const uint16_t* row = row_ptr(src.U[0], src.U[1], src.rstride, (size_t)r_stored, rb, frag_row(lane, i));
+    const uint32_t lo = row[16 * c + u_rank(lane, i, 0)];
+    const uint32_t hi = row[16 * c + u_rank(lane, i, 1)];
     out[tid * 4 + i] = lo | (hi << 16);
   }
 }
@@ -76,19 +71,22 @@ __global__ void repack_v_kernel(const uint16_t* __restrict__ V, int K, int r_sto
   }
 }
 
-cudaError_t launch_repack(const uint32_t* codes, const uint16_t* scales, const uint8_t* zeros,
-                          const uint16_t* U, const uint16_t* V, int K, int bits, int r_stored,
-                          int row0, int n_rows, uint8_t* rec_out, uint32_t* u_out, uint32_t* v_out,
-                          cudaStream_t st) {
-  const int n_rb = n_rows / kRows, G = K / kGroup;
+cudaError_t launch_repack_records(const RepackSrc& src, int K, int bits, int r_stored, int n_rb, uint8_t* rec_out,
+                                  uint32_t* u_out, cudaStream_t st) {
+  const int G = K / kGroup;
   long long n = (long long)n_rb * G * 32;
-  repack_codes_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(codes, scales, zeros, n_rb, K, bits, row0, rec_out);
+  repack_codes_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, n_rb, K, bits, rec_out);
   if (r_stored > 0) {
     n = (long long)n_rb * (r_stored / 16) * 32;
-    repack_u_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(U, n_rb, r_stored, row0, u_out);
-    n = (long long)(r_stored / 16) * G * 8 * 32;
-    repack_v_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(V, K, r_stored, v_out);
+    repack_u_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, n_rb, r_stored, u_out);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_repack_v(const uint16_t* V, int K, int r_stored, uint32_t* v_out, cudaStream_t st) {
+  if (r_stored <= 0) return cudaSuccess;
+  const long long n = (long long)(r_stored / 16) * (K / kGroup) * 8 * 32;
+  repack_v_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(V, K, r_stored, v_out);
   return cudaGetLastError();
 }
 
@@ -115,7 +113,7 @@ extern "C" hc_status hc_repack_host(const uint32_t* codes, const uint16_t* scale
       std::memset(rec, 0, rec_bytes(bits));
       for (int lane = 0; lane < 32; ++lane) {
         uint32_t words[8];
-        pack_lane_words(codes, wpr, rb, g, lane, bits, words);
+        pack_lane_words(codes, codes + (size_t)8 * wpr, kRows, wpr, rb, g, lane, bits, words);
         for (int w = 0; w < 2 * bits; ++w) std::memcpy(rec + word_offset(bits, w, lane), &words[w], 4);
       }
       for (int gid = 0; gid < 8; ++gid) {

@@ -15,16 +15,23 @@ HC_HD uint32_t canon_code(const uint32_t* row, int k, int bits) {
   return v & ((1u << bits) - 1u);
 }
 
+// Row r (0..15) of row block rb comes from `lo` (r < 8) or `hi` (r >= 8), source row
+// rb*rstride + (r & 7).  Plain matrices: lo = rows, hi = rows + 8 rows, rstride = 16.
+// Fused SiLU(gate)·up windows: lo = up, hi = gate, rstride = 8 (row blocks interleave 8 + 8 rows).
+template <typename T>
+HC_HD const T* row_ptr(const T* lo, const T* hi, int rstride, size_t row_elems, int rb, int r) {
+  return (r < 8 ? lo : hi) + ((size_t)rb * rstride + (r & 7)) * row_elems;
+}
+
 // The 2*bits code words of lane `lane` for record (rb, g).
 // codes: canonical [N][K*bits/32] (row stride `wpr` words).
-HC_HD void pack_lane_words(const uint32_t* codes, int wpr, int rb, int g, int lane, int bits,
-                           uint32_t* out /* [2*bits] */) {
+HC_HD void pack_lane_words(const uint32_t* lo, const uint32_t* hi, int rstride, int wpr, int rb, int g, int lane,
+                           int bits, uint32_t* out /* [2*bits] */) {
   for (int w = 0; w < 2 * bits; ++w) out[w] = 0u;
   for (int j = 0; j < 8; ++j) {
     for (int i = 0; i < 4; ++i) {
       const Slot s = slot(bits, j, i);
-      const int row = rb * kRows + frag_row(lane, i);
-      const uint32_t* r = codes + (size_t)row * wpr;
+      const uint32_t* r = row_ptr(lo, hi, rstride, (size_t)wpr, rb, frag_row(lane, i));
       for (int h = 0; h < 2; ++h) {
         const int k = g * kGroup + frag_k(lane, j, i, h);
         const uint32_t val = canon_code(r, k, bits) << s.fp;   // field value in the 16-bit half

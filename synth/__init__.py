@@ -33,6 +33,10 @@ SHAPES = {
 }
 
 
+# decode-stack gains per slot (q, k, v, o, up, gate, down)
+STACK_GAINS = (1.0, 1.0, 1.0, 0.25, 0.25, 0.25, 0.05)
+
+
 def rng(seed: int) -> np.random.Generator:
     return np.random.Generator(np.random.PCG64(seed))
 
@@ -51,7 +55,7 @@ def bf16_bits_to_f32(b) -> np.ndarray:
 
 
 def linear_case(seed: int, N: int, K: int, bits: int = 4, group: int = 128,
-                r_stored: int = 64, B: int = 1, zeros: str = "sym") -> dict:
+                r_stored: int = 64, B: int = 1, zeros: str = "sym", unit_gain=False) -> dict:
     """One compensated linear's inputs in the C-ABI storage formats.
 
     codes  uint32 [N, K*bits/32]   (canonical little-endian bitstream per row)
@@ -66,7 +70,15 @@ def linear_case(seed: int, N: int, K: int, bits: int = 4, group: int = 128,
     words = K * bits // 32
     codes = g.integers(0, 2**32, size=(N, words), dtype=np.uint64).astype(np.uint32)
     ng = K // group
-    scales = f32_to_bf16_bits(0.002 + 0.01 * g.random((N, ng), dtype=np.float32))
+    if unit_gain:
+        # stack recipe: |W x| ~ |x| so activations stay O(1) through many layers.
+        # E[(q - z)^2] = (4^b - 1)/12 + 1/4 for uniform codes and z = 2^(b-1)
+        # unit_gain may be a float gain (True = 1.0); see STACK_GAINS
+        e2 = ((4 ** bits) - 1) / 12.0 + 0.25
+        gain = np.float32(1.0 if unit_gain is True else float(unit_gain))
+        scales = f32_to_bf16_bits(gain * (0.5 + g.random((N, ng), dtype=np.float32)) / np.float32(np.sqrt(e2 * K)))
+    else:
+        scales = f32_to_bf16_bits(0.002 + 0.01 * g.random((N, ng), dtype=np.float32))
     if zeros == "sym":
         z = np.full((N, ng), 1 << (bits - 1), dtype=np.uint8)
     elif zeros == "asym":
@@ -74,7 +86,9 @@ def linear_case(seed: int, N: int, K: int, bits: int = 4, group: int = 128,
     else:
         raise ValueError(zeros)
     U = f32_to_bf16_bits(g.standard_normal((N, r_stored), dtype=np.float32) / np.float32(np.sqrt(N)))
-    V = f32_to_bf16_bits(0.02 * g.standard_normal((r_stored, K), dtype=np.float32))
+    # compensation ~5% of |y|: unit gain -> sigma_V = 0.05 sqrt(N / (r K)); C1 recipe -> 0.02
+    sv = 0.05 * np.sqrt(N / (max(r_stored, 1) * K)) if unit_gain else 0.02
+    V = f32_to_bf16_bits(np.float32(sv) * g.standard_normal((r_stored, K), dtype=np.float32))
     x = f32_to_bf16_bits(g.standard_normal((B, K), dtype=np.float32))
     return dict(codes=codes, scales=scales, zeros=z, U=U, V=V, x=x,
                 N=N, K=K, bits=bits, group=group, r_stored=r_stored, B=B)
