@@ -181,6 +181,153 @@ def oracle_c1_sample(seconds: float = 12.0):
     return n, el
 
 
+# ------------------------------------------------------------------ workload C2 (headline)
+C2 = dict(model="llama2_7b", hidden=4096, kv=4096, ffn=11008, layers=32, bits=4, group=128, r_stored=128)
+
+
+def window_bytes_base(Ns, K, bits, g=128):
+    return sum(N * K * bits // 8 + N * (K // g) * (16 + bits) // 8 for N in Ns)
+
+
+def c2_windows(c=C2):
+    d, kv, f = c["hidden"], c["kv"], c["ffn"]
+    # (kind, member N list, K)
+    return [(0, [d, kv, kv], d), (1, [d], d), (2, [f, f], d), (3, [d], f)]
+
+
+def c2_r_std(c=C2):
+    """B200 reading of r_std (R17): the largest rank whose extra bytes stay
+    within 10% of the window's base bytes: floor(0.1·bytes_base / (2·(mean N + K)))."""
+    out = []
+    for kind, Ns, K in c2_windows(c):
+        nbar = sum(Ns) / len(Ns)
+        out.append(float(int(0.1 * window_bytes_base(Ns, K, c["bits"]) / (2 * (nbar + K)))))
+    return out
+
+
+def c2_ranks(c=C2, seed=0):
+    """Ranks from the library's allocator on synthetic sensitivity inputs (planted spectra)."""
+    import synth
+    import paper_2605_05819_b200 as hc
+    case = synth.sensitivity_case(seed, n_layers=c["layers"], members_per_window=(3, 1, 2, 1), n_sigma=256)
+    caps = []
+    for rec in case["records"]:
+        kind, Ns, K = c2_windows(c)[rec["window"]]
+        caps.append(min(c["r_stored"], Ns[rec["slot"]], K))
+    ranks, prio = hc.allocate_ranks(case["records"], case["D_layer"], (c["layers"] + 3) // 4, c2_r_std(c), caps)
+    out = {}
+    for rec, r in zip(case["records"], ranks):
+        out[(rec["layer"], rec["window"], rec["slot"])] = int(r)
+    return out
+
+
+def c2_bytes(ranks, B, c=C2):
+    """Algorithmic bytes of one decode step: every base weight byte (codes, bf16 scale, b-bit zero),
+    the allocated rank slices of U and V (bf16), and the activations in/out of each window."""
+    tot = 0
+    for l in range(c["layers"]):
+        for kind, Ns, K in c2_windows(c):
+            tot += window_bytes_base(Ns, K, c["bits"])
+            for s, N in enumerate(Ns):
+                tot += 2 * ranks[(l, kind, s)] * (N + K)
+            tot += B * 2 * K + B * 2 * (sum(Ns) if kind != 2 else Ns[0])
+    return tot
+
+
+def build_c2(ctx, ranks, rank_id, c=C2):
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(4242 + rank_id)
+    gains = (1.0, 1.0, 1.0, 0.25, 0.25, 0.25, 0.05)   # synth.STACK_GAINS (finite over 32 layers)
+    b = c["bits"]
+    e2 = ((4 ** b) - 1) / 12.0 + 0.25
+    slot_gain = {(0, 0): 0, (0, 1): 1, (0, 2): 2, (1, 0): 3, (2, 0): 4, (2, 1): 5, (3, 0): 6}
+    for l in range(c["layers"]):
+        mats = []
+        for kind, Ns, K in c2_windows(c):
+            G = K // c["group"]
+            for s, N in enumerate(Ns):
+                gain = gains[slot_gain[(kind, s)]]
+                rs = c["r_stored"]
+                mats.append(dict(
+                    layer=l, window=kind, slot=s, N=N, K=K, bits=b,
+                    codes=torch.randint(-2**31, 2**31, (N, K * b // 32), generator=g, device="cuda", dtype=torch.int32),
+                    scales=(gain * (0.5 + torch.rand((N, G), generator=g, device="cuda")) / (e2 * K) ** 0.5).to(torch.bfloat16),
+                    zeros=torch.randint(0, 1 << b, (N, G), generator=g, device="cuda", dtype=torch.uint8),
+                    U=(torch.randn((N, rs), generator=g, device="cuda") / N ** 0.5).to(torch.bfloat16),
+                    V=(0.05 * (N / (rs * K)) ** 0.5 * torch.randn((rs, K), generator=g, device="cuda")).to(torch.bfloat16),
+                    r_stored=rs, r_alloc=ranks[(l, kind, s)], glue=1 if kind == 2 else 0))
+        ctx.load_layer(mats)
+        del mats
+    torch.cuda.synchronize()
+
+
+def run_c2_ours(args, rank, world, device, B):
+    import torch
+    import paper_2605_05819_b200 as hc
+    c = C2
+    ranks = c2_ranks(c)
+    ctx = hc.Context(device)
+    build_c2(ctx, ranks, rank, c)
+    x = torch.randn((B, c["hidden"]), device="cuda").to(torch.bfloat16)
+    y = torch.empty((B, c["hidden"]), dtype=torch.bfloat16, device="cuda")
+    st = torch.cuda.Stream()
+    for _ in range(max(args.warmup, 3)):
+        ctx.stack_forward(x, y, stream=st)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(device) as clk:
+        e0.record(st)
+        for _ in range(args.steps):
+            ctx.stack_forward(x, y, stream=st)
+        e1.record(st)
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ms = e0.elapsed_time(e1)
+    finite = bool(torch.isfinite(y.float()).all().item())
+    # end to end through the public API with pinned HOST buffers (H2D of x, D2H of y every step)
+    xh = x.cpu().pin_memory()
+    yh = torch.empty((B, c["hidden"]), dtype=torch.bfloat16).pin_memory()
+    ctx.stack_forward(xh, yh, stream=st)
+    n_e2e = max(3, min(args.steps, 50))
+    t0 = time.perf_counter()
+    for _ in range(n_e2e):
+        ctx.stack_forward(xh, yh, stream=st)      # synchronises (host result)
+    e2e_s = time.perf_counter() - t0
+    ctx.close()
+    mean_rank = sum(ranks.values()) / len(ranks)
+    return dict(ms=ms, steps=args.steps, clocks=clk.summary, e2e_s=e2e_s, n_e2e=n_e2e, finite=finite,
+                launches=args.steps * 4 * c["layers"], h2d=B * c["hidden"] * 2, d2h=B * c["hidden"] * 2,
+                bytes=c2_bytes(ranks, B, c), mean_rank=mean_rank, ranks=ranks)
+
+
+def oracle_c2_sample(seconds: float = 15.0, c=C2):
+    """The float64 oracle on a bounded sample of the C2 workload: whole layers (all 4 windows,
+    glue included) of the Llama-2-7B-shaped stack at B = 1; tokens/s extrapolated x32 layers."""
+    import synth
+    from oracle import linear
+    d, kv, f = c["hidden"], c["kv"], c["ffn"]
+    mk = lambda N, K, s: synth.linear_case(100 + s, N=N, K=K, bits=c["bits"], r_stored=16, zeros="asym",
+                                           unit_gain=synth.STACK_GAINS[s])
+    L = dict(qkv=[mk(d, d, 0), mk(kv, d, 1), mk(kv, d, 2)], o=[mk(d, d, 3)], upgate=[mk(f, d, 4), mk(f, d, 5)],
+             down=[mk(d, f, 6)])
+    R = dict(qkv=[16, 16, 16], o=[16], upgate=[16, 16], down=[16])
+    h = synth.activations(1, 1, d)
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        linear.stack_forward([L], [R], h)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or n >= 8:
+            break
+    per_layer = el / n
+    return 1.0 / (per_layer * c["layers"]), n, el
+
+
 def cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -191,10 +338,12 @@ def cores():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1024)
-    ap.add_argument("--warmup", type=int, default=256)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c1", choices=["c1"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2"])
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--sweep", action="store_true", help="c2: also time B = 2, 4, 8, 16")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -203,21 +352,37 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
     hbm, tflops, peak_src = peaks()
-    config = {"workload": "c1: single 4096x4096 linear, 4-bit g128, rank-64 compensation, batch-1 decode",
-              "N": 4096, "K": 4096, "bits": 4, "group": 128, "rank": 64, "batch": 1,
-              "l2": "defeated: 128 distinct weight copies (1.25 GB) rotated per step"}
+    if args.workload == "c1":
+        config = {"workload": "c1: single 4096x4096 linear, 4-bit g128, rank-64 compensation, batch-1 decode",
+                  "N": 4096, "K": 4096, "bits": 4, "group": 128, "rank": 64, "batch": 1,
+                  "l2": "defeated: 128 distinct weight copies (1.25 GB) rotated per step"}
+    else:
+        config = {"workload": "c2: Llama-2-7B-shaped 32-layer decode stack, 4-bit g128 + dynamic ranks "
+                              "(hc_allocate_ranks, r_std = 10%-bytes rule), 1 GPU",
+                  "layers": 32, "hidden": 4096, "kv": 4096, "ffn": 11008, "bits": 4, "group": 128,
+                  "r_stored": C2["r_stored"], "batch": args.batch,
+                  "l2": "inputs larger than L2 (3.5 GB of weights streamed per step)",
+                  "attention": "identity stand-in on the q-part (out of scope, DESIGN.md R9)"}
 
     if args.impl == "reference":
         if rank != 0:
             return
-        n, el = oracle_c1_sample(seconds=max(5.0, min(60.0, 0.05 * (args.steps + args.warmup))))
-        gbs = c1_bytes() * n / el / 1e9
-        line = {"impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": args.gpus,
-                "steps": n, "warmup": 0, "ms_per_step": round(1e3 * el / n, 3), "higher_is_better": True,
+        if args.workload == "c1":
+            n, el = oracle_c1_sample(seconds=max(5.0, min(60.0, 0.05 * (args.steps + args.warmup))))
+            val, unit = c1_bytes() * n / el / 1e9, "GB/s"
+            sample = f"{n} whole C1 calls (numpy float64, unpack+dequant+matvec)"
+            ms = 1e3 * el / n
+        else:
+            val, n, el = oracle_c2_sample(seconds=20.0)
+            unit = "tokens/s"
+            sample = f"{n} whole Llama-2-7B layers at B=1 (float64, all 4 windows + glue), extrapolated x32 layers"
+            ms = 1e3 / val
+        line = {"impl": "reference", "metric": METRIC, "value": round(val, 6), "unit": unit, "n_gpus": args.gpus,
+                "steps": n, "warmup": 0, "ms_per_step": round(ms, 3), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
-                "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": cores(), "kind": "oracle",
-                                 "sample": f"{n} whole C1 calls (numpy float64, unpack+dequant+matvec)"},
-                "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                "cpu_baseline": {"value": round(val, 6), "unit": unit, "cores": cores(), "kind": "oracle",
+                                 "sample": sample},
+                "e2e": {"value": round(val, 6), "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
 
@@ -225,30 +390,56 @@ def main():
     if world > 1:
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
-    r = run_c1_ours(args, rank, world, local)
-    ms_step = r["ms"] / r["steps"]
-    nbytes = c1_bytes()
+    if args.workload == "c1":
+        r = run_c1_ours(args, rank, world, local)
+        nbytes = c1_bytes()
+        unit, kernel = "GB/s", "hc::decode_kernel<4,1,true>"
+    else:
+        r = run_c2_ours(args, rank, world, local, args.batch)
+        nbytes = r["bytes"]
+        unit, kernel = "tokens/s", "hc::decode_kernel (4 fused windows per layer)"
     per_rank = torch.tensor([r["ms"]], dtype=torch.float64, device="cuda")
     if world > 1:
         torch.distributed.all_reduce(per_rank, op=torch.distributed.ReduceOp.MAX)
     ms_max = float(per_rank.item())
-    value = world * nbytes * r["steps"] / (ms_max * 1e-3) / 1e9
     achieved = nbytes / (r["ms"] / r["steps"] * 1e-3) / 1e9
+    if args.workload == "c1":
+        value = world * nbytes * r["steps"] / (ms_max * 1e-3) / 1e9
+        e2e = {"value": round(nbytes * r["n_e2e"] / r["e2e_s"] / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]}
+    else:
+        value = world * args.batch * r["steps"] / (ms_max * 1e-3)
+        e2e = {"value": round(args.batch * r["n_e2e"] / r["e2e_s"], 2), "unit": "tokens/s",
+               "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]}
+        config["mean_rank"] = round(r["mean_rank"], 2)
+        config["bytes_per_step"] = nbytes
+        config["output_finite"] = r["finite"]
     if rank == 0:
-        line = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": r["steps"],
+        line = {"metric": METRIC, "value": round(value, 2), "unit": unit, "n_gpus": world, "steps": r["steps"],
                 "warmup": args.warmup, "ms_per_step": round(ms_max / r["steps"], 6), "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "bf16x int4 (fp32 accumulate)",
-                "data": "synthetic (seeded on device)", "config": config,
+                "scaling": "weak", "vs_baseline": None, "dtype": "bf16 x int4 (exact int dequant, fp32 accumulate)",
+                "data": "synthetic (seeded on device, random weights of the named shapes)", "config": config,
                 "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
                              "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": peak_src,
-                             "kernel": "hc::decode_kernel<4,1>", "bytes_per_launch": nbytes},
-                "clocks": r["clocks"], "gpu_launches": r["launches"],
-                "e2e": {"value": round(nbytes * r["n_e2e"] / r["e2e_s"] / 1e9, 3), "unit": "GB/s",
-                        "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]}}
+                             "kernel": kernel, "bytes_per_step": nbytes},
+                "clocks": r["clocks"], "gpu_launches": r["launches"], "e2e": e2e}
+        if args.workload == "c2" and args.sweep:
+            sweep = {}
+            for Bs in (2, 4, 8, 16):
+                rs = run_c2_ours(args, rank, world, local, Bs)
+                sweep[str(Bs)] = {"tokens_per_s": round(Bs * rs["steps"] / (rs["ms"] * 1e-3), 1),
+                                  "ms_per_step": round(rs["ms"] / rs["steps"], 4),
+                                  "GBps": round(rs["bytes"] / (rs["ms"] / rs["steps"] * 1e-3) / 1e9, 1)}
+            line["batch_sweep"] = sweep
         if not args.no_cpu_baseline:
-            n, el = oracle_c1_sample(12.0)
-            line["cpu_baseline"] = {"value": round(nbytes * n / el / 1e9, 4), "unit": "GB/s", "cores": cores(),
-                                    "kind": "oracle", "sample": f"{n} whole C1 calls, numpy float64"}
+            if args.workload == "c1":
+                n, el = oracle_c1_sample(12.0)
+                line["cpu_baseline"] = {"value": round(nbytes * n / el / 1e9, 4), "unit": "GB/s", "cores": cores(),
+                                        "kind": "oracle", "sample": f"{n} whole C1 calls, numpy float64"}
+            else:
+                tps, n, el = oracle_c2_sample(15.0)
+                line["cpu_baseline"] = {"value": round(tps, 6), "unit": "tokens/s", "cores": cores(), "kind": "oracle",
+                                        "sample": f"{n} whole Llama-2-7B layers at B=1 (float64), extrapolated x32"}
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
