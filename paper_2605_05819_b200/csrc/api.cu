@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "decode.h"
+#include "prefill.h"
 #include "hcinfer.h"
 #include "layout.h"
 #include "repack_kernels.h"
@@ -37,6 +38,9 @@ struct DevBuf {
 struct Member {
   int slot = 0, N = 0, K = 0, bits = 0, r_stored = 0, r_alloc = 0, row_begin = 0, row_end = 0;
   std::shared_ptr<DevBuf> rec, U, V;   // rec/U empty for the gate member of a fused SiLU window
+  // prefill (tcgen05) copies, 4-bit plain members only: nibble-paired codes, canonical scales /
+  // zeros of the shard rows, fp16 U [rows][r_stored] and V [r_stored][K]
+  std::shared_ptr<DevBuf> pcodes, pscales, pzeros, U16, V16;
   int rows() const { return row_end - row_begin; }
   int cap() const { return std::min(std::min(r_stored, N), K); }
 };
@@ -79,6 +83,7 @@ struct hc_ctx {
   std::map<Key, Window> windows;
   std::map<std::tuple<int, int, int, int, int>, int> max_ctas;   // (bits, B, K, chunks, vks) -> co-resident CTAs
   DevBuf stage_x, stage_y;
+  DevBuf p_x16, p_t16;                 // prefill scratch: fp16 activations, fp16 T = X·Vᵀ
   // decode stack (hc_stack_forward)
   DevBuf s_h, s_h1, s_qkv, s_m;
   std::map<std::tuple<int, const void*, void*>, std::unique_ptr<StackGraph>> graphs;
@@ -190,7 +195,31 @@ static Member make_member(const hc_matrix_desc& d) {
   m.rec = std::make_shared<DevBuf>();
   m.U = std::make_shared<DevBuf>();
   m.V = std::make_shared<DevBuf>();
+  m.pcodes = std::make_shared<DevBuf>();
+  m.pscales = std::make_shared<DevBuf>();
+  m.pzeros = std::make_shared<DevBuf>();
+  m.U16 = std::make_shared<DevBuf>();
+  m.V16 = std::make_shared<DevBuf>();
   return m;
+}
+
+// Prefill copies of a plain 4-bit member (rows [row_begin, row_end) of the staged canonical inputs).
+static hc_status build_prefill(Member& m, const Staged& sd, cudaStream_t st) {
+  if (m.bits != 4) return HC_OK;
+  const int rows = m.rows(), G = m.K / hc::kGroup, wpr = m.K / 8;
+  CUDA_TRY(m.pcodes->alloc((size_t)rows * wpr * 4));
+  CUDA_TRY(hc::launch_prefill_codes(sd.codes + (size_t)m.row_begin * wpr, (uint32_t*)m.pcodes->p, (size_t)rows * wpr, st));
+  CUDA_TRY(m.pscales->alloc((size_t)rows * G * 2));
+  CUDA_TRY(cudaMemcpyAsync(m.pscales->p, sd.scales + (size_t)m.row_begin * G, (size_t)rows * G * 2, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(m.pzeros->alloc((size_t)rows * G));
+  CUDA_TRY(cudaMemcpyAsync(m.pzeros->p, sd.zeros + (size_t)m.row_begin * G, (size_t)rows * G, cudaMemcpyDeviceToDevice, st));
+  if (m.r_stored > 0) {
+    CUDA_TRY(m.U16->alloc((size_t)rows * m.r_stored * 2));
+    CUDA_TRY(hc::launch_bf16_to_f16(sd.U + (size_t)m.row_begin * m.r_stored, (uint16_t*)m.U16->p, (size_t)rows * m.r_stored, st));
+    CUDA_TRY(m.V16->alloc((size_t)m.r_stored * m.K * 2));
+    CUDA_TRY(hc::launch_bf16_to_f16(sd.V, (uint16_t*)m.V16->p, (size_t)m.r_stored * m.K, st));
+  }
+  return HC_OK;
 }
 
 extern "C" hc_status hc_load_layer(hc_ctx* ctx, const hc_matrix_desc* mats, int32_t n_mats, void* stream) {
@@ -286,6 +315,8 @@ extern "C" hc_status hc_load_layer(hc_ctx* ctx, const hc_matrix_desc* mats, int3
     CUDA_TRY(hc::launch_repack_records(src, d.K, d.bits, d.r_stored, rows / hc::kRows, (uint8_t*)m.rec->p,
                                        (uint32_t*)m.U->p, st));
     CUDA_TRY(hc::launch_repack_v(sd.V, d.K, d.r_stored, (uint32_t*)m.V->p, st));
+    s = build_prefill(m, sd, st);
+    if (s != HC_OK) return s;
     CUDA_TRY(cudaStreamSynchronize(st));   // staged temporaries die at scope end
     auto it = std::find_if(w.members.begin(), w.members.end(), [&](const Member& o) { return o.slot == d.slot; });
     if (it != w.members.end()) *it = m; else w.members.push_back(m);
@@ -404,12 +435,54 @@ static hc_status launch_window(hc_ctx* ctx, Window& w, const void* x, int ldx, i
   return HC_OK;
 }
 
+// Prefill / batched (B > 16) window: per member, T = X·V[:r]ᵀ (tcgen05, fp16 out) then
+// Y = X·deq(W)ᵀ + T·U[:, :r]ᵀ (tcgen05, dequant producers + rank slice in the same accumulator).
+static hc_status launch_prefill_window(hc_ctx* ctx, Window& w, const void* x, int M, void* y, int y_dtype,
+                                       cudaStream_t st) {
+  if (w.glue != HC_GLUE_NONE) return fail(HC_ERR_CONFIG, "prefill of a fused SiLU window is not supported");
+  const int K = w.members.front().K;
+  for (const Member& m : w.members) {
+    if (m.bits != 4) return fail(HC_ERR_CONFIG, "prefill (B > 16) supports 4-bit windows only (got %d-bit)", m.bits);
+    if (m.rows() % kPBN) return fail(HC_ERR_CONFIG, "prefill needs member rows %% 256 == 0 (got %d)", m.rows());
+  }
+  const size_t xel = (size_t)M * K;
+  if (ctx->p_x16.bytes < xel * 2) CUDA_TRY(ctx->p_x16.alloc(xel * 2));
+  CUDA_TRY(launch_bf16_to_f16((const uint16_t*)x, (uint16_t*)ctx->p_x16.p, xel, st));
+  const int64_t ldy = w.out_rows();
+  CUtensorMap tmX, tmV, tmT, tmU;
+  if (!encode_tmap_f16(&tmX, ctx->p_x16.p, K, M, K, kPBM)) return fail(HC_ERR_RUNTIME, "tensor map (X) encoding failed");
+  int row_off = 0;
+  for (const Member& m : w.members) {
+    const int r = m.r_alloc, rpad = (r + 15) / 16 * 16, tw = (rpad + 63) / 64 * 64;
+    if (r > 0) {
+      if (ctx->p_t16.bytes < (size_t)M * tw * 2) CUDA_TRY(ctx->p_t16.alloc((size_t)M * tw * 2));
+      if (!encode_tmap_f16(&tmV, m.V16->p, K, r, K, kPBN)) return fail(HC_ERR_RUNTIME, "tensor map (V) encoding failed");
+      PArgs pt{};
+      pt.M = M; pt.N = tw; pt.K = K; pt.K2 = 0; pt.n_dim = rpad; pt.b_mode = 1;
+      pt.out = ctx->p_t16.p; pt.ldo = tw; pt.out_type = 2;
+      pt.tiles_m = (M + kPBM - 1) / kPBM; pt.tiles_n = 1;
+      CUDA_TRY(launch_prefill(tmX, tmV, tmX, tmX, pt, st));
+      if (!encode_tmap_f16(&tmT, ctx->p_t16.p, tw, M, tw, kPBM)) return fail(HC_ERR_RUNTIME, "tensor map (T) encoding failed");
+      if (!encode_tmap_f16(&tmU, m.U16->p, r, m.rows(), m.r_stored, kPBN)) return fail(HC_ERR_RUNTIME, "tensor map (U) encoding failed");
+    }
+    PArgs pm{};
+    pm.M = M; pm.N = m.rows(); pm.K = K; pm.K2 = r > 0 ? rpad : 0; pm.n_dim = kPBN; pm.b_mode = 0;
+    pm.codes = (const uint32_t*)m.pcodes->p; pm.scales = (const uint16_t*)m.pscales->p; pm.zeros = (const uint8_t*)m.pzeros->p;
+    pm.out = y_dtype == HC_OUT_F32 ? (void*)((float*)y + row_off) : (void*)((uint16_t*)y + row_off);
+    pm.ldo = (int)ldy; pm.out_type = y_dtype == HC_OUT_F32 ? 0 : 1;
+    pm.tiles_m = (M + kPBM - 1) / kPBM; pm.tiles_n = m.rows() / kPBN;
+    CUDA_TRY(launch_prefill(tmX, tmX, r > 0 ? tmT : tmX, r > 0 ? tmU : tmX, pm, st));
+    row_off += m.rows();
+  }
+  return HC_OK;
+}
+
 }  // namespace hc
 
 extern "C" hc_status hc_compensated_linear(hc_ctx* ctx, int32_t layer, int32_t kind, int32_t expert,
                                            const void* x, int32_t B, void* y, int32_t y_dtype, void* stream) {
   if (!ctx) return fail(HC_ERR_STATE, "hc_compensated_linear: null context");
-  if (B < 1 || B > 16) return fail(HC_ERR_CONFIG, "hc_compensated_linear: B = %d outside [1, 16]", B);
+  if (B < 1) return fail(HC_ERR_CONFIG, "hc_compensated_linear: B = %d < 1", B);
   if (y_dtype != HC_OUT_F32 && y_dtype != HC_OUT_BF16) return fail(HC_ERR_CONFIG, "bad y_dtype %d", y_dtype);
   if (!x || !y) return fail(HC_ERR_CONFIG, "hc_compensated_linear: null x or y");
   auto it = ctx->windows.find(Key{layer, kind, expert});
@@ -433,7 +506,8 @@ extern "C" hc_status hc_compensated_linear(hc_ctx* ctx, int32_t layer, int32_t k
     if (ctx->stage_y.bytes < yb) CUDA_TRY(ctx->stage_y.alloc(yb));
     dy = ctx->stage_y.p;
   }
-  hc_status s = hc::launch_window(ctx, w, dx, K, B, dy, y_dtype == HC_OUT_BF16, nullptr, 0, st);
+  hc_status s = B <= 16 ? hc::launch_window(ctx, w, dx, K, B, dy, y_dtype == HC_OUT_BF16, nullptr, 0, st)
+                        : hc::launch_prefill_window(ctx, w, dx, B, dy, y_dtype, st);
   if (s != HC_OK) return s;
   if (hy) CUDA_TRY(cudaMemcpyAsync(y, dy, yb, cudaMemcpyDeviceToHost, st));
   if (hx || hy) CUDA_TRY(cudaStreamSynchronize(st));

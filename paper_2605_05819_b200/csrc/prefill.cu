@@ -1,0 +1,374 @@
+// Prefill compensated GEMM on 5th-generation tensor cores (tcgen05 + TMEM + TMA + mbarriers).
+//
+//     Y[m][n] = Σ_k X[m][k] · s[n][k/128]·(q[n][k] − z[n][k/128])  +  Σ_j T[m][j] · U[n][j],
+//     T = X · V[:r]ᵀ
+//
+// i.e. Y = [X | T] · [deq(W) | U]ᵀ: the rank-r update is appended to the K loop and lands in the
+// same TMEM accumulator.  One CTA computes a 128 (tokens) x 256 (weight rows) tile:
+//   warp 0      TMA producer: X tiles (and T / U tiles for the rank slice, V tiles for T = X·Vᵀ)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (kind::f16, M=128, N<=256, K=16)
+//   warps 2-5   dequant producers: 4-bit codes -> fp16 s·(q−z) written straight into the UMMA
+//               K-major 128-byte-swizzled smem layout (exact (q−z), one fp16 rounding of s·(q−z))
+//   warps 6-9   epilogue: tcgen05.ld TMEM -> registers -> fp32 / bf16 / fp16 global stores
+// 4-stage smem ring (48 KB per stage) with full/empty mbarriers; tcgen05.commit releases stages.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include "layout.h"
+#include "prefill.h"
+
+namespace hc {
+
+namespace {
+
+constexpr int kABytes = kPBM * kPBK * 2;   // 16 KB
+constexpr int kBBytes = kPBN * kPBK * 2;   // 32 KB
+constexpr int kThreads = 320;
+
+__device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(s_u32(b)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(b)) : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
+          "r"(s_u32(dst)),
+      "l"(map), "r"(s_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row atoms 1024 B apart (SBO),
+// sm100 descriptor version 1.
+__device__ __forceinline__ uint64_t umma_desc(const void* smem) {
+  const uint64_t addr = s_u32(smem);
+  uint64_t d = 0;
+  d |= (addr >> 4) & 0x3FFFull;                 // start address
+  d |= (uint64_t)(16 >> 4) << 16;               // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;             // SBO
+  d |= (uint64_t)1 << 46;                       // version (sm100)
+  d |= (uint64_t)2 << 61;                       // SWIZZLE_128B
+  return d;
+}
+
+// kind::f16 instruction descriptor: A = B = F16 (K-major), D = F32, M = 128, N = n.
+__device__ __forceinline__ uint32_t umma_idesc(int n) {
+  uint32_t d = 0;
+  d |= 1u << 4;                                 // D format F32
+  d |= 0u << 7;                                 // A F16
+  d |= 0u << 10;                                // B F16
+  d |= (uint32_t)(n >> 3) << 17;                // N >> 3
+  d |= (uint32_t)(kPBM >> 4) << 24;             // M >> 4
+  return d;
+}
+
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s_u32(bar))
+               : "memory");
+}
+
+// byte offset of (row, 16-byte chunk) inside a K-major SW128 tile (rows of 128 B, 8-row atoms)
+__device__ __forceinline__ uint32_t sw128(int row, int chunk) {
+  return ((row >> 3) << 10) + ((row & 7) << 7) + (((chunk ^ row) & 7) << 4);
+}
+
+__device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kThreads, 1)
+    prefill_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
+                   const __grid_constant__ PArgs p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = base;
+  uint8_t* sB = base + kPStages * kABytes;
+  uint64_t* full_a = reinterpret_cast<uint64_t*>(sB + kPStages * kBBytes);
+  uint64_t* full_b = full_a + kPStages;
+  uint64_t* empty = full_b + kPStages;
+  uint64_t* tmem_full = empty + kPStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tm = blockIdx.x % p.tiles_m, tn = blockIdx.x / p.tiles_m;
+  const int m0 = tm * kPBM, n0 = tn * kPBN;
+  const int nkb1 = p.K / kPBK;
+  const int nkb2 = (p.K2 + kPBK - 1) / kPBK;
+  const int nkb = nkb1 + nkb2;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kPStages; ++s) {
+      bar_init(&full_a[s], 1);
+      bar_init(&full_b[s], 128);
+      bar_init(&empty[s], 1);
+    }
+    bar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_u32(tmem_slot)),
+                 "r"(256)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ======================= TMA producer =======================
+    if (lane == 0) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % kPStages;
+        if (kb >= kPStages) bar_wait(&empty[s], ((kb / kPStages) + 1) & 1);
+        const bool main = kb < nkb1;
+        const bool b_tma = !main || p.b_mode == 1;
+        bar_expect_tx(&full_a[s], (uint32_t)(kABytes + (b_tma ? kBBytes : 0)));
+        if (main) {
+          tma_2d(sA + s * kABytes, &tmA, kb * kPBK, m0, &full_a[s]);
+          if (b_tma) tma_2d(sB + s * kBBytes, &tmB, kb * kPBK, n0, &full_a[s]);
+        } else {
+          tma_2d(sA + s * kABytes, &tmA2, (kb - nkb1) * kPBK, m0, &full_a[s]);
+          tma_2d(sB + s * kBBytes, &tmB2, (kb - nkb1) * kPBK, n0, &full_a[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer (one thread) =======================
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc(p.n_dim);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % kPStages;
+        const uint32_t ph = (kb / kPStages) & 1;
+        bar_wait(&full_a[s], ph);
+        bar_wait(&full_b[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int nk = kb < nkb1 ? kPBK / 16 : min(kPBK, p.K2 - (kb - nkb1) * kPBK) / 16;
+        const uint64_t ad = umma_desc(sA + s * kABytes), bd = umma_desc(sB + s * kBBytes);
+        for (int k = 0; k < nk; ++k)   // advance 16 fp16 = 32 bytes along K inside the swizzled rows
+          umma_f16(tmem_base, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc, (kb | k) != 0);
+        umma_commit(&empty[s]);
+      }
+      umma_commit(tmem_full);
+    }
+  } else if (warp < 6) {
+    // ======================= dequant producers =======================
+    const int t = threadIdx.x - 64;            // 0..127: rows t and t + 128 of the B tile
+    const int G = p.K / kGroup;
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % kPStages;
+      const bool dq = kb < nkb1 && p.b_mode == 0;
+      uint4 cw[2][2];
+      uint32_t sc[2], zz[2];
+      if (dq) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int n = min(n0 + t + 128 * h, p.N - 1);
+          const uint4* src = reinterpret_cast<const uint4*>(p.codes + (size_t)n * (p.K / 8) + 8 * kb);
+          cw[h][0] = __ldg(src);
+          cw[h][1] = __ldg(src + 1);
+          const int g = kb >> 1;
+          const float sf = __uint_as_float((uint32_t)p.scales[(size_t)n * G + g] << 16);
+          const __half s16 = __float2half_rn(sf);
+          sc[h] = (uint32_t)__half_as_ushort(s16) * 0x00010001u;                  // half2(s, s)
+          zz[h] = (0x6400u + (uint32_t)p.zeros[(size_t)n * G + g]) * 0x00010001u;  // half2(1024+z)
+        }
+      }
+      if (kb >= kPStages) bar_wait(&empty[s], ((kb / kPStages) + 1) & 1);
+      if (dq) {
+        uint8_t* tile = sB + s * kBBytes;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int row = t + 128 * h;
+          const uint32_t words[8] = {cw[h][0].x, cw[h][0].y, cw[h][0].z, cw[h][0].w,
+                                     cw[h][1].x, cw[h][1].y, cw[h][1].z, cw[h][1].w};
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {        // word c = k 8c..8c+7 = 16-byte chunk c of the row
+            uint32_t v[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              uint32_t hv = lop3_and_or(words[c] >> (4 * i), 0x000F000Fu, 0x64006400u);   // half2(1024 + q)
+              __half2 d = __hsub2(*reinterpret_cast<__half2*>(&hv), *reinterpret_cast<const __half2*>(&zz[h]));
+              d = __hmul2(d, *reinterpret_cast<const __half2*>(&sc[h]));                 // fp16(s·(q − z))
+              v[i] = *reinterpret_cast<uint32_t*>(&d);
+            }
+            *reinterpret_cast<uint4*>(tile + sw128(row, c)) = make_uint4(v[0], v[1], v[2], v[3]);
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
+      }
+      bar_arrive(&full_b[s]);
+    }
+  } else {
+    // ======================= epilogue =======================
+    const int q = warp & 3;                    // TMEM lane quadrant this warp may access
+    const int m = m0 + 32 * q + lane;
+    bar_wait(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    for (int c0 = 0; c0 < p.n_dim; c0 += 32) {
+      uint32_t v[32];
+      const uint32_t addr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+            "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+            "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+          : "r"(addr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      const int n = n0 + c0;
+      if (m < p.M && n < p.N) {
+        if (p.out_type == 0) {
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + (size_t)m * p.ldo + n);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                 __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+        } else {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float a = __uint_as_float(v[2 * i]), b = __uint_as_float(v[2 * i + 1]);
+            if (p.out_type == 1) {
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+              pk[i] = *reinterpret_cast<uint32_t*>(&h2);
+            } else {
+              __half2 h2 = __floats2half2_rn(a, b);
+              pk[i] = *reinterpret_cast<uint32_t*>(&h2);
+            }
+          }
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) + (size_t)m * p.ldo + n);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256) : "memory");
+  }
+}
+
+static size_t prefill_smem() {
+  return (size_t)kPStages * (kABytes + kBBytes) + (3 * kPStages + 2) * 8 + 1024;
+}
+
+cudaError_t launch_prefill(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmA2,
+                           const CUtensorMap& tmB2, const PArgs& p, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prefill_smem());
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  prefill_kernel<<<p.tiles_m * p.tiles_n, kThreads, prefill_smem(), st>>>(tmA, tmB, tmA2, tmB2, p);
+  return cudaGetLastError();
+}
+
+__global__ void bf16_to_f16_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out, size_t n) {
+  const size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (i + 8 <= n) {
+    const uint4 v = *reinterpret_cast<const uint4*>(in + i);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float a = __uint_as_float(w[j] << 16), b = __uint_as_float(w[j] & 0xFFFF0000u);
+      __half2 h = __floats2half2_rn(a, b);
+      o[j] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    *reinterpret_cast<uint4*>(out + i) = make_uint4(o[0], o[1], o[2], o[3]);
+  } else {
+    for (size_t j = i; j < n; ++j) out[j] = __half_as_ushort(__float2half_rn(__uint_as_float((uint32_t)in[j] << 16)));
+  }
+}
+
+cudaError_t launch_bf16_to_f16(const uint16_t* in, uint16_t* out, size_t n, cudaStream_t st) {
+  const size_t threads = (n + 7) / 8;
+  bf16_to_f16_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(in, out, n);
+  return cudaGetLastError();
+}
+
+// word w of a row (elements 8w..8w+7, canonical nibble j = element 8w+j) -> prefill order:
+// nibble 0 = k0, 4 = k1, 1 = k2, 5 = k3, 2 = k4, 6 = k5, 3 = k6, 7 = k7 (so that (w >> 4i) & 0x000F000F
+// is the fp16 pair (k_{2i}, k_{2i+1}))
+__global__ void prefill_codes_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, size_t n) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t w = in[i];
+  uint32_t o = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int pos = (j >> 1) + 4 * (j & 1);
+    o |= ((w >> (4 * j)) & 0xFu) << (4 * pos);
+  }
+  out[i] = o;
+}
+
+cudaError_t launch_prefill_codes(const uint32_t* canon, uint32_t* out, size_t n_words, cudaStream_t st) {
+  prefill_codes_kernel<<<(unsigned)((n_words + 255) / 256), 256, 0, st>>>(canon, out, n_words);
+  return cudaGetLastError();
+}
+
+bool encode_tmap_f16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+                     uint32_t box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !f)
+      return false;
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {ld * 2};
+  const cuuint32_t box[2] = {64, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace hc

@@ -1,0 +1,42 @@
+// Prefill / batched path: tcgen05 (5th-gen tensor core) compensated GEMM.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hc {
+
+constexpr int kPBM = 128;   // tokens per tile (UMMA M, TMEM lanes)
+constexpr int kPBN = 256;   // weight rows per tile (UMMA N, TMEM columns)
+constexpr int kPBK = 64;    // K per pipeline stage (one 128-byte swizzle row of fp16)
+constexpr int kPStages = 4;
+
+// C[m][n] = Σ_k A[m][k]·B[n][k]  (+ Σ_j A2[m][j]·B2[n][j])   fp16 operands, fp32 accumulate in TMEM
+struct PArgs {
+  int M, N, K;          // tokens, output columns (weight rows), reduction length (K % 64 == 0)
+  int K2;               // rank-slice reduction length (multiple of 16, <= 256), 0 = none
+  int n_dim;            // UMMA N of this launch (multiple of 16, <= 256)
+  int b_mode;           // 0: B = dequantised 4-bit weights (prefill codes); 1: B by TMA (fp16)
+  const uint32_t* codes;    // [N][K/8] nibble-paired 4-bit codes (b_mode 0)
+  const uint16_t* scales;   // bf16 [N][K/128]
+  const uint8_t* zeros;     // [N][K/128]
+  void* out;
+  int ldo;                  // row stride of out (elements)
+  int out_type;             // 0 fp32, 1 bf16, 2 fp16
+  int tiles_m, tiles_n;
+};
+
+cudaError_t launch_prefill(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmA2,
+                           const CUtensorMap& tmB2, const PArgs& p, cudaStream_t st);
+
+// bf16 [n] -> fp16 [n]
+cudaError_t launch_bf16_to_f16(const uint16_t* in, uint16_t* out, size_t n, cudaStream_t st);
+// canonical 4-bit codes [rows][K/8] -> prefill nibble order (word w: nibbles k0,k2,k4,k6,k1,k3,k5,k7)
+cudaError_t launch_prefill_codes(const uint32_t* canon, uint32_t* out, size_t n_words, cudaStream_t st);
+
+// Encode a 2-D fp16 tensor map (row-major [outer][inner], row stride ld elements) with a
+// 64 x box_rows box and 128-byte swizzle.  Returns false on failure.
+bool encode_tmap_f16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+                     uint32_t box_rows);
+
+}  // namespace hc
