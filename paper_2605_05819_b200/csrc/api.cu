@@ -83,7 +83,7 @@ struct hc_ctx {
   std::map<Key, Window> windows;
   std::map<std::tuple<int, int, int, int, int>, int> max_ctas;   // (bits, B, K, chunks, vks) -> co-resident CTAs
   DevBuf stage_x, stage_y;
-  DevBuf p_x16, p_t16;                 // prefill scratch: fp16 activations, fp16 T = X·Vᵀ
+  DevBuf p_x16, p_t16, p_tpart;        // prefill scratch: fp16 activations, fp16 T = X·Vᵀ, split-K partials
   // decode stack (hc_stack_forward)
   DevBuf s_h, s_h1, s_qkv, s_m;
   std::map<std::tuple<int, const void*, void*>, std::unique_ptr<StackGraph>> graphs;
@@ -209,10 +209,10 @@ static hc_status build_prefill(Member& m, const Staged& sd, cudaStream_t st) {
   const int rows = m.rows(), G = m.K / hc::kGroup, wpr = m.K / 8;
   CUDA_TRY(m.pcodes->alloc((size_t)rows * wpr * 4));
   CUDA_TRY(hc::launch_prefill_codes(sd.codes + (size_t)m.row_begin * wpr, (uint32_t*)m.pcodes->p, (size_t)rows * wpr, st));
-  CUDA_TRY(m.pscales->alloc((size_t)rows * G * 2));
-  CUDA_TRY(cudaMemcpyAsync(m.pscales->p, sd.scales + (size_t)m.row_begin * G, (size_t)rows * G * 2, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(m.pscales->alloc((size_t)rows * G * 2));   // transposed [G][rows]
   CUDA_TRY(m.pzeros->alloc((size_t)rows * G));
-  CUDA_TRY(cudaMemcpyAsync(m.pzeros->p, sd.zeros + (size_t)m.row_begin * G, (size_t)rows * G, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(hc::launch_transpose_groups(sd.scales + (size_t)m.row_begin * G, sd.zeros + (size_t)m.row_begin * G, rows, G,
+                                       (uint16_t*)m.pscales->p, (uint8_t*)m.pzeros->p, st));
   if (m.r_stored > 0) {
     CUDA_TRY(m.U16->alloc((size_t)rows * m.r_stored * 2));
     CUDA_TRY(hc::launch_bf16_to_f16(sd.U + (size_t)m.row_begin * m.r_stored, (uint16_t*)m.U16->p, (size_t)rows * m.r_stored, st));
@@ -454,24 +454,31 @@ static hc_status launch_prefill_window(hc_ctx* ctx, Window& w, const void* x, in
   int row_off = 0;
   for (const Member& m : w.members) {
     const int r = m.r_alloc, rpad = (r + 15) / 16 * 16, tw = (rpad + 63) / 64 * 64;
+    CUtensorMap tmC;
+    if (!encode_tmap_codes(&tmC, m.pcodes->p, K / 8, m.rows())) return fail(HC_ERR_RUNTIME, "tensor map (codes) encoding failed");
     if (r > 0) {
+      // T = X·V[:r]ᵀ: one 128 x rpad tile column, split-K over the SMs, deterministic reduce to fp16
+      const int tiles_m = (M + kPBM - 1) / kPBM;
+      const int ksplit = std::max(1, std::min(K / kPBK / 4, (ctx->sms + tiles_m - 1) / tiles_m));
       if (ctx->p_t16.bytes < (size_t)M * tw * 2) CUDA_TRY(ctx->p_t16.alloc((size_t)M * tw * 2));
+      if (ctx->p_tpart.bytes < (size_t)ksplit * M * tw * 4) CUDA_TRY(ctx->p_tpart.alloc((size_t)ksplit * M * tw * 4));
       if (!encode_tmap_f16(&tmV, m.V16->p, K, r, K, kPBN)) return fail(HC_ERR_RUNTIME, "tensor map (V) encoding failed");
       PArgs pt{};
-      pt.M = M; pt.N = tw; pt.K = K; pt.K2 = 0; pt.n_dim = rpad; pt.b_mode = 1;
-      pt.out = ctx->p_t16.p; pt.ldo = tw; pt.out_type = 2;
-      pt.tiles_m = (M + kPBM - 1) / kPBM; pt.tiles_n = 1;
-      CUDA_TRY(launch_prefill(tmX, tmV, tmX, tmX, pt, st));
+      pt.M = M; pt.N = tw; pt.K = K; pt.K2 = 0; pt.n_dim = rpad; pt.b_mode = 1; pt.ksplit = ksplit;
+      pt.out = ctx->p_tpart.p; pt.ldo = tw; pt.out_type = 0;
+      pt.tiles_m = tiles_m; pt.tiles_n = 1;
+      CUDA_TRY(launch_prefill(tmX, tmV, tmX, tmX, tmC, pt, st));
+      CUDA_TRY(launch_splitk_reduce_f16((const float*)ctx->p_tpart.p, ksplit, M, tw, (uint16_t*)ctx->p_t16.p, st));
       if (!encode_tmap_f16(&tmT, ctx->p_t16.p, tw, M, tw, kPBM)) return fail(HC_ERR_RUNTIME, "tensor map (T) encoding failed");
       if (!encode_tmap_f16(&tmU, m.U16->p, r, m.rows(), m.r_stored, kPBN)) return fail(HC_ERR_RUNTIME, "tensor map (U) encoding failed");
     }
     PArgs pm{};
-    pm.M = M; pm.N = m.rows(); pm.K = K; pm.K2 = r > 0 ? rpad : 0; pm.n_dim = kPBN; pm.b_mode = 0;
-    pm.codes = (const uint32_t*)m.pcodes->p; pm.scales = (const uint16_t*)m.pscales->p; pm.zeros = (const uint8_t*)m.pzeros->p;
+    pm.M = M; pm.N = m.rows(); pm.K = K; pm.K2 = r > 0 ? rpad : 0; pm.n_dim = kPBN; pm.b_mode = 0; pm.ksplit = 1;
+    pm.scales_t = (const uint16_t*)m.pscales->p; pm.zeros_t = (const uint8_t*)m.pzeros->p;
     pm.out = y_dtype == HC_OUT_F32 ? (void*)((float*)y + row_off) : (void*)((uint16_t*)y + row_off);
     pm.ldo = (int)ldy; pm.out_type = y_dtype == HC_OUT_F32 ? 0 : 1;
     pm.tiles_m = (M + kPBM - 1) / kPBM; pm.tiles_n = m.rows() / kPBN;
-    CUDA_TRY(launch_prefill(tmX, tmX, r > 0 ? tmT : tmX, r > 0 ? tmU : tmX, pm, st));
+    CUDA_TRY(launch_prefill(tmX, tmX, r > 0 ? tmT : tmX, r > 0 ? tmU : tmX, tmC, pm, st));
     row_off += m.rows();
   }
   return HC_OK;

@@ -26,6 +26,9 @@ namespace {
 
 constexpr int kABytes = kPBM * kPBK * 2;   // 16 KB
 constexpr int kBBytes = kPBN * kPBK * 2;   // 32 KB
+constexpr int kCBytes = kPBN * kPBK / 2;   // 8 KB of 4-bit codes per stage
+constexpr int kSBytes = kPBN * 2;          // bf16 scales of the stage's group
+constexpr int kZBytes = kPBN;              // zeros
 constexpr int kThreads = 320;
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -50,6 +53,11 @@ __device__ __forceinline__ void bar_expect_tx(uint64_t* b, uint32_t bytes) {
 }
 __device__ __forceinline__ void bar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(b)) : "memory");
+}
+__device__ __forceinline__ void bulk_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(s_u32(dst)),
+               "l"(src), "r"(bytes), "r"(s_u32(bar))
+               : "memory");
 }
 __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
   asm volatile(
@@ -113,22 +121,29 @@ __device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t b, uint32_t
 __global__ void __launch_bounds__(kThreads, 1)
     prefill_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
-                   const __grid_constant__ PArgs p) {
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ PArgs p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = base;
-  uint8_t* sB = base + kPStages * kABytes;
-  uint64_t* full_a = reinterpret_cast<uint64_t*>(sB + kPStages * kBBytes);
+  uint8_t* sB = sA + kPStages * kABytes;
+  uint8_t* sC = sB + kPStages * kBBytes;
+  uint8_t* sS = sC + kPStages * kCBytes;
+  uint8_t* sZ = sS + kPStages * kSBytes;
+  uint64_t* full_a = reinterpret_cast<uint64_t*>(sZ + kPStages * kZBytes);
   uint64_t* full_b = full_a + kPStages;
   uint64_t* empty = full_b + kPStages;
   uint64_t* tmem_full = empty + kPStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tm = blockIdx.x % p.tiles_m, tn = blockIdx.x / p.tiles_m;
+  const int n_tiles = p.tiles_m * p.tiles_n;
+  const int tile = blockIdx.x % n_tiles, ks = blockIdx.x / n_tiles;
+  const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
   const int m0 = tm * kPBM, n0 = tn * kPBN;
-  const int nkb1 = p.K / kPBK;
-  const int nkb2 = (p.K2 + kPBK - 1) / kPBK;
+  const int nkb_all = p.K / kPBK;
+  const int kb_lo = ks * nkb_all / p.ksplit, kb_hi = (ks + 1) * nkb_all / p.ksplit;
+  const int nkb1 = kb_hi - kb_lo;                        // main k-blocks of this CTA
+  const int nkb2 = (p.K2 + kPBK - 1) / kPBK;             // rank-slice k-blocks
   const int nkb = nkb1 + nkb2;
 
   if (threadIdx.x == 0) {
@@ -155,18 +170,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ======================= TMA producer =======================
     if (lane == 0) {
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % kPStages;
-        if (kb >= kPStages) bar_wait(&empty[s], ((kb / kPStages) + 1) & 1);
-        const bool main = kb < nkb1;
-        const bool b_tma = !main || p.b_mode == 1;
-        bar_expect_tx(&full_a[s], (uint32_t)(kABytes + (b_tma ? kBBytes : 0)));
-        if (main) {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % kPStages;
+        if (i >= kPStages) bar_wait(&empty[s], ((i / kPStages) + 1) & 1);
+        const bool main = i < nkb1;
+        const int kb = kb_lo + i;
+        if (main && p.b_mode == 0) {
+          // X tile + this k-block's codes (256 rows x 32 B) + the group's scales and zeros
+          bar_expect_tx(&full_a[s], (uint32_t)(kABytes + kCBytes + kSBytes + kZBytes));
           tma_2d(sA + s * kABytes, &tmA, kb * kPBK, m0, &full_a[s]);
-          if (b_tma) tma_2d(sB + s * kBBytes, &tmB, kb * kPBK, n0, &full_a[s]);
+          tma_2d(sC + s * kCBytes, &tmC, kb * (kPBK / 8), n0, &full_a[s]);
+          const int g = kb >> 1;
+          bulk_1d(sS + s * kSBytes, p.scales_t + (size_t)g * p.N + n0, kSBytes, &full_a[s]);
+          bulk_1d(sZ + s * kZBytes, p.zeros_t + (size_t)g * p.N + n0, kZBytes, &full_a[s]);
+        } else if (main) {
+          bar_expect_tx(&full_a[s], (uint32_t)(kABytes + kBBytes));
+          tma_2d(sA + s * kABytes, &tmA, kb * kPBK, m0, &full_a[s]);
+          tma_2d(sB + s * kBBytes, &tmB, kb * kPBK, n0, &full_a[s]);
         } else {
-          tma_2d(sA + s * kABytes, &tmA2, (kb - nkb1) * kPBK, m0, &full_a[s]);
-          tma_2d(sB + s * kBBytes, &tmB2, (kb - nkb1) * kPBK, n0, &full_a[s]);
+          bar_expect_tx(&full_a[s], (uint32_t)(kABytes + kBBytes));
+          tma_2d(sA + s * kABytes, &tmA2, (i - nkb1) * kPBK, m0, &full_a[s]);
+          tma_2d(sB + s * kBBytes, &tmB2, (i - nkb1) * kPBK, n0, &full_a[s]);
         }
       }
     }
@@ -174,60 +198,47 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ======================= MMA issuer (one thread) =======================
     if (lane == 0) {
       const uint32_t idesc = umma_idesc(p.n_dim);
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % kPStages;
-        const uint32_t ph = (kb / kPStages) & 1;
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % kPStages;
+        const uint32_t ph = (i / kPStages) & 1;
         bar_wait(&full_a[s], ph);
         bar_wait(&full_b[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int nk = kb < nkb1 ? kPBK / 16 : min(kPBK, p.K2 - (kb - nkb1) * kPBK) / 16;
+        const int nk = i < nkb1 ? kPBK / 16 : min(kPBK, p.K2 - (i - nkb1) * kPBK) / 16;
         const uint64_t ad = umma_desc(sA + s * kABytes), bd = umma_desc(sB + s * kBBytes);
         for (int k = 0; k < nk; ++k)   // advance 16 fp16 = 32 bytes along K inside the swizzled rows
-          umma_f16(tmem_base, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc, (kb | k) != 0);
+          umma_f16(tmem_base, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc, (i | k) != 0);
         umma_commit(&empty[s]);
       }
       umma_commit(tmem_full);
     }
   } else if (warp < 6) {
-    // ======================= dequant producers =======================
+    // ======================= dequant producers (smem -> smem) =======================
     const int t = threadIdx.x - 64;            // 0..127: rows t and t + 128 of the B tile
-    const int G = p.K / kGroup;
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % kPStages;
-      const bool dq = kb < nkb1 && p.b_mode == 0;
-      uint4 cw[2][2];
-      uint32_t sc[2], zz[2];
-      if (dq) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int n = min(n0 + t + 128 * h, p.N - 1);
-          const uint4* src = reinterpret_cast<const uint4*>(p.codes + (size_t)n * (p.K / 8) + 8 * kb);
-          cw[h][0] = __ldg(src);
-          cw[h][1] = __ldg(src + 1);
-          const int g = kb >> 1;
-          const float sf = __uint_as_float((uint32_t)p.scales[(size_t)n * G + g] << 16);
-          const __half s16 = __float2half_rn(sf);
-          sc[h] = (uint32_t)__half_as_ushort(s16) * 0x00010001u;                  // half2(s, s)
-          zz[h] = (0x6400u + (uint32_t)p.zeros[(size_t)n * G + g]) * 0x00010001u;  // half2(1024+z)
-        }
-      }
-      if (kb >= kPStages) bar_wait(&empty[s], ((kb / kPStages) + 1) & 1);
-      if (dq) {
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % kPStages;
+      bar_wait(&full_a[s], (i / kPStages) & 1);   // codes of this stage landed (and stage s is free)
+      if (i < nkb1 && p.b_mode == 0) {
         uint8_t* tile = sB + s * kBBytes;
+        const uint8_t* codes = sC + s * kCBytes;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int row = t + 128 * h;
-          const uint32_t words[8] = {cw[h][0].x, cw[h][0].y, cw[h][0].z, cw[h][0].w,
-                                     cw[h][1].x, cw[h][1].y, cw[h][1].z, cw[h][1].w};
+          const uint4 c0 = *reinterpret_cast<const uint4*>(codes + row * 32);
+          const uint4 c1 = *reinterpret_cast<const uint4*>(codes + row * 32 + 16);
+          const uint32_t words[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+          const float sf = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(sS + s * kSBytes)[row] << 16);
+          const uint32_t sc = (uint32_t)__half_as_ushort(__float2half_rn(sf)) * 0x00010001u;      // half2(s, s)
+          const uint32_t zz = (0x6400u + (uint32_t)(sZ + s * kZBytes)[row]) * 0x00010001u;       // half2(1024+z)
 #pragma unroll
           for (int c = 0; c < 8; ++c) {        // word c = k 8c..8c+7 = 16-byte chunk c of the row
             uint32_t v[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              uint32_t hv = lop3_and_or(words[c] >> (4 * i), 0x000F000Fu, 0x64006400u);   // half2(1024 + q)
-              __half2 d = __hsub2(*reinterpret_cast<__half2*>(&hv), *reinterpret_cast<const __half2*>(&zz[h]));
-              d = __hmul2(d, *reinterpret_cast<const __half2*>(&sc[h]));                 // fp16(s·(q − z))
-              v[i] = *reinterpret_cast<uint32_t*>(&d);
+            for (int j = 0; j < 4; ++j) {
+              uint32_t hv = lop3_and_or(words[c] >> (4 * j), 0x000F000Fu, 0x64006400u);   // half2(1024 + q)
+              __half2 d = __hsub2(*reinterpret_cast<__half2*>(&hv), *reinterpret_cast<const __half2*>(&zz));
+              d = __hmul2(d, *reinterpret_cast<const __half2*>(&sc));                      // fp16(s·(q − z))
+              v[j] = *reinterpret_cast<uint32_t*>(&d);
             }
             *reinterpret_cast<uint4*>(tile + sw128(row, c)) = make_uint4(v[0], v[1], v[2], v[3]);
           }
@@ -242,6 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int m = m0 + 32 * q + lane;
     bar_wait(tmem_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    void* outp = p.ksplit > 1 ? (void*)(reinterpret_cast<float*>(p.out) + (size_t)ks * p.M * p.ldo) : p.out;
     for (int c0 = 0; c0 < p.n_dim; c0 += 32) {
       uint32_t v[32];
       const uint32_t addr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
@@ -257,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int n = n0 + c0;
       if (m < p.M && n < p.N) {
         if (p.out_type == 0) {
-          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + (size_t)m * p.ldo + n);
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(outp) + (size_t)m * p.ldo + n);
 #pragma unroll
           for (int i = 0; i < 8; ++i)
             dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
@@ -275,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               pk[i] = *reinterpret_cast<uint32_t*>(&h2);
             }
           }
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) + (size_t)m * p.ldo + n);
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(outp) + (size_t)m * p.ldo + n);
 #pragma unroll
           for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
         }
@@ -291,19 +303,68 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 static size_t prefill_smem() {
-  return (size_t)kPStages * (kABytes + kBBytes) + (3 * kPStages + 2) * 8 + 1024;
+  return (size_t)kPStages * (kABytes + kBBytes + kCBytes + kSBytes + kZBytes) + (3 * kPStages + 2) * 8 + 1024;
 }
 
 cudaError_t launch_prefill(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmA2,
-                           const CUtensorMap& tmB2, const PArgs& p, cudaStream_t st) {
+                           const CUtensorMap& tmB2, const CUtensorMap& tmC, const PArgs& p, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prefill_smem());
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  prefill_kernel<<<p.tiles_m * p.tiles_n, kThreads, prefill_smem(), st>>>(tmA, tmB, tmA2, tmB2, p);
+  prefill_kernel<<<p.tiles_m * p.tiles_n * p.ksplit, kThreads, prefill_smem(), st>>>(tmA, tmB, tmA2, tmB2, tmC, p);
   return cudaGetLastError();
+}
+
+__global__ void splitk_reduce_kernel(const float* __restrict__ part, int ksplit, size_t n, uint16_t* __restrict__ out) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float acc = 0.f;
+  for (int k = 0; k < ksplit; ++k) acc += part[(size_t)k * n + i];   // fixed order: deterministic
+  out[i] = __half_as_ushort(__float2half_rn(acc));
+}
+
+cudaError_t launch_splitk_reduce_f16(const float* partial, int ksplit, int M, int ld, uint16_t* out, cudaStream_t st) {
+  const size_t n = (size_t)M * ld;
+  splitk_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(partial, ksplit, n, out);
+  return cudaGetLastError();
+}
+
+__global__ void transpose_groups_kernel(const uint16_t* __restrict__ s_in, const uint8_t* __restrict__ z_in, int rows,
+                                        int G, uint16_t* __restrict__ s_out, uint8_t* __restrict__ z_out) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (size_t)rows * G) return;
+  const int r = (int)(i / G), g = (int)(i % G);
+  s_out[(size_t)g * rows + r] = s_in[i];
+  z_out[(size_t)g * rows + r] = z_in[i];
+}
+
+cudaError_t launch_transpose_groups(const uint16_t* s_in, const uint8_t* z_in, int rows, int G, uint16_t* s_out,
+                                    uint8_t* z_out, cudaStream_t st) {
+  const size_t n = (size_t)rows * G;
+  transpose_groups_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s_in, z_in, rows, G, s_out, z_out);
+  return cudaGetLastError();
+}
+
+bool encode_tmap_codes(CUtensorMap* map, const void* base, uint64_t words_per_row, uint64_t rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !f)
+      return false;
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  const cuuint64_t dims[2] = {words_per_row, rows};
+  const cuuint64_t strides[1] = {words_per_row * 4};
+  const cuuint32_t box[2] = {8, 256};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 __global__ void bf16_to_f16_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out, size_t n) {

@@ -9,7 +9,7 @@ namespace hc {
 constexpr int kPBM = 128;   // tokens per tile (UMMA M, TMEM lanes)
 constexpr int kPBN = 256;   // weight rows per tile (UMMA N, TMEM columns)
 constexpr int kPBK = 64;    // K per pipeline stage (one 128-byte swizzle row of fp16)
-constexpr int kPStages = 4;
+constexpr int kPStages = 3;
 
 // C[m][n] = Σ_k A[m][k]·B[n][k]  (+ Σ_j A2[m][j]·B2[n][j])   fp16 operands, fp32 accumulate in TMEM
 struct PArgs {
@@ -17,17 +17,24 @@ struct PArgs {
   int K2;               // rank-slice reduction length (multiple of 16, <= 256), 0 = none
   int n_dim;            // UMMA N of this launch (multiple of 16, <= 256)
   int b_mode;           // 0: B = dequantised 4-bit weights (prefill codes); 1: B by TMA (fp16)
-  const uint32_t* codes;    // [N][K/8] nibble-paired 4-bit codes (b_mode 0)
-  const uint16_t* scales;   // bf16 [N][K/128]
-  const uint8_t* zeros;     // [N][K/128]
+  const uint16_t* scales_t; // bf16 [K/128][N]  (b_mode 0; transposed so a stage reads 256 contiguous)
+  const uint8_t* zeros_t;   // [K/128][N]
+  int ksplit;               // split-K factor (>= 1); partial sums go to out + ks·M·ldo (fp32 only)
   void* out;
   int ldo;                  // row stride of out (elements)
   int out_type;             // 0 fp32, 1 bf16, 2 fp16
   int tiles_m, tiles_n;
 };
 
+// tmC: 2-D u32 tensor map over the nibble-paired codes [N][K/8] (box 8 words x 256 rows), b_mode 0.
 cudaError_t launch_prefill(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmA2,
-                           const CUtensorMap& tmB2, const PArgs& p, cudaStream_t st);
+                           const CUtensorMap& tmB2, const CUtensorMap& tmC, const PArgs& p, cudaStream_t st);
+// Σ_ks partial[ks][m][0..n) -> fp16 out[m][0..ld) (deterministic split-K reduction)
+cudaError_t launch_splitk_reduce_f16(const float* partial, int ksplit, int M, int ld, uint16_t* out, cudaStream_t st);
+bool encode_tmap_codes(CUtensorMap* map, const void* base, uint64_t words_per_row, uint64_t rows);
+// [rows][G] -> [G][rows] transposes of the per-group scales (bf16) and zeros (u8)
+cudaError_t launch_transpose_groups(const uint16_t* s_in, const uint8_t* z_in, int rows, int G, uint16_t* s_out,
+                                    uint8_t* z_out, cudaStream_t st);
 
 // bf16 [n] -> fp16 [n]
 cudaError_t launch_bf16_to_f16(const uint16_t* in, uint16_t* out, size_t n, cudaStream_t st);
