@@ -165,6 +165,15 @@ hc_status hc_compensated_linear(hc_ctx* ctx, int32_t layer, int32_t window_kind,
  * HC_ERR_STATE if a layer lacks a window or its UPGATE window is not SiLU-fused. */
 hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, void* y, void* stream);
 
+/* Column sharding across GPUs.  Rank 0 calls hc_nccl_unique_id and shares the 128
+ * bytes with every rank (e.g. through torch.distributed); each rank then calls hc_set_comm with its
+ * rank and the world size (ncclCommInitRank on the context's device; NCCL is loaded at run time).
+ * With a communicator set, every member of the stack must hold rows [rank·N/G, (rank+1)·N/G) and
+ * hc_stack_forward gathers each window's output slices with ncclAllGather over NVLink before the
+ * next window (x and V·x stay replicated).  HC_ERR_RUNTIME if NCCL is unavailable. */
+hc_status hc_nccl_unique_id(uint8_t* out128);
+hc_status hc_set_comm(hc_ctx* ctx, const uint8_t* id128, int32_t rank, int32_t world);
+
 /* Debug/test exports (host only, no GPU needed): the load-time repack and its inverse. */
 size_t hc_repacked_bytes(int32_t N, int32_t K, int32_t bits);
 hc_status hc_repack_host(const uint32_t* codes, const uint16_t* scales, const uint8_t* zeros,
@@ -173,6 +182,12 @@ hc_status hc_repack_host(const uint32_t* codes, const uint16_t* scales, const ui
  * through the kernel's own fragment/slot mapping. */
 hc_status hc_unpack_repacked_host(const uint8_t* packed, int32_t N, int32_t K, int32_t bits,
                                   uint8_t* q_out, uint16_t* scales_out, uint8_t* zeros_out);
+/* The column-sharding gather permutation on the host: all-gathered slices [G][B][n_local] (a window
+ * of n_members members with local widths widths[], n_local = Σ widths) -> canonical [B][G·n_local]
+ * (member m's full rows are the G local slices in rank order).  Same index map as the device kernel
+ * hc_stack_forward uses after ncclAllGather. */
+hc_status hc_unshard_host(const uint16_t* gathered, uint16_t* out, int32_t G, int32_t B, int32_t n_members,
+                          const int32_t* widths);
 
 #ifdef __cplusplus
 }

@@ -18,7 +18,16 @@ from ._lib import (HCError, HC_OK, HC_ERR_CONFIG, HC_ERR_STATE, HC_ERR_NUMERIC, 
 
 __all__ = ["allocate_ranks", "Context", "HCError", "QKV", "O", "UPGATE", "DOWN", "OUT_F32", "OUT_BF16",
            "GLUE_NONE", "GLUE_SILU_MUL",
-           "repack_host", "unpack_repacked_host", "lib"]
+           "repack_host", "unpack_repacked_host", "shard_rows", "unshard_host", "lib"]
+
+
+def shard_rows(N: int, world: int, rank: int, unit: int = 16):
+    """Column sharding of a weight matrix's output rows: rank p keeps rows
+    [p·N/G, (p+1)·N/G).  N/G must be a multiple of `unit` (16 = the kernel's row block)."""
+    if N % world or (N // world) % unit:
+        raise ValueError(f"N={N} cannot be column-sharded over {world} ranks in {unit}-row units")
+    n = N // world
+    return rank * n, (rank + 1) * n
 
 
 def _ptr(a):
@@ -99,6 +108,15 @@ def unpack_repacked_host(packed, N, K, bits):
     return q, s, z
 
 
+def unshard_host(gathered, G, B, widths):
+    """hc_unshard_host: [G][B][Σw] gathered slices -> [B][G·Σw] canonical (uint16 bit patterns)."""
+    widths = np.ascontiguousarray(widths, dtype=np.int32)
+    gathered = np.ascontiguousarray(gathered, dtype=np.uint16)
+    out = np.zeros((B, G * int(widths.sum())), dtype=np.uint16)
+    check(lib().hc_unshard_host(_ptr(gathered), _ptr(out), G, B, len(widths), _ptr(widths)))
+    return out
+
+
 # ------------------------------------------------------------------ device context
 class Context:
     """hc_ctx: owns the repacked weights of loaded windows on one CUDA device."""
@@ -135,6 +153,19 @@ class Context:
             d.row_begin, d.row_end = int(m.get("row_begin", 0)), int(m.get("row_end", m["N"]))
             d.glue = int(m.get("glue", 0))
         check(lib().hc_load_layer(self._h, arr, len(mats), _stream(stream)))
+
+    def init_comm(self, rank: int, world: int, group=None):
+        """Create the context's NCCL communicator: rank 0's unique id is broadcast through
+        torch.distributed (any backend), then hc_set_comm."""
+        import torch
+        import torch.distributed as dist
+        buf = np.zeros(128, dtype=np.uint8)
+        if rank == 0:
+            check(lib().hc_nccl_unique_id(buf.ctypes.data))
+        obj = [buf.tobytes()]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        buf = np.frombuffer(obj[0], dtype=np.uint8).copy()
+        check(lib().hc_set_comm(self._h, buf.ctypes.data, int(rank), int(world)))
 
     def set_rank(self, layer, window, slot, r, expert=-1):
         check(lib().hc_set_rank(self._h, layer, window, slot, expert, r))

@@ -18,7 +18,7 @@ BUILD = os.path.join(PKG, "_build")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["api.cu", "decode.cu", "prefill.cu", "repack.cu"]
+CU_SOURCES = ["api.cu", "comm.cu", "decode.cu", "prefill.cu", "repack.cu"]
 CPP_SOURCES = ["alloc.cpp"]
 
 
@@ -59,7 +59,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
             log.append(_run(["g++", "-c", s, "-o", o, "-std=c++17", "-O2", "-fPIC", "-ffp-contract=off",
                              "-fno-fast-math", "-I", INC, "-I", CSRC]))
     if force or _stale(LIB, objs):
-        log.append(_run([NVCC, "-shared", "-o", LIB, *objs, *ARCH, "-lcudart"]))
+        log.append(_run([NVCC, "-shared", "-o", LIB, *objs, *ARCH, "-lcudart", "-ldl"]))
     out = "\n".join(x for x in log if x)
     if verbose and out:
         print(out)

@@ -10,6 +10,7 @@
 #include <tuple>
 #include <vector>
 
+#include "comm.h"
 #include "decode.h"
 #include "prefill.h"
 #include "hcinfer.h"
@@ -88,6 +89,10 @@ struct hc_ctx {
   DevBuf s_h, s_h1, s_qkv, s_m;
   std::map<std::tuple<int, const void*, void*>, std::unique_ptr<StackGraph>> graphs;
   cudaStream_t cap_stream = nullptr;
+  // column sharding (hc_set_comm): NCCL communicator, send / gather staging
+  hc::Comm* comm = nullptr;
+  int rank = 0, world = 1;
+  DevBuf t_send, t_gather;
   void invalidate_graphs() { graphs.clear(); }
 };
 
@@ -129,7 +134,30 @@ extern "C" hc_status hc_destroy(hc_ctx* ctx) {
   cudaDeviceSynchronize();
   ctx->graphs.clear();
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+  hc::comm_destroy(ctx->comm);
   delete ctx;
+  return HC_OK;
+}
+
+extern "C" hc_status hc_nccl_unique_id(uint8_t* out) {
+  if (!out) return fail(HC_ERR_CONFIG, "hc_nccl_unique_id: null output");
+  char msg[256];
+  if (!hc::comm_unique_id(out, msg, sizeof(msg))) return fail(HC_ERR_RUNTIME, "%s", msg);
+  return HC_OK;
+}
+
+extern "C" hc_status hc_set_comm(hc_ctx* ctx, const uint8_t* id, int32_t rank, int32_t world) {
+  if (!ctx) return fail(HC_ERR_STATE, "hc_set_comm: null context");
+  if (!id || world < 1 || rank < 0 || rank >= world) return fail(HC_ERR_CONFIG, "hc_set_comm: rank %d / world %d", rank, world);
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  char msg[256];
+  hc::Comm* c = hc::comm_create(id, rank, world, msg, sizeof(msg));
+  if (!c) return fail(HC_ERR_RUNTIME, "%s", msg);
+  hc::comm_destroy(ctx->comm);
+  ctx->comm = c;
+  ctx->rank = rank;
+  ctx->world = world;
+  ctx->invalidate_graphs();
   return HC_OK;
 }
 
@@ -543,18 +571,49 @@ hc_status stack_plan(hc_ctx* ctx, std::vector<LayerPlan>& plan, int& d, int& nqk
     plan.push_back(LayerPlan{&f0->second, &f1->second, &f2->second, &f3->second});
   }
   if (plan.empty()) return fail(HC_ERR_STATE, "hc_stack_forward: no layer 0 QKV window loaded");
+  // full (unsharded) widths: G x the local rows of every member
+  const int G = ctx->world;
   const LayerPlan& p0 = plan.front();
   d = p0.qkv->members.front().K;
-  nqkv = (int)p0.qkv->out_rows();
-  f = (int)p0.ug->out_rows();
+  nqkv = (int)(G * p0.qkv->out_rows());
+  f = (int)(G * p0.ug->out_rows());
   for (size_t l = 0; l < plan.size(); ++l) {
     const LayerPlan& p = plan[l];
-    const int q_rows = p.qkv->members.front().rows();
-    if (p.qkv->members.front().K != d || p.qkv->out_rows() != nqkv || q_rows != d || p.o->members.front().K != d ||
-        p.o->out_rows() != d || p.ug->members.front().K != d || p.ug->out_rows() != f ||
-        p.down->members.front().K != f || p.down->out_rows() != d)
+    const int q_rows = G * p.qkv->members.front().rows();
+    if (p.qkv->members.front().K != d || G * p.qkv->out_rows() != nqkv || q_rows != d || p.o->members.front().K != d ||
+        G * p.o->out_rows() != d || p.ug->members.front().K != d || G * p.ug->out_rows() != f ||
+        p.down->members.front().K != f || G * p.down->out_rows() != d)
       return fail(HC_ERR_CONFIG, "hc_stack_forward: layer %zu shapes inconsistent (need q rows = hidden = O/DOWN rows)", l);
+    if (G > 1)
+      for (Window* w : {p.qkv, p.o, p.ug, p.down})
+        for (const Member& m : w->members)
+          if (G * m.rows() != m.N || m.row_begin != ctx->rank * m.rows())
+            return fail(HC_ERR_CONFIG, "hc_stack_forward: layer %zu member not column-sharded as rows [rank*N/G, (rank+1)*N/G)", l);
   }
+  return HC_OK;
+}
+
+// One window of a column-sharded stack: local rows -> NCCL all-gather -> canonical full layout.
+static hc_status tp_window(hc_ctx* ctx, Window& w, const void* x, int ldx, int B, void* full_out, const void* resid_full,
+                           int ld_resid, cudaStream_t st) {
+  const int n_local = (int)w.out_rows();
+  uint16_t* send = (uint16_t*)ctx->t_send.p;
+  const void* resid = resid_full ? (const void*)((const uint16_t*)resid_full + (size_t)ctx->rank * n_local) : nullptr;
+  hc_status s = hc::launch_window(ctx, w, x, ldx, B, send, 1, resid, ld_resid, st);
+  if (s != HC_OK) return s;
+  char msg[256];
+  if (!hc::comm_allgather_bf16(ctx->comm, send, ctx->t_gather.p, (size_t)B * n_local, st, msg, sizeof(msg)))
+    return fail(HC_ERR_RUNTIME, "%s", msg);
+  hc::GatherPlan gp{};
+  gp.G = ctx->world; gp.B = B; gp.n_local = n_local;
+  if (w.glue == HC_GLUE_SILU_MUL) {
+    gp.n_members = 1; gp.w[0] = n_local; gp.o[0] = 0;
+  } else {
+    gp.n_members = (int)w.members.size();
+    int o = 0;
+    for (int i = 0; i < gp.n_members; ++i) { gp.w[i] = w.members[i].rows(); gp.o[i] = o; o += gp.w[i]; }
+  }
+  CUDA_TRY(hc::launch_unshard((const uint16_t*)ctx->t_gather.p, (uint16_t*)full_out, gp, st));
   return HC_OK;
 }
 
@@ -590,6 +649,12 @@ extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, voi
   }
   if (ctx->s_qkv.bytes < (size_t)16 * nqkv * 2) { ctx->invalidate_graphs(); CUDA_TRY(ctx->s_qkv.alloc((size_t)16 * nqkv * 2)); }
   if (ctx->s_m.bytes < (size_t)16 * f * 2) { ctx->invalidate_graphs(); CUDA_TRY(ctx->s_m.alloc((size_t)16 * f * 2)); }
+  const bool tp = ctx->comm != nullptr;
+  if (tp) {
+    const size_t widest = (size_t)std::max(std::max(nqkv, f), d);   // full width of any window output
+    if (ctx->t_send.bytes < (size_t)16 * widest * 2) { ctx->invalidate_graphs(); CUDA_TRY(ctx->t_send.alloc((size_t)16 * widest * 2)); }
+    if (ctx->t_gather.bytes < (size_t)16 * widest * 2) { ctx->invalidate_graphs(); CUDA_TRY(ctx->t_gather.alloc((size_t)16 * widest * 2)); }
+  }
 
   auto key = std::make_tuple((int)B, dx, dy);
   auto git = ctx->graphs.find(key);
@@ -614,10 +679,17 @@ extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, voi
     for (size_t l = 0; l < plan.size() && cap == HC_OK; ++l) {
       LayerPlan& p = plan[l];
       uint16_t* hout = (l + 1 == plan.size()) ? (uint16_t*)dy : h;
-      cap = hc::launch_window(ctx, *p.qkv, hin, d, B, qkv, 1, nullptr, 0, cs);                 // q | k | v
-      if (cap == HC_OK) cap = hc::launch_window(ctx, *p.o, qkv, nqkv, B, h1, 1, hin, d, cs);   // h1 = h + O(q)
-      if (cap == HC_OK) cap = hc::launch_window(ctx, *p.ug, h1, d, B, mm, 1, nullptr, 0, cs);  // m = silu(g)·u
-      if (cap == HC_OK) cap = hc::launch_window(ctx, *p.down, mm, f, B, hout, 1, h1, d, cs);   // h' = h1 + DOWN(m)
+      if (!tp) {
+        cap = hc::launch_window(ctx, *p.qkv, hin, d, B, qkv, 1, nullptr, 0, cs);                 // q | k | v
+        if (cap == HC_OK) cap = hc::launch_window(ctx, *p.o, qkv, nqkv, B, h1, 1, hin, d, cs);   // h1 = h + O(q)
+        if (cap == HC_OK) cap = hc::launch_window(ctx, *p.ug, h1, d, B, mm, 1, nullptr, 0, cs);  // m = silu(g)·u
+        if (cap == HC_OK) cap = hc::launch_window(ctx, *p.down, mm, f, B, hout, 1, h1, d, cs);   // h' = h1 + DOWN(m)
+      } else {                                                   // column-sharded: gather every window
+        cap = tp_window(ctx, *p.qkv, hin, d, B, qkv, nullptr, 0, cs);
+        if (cap == HC_OK) cap = tp_window(ctx, *p.o, qkv, nqkv, B, h1, hin, d, cs);
+        if (cap == HC_OK) cap = tp_window(ctx, *p.ug, h1, d, B, mm, nullptr, 0, cs);
+        if (cap == HC_OK) cap = tp_window(ctx, *p.down, mm, f, B, hout, h1, d, cs);
+      }
       hin = hout;
     }
     cudaGraph_t g = nullptr;

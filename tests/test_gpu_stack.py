@@ -141,3 +141,30 @@ def test_stack_errors(hc):
         ctx.stack_forward(dev(synth.activations(1, 1, 256)), torch.empty((1, 256), dtype=torch.int16, device="cuda"))
     assert ei.value.code == hc.HC_ERR_STATE
     ctx.close()
+
+
+def test_stack_nccl_path_single_rank_matches(hc):
+    """The column-sharded code path (local rows -> ncclAllGather -> unshard) with one rank must equal
+    the plain stack bit-for-bit (G = 1 exercises every launch of the multi-GPU path)."""
+    import os
+    import torch.distributed as dist
+    L, d, kv, f = 2, 256, 128, 384
+    layers, ranks = make_stack(L, d, kv, f, 4, 32, seed=91)
+    x = synth.activations(4, 3, d)
+    plain = hc.Context(0)
+    load_stack(hc, plain, layers, ranks)
+    y0 = torch.empty((3, d), dtype=torch.int16, device="cuda")
+    plain.stack_forward(dev(x), y0)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29531")
+    if not dist.is_initialized():
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    tp = hc.Context(0)
+    tp.init_comm(0, 1)
+    load_stack(hc, tp, layers, ranks)
+    y1 = torch.empty((3, d), dtype=torch.int16, device="cuda")
+    tp.stack_forward(dev(x), y1)
+    torch.cuda.synchronize()
+    assert np.array_equal(y0.cpu().numpy(), y1.cpu().numpy())
+    tp.close()
+    plain.close()
