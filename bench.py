@@ -181,8 +181,12 @@ def oracle_c1_sample(seconds: float = 12.0):
     return n, el
 
 
-# ------------------------------------------------------------------ workload C2 (headline)
-C2 = dict(model="llama2_7b", hidden=4096, kv=4096, ffn=11008, layers=32, bits=4, group=128, r_stored=128)
+# ------------------------------------------------------------------ stacks: C2 (headline), C5 (multi-GPU)
+C2 = dict(name="c2", model="llama2_7b", hidden=4096, kv=4096, ffn=11008, layers=32, bits=4, group=128,
+          r_stored=128, fixed_rank=None)
+C5 = dict(name="c5", model="llama3_70b", hidden=8192, kv=1024, ffn=28672, layers=80, bits=2, group=128,
+          r_stored=64, fixed_rank=64)
+STACKS = {"c2": C2, "c5": C5}
 
 
 def window_bytes_base(Ns, K, bits, g=128):
@@ -206,7 +210,11 @@ def c2_r_std(c=C2):
 
 
 def c2_ranks(c=C2, seed=0):
-    """Ranks from the library's allocator on synthetic sensitivity inputs (planted spectra)."""
+    """Ranks from the library's allocator on synthetic sensitivity inputs (planted spectra); C5 uses the
+    fixed rank of its BASELINE config (r = 64)."""
+    if c.get("fixed_rank") is not None:
+        return {(l, kind, s): c["fixed_rank"] for l in range(c["layers"]) for kind, Ns, K in c2_windows(c)
+                for s in range(len(Ns))}
     import synth
     import paper_2605_05819_b200 as hc
     case = synth.sensitivity_case(seed, n_layers=c["layers"], members_per_window=(3, 1, 2, 1), n_sigma=256)
@@ -221,23 +229,28 @@ def c2_ranks(c=C2, seed=0):
     return out
 
 
-def c2_bytes(ranks, B, c=C2):
-    """Algorithmic bytes of one decode step: every base weight byte (codes, bf16 scale, b-bit zero),
-    the allocated rank slices of U and V (bf16), and the activations in/out of each window."""
+def c2_bytes(ranks, B, c=C2, G=1):
+    """Algorithmic bytes one GPU moves per decode step: its rows of every base weight (codes, bf16 scale,
+    b-bit zero), its rows of the allocated U slices and ALL of the allocated V slices (V·x is replicated
+    under column sharding), and the activations in/out of each window."""
     tot = 0
     for l in range(c["layers"]):
         for kind, Ns, K in c2_windows(c):
-            tot += window_bytes_base(Ns, K, c["bits"])
+            tot += window_bytes_base([N // G for N in Ns], K, c["bits"])
             for s, N in enumerate(Ns):
-                tot += 2 * ranks[(l, kind, s)] * (N + K)
-            tot += B * 2 * K + B * 2 * (sum(Ns) if kind != 2 else Ns[0])
+                tot += 2 * ranks[(l, kind, s)] * (N // G + K)
+            tot += B * 2 * K + B * 2 * ((sum(Ns) if kind != 2 else Ns[0]) // G)
     return tot
 
 
-def build_c2(ctx, ranks, rank_id, c=C2):
+def build_c2(ctx, ranks, c=C2, shard=None):
+    """Random-init weights of the named shapes, generated on the device; every matrix has its own seed so
+    all ranks of a column-sharded run see the same model and load rows [rank·N/G, (rank+1)·N/G)."""
     import torch
-    g = torch.Generator(device="cuda").manual_seed(4242 + rank_id)
+    import paper_2605_05819_b200 as hc
     gains = (1.0, 1.0, 1.0, 0.25, 0.25, 0.25, 0.05)   # synth.STACK_GAINS (finite over 32 layers)
+    if c["layers"] > 32:
+        gains = (1.0, 1.0, 1.0, 0.2, 0.2, 0.2, 0.02)  # 80 layers: stronger damping keeps the output finite
     b = c["bits"]
     e2 = ((4 ** b) - 1) / 12.0 + 0.25
     slot_gain = {(0, 0): 0, (0, 1): 1, (0, 2): 2, (1, 0): 3, (2, 0): 4, (2, 1): 5, (3, 0): 6}
@@ -246,10 +259,12 @@ def build_c2(ctx, ranks, rank_id, c=C2):
         for kind, Ns, K in c2_windows(c):
             G = K // c["group"]
             for s, N in enumerate(Ns):
+                g = torch.Generator(device="cuda").manual_seed(4242 + 100 * l + 10 * kind + s)
                 gain = gains[slot_gain[(kind, s)]]
                 rs = c["r_stored"]
+                lo, hi = (0, N) if shard is None else hc.shard_rows(N, shard[1], shard[0])
                 mats.append(dict(
-                    layer=l, window=kind, slot=s, N=N, K=K, bits=b,
+                    layer=l, window=kind, slot=s, N=N, K=K, bits=b, row_begin=lo, row_end=hi,
                     codes=torch.randint(-2**31, 2**31, (N, K * b // 32), generator=g, device="cuda", dtype=torch.int32),
                     scales=(gain * (0.5 + torch.rand((N, G), generator=g, device="cuda")) / (e2 * K) ** 0.5).to(torch.bfloat16),
                     zeros=torch.randint(0, 1 << b, (N, G), generator=g, device="cuda", dtype=torch.uint8),
@@ -261,14 +276,19 @@ def build_c2(ctx, ranks, rank_id, c=C2):
     torch.cuda.synchronize()
 
 
-def run_c2_ours(args, rank, world, device, B):
+def run_c2_ours(args, rank, world, device, B, c=C2, tp=False):
     import torch
     import paper_2605_05819_b200 as hc
-    c = C2
     ranks = c2_ranks(c)
+    if getattr(args, "rank_override", None) is not None:
+        ranks = {k: args.rank_override for k in ranks}
     ctx = hc.Context(device)
-    build_c2(ctx, ranks, rank, c)
-    x = torch.randn((B, c["hidden"]), device="cuda").to(torch.bfloat16)
+    G = world if tp else 1
+    if tp:
+        ctx.init_comm(rank, world)
+    build_c2(ctx, ranks, c, shard=(rank, world) if tp else None)
+    gx = torch.Generator(device="cuda").manual_seed(7 + (0 if tp else rank))
+    x = torch.randn((B, c["hidden"]), generator=gx, device="cuda").to(torch.bfloat16)
     y = torch.empty((B, c["hidden"]), dtype=torch.bfloat16, device="cuda")
     st = torch.cuda.Stream()
     for _ in range(max(args.warmup, 3)):
@@ -293,15 +313,18 @@ def run_c2_ours(args, rank, world, device, B):
     yh = torch.empty((B, c["hidden"]), dtype=torch.bfloat16).pin_memory()
     ctx.stack_forward(xh, yh, stream=st)
     n_e2e = max(3, min(args.steps, 50))
+    if world > 1:
+        torch.distributed.barrier()
     t0 = time.perf_counter()
     for _ in range(n_e2e):
         ctx.stack_forward(xh, yh, stream=st)      # synchronises (host result)
     e2e_s = time.perf_counter() - t0
     ctx.close()
     mean_rank = sum(ranks.values()) / len(ranks)
+    launches = args.steps * 4 * c["layers"] * (2 if tp else 1)   # decode kernel (+ unshard permute under TP)
     return dict(ms=ms, steps=args.steps, clocks=clk.summary, e2e_s=e2e_s, n_e2e=n_e2e, finite=finite,
-                launches=args.steps * 4 * c["layers"], h2d=B * c["hidden"] * 2, d2h=B * c["hidden"] * 2,
-                bytes=c2_bytes(ranks, B, c), mean_rank=mean_rank, ranks=ranks)
+                launches=launches, h2d=B * c["hidden"] * 2, d2h=B * c["hidden"] * 2,
+                bytes=c2_bytes(ranks, B, c, G), mean_rank=mean_rank, ranks=ranks)
 
 
 def oracle_c2_sample(seconds: float = 15.0, c=C2):
@@ -341,10 +364,14 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c5"])
+    ap.add_argument("--mode", default="auto", choices=["auto", "tp", "replicas"],
+                    help="N>1: tp = column-sharded stack with NCCL all-gather (strong scaling, default); "
+                         "replicas = independent full-model replicas (weak scaling)")
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--sweep", action="store_true", help="c2: also time B = 2, 4, 8, 16")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--rank-override", type=int, default=None, help="dev: use this rank for every matrix")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -352,16 +379,22 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
     hbm, tflops, peak_src = peaks()
+    tp = world > 1 and args.mode in ("auto", "tp")
     if args.workload == "c1":
         config = {"workload": "c1: single 4096x4096 linear, 4-bit g128, rank-64 compensation, batch-1 decode",
                   "N": 4096, "K": 4096, "bits": 4, "group": 128, "rank": 64, "batch": 1,
                   "l2": "defeated: 128 distinct weight copies (1.25 GB) rotated per step"}
     else:
-        config = {"workload": "c2: Llama-2-7B-shaped 32-layer decode stack, 4-bit g128 + dynamic ranks "
-                              "(hc_allocate_ranks, r_std = 10%-bytes rule), 1 GPU",
-                  "layers": 32, "hidden": 4096, "kv": 4096, "ffn": 11008, "bits": 4, "group": 128,
-                  "r_stored": C2["r_stored"], "batch": args.batch,
-                  "l2": "inputs larger than L2 (3.5 GB of weights streamed per step)",
+        c = STACKS[args.workload]
+        desc = ("c2: Llama-2-7B-shaped 32-layer decode stack, 4-bit g128 + dynamic ranks (hc_allocate_ranks, "
+                "r_std = 10%-bytes rule)" if args.workload == "c2" else
+                "c5: Llama-3-70B-shaped 80-layer decode stack, 2-bit g128 + rank-64 compensation")
+        config = {"workload": desc + (f", column-sharded over {world} GPUs (NCCL all-gather per window)" if tp else
+                                      (f", {world} independent replicas" if world > 1 else ", 1 GPU")),
+                  "layers": c["layers"], "hidden": c["hidden"], "kv": c["kv"], "ffn": c["ffn"], "bits": c["bits"],
+                  "group": 128, "r_stored": c["r_stored"], "batch": args.batch,
+                  "parallelism": f"tp{world}" if tp else f"dp{world}",
+                  "l2": "inputs larger than L2 (all weights streamed per step)",
                   "attention": "identity stand-in on the q-part (out of scope, DESIGN.md R9)"}
 
     if args.impl == "reference":
@@ -395,7 +428,7 @@ def main():
         nbytes = c1_bytes()
         unit, kernel = "GB/s", "hc::decode_kernel<4,1,true>"
     else:
-        r = run_c2_ours(args, rank, world, local, args.batch)
+        r = run_c2_ours(args, rank, world, local, args.batch, STACKS[args.workload], tp)
         nbytes = r["bytes"]
         unit, kernel = "tokens/s", "hc::decode_kernel (4 fused windows per layer)"
     per_rank = torch.tensor([r["ms"]], dtype=torch.float64, device="cuda")
@@ -408,8 +441,9 @@ def main():
         e2e = {"value": round(nbytes * r["n_e2e"] / r["e2e_s"] / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]}
     else:
-        value = world * args.batch * r["steps"] / (ms_max * 1e-3)
-        e2e = {"value": round(args.batch * r["n_e2e"] / r["e2e_s"], 2), "unit": "tokens/s",
+        streams = 1 if tp else world           # column sharding serves one stream; replicas serve `world`
+        value = streams * args.batch * r["steps"] / (ms_max * 1e-3)
+        e2e = {"value": round(streams * args.batch * r["n_e2e"] / r["e2e_s"], 2), "unit": "tokens/s",
                "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]}
         config["mean_rank"] = round(r["mean_rank"], 2)
         config["bytes_per_step"] = nbytes
@@ -417,16 +451,16 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 2), "unit": unit, "n_gpus": world, "steps": r["steps"],
                 "warmup": args.warmup, "ms_per_step": round(ms_max / r["steps"], 6), "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "bf16 x int4 (exact int dequant, fp32 accumulate)",
+                "scaling": "strong" if tp else "weak", "vs_baseline": None, "dtype": "bf16 x int4 (exact int dequant, fp32 accumulate)",
                 "data": "synthetic (seeded on device, random weights of the named shapes)", "config": config,
                 "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
                              "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": peak_src,
                              "kernel": kernel, "bytes_per_step": nbytes},
                 "clocks": r["clocks"], "gpu_launches": r["launches"], "e2e": e2e}
-        if args.workload == "c2" and args.sweep:
+        if args.workload != "c1" and args.sweep:
             sweep = {}
             for Bs in (2, 4, 8, 16):
-                rs = run_c2_ours(args, rank, world, local, Bs)
+                rs = run_c2_ours(args, rank, world, local, Bs, STACKS[args.workload], tp)
                 sweep[str(Bs)] = {"tokens_per_s": round(Bs * rs["steps"] / (rs["ms"] * 1e-3), 1),
                                   "ms_per_step": round(rs["ms"] / rs["steps"], 4),
                                   "GBps": round(rs["bytes"] / (rs["ms"] / rs["steps"] * 1e-3) / 1e9, 1)}
@@ -436,7 +470,7 @@ def main():
                 n, el = oracle_c1_sample(12.0)
                 line["cpu_baseline"] = {"value": round(nbytes * n / el / 1e9, 4), "unit": "GB/s", "cores": cores(),
                                         "kind": "oracle", "sample": f"{n} whole C1 calls, numpy float64"}
-            else:
+            elif args.workload == "c2":
                 tps, n, el = oracle_c2_sample(15.0)
                 line["cpu_baseline"] = {"value": round(tps, 6), "unit": "tokens/s", "cores": cores(), "kind": "oracle",
                                         "sample": f"{n} whole Llama-2-7B layers at B=1 (float64), extrapolated x32"}

@@ -50,7 +50,7 @@ struct Window {
   int layer = 0, kind = 0, expert = -1;
   int glue = HC_GLUE_NONE;            // SILU_MUL: members[0] = up (interleaved records), [1] = gate
   std::vector<Member> members;        // sorted by slot
-  DevBuf vpart, cnt;                  // launch workspace (self-resetting counters)
+  DevBuf tacc, cnt;                   // launch workspace: fixed-point t, counters (self-resetting)
   int ws_chunks = -1;
   int64_t out_rows() const {
     if (glue == HC_GLUE_SILU_MUL) return members.front().rows();
@@ -428,25 +428,23 @@ static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int
     a.n_rb = rb;
     a.n_chunks = chunks;
   }
-  a.vks = std::max(1, std::min(4, a.G / 8));   // ~8 groups (32 KB of V) per rank-projection item
   if (a.n_chunks > kMaxChunks) return fail(HC_ERR_CONFIG, "window ranks need %d chunks > %d", a.n_chunks, kMaxChunks);
   if (w.ws_chunks < max_chunks) {
     const int mc = std::max(max_chunks, 1);
-    CUDA_TRY(w.vpart.alloc((size_t)mc * kMaxVks * 256 * sizeof(float)));
+    CUDA_TRY(w.tacc.alloc((size_t)mc * 256 * sizeof(long long)));
+    CUDA_TRY(cudaMemset(w.tacc.p, 0, w.tacc.bytes));
     CUDA_TRY(w.cnt.alloc(2 * sizeof(unsigned)));
     CUDA_TRY(cudaMemset(w.cnt.p, 0, w.cnt.bytes));
     w.ws_chunks = max_chunks;
   }
-  static const int dbg = [] { const char* e = getenv("HC_DECODE_DEBUG"); return e ? atoi(e) : 0; }();
-  a.dbg = dbg;
-  a.vpart = (float*)w.vpart.p;
+  a.tacc = (long long*)w.tacc.p;
   a.cnt = (unsigned*)w.cnt.p;
-  const auto key = std::make_tuple(m0.bits, B, a.K, a.n_chunks, a.vks);
+  const auto key = std::make_tuple(m0.bits, B, a.K, a.n_chunks, 0);
   auto it = ctx->max_ctas.find(key);
   if (it == ctx->max_ctas.end())
-    it = ctx->max_ctas.emplace(key, decode_max_ctas(m0.bits, B, a.K, a.n_chunks, a.vks)).first;
+    it = ctx->max_ctas.emplace(key, decode_max_ctas(m0.bits, B, a.K, a.n_chunks)).first;
   if (it->second <= 0) return fail(HC_ERR_RUNTIME, "decode kernel cannot be resident on this device");
-  const int n_items = a.n_chunks * a.vks + a.n_rb;
+  const int n_items = a.n_rb;
   static const int per_sm = [] { const char* e = getenv("HC_DECODE_CTAS_PER_SM"); return e ? atoi(e) : 0; }();
   const int cap = per_sm > 0 ? std::min(it->second, per_sm * ctx->sms) : it->second;
   grid = std::max(1, std::min(n_items, cap));

@@ -4,10 +4,9 @@
 //     t[b, j] = Σ_k V[j,k] · x[b,k]                                      (north_star)
 //
 // Design (DESIGN.md §"Decode kernel"):
-//  * one CTA work item is either a rank-projection item (16 ranks of V × a 4-group K-slice) or a
-//    row-block item (16 output rows × all of K); rank-projection items come first so that t is
-//    ready long before the row-block epilogues need it; the grid is one resident wave
-//    (persistent loop beyond that);
+//  * one CTA work item is a row block (16 output rows × all of K), striped over a grid of one
+//    resident wave (persistent loop beyond that); the rank projection is spread over every tile warp
+//    of the grid as a small prologue;
 //  * each warp streams its tiles — a (row-block, group) record or a 1 KB V piece — from HBM with
 //    cp.async.bulk (TMA engine, L2 evict-first) into a private 4-slot shared-memory ring guarded
 //    by mbarriers; W is never materialised;
@@ -22,9 +21,9 @@
 //  * the 8 warps' partial sums are reduced in shared memory in a fixed order; the CTA's epilogue
 //    warp adds U[:, :r]·t with t split into bf16 hi + lo (fp32-accurate) on the same mma and
 //    writes y once (fp32, or bf16 = RNE of the fp32 value), optionally adding a bf16 residual;
-//  * t is produced inside the launch: rank-projection items publish per-slice partials and bump a
-//    release counter; each row-block epilogue acquires it and sums the slices of its member's
-//    chunks in slice order (deterministic).  The counters self-reset before the kernel exits.
+//  * t is produced inside the launch with 64-bit fixed-point atomics (2^-28 resolution; integer adds
+//    are associative, so t is deterministic); epilogues acquire a release counter.  The accumulators
+//    and counters self-reset before the kernel exits.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -158,35 +157,34 @@ __device__ __forceinline__ int member_of_chunk(const DArgs& a, int cc) {
   return m;
 }
 
+// The tiles of one row-block item a tile warp streams: contiguous group range [g0, g0 + n).
 template <int BITS>
-__device__ __forceinline__ Share warp_share(const DArgs& a, int item, int warp) {
+__device__ __forceinline__ Share warp_share(const DArgs& a, int rb, int warp) {
   Share s;
-  const int nV = a.n_chunks * a.vks;
-  if (item < nV) {   // V pieces of (chunk, slice), split evenly over the warps at piece granularity
-    const int cc = item / a.vks, vs = item - cc * a.vks;
-    s.member = member_of_chunk(a, cc);
-    const DMember& m = a.m[s.member];
-    const int lo = vs * a.G / a.vks, hi = (vs + 1) * a.G / a.vks;
-    const int np = 4 * (hi - lo);
-    const int p0 = warp * np / kDecodeWarps, p1 = (warp + 1) * np / kDecodeWarps;
-    s.n = p1 - p0;
-    s.g0 = 4 * lo + p0;   // absolute piece index inside the chunk (4 pieces of 1 KB per group)
-    s.base = reinterpret_cast<const uint8_t*>(m.V + (size_t)(cc - m.chunk_begin) * a.G * 256) + (size_t)s.g0 * 1024;
-    s.tb = 1024;
-    s.is_v = 1;
-  } else {           // all of K of one row block, contiguous group ranges per warp
-    const int rb = item - nV;
-    s.member = member_of_rb(a, rb);
-    const DMember& m = a.m[s.member];
-    const int g0 = warp * a.G / kDecodeWarps, g1 = (warp + 1) * a.G / kDecodeWarps;
-    s.n = g1 - g0;
-    s.g0 = g0;
-    s.base = m.rec + ((size_t)(rb - m.rb_begin) * a.G + g0) * rec_bytes(BITS);
-    s.tb = rec_bytes(BITS);
-    s.is_v = 0;
-  }
+  s.member = member_of_rb(a, rb);
+  const DMember& m = a.m[s.member];
+  const int g0 = warp * a.G / kDecodeWarps, g1 = (warp + 1) * a.G / kDecodeWarps;
+  s.n = g1 - g0;
+  s.g0 = g0;
+  s.base = m.rec + ((size_t)(rb - m.rb_begin) * a.G + g0) * rec_bytes(BITS);
+  s.tb = rec_bytes(BITS);
+  s.is_v = 0;
   return s;
 }
+
+// V piece vp of the window (chunk-major, then group, then part p of 2 k16 steps): 1 KB of fragments
+__device__ __forceinline__ const uint8_t* v_piece(const DArgs& a, int vp, int& g, int& part) {
+  const int per_chunk = 4 * a.G;
+  const int cc = vp / per_chunk, rem = vp - cc * per_chunk;
+  g = rem >> 2;
+  part = rem & 3;
+  const DMember& m = a.m[member_of_chunk(a, cc)];
+  return reinterpret_cast<const uint8_t*>(m.V + ((size_t)(cc - m.chunk_begin) * a.G * 256 + (size_t)rem * 64));
+}
+
+constexpr int kVPerWarp = 2;                    // V·x pieces per tile warp of the V CTAs
+constexpr float kTScale = 268435456.f;          // 2^28: fixed-point scale of the t accumulators
+constexpr float kTInv = 1.f / 268435456.f;
 
 // Row of x used by mma column `col` (batch index).  Columns >= B read a valid row; their
 // outputs are never stored, so no zeroing is needed.
@@ -211,7 +209,7 @@ __device__ __forceinline__ void load_x_global(const DArgs& a, int g, int lane, u
 // XS: x fragments come from shared memory (xrow_s[nb] = this lane's run start for the group).
 template <int BITS, int NB8, bool XS>
 __device__ __forceinline__ void w_tile(const uint8_t* rec, int lane, const uint4* const (&xrow_s)[NB8],
-                                       const uint32_t (&xr)[NB8][16], float (&tot)[NB8][4]) {
+                                       const uint32_t (&xr)[NB8][16], const float* xsum_g, float (&tot)[NB8][4]) {
   uint32_t w[2 * BITS];
 #pragma unroll
   for (int q = 0; q < (2 * BITS) / 4; ++q) {
@@ -229,10 +227,12 @@ __device__ __forceinline__ void w_tile(const uint8_t* rec, int lane, const uint4
   const uint32_t zr[2] = {(z0 >> (4 * gid)) & 15u, (z1 >> (4 * gid)) & 15u};
   constexpr int kFpHi = BITS == 2 ? 2 : (BITS == 3 ? 3 : 0);   // the non-zero field weight exponent
   uint32_t zc[2][2];                                            // [row parity][fp == 0 ? 0 : 1]
+  if constexpr (!XS) {
 #pragma unroll
-  for (int rp = 0; rp < 2; ++rp) {
-    zc[rp][0] = (0x4300u + zr[rp]) * 0x00010001u;               // bf16x2(128 + z), exact
-    zc[rp][1] = (0x4300u + (zr[rp] << kFpHi)) * 0x00010001u;    // bf16x2(128 + z·2^fp), exact
+    for (int rp = 0; rp < 2; ++rp) {
+      zc[rp][0] = (0x4300u + zr[rp]) * 0x00010001u;               // bf16x2(128 + z), exact
+      zc[rp][1] = (0x4300u + (zr[rp] << kFpHi)) * 0x00010001u;    // bf16x2(128 + z·2^fp), exact
+    }
   }
   float acc[2][NB8][4];
 #pragma unroll
@@ -260,7 +260,8 @@ __device__ __forceinline__ void w_tile(const uint8_t* rec, int lane, const uint4
       uint32_t af[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        af[i] = bf2_sub(extract<BITS>(w, j, i), zc[i & 1][slot(BITS, j, i).fp ? 1 : 0]);   // 2^fp·(q − z), exact
+        af[i] = extract<BITS>(w, j, i);                                  // 128 + 2^fp·q (exact)
+        if constexpr (!XS) af[i] = bf2_sub(af[i], zc[i & 1][slot(BITS, j, i).fp ? 1 : 0]);   // 2^fp·(q − z)
       }
       const int fp0 = step_fp(BITS, j, 0), fp1 = step_fp(BITS, j, 1);
 #pragma unroll
@@ -273,6 +274,20 @@ __device__ __forceinline__ void w_tile(const uint8_t* rec, int lane, const uint4
     }
   }
   const float s0 = bf16_bits_to_f32(sw & 0xFFFFu), s1 = bf16_bits_to_f32(sw >> 16);
+  if constexpr (XS) {
+    // Σ_k (128 + 2^fp q)·x'_k − (128·Σ_k x'_k + z·Σ_k x_k) = Σ_k (q − z)·x_k   (x' = 2^-fp x);
+    // xsum_g[col] = (Σx, Σx') of this group, computed once per CTA from the staged x
+    const float zf0 = (float)zr[0], zf1 = (float)zr[1];
+#pragma unroll
+    for (int nb = 0; nb < NB8; ++nb) {
+      const float4 xs2 = *reinterpret_cast<const float4*>(xsum_g + 2 * (2 * (lane & 3) + 8 * nb));
+      const float c0 = 128.f * xs2.y, c1 = 128.f * xs2.w;
+      acc[0][nb][0] -= fmaf(zf0, xs2.x, c0);
+      acc[0][nb][1] -= fmaf(zf0, xs2.z, c1);
+      acc[0][nb][2] -= fmaf(zf1, xs2.x, c0);
+      acc[0][nb][3] -= fmaf(zf1, xs2.z, c1);
+    }
+  }
 #pragma unroll
   for (int nb = 0; nb < NB8; ++nb) {
     tot[nb][0] = fmaf(s0, acc[0][nb][0] + acc[1][nb][0], tot[nb][0]);
@@ -300,11 +315,16 @@ __device__ __forceinline__ void v_tile(const uint8_t* piece, int lane, const uin
 }  // namespace
 
 // Warp roles: warps 0..7 stream and contract tiles; warp 8 is the epilogue warp (reduction of the
-// 8 partial sums, rank-projection publication, U·t, output).  Named barriers hand the shared
-// reduction buffer red[p] (p = item parity) between them:
+// 8 partial sums, U·t, output).  Named barriers hand the shared reduction buffer red[p] (p = item
+// parity) between them:
 //   FULL[p]  (id 1+p): 256 tile threads arrive, the epilogue warp syncs
 //   EMPTY[p] (id 3+p): the epilogue warp arrives after reading red[p], the tile warps sync before
 //                      writing red[p] again two items later.
+// Rank projection t = V·x: every tile warp of the grid first contracts an equal share of the
+// window's 1 KB V pieces (requested before its weight tiles) and adds its partial into the
+// window's t accumulators with 64-bit fixed-point atomics (exact integer adds: t is bit-identical
+// for any arrival order), then bumps v_done; each CTA's epilogue warp acquires v_done once and reads
+// t while its tile warps are still streaming.
 template <int BITS, int NB8, bool XS>
 __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_constant__ DArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -317,18 +337,17 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_
   uint64_t* bars_all = reinterpret_cast<uint64_t*>(ubuf + 2 * kUPre * 32);
   uint64_t* ubar = bars_all + kDecodeWarps * kNBuf;       // [2]
   uint64_t* xbar = ubar + 2;
-  uint64_t* pbar = xbar + 1;
-  float4* tsm = reinterpret_cast<float4*>(xbar + 2);      // [n_chunks][NB8][32] t fragments (hi/lo source)
-  float* pstage = reinterpret_cast<float*>(tsm + (size_t)a.n_chunks * NB8 * 32);   // [nV][NB8][128]
-  uint16_t* xs = reinterpret_cast<uint16_t*>(pstage + (size_t)a.n_chunks * a.vks * NB8 * 128);
+  float4* tsm = reinterpret_cast<float4*>(xbar + 2);      // [n_chunks][NB8][32] t fragments
+  uint16_t* xs = reinterpret_cast<uint16_t*>(tsm + (size_t)a.n_chunks * NB8 * 32);
   const int xs_ld = a.K + 32;   // +64 B per row: consecutive batch rows fall in disjoint banks
+  float* xsum = reinterpret_cast<float*>(xs + (size_t)a.B * xs_ld);   // [G][16 cols][Σx, Σx'] (XS only)
 
   if (lane == 0) {
     if (warp < kDecodeWarps) {
 #pragma unroll
       for (int s = 0; s < kNBuf; ++s) mbar_init(&bars_all[warp * kNBuf + s], 1);
     } else {
-      mbar_init(&ubar[0], 1); mbar_init(&ubar[1], 1); mbar_init(xbar, 1); mbar_init(pbar, 1);
+      mbar_init(&ubar[0], 1); mbar_init(&ubar[1], 1); mbar_init(xbar, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -336,21 +355,24 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_
   __syncthreads();
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
-  const int nV = a.n_chunks * a.vks;
-  const int n_items = nV + a.n_rb;
+  const int n_items = a.n_rb;
+  // the V·x share lives on the first CTAs (started first), ~kVPerWarp 1 KB pieces per tile warp
+  const int n_vp = a.n_chunks * 4 * a.G;
+  const int n_vctas = n_vp == 0 ? 0 : min((int)gridDim.x, (n_vp + kDecodeWarps * kVPerWarp - 1) / (kDecodeWarps * kVPerWarp));
+  const int n_vwarps = n_vctas * kDecodeWarps;            // v_done target
 
   if (warp == kEpi) {
     // ======================= epilogue warp =======================
-    auto prefetch_u = [&](int item, int par) {   // U fragments of a row-block item -> ubuf[par]
-      if (item < nV || item >= n_items) return;
-      const DMember& m = a.m[member_of_rb(a, item - nV)];
+    auto prefetch_u = [&](int rb, int par) {   // U fragments of a row-block item -> ubuf[par]
+      if (rb >= n_items) return;
+      const DMember& m = a.m[member_of_rb(a, rb)];
       const int r_eff = a.glue ? max(a.m[0].r, a.m[1].r) : m.r;
       const int nck = min((r_eff + 15) >> 4, kUPre);
       if (nck == 0) return;
       if (lane == 0) {
         const uint32_t bytes = (uint32_t)nck * 512u;
         mbar_expect_tx(&ubar[par], bytes);
-        bulk_copy(ubuf + par * kUPre * 32, m.U + (size_t)(item - nV - m.rb_begin) * (m.r_stored >> 4) * 32, bytes,
+        bulk_copy(ubuf + par * kUPre * 32, m.U + (size_t)(rb - m.rb_begin) * (m.r_stored >> 4) * 32, bytes,
                   &ubar[par], evict_first_policy());
       }
     };
@@ -369,31 +391,23 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_
     int k = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++k) {
       const int par = k & 1;
-      if (!t_ready && item >= nV && (a.m[member_of_rb(a, item - nV)].r > 0 || (a.glue && a.m[1].r > 0))) {
-        // once per CTA, while the tile warps still stream this item: acquire the rank-projection
-        // partials, bring all of them into smem with one round of bulk copies, and sum them per
-        // chunk in slice order (deterministic t) into t fragments
+      const DMember& m = a.m[member_of_rb(a, item)];
+      const int r_eff = a.glue ? max(a.m[0].r, a.m[1].r) : m.r;
+      if (!t_ready && r_eff > 0) {
+        // once per CTA, while the tile warps still stream: acquire t (all tile warps of the grid
+        // have added their V·x shares) and keep its fragments in smem as fp32
         if (lane == 0)
-          while (ld_relaxed(&a.cnt[0]) < (unsigned)nV) __nanosleep(20);
+          while (ld_relaxed(&a.cnt[0]) < (unsigned)n_vwarps) __nanosleep(32);
         __syncwarp();
         __threadfence();
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        constexpr uint32_t kPB = NB8 * 512;               // bytes of one partial this CTA needs
-        if (lane == 0) mbar_expect_tx(pbar, (uint32_t)nV * kPB);
-        __syncwarp();
-        for (int i = lane; i < nV; i += 32)
-          bulk_copy(pstage + (size_t)i * (kPB / 4), a.vpart + (size_t)i * 256, kPB, pbar, evict_last_policy());
-        while (!mbar_try_wait(pbar, 0)) {}
+#pragma unroll 4
         for (int cc = 0; cc < a.n_chunks; ++cc) {
 #pragma unroll
           for (int nb = 0; nb < NB8; ++nb) {
-            float4 ts = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int vs = 0; vs < a.vks; ++vs) {
-              const float4 v = *reinterpret_cast<const float4*>(
-                  pstage + ((size_t)(cc * a.vks + vs) * NB8 + nb) * 128 + gid * 16 + tig * 4);
-              ts.x += v.x; ts.y += v.y; ts.z += v.z; ts.w += v.w;
-            }
-            tsm[((size_t)cc * NB8 + nb) * 32 + lane] = ts;
+            const long long* src = a.tacc + ((size_t)cc * 16 + ((gid + 8 * nb) & 15)) * 16 + 2 * tig;
+            const long long t0 = __ldcg(src), t1 = __ldcg(src + 1), t8 = __ldcg(src + 8), t9 = __ldcg(src + 9);
+            tsm[((size_t)cc * NB8 + nb) * 32 + lane] =
+                make_float4((float)t0 * kTInv, (float)t1 * kTInv, (float)t8 * kTInv, (float)t9 * kTInv);
           }
         }
         __syncwarp();
@@ -418,25 +432,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_
         asm volatile("bar.arrive %0, %1;" ::"r"(3 + par), "n"(kDecodeThreads) : "memory");   // EMPTY[par]
       prefetch_u(item + gridDim.x, par ^ 1);
 
-      if (item < nV) {
-        // ---- rank-projection partial in "t layout" [b][tig][4]; publish with a release counter
-        float* vp = a.vpart + (size_t)item * 256;
-#pragma unroll
-        for (int nb = 0; nb < NB8; ++nb)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int rank = gid + 8 * (e >> 1), bl = 2 * tig + (e & 1);   // batch column nb*8 + bl
-            __stcg(vp + nb * 128 + bl * 16 + ((rank & 7) >> 1) * 4 + (rank >> 3) * 2 + (rank & 1), fin[nb][e]);
-          }
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) atomicAdd(&a.cnt[0], 1u);
-        continue;
-      }
       // ---- row-block epilogue: + U[:, :r]·t, residual, output
-      const int rb = item - nV;
-      const DMember& m = a.m[member_of_rb(a, rb)];
-      const int rbl = rb - m.rb_begin;
+      const int rbl = item - m.rb_begin;
       // U·t: plain windows use the member's own chunks for all 16 rows; a fused SiLU window runs
       // the up chunks (rows 0-7 = up rows) and the gate chunks (rows 8-15 = gate rows) separately
       float comp[2][NB8][4];
@@ -446,7 +443,6 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_
         for (int nb = 0; nb < NB8; ++nb)
 #pragma unroll
           for (int e = 0; e < 4; ++e) comp[h][nb][e] = 0.f;
-      const int r_eff = a.glue ? max(a.m[0].r, a.m[1].r) : m.r;
       if (r_eff > 0) {
         const int nck = (r_eff + 15) >> 4;
         while (!mbar_try_wait(&ubar[par], (u_phase >> par) & 1u)) {}
@@ -515,16 +511,19 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_
       }
       ++my_rb;
     }
-    // one counter update per CTA: the CTA that completes the last row block resets the counters
-    // (every v_done reader has finished by then: they are row-block epilogues)
+    // one counter update per CTA: the CTA completing the last row block resets t and the counters
+    // (every t reader is a row-block epilogue, all of which have finished by then)
     __syncwarp();
+    unsigned last = 0;
     if (lane == 0 && my_rb > 0) {
       __threadfence();
       const unsigned old = atomicAdd(&a.cnt[1], (unsigned)my_rb);
-      if (old + (unsigned)my_rb == (unsigned)a.n_rb) {
-        a.cnt[0] = 0u;
-        a.cnt[1] = 0u;
-      }
+      last = (old + (unsigned)my_rb == (unsigned)a.n_rb);
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      for (int i = lane; i < a.n_chunks * 256; i += 32) a.tacc[i] = 0;
+      if (lane == 0) { a.cnt[0] = 0u; a.cnt[1] = 0u; }
     }
     return;
   }
@@ -533,13 +532,30 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_
   uint8_t* bufs = smem + (size_t)warp * kNBuf * kBlk;    // [kNBuf][kBlk]
   uint64_t* bars = bars_all + warp * kNBuf;
   const uint64_t pol_w = evict_first_policy();
-  // producer: blocks of up to kTPB consecutive tiles of a share, one bulk copy each,
-  // double-buffered per warp.  State is warp-uniform; lane 0 issues.
+  // this warp's share of the window's V pieces (rank projection)
+  const int gw = blockIdx.x * kDecodeWarps + warp;
+  const bool v_warp = gw < n_vwarps;
+  const int vp0 = v_warp ? (int)((long long)gw * n_vp / n_vwarps) : 0;
+  const int vp1 = v_warp ? (int)((long long)(gw + 1) * n_vp / n_vwarps) : 0;
+  // producer: first the V pieces (one per slot), then blocks of up to kTPB consecutive tiles of each
+  // row-block share; double-buffered per warp.  State is warp-uniform; lane 0 issues.
+  int vp_issue = vp0;
   int p_item = blockIdx.x, p_t = 0;
   Share p_sh = p_item < n_items ? warp_share<BITS>(a, p_item, warp) : Share{nullptr, 0, 1024, 0, 0, 0};
   unsigned blk_issued = 0;
-  auto issue_block = [&]() {   // issue the next non-empty block, if any
-    if (a.dbg == 2 && blk_issued >= kNBuf) return;   // dev knob: compute on stale tiles, no streaming
+  auto issue_block = [&]() {   // issue the next block (a V piece or up to kTPB weight tiles), if any
+    const int s = blk_issued % kNBuf;
+    if (vp_issue < vp1) {
+      int g, part;
+      const uint8_t* src = v_piece(a, vp_issue, g, part);
+      if (lane == 0) {
+        mbar_expect_tx(&bars[s], 1024u);
+        bulk_copy(bufs + s * kBlk, src, 1024u, &bars[s], pol_w);
+      }
+      ++vp_issue;
+      ++blk_issued;
+      return;
+    }
     while (p_item < n_items && p_t >= p_sh.n) {
       p_item += gridDim.x;
       p_t = 0;
@@ -547,7 +563,6 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_
     }
     if (p_item >= n_items) return;
     const int nt = min(kTPB, p_sh.n - p_t);
-    const int s = blk_issued % kNBuf;
     if (lane == 0) {
       const uint32_t bytes = (uint32_t)(nt * p_sh.tb);
       mbar_expect_tx(&bars[s], bytes);
@@ -557,16 +572,89 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_
     ++blk_issued;
   };
 #pragma unroll
-  for (int s = 0; s < kNBuf; ++s) issue_block();   // weights: before the PDL wait
+  for (int s = 0; s < kNBuf; ++s) issue_block();   // weights / V: before the PDL wait
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if constexpr (XS) {
     while (!mbar_try_wait(xbar, 0)) {}
+    // per-(group, batch column) sums of x and of the pre-scaled x' (x·2^-fp at the positions whose
+    // code field carries weight 2^fp): the exact zero-point / magic-offset correction of w_tile.
+    // 8 threads per (group, column), 16 elements each, fixed-order shuffle reduction.
+    const int tid = threadIdx.x;   // 0..255 (tile warps)
+    const int n_sum = a.G * a.B * 8, n_sum_w = (n_sum + 31) & ~31;   // warp-uniform trip count
+    for (int i = tid; i < n_sum_w; i += kDecodeWarps * 32) {
+      const bool live = i < n_sum;
+      const int part = i & 7, gb = live ? i >> 3 : 0, b = gb % a.B, g = gb / a.B;
+      const uint4* src = reinterpret_cast<const uint4*>(xs + (size_t)b * xs_ld + g * kGroup + part * 16);
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint4 v = src[h];
+        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int k = part * 16 + h * 8 + e;                       // k within the group
+          const int j = 2 * (k >> 5) + ((k >> 2) & 1), pr = (k >> 1) & 1;
+          const float xv = bf16_bits_to_f32((wv[e >> 1] >> (16 * (e & 1))) & 0xFFFFu);
+          s0 += xv;
+          s1 += xv * __uint_as_float((uint32_t)(127 - step_fp(BITS, j, pr)) << 23);
+        }
+      }
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      }
+      if (live && part == 0) { xsum[(size_t)g * 32 + 2 * b] = s0; xsum[(size_t)g * 32 + 2 * b + 1] = s1; }
+    }
+    for (int i = tid; i < a.G * 16; i += kDecodeWarps * 32)   // padding columns: finite, unused
+      if ((i & 15) >= a.B) { xsum[(size_t)(i >> 4) * 32 + 2 * (i & 15)] = 0.f; xsum[(size_t)(i >> 4) * 32 + 2 * (i & 15) + 1] = 0.f; }
+    asm volatile("bar.sync 5, %0;" ::"n"(kDecodeWarps * 32) : "memory");   // tile warps only
   }
   const uint16_t* xs_row[NB8];
 #pragma unroll
   for (int nb = 0; nb < NB8; ++nb) xs_row[nb] = xs + (size_t)xrow(a, gid + 8 * nb) * xs_ld + 8 * tig;
 
   unsigned blk_done = 0;
+  // ---- rank projection share: t[cc][col][rank] += V piece · x   (64-bit fixed point, exact adds)
+  for (int vp = vp0; vp < vp1; ++vp) {
+    const int s = blk_done % kNBuf;
+    const uint32_t ph = (blk_done / kNBuf) & 1u;
+    int g, part;
+    v_piece(a, vp, g, part);
+    const int cc = vp / (4 * a.G);
+    uint4 xv[NB8];
+#pragma unroll
+    for (int nb = 0; nb < NB8; ++nb) {
+      const uint4* p = reinterpret_cast<const uint4*>(
+          (XS ? xs_row[nb] : a.x + (size_t)xrow(a, gid + 8 * nb) * a.ldx + 8 * tig) + g * kGroup + 32 * part);
+      xv[nb] = XS ? *p : __ldg(p);
+    }
+    while (!mbar_try_wait(&bars[s], ph)) {}
+    float tp[NB8][4];
+#pragma unroll
+    for (int nb = 0; nb < NB8; ++nb)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) tp[nb][e] = 0.f;
+    v_tile<NB8>(bufs + s * kBlk, lane, xv, tp);
+    __syncwarp();
+    ++blk_done;
+    issue_block();
+#pragma unroll
+    for (int nb = 0; nb < NB8; ++nb)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int col = 2 * tig + (e & 1) + 8 * nb, rank = gid + 8 * (e >> 1);
+        if (col < a.B)
+          atomicAdd(reinterpret_cast<unsigned long long*>(a.tacc + ((size_t)cc * 16 + col) * 16 + rank),
+                    (unsigned long long)__float2ll_rn(tp[nb][e] * kTScale));
+      }
+  }
+  if (v_warp) {
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) atomicAdd(&a.cnt[0], 1u);            // v_done (release via the fence above)
+  }
+
   int k = 0;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++k) {
     const int par = k & 1;
@@ -581,35 +669,15 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_
       const uint32_t ph = (blk_done / kNBuf) & 1u;
       const int nt = min(kTPB, sh.n - t0);
       const uint8_t* blk = bufs + s * kBlk;
-      if (sh.is_v) {
-        uint4 xv[kTPB][NB8];
+      while (!mbar_try_wait(&bars[s], ph)) {}
+      for (int t = 0; t < nt; ++t) {
+        const int g = sh.g0 + t0 + t;
+        uint32_t xr[NB8][16];
+        const uint4* xrs[NB8];
 #pragma unroll
-        for (int t = 0; t < kTPB; ++t) {
-          const int piece = sh.g0 + t0 + min(t, nt - 1);
-#pragma unroll
-          for (int nb = 0; nb < NB8; ++nb) {
-            const uint4* p = reinterpret_cast<const uint4*>(
-                (XS ? xs_row[nb] : a.x + (size_t)xrow(a, gid + 8 * nb) * a.ldx + 8 * tig) +
-                (piece >> 2) * kGroup + 32 * (piece & 3));
-            xv[t][nb] = XS ? *p : __ldg(p);
-          }
-        }
-        while (!mbar_try_wait(&bars[s], ph)) {}
-#pragma unroll
-        for (int t = 0; t < kTPB; ++t)
-          if (t < nt) v_tile<NB8>(blk + t * 1024, lane, xv[t], tot);
-      } else {
-        if (a.dbg != 2 || blk_done < kNBuf) { while (!mbar_try_wait(&bars[s], ph)) {} }
-        for (int t = 0; t < nt; ++t) {
-          const int g = sh.g0 + t0 + t;
-          uint32_t xr[NB8][16];
-          const uint4* xrs[NB8];
-#pragma unroll
-          for (int nb = 0; nb < NB8; ++nb) xrs[nb] = reinterpret_cast<const uint4*>(xs_row[nb] + g * kGroup);
-          if (a.dbg == 1) { tot[0][0] += (float)blk[t * rec_bytes(BITS) + lane]; continue; }
-          if constexpr (!XS) load_x_global<NB8>(a, g, lane, xr);
-          w_tile<BITS, NB8, XS>(blk + t * rec_bytes(BITS), lane, xrs, xr, tot);
-        }
+        for (int nb = 0; nb < NB8; ++nb) xrs[nb] = reinterpret_cast<const uint4*>(xs_row[nb] + g * kGroup);
+        if constexpr (!XS) load_x_global<NB8>(a, g, lane, xr);
+        w_tile<BITS, NB8, XS>(blk + t * rec_bytes(BITS), lane, xrs, xr, xsum + (size_t)g * 32, tot);
       }
       __syncwarp();
       ++blk_done;
@@ -625,12 +693,12 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_
   }
 }
 
-static size_t decode_smem_bytes(bool xs, int B, int K, int n_chunks, int vks) {
+static size_t decode_smem_bytes(bool xs, int B, int K, int n_chunks) {
   const int nb8 = B > 8 ? 2 : 1;
   size_t s = (size_t)kDecodeWarps * kNBuf * kTPB * kTileMax + 2 * kDecodeWarps * 32 * 8 * sizeof(float) +
              2 * kUPre * 32 * 16 + (kDecodeWarps * kNBuf + 4) * sizeof(uint64_t) +
-             (size_t)n_chunks * nb8 * 32 * 16 + (size_t)n_chunks * vks * nb8 * 512;
-  if (xs) s += (size_t)B * (K + 32) * 2;
+             (size_t)n_chunks * nb8 * 32 * 16;
+  if (xs) s += (size_t)B * (K + 32) * 2 + (size_t)(K / 128) * 32 * sizeof(float);
   return s;
 }
 
@@ -641,7 +709,7 @@ static bool use_xs(int B, int K) { return B <= 8 && (size_t)B * (K + 32) * 2 <= 
 
 template <int BITS, int NB8, bool XS>
 static cudaError_t launch_t(const DArgs& a, int grid, cudaStream_t st) {
-  const size_t smem = decode_smem_bytes(XS, a.B, a.K, a.n_chunks, a.vks);
+  const size_t smem = decode_smem_bytes(XS, a.B, a.K, a.n_chunks);
   if (smem > kSmemOptin) return cudaErrorInvalidConfiguration;
   static bool attr = false;
   if (!attr) {
@@ -664,8 +732,8 @@ static cudaError_t launch_t(const DArgs& a, int grid, cudaStream_t st) {
 }
 
 template <int BITS, int NB8, bool XS>
-static int max_ctas_t(int B, int K, int n_chunks, int vks) {
-  const size_t smem = decode_smem_bytes(XS, B, K, n_chunks, vks);
+static int max_ctas_t(int B, int K, int n_chunks) {
+  const size_t smem = decode_smem_bytes(XS, B, K, n_chunks);
   cudaFuncSetAttribute(decode_kernel<BITS, NB8, XS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)kSmemOptin);
   int per_sm = 0, dev = 0, sms = 0;
@@ -695,9 +763,9 @@ cudaError_t launch_decode(const DArgs& a, int bits, int grid, cudaStream_t st) {
   return cudaErrorInvalidValue;
 }
 
-int decode_max_ctas(int bits, int B, int K, int n_chunks, int vks) {
+int decode_max_ctas(int bits, int B, int K, int n_chunks) {
   const int a_B = B, a_K = K;
-  HC_DISPATCH(max_ctas_t, B, K, n_chunks, vks);
+  HC_DISPATCH(max_ctas_t, B, K, n_chunks);
   return 0;
 }
 

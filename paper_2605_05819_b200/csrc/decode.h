@@ -13,7 +13,6 @@ constexpr int kTPB = 2;                  // tiles per bulk-copy block
 constexpr int kNBuf = 4;                 // block buffers per warp (3 blocks in flight while one computes)
 constexpr int kTileMax = 1088;           // >= rec_bytes(4) = 1072, >= 1 KB V piece
 constexpr int kUPre = 4;                 // U chunks (16 ranks each) staged in smem per item
-constexpr int kMaxVks = 16;
 
 struct DMember {
   const uint8_t* rec;   // [n_rb][G][rec_bytes]          (layout.h)
@@ -41,15 +40,13 @@ struct DArgs {
                         //   m[1] = gate (V / rank only); row block = 8 up rows + 8 gate rows
   int n_rb;             // Σ members
   int n_chunks;         // Σ ceil(r_m / 16)
-  int vks;              // K-slices per V chunk (<= kMaxVks)
-  float* vpart;         // [n_chunks * vks][16 batch][4 tig][4]  rank-projection partials
-  unsigned* cnt;        // [0] v_done, [1] w_done (self-resetting)
-  int dbg;              // development knob (HC_DECODE_DEBUG): 1 = stream tiles without contracting them
+  long long* tacc;      // [n_chunks][16 batch][16 ranks] t = V·x in 2^-28 fixed point (self-resetting)
+  unsigned* cnt;        // [0] v_done (tile warps done with their V share), [1] w_done (row blocks)
 };
 
 // Launch the fused window kernel; bits in {2,3,4}; 1 <= B <= 16.
 cudaError_t launch_decode(const DArgs& a, int bits, int grid, cudaStream_t st);
 // Max co-resident CTAs of the decode kernel on this device (persistent grid size).
-int decode_max_ctas(int bits, int B, int K, int n_chunks, int vks);
+int decode_max_ctas(int bits, int B, int K, int n_chunks);
 
 }  // namespace hc
