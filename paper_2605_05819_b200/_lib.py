@@ -7,7 +7,7 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libhcinfer.so")
+LIB_PATH = os.environ.get("HC_LIB_PATH") or os.path.join(_PKG, "libhcinfer.so")   # override: dev variant builds
 
 HC_OK, HC_ERR_CONFIG, HC_ERR_STATE, HC_ERR_NUMERIC, HC_ERR_RUNTIME = 0, 2, 3, 4, 5
 QKV, O, UPGATE, DOWN = 0, 1, 2, 3

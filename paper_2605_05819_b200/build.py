@@ -37,35 +37,44 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, defines=(), lib_out: str = None) -> str:
+    """Compile libhcinfer.so (or, for development sweeps, a variant with extra -D defines into lib_out)."""
+    build_dir = BUILD if not defines else os.path.join(BUILD, "v_" + "_".join(d.replace("=", "") for d in defines))
+    lib_path = lib_out or LIB
+    os.makedirs(build_dir, exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(INC, "hcinfer.h"))
     objs = []
     log = []
     for src in CU_SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src + ".o")
+        o = os.path.join(build_dir, src + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
             log.append(_run([NVCC, "-c", s, "-o", o, "-std=c++17", "-O3", "-lineinfo", *ARCH,
                              "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
-                             "-I", INC, "-I", CSRC]))
+                             "-I", INC, "-I", CSRC, *dflags]))
     for src in CPP_SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src + ".o")
+        o = os.path.join(build_dir, src + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
             log.append(_run(["g++", "-c", s, "-o", o, "-std=c++17", "-O2", "-fPIC", "-ffp-contract=off",
                              "-fno-fast-math", "-I", INC, "-I", CSRC]))
-    if force or _stale(LIB, objs):
-        log.append(_run([NVCC, "-shared", "-o", LIB, *objs, *ARCH, "-lcudart", "-ldl"]))
+    if force or _stale(lib_path, objs):
+        log.append(_run([NVCC, "-shared", "-o", lib_path, *objs, *ARCH, "-lcudart", "-ldl"]))
     out = "\n".join(x for x in log if x)
     if verbose and out:
         print(out)
-    return LIB
+    return lib_path
 
 
 if __name__ == "__main__":
-    build(verbose=True, force="--force" in sys.argv)
-    print(LIB)
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-D", dest="defines", action="append", default=[])
+    ap.add_argument("-o", dest="out", default=None)
+    a = ap.parse_args()
+    print(build(verbose=True, force=a.force, defines=tuple(a.defines), lib_out=a.out))

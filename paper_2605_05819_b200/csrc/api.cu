@@ -51,6 +51,7 @@ struct Window {
   int glue = HC_GLUE_NONE;            // SILU_MUL: members[0] = up (interleaved records), [1] = gate
   std::vector<Member> members;        // sorted by slot
   DevBuf tacc, cnt;                   // launch workspace: fixed-point t, counters (self-resetting)
+  DevBuf xprep;                       // !XS launches: fp16 x' [16][K]
   int ws_chunks = -1;
   int64_t out_rows() const {
     if (glue == HC_GLUE_SILU_MUL) return members.front().rows();
@@ -439,6 +440,11 @@ static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int
   }
   a.tacc = (long long*)w.tacc.p;
   a.cnt = (unsigned*)w.cnt.p;
+  if (!decode_stages_x(B, a.K)) {
+    const size_t need = (size_t)16 * a.K * 2;
+    if (w.xprep.bytes < need) CUDA_TRY(w.xprep.alloc(need));
+    a.x16 = (const uint16_t*)w.xprep.p;
+  }
   const auto key = std::make_tuple(m0.bits, B, a.K, a.n_chunks, 0);
   auto it = ctx->max_ctas.find(key);
   if (it == ctx->max_ctas.end())
@@ -457,6 +463,8 @@ static hc_status launch_window(hc_ctx* ctx, Window& w, const void* x, int ldx, i
   int grid = 0;
   hc_status s = window_args(ctx, w, x, ldx, B, y, y_bf16, resid, ld_resid, a, grid);
   if (s != HC_OK) return s;
+  if (a.x16)
+    CUDA_TRY(launch_xprep(a.x, a.ldx, B, a.K, w.members.front().bits, (uint16_t*)a.x16, st));
   CUDA_TRY(launch_decode(a, w.members.front().bits, grid, st));
   return HC_OK;
 }

@@ -15,9 +15,10 @@
 //    after it;
 //  * x is staged once per CTA in shared memory (rows padded so 128-bit fragment loads are
 //    bank-conflict-free), or read through L1 when it does not fit;
-//  * codes -> bf16 A-fragments with shift/lop3 and the 0x4300 magic (exact integers), minus the
-//    per-group zero (exact), on mma.sync m16n8k16 with fp32 accumulation, two independent
-//    accumulator chains, per-group partials scaled by the fp32 group scale afterwards;
+//  * codes -> fp16 A-fragments with at most one shift per word + one lop3 per register (the 0x6400
+//    magic, exact integers), minus the per-group zero with one hsub2 (exact), times x' = x·2^-fp
+//    (fp16, exact) on mma.sync m16n8k16 with fp32 accumulation; per-group partials are scaled by the
+//    fp32 group scale afterwards;
 //  * the 8 warps' partial sums are reduced in shared memory in a fixed order; the CTA's epilogue
 //    warp adds U[:, :r]·t with t split into bf16 hi + lo (fp32-accurate) on the same mma and
 //    writes y once (fp32, or bf16 = RNE of the fp32 value), optionally adding a bf16 residual;
@@ -25,6 +26,7 @@
 //    are associative, so t is deterministic); epilogues acquire a release counter.  The accumulators
 //    and counters self-reset before the kernel exits.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "decode.h"
@@ -91,21 +93,23 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-__device__ __forceinline__ uint32_t bf2_sub(uint32_t a, uint32_t b) {
-  __nv_bfloat162 r = __hsub2(*reinterpret_cast<__nv_bfloat162*>(&a), *reinterpret_cast<__nv_bfloat162*>(&b));
-  return *reinterpret_cast<uint32_t*>(&r);
+// W tiles: fp16 A-fragments (1024 + 2^fp·q, exact) times fp16 x' = x·2^-fp
+__device__ __forceinline__ void mma16816_f16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
-__device__ __forceinline__ uint32_t bf2_mul(uint32_t a, uint32_t b) {
-  __nv_bfloat162 r = __hmul2(*reinterpret_cast<__nv_bfloat162*>(&a), *reinterpret_cast<__nv_bfloat162*>(&b));
+
+__device__ __forceinline__ uint32_t hf2_sub(uint32_t a, uint32_t b) {
+  __half2 r = __hsub2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b));
   return *reinterpret_cast<uint32_t*>(&r);
 }
 __device__ __forceinline__ float bf16_bits_to_f32(uint32_t h) { return __uint_as_float(h << 16); }
 __device__ __forceinline__ uint32_t f32_to_bf16_rn(float f) {
   __nv_bfloat16 b = __float2bfloat16_rn(f);
   return (uint32_t)(*reinterpret_cast<uint16_t*>(&b));
-}
-__device__ __forceinline__ constexpr uint32_t pow2neg_bf16x2(int fp) {   // bf16x2(2^-fp)
-  return (uint32_t)(0x3F80 - (fp << 7)) * 0x00010001u;
 }
 
 // (a & b) | c in one LOP3 (nvcc otherwise emits two)
@@ -190,12 +194,13 @@ constexpr float kTInv = 1.f / 268435456.f;
 // outputs are never stored, so no zeroing is needed.
 __device__ __forceinline__ int xrow(const DArgs& a, int col) { return col < a.B ? col : a.B - 1; }
 
-// x fragments of group g from global memory (L1-cached): xr[nb][4q + e] = x[b][g*128 + 32q + 8tig .. +7]
+// x' fragments of group g from the window's fp16 x' buffer (global, L1-cached):
+// xr[nb][4q + e] = x'[b][g*128 + 32q + 8tig .. +7]
 template <int NB8>
 __device__ __forceinline__ void load_x_global(const DArgs& a, int g, int lane, uint32_t (&xr)[NB8][16]) {
 #pragma unroll
   for (int nb = 0; nb < NB8; ++nb) {
-    const uint4* p = reinterpret_cast<const uint4*>(a.x + (size_t)xrow(a, (lane >> 2) + 8 * nb) * a.ldx +
+    const uint4* p = reinterpret_cast<const uint4*>(a.x16 + (size_t)xrow(a, (lane >> 2) + 8 * nb) * a.K +
                                                     g * kGroup + 8 * (lane & 3));
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -206,10 +211,12 @@ __device__ __forceinline__ void load_x_global(const DArgs& a, int g, int lane, u
 }
 
 // One (row-block, group) record: tot[nb][e] += s_row · Σ_k (q − z)·x.
-// XS: x fragments come from shared memory (xrow_s[nb] = this lane's run start for the group).
+// The A registers hold 2^fp·(q − z) (fp16, exact) and the B operand is x' = x·2^-fp (fp16), so every
+// product is exact and one mma chain accumulates Σ_k (q − z)·x_k in fp32.
+// XS: x' fragments come from shared memory (xrow_s[nb] = this lane's run start for the group).
 template <int BITS, int NB8, bool XS>
 __device__ __forceinline__ void w_tile(const uint8_t* rec, int lane, const uint4* const (&xrow_s)[NB8],
-                                       const uint32_t (&xr)[NB8][16], const float* xsum_g, float (&tot)[NB8][4]) {
+                                       const uint32_t (&xr)[NB8][16], float (&tot)[NB8][4]) {
   uint32_t w[2 * BITS];
 #pragma unroll
   for (int q = 0; q < (2 * BITS) / 4; ++q) {
@@ -222,25 +229,16 @@ __device__ __forceinline__ void w_tile(const uint8_t* rec, int lane, const uint4
   }
   const int gid = lane >> 2;
   const uint32_t sw = *reinterpret_cast<const uint32_t*>(rec + scales_off(BITS) + 4 * gid);
-  const uint32_t z0 = *reinterpret_cast<const uint32_t*>(rec + zeros_off(BITS));       // rows 0..7
-  const uint32_t z1 = *reinterpret_cast<const uint32_t*>(rec + zeros_off(BITS) + 4);   // rows 8..15
-  const uint32_t zr[2] = {(z0 >> (4 * gid)) & 15u, (z1 >> (4 * gid)) & 15u};
-  constexpr int kFpHi = BITS == 2 ? 2 : (BITS == 3 ? 3 : 0);   // the non-zero field weight exponent
-  uint32_t zc[2][2];                                            // [row parity][fp == 0 ? 0 : 1]
-  if constexpr (!XS) {
+  const uint2 zz = *reinterpret_cast<const uint2*>(rec + zeros_off(BITS));   // rows 0..7 | rows 8..15
+  // fp16x2 (1024 + 2^fp·z) of rows gid / gid + 8 for each field exponent fp: subtracting it turns a
+  // register into 2^fp·(q − z) exactly, so the mma accumulates Σ (q − z)·x with no large offset
+  const uint32_t zr0 = (zz.x >> (4 * gid)) & 15u, zr1 = (zz.y >> (4 * gid)) & 15u;
+  auto zc = [&](int row_hi, int fp) -> uint32_t { return (0x6400u + ((row_hi ? zr1 : zr0) << fp)) * 0x00010001u; };
+  float acc[NB8][4];
 #pragma unroll
-    for (int rp = 0; rp < 2; ++rp) {
-      zc[rp][0] = (0x4300u + zr[rp]) * 0x00010001u;               // bf16x2(128 + z), exact
-      zc[rp][1] = (0x4300u + (zr[rp] << kFpHi)) * 0x00010001u;    // bf16x2(128 + z·2^fp), exact
-    }
-  }
-  float acc[2][NB8][4];
+  for (int nb = 0; nb < NB8; ++nb)
 #pragma unroll
-  for (int h = 0; h < 2; ++h)
-#pragma unroll
-    for (int nb = 0; nb < NB8; ++nb)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) acc[h][nb][e] = 0.f;
+    for (int e = 0; e < 4; ++e) acc[nb][e] = 0.f;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     uint32_t xq[NB8][4];
@@ -260,40 +258,46 @@ __device__ __forceinline__ void w_tile(const uint8_t* rec, int lane, const uint4
       uint32_t af[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        af[i] = extract<BITS>(w, j, i);                                  // 128 + 2^fp·q (exact)
-        if constexpr (!XS) af[i] = bf2_sub(af[i], zc[i & 1][slot(BITS, j, i).fp ? 1 : 0]);   // 2^fp·(q − z)
+        af[i] = extract<BITS>(w, j, i);                            // 1024 + 2^fp·q (exact)
+        af[i] = hf2_sub(af[i], zc(i & 1, slot(BITS, j, i).fp));   // 2^fp·(q − z) (exact)
       }
-      const int fp0 = step_fp(BITS, j, 0), fp1 = step_fp(BITS, j, 1);
 #pragma unroll
-      for (int nb = 0; nb < NB8; ++nb) {
-        uint32_t b0 = xq[nb][2 * jj], b1 = xq[nb][2 * jj + 1];
-        if (fp0) b0 = bf2_mul(b0, pow2neg_bf16x2(fp0));
-        if (fp1) b1 = bf2_mul(b1, pow2neg_bf16x2(fp1));
-        mma16816(acc[jj][nb], af, b0, b1);
-      }
+      for (int nb = 0; nb < NB8; ++nb) mma16816_f16(acc[nb], af, xq[nb][2 * jj], xq[nb][2 * jj + 1]);
     }
   }
   const float s0 = bf16_bits_to_f32(sw & 0xFFFFu), s1 = bf16_bits_to_f32(sw >> 16);
-  if constexpr (XS) {
-    // Σ_k (128 + 2^fp q)·x'_k − (128·Σ_k x'_k + z·Σ_k x_k) = Σ_k (q − z)·x_k   (x' = 2^-fp x);
-    // xsum_g[col] = (Σx, Σx') of this group, computed once per CTA from the staged x
-    const float zf0 = (float)zr[0], zf1 = (float)zr[1];
-#pragma unroll
-    for (int nb = 0; nb < NB8; ++nb) {
-      const float4 xs2 = *reinterpret_cast<const float4*>(xsum_g + 2 * (2 * (lane & 3) + 8 * nb));
-      const float c0 = 128.f * xs2.y, c1 = 128.f * xs2.w;
-      acc[0][nb][0] -= fmaf(zf0, xs2.x, c0);
-      acc[0][nb][1] -= fmaf(zf0, xs2.z, c1);
-      acc[0][nb][2] -= fmaf(zf1, xs2.x, c0);
-      acc[0][nb][3] -= fmaf(zf1, xs2.z, c1);
-    }
-  }
 #pragma unroll
   for (int nb = 0; nb < NB8; ++nb) {
-    tot[nb][0] = fmaf(s0, acc[0][nb][0] + acc[1][nb][0], tot[nb][0]);
-    tot[nb][1] = fmaf(s0, acc[0][nb][1] + acc[1][nb][1], tot[nb][1]);
-    tot[nb][2] = fmaf(s1, acc[0][nb][2] + acc[1][nb][2], tot[nb][2]);
-    tot[nb][3] = fmaf(s1, acc[0][nb][3] + acc[1][nb][3], tot[nb][3]);
+    tot[nb][0] = fmaf(s0, acc[nb][0], tot[nb][0]);
+    tot[nb][1] = fmaf(s0, acc[nb][1], tot[nb][1]);
+    tot[nb][2] = fmaf(s1, acc[nb][2], tot[nb][2]);
+    tot[nb][3] = fmaf(s1, acc[nb][3], tot[nb][3]);
+  }
+}
+
+// x' = x·2^-fp (fp16) of 16 consecutive k of one batch row: `part` (0..7) selects k = 16·part .. +15
+// within the group; fp is the code-field exponent of that k's column pair (layout.h).  Shared by the
+// in-kernel staging pass (XS) and the x-prep kernel (global x').
+template <int BITS>
+__device__ __forceinline__ void xprime16(const uint4 (&in)[2], int part, uint4 (&out)[2]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t wv[4] = {in[h].x, in[h].y, in[h].z, in[h].w};
+    uint32_t ov[4];
+#pragma unroll
+    for (int e2 = 0; e2 < 4; ++e2) {
+      float xp[2];
+#pragma unroll
+      for (int hi = 0; hi < 2; ++hi) {
+        const int k = part * 16 + h * 8 + 2 * e2 + hi;               // k within the group
+        const int j = 2 * (k >> 5) + ((k >> 2) & 1), pr = (k >> 1) & 1;
+        const float xv = bf16_bits_to_f32((wv[e2] >> (16 * hi)) & 0xFFFFu);
+        xp[hi] = xv * __uint_as_float((uint32_t)(127 - step_fp(BITS, j, pr)) << 23);
+      }
+      const __half2 hv = __floats2half2_rn(xp[0], xp[1]);
+      ov[e2] = *reinterpret_cast<const uint32_t*>(&hv);
+    }
+    out[h] = make_uint4(ov[0], ov[1], ov[2], ov[3]);
   }
 }
 
@@ -326,7 +330,7 @@ __device__ __forceinline__ void v_tile(const uint8_t* piece, int lane, const uin
 // for any arrival order), then bumps v_done; each CTA's epilogue warp acquires v_done once and reads
 // t while its tile warps are still streaming.
 template <int BITS, int NB8, bool XS>
-__global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_constant__ DArgs a) {
+__global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(const __grid_constant__ DArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
@@ -340,7 +344,6 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_
   float4* tsm = reinterpret_cast<float4*>(xbar + 2);      // [n_chunks][NB8][32] t fragments
   uint16_t* xs = reinterpret_cast<uint16_t*>(tsm + (size_t)a.n_chunks * NB8 * 32);
   const int xs_ld = a.K + 32;   // +64 B per row: consecutive batch rows fall in disjoint banks
-  float* xsum = reinterpret_cast<float*>(xs + (size_t)a.B * xs_ld);   // [G][16 cols][Σx, Σx'] (XS only)
 
   if (lane == 0) {
     if (warp < kDecodeWarps) {
@@ -576,38 +579,16 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if constexpr (XS) {
     while (!mbar_try_wait(xbar, 0)) {}
-    // per-(group, batch column) sums of x and of the pre-scaled x' (x·2^-fp at the positions whose
-    // code field carries weight 2^fp): the exact zero-point / magic-offset correction of w_tile.
-    // 8 threads per (group, column), 16 elements each, fixed-order shuffle reduction.
+    // in place: x (bf16) -> x' = x·2^-fp (fp16, the B operand of the W mma); 16 elements per thread
     const int tid = threadIdx.x;   // 0..255 (tile warps)
-    const int n_sum = a.G * a.B * 8, n_sum_w = (n_sum + 31) & ~31;   // warp-uniform trip count
-    for (int i = tid; i < n_sum_w; i += kDecodeWarps * 32) {
-      const bool live = i < n_sum;
-      const int part = i & 7, gb = live ? i >> 3 : 0, b = gb % a.B, g = gb / a.B;
-      const uint4* src = reinterpret_cast<const uint4*>(xs + (size_t)b * xs_ld + g * kGroup + part * 16);
-      float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint4 v = src[h];
-        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int k = part * 16 + h * 8 + e;                       // k within the group
-          const int j = 2 * (k >> 5) + ((k >> 2) & 1), pr = (k >> 1) & 1;
-          const float xv = bf16_bits_to_f32((wv[e >> 1] >> (16 * (e & 1))) & 0xFFFFu);
-          s0 += xv;
-          s1 += xv * __uint_as_float((uint32_t)(127 - step_fp(BITS, j, pr)) << 23);
-        }
-      }
-#pragma unroll
-      for (int o = 1; o < 8; o <<= 1) {
-        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-      }
-      if (live && part == 0) { xsum[(size_t)g * 32 + 2 * b] = s0; xsum[(size_t)g * 32 + 2 * b + 1] = s1; }
+    for (int i = tid; i < a.G * a.B * 8; i += kDecodeWarps * 32) {
+      const int part = i & 7, gb = i >> 3, b = gb % a.B, g = gb / a.B;
+      uint4* src = reinterpret_cast<uint4*>(xs + (size_t)b * xs_ld + g * kGroup + part * 16);
+      const uint4 in[2] = {src[0], src[1]};
+      uint4 out[2];
+      xprime16<BITS>(in, part, out);
+      src[0] = out[0]; src[1] = out[1];
     }
-    for (int i = tid; i < a.G * 16; i += kDecodeWarps * 32)   // padding columns: finite, unused
-      if ((i & 15) >= a.B) { xsum[(size_t)(i >> 4) * 32 + 2 * (i & 15)] = 0.f; xsum[(size_t)(i >> 4) * 32 + 2 * (i & 15) + 1] = 0.f; }
     asm volatile("bar.sync 5, %0;" ::"n"(kDecodeWarps * 32) : "memory");   // tile warps only
   }
   const uint16_t* xs_row[NB8];
@@ -625,9 +606,9 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_
     uint4 xv[NB8];
 #pragma unroll
     for (int nb = 0; nb < NB8; ++nb) {
-      const uint4* p = reinterpret_cast<const uint4*>(
-          (XS ? xs_row[nb] : a.x + (size_t)xrow(a, gid + 8 * nb) * a.ldx + 8 * tig) + g * kGroup + 32 * part);
-      xv[nb] = XS ? *p : __ldg(p);
+      const uint4* p = reinterpret_cast<const uint4*>(a.x + (size_t)xrow(a, gid + 8 * nb) * a.ldx + 8 * tig +
+                                                      g * kGroup + 32 * part);
+      xv[nb] = __ldg(p);                                 // bf16 x (V is bf16; x' is for the W tiles)
     }
     while (!mbar_try_wait(&bars[s], ph)) {}
     float tp[NB8][4];
@@ -670,14 +651,28 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_kernel(const __grid_
       const int nt = min(kTPB, sh.n - t0);
       const uint8_t* blk = bufs + s * kBlk;
       while (!mbar_try_wait(&bars[s], ph)) {}
-      for (int t = 0; t < nt; ++t) {
-        const int g = sh.g0 + t0 + t;
-        uint32_t xr[NB8][16];
-        const uint4* xrs[NB8];
+      if (nt == kTPB) {
+        // full block: the records are independent straight-line code, so their mma chains interleave
 #pragma unroll
-        for (int nb = 0; nb < NB8; ++nb) xrs[nb] = reinterpret_cast<const uint4*>(xs_row[nb] + g * kGroup);
-        if constexpr (!XS) load_x_global<NB8>(a, g, lane, xr);
-        w_tile<BITS, NB8, XS>(blk + t * rec_bytes(BITS), lane, xrs, xr, xsum + (size_t)g * 32, tot);
+        for (int t = 0; t < kTPB; ++t) {
+          const int g = sh.g0 + t0 + t;
+          uint32_t xr[NB8][16];
+          const uint4* xrs[NB8];
+#pragma unroll
+          for (int nb = 0; nb < NB8; ++nb) xrs[nb] = reinterpret_cast<const uint4*>(xs_row[nb] + g * kGroup);
+          if constexpr (!XS) load_x_global<NB8>(a, g, lane, xr);
+          w_tile<BITS, NB8, XS>(blk + t * rec_bytes(BITS), lane, xrs, xr, tot);
+        }
+      } else {
+        for (int t = 0; t < nt; ++t) {
+          const int g = sh.g0 + t0 + t;
+          uint32_t xr[NB8][16];
+          const uint4* xrs[NB8];
+#pragma unroll
+          for (int nb = 0; nb < NB8; ++nb) xrs[nb] = reinterpret_cast<const uint4*>(xs_row[nb] + g * kGroup);
+          if constexpr (!XS) load_x_global<NB8>(a, g, lane, xr);
+          w_tile<BITS, NB8, XS>(blk + t * rec_bytes(BITS), lane, xrs, xr, tot);
+        }
       }
       __syncwarp();
       ++blk_done;
@@ -698,7 +693,7 @@ static size_t decode_smem_bytes(bool xs, int B, int K, int n_chunks) {
   size_t s = (size_t)kDecodeWarps * kNBuf * kTPB * kTileMax + 2 * kDecodeWarps * 32 * 8 * sizeof(float) +
              2 * kUPre * 32 * 16 + (kDecodeWarps * kNBuf + 4) * sizeof(uint64_t) +
              (size_t)n_chunks * nb8 * 32 * 16;
-  if (xs) s += (size_t)B * (K + 32) * 2 + (size_t)(K / 128) * 32 * sizeof(float);
+  if (xs) s += (size_t)B * (K + 32) * 2;
   return s;
 }
 
@@ -706,6 +701,44 @@ constexpr size_t kXsMax = 48 * 1024;
 constexpr size_t kSmemOptin = 227 * 1024;   // x staged in smem when B*(K+32)*2 fits this
 
 static bool use_xs(int B, int K) { return B <= 8 && (size_t)B * (K + 32) * 2 <= kXsMax; }
+bool decode_stages_x(int B, int K) { return B <= 8 && use_xs(B, K); }
+
+// x -> x' (fp16, pre-scaled per the code layout) for the !XS decode launches.
+// One thread per (group, batch row, 16-element part).
+template <int BITS>
+__global__ void xprep_kernel(const uint16_t* __restrict__ x, int ldx, int B, int K, uint16_t* __restrict__ x16) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;   // over G * B * 8
+  if (i < (K / kGroup) * B * 8) {
+    const int part = i & 7, gb = i >> 3, b = gb % B, g = gb / B;
+    const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)b * ldx + g * kGroup + part * 16);
+    const uint4 in[2] = {__ldg(src), __ldg(src + 1)};
+    uint4 out[2];
+    xprime16<BITS>(in, part, out);
+    uint4* dst = reinterpret_cast<uint4*>(x16 + (size_t)b * K + g * kGroup + part * 16);
+    dst[0] = out[0]; dst[1] = out[1];
+  }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+cudaError_t launch_xprep(const uint16_t* x, int ldx, int B, int K, int bits, uint16_t* x16, cudaStream_t st) {
+  const int n = (K / kGroup) * B * 8;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((n + 255) / 256);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  switch (bits) {
+    case 2: return cudaLaunchKernelEx(&cfg, xprep_kernel<2>, x, ldx, B, K, x16);
+    case 3: return cudaLaunchKernelEx(&cfg, xprep_kernel<3>, x, ldx, B, K, x16);
+    case 4: return cudaLaunchKernelEx(&cfg, xprep_kernel<4>, x, ldx, B, K, x16);
+    default: return cudaErrorInvalidValue;
+  }
+}
 
 template <int BITS, int NB8, bool XS>
 static cudaError_t launch_t(const DArgs& a, int grid, cudaStream_t st) {

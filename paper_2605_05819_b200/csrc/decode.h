@@ -9,8 +9,17 @@ constexpr int kMaxMembers = 4;
 constexpr int kDecodeWarps = 8;          // tile (streaming + contraction) warps per CTA
 constexpr int kDecodeThreads = (kDecodeWarps + 1) * 32;   // + one epilogue warp
 constexpr int kMaxChunks = 32;           // Σ ceil(r_m/16) over a window's members
-constexpr int kTPB = 2;                  // tiles per bulk-copy block
-constexpr int kNBuf = 4;                 // block buffers per warp (3 blocks in flight while one computes)
+#ifndef HC_DEC_TPB
+#define HC_DEC_TPB 4
+#endif
+#ifndef HC_DEC_NBUF
+#define HC_DEC_NBUF 2
+#endif
+#ifndef HC_DEC_MINB
+#define HC_DEC_MINB 2
+#endif
+constexpr int kTPB = HC_DEC_TPB;         // tiles per bulk-copy block
+constexpr int kNBuf = HC_DEC_NBUF;       // block buffers per warp (kNBuf - 1 blocks in flight while one computes)
 constexpr int kTileMax = 1088;           // >= rec_bytes(4) = 1072, >= 1 KB V piece
 constexpr int kUPre = 4;                 // U chunks (16 ranks each) staged in smem per item
 
@@ -40,12 +49,17 @@ struct DArgs {
                         //   m[1] = gate (V / rank only); row block = 8 up rows + 8 gate rows
   int n_rb;             // Σ members
   int n_chunks;         // Σ ceil(r_m / 16)
+  const uint16_t* x16;  // !XS launches: fp16 x' = x·2^-fp [B][K] written by launch_xprep (else unused)
   long long* tacc;      // [n_chunks][16 batch][16 ranks] t = V·x in 2^-28 fixed point (self-resetting)
   unsigned* cnt;        // [0] v_done (tile warps done with their V share), [1] w_done (row blocks)
 };
 
 // Launch the fused window kernel; bits in {2,3,4}; 1 <= B <= 16.
 cudaError_t launch_decode(const DArgs& a, int bits, int grid, cudaStream_t st);
+// Whether a launch with this batch / K stages x in shared memory (else it needs launch_xprep first).
+bool decode_stages_x(int B, int K);
+// x' (fp16, pre-scaled per the code layout of `bits`) for a !XS decode launch.
+cudaError_t launch_xprep(const uint16_t* x, int ldx, int B, int K, int bits, uint16_t* x16, cudaStream_t st);
 // Max co-resident CTAs of the decode kernel on this device (persistent grid size).
 int decode_max_ctas(int bits, int B, int K, int n_chunks);
 

@@ -3,8 +3,9 @@
 // The C-ABI takes canonical formats (include/hcinfer.h); hc_load_layer repacks them
 // once into the layout below, chosen so that the decode kernel
 //   * streams every weight byte exactly once with 16-byte-aligned bulk (TMA) copies,
-//   * turns each 32-bit code word into mma.sync A-fragment registers with only
-//     shift + lop3 (the bf16 "magic number" trick: 0x4300 | bits = 128 + bits),
+//   * turns each 32-bit code word into mma.sync A-fragment registers with at most one
+//     shift per word plus one lop3 per register (the fp16 "magic number" trick:
+//     0x6400 | field = 1024 + field, exact: fp16 has 10 mantissa bits),
 //   * never materialises W.
 //
 // Row block (rb) = 16 output rows (the mma M dimension).  Group = 128 input
@@ -22,11 +23,16 @@
 //   scales word gid = bf16 s[row gid] | bf16 s[row gid+8] << 16
 //   zeros  u64: row r's zero in bits [4r, 4r+4)
 //
-// Register extraction ("slots"): register (j, i) = 0x43004300 | field bits, where a
+// Register extraction ("slots"): register (j, i) = 0x64006400 | field bits, where a
 // field is up to 3 "parts" (word, shift, pos, nbits) taken from the lo 16-bit half
 // (and the same bits +16 from the hi half).  The register then holds
-// 128 + q*2^fp in both halves (exact in bf16), fp in {0, 2, 3}.  The B operand
-// (x) of the two registers sharing a column pair is pre-scaled by 2^-fp (exact).
+// 1024 + q*2^fp in both halves (exact in fp16), fp = the field's bit position.  The two
+// registers of a column pair (i, i^1) share fp, so the B operand (x) of that pair is
+// pre-scaled by 2^-fp once (x' = x·2^-fp, exact in fp16 for normal-range x; R20).
+//   4-bit: word j, fields at bits [0,4) (fp 0) and [4,8) (fp 4) of w and of w >> 8;
+//   2-bit: word j/2, fields at bits 2p (fp 2p, p = (i>>1) + 2(j&1)) of w and of w >> 8;
+//   3-bit: fields at bits 0-2 and 3-5 (fp 3) of w >> {0, 6, 12}, plus two registers gathered
+//          from bit 15 of the six words.
 #pragma once
 #include <stdint.h>
 
@@ -40,7 +46,8 @@ namespace hc {
 
 constexpr int kRows = 16;
 constexpr int kGroup = 128;
-constexpr uint32_t kMagic = 0x43004300u;   // bf16x2(128, 128)
+constexpr uint32_t kMagic = 0x64006400u;   // fp16x2(1024, 1024)
+constexpr float kMagicF = 1024.f;
 
 HC_HD constexpr int code_words(int bits) { return 2 * bits; }            // per lane per group
 HC_HD constexpr int code_bytes(int bits) { return 256 * bits; }          // per (rb, group)
@@ -60,11 +67,12 @@ struct Slot { int nparts; int fp; Part p[3]; };
 // Slot table for register (j, i) at a given bit width.  See the header comment.
 HC_HD constexpr Slot slot(int bits, int j, int i) {
   if (bits == 4) {
-    return Slot{1, 0, {Part{j, 4 * i, 0, 4}, Part{0, 0, 0, 0}, Part{0, 0, 0, 0}}};
+    const int fp = 4 * (i >> 1);
+    return Slot{1, fp, {Part{j, 8 * (i & 1), fp, 4}, Part{0, 0, 0, 0}, Part{0, 0, 0, 0}}};
   }
   if (bits == 2) {
-    const int fp = 2 * (i >> 1);
-    return Slot{1, fp, {Part{j / 2, 8 * (j & 1) + 4 * (i & 1), fp, 2}, Part{0, 0, 0, 0}, Part{0, 0, 0, 0}}};
+    const int fp = 2 * (i >> 1) + 4 * (j & 1);
+    return Slot{1, fp, {Part{j / 2, 8 * (i & 1), fp, 2}, Part{0, 0, 0, 0}, Part{0, 0, 0, 0}}};
   }
   // bits == 3: 20 weight-1 slots (18 plain + 2 gathered from bit 15 of each word),
   // 12 weight-8 slots; steps 0..5 pair (w1, w8), steps 6..7 pair (w1, w1).

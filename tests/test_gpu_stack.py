@@ -82,17 +82,30 @@ def load_stack(hc, ctx, layers, ranks):
         ctx.load_layer(mats)
 
 
-def stack_close(y_bits, ref):
-    """bf16 outputs: |y - ref| <= 2e-3 max|ref| + one bf16 ulp of the element (the last rounding
-    may land on the other side of a tie-break)."""
+def stack_close(y_bits, ref, n_layers=1):
+    """bf16 stack outputs against the float64 oracle.
+
+    The stack rounds its activations to bf16 between linears (R8), so an fp32 kernel and
+    the float64 oracle can legitimately round an intermediate value to neighbouring bf16 values
+    when it lies within fp32 error (≈2e-5 relative, R20) of a rounding boundary; a flip in the
+    residual stream (h1) carries one bf16 ulp (≤ 2^-7·|v|) straight to the layer output, the final
+    rounding another.  Bound per element: 2e-3·max|ref| (north_star) + 2 ulps per layer."""
     y = bf16_to_f64(y_bits)
-    bound = 2e-3 * np.abs(ref).max() + np.abs(ref) * 2.0 ** -8
+    bound = 2e-3 * np.abs(ref).max() + np.abs(ref) * 2.0 ** -6 * n_layers
     return np.all(np.abs(y - ref) <= bound), np.abs(y - ref).max() / np.abs(ref).max()
+
+
+def one_layer_ctx(hc, layers, ranks, l):
+    ctx = hc.Context(0)
+    load_stack(hc, ctx, [layers[l]], [ranks[l]])
+    return ctx
 
 
 @pytest.mark.parametrize("bits", [4, 2])
 @pytest.mark.parametrize("B", [1, 4, 16])
 def test_stack_forward_parity(hc, bits, B):
+    """Per-layer parity against the oracle fed the kernel's own bf16 input (so every comparison is
+    one layer deep), and the multi-layer graph equal bit-for-bit to the chain of those layers."""
     L, d, kv, f = 3, 256, 128, 512
     layers, ranks = make_stack(L, d, kv, f, bits, 32, seed=bits * 10 + B)
     ctx = hc.Context(0)
@@ -105,8 +118,23 @@ def test_stack_forward_parity(hc, bits, B):
     torch.cuda.synchronize()
     yb = y.cpu().numpy().view(np.uint16)
     assert np.array_equal(yb, y2.cpu().numpy().view(np.uint16))
-    ref = linear.stack_forward(layers, ranks, x)
-    ok, rel = stack_close(yb, ref)
+    h = x
+    exact = 0
+    for l in range(L):
+        c1 = one_layer_ctx(hc, layers, ranks, l)
+        yl = torch.empty((B, d), dtype=torch.int16, device="cuda")
+        c1.stack_forward(dev(h), yl)
+        torch.cuda.synchronize()
+        hl = yl.cpu().numpy().view(np.uint16).copy()
+        ref = linear.stack_forward([layers[l]], [ranks[l]], h)
+        ok, rel = stack_close(hl, ref)
+        assert ok, (l, rel)
+        exact += int(np.sum(hl == f64_to_bf16_bits_rne(ref)))
+        c1.close()
+        h = hl
+    assert np.array_equal(h, yb)                                   # graph == chain of layers
+    assert exact >= 0.98 * L * B * d                                # rounding flips are rare
+    ok, rel = stack_close(yb, linear.stack_forward(layers, ranks, x), n_layers=L)
     assert ok, rel
     # host buffers through the public API
     yh = np.zeros((B, d), dtype=np.uint16)
@@ -130,7 +158,7 @@ def test_stack_rank_change_recaptures(hc):
                 ranks[l][key][s] = 0
     ctx.stack_forward(dev(x), y)
     torch.cuda.synchronize()
-    ok, rel = stack_close(y.cpu().numpy().view(np.uint16), linear.stack_forward(layers, ranks, x))
+    ok, rel = stack_close(y.cpu().numpy().view(np.uint16), linear.stack_forward(layers, ranks, x), n_layers=L)
     assert ok, rel
     ctx.close()
 
