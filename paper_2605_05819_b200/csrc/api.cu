@@ -13,6 +13,7 @@
 #include "comm.h"
 #include "decode.h"
 #include "prefill.h"
+#include "stack.h"
 #include "hcinfer.h"
 #include "layout.h"
 #include "repack_kernels.h"
@@ -74,6 +75,7 @@ bool admissible_rank(int r) { return r == 0 || (r >= 8 && (r & (r - 1)) == 0); }
 
 struct StackGraph {
   cudaGraphExec_t exec = nullptr;
+  DevBuf table, cnt;                  // persistent stack kernel: this graph's window table and counters
   ~StackGraph() { if (exec) cudaGraphExecDestroy(exec); }
 };
 
@@ -625,6 +627,10 @@ static hc_status tp_window(hc_ctx* ctx, Window& w, const void* x, int ldx, int B
 
 }  // namespace
 
+// dev-only (not in hcinfer.h): point the stack kernel's trace stamps at a device buffer
+extern "C" int hc_dev_stack_trace(void* buf) { return (int)hc::stack_set_trace(buf); }
+extern "C" int hc_dev_stack_acct(void* buf) { return (int)hc::stack_set_acct(buf); }
+
 extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, void* y, void* stream) {
   if (!ctx) return fail(HC_ERR_STATE, "hc_stack_forward: null context");
   if (B < 1 || B > 16) return fail(HC_ERR_CONFIG, "hc_stack_forward: B = %d outside [1, 16]", B);
@@ -675,6 +681,86 @@ extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, voi
         if (s != HC_OK) return s;
       }
     cudaStream_t cs = ctx->cap_stream;
+    // persistent stack kernel (one launch for all windows) when the plan qualifies
+    const char* stack_ev = getenv("HC_STACK_KERNEL");   // "1": persistent stack kernel (opt-in)
+    const bool stack_env = stack_ev && stack_ev[0] == '1';
+    const int bits0 = plan.front().qkv->members.front().bits;
+    bool use_stack = stack_env && !tp && B <= 8;
+    int k_max = 0;
+    for (LayerPlan& p : plan)
+      for (Window* w : {p.qkv, p.o, p.ug, p.down}) {
+        k_max = std::max(k_max, w->members.front().K);
+        if (w->members.front().bits != bits0) use_stack = false;
+      }
+    int u_chunks = 1;                                    // largest U slice (16-rank chunks) of any row block
+    for (LayerPlan& p : plan)
+      for (Window* w : {p.qkv, p.o, p.ug, p.down}) {
+        if (w->glue == HC_GLUE_SILU_MUL) u_chunks = std::max(u_chunks, (std::max(w->members[0].r_alloc, w->members[1].r_alloc) + 15) / 16);
+        else for (const Member& m : w->members) u_chunks = std::max(u_chunks, (m.r_alloc + 15) / 16);
+      }
+    int n_us = hc::stack_uslots_max();
+    while (n_us > 2 && use_stack && hc::stack_smem_bytes(B, k_max, u_chunks, n_us) == 0) --n_us;
+    const size_t s_smem = use_stack ? hc::stack_smem_bytes(B, k_max, u_chunks, n_us) : 0;
+    const int s_grid = s_smem ? hc::stack_grid(bits0, s_smem) : 0;
+    if (use_stack && s_grid > 0) {
+      std::vector<hc::SWin> tab;
+      const uint16_t* hin = (const uint16_t*)dx;
+      uint16_t* h = (uint16_t*)ctx->s_h.p;
+      uint16_t* h1 = (uint16_t*)ctx->s_h1.p;
+      uint16_t* qkv = (uint16_t*)ctx->s_qkv.p;
+      uint16_t* mm = (uint16_t*)ctx->s_m.p;
+      int rot = 0;
+      auto add = [&](Window& w, const void* x, int ldx, void* y, const void* resid, int ld_resid) -> hc_status {
+        hc::SWin sw;
+        std::memset(&sw, 0, sizeof(sw));
+        int grid_unused = 0;
+        hc_status st2 = hc::window_args(ctx, w, x, ldx, B, y, 1, resid, ld_resid, sw.a, grid_unused);
+        if (st2 != HC_OK) return st2;
+        sw.rot = rot;
+        sw.n_vwarps = hc::stack_vwarps(sw.a.n_chunks * 4 * sw.a.G, s_grid);
+        rot = (rot + sw.a.n_rb) % s_grid;
+        tab.push_back(sw);
+        return HC_OK;
+      };
+      for (size_t l = 0; l < plan.size(); ++l) {
+        LayerPlan& p = plan[l];
+        uint16_t* hout = (l + 1 == plan.size()) ? (uint16_t*)dy : h;
+        s = add(*p.qkv, hin, d, qkv, nullptr, 0);
+        if (s == HC_OK) s = add(*p.o, qkv, nqkv, h1, hin, d);
+        if (s == HC_OK) s = add(*p.ug, h1, d, mm, nullptr, 0);
+        if (s == HC_OK) s = add(*p.down, mm, f, hout, h1, d);
+        if (s != HC_OK) return s;
+        hin = hout;
+      }
+      const size_t tb = tab.size() * sizeof(hc::SWin), cb = 2 * tab.size() * sizeof(unsigned);
+      std::unique_ptr<StackGraph> sg(new StackGraph());
+      CUDA_TRY(sg->table.alloc(tb));
+      CUDA_TRY(sg->cnt.alloc(cb));
+      CUDA_TRY(cudaMemcpy(sg->table.p, tab.data(), tb, cudaMemcpyHostToDevice));
+      hc::StackArgs sa;
+      sa.wins = (const hc::SWin*)sg->table.p;
+      sa.n_win = (int)tab.size();
+      sa.xs_ld = k_max + 32;
+      sa.u_slot_chunks = u_chunks;
+      sa.n_uslots = n_us;
+      sa.done = (unsigned*)sg->cnt.p;
+      sa.vdone = sa.done + tab.size();
+      CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      cudaError_t e1 = cudaMemsetAsync(sg->cnt.p, 0, cb, cs);
+      cudaError_t e2 = e1 == cudaSuccess ? hc::launch_stack(sa, bits0, s_grid, s_smem, cs) : e1;
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamEndCapture(cs, &g);
+      if (e2 != cudaSuccess) { if (g) cudaGraphDestroy(g); return fail(HC_ERR_RUNTIME, "stack kernel capture: %s", cudaGetErrorString(e2)); }
+      CUDA_TRY(e);
+      e = cudaGraphInstantiate(&sg->exec, g, 0);
+      cudaGraphDestroy(g);
+      CUDA_TRY(e);
+      git = ctx->graphs.emplace(key, std::move(sg)).first;
+      CUDA_TRY(cudaGraphLaunch(git->second->exec, st));
+      if (hy) CUDA_TRY(cudaMemcpyAsync(y, dy, hb, cudaMemcpyDeviceToHost, st));
+      if (hx || hy) CUDA_TRY(cudaStreamSynchronize(st));
+      return HC_OK;
+    }
     CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
     hc_status cap = HC_OK;
     const uint16_t* hin = (const uint16_t*)dx;

@@ -50,6 +50,18 @@ struct DArgs {
   int n_rb;             // Σ members
   int n_chunks;         // Σ ceil(r_m / 16)
   const uint16_t* x16;  // !XS launches: fp16 x' = x·2^-fp [B][K] written by launch_xprep (else unused)
+  int t_in;             // 1: t = V·x of this window was already accumulated into tacc by the kernel that
+                        //    produced x (t forwarding); the launch runs no rank-projection pieces
+  // t forwarding to the next window (the one whose input x' is this window's output):
+  //   t_next[c][col][rank] += Σ_k Vn[c][k/16] · y[col][k]   for output columns k in [fwd_lo, fwd_hi)
+  int fwd;              // 0 off, 1 on
+  int fwd_lo, fwd_hi;   // output columns of this window that are the next window's x (k = col - fwd_lo)
+  int fwd_chunks;       // Σ ceil(r/16) over the next window's members
+  const uint4* fwd_vn[kMaxMembers];   // natural-k V fragments [r_stored/16][K/16][32] of the next members
+  int fwd_cb[kMaxMembers + 1];        // chunk ranges: member i owns chunks [fwd_cb[i], fwd_cb[i+1])
+  int fwd_kb;           // next window's K / 16 (row stride of a chunk in fwd_vn, in 16-k blocks)
+  int fwd_nm;           // next window's member count
+  long long* fwd_tacc;  // next window's t accumulators
   long long* tacc;      // [n_chunks][16 batch][16 ranks] t = V·x in 2^-28 fixed point (self-resetting)
   unsigned* cnt;        // [0] v_done (tile warps done with their V share), [1] w_done (row blocks)
 };

@@ -1,0 +1,311 @@
+// Device helpers shared by the per-window decode kernel (decode.cu) and the persistent stack kernel
+// (stack.cu): async-copy / mbarrier wrappers, the mma.sync tiles and the record (layout.h) decoding.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "decode.h"
+#include "layout.h"
+
+namespace hc {
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                          uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t evict_last_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// counter += v with release semantics (orders the writes made before it — by this thread, or by others
+// ordered before it through a warp / CTA barrier — without a sequentially consistent fence)
+__device__ __forceinline__ unsigned add_release(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.release.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// W tiles: fp16 A-fragments (1024 + 2^fp·q, exact) times fp16 x' = x·2^-fp
+__device__ __forceinline__ void mma16816_f16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t hf2_sub(uint32_t a, uint32_t b) {
+  __half2 r = __hsub2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+__device__ __forceinline__ float bf16_bits_to_f32(uint32_t h) { return __uint_as_float(h << 16); }
+__device__ __forceinline__ uint32_t f32_to_bf16_rn(float f) {
+  __nv_bfloat16 b = __float2bfloat16_rn(f);
+  return (uint32_t)(*reinterpret_cast<uint16_t*>(&b));
+}
+
+// (a & b) | c in one LOP3 (nvcc otherwise emits two)
+__device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// w >> s; shifts of 8 or more run as IMAD.HI on the FMA pipe to balance it against the ALU pipe
+// (which carries the LOP3s)
+__device__ __forceinline__ uint32_t shr(uint32_t w, int s) {
+  return s == 0 ? w : (s >= 8 ? __umulhi(w, 1u << (32 - s)) : (w >> s));
+}
+
+template <int BITS>
+__device__ __forceinline__ uint32_t extract(const uint32_t (&w)[2 * BITS], int j, int i) {
+  const Slot s = slot(BITS, j, i);
+  uint32_t acc = kMagic;
+#pragma unroll
+  for (int p = 0; p < 3; ++p) {
+    if (p < s.nparts) {
+      uint32_t m = ((1u << s.p[p].nbits) - 1u) << s.p[p].pos;
+      m |= m << 16;
+      acc = and_or(shr(w[s.p[p].word], s.p[p].shift), m, acc);
+    }
+  }
+  return acc;
+}
+
+// A warp's share of one CTA work item: n tiles at base + t*tb (tb bytes each).
+struct Share {
+  const uint8_t* base;
+  int n, tb, g0, member, is_v;
+};
+
+__device__ __forceinline__ int member_of_rb(const DArgs& a, int rb) {
+  int m = 0;
+#pragma unroll
+  for (int i = 1; i < kMaxMembers; ++i)
+    if (i < a.n_members && rb >= a.m[i].rb_begin) m = i;
+  return m;
+}
+__device__ __forceinline__ int member_of_chunk(const DArgs& a, int cc) {
+  int m = 0;
+#pragma unroll
+  for (int i = 0; i < kMaxMembers; ++i)
+    if (i < a.n_members && a.m[i].r > 0 && cc >= a.m[i].chunk_begin) m = i;
+  return m;
+}
+
+// The tiles of one row-block item a tile warp streams: contiguous group range [g0, g0 + n).
+template <int BITS, int NW = kDecodeWarps>
+__device__ __forceinline__ Share warp_share(const DArgs& a, int rb, int warp) {
+  Share s;
+  s.member = member_of_rb(a, rb);
+  const DMember& m = a.m[s.member];
+  const int g0 = warp * a.G / NW, g1 = (warp + 1) * a.G / NW;
+  s.n = g1 - g0;
+  s.g0 = g0;
+  s.base = m.rec + ((size_t)(rb - m.rb_begin) * a.G + g0) * rec_bytes(BITS);
+  s.tb = rec_bytes(BITS);
+  s.is_v = 0;
+  return s;
+}
+
+// V piece vp of the window (chunk-major, then group, then part p of 2 k16 steps): 1 KB of fragments
+__device__ __forceinline__ const uint8_t* v_piece(const DArgs& a, int vp, int& g, int& part) {
+  const int per_chunk = 4 * a.G;
+  const int cc = vp / per_chunk, rem = vp - cc * per_chunk;
+  g = rem >> 2;
+  part = rem & 3;
+  const DMember& m = a.m[member_of_chunk(a, cc)];
+  return reinterpret_cast<const uint8_t*>(m.V + ((size_t)(cc - m.chunk_begin) * a.G * 256 + (size_t)rem * 64));
+}
+
+constexpr int kVPerWarp = 2;                    // V·x pieces per tile warp of the V CTAs
+constexpr float kTScale = 268435456.f;          // 2^28: fixed-point scale of the t accumulators
+constexpr float kTInv = 1.f / 268435456.f;
+
+// Row of x used by mma column `col` (batch index).  Columns >= B read a valid row; their
+// outputs are never stored, so no zeroing is needed.
+__device__ __forceinline__ int xrow(const DArgs& a, int col) { return col < a.B ? col : a.B - 1; }
+
+// x' fragments of group g from the window's fp16 x' buffer (global, L1-cached):
+// xr[nb][4q + e] = x'[b][g*128 + 32q + 8tig .. +7]
+template <int NB8>
+__device__ __forceinline__ void load_x_global(const DArgs& a, int g, int lane, uint32_t (&xr)[NB8][16]) {
+#pragma unroll
+  for (int nb = 0; nb < NB8; ++nb) {
+    const uint4* p = reinterpret_cast<const uint4*>(a.x16 + (size_t)xrow(a, (lane >> 2) + 8 * nb) * a.K +
+                                                    g * kGroup + 8 * (lane & 3));
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 v = __ldg(p + 4 * q);
+      xr[nb][4 * q + 0] = v.x; xr[nb][4 * q + 1] = v.y; xr[nb][4 * q + 2] = v.z; xr[nb][4 * q + 3] = v.w;
+    }
+  }
+}
+
+// One (row-block, group) record: tot[nb][e] += s_row · Σ_k (q − z)·x.
+// The A registers hold 2^fp·(q − z) (fp16, exact) and the B operand is x' = x·2^-fp (fp16), so every
+// product is exact and one mma chain accumulates Σ_k (q − z)·x_k in fp32.
+// XS: x' fragments come from shared memory (xrow_s[nb] = this lane's run start for the group).
+template <int BITS, int NB8, bool XS>
+__device__ __forceinline__ void w_tile(const uint8_t* rec, int lane, const uint4* const (&xrow_s)[NB8],
+                                       const uint32_t (&xr)[NB8][16], float (&tot)[NB8][4]) {
+  uint32_t w[2 * BITS];
+#pragma unroll
+  for (int q = 0; q < (2 * BITS) / 4; ++q) {
+    const uint4 v = *reinterpret_cast<const uint4*>(rec + q * 512 + lane * 16);
+    w[4 * q + 0] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+  }
+  if constexpr ((2 * BITS) % 4) {
+    const uint2 v = *reinterpret_cast<const uint2*>(rec + 512 * ((2 * BITS) / 4) + lane * 8);
+    w[2 * BITS - 2] = v.x; w[2 * BITS - 1] = v.y;
+  }
+  const int gid = lane >> 2;
+  const uint32_t sw = *reinterpret_cast<const uint32_t*>(rec + scales_off(BITS) + 4 * gid);
+  const uint2 zz = *reinterpret_cast<const uint2*>(rec + zeros_off(BITS));   // rows 0..7 | rows 8..15
+  // fp16x2 (1024 + 2^fp·z) of rows gid / gid + 8 for each field exponent fp: subtracting it turns a
+  // register into 2^fp·(q − z) exactly, so the mma accumulates Σ (q − z)·x with no large offset
+  const uint32_t zr0 = (zz.x >> (4 * gid)) & 15u, zr1 = (zz.y >> (4 * gid)) & 15u;
+  auto zc = [&](int row_hi, int fp) -> uint32_t { return (0x6400u + ((row_hi ? zr1 : zr0) << fp)) * 0x00010001u; };
+  float acc[NB8][4];
+#pragma unroll
+  for (int nb = 0; nb < NB8; ++nb)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[nb][e] = 0.f;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t xq[NB8][4];
+#pragma unroll
+    for (int nb = 0; nb < NB8; ++nb) {
+      if constexpr (XS) {
+        const uint4 v = xrow_s[nb][4 * q];
+        xq[nb][0] = v.x; xq[nb][1] = v.y; xq[nb][2] = v.z; xq[nb][3] = v.w;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) xq[nb][e] = xr[nb][4 * q + e];
+      }
+    }
+#pragma unroll
+    for (int jj = 0; jj < 2; ++jj) {
+      const int j = 2 * q + jj;
+      uint32_t af[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        af[i] = extract<BITS>(w, j, i);                            // 1024 + 2^fp·q (exact)
+        af[i] = hf2_sub(af[i], zc(i & 1, slot(BITS, j, i).fp));   // 2^fp·(q − z) (exact)
+      }
+#pragma unroll
+      for (int nb = 0; nb < NB8; ++nb) mma16816_f16(acc[nb], af, xq[nb][2 * jj], xq[nb][2 * jj + 1]);
+    }
+  }
+  const float s0 = bf16_bits_to_f32(sw & 0xFFFFu), s1 = bf16_bits_to_f32(sw >> 16);
+#pragma unroll
+  for (int nb = 0; nb < NB8; ++nb) {
+    tot[nb][0] = fmaf(s0, acc[nb][0], tot[nb][0]);
+    tot[nb][1] = fmaf(s0, acc[nb][1], tot[nb][1]);
+    tot[nb][2] = fmaf(s1, acc[nb][2], tot[nb][2]);
+    tot[nb][3] = fmaf(s1, acc[nb][3], tot[nb][3]);
+  }
+}
+
+// x' = x·2^-fp (fp16) of 16 consecutive k of one batch row: `part` (0..7) selects k = 16·part .. +15
+// within the group; fp is the code-field exponent of that k's column pair (layout.h).  Shared by the
+// in-kernel staging pass (XS) and the x-prep kernel (global x').
+template <int BITS>
+__device__ __forceinline__ void xprime16(const uint4 (&in)[2], int part, uint4 (&out)[2]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t wv[4] = {in[h].x, in[h].y, in[h].z, in[h].w};
+    uint32_t ov[4];
+#pragma unroll
+    for (int e2 = 0; e2 < 4; ++e2) {
+      float xp[2];
+#pragma unroll
+      for (int hi = 0; hi < 2; ++hi) {
+        const int k = part * 16 + h * 8 + 2 * e2 + hi;               // k within the group
+        const int j = 2 * (k >> 5) + ((k >> 2) & 1), pr = (k >> 1) & 1;
+        const float xv = bf16_bits_to_f32((wv[e2] >> (16 * hi)) & 0xFFFFu);
+        xp[hi] = xv * __uint_as_float((uint32_t)(127 - step_fp(BITS, j, pr)) << 23);
+      }
+      const __half2 hv = __floats2half2_rn(xp[0], xp[1]);
+      ov[e2] = *reinterpret_cast<const uint32_t*>(&hv);
+    }
+    out[h] = make_uint4(ov[0], ov[1], ov[2], ov[3]);
+  }
+}
+
+// One 1 KB V piece = steps 2p, 2p+1 of a (chunk, group) tile; xv = the lane's 16 B x run.
+template <int NB8>
+__device__ __forceinline__ void v_tile(const uint8_t* piece, int lane, const uint4 (&xv)[NB8], float (&tot)[NB8][4]) {
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const uint4 v = *reinterpret_cast<const uint4*>(piece + s * 512 + lane * 16);
+    const uint32_t af[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int nb = 0; nb < NB8; ++nb) {
+      if (s == 0) mma16816(tot[nb], af, xv[nb].x, xv[nb].y);
+      else        mma16816(tot[nb], af, xv[nb].z, xv[nb].w);
+    }
+  }
+}
+
+}  // namespace
+
+}  // namespace hc

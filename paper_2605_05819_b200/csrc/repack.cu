@@ -71,6 +71,28 @@ __global__ void repack_v_kernel(const uint16_t* __restrict__ V, int K, int r_sto
   }
 }
 
+// Vn: [c][kb][lane][4 regs]; reg i of lane: rank 16c + gid + 8(i&1), k = 16kb + 2tig + 8(i>>1) + {0,1}
+__global__ void repack_vn_kernel(const uint16_t* __restrict__ V, int K, int r_stored, uint32_t* __restrict__ out) {
+  const int KB = K / 16, nc = r_stored / 16;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= (long long)nc * KB * 32) return;
+  const int lane = (int)(tid & 31);
+  const long long ck = tid >> 5;
+  const int kb = (int)(ck % KB), c = (int)(ck / KB);
+  for (int i = 0; i < 4; ++i) {
+    const size_t rank = (size_t)(16 * c + (lane >> 2) + 8 * (i & 1));
+    const int k = 16 * kb + 2 * (lane & 3) + 8 * (i >> 1);
+    out[tid * 4 + i] = (uint32_t)V[rank * K + k] | ((uint32_t)V[rank * K + k + 1] << 16);
+  }
+}
+
+cudaError_t launch_repack_vn(const uint16_t* V, int K, int r_stored, uint32_t* out, cudaStream_t st) {
+  if (r_stored <= 0) return cudaSuccess;
+  const long long n = (long long)(r_stored / 16) * (K / 16) * 32;
+  repack_vn_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(V, K, r_stored, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_repack_records(const RepackSrc& src, int K, int bits, int r_stored, int n_rb, uint8_t* rec_out,
                                   uint32_t* u_out, cudaStream_t st) {
   const int G = K / kGroup;
