@@ -40,6 +40,7 @@ struct DevBuf {
 struct Member {
   int slot = 0, N = 0, K = 0, bits = 0, r_stored = 0, r_alloc = 0, row_begin = 0, row_end = 0;
   std::shared_ptr<DevBuf> rec, U, V;   // rec/U empty for the gate member of a fused SiLU window
+  std::shared_ptr<DevBuf> Vn;          // natural-k V fragments [K/16][r_stored/16][32] (t forwarding)
   // prefill (tcgen05) copies, 4-bit plain members only: nibble-paired codes, canonical scales /
   // zeros of the shard rows, fp16 U [rows][r_stored] and V [r_stored][K]
   std::shared_ptr<DevBuf> pcodes, pscales, pzeros, U16, V16;
@@ -226,6 +227,7 @@ static Member make_member(const hc_matrix_desc& d) {
   m.rec = std::make_shared<DevBuf>();
   m.U = std::make_shared<DevBuf>();
   m.V = std::make_shared<DevBuf>();
+  m.Vn = std::make_shared<DevBuf>();
   m.pcodes = std::make_shared<DevBuf>();
   m.pscales = std::make_shared<DevBuf>();
   m.pzeros = std::make_shared<DevBuf>();
@@ -310,6 +312,12 @@ extern "C" hc_status hc_load_layer(hc_ctx* ctx, const hc_matrix_desc* mats, int3
                                          (uint32_t*)mu.U->p, st));
       CUDA_TRY(hc::launch_repack_v(su.V, up.K, up.r_stored, (uint32_t*)mu.V->p, st));
       CUDA_TRY(hc::launch_repack_v(sg.V, gate.K, gate.r_stored, (uint32_t*)mg.V->p, st));
+      if (up.r_stored > 0) {
+        CUDA_TRY(mu.Vn->alloc((size_t)up.r_stored * up.K * 2));
+        CUDA_TRY(mg.Vn->alloc((size_t)gate.r_stored * gate.K * 2));
+        CUDA_TRY(hc::launch_repack_vn(su.V, up.K, up.r_stored, (uint32_t*)mu.Vn->p, st));
+        CUDA_TRY(hc::launch_repack_vn(sg.V, gate.K, gate.r_stored, (uint32_t*)mg.Vn->p, st));
+      }
       CUDA_TRY(cudaStreamSynchronize(st));
       w.members.clear();
       w.members.push_back(mu);
@@ -346,6 +354,10 @@ extern "C" hc_status hc_load_layer(hc_ctx* ctx, const hc_matrix_desc* mats, int3
     CUDA_TRY(hc::launch_repack_records(src, d.K, d.bits, d.r_stored, rows / hc::kRows, (uint8_t*)m.rec->p,
                                        (uint32_t*)m.U->p, st));
     CUDA_TRY(hc::launch_repack_v(sd.V, d.K, d.r_stored, (uint32_t*)m.V->p, st));
+    if (d.r_stored > 0) {
+      CUDA_TRY(m.Vn->alloc((size_t)d.r_stored * d.K * 2));
+      CUDA_TRY(hc::launch_repack_vn(sd.V, d.K, d.r_stored, (uint32_t*)m.Vn->p, st));
+    }
     s = build_prefill(m, sd, st);
     if (s != HC_OK) return s;
     CUDA_TRY(cudaStreamSynchronize(st));   // staged temporaries die at scope end
@@ -382,10 +394,35 @@ extern "C" int64_t hc_window_rows(hc_ctx* ctx, int32_t layer, int32_t kind, int3
 
 namespace hc {
 
+// t forwarding target: the next window, fed by this window's output columns [lo, hi)
+struct FwdSpec {
+  Window* next = nullptr;
+  int lo = 0, hi = 0;
+};
+
+static int window_chunks(const Window& w) {
+  int c = 0;
+  for (const Member& m : w.members) c += (m.r_alloc + 15) / 16;
+  return c;
+}
+
+// Whether `next` can receive t from the kernel producing its input (DArgs::fwd / t_in).
+static bool can_forward(const Window& next) {
+  const char* e = getenv("HC_TFWD");                  // "0": every window computes its own V·x (A/B testing)
+  if (e && e[0] == '0') return false;
+  const int c = window_chunks(next);
+  if (c == 0 || c > kFwdMax || (int)next.members.size() > kMaxMembers) return false;
+  for (const Member& m : next.members)
+    if (m.r_alloc > 0 && !(m.Vn && m.Vn->p)) return false;
+  return true;
+}
+
 // Launch arguments of one window (also used by the stack driver).
 static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int B, void* y, int y_bf16,
-                             const void* resid, int ld_resid, DArgs& a, int& grid) {
+                             const void* resid, int ld_resid, DArgs& a, int& grid, bool t_in = false,
+                             const FwdSpec* fw = nullptr) {
   std::memset(&a, 0, sizeof(a));
+  a.t_in = t_in ? 1 : 0;
   const Member& m0 = w.members.front();
   a.K = m0.K; a.G = m0.K / kGroup; a.B = B;
   a.x = (const uint16_t*)x; a.ldx = ldx; a.y = y; a.y_bf16 = y_bf16;
@@ -447,10 +484,30 @@ static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int
     if (w.xprep.bytes < need) CUDA_TRY(w.xprep.alloc(need));
     a.x16 = (const uint16_t*)w.xprep.p;
   }
-  const auto key = std::make_tuple(m0.bits, B, a.K, a.n_chunks, 0);
+  if (fw && fw->next) {
+    Window& nx = *fw->next;
+    const int nch = window_chunks(nx);
+    if (nx.ws_chunks < 0 || !nx.tacc.p) return fail(HC_ERR_STATE, "t forwarding: next window workspace missing");
+    a.fwd = 1;
+    a.fwd_lo = fw->lo;
+    a.fwd_hi = fw->hi;
+    a.fwd_chunks = nch;
+    a.fwd_nm = (int)nx.members.size();
+    int cb = 0;
+    for (int i = 0; i < a.fwd_nm; ++i) {
+      const Member& mm = nx.members[i];
+      a.fwd_cb[i] = cb;
+      a.fwd_vn[i] = (const uint4*)(mm.Vn ? mm.Vn->p : nullptr);
+      a.fwd_rs[i] = mm.r_stored / 16;
+      cb += (mm.r_alloc + 15) / 16;
+    }
+    a.fwd_cb[a.fwd_nm] = cb;
+    a.fwd_tacc = (long long*)nx.tacc.p;
+  }
+  const auto key = std::make_tuple(m0.bits, B, a.K, a.n_chunks, a.fwd ? a.fwd_chunks : 0);
   auto it = ctx->max_ctas.find(key);
   if (it == ctx->max_ctas.end())
-    it = ctx->max_ctas.emplace(key, decode_max_ctas(m0.bits, B, a.K, a.n_chunks)).first;
+    it = ctx->max_ctas.emplace(key, decode_max_ctas(m0.bits, B, a.K, a.n_chunks, a.fwd ? a.fwd_chunks : 0)).first;
   if (it->second <= 0) return fail(HC_ERR_RUNTIME, "decode kernel cannot be resident on this device");
   const int n_items = a.n_rb;
   static const int per_sm = [] { const char* e = getenv("HC_DECODE_CTAS_PER_SM"); return e ? atoi(e) : 0; }();
@@ -460,10 +517,11 @@ static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int
 }
 
 static hc_status launch_window(hc_ctx* ctx, Window& w, const void* x, int ldx, int B, void* y, int y_bf16,
-                               const void* resid, int ld_resid, cudaStream_t st) {
+                               const void* resid, int ld_resid, cudaStream_t st, bool t_in = false,
+                               const FwdSpec* fw = nullptr) {
   DArgs a;
   int grid = 0;
-  hc_status s = window_args(ctx, w, x, ldx, B, y, y_bf16, resid, ld_resid, a, grid);
+  hc_status s = window_args(ctx, w, x, ldx, B, y, y_bf16, resid, ld_resid, a, grid, t_in, fw);
   if (s != HC_OK) return s;
   if (a.x16)
     CUDA_TRY(launch_xprep(a.x, a.ldx, B, a.K, w.members.front().bits, (uint16_t*)a.x16, st));
@@ -772,10 +830,17 @@ extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, voi
       LayerPlan& p = plan[l];
       uint16_t* hout = (l + 1 == plan.size()) ? (uint16_t*)dy : h;
       if (!tp) {
-        cap = hc::launch_window(ctx, *p.qkv, hin, d, B, qkv, 1, nullptr, 0, cs);                 // q | k | v
-        if (cap == HC_OK) cap = hc::launch_window(ctx, *p.o, qkv, nqkv, B, h1, 1, hin, d, cs);   // h1 = h + O(q)
-        if (cap == HC_OK) cap = hc::launch_window(ctx, *p.ug, h1, d, B, mm, 1, nullptr, 0, cs);  // m = silu(g)·u
-        if (cap == HC_OK) cap = hc::launch_window(ctx, *p.down, mm, f, B, hout, 1, h1, d, cs);   // h' = h1 + DOWN(m)
+        // t forwarding: each window's epilogue accumulates the next window's t = V·x from
+        // the outputs it writes, so only layer 0's QKV computes its own V·x
+        const bool f_o = hc::can_forward(*p.o), f_ug = hc::can_forward(*p.ug), f_dn = hc::can_forward(*p.down);
+        const bool f_q = l + 1 < plan.size() && hc::can_forward(*plan[l + 1].qkv);
+        const bool t_q = l > 0 && hc::can_forward(*p.qkv);
+        const hc::FwdSpec s_o{f_o ? p.o : nullptr, 0, d}, s_ug{f_ug ? p.ug : nullptr, 0, d},
+            s_dn{f_dn ? p.down : nullptr, 0, f}, s_q{f_q ? plan[l + 1].qkv : nullptr, 0, d};
+        cap = hc::launch_window(ctx, *p.qkv, hin, d, B, qkv, 1, nullptr, 0, cs, t_q, &s_o);                 // q | k | v
+        if (cap == HC_OK) cap = hc::launch_window(ctx, *p.o, qkv, nqkv, B, h1, 1, hin, d, cs, f_o, &s_ug);   // h1 = h + O(q)
+        if (cap == HC_OK) cap = hc::launch_window(ctx, *p.ug, h1, d, B, mm, 1, nullptr, 0, cs, f_ug, &s_dn); // m = silu(g)·u
+        if (cap == HC_OK) cap = hc::launch_window(ctx, *p.down, mm, f, B, hout, 1, h1, d, cs, f_dn, &s_q);   // h' = h1 + DOWN(m)
       } else {                                                   // column-sharded: gather every window
         cap = tp_window(ctx, *p.qkv, hin, d, B, qkv, nullptr, 0, cs);
         if (cap == HC_OK) cap = tp_window(ctx, *p.o, qkv, nqkv, B, h1, hin, d, cs);

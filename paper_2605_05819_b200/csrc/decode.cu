@@ -54,13 +54,16 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
   const int gid = lane >> 2, tig = lane & 3;
   constexpr int kBlk = kTPB * kTileMax;
   constexpr int kEpi = kDecodeWarps;          // epilogue warp index
-  float* red = reinterpret_cast<float*>(smem + (size_t)kDecodeWarps * kNBuf * kBlk);        // [2][8][32][8]
-  uint4* ubuf = reinterpret_cast<uint4*>(red + 2 * kDecodeWarps * 32 * 8);                   // [2][kUPre][32]
+  float* red = reinterpret_cast<float*>(smem + (size_t)kDecodeWarps * kNBuf * kBlk);        // [2][8][32][4·NB8]
+  uint4* ubuf = reinterpret_cast<uint4*>(red + 2 * kDecodeWarps * 32 * 4 * NB8);             // [2][kUPre][32]
   uint64_t* bars_all = reinterpret_cast<uint64_t*>(ubuf + 2 * kUPre * 32);
   uint64_t* ubar = bars_all + kDecodeWarps * kNBuf;       // [2]
   uint64_t* xbar = ubar + 2;
-  float4* tsm = reinterpret_cast<float4*>(xbar + 2);      // [n_chunks][NB8][32] t fragments
-  uint16_t* xs = reinterpret_cast<uint16_t*>(tsm + (size_t)a.n_chunks * NB8 * 32);
+  uint64_t* fbar = xbar + 1;                              // t forwarding: Vn blocks landed
+  uint4* tsm = reinterpret_cast<uint4*>(xbar + 2);       // [n_chunks][NB8][32] t hi|lo fragments
+  uint16_t* xt = reinterpret_cast<uint16_t*>(tsm + (size_t)a.n_chunks * NB8 * 32);   // [16 k][16 cols] fwd x tile
+  uint4* fbuf = reinterpret_cast<uint4*>(xt + 256);                                  // [fwd_chunks][32] Vn fragments
+  uint16_t* xs = reinterpret_cast<uint16_t*>(fbuf + (size_t)(a.fwd ? a.fwd_chunks : 0) * 32);
   const int xs_ld = a.K + 32;   // +64 B per row: consecutive batch rows fall in disjoint banks
 
   if (lane == 0) {
@@ -68,7 +71,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
 #pragma unroll
       for (int s = 0; s < kNBuf; ++s) mbar_init(&bars_all[warp * kNBuf + s], 1);
     } else {
-      mbar_init(&ubar[0], 1); mbar_init(&ubar[1], 1); mbar_init(xbar, 1);
+      mbar_init(&ubar[0], 1); mbar_init(&ubar[1], 1); mbar_init(xbar, 1); mbar_init(fbar, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -78,7 +81,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
 
   const int n_items = a.n_rb;
   // the V·x share lives on the first CTAs (started first), ~kVPerWarp 1 KB pieces per tile warp
-  const int n_vp = a.n_chunks * 4 * a.G;
+  const int n_vp = a.t_in ? 0 : a.n_chunks * 4 * a.G;   // t_in: t already accumulated by the producer of x
   const int n_vctas = n_vp == 0 ? 0 : min((int)gridDim.x, (n_vp + kDecodeWarps * kVPerWarp - 1) / (kDecodeWarps * kVPerWarp));
   const int n_vwarps = n_vctas * kDecodeWarps;            // v_done target
 
@@ -107,6 +110,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
       }
     }
     unsigned u_phase = 0;   // bit p = phase of ubar[p]
+    unsigned f_phase = 0;
     bool t_ready = false;
     int my_rb = 0;
     int k = 0;
@@ -122,18 +126,47 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
           (void)ld_acquire(&a.cnt[0]);
         }
         __syncwarp();
+        // kept as the bf16 hi + lo B-fragments of the U·t mma (fp32-accurate), ranks >= r masked to 0
 #pragma unroll 4
         for (int cc = 0; cc < a.n_chunks; ++cc) {
+          const DMember& mt = a.m[member_of_chunk(a, cc)];
+          const int r0 = 16 * (cc - mt.chunk_begin) + 2 * tig;
 #pragma unroll
           for (int nb = 0; nb < NB8; ++nb) {
             const long long* src = a.tacc + ((size_t)cc * 16 + ((gid + 8 * nb) & 15)) * 16 + 2 * tig;
-            const long long t0 = __ldcg(src), t1 = __ldcg(src + 1), t8 = __ldcg(src + 8), t9 = __ldcg(src + 9);
-            tsm[((size_t)cc * NB8 + nb) * 32 + lane] =
-                make_float4((float)t0 * kTInv, (float)t1 * kTInv, (float)t8 * kTInv, (float)t9 * kTInv);
+            const long long tr[4] = {__ldcg(src), __ldcg(src + 1), __ldcg(src + 8), __ldcg(src + 9)};
+            uint32_t hi[2], lo[2];
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const float ta = (r0 + 8 * hh < mt.r) ? (float)tr[2 * hh] * kTInv : 0.f;
+              const float tb = (r0 + 8 * hh + 1 < mt.r) ? (float)tr[2 * hh + 1] * kTInv : 0.f;
+              const uint32_t ha = f32_to_bf16_rn(ta), hb = f32_to_bf16_rn(tb);
+              hi[hh] = ha | (hb << 16);
+              lo[hh] = f32_to_bf16_rn(ta - bf16_bits_to_f32(ha)) | (f32_to_bf16_rn(tb - bf16_bits_to_f32(hb)) << 16);
+            }
+            tsm[((size_t)cc * NB8 + nb) * 32 + lane] = make_uint4(hi[0], hi[1], lo[0], lo[1]);
           }
         }
         __syncwarp();
         t_ready = true;
+      }
+      // t forwarding: this item's outputs are x of the next window at k = n0 - fwd_lo .. (16 or 8 of them);
+      // fetch the next window's natural-k V fragments of that 16-k block while the tile warps work
+      const int f_n0 = a.glue ? m.row_off + (item - m.rb_begin) * 8 : m.row_off + (item - m.rb_begin) * kRows;
+      const bool f_on = a.fwd && f_n0 >= a.fwd_lo && f_n0 < a.fwd_hi;
+      if (f_on && lane == 0) {
+        const int kb = (f_n0 - a.fwd_lo) >> 4;
+        mbar_expect_tx(fbar, (uint32_t)a.fwd_chunks * 512u);
+        for (int i = 0; i < a.fwd_nm; ++i) {
+          const int nc = a.fwd_cb[i + 1] - a.fwd_cb[i];
+          if (nc > 0)
+            bulk_copy(fbuf + a.fwd_cb[i] * 32, a.fwd_vn[i] + (size_t)kb * a.fwd_rs[i] * 32, (uint32_t)nc * 512u, fbar,
+                      evict_first_policy());
+        }
+      }
+      if (f_on) {                                        // zero the x tile (cols >= B and the other 8 k stay 0)
+        reinterpret_cast<uint4*>(xt)[lane] = make_uint4(0u, 0u, 0u, 0u);
+        __syncwarp();
       }
       asm volatile("bar.sync %0, %1;" ::"r"(1 + par), "n"(kDecodeThreads) : "memory");   // FULL[par]
       float fin[NB8][4];
@@ -143,7 +176,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
         for (int e = 0; e < 4; ++e) fin[nb][e] = 0.f;
 #pragma unroll
       for (int w = 0; w < kDecodeWarps; ++w) {            // fixed order: deterministic
-        const float* src = red + ((size_t)(par * kDecodeWarps + w) * 32 + lane) * 8;
+        const float* src = red + ((size_t)(par * kDecodeWarps + w) * 32 + lane) * 4 * NB8;
 #pragma unroll
         for (int nb = 0; nb < NB8; ++nb) {
           const float4 v = *reinterpret_cast<const float4*>(src + 4 * nb);
@@ -180,20 +213,9 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
             if (16 * c >= mt.r) continue;
 #pragma unroll
             for (int nb = 0; nb < NB8; ++nb) {
-              const float4 t4 = tsm[((size_t)(mt.chunk_begin + c) * NB8 + nb) * 32 + lane];
-              const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
-              uint32_t hi[2], lo[2];
-#pragma unroll
-              for (int hh = 0; hh < 2; ++hh) {
-                const int rank0 = 16 * c + 2 * tig + 8 * hh;
-                const float ta = (rank0 < mt.r) ? tv[2 * hh] : 0.f;
-                const float tb = (rank0 + 1 < mt.r) ? tv[2 * hh + 1] : 0.f;
-                const uint32_t ha = f32_to_bf16_rn(ta), hb = f32_to_bf16_rn(tb);
-                hi[hh] = ha | (hb << 16);
-                lo[hh] = f32_to_bf16_rn(ta - bf16_bits_to_f32(ha)) | (f32_to_bf16_rn(tb - bf16_bits_to_f32(hb)) << 16);
-              }
-              mma16816(comp[h][nb], af, hi[0], hi[1]);
-              mma16816(comp[h][nb], af, lo[0], lo[1]);
+              const uint4 q = tsm[((size_t)(mt.chunk_begin + c) * NB8 + nb) * 32 + lane];
+              mma16816(comp[h][nb], af, q.x, q.y);     // U·t_hi
+              mma16816(comp[h][nb], af, q.z, q.w);     // U·t_lo
             }
           }
         }
@@ -210,10 +232,13 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
             const float gt = fin[nb][e + 2] + comp[1][nb][e + 2];
             const float v = up * (gt / (1.f + __expf(-gt)));
             const int n = m.row_off + rbl * 8 + gid;
-            if (a.y_bf16)
-              reinterpret_cast<uint16_t*>(a.y)[(size_t)b * a.ldy + n] = (uint16_t)f32_to_bf16_rn(v);
-            else
+            if (a.y_bf16) {
+              const uint16_t bits = (uint16_t)f32_to_bf16_rn(v);
+              reinterpret_cast<uint16_t*>(a.y)[(size_t)b * a.ldy + n] = bits;
+              if (f_on) xt[(((f_n0 - a.fwd_lo) & 15) + gid) * 16 + b] = bits;
+            } else {
               reinterpret_cast<float*>(a.y)[(size_t)b * a.ldy + n] = v;
+            }
           }
       } else {
 #pragma unroll
@@ -225,11 +250,45 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
             const int n = m.row_off + rbl * kRows + gid + 8 * (e >> 1);
             float v = fin[nb][e] + comp[0][nb][e];
             if (a.resid) v += bf16_bits_to_f32(a.resid[(size_t)b * a.ld_resid + n]);
-            if (a.y_bf16)
-              reinterpret_cast<uint16_t*>(a.y)[(size_t)b * a.ldy + n] = (uint16_t)f32_to_bf16_rn(v);
-            else
+            if (a.y_bf16) {
+              const uint16_t bits = (uint16_t)f32_to_bf16_rn(v);
+              reinterpret_cast<uint16_t*>(a.y)[(size_t)b * a.ldy + n] = bits;
+              if (f_on) xt[(gid + 8 * (e >> 1)) * 16 + b] = bits;
+            } else {
               reinterpret_cast<float*>(a.y)[(size_t)b * a.ldy + n] = v;
+            }
           }
+      }
+      if (f_on) {
+        // t_next[c][col][rank] += Σ_{k in this block} Vn[c][rank][k] · x[col][k]  (bf16 mma, fp32, then
+        // 2^-28 fixed point: integer adds, so the sum is independent of the order items arrive)
+        __syncwarp();
+        uint32_t b0[NB8], b1[NB8];
+#pragma unroll
+        for (int nb = 0; nb < NB8; ++nb) {
+          const int col = gid + 8 * nb;
+          b0[nb] = (uint32_t)xt[(2 * tig) * 16 + col] | ((uint32_t)xt[(2 * tig + 1) * 16 + col] << 16);
+          b1[nb] = (uint32_t)xt[(2 * tig + 8) * 16 + col] | ((uint32_t)xt[(2 * tig + 9) * 16 + col] << 16);
+        }
+        while (!mbar_try_wait(fbar, f_phase)) {}
+        f_phase ^= 1u;
+        for (int cc = 0; cc < a.fwd_chunks; ++cc) {
+          const uint4 v4 = fbuf[cc * 32 + lane];
+          const uint32_t af[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+          for (int nb = 0; nb < NB8; ++nb) {
+            float tp[4] = {0.f, 0.f, 0.f, 0.f};
+            mma16816(tp, af, b0[nb], b1[nb]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int col = 2 * tig + (e & 1) + 8 * nb, rank = gid + 8 * (e >> 1);
+              if (col < a.B)
+                atomicAdd(reinterpret_cast<unsigned long long*>(a.fwd_tacc + ((size_t)cc * 16 + col) * 16 + rank),
+                          (unsigned long long)__float2ll_rn(tp[e] * kTScale));
+            }
+          }
+        }
+        __syncwarp();                                    // fbuf / xt reused by the next item
       }
       ++my_rb;
     }
@@ -397,7 +456,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
     }
     // ---- hand the partial sums to the epilogue warp
     if (k >= 2) asm volatile("bar.sync %0, %1;" ::"r"(3 + par), "n"(kDecodeThreads) : "memory");   // EMPTY[par]
-    float* rb_ = red + ((size_t)(par * kDecodeWarps + warp) * 32 + lane) * 8;
+    float* rb_ = red + ((size_t)(par * kDecodeWarps + warp) * 32 + lane) * 4 * NB8;
 #pragma unroll
     for (int nb = 0; nb < NB8; ++nb)
       *reinterpret_cast<float4*>(rb_ + 4 * nb) = make_float4(tot[nb][0], tot[nb][1], tot[nb][2], tot[nb][3]);
@@ -405,11 +464,11 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
   }
 }
 
-static size_t decode_smem_bytes(bool xs, int B, int K, int n_chunks) {
+static size_t decode_smem_bytes(bool xs, int B, int K, int n_chunks, int fwd_chunks) {
   const int nb8 = B > 8 ? 2 : 1;
-  size_t s = (size_t)kDecodeWarps * kNBuf * kTPB * kTileMax + 2 * kDecodeWarps * 32 * 8 * sizeof(float) +
+  size_t s = (size_t)kDecodeWarps * kNBuf * kTPB * kTileMax + 2 * kDecodeWarps * 32 * 4 * nb8 * sizeof(float) +
              2 * kUPre * 32 * 16 + (kDecodeWarps * kNBuf + 4) * sizeof(uint64_t) +
-             (size_t)n_chunks * nb8 * 32 * 16;
+             (size_t)n_chunks * nb8 * 32 * 16 + 512 + (size_t)fwd_chunks * 512;
   if (xs) s += (size_t)B * (K + 32) * 2;
   return s;
 }
@@ -459,7 +518,7 @@ cudaError_t launch_xprep(const uint16_t* x, int ldx, int B, int K, int bits, uin
 
 template <int BITS, int NB8, bool XS>
 static cudaError_t launch_t(const DArgs& a, int grid, cudaStream_t st) {
-  const size_t smem = decode_smem_bytes(XS, a.B, a.K, a.n_chunks);
+  const size_t smem = decode_smem_bytes(XS, a.B, a.K, a.n_chunks, a.fwd ? a.fwd_chunks : 0);
   if (smem > kSmemOptin) return cudaErrorInvalidConfiguration;
   static bool attr = false;
   if (!attr) {
@@ -482,8 +541,8 @@ static cudaError_t launch_t(const DArgs& a, int grid, cudaStream_t st) {
 }
 
 template <int BITS, int NB8, bool XS>
-static int max_ctas_t(int B, int K, int n_chunks) {
-  const size_t smem = decode_smem_bytes(XS, B, K, n_chunks);
+static int max_ctas_t(int B, int K, int n_chunks, int fwd_chunks) {
+  const size_t smem = decode_smem_bytes(XS, B, K, n_chunks, fwd_chunks);
   cudaFuncSetAttribute(decode_kernel<BITS, NB8, XS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)kSmemOptin);
   int per_sm = 0, dev = 0, sms = 0;
@@ -513,9 +572,9 @@ cudaError_t launch_decode(const DArgs& a, int bits, int grid, cudaStream_t st) {
   return cudaErrorInvalidValue;
 }
 
-int decode_max_ctas(int bits, int B, int K, int n_chunks) {
+int decode_max_ctas(int bits, int B, int K, int n_chunks, int fwd_chunks) {
   const int a_B = B, a_K = K;
-  HC_DISPATCH(max_ctas_t, B, K, n_chunks);
+  HC_DISPATCH(max_ctas_t, B, K, n_chunks, fwd_chunks);
   return 0;
 }
 

@@ -21,7 +21,8 @@ constexpr int kMaxChunks = 32;           // Σ ceil(r_m/16) over a window's memb
 constexpr int kTPB = HC_DEC_TPB;         // tiles per bulk-copy block
 constexpr int kNBuf = HC_DEC_NBUF;       // block buffers per warp (kNBuf - 1 blocks in flight while one computes)
 constexpr int kTileMax = 1088;           // >= rec_bytes(4) = 1072, >= 1 KB V piece
-constexpr int kUPre = 4;                 // U chunks (16 ranks each) staged in smem per item
+constexpr int kUPre = 8;                 // U chunks (16 ranks each) staged in smem per item (r <= 128)
+constexpr int kFwdMax = 24;              // next-window rank chunks a launch can forward t to (smem: 512 B each)
 
 struct DMember {
   const uint8_t* rec;   // [n_rb][G][rec_bytes]          (layout.h)
@@ -57,9 +58,9 @@ struct DArgs {
   int fwd;              // 0 off, 1 on
   int fwd_lo, fwd_hi;   // output columns of this window that are the next window's x (k = col - fwd_lo)
   int fwd_chunks;       // Σ ceil(r/16) over the next window's members
-  const uint4* fwd_vn[kMaxMembers];   // natural-k V fragments [r_stored/16][K/16][32] of the next members
-  int fwd_cb[kMaxMembers + 1];        // chunk ranges: member i owns chunks [fwd_cb[i], fwd_cb[i+1])
-  int fwd_kb;           // next window's K / 16 (row stride of a chunk in fwd_vn, in 16-k blocks)
+  const uint4* fwd_vn[kMaxMembers];   // natural-k V fragments [K/16][r_stored/16][32] of the next members
+  int fwd_cb[kMaxMembers + 1];        // chunk ranges: member i owns next-window chunks [fwd_cb[i], fwd_cb[i+1])
+  int fwd_rs[kMaxMembers];            // r_stored / 16 of the next members (chunk stride of fwd_vn)
   int fwd_nm;           // next window's member count
   long long* fwd_tacc;  // next window's t accumulators
   long long* tacc;      // [n_chunks][16 batch][16 ranks] t = V·x in 2^-28 fixed point (self-resetting)
@@ -73,6 +74,6 @@ bool decode_stages_x(int B, int K);
 // x' (fp16, pre-scaled per the code layout of `bits`) for a !XS decode launch.
 cudaError_t launch_xprep(const uint16_t* x, int ldx, int B, int K, int bits, uint16_t* x16, cudaStream_t st);
 // Max co-resident CTAs of the decode kernel on this device (persistent grid size).
-int decode_max_ctas(int bits, int B, int K, int n_chunks);
+int decode_max_ctas(int bits, int B, int K, int n_chunks, int fwd_chunks);
 
 }  // namespace hc

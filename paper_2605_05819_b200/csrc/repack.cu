@@ -71,14 +71,15 @@ __global__ void repack_v_kernel(const uint16_t* __restrict__ V, int K, int r_sto
   }
 }
 
-// Vn: [c][kb][lane][4 regs]; reg i of lane: rank 16c + gid + 8(i&1), k = 16kb + 2tig + 8(i>>1) + {0,1}
+// Vn: [kb][c][lane][4 regs]; reg i of lane: rank 16c + gid + 8(i&1), k = 16kb + 2tig + 8(i>>1) + {0,1}
+// (k-block major: the chunks of one 16-k block are contiguous, one bulk copy per member)
 __global__ void repack_vn_kernel(const uint16_t* __restrict__ V, int K, int r_stored, uint32_t* __restrict__ out) {
   const int KB = K / 16, nc = r_stored / 16;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= (long long)nc * KB * 32) return;
   const int lane = (int)(tid & 31);
   const long long ck = tid >> 5;
-  const int kb = (int)(ck % KB), c = (int)(ck / KB);
+  const int c = (int)(ck % nc), kb = (int)(ck / nc);
   for (int i = 0; i < 4; ++i) {
     const size_t rank = (size_t)(16 * c + (lane >> 2) + 8 * (i & 1));
     const int k = 16 * kb + 2 * (lane & 3) + 8 * (i >> 1);

@@ -17,7 +17,7 @@ cudaError_t launch_repack_records(const RepackSrc& src, int K, int bits, int r_s
                                   uint32_t* u_out, cudaStream_t st);
 // V fragments [c][g][j][lane][4] of one matrix.
 cudaError_t launch_repack_v(const uint16_t* V, int K, int r_stored, uint32_t* v_out, cudaStream_t st);
-// Natural-k V fragments [c][K/16][lane][4] (standard m16n8k16 A layout: ranks = rows, 16 consecutive k)
+// Natural-k V fragments [K/16][c][lane][4] (standard m16n8k16 A layout: ranks = rows, 16 consecutive k)
 // for t forwarding (DArgs::fwd_vn).
 cudaError_t launch_repack_vn(const uint16_t* V, int K, int r_stored, uint32_t* out, cudaStream_t st);
 }  // namespace hc
