@@ -165,6 +165,21 @@ hc_status hc_compensated_linear(hc_ctx* ctx, int32_t layer, int32_t window_kind,
  * HC_ERR_STATE if a layer lacks a window or its UPGATE window is not SiLU-fused. */
 hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, void* y, void* stream);
 
+/* Grouped MoE expert layer (C3; "Y_MoE = Σ_e g_e E_e(X)"):
+ *   y[t, :] = Σ_{j<topk} topk_gate[t, j] · DOWN_e(m),  m = bf16(silu(GATE_e(x_t)) ⊙ UP_e(x_t)),
+ *   e = topk_idx[t, j], every product compensated at its own rank.
+ * The layer's experts are windows (layer, HC_WIN_UPGATE, e) loaded with HC_GLUE_SILU_MUL (slot 0 up,
+ * slot 1 gate) and (layer, HC_WIN_DOWN, e) for e = 0 .. E-1 (E = first missing id); all experts share
+ * shapes and bits and are unsharded.  x: bf16 [T][K]; topk_idx: int32 [T][topk] (ids outside
+ * [0, E) are skipped); topk_gate: fp32 [T][topk] (used as given); y: fp32 [T][D].  1 <= T <= 1024,
+ * 1 <= topk <= 16.  One launch per stage over all activated experts: route (group the T·topk
+ * (token, expert) rows by expert, tokens ascending), gather + pre-scale x, rank projection
+ * t = V·x, grouped compensated GEMV (UPGATE with the SiLU glue), the same for DOWN, combine in slot
+ * order.  Deterministic.  Host pointers are staged (the call then synchronises the stream).
+ * HC_ERR_STATE if expert 0 is missing or a window is not shaped as above. */
+hc_status hc_moe_forward(hc_ctx* ctx, int32_t layer, const void* x, int32_t T, const int32_t* topk_idx,
+                         const float* topk_gate, int32_t topk, void* y, void* stream);
+
 /* Column sharding across GPUs.  Rank 0 calls hc_nccl_unique_id and shares the 128
  * bytes with every rank (e.g. through torch.distributed); each rank then calls hc_set_comm with its
  * rank and the world size (ncclCommInitRank on the context's device; NCCL is loaded at run time).

@@ -180,6 +180,14 @@ class Context:
         check(lib().hc_stack_forward(self._h, _ptr(x), int(B), _ptr(y), _stream(stream)))
         return y
 
+    def moe_forward(self, layer, x, topk_idx, topk_gate, y, stream=None):
+        """hc_moe_forward: grouped MoE expert layer.  x bf16 [T, K]; topk_idx int32 [T, k];
+        topk_gate fp32 [T, k]; y fp32 [T, D] (device tensors or host arrays)."""
+        T, k = int(topk_idx.shape[0]), int(topk_idx.shape[1])
+        check(lib().hc_moe_forward(self._h, int(layer), _ptr(x), T, _ptr(topk_idx), _ptr(topk_gate), k, _ptr(y),
+                                   _stream(stream)))
+        return y
+
     def compensated_linear(self, layer, window, x, y, B=None, expert=-1, out_dtype=OUT_F32, stream=None):
         """y[b, :] = concat_m ( deq(W_m)·x_b + U_m[:, :r_m]·(V_m[:r_m, :]·x_b) ).
         x: bf16 [B, K] (torch bf16 / uint16 bits, device or host); y: [B, rows] fp32 or bf16."""

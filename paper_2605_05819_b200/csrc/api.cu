@@ -14,6 +14,7 @@
 #include "decode.h"
 #include "prefill.h"
 #include "stack.h"
+#include "moe.h"
 #include "hcinfer.h"
 #include "layout.h"
 #include "repack_kernels.h"
@@ -97,7 +98,18 @@ struct hc_ctx {
   hc::Comm* comm = nullptr;
   int rank = 0, world = 1;
   DevBuf t_send, t_gather;
-  void invalidate_graphs() { graphs.clear(); }
+  // grouped MoE (hc_moe_forward): per-layer device expert tables, rebuilt after load / set_rank
+  struct MoECache {
+    DevBuf ex_ug, ex_dn;
+    int E = 0, K = 0, F = 0, D = 0, bits = 0, t_ug = 32, t_dn = 32;
+    bool valid = false;
+  };
+  std::map<int, MoECache> moe;
+  DevBuf moe_ws, moe_idx, moe_gate;
+  void invalidate_graphs() {
+    graphs.clear();
+    for (auto& kv : moe) kv.second.valid = false;
+  }
 };
 
 #define CUDA_TRY(expr)                                                                       \
@@ -612,6 +624,120 @@ extern "C" hc_status hc_compensated_linear(hc_ctx* ctx, int32_t layer, int32_t k
   if (s != HC_OK) return s;
   if (hy) CUDA_TRY(cudaMemcpyAsync(y, dy, yb, cudaMemcpyDeviceToHost, st));
   if (hx || hy) CUDA_TRY(cudaStreamSynchronize(st));
+  return HC_OK;
+}
+
+// ------------------------------------------------------------------ grouped MoE
+static hc_status moe_tables(hc_ctx* ctx, int layer, hc_ctx::MoECache*& out) {
+  hc_ctx::MoECache& c = ctx->moe[layer];
+  out = &c;
+  if (c.valid) return HC_OK;
+  std::vector<hc::MoEExpert> ug, dn;
+  int E = 0, cu = 1, cd = 1;
+  for (;; ++E) {
+    auto fu = ctx->windows.find(Key{layer, HC_WIN_UPGATE, E});
+    auto fd = ctx->windows.find(Key{layer, HC_WIN_DOWN, E});
+    if (fu == ctx->windows.end() || fd == ctx->windows.end()) break;
+    Window& wu = fu->second;
+    Window& wd = fd->second;
+    if (wu.glue != HC_GLUE_SILU_MUL || wu.members.size() != 2 || wd.members.size() != 1)
+      return fail(HC_ERR_STATE, "hc_moe_forward: expert %d of layer %d needs a SiLU-fused UPGATE window and one DOWN matrix", E, layer);
+    const Member& up = wu.members[0];
+    const Member& gt = wu.members[1];
+    const Member& d = wd.members[0];
+    if (E == 0) { c.K = up.K; c.F = up.rows(); c.D = d.rows(); c.bits = up.bits; }
+    if (up.K != c.K || up.rows() != c.F || d.K != c.F || d.rows() != c.D || up.bits != c.bits || d.bits != c.bits ||
+        up.rows() != up.N || d.rows() != d.N)
+      return fail(HC_ERR_CONFIG, "hc_moe_forward: experts of layer %d differ in shape / bits (or are sharded)", layer);
+    hc::MoEExpert a{}, b{};
+    a.rec = (const uint8_t*)up.rec->p; a.U = (const uint4*)up.U->p;
+    a.Vn[0] = (const uint4*)(up.Vn ? up.Vn->p : nullptr); a.Vn[1] = (const uint4*)(gt.Vn ? gt.Vn->p : nullptr);
+    a.r[0] = up.r_alloc; a.r[1] = gt.r_alloc; a.rs[0] = up.r_stored; a.rs[1] = gt.r_stored;
+    b.rec = (const uint8_t*)d.rec->p; b.U = (const uint4*)d.U->p;
+    b.Vn[0] = (const uint4*)(d.Vn ? d.Vn->p : nullptr); b.r[0] = d.r_alloc; b.rs[0] = d.r_stored;
+    cu = std::max(cu, std::max((up.r_alloc + 15) / 16, (gt.r_alloc + 15) / 16));
+    cd = std::max(cd, (d.r_alloc + 15) / 16);
+    ug.push_back(a);
+    dn.push_back(b);
+  }
+  if (E == 0) return fail(HC_ERR_STATE, "hc_moe_forward: layer %d has no expert 0 (UPGATE + DOWN windows)", layer);
+  if (E > 256) return fail(HC_ERR_CONFIG, "hc_moe_forward: %d experts > 256", E);
+  c.E = E;
+  c.t_ug = 32 * cu;
+  c.t_dn = 32 * cd;
+  CUDA_TRY(c.ex_ug.alloc(ug.size() * sizeof(hc::MoEExpert)));
+  CUDA_TRY(c.ex_dn.alloc(dn.size() * sizeof(hc::MoEExpert)));
+  CUDA_TRY(cudaMemcpy(c.ex_ug.p, ug.data(), ug.size() * sizeof(hc::MoEExpert), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(c.ex_dn.p, dn.data(), dn.size() * sizeof(hc::MoEExpert), cudaMemcpyHostToDevice));
+  c.valid = true;
+  return HC_OK;
+}
+
+extern "C" hc_status hc_moe_forward(hc_ctx* ctx, int32_t layer, const void* x, int32_t T, const int32_t* topk_idx,
+                                    const float* topk_gate, int32_t topk, void* y, void* stream) {
+  if (!ctx) return fail(HC_ERR_STATE, "hc_moe_forward: null context");
+  if (T < 1 || T > 1024) return fail(HC_ERR_CONFIG, "hc_moe_forward: T = %d outside [1, 1024]", T);
+  if (topk < 1 || topk > hc::kMoEMaxK) return fail(HC_ERR_CONFIG, "hc_moe_forward: topk = %d outside [1, %d]", topk, hc::kMoEMaxK);
+  if (!x || !topk_idx || !topk_gate || !y) return fail(HC_ERR_CONFIG, "hc_moe_forward: null pointer");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  hc_ctx::MoECache* c = nullptr;
+  hc_status s = moe_tables(ctx, layer, c);
+  if (s != HC_OK) return s;
+  const int R = T * topk, maxe = c->E + R;
+  // workspace carve (256-byte aligned pieces)
+  size_t off = 0;
+  auto take = [&](size_t bytes) { const size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
+  const size_t o_nr = take(4), o_ne = take(4), o_rt = take((size_t)R * 4), o_tr = take((size_t)R * 4), o_ee = take((size_t)maxe * 4),
+               o_er = take((size_t)maxe * 4), o_ec = take((size_t)maxe * 4), o_xg = take((size_t)R * c->K * 2),
+               o_x16 = take((size_t)R * c->K * 2), o_tug = take((size_t)R * c->t_ug * 4), o_m = take((size_t)R * c->F * 2),
+               o_md = take((size_t)R * c->F * 2), o_tdn = take((size_t)R * c->t_dn * 4), o_do = take((size_t)R * c->D * 4),
+               o_x = take((size_t)T * c->K * 2), o_y = take((size_t)T * c->D * 4);
+  if (ctx->moe_ws.bytes < off) CUDA_TRY(ctx->moe_ws.alloc(off));
+  uint8_t* ws = (uint8_t*)ctx->moe_ws.p;
+  hc::MoERoute rt;
+  rt.n_rows = (int*)(ws + o_nr); rt.n_ent = (int*)(ws + o_ne); rt.row_tok = (int*)(ws + o_rt); rt.tok_row = (int*)(ws + o_tr);
+  rt.ent_e = (int*)(ws + o_ee); rt.ent_row0 = (int*)(ws + o_er); rt.ent_ncol = (int*)(ws + o_ec);
+  // host inputs are staged (stream-ordered); device inputs are used in place
+  const int32_t* didx = topk_idx;
+  const float* dgate = topk_gate;
+  const void* dx = x;
+  void* dy = y;
+  const bool hi = !is_device_ptr(topk_idx), hg = !is_device_ptr(topk_gate), hx = !is_device_ptr(x), hy = !is_device_ptr(y);
+  if (hi) {
+    if (ctx->moe_idx.bytes < (size_t)R * 4) CUDA_TRY(ctx->moe_idx.alloc((size_t)R * 4));
+    CUDA_TRY(cudaMemcpyAsync(ctx->moe_idx.p, topk_idx, (size_t)R * 4, cudaMemcpyHostToDevice, st));
+    didx = (const int32_t*)ctx->moe_idx.p;
+  }
+  if (hg) {
+    if (ctx->moe_gate.bytes < (size_t)R * 4) CUDA_TRY(ctx->moe_gate.alloc((size_t)R * 4));
+    CUDA_TRY(cudaMemcpyAsync(ctx->moe_gate.p, topk_gate, (size_t)R * 4, cudaMemcpyHostToDevice, st));
+    dgate = (const float*)ctx->moe_gate.p;
+  }
+  if (hx) {
+    CUDA_TRY(cudaMemcpyAsync(ws + o_x, x, (size_t)T * c->K * 2, cudaMemcpyHostToDevice, st));
+    dx = ws + o_x;
+  }
+  if (hy) dy = ws + o_y;
+  hc::MoEWin wu{(const hc::MoEExpert*)c->ex_ug.p, c->F / 8, c->K, c->K / hc::kGroup, 1, c->t_ug};
+  hc::MoEWin wd{(const hc::MoEExpert*)c->ex_dn.p, c->D / hc::kRows, c->F, c->F / hc::kGroup, 0, c->t_dn};
+  uint16_t* xg = (uint16_t*)(ws + o_xg);
+  uint16_t* x16 = (uint16_t*)(ws + o_x16);
+  uint16_t* m = (uint16_t*)(ws + o_m);
+  uint16_t* md = (uint16_t*)(ws + o_md);
+  float* tug = (float*)(ws + o_tug);
+  float* tdn = (float*)(ws + o_tdn);
+  float* dout = (float*)(ws + o_do);
+  CUDA_TRY(hc::moe_route(didx, T, topk, c->E, rt, st));
+  CUDA_TRY(hc::moe_prep((const uint16_t*)dx, c->K, c->K, c->bits, 1, rt, R, xg, x16, st));
+  CUDA_TRY(hc::moe_rank_proj(wu, rt, maxe, xg, tug, st));
+  CUDA_TRY(hc::moe_gemv(wu, c->bits, rt, maxe, x16, tug, m, st));                  // m = bf16(silu(gate)·up)
+  CUDA_TRY(hc::moe_prep(m, c->F, c->F, c->bits, 0, rt, R, nullptr, md, st));
+  CUDA_TRY(hc::moe_rank_proj(wd, rt, maxe, m, tdn, st));
+  CUDA_TRY(hc::moe_gemv(wd, c->bits, rt, maxe, md, tdn, dout, st));                // DOWN_e(m) per row, fp32
+  CUDA_TRY(hc::moe_combine(dout, c->D, dgate, T, topk, rt, (float*)dy, st));
+  if (hy) CUDA_TRY(cudaMemcpyAsync(y, dy, (size_t)T * c->D * 4, cudaMemcpyDeviceToHost, st));
+  if (hi || hg || hx || hy) CUDA_TRY(cudaStreamSynchronize(st));
   return HC_OK;
 }
 

@@ -1,0 +1,300 @@
+// Grouped MoE expert path (C3).
+//
+//   y[t] = Σ_j g[t,j] · DOWN_e(m_e),  m_e = bf16(silu(GATE_e(x_t)) ⊙ UP_e(x_t)),  e = topk_idx[t,j],
+//   every product compensated at its own rank (north_star; oracle.linear.moe_forward).
+//
+// Pipeline (one launch each, all activated experts of the layer together — the paper's cross-expert
+// window fusion on the GPU instead of one CPU task per expert):
+//   route     group the T·k (token, expert) pairs by expert (ascending), tokens ascending inside an
+//             expert; entries = chunks of <= 16 rows of one expert (the mma N dimension)
+//   prep      gather x rows per (token, expert) row: bf16 copy (for V·x) and x' = x·2^-fp (fp16)
+//   rank_proj t[row] = V_e·x_row with the natural-k V fragments (one warp per entry, member, 16 ranks;
+//             fixed k order: deterministic)
+//   gemv      items = (entry, row block); 8 warps split the K groups of a row block, each record
+//             decoded exactly as the decode kernel does (w_tile), partials reduced in a fixed order,
+//             U·t (bf16 hi + lo) and the SiLU glue in the epilogue
+//   combine   y[t] = Σ_j g[t,j]·dout[row(t,j)] in slot order j
+#include <cuda_bf16.h>
+
+#include "decode_dev.cuh"
+#include "moe.h"
+
+namespace hc {
+
+namespace {
+
+constexpr int kRouteThreads = 1024;
+constexpr int kMoEWarps = 8;
+
+// Single CTA: T <= 1024 tokens, E <= 256 experts, k <= 16.
+__global__ void moe_route_kernel(const int32_t* __restrict__ idx, int T, int k, int E, MoERoute rt) {
+  extern __shared__ unsigned bm[];                 // [E][W] token bitmaps, W = ceil(T/32)
+  __shared__ int off[257];
+  const int W = (T + 31) / 32;
+  for (int i = threadIdx.x; i < E * W; i += blockDim.x) bm[i] = 0u;
+  __syncthreads();
+  for (int i = threadIdx.x; i < T * k; i += blockDim.x) {
+    const int e = idx[i], t = i / k;
+    if (e >= 0 && e < E) atomicOr(&bm[e * W + (t >> 5)], 1u << (t & 31));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int o = 0, ne = 0;
+    for (int e = 0; e < E; ++e) {
+      int c = 0;
+      for (int w = 0; w < W; ++w) c += __popc(bm[e * W + w]);
+      off[e] = o;
+      for (int r = 0; r < c; r += 16) {
+        rt.ent_e[ne] = e;
+        rt.ent_row0[ne] = o + r;
+        rt.ent_ncol[ne] = min(16, c - r);
+        ++ne;
+      }
+      o += c;
+    }
+    off[E] = o;
+    *rt.n_rows = o;
+    *rt.n_ent = ne;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < T * k; i += blockDim.x) {
+    const int e = idx[i], t = i / k;
+    if (e < 0 || e >= E) { rt.tok_row[i] = -1; continue; }
+    int before = 0;                                 // tokens < t routed to e
+    for (int w = 0; w < (t >> 5); ++w) before += __popc(bm[e * W + w]);
+    before += __popc(bm[e * W + (t >> 5)] & ((1u << (t & 31)) - 1u));
+    const int row = off[e] + before;
+    rt.row_tok[row] = t;
+    rt.tok_row[i] = row;
+  }
+}
+
+template <int BITS>
+__global__ void moe_prep_kernel(const uint16_t* __restrict__ x, int ldx, int K, int gather, MoERoute rt, int R_max,
+                                uint16_t* __restrict__ xg, uint16_t* __restrict__ x16) {
+  const int parts = K / 16;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)R_max * parts) return;
+  const int r = (int)(i / parts), p = (int)(i % parts);
+  if (r >= *rt.n_rows) return;
+  const int src = gather ? rt.row_tok[r] : r;
+  const uint4* s = reinterpret_cast<const uint4*>(x + (size_t)src * ldx + p * 16);
+  const uint4 in[2] = {s[0], s[1]};
+  if (gather) {
+    uint4* d = reinterpret_cast<uint4*>(xg + (size_t)r * K + p * 16);
+    d[0] = in[0]; d[1] = in[1];
+  }
+  uint4 out[2];
+  xprime16<BITS>(in, p & 7, out);                   // 16-element part p & 7 of group p / 8
+  uint4* d = reinterpret_cast<uint4*>(x16 + (size_t)r * K + p * 16);
+  d[0] = out[0]; d[1] = out[1];
+}
+
+// one warp per (entry, member, 16-rank chunk)
+__global__ void moe_rank_proj_kernel(MoEWin w, MoERoute rt, int max_ent, int max_chunks,
+                                     const uint16_t* __restrict__ xg, float* __restrict__ t) {
+  const int lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int per_ent = 2 * max_chunks;
+  if (gw >= (long long)max_ent * per_ent) return;
+  const int ent = (int)(gw / per_ent), rem = (int)(gw % per_ent), mb = rem / max_chunks, c = rem % max_chunks;
+  if (ent >= *rt.n_ent || (mb == 1 && !w.glue)) return;
+  const MoEExpert& ex = w.ex[rt.ent_e[ent]];
+  if (16 * c >= ex.r[mb]) return;
+  const int row0 = rt.ent_row0[ent], ncol = rt.ent_ncol[ent];
+  const int cs = ex.rs[mb] / 16;
+  const uint4* vn = ex.Vn[mb];
+  float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+  const int KB = w.K / 16;
+  for (int kb = 0; kb < KB; ++kb) {
+    const uint4 a4 = __ldg(vn + ((size_t)kb * cs + c) * 32 + lane);
+    const uint32_t af[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) {
+      const int col = gid + 8 * nb;
+      const uint16_t* xr = xg + (size_t)(row0 + (col < ncol ? col : 0)) * w.K + 16 * kb + 2 * tig;
+      const uint32_t b0 = col < ncol ? __ldg(reinterpret_cast<const uint32_t*>(xr)) : 0u;
+      const uint32_t b1 = col < ncol ? __ldg(reinterpret_cast<const uint32_t*>(xr + 8)) : 0u;
+      mma16816(acc[nb], af, b0, b1);
+    }
+  }
+#pragma unroll
+  for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int col = 2 * tig + (e & 1) + 8 * nb, rank = 16 * c + gid + 8 * (e >> 1);
+      if (col < ncol && rank < ex.r[mb]) t[(size_t)(row0 + col) * w.t_ld + mb * (w.t_ld / 2) + rank] = acc[nb][e];
+    }
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(kMoEWarps * 32) moe_gemv_kernel(MoEWin w, MoERoute rt, int max_ent,
+                                                                  const uint16_t* __restrict__ x16,
+                                                                  const float* __restrict__ t, void* out) {
+  __shared__ float red[kMoEWarps][32][8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
+  const int n_ent = *rt.n_ent;
+  const long long n_items = (long long)n_ent * w.n_rb;
+  const int g0 = warp * w.G / kMoEWarps, g1 = (warp + 1) * w.G / kMoEWarps;
+  for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const int ent = (int)(it / w.n_rb), rb = (int)(it % w.n_rb);
+    const MoEExpert& ex = w.ex[rt.ent_e[ent]];
+    const int row0 = rt.ent_row0[ent], ncol = rt.ent_ncol[ent];
+    float tot[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    for (int g = g0; g < g1; ++g) {
+      uint32_t xr[2][16];
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) {
+        const int col = (lane >> 2) + 8 * nb;
+        const uint4* p = reinterpret_cast<const uint4*>(x16 + (size_t)(row0 + (col < ncol ? col : 0)) * w.K +
+                                                        g * kGroup + 8 * (lane & 3));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint4 v = __ldg(p + 4 * q);
+          xr[nb][4 * q + 0] = v.x; xr[nb][4 * q + 1] = v.y; xr[nb][4 * q + 2] = v.z; xr[nb][4 * q + 3] = v.w;
+        }
+      }
+      const uint4* const unused[2] = {nullptr, nullptr};
+      w_tile<BITS, 2, false>(ex.rec + ((size_t)rb * w.G + g) * rec_bytes(BITS), lane, unused, xr, tot);
+    }
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) red[warp][lane][4 * nb + e] = tot[nb][e];
+    __syncthreads();
+    if (warp == 0) {
+      float fin[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      for (int ww = 0; ww < kMoEWarps; ++ww)                 // fixed order: deterministic
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) fin[nb][e] += red[ww][lane][4 * nb + e];
+      // U·t: plain windows use member 0 for all 16 rows; a fused SiLU window runs the up chunks (rows
+      // 0-7) with t of member 0 and the gate chunks (rows 8-15) with t of member 1
+      float comp[2][2][4] = {};
+      const int r_eff = w.glue ? max(ex.r[0], ex.r[1]) : ex.r[0];
+      const int nck = (r_eff + 15) >> 4;
+      for (int c = 0; c < nck; ++c) {
+        const uint4 u = __ldg(ex.U + ((size_t)rb * (ex.rs[0] >> 4) + c) * 32 + lane);
+        const uint32_t af[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h == 1 && !w.glue) break;
+          if (16 * c >= ex.r[h]) continue;
+#pragma unroll
+          for (int nb = 0; nb < 2; ++nb) {
+            const int col = gid + 8 * nb;
+            const float* tr = t + (size_t)(row0 + (col < ncol ? col : 0)) * w.t_ld + h * (w.t_ld / 2);
+            uint32_t hi[2], lo[2];
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const int rk = 16 * c + 2 * tig + 8 * hh;
+              const float ta = (col < ncol && rk < ex.r[h]) ? tr[rk] : 0.f;
+              const float tb = (col < ncol && rk + 1 < ex.r[h]) ? tr[rk + 1] : 0.f;
+              const uint32_t ha = f32_to_bf16_rn(ta), hb = f32_to_bf16_rn(tb);
+              hi[hh] = ha | (hb << 16);
+              lo[hh] = f32_to_bf16_rn(ta - bf16_bits_to_f32(ha)) | (f32_to_bf16_rn(tb - bf16_bits_to_f32(hb)) << 16);
+            }
+            mma16816(comp[h][nb], af, hi[0], hi[1]);
+            mma16816(comp[h][nb], af, lo[0], lo[1]);
+          }
+        }
+      }
+      if (w.glue) {
+        uint16_t* m = reinterpret_cast<uint16_t*>(out);
+        const int ldm = w.n_rb * 8;
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int col = 2 * tig + e + 8 * nb;
+            if (col >= ncol) continue;
+            const float up = fin[nb][e] + comp[0][nb][e];
+            const float gt = fin[nb][e + 2] + comp[1][nb][e + 2];
+            m[(size_t)(row0 + col) * ldm + rb * 8 + gid] = (uint16_t)f32_to_bf16_rn(up * (gt / (1.f + __expf(-gt))));
+          }
+      } else {
+        float* o = reinterpret_cast<float*>(out);
+        const int ldo = w.n_rb * kRows;
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int col = 2 * tig + (e & 1) + 8 * nb;
+            if (col >= ncol) continue;
+            o[(size_t)(row0 + col) * ldo + rb * kRows + gid + 8 * (e >> 1)] = fin[nb][e] + comp[0][nb][e];
+          }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void moe_combine_kernel(const float* __restrict__ dout, int N, const float* __restrict__ gate, int T, int k,
+                                   MoERoute rt, float* __restrict__ y) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)T * N) return;
+  const int tk = (int)(i / N), n = (int)(i % N);
+  float acc = 0.f;
+  for (int j = 0; j < k; ++j) {
+    const int row = rt.tok_row[tk * k + j];
+    if (row >= 0) acc = fmaf(gate[tk * k + j], dout[(size_t)row * N + n], acc);
+  }
+  y[i] = acc;
+}
+
+}  // namespace
+
+cudaError_t moe_route(const int32_t* topk_idx, int T, int k, int E, const MoERoute& rt, cudaStream_t st) {
+  if (T < 1 || T > 1024 || k < 1 || k > kMoEMaxK || E < 1 || E > 256) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)E * ((T + 31) / 32) * sizeof(unsigned);
+  moe_route_kernel<<<1, kRouteThreads, smem, st>>>(topk_idx, T, k, E, rt);
+  return cudaGetLastError();
+}
+
+cudaError_t moe_prep(const uint16_t* x, int ldx, int K, int bits, int gather, const MoERoute& rt, int R_max,
+                     uint16_t* xg, uint16_t* x16, cudaStream_t st) {
+  const long long n = (long long)R_max * (K / 16);
+  const unsigned grid = (unsigned)((n + 255) / 256);
+  switch (bits) {
+    case 2: moe_prep_kernel<2><<<grid, 256, 0, st>>>(x, ldx, K, gather, rt, R_max, xg, x16); break;
+    case 3: moe_prep_kernel<3><<<grid, 256, 0, st>>>(x, ldx, K, gather, rt, R_max, xg, x16); break;
+    case 4: moe_prep_kernel<4><<<grid, 256, 0, st>>>(x, ldx, K, gather, rt, R_max, xg, x16); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t moe_rank_proj(const MoEWin& w, const MoERoute& rt, int max_ent, const uint16_t* xg, float* t,
+                          cudaStream_t st) {
+  const int max_chunks = w.t_ld / 32;
+  const long long warps = (long long)max_ent * 2 * max_chunks;
+  if (warps == 0) return cudaSuccess;
+  moe_rank_proj_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(w, rt, max_ent, max_chunks, xg, t);
+  return cudaGetLastError();
+}
+
+cudaError_t moe_gemv(const MoEWin& w, int bits, const MoERoute& rt, int max_ent, const uint16_t* x16,
+                     const float* t, void* out, cudaStream_t st) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long items = (long long)max_ent * w.n_rb;
+  const unsigned grid = (unsigned)(items < 8LL * sms ? items : 8LL * sms);
+  switch (bits) {
+    case 2: moe_gemv_kernel<2><<<grid, kMoEWarps * 32, 0, st>>>(w, rt, max_ent, x16, t, out); break;
+    case 3: moe_gemv_kernel<3><<<grid, kMoEWarps * 32, 0, st>>>(w, rt, max_ent, x16, t, out); break;
+    case 4: moe_gemv_kernel<4><<<grid, kMoEWarps * 32, 0, st>>>(w, rt, max_ent, x16, t, out); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t moe_combine(const float* dout, int N, const float* topk_gate, int T, int k, const MoERoute& rt,
+                        float* y, cudaStream_t st) {
+  const long long n = (long long)T * N;
+  moe_combine_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(dout, N, topk_gate, T, k, rt, y);
+  return cudaGetLastError();
+}
+
+}  // namespace hc

@@ -1,0 +1,101 @@
+"""GPU parity of the grouped MoE expert path (hc_moe_forward, C3) against the float64 oracle
+(oracle.linear.moe_forward): routed token batches over several experts, 3-bit weights with per-expert
+compensation ranks, entries of > 16 rows per expert, host and device inputs, determinism."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import linear
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def hc():
+    import paper_2605_05819_b200 as m
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    return m
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def desc(case, layer, window, slot, expert, r, glue=0):
+    return dict(layer=layer, window=window, slot=slot, expert=expert, N=case["N"], K=case["K"], bits=case["bits"],
+                codes=dev(case["codes"]), scales=dev(case["scales"]), zeros=dev(case["zeros"]),
+                U=dev(case["U"]), V=dev(case["V"]), r_stored=case["r_stored"], r_alloc=r, glue=glue)
+
+
+def make_experts(E, d, f, bits, seed):
+    g = synth.rng(seed)
+    experts, ranks = [], []
+    for e in range(E):
+        c = lambda n, k, s: synth.linear_case(seed * 100 + 3 * e + s, N=n, K=k, bits=bits, r_stored=16,
+                                              zeros="asym", unit_gain=synth.STACK_GAINS[4 + s])
+        experts.append(dict(up=c(f, d, 0), gate=c(f, d, 1), down=c(d, f, 2)))
+        lv = [0, 8, 16]
+        ranks.append(dict(up=lv[int(g.integers(0, 3))], gate=lv[int(g.integers(0, 3))], down=lv[int(g.integers(0, 3))]))
+    return experts, ranks
+
+
+def load(hc, ctx, layer, experts, ranks):
+    for e, (ex, r) in enumerate(zip(experts, ranks)):
+        ctx.load_layer([desc(ex["up"], layer, hc.UPGATE, 0, e, r["up"], hc.GLUE_SILU_MUL),
+                        desc(ex["gate"], layer, hc.UPGATE, 1, e, r["gate"], hc.GLUE_SILU_MUL),
+                        desc(ex["down"], layer, hc.DOWN, 0, e, r["down"])])
+
+
+@pytest.mark.parametrize("bits", [3, 4])
+@pytest.mark.parametrize("T,topk", [(1, 2), (5, 3), (40, 2)])
+def test_moe_forward_parity(hc, bits, T, topk):
+    E, d, f = 6, 256, 384
+    experts, ranks = make_experts(E, d, f, bits, seed=bits * 10 + T)
+    ctx = hc.Context(0)
+    load(hc, ctx, 0, experts, ranks)
+    x = synth.activations(T + 3, T, d)
+    idx, gate = synth.routing_case(T + 7, T, E, topk)
+    y = torch.empty((T, d), dtype=torch.float32, device="cuda")
+    ctx.moe_forward(0, dev(x), dev(idx), dev(gate), y)
+    y2 = torch.empty_like(y)
+    ctx.moe_forward(0, dev(x), dev(idx), dev(gate), y2)
+    torch.cuda.synchronize()
+    yc = y.cpu().numpy()
+    assert np.array_equal(yc, y2.cpu().numpy())                     # deterministic
+    ref = linear.moe_forward(experts, ranks, x, idx, gate)
+    # m = bf16(silu(gate)·up) is a rounding point (R8): an fp32-vs-float64 flip of one m element
+    # moves y by one bf16 ulp of m times a DOWN weight, far inside 2e-3·max|y|
+    err = np.abs(yc - ref).max() / np.abs(ref).max()
+    assert err <= 2e-3, err
+    # host inputs / output through the same entry point
+    yh = np.zeros((T, d), dtype=np.float32)
+    ctx.moe_forward(0, np.ascontiguousarray(x), idx, gate, yh)
+    assert np.array_equal(yh, yc)
+    ctx.close()
+
+
+def test_moe_rank_change_and_skipped_ids(hc):
+    E, d, f = 4, 128, 256
+    experts, ranks = make_experts(E, d, f, 3, seed=99)
+    ctx = hc.Context(0)
+    load(hc, ctx, 2, experts, ranks)
+    T = 9
+    x = synth.activations(5, T, d)
+    idx, gate = synth.routing_case(6, T, E, 2)
+    idx[0, 1] = E + 3                                               # outside [0, E): skipped
+    y = torch.empty((T, d), dtype=torch.float32, device="cuda")
+    for e in range(E):                                              # all ranks to 16 / 0 via hc_set_rank
+        ctx.set_rank(2, hc.UPGATE, 0, 16, expert=e)
+        ctx.set_rank(2, hc.DOWN, 0, 0, expert=e)
+        ranks[e]["up"], ranks[e]["down"] = 16, 0
+    ctx.moe_forward(2, dev(x), dev(idx), dev(gate), y)
+    torch.cuda.synchronize()
+    keep = idx < E
+    ref = linear.moe_forward(experts, ranks, x, np.where(keep, idx, 0), np.where(keep, gate, 0.0).astype(np.float32))
+    err = np.abs(y.cpu().numpy() - ref).max() / np.abs(ref).max()
+    assert err <= 2e-3, err
+    with pytest.raises(hc.HCError):
+        ctx.moe_forward(7, dev(x), dev(idx), dev(gate), y)           # no experts on layer 7
+    ctx.close()

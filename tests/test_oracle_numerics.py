@@ -218,3 +218,22 @@ def test_moe_single_expert_equals_dense():
     xf = packing.bf16_to_f64(x)
     m = linear.round_bf16(linear.silu(linear._lin(gate, 0, xf)) * linear._lin(up, 8, xf))
     assert np.array_equal(y, linear._lin(down, 16, m))
+
+
+def test_moe_gate_linearity_two_identical_experts():
+    # P:852 Y = Σ_e g_e E_e(X): two copies of one expert routed with gates (g, 1 - g) equal the dense FFN,
+    # and a single expert with gate g scales its output by exactly g (float64 weighting)
+    d, f = 128, 128
+    up = synth.linear_case(30, f, d, 4, 128, 16, 1, "asym")
+    gate = synth.linear_case(31, f, d, 4, 128, 16, 1, "asym")
+    down = synth.linear_case(32, d, f, 4, 128, 16, 1, "asym")
+    ex = dict(up=up, gate=gate, down=down)
+    r = dict(up=16, gate=8, down=0)
+    x = synth.activations(33, 4, d)
+    one = linear.moe_forward([ex], [r], x, np.zeros((4, 1), np.int32), np.ones((4, 1), np.float32))
+    g = np.float32(0.375)                                             # exact in binary: no rounding in g, 1-g
+    two = linear.moe_forward([ex, ex], [r, r], x, np.array([[0, 1]] * 4, np.int32),
+                             np.array([[g, 1 - g]] * 4, np.float32))
+    assert np.allclose(two, one, rtol=1e-14, atol=0)
+    half = linear.moe_forward([ex], [r], x, np.zeros((4, 1), np.int32), np.full((4, 1), g, np.float32))
+    assert np.array_equal(half, one * float(g))
