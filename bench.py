@@ -351,6 +351,120 @@ def oracle_c2_sample(seconds: float = 15.0, c=C2):
     return 1.0 / (per_layer * c["layers"]), n, el
 
 
+# ------------------------------------------------------------------ workload C3 (grouped MoE experts)
+C3 = dict(name="c3", model="qwen3_30b_a3b", hidden=2048, ffn=768, experts=128, topk=8, layers=48, bits=3, group=128,
+          r_stored=16)
+
+
+def c3_matrix_bytes(N, K, bits, r):
+    return N * K * bits // 8 + N * (K // 128) * (16 + bits) // 8 + 2 * r * (N + K)
+
+
+def run_c3_ours(args, rank, world, device, T, c=C3):
+    """48 MoE layers of 128 experts (3-bit, per-expert ranks in {0, 8, 16}); one step = hc_moe_forward on every
+    layer for the same T routed tokens (routing drawn per layer as in SURVEY.md §8(d) C3)."""
+    import torch
+    import synth
+    import paper_2605_05819_b200 as hc
+    d, f, E, k, b, rs = c["hidden"], c["ffn"], c["experts"], c["topk"], c["bits"], c["r_stored"]
+    ctx = hc.Context(device)
+    levels = (0, 8, 16)
+    rng = np.random.default_rng(123)
+    ranks = {}
+    e2 = ((4 ** b) - 1) / 12.0 + 0.25
+    for l in range(c["layers"]):
+        for e in range(E):
+            rr = [levels[int(v)] for v in rng.integers(0, 3, size=3)]
+            ranks[(l, e)] = rr
+            mats = []
+            for (win, slot, N, K, gl, r) in ((2, 0, f, d, 1, rr[0]), (2, 1, f, d, 1, rr[1]), (3, 0, d, f, 0, rr[2])):
+                g = torch.Generator(device="cuda").manual_seed(10007 * l + 31 * e + 7 * win + slot)
+                G = K // 128
+                gain = 0.25 if win == 2 else 0.05
+                mats.append(dict(layer=l, window=win, slot=slot, expert=e, N=N, K=K, bits=b, glue=gl,
+                                 codes=torch.randint(-2**31, 2**31, (N, K * b // 32), generator=g, device="cuda", dtype=torch.int32),
+                                 scales=(gain * (0.5 + torch.rand((N, G), generator=g, device="cuda")) / (e2 * K) ** 0.5).to(torch.bfloat16),
+                                 zeros=torch.randint(0, 1 << b, (N, G), generator=g, device="cuda", dtype=torch.uint8),
+                                 U=(torch.randn((N, rs), generator=g, device="cuda") / N ** 0.5).to(torch.bfloat16),
+                                 V=(0.05 * (N / (rs * K)) ** 0.5 * torch.randn((rs, K), generator=g, device="cuda")).to(torch.bfloat16),
+                                 r_stored=rs, r_alloc=r))
+            ctx.load_layer(mats)
+    torch.cuda.synchronize()
+    x = torch.randn((T, d), generator=torch.Generator(device="cuda").manual_seed(5), device="cuda").to(torch.bfloat16)
+    routes = [synth.routing_case(900 + l, T, E, k) for l in range(c["layers"])]
+    idx = [torch.from_numpy(r[0]).cuda() for r in routes]
+    gate = [torch.from_numpy(r[1]).cuda() for r in routes]
+    ys = [torch.empty((T, d), dtype=torch.float32, device="cuda") for _ in range(c["layers"])]
+    nbytes = 0
+    for l, (ri, _) in enumerate(routes):
+        for e in sorted(set(int(v) for v in ri.reshape(-1))):
+            ru, rg, rd = ranks[(l, e)]
+            nbytes += c3_matrix_bytes(f, d, b, ru) + c3_matrix_bytes(f, d, b, rg) + c3_matrix_bytes(d, f, b, rd)
+        nbytes += T * (2 * d + 4 * d) + T * k * 8
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        for l in range(c["layers"]):
+            ctx.moe_forward(l, x, idx[l], gate[l], ys[l], stream=st)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=st):
+            for l in range(c["layers"]):
+                ctx.moe_forward(l, x, idx[l], gate[l], ys[l], stream=st)
+        for _ in range(max(args.warmup, 3)):
+            graph.replay()
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(device) as clk, torch.cuda.stream(st):
+        e0.record(st)
+        for _ in range(args.steps):
+            graph.replay()
+        e1.record(st)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    finite = bool(all(torch.isfinite(yy).all().item() for yy in ys))
+    # end to end with host buffers: x, routing in; y of the last layer out, every layer through the API
+    xh = x.cpu()
+    yh = np.zeros((T, d), dtype=np.float32)
+    ih = [r[0] for r in routes]
+    gh = [r[1] for r in routes]
+    n_e2e = max(2, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(n_e2e):
+        for l in range(c["layers"]):
+            ctx.moe_forward(l, xh, ih[l], gh[l], yh)
+    e2e_s = time.perf_counter() - t0
+    ctx.close()
+    return dict(ms=ms, steps=args.steps, clocks=clk.summary, e2e_s=e2e_s, n_e2e=n_e2e, finite=finite,
+                launches=args.steps * c["layers"] * 8, bytes=nbytes,
+                h2d=c["layers"] * (T * d * 2 + T * k * 8), d2h=c["layers"] * T * d * 4)
+
+
+def oracle_c3_sample(seconds: float = 15.0, c=C3, T=16):
+    """The float64 oracle on a bounded sample of C3: whole MoE layers (T routed tokens, top-8 of 128
+    experts) of Qwen3-30B-A3B expert shapes; tokens/s extrapolated x48 layers."""
+    import synth
+    from oracle import linear
+    d, f, E, k = c["hidden"], c["ffn"], c["experts"], c["topk"]
+    idx, gate = synth.routing_case(901, T, E, k)
+    act = sorted(set(int(v) for v in idx.reshape(-1)))
+    mk = lambda N, K, s: synth.linear_case(200 + s, N=N, K=K, bits=c["bits"], r_stored=16, zeros="asym")
+    experts = [dict(up=mk(f, d, 3 * i), gate=mk(f, d, 3 * i + 1), down=mk(d, f, 3 * i + 2)) if i in act else None
+               for i in range(E)]
+    ranks = [dict(up=8, gate=8, down=8) for _ in range(E)]
+    x = synth.activations(3, T, d)
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        linear.moe_forward(experts, ranks, x, idx, gate)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or n >= 4:
+            break
+    return T / (el / n * c["layers"]), n, el
+
+
 def cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -364,7 +478,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c5"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c5"])
     ap.add_argument("--mode", default="auto", choices=["auto", "tp", "replicas"],
                     help="N>1: tp = column-sharded stack with NCCL all-gather (strong scaling, default); "
                          "replicas = independent full-model replicas (weak scaling)")
@@ -380,7 +494,14 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", 0))
     hbm, tflops, peak_src = peaks()
     tp = world > 1 and args.mode in ("auto", "tp")
-    if args.workload == "c1":
+    if args.workload == "c3":
+        config = {"workload": f"c3: Qwen3-30B-A3B-shaped MoE expert linears (128 experts, top-8, 48 layers), 3-bit g128 + "
+                              f"per-expert ranks in {{0, 8, 16}}, {args.batch} routed tokens per step, grouped launches",
+                  "hidden": 2048, "expert_ffn": 768, "experts": 128, "topk": 8, "layers": 48, "bits": 3, "group": 128,
+                  "tokens": args.batch, "parallelism": f"dp{world}",
+                  "l2": "inputs larger than L2 (11.4 GB of expert weights; each step touches every layer)",
+                  "routing": "softmax(N(0,1) logits) top-8, renormalised gates (synth.routing_case)"}
+    elif args.workload == "c1":
         config = {"workload": "c1: single 4096x4096 linear, 4-bit g128, rank-64 compensation, batch-1 decode",
                   "N": 4096, "K": 4096, "bits": 4, "group": 128, "rank": 64, "batch": 1,
                   "l2": "defeated: 128 distinct weight copies (1.25 GB) rotated per step"}
@@ -405,6 +526,11 @@ def main():
             val, unit = c1_bytes() * n / el / 1e9, "GB/s"
             sample = f"{n} whole C1 calls (numpy float64, unpack+dequant+matvec)"
             ms = 1e3 * el / n
+        elif args.workload == "c3":
+            val, n, el = oracle_c3_sample(seconds=20.0, T=args.batch)
+            unit = "tokens/s"
+            sample = f"{n} whole MoE layers ({args.batch} tokens, top-8 of 128 experts, float64), extrapolated x48 layers"
+            ms = 1e3 * args.batch / val
         else:
             val, n, el = oracle_c2_sample(seconds=20.0)
             unit = "tokens/s"
@@ -423,7 +549,11 @@ def main():
     if world > 1:
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
-    if args.workload == "c1":
+    if args.workload == "c3":
+        r = run_c3_ours(args, rank, world, local, args.batch)
+        nbytes = r["bytes"]
+        unit, kernel = "tokens/s", "hc::moe_gemv_kernel<3> (grouped UPGATE + DOWN per layer)"
+    elif args.workload == "c1":
         r = run_c1_ours(args, rank, world, local)
         nbytes = c1_bytes()
         unit, kernel = "GB/s", "hc::decode_kernel<4,1,true>"
@@ -445,19 +575,28 @@ def main():
         value = streams * args.batch * r["steps"] / (ms_max * 1e-3)
         e2e = {"value": round(streams * args.batch * r["n_e2e"] / r["e2e_s"], 2), "unit": "tokens/s",
                "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]}
-        config["mean_rank"] = round(r["mean_rank"], 2)
+        if "mean_rank" in r:
+            config["mean_rank"] = round(r["mean_rank"], 2)
         config["bytes_per_step"] = nbytes
         config["output_finite"] = r["finite"]
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 2), "unit": unit, "n_gpus": world, "steps": r["steps"],
                 "warmup": args.warmup, "ms_per_step": round(ms_max / r["steps"], 6), "higher_is_better": True,
-                "scaling": "strong" if tp else "weak", "vs_baseline": None, "dtype": "bf16 x int4 (exact int dequant, fp32 accumulate)",
+                "scaling": "strong" if tp else "weak", "vs_baseline": None, "dtype": f"bf16 x int{config.get('bits', 4)} (exact int dequant, fp32 accumulate)",
                 "data": "synthetic (seeded on device, random weights of the named shapes)", "config": config,
                 "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
                              "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": peak_src,
                              "kernel": kernel, "bytes_per_step": nbytes},
                 "clocks": r["clocks"], "gpu_launches": r["launches"], "e2e": e2e}
-        if args.workload != "c1" and args.sweep:
+        if args.workload == "c3" and args.sweep:
+            sweep = {}
+            for Ts in (1, 16, 64, 256):
+                rs = run_c3_ours(args, rank, world, local, Ts)
+                sweep[str(Ts)] = {"tokens_per_s": round(Ts * rs["steps"] / (rs["ms"] * 1e-3), 1),
+                                  "ms_per_step": round(rs["ms"] / rs["steps"], 4),
+                                  "GBps": round(rs["bytes"] / (rs["ms"] / rs["steps"] * 1e-3) / 1e9, 1)}
+            line["token_sweep"] = sweep
+        elif args.workload not in ("c1", "c3") and args.sweep:
             sweep = {}
             for Bs in (2, 4, 8, 16):
                 rs = run_c2_ours(args, rank, world, local, Bs, STACKS[args.workload], tp)
@@ -470,6 +609,10 @@ def main():
                 n, el = oracle_c1_sample(12.0)
                 line["cpu_baseline"] = {"value": round(nbytes * n / el / 1e9, 4), "unit": "GB/s", "cores": cores(),
                                         "kind": "oracle", "sample": f"{n} whole C1 calls, numpy float64"}
+            elif args.workload == "c3":
+                tps, n, el = oracle_c3_sample(15.0, T=args.batch)
+                line["cpu_baseline"] = {"value": round(tps, 6), "unit": "tokens/s", "cores": cores(), "kind": "oracle",
+                                        "sample": f"{n} whole MoE layers ({args.batch} tokens, float64), extrapolated x48"}
             elif args.workload == "c2":
                 tps, n, el = oracle_c2_sample(15.0)
                 line["cpu_baseline"] = {"value": round(tps, 6), "unit": "tokens/s", "cores": cores(), "kind": "oracle",
