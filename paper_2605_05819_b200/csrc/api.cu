@@ -92,6 +92,7 @@ struct hc_ctx {
   DevBuf p_x16, p_t16, p_tpart;        // prefill scratch: fp16 activations, fp16 T = X·Vᵀ, split-K partials
   // decode stack (hc_stack_forward)
   DevBuf s_h, s_h1, s_qkv, s_m;
+  int trace_slot = 0;                  // dev tracing: slot of the next decode launch (HC_DEC_TRACE builds)
   std::map<std::tuple<int, const void*, void*>, std::unique_ptr<StackGraph>> graphs;
   cudaStream_t cap_stream = nullptr;
   // column sharding (hc_set_comm): NCCL communicator, send / gather staging
@@ -432,9 +433,18 @@ static bool can_forward(const Window& next) {
 // Launch arguments of one window (also used by the stack driver).
 static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int B, void* y, int y_bf16,
                              const void* resid, int ld_resid, DArgs& a, int& grid, bool t_in = false,
-                             const FwdSpec* fw = nullptr) {
+                             const FwdSpec* fw = nullptr, Window* dep = nullptr, bool keep_done = false) {
   std::memset(&a, 0, sizeof(a));
   a.t_in = t_in ? 1 : 0;
+  a.keep_done = keep_done ? 1 : 0;
+  if (dep) {
+    if (!dep->cnt.p) return fail(HC_ERR_STATE, "dataflow dependency: producer window workspace missing");
+    a.dep_cnt = (unsigned*)dep->cnt.p + 1;
+    int n = 0;
+    if (dep->glue == HC_GLUE_SILU_MUL) n = dep->members.front().rows() / 8;
+    else for (const Member& m : dep->members) n += m.rows() / kRows;
+    a.dep_target = (unsigned)n;
+  }
   const Member& m0 = w.members.front();
   a.K = m0.K; a.G = m0.K / kGroup; a.B = B;
   a.x = (const uint16_t*)x; a.ldx = ldx; a.y = y; a.y_bf16 = y_bf16;
@@ -530,11 +540,12 @@ static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int
 
 static hc_status launch_window(hc_ctx* ctx, Window& w, const void* x, int ldx, int B, void* y, int y_bf16,
                                const void* resid, int ld_resid, cudaStream_t st, bool t_in = false,
-                               const FwdSpec* fw = nullptr) {
+                               const FwdSpec* fw = nullptr, Window* dep = nullptr, bool keep_done = false) {
   DArgs a;
   int grid = 0;
-  hc_status s = window_args(ctx, w, x, ldx, B, y, y_bf16, resid, ld_resid, a, grid, t_in, fw);
+  hc_status s = window_args(ctx, w, x, ldx, B, y, y_bf16, resid, ld_resid, a, grid, t_in, fw, dep, keep_done);
   if (s != HC_OK) return s;
+  a.trace_slot = ctx->trace_slot++;
   if (a.x16)
     CUDA_TRY(launch_xprep(a.x, a.ldx, B, a.K, w.members.front().bits, (uint16_t*)a.x16, st));
   CUDA_TRY(launch_decode(a, w.members.front().bits, grid, st));
@@ -814,6 +825,7 @@ static hc_status tp_window(hc_ctx* ctx, Window& w, const void* x, int ldx, int B
 // dev-only (not in hcinfer.h): point the stack kernel's trace stamps at a device buffer
 extern "C" int hc_dev_stack_trace(void* buf) { return (int)hc::stack_set_trace(buf); }
 extern "C" int hc_dev_stack_acct(void* buf) { return (int)hc::stack_set_acct(buf); }
+extern "C" int hc_dev_decode_trace(void* buf) { return (int)hc::decode_set_trace(buf); }
 
 extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, void* y, void* stream) {
   if (!ctx) return fail(HC_ERR_STATE, "hc_stack_forward: null context");
@@ -963,10 +975,22 @@ extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, voi
         const bool t_q = l > 0 && hc::can_forward(*p.qkv);
         const hc::FwdSpec s_o{f_o ? p.o : nullptr, 0, d}, s_ug{f_ug ? p.ug : nullptr, 0, d},
             s_dn{f_dn ? p.down : nullptr, 0, f}, s_q{f_q ? plan[l + 1].qkv : nullptr, 0, d};
-        cap = hc::launch_window(ctx, *p.qkv, hin, d, B, qkv, 1, nullptr, 0, cs, t_q, &s_o);                 // q | k | v
-        if (cap == HC_OK) cap = hc::launch_window(ctx, *p.o, qkv, nqkv, B, h1, 1, hin, d, cs, f_o, &s_ug);   // h1 = h + O(q)
-        if (cap == HC_OK) cap = hc::launch_window(ctx, *p.ug, h1, d, B, mm, 1, nullptr, 0, cs, f_ug, &s_dn); // m = silu(g)·u
-        if (cap == HC_OK) cap = hc::launch_window(ctx, *p.down, mm, f, B, hout, 1, h1, d, cs, f_dn, &s_q);   // h' = h1 + DOWN(m)
+        // dataflow dependencies: a window whose x is staged in shared memory waits on
+        // its producer's row-block counter instead of the kernel boundary (an unstaged window keeps the
+        // grid dependency: its x-prep kernel sits in between)
+        const bool dx_ok = getenv("HC_DEPWAIT") == nullptr || getenv("HC_DEPWAIT")[0] != '0';
+        const bool sx_q = dx_ok && hc::decode_stages_x(B, d), sx_f = dx_ok && hc::decode_stages_x(B, f);
+        Window* prev_dn = l > 0 ? plan[l - 1].down : nullptr;
+        const bool next_q = l + 1 < plan.size() && sx_q;
+        ctx->trace_slot = (int)(4 * l);
+        cap = hc::launch_window(ctx, *p.qkv, hin, d, B, qkv, 1, nullptr, 0, cs, t_q, &s_o,
+                                (prev_dn && sx_q) ? prev_dn : nullptr, sx_q);                                 // q | k | v
+        if (cap == HC_OK) cap = hc::launch_window(ctx, *p.o, qkv, nqkv, B, h1, 1, hin, d, cs, f_o, &s_ug,
+                                                  sx_q ? p.qkv : nullptr, sx_q);                              // h1 = h + O(q)
+        if (cap == HC_OK) cap = hc::launch_window(ctx, *p.ug, h1, d, B, mm, 1, nullptr, 0, cs, f_ug, &s_dn,
+                                                  sx_q ? p.o : nullptr, sx_f);                                // m = silu(g)·u
+        if (cap == HC_OK) cap = hc::launch_window(ctx, *p.down, mm, f, B, hout, 1, h1, d, cs, f_dn, &s_q,
+                                                  sx_f ? p.ug : nullptr, next_q);                             // h' = h1 + DOWN(m)
       } else {                                                   // column-sharded: gather every window
         cap = tp_window(ctx, *p.qkv, hin, d, B, qkv, nullptr, 0, cs);
         if (cap == HC_OK) cap = tp_window(ctx, *p.o, qkv, nqkv, B, h1, hin, d, cs);

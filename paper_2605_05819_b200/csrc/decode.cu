@@ -35,6 +35,21 @@
 
 namespace hc {
 
+#ifndef HC_DEC_TRACE
+#define HC_DEC_TRACE 0
+#endif
+// dev tracing: globaltimer stamps per (launch slot, CTA): [0] start, [1] after the PDL wait (epilogue),
+// [2] first FULL passed, [3] last FULL passed, [4] epilogue done
+__device__ unsigned long long* g_dtrace = nullptr;
+__device__ __forceinline__ void dtrace(const DArgs& a, int ev) {
+#if HC_DEC_TRACE
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (g_dtrace) g_dtrace[((size_t)a.trace_slot * 512 + blockIdx.x) * 8 + ev] = t;
+#endif
+}
+cudaError_t decode_set_trace(void* buf) { return cudaMemcpyToSymbol(g_dtrace, &buf, sizeof(buf)); }
+
 
 // Warp roles: warps 0..7 stream and contract tiles; warp 8 is the epilogue warp (reduction of the
 // 8 partial sums, U·t, output).  Named barriers hand the shared reduction buffer red[p] (p = item
@@ -47,6 +62,21 @@ namespace hc {
 // window's t accumulators with 64-bit fixed-point atomics (exact integer adds: t is bit-identical
 // for any arrival order), then bumps v_done; each CTA's epilogue warp acquires v_done once and reads
 // t while its tile warps are still streaming.
+// Wait for this window's inputs: the producer window's completion counter (acquire; every warp that
+// reads activations calls this), else the programmatic-dependent-launch grid dependency.
+__device__ __forceinline__ void dep_wait(const DArgs& a, int lane) {
+  if (a.dep_cnt) {
+    if (lane == 0) {
+      while (ld_relaxed(a.dep_cnt) < a.dep_target) __nanosleep(64);
+      (void)ld_acquire(a.dep_cnt);
+      asm volatile("fence.proxy.async.global;" ::: "memory");   // generic writes -> async-proxy (TMA) reads
+    }
+    __syncwarp();
+  } else {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
+}
+
 template <int BITS, int NB8, bool XS>
 __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(const __grid_constant__ DArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -87,6 +117,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
 
   if (warp == kEpi) {
     // ======================= epilogue warp =======================
+    if (lane == 0) dtrace(a, 0);
     auto prefetch_u = [&](int rb, int par) {   // U fragments of a row-block item -> ubuf[par]
       if (rb >= n_items) return;
       const DMember& m = a.m[member_of_rb(a, rb)];
@@ -101,7 +132,8 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
       }
     };
     prefetch_u(blockIdx.x, 0);                           // weights: before the PDL wait
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    dep_wait(a, lane);
+    if (lane == 0) dtrace(a, 1);
     if constexpr (XS) {
       if (lane == 0) {
         mbar_expect_tx(xbar, (uint32_t)(a.B * a.K * 2));
@@ -169,6 +201,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
         __syncwarp();
       }
       asm volatile("bar.sync %0, %1;" ::"r"(1 + par), "n"(kDecodeThreads) : "memory");   // FULL[par]
+      if (lane == 0) { if (k == 0) dtrace(a, 2); if (item + (int)gridDim.x >= n_items) dtrace(a, 3); }
       float fin[NB8][4];
 #pragma unroll
       for (int nb = 0; nb < NB8; ++nb)
@@ -249,7 +282,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
             if (b >= a.B) continue;
             const int n = m.row_off + rbl * kRows + gid + 8 * (e >> 1);
             float v = fin[nb][e] + comp[0][nb][e];
-            if (a.resid) v += bf16_bits_to_f32(a.resid[(size_t)b * a.ld_resid + n]);
+            if (a.resid) v += bf16_bits_to_f32(__ldcg(a.resid + (size_t)b * a.ld_resid + n));
             if (a.y_bf16) {
               const uint16_t bits = (uint16_t)f32_to_bf16_rn(v);
               reinterpret_cast<uint16_t*>(a.y)[(size_t)b * a.ldy + n] = bits;
@@ -292,6 +325,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
       }
       ++my_rb;
     }
+    if (lane == 0) dtrace(a, 4);
     // one counter update per CTA: the CTA completing the last row block resets t and the counters
     // (every t reader is a row-block epilogue, all of which have finished by then)
     __syncwarp();
@@ -303,7 +337,11 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
     last = __shfl_sync(0xffffffffu, last, 0);
     if (last) {
       for (int i = lane; i < a.n_chunks * 256; i += 32) a.tacc[i] = 0;
-      if (lane == 0) { a.cnt[0] = 0u; a.cnt[1] = 0u; }
+      if (lane == 0) {
+        a.cnt[0] = 0u;
+        if (!a.keep_done) a.cnt[1] = 0u;             // else the consumer window resets it
+        if (a.dep_cnt) *a.dep_cnt = 0u;              // every CTA of this window passed its wait
+      }
     }
     return;
   }
@@ -353,7 +391,9 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
   };
 #pragma unroll
   for (int s = 0; s < kNBuf; ++s) issue_block();   // weights / V: before the PDL wait
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // tile warps read activations only through the x staged by the epilogue warp (XS, ordered by its
+  // acquire and the x mbarrier), except for V pieces and unstaged x: only then do they wait themselves
+  if (!a.dep_cnt || !XS || n_vp > 0) dep_wait(a, lane);
   if constexpr (XS) {
     while (!mbar_try_wait(xbar, 0)) {}
     // in place: x (bf16) -> x' = x·2^-fp (fp16, the B operand of the W mma); 16 elements per thread
@@ -385,7 +425,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
     for (int nb = 0; nb < NB8; ++nb) {
       const uint4* p = reinterpret_cast<const uint4*>(a.x + (size_t)xrow(a, gid + 8 * nb) * a.ldx + 8 * tig +
                                                       g * kGroup + 32 * part);
-      xv[nb] = __ldg(p);                                 // bf16 x (V is bf16; x' is for the W tiles)
+      xv[nb] = __ldcg(p);                                // bf16 x from L2 (written by the producer window)
     }
     while (!mbar_try_wait(&bars[s], ph)) {}
     float tp[NB8][4];

@@ -21,7 +21,10 @@ constexpr int kMaxChunks = 32;           // Σ ceil(r_m/16) over a window's memb
 constexpr int kTPB = HC_DEC_TPB;         // tiles per bulk-copy block
 constexpr int kNBuf = HC_DEC_NBUF;       // block buffers per warp (kNBuf - 1 blocks in flight while one computes)
 constexpr int kTileMax = 1088;           // >= rec_bytes(4) = 1072, >= 1 KB V piece
-constexpr int kUPre = 8;                 // U chunks (16 ranks each) staged in smem per item (r <= 128)
+#ifndef HC_DEC_UPRE
+#define HC_DEC_UPRE 8
+#endif
+constexpr int kUPre = HC_DEC_UPRE;       // U chunks (16 ranks each) staged in smem per item (r <= 128)
 constexpr int kFwdMax = 24;              // next-window rank chunks a launch can forward t to (smem: 512 B each)
 
 struct DMember {
@@ -63,6 +66,13 @@ struct DArgs {
   int fwd_rs[kMaxMembers];            // r_stored / 16 of the next members (chunk stride of fwd_vn)
   int fwd_nm;           // next window's member count
   long long* fwd_tacc;  // next window's t accumulators
+  int trace_slot;       // dev (HC_DEC_TRACE builds): row of the timestamp trace this launch writes
+  // dataflow dependency on the producer window (stack graphs): instead of griddepcontrol.wait (the
+  // kernel-boundary release, ~2 µs), wait until the producer's row-block counter reaches its n_rb
+  // (release / acquire), and reset that counter when this window completes
+  unsigned* dep_cnt;    // producer's cnt[1], or NULL (griddepcontrol.wait)
+  unsigned dep_target;  // producer's n_rb
+  int keep_done;        // 1: a consumer window resets this window's cnt[1] (do not self-reset it)
   long long* tacc;      // [n_chunks][16 batch][16 ranks] t = V·x in 2^-28 fixed point (self-resetting)
   unsigned* cnt;        // [0] v_done (tile warps done with their V share), [1] w_done (row blocks)
 };
@@ -73,6 +83,7 @@ cudaError_t launch_decode(const DArgs& a, int bits, int grid, cudaStream_t st);
 bool decode_stages_x(int B, int K);
 // x' (fp16, pre-scaled per the code layout of `bits`) for a !XS decode launch.
 cudaError_t launch_xprep(const uint16_t* x, int ldx, int B, int K, int bits, uint16_t* x16, cudaStream_t st);
+cudaError_t decode_set_trace(void* buf);   // dev: [slots][grid][8] globaltimer stamps (HC_DEC_TRACE builds)
 // Max co-resident CTAs of the decode kernel on this device (persistent grid size).
 int decode_max_ctas(int bits, int B, int K, int n_chunks, int fwd_chunks);
 
