@@ -742,10 +742,11 @@ extern "C" hc_status hc_moe_forward(hc_ctx* ctx, int32_t layer, const void* x, i
   CUDA_TRY(hc::moe_route(didx, T, topk, c->E, rt, st));
   CUDA_TRY(hc::moe_prep((const uint16_t*)dx, c->K, c->K, c->bits, 1, rt, R, xg, x16, st));
   CUDA_TRY(hc::moe_rank_proj(wu, rt, maxe, xg, tug, st));
-  CUDA_TRY(hc::moe_gemv(wu, c->bits, rt, maxe, x16, tug, m, st));                  // m = bf16(silu(gate)·up)
+  const int max_cols = std::min(T, 16);                                             // rows of one expert <= T
+  CUDA_TRY(hc::moe_gemv(wu, c->bits, rt, maxe, x16, tug, m, max_cols, st));        // m = bf16(silu(gate)·up)
   CUDA_TRY(hc::moe_prep(m, c->F, c->F, c->bits, 0, rt, R, nullptr, md, st));
   CUDA_TRY(hc::moe_rank_proj(wd, rt, maxe, m, tdn, st));
-  CUDA_TRY(hc::moe_gemv(wd, c->bits, rt, maxe, md, tdn, dout, st));                // DOWN_e(m) per row, fp32
+  CUDA_TRY(hc::moe_gemv(wd, c->bits, rt, maxe, md, tdn, dout, max_cols, st));      // DOWN_e(m) per row, fp32
   CUDA_TRY(hc::moe_combine(dout, c->D, dgate, T, topk, rt, (float*)dy, st));
   if (hy) CUDA_TRY(cudaMemcpyAsync(y, dy, (size_t)T * c->D * 4, cudaMemcpyDeviceToHost, st));
   if (hi || hg || hx || hy) CUDA_TRY(cudaStreamSynchronize(st));

@@ -204,22 +204,13 @@ __device__ __forceinline__ void load_x_global(const DArgs& a, int g, int lane, u
 // The A registers hold 2^fp·(q − z) (fp16, exact) and the B operand is x' = x·2^-fp (fp16), so every
 // product is exact and one mma chain accumulates Σ_k (q − z)·x_k in fp32.
 // XS: x' fragments come from shared memory (xrow_s[nb] = this lane's run start for the group).
+// The compute part of w_tile on a record already in registers (w = the lane's code words, sw = its
+// scales word, zz = the record's zeros).
 template <int BITS, int NB8, bool XS>
-__device__ __forceinline__ void w_tile(const uint8_t* rec, int lane, const uint4* const (&xrow_s)[NB8],
-                                       const uint32_t (&xr)[NB8][16], float (&tot)[NB8][4]) {
-  uint32_t w[2 * BITS];
-#pragma unroll
-  for (int q = 0; q < (2 * BITS) / 4; ++q) {
-    const uint4 v = *reinterpret_cast<const uint4*>(rec + q * 512 + lane * 16);
-    w[4 * q + 0] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
-  }
-  if constexpr ((2 * BITS) % 4) {
-    const uint2 v = *reinterpret_cast<const uint2*>(rec + 512 * ((2 * BITS) / 4) + lane * 8);
-    w[2 * BITS - 2] = v.x; w[2 * BITS - 1] = v.y;
-  }
+__device__ __forceinline__ void w_tile_regs(const uint32_t (&w)[2 * BITS], uint32_t sw, uint2 zz, int lane,
+                                            const uint4* const (&xrow_s)[NB8], const uint32_t (&xr)[NB8][16],
+                                            float (&tot)[NB8][4]) {
   const int gid = lane >> 2;
-  const uint32_t sw = *reinterpret_cast<const uint32_t*>(rec + scales_off(BITS) + 4 * gid);
-  const uint2 zz = *reinterpret_cast<const uint2*>(rec + zeros_off(BITS));   // rows 0..7 | rows 8..15
   // fp16x2 (1024 + 2^fp·z) of rows gid / gid + 8 for each field exponent fp: subtracting it turns a
   // register into 2^fp·(q − z) exactly, so the mma accumulates Σ (q − z)·x with no large offset
   const uint32_t zr0 = (zz.x >> (4 * gid)) & 15u, zr1 = (zz.y >> (4 * gid)) & 15u;
@@ -263,6 +254,42 @@ __device__ __forceinline__ void w_tile(const uint8_t* rec, int lane, const uint4
     tot[nb][2] = fmaf(s1, acc[nb][2], tot[nb][2]);
     tot[nb][3] = fmaf(s1, acc[nb][3], tot[nb][3]);
   }
+}
+
+template <int BITS, int NB8, bool XS>
+__device__ __forceinline__ void w_tile(const uint8_t* rec, int lane, const uint4* const (&xrow_s)[NB8],
+                                       const uint32_t (&xr)[NB8][16], float (&tot)[NB8][4]) {
+  uint32_t w[2 * BITS];
+#pragma unroll
+  for (int q = 0; q < (2 * BITS) / 4; ++q) {
+    const uint4 v = *reinterpret_cast<const uint4*>(rec + q * 512 + lane * 16);
+    w[4 * q + 0] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+  }
+  if constexpr ((2 * BITS) % 4) {
+    const uint2 v = *reinterpret_cast<const uint2*>(rec + 512 * ((2 * BITS) / 4) + lane * 8);
+    w[2 * BITS - 2] = v.x; w[2 * BITS - 1] = v.y;
+  }
+  const int gid = lane >> 2;
+  const uint32_t sw = *reinterpret_cast<const uint32_t*>(rec + scales_off(BITS) + 4 * gid);
+  const uint2 zz = *reinterpret_cast<const uint2*>(rec + zeros_off(BITS));   // rows 0..7 | rows 8..15
+  w_tile_regs<BITS, NB8, XS>(w, sw, zz, lane, xrow_s, xr, tot);
+}
+
+// Load the lane's part of one record (code words, scales word, zeros) from shared or global memory.
+template <int BITS>
+__device__ __forceinline__ void load_record(const uint8_t* rec, int lane, uint32_t (&w)[2 * BITS], uint32_t& sw,
+                                            uint2& zz) {
+#pragma unroll
+  for (int q = 0; q < (2 * BITS) / 4; ++q) {
+    const uint4 v = *reinterpret_cast<const uint4*>(rec + q * 512 + lane * 16);
+    w[4 * q + 0] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+  }
+  if constexpr ((2 * BITS) % 4) {
+    const uint2 v = *reinterpret_cast<const uint2*>(rec + 512 * ((2 * BITS) / 4) + lane * 8);
+    w[2 * BITS - 2] = v.x; w[2 * BITS - 1] = v.y;
+  }
+  sw = *reinterpret_cast<const uint32_t*>(rec + scales_off(BITS) + 4 * (lane >> 2));
+  zz = *reinterpret_cast<const uint2*>(rec + zeros_off(BITS));
 }
 
 // x' = x·2^-fp (fp16) of 16 consecutive k of one batch row: `part` (0..7) selects k = 16·part .. +15

@@ -10,9 +10,9 @@
 //   prep      gather x rows per (token, expert) row: bf16 copy (for V·x) and x' = x·2^-fp (fp16)
 //   rank_proj t[row] = V_e·x_row with the natural-k V fragments (one warp per entry, member, 16 ranks;
 //             fixed k order: deterministic)
-//   gemv      items = (entry, row block); 8 warps split the K groups of a row block, each record
-//             decoded exactly as the decode kernel does (w_tile), partials reduced in a fixed order,
-//             U·t (bf16 hi + lo) and the SiLU glue in the epilogue
+//   gemv      one warp per (entry, row block) over all K groups: records decoded exactly as the
+//             decode kernel does (w_tile_regs; the next record's words load while one is decoded),
+//             U·t (bf16 hi + lo) and the SiLU glue in the same warp — no reduction, no barrier
 //   combine   y[t] = Σ_j g[t,j]·dout[row(t,j)] in slot order j
 #include <cuda_bf16.h>
 
@@ -24,7 +24,6 @@ namespace hc {
 namespace {
 
 constexpr int kRouteThreads = 1024;
-constexpr int kMoEWarps = 8;
 
 // Single CTA: T <= 1024 tokens, E <= 256 experts, k <= 16.
 __global__ void moe_route_kernel(const int32_t* __restrict__ idx, int T, int k, int E, MoERoute rt) {
@@ -127,106 +126,115 @@ __global__ void moe_rank_proj_kernel(MoEWin w, MoERoute rt, int max_ent, int max
     }
 }
 
-template <int BITS>
-__global__ void __launch_bounds__(kMoEWarps * 32) moe_gemv_kernel(MoEWin w, MoERoute rt, int max_ent,
-                                                                  const uint16_t* __restrict__ x16,
-                                                                  const float* __restrict__ t, void* out) {
-  __shared__ float red[kMoEWarps][32][8];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
-  const int n_ent = *rt.n_ent;
-  const long long n_items = (long long)n_ent * w.n_rb;
-  const int g0 = warp * w.G / kMoEWarps, g1 = (warp + 1) * w.G / kMoEWarps;
-  for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+// One warp per (entry, row block) over all K: no cross-warp reduction, no CTA barrier; the next
+// record's words are loaded while the current one is decoded (many warps per SM hide the rest).
+template <int BITS, int NB8>
+__global__ void __launch_bounds__(128) moe_gemv_warp_kernel(MoEWin w, MoERoute rt, const uint16_t* __restrict__ x16,
+                                                           const float* __restrict__ t, void* out) {
+  const int lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
+  const long long n_items = (long long)(*rt.n_ent) * w.n_rb;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long it = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < n_items; it += warps) {
     const int ent = (int)(it / w.n_rb), rb = (int)(it % w.n_rb);
     const MoEExpert& ex = w.ex[rt.ent_e[ent]];
     const int row0 = rt.ent_row0[ent], ncol = rt.ent_ncol[ent];
-    float tot[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-    for (int g = g0; g < g1; ++g) {
-      uint32_t xr[2][16];
+    const uint8_t* rec0 = ex.rec + (size_t)rb * w.G * rec_bytes(BITS);
+    float tot[NB8][4];
 #pragma unroll
-      for (int nb = 0; nb < 2; ++nb) {
-        const int col = (lane >> 2) + 8 * nb;
-        const uint4* p = reinterpret_cast<const uint4*>(x16 + (size_t)(row0 + (col < ncol ? col : 0)) * w.K +
-                                                        g * kGroup + 8 * (lane & 3));
+    for (int nb = 0; nb < NB8; ++nb)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) tot[nb][e] = 0.f;
+    const uint16_t* xrow[NB8];
+#pragma unroll
+    for (int nb = 0; nb < NB8; ++nb) {
+      const int col = gid + 8 * nb;
+      xrow[nb] = x16 + (size_t)(row0 + (col < ncol ? col : 0)) * w.K + 8 * tig;
+    }
+    uint32_t wn[2 * BITS], swn;
+    uint2 zzn;
+    load_record<BITS>(rec0, lane, wn, swn, zzn);
+    for (int g = 0; g < w.G; ++g) {
+      uint32_t wc[2 * BITS];
+#pragma unroll
+      for (int i = 0; i < 2 * BITS; ++i) wc[i] = wn[i];
+      const uint32_t swc = swn;
+      const uint2 zzc = zzn;
+      if (g + 1 < w.G) load_record<BITS>(rec0 + (size_t)(g + 1) * rec_bytes(BITS), lane, wn, swn, zzn);
+      uint32_t xr[NB8][16];
+#pragma unroll
+      for (int nb = 0; nb < NB8; ++nb) {
+        const uint4* p = reinterpret_cast<const uint4*>(xrow[nb] + g * kGroup);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const uint4 v = __ldg(p + 4 * q);
           xr[nb][4 * q + 0] = v.x; xr[nb][4 * q + 1] = v.y; xr[nb][4 * q + 2] = v.z; xr[nb][4 * q + 3] = v.w;
         }
       }
-      const uint4* const unused[2] = {nullptr, nullptr};
-      w_tile<BITS, 2, false>(ex.rec + ((size_t)rb * w.G + g) * rec_bytes(BITS), lane, unused, xr, tot);
+      const uint4* unused[NB8] = {};
+      w_tile_regs<BITS, NB8, false>(wc, swc, zzc, lane, unused, xr, tot);
     }
+    // U·t (plain: member 0 on all 16 rows; SiLU window: up chunks on rows 0-7 with t of member 0,
+    // gate chunks on rows 8-15 with t of member 1), then the glue and the output
+    float comp[2][NB8][4];
 #pragma unroll
-    for (int nb = 0; nb < 2; ++nb)
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) red[warp][lane][4 * nb + e] = tot[nb][e];
-    __syncthreads();
-    if (warp == 0) {
-      float fin[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-      for (int ww = 0; ww < kMoEWarps; ++ww)                 // fixed order: deterministic
+      for (int nb = 0; nb < NB8; ++nb)
 #pragma unroll
-        for (int nb = 0; nb < 2; ++nb)
+        for (int e = 0; e < 4; ++e) comp[h][nb][e] = 0.f;
+    const int r_eff = w.glue ? max(ex.r[0], ex.r[1]) : ex.r[0];
+    const int nck = (r_eff + 15) >> 4;
+    for (int c = 0; c < nck; ++c) {
+      const uint4 u = __ldg(ex.U + ((size_t)rb * (ex.rs[0] >> 4) + c) * 32 + lane);
+      const uint32_t af[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-          for (int e = 0; e < 4; ++e) fin[nb][e] += red[ww][lane][4 * nb + e];
-      // U·t: plain windows use member 0 for all 16 rows; a fused SiLU window runs the up chunks (rows
-      // 0-7) with t of member 0 and the gate chunks (rows 8-15) with t of member 1
-      float comp[2][2][4] = {};
-      const int r_eff = w.glue ? max(ex.r[0], ex.r[1]) : ex.r[0];
-      const int nck = (r_eff + 15) >> 4;
-      for (int c = 0; c < nck; ++c) {
-        const uint4 u = __ldg(ex.U + ((size_t)rb * (ex.rs[0] >> 4) + c) * 32 + lane);
-        const uint32_t af[4] = {u.x, u.y, u.z, u.w};
+      for (int h = 0; h < 2; ++h) {
+        if (h == 1 && !w.glue) break;
+        if (16 * c >= ex.r[h]) continue;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          if (h == 1 && !w.glue) break;
-          if (16 * c >= ex.r[h]) continue;
+        for (int nb = 0; nb < NB8; ++nb) {
+          const int col = gid + 8 * nb;
+          const float* tr = t + (size_t)(row0 + (col < ncol ? col : 0)) * w.t_ld + h * (w.t_ld / 2);
+          uint32_t hi[2], lo[2];
 #pragma unroll
-          for (int nb = 0; nb < 2; ++nb) {
-            const int col = gid + 8 * nb;
-            const float* tr = t + (size_t)(row0 + (col < ncol ? col : 0)) * w.t_ld + h * (w.t_ld / 2);
-            uint32_t hi[2], lo[2];
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-              const int rk = 16 * c + 2 * tig + 8 * hh;
-              const float ta = (col < ncol && rk < ex.r[h]) ? tr[rk] : 0.f;
-              const float tb = (col < ncol && rk + 1 < ex.r[h]) ? tr[rk + 1] : 0.f;
-              const uint32_t ha = f32_to_bf16_rn(ta), hb = f32_to_bf16_rn(tb);
-              hi[hh] = ha | (hb << 16);
-              lo[hh] = f32_to_bf16_rn(ta - bf16_bits_to_f32(ha)) | (f32_to_bf16_rn(tb - bf16_bits_to_f32(hb)) << 16);
-            }
-            mma16816(comp[h][nb], af, hi[0], hi[1]);
-            mma16816(comp[h][nb], af, lo[0], lo[1]);
+          for (int hh = 0; hh < 2; ++hh) {
+            const int rk = 16 * c + 2 * tig + 8 * hh;
+            const float ta = (col < ncol && rk < ex.r[h]) ? tr[rk] : 0.f;
+            const float tb = (col < ncol && rk + 1 < ex.r[h]) ? tr[rk + 1] : 0.f;
+            const uint32_t ha = f32_to_bf16_rn(ta), hb = f32_to_bf16_rn(tb);
+            hi[hh] = ha | (hb << 16);
+            lo[hh] = f32_to_bf16_rn(ta - bf16_bits_to_f32(ha)) | (f32_to_bf16_rn(tb - bf16_bits_to_f32(hb)) << 16);
           }
+          mma16816(comp[h][nb], af, hi[0], hi[1]);
+          mma16816(comp[h][nb], af, lo[0], lo[1]);
         }
       }
-      if (w.glue) {
-        uint16_t* m = reinterpret_cast<uint16_t*>(out);
-        const int ldm = w.n_rb * 8;
-#pragma unroll
-        for (int nb = 0; nb < 2; ++nb)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int col = 2 * tig + e + 8 * nb;
-            if (col >= ncol) continue;
-            const float up = fin[nb][e] + comp[0][nb][e];
-            const float gt = fin[nb][e + 2] + comp[1][nb][e + 2];
-            m[(size_t)(row0 + col) * ldm + rb * 8 + gid] = (uint16_t)f32_to_bf16_rn(up * (gt / (1.f + __expf(-gt))));
-          }
-      } else {
-        float* o = reinterpret_cast<float*>(out);
-        const int ldo = w.n_rb * kRows;
-#pragma unroll
-        for (int nb = 0; nb < 2; ++nb)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int col = 2 * tig + (e & 1) + 8 * nb;
-            if (col >= ncol) continue;
-            o[(size_t)(row0 + col) * ldo + rb * kRows + gid + 8 * (e >> 1)] = fin[nb][e] + comp[0][nb][e];
-          }
-      }
     }
-    __syncthreads();
+    if (w.glue) {
+      uint16_t* m = reinterpret_cast<uint16_t*>(out);
+      const int ldm = w.n_rb * 8;
+#pragma unroll
+      for (int nb = 0; nb < NB8; ++nb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = 2 * tig + e + 8 * nb;
+          if (col >= ncol) continue;
+          const float up = tot[nb][e] + comp[0][nb][e];
+          const float gt = tot[nb][e + 2] + comp[1][nb][e + 2];
+          m[(size_t)(row0 + col) * ldm + rb * 8 + gid] = (uint16_t)f32_to_bf16_rn(up * (gt / (1.f + __expf(-gt))));
+        }
+    } else {
+      float* o = reinterpret_cast<float*>(out);
+      const int ldo = w.n_rb * kRows;
+#pragma unroll
+      for (int nb = 0; nb < NB8; ++nb)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int col = 2 * tig + (e & 1) + 8 * nb;
+          if (col >= ncol) continue;
+          o[(size_t)(row0 + col) * ldo + rb * kRows + gid + 8 * (e >> 1)] = tot[nb][e] + comp[0][nb][e];
+        }
+    }
   }
 }
 
@@ -275,18 +283,24 @@ cudaError_t moe_rank_proj(const MoEWin& w, const MoERoute& rt, int max_ent, cons
 }
 
 cudaError_t moe_gemv(const MoEWin& w, int bits, const MoERoute& rt, int max_ent, const uint16_t* x16,
-                     const float* t, void* out, cudaStream_t st) {
+                     const float* t, void* out, int max_cols, cudaStream_t st) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long items = (long long)max_ent * w.n_rb;
-  const unsigned grid = (unsigned)(items < 8LL * sms ? items : 8LL * sms);
+  const long long items = (long long)max_ent * w.n_rb;           // warps needed at most
+  const long long blocks = (items + 3) / 4;
+  const unsigned grid = (unsigned)(blocks < 16LL * sms ? blocks : 16LL * sms);
+  const bool one = max_cols <= 8;                                  // NB8 = 1: at most 8 rows per entry
+#define HC_MOE_LAUNCH(B_)                                                                                       \
+  if (one) moe_gemv_warp_kernel<B_, 1><<<grid, 128, 0, st>>>(w, rt, x16, t, out);                               \
+  else     moe_gemv_warp_kernel<B_, 2><<<grid, 128, 0, st>>>(w, rt, x16, t, out);
   switch (bits) {
-    case 2: moe_gemv_kernel<2><<<grid, kMoEWarps * 32, 0, st>>>(w, rt, max_ent, x16, t, out); break;
-    case 3: moe_gemv_kernel<3><<<grid, kMoEWarps * 32, 0, st>>>(w, rt, max_ent, x16, t, out); break;
-    case 4: moe_gemv_kernel<4><<<grid, kMoEWarps * 32, 0, st>>>(w, rt, max_ent, x16, t, out); break;
+    case 2: HC_MOE_LAUNCH(2) break;
+    case 3: HC_MOE_LAUNCH(3) break;
+    case 4: HC_MOE_LAUNCH(4) break;
     default: return cudaErrorInvalidValue;
   }
+#undef HC_MOE_LAUNCH
   return cudaGetLastError();
 }
 

@@ -45,8 +45,9 @@ cudaError_t moe_rank_proj(const MoEWin& w, const MoERoute& rt, int max_ent, cons
                           cudaStream_t st);
 // Grouped compensated GEMV: out rows of every entry.  glue: out = bf16 m [R][n_rb·8];
 // else out = fp32 [R][n_rb·16].
+// max_cols: an upper bound on the rows of an entry (min(T, 16)): <= 8 selects the 8-column mma variant.
 cudaError_t moe_gemv(const MoEWin& w, int bits, const MoERoute& rt, int max_ent, const uint16_t* x16,
-                     const float* t, void* out, cudaStream_t st);
+                     const float* t, void* out, int max_cols, cudaStream_t st);
 // y[t][n] = Σ_j g[t][j] · dout[tok_row[t][j]][n]   (fixed slot order)
 cudaError_t moe_combine(const float* dout, int N, const float* topk_gate, int T, int k, const MoERoute& rt,
                         float* y, cudaStream_t st);
