@@ -465,6 +465,105 @@ def oracle_c3_sample(seconds: float = 15.0, c=C3, T=16):
     return T / (el / n * c["layers"]), n, el
 
 
+# ------------------------------------------------------------------ workload C4 (prefill, tcgen05)
+C4 = dict(name="c4", model="llama3_8b", hidden=4096, kv=1024, ffn=14336, layers=32, bits=4, group=128, M=2048,
+          r_stored=256)
+
+
+def c4_windows(c=C4):
+    d, kv, f = c["hidden"], c["kv"], c["ffn"]
+    return [(0, [d, kv, kv], d), (1, [d], d), (2, [f, f], d), (3, [d], f)]
+
+
+def run_c4_ours(args, rank, world, device, r_all, c=C4):
+    """Prefill of M = 2048 tokens through 32 Llama-3-8B-shaped layers (4 windows each; UPGATE runs as a
+    plain 2-member window: the SiLU glue is a decode-path fusion), every matrix at rank r_all.  One
+    step = the 128 window GEMMs on the same X (attention and the inter-window activations are out of
+    scope); TFLOPS = algorithmic 2MNK + 2Mr(N+K) over the step."""
+    import torch
+    import paper_2605_05819_b200 as hc
+    M, b, rs = c["M"], c["bits"], c["r_stored"]
+    ctx = hc.Context(device)
+    flops = 0
+    outs = {}
+    for l in range(c["layers"]):
+        mats = []
+        for kind, Ns, K in c4_windows(c):
+            G = K // 128
+            for sl, N in enumerate(Ns):
+                g = torch.Generator(device="cuda").manual_seed(7919 * l + 13 * kind + sl)
+                mats.append(dict(layer=l, window=kind, slot=sl, N=N, K=K, bits=b,
+                                 codes=torch.randint(-2**31, 2**31, (N, K * b // 32), generator=g, device="cuda", dtype=torch.int32),
+                                 scales=((0.5 + torch.rand((N, G), generator=g, device="cuda")) / (21.5 * K) ** 0.5).to(torch.bfloat16),
+                                 zeros=torch.randint(0, 16, (N, G), generator=g, device="cuda", dtype=torch.uint8),
+                                 U=(torch.randn((N, rs), generator=g, device="cuda") / N ** 0.5).to(torch.bfloat16),
+                                 V=(0.05 * torch.randn((rs, K), generator=g, device="cuda") / K ** 0.5).to(torch.bfloat16),
+                                 r_stored=rs, r_alloc=r_all))
+                flops += 2 * M * N * K + 2 * M * r_all * (N + K)
+        ctx.load_layer(mats)
+        del mats
+    torch.cuda.synchronize()
+    xs = {K: torch.randn((M, K), generator=torch.Generator(device="cuda").manual_seed(K), device="cuda").to(torch.bfloat16)
+          for K in (c["hidden"], c["ffn"])}
+    for kind, Ns, K in c4_windows(c):
+        outs[kind] = torch.empty((M, sum(Ns)), dtype=torch.bfloat16, device="cuda")
+    st = torch.cuda.Stream()
+
+    def step():
+        for l in range(c["layers"]):
+            for kind, Ns, K in c4_windows(c):
+                ctx.compensated_linear(l, kind, xs[K], outs[kind], out_dtype=hc.OUT_BF16, stream=st)
+    with torch.cuda.stream(st):
+        step()
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=st):
+            step()
+        for _ in range(max(args.warmup, 3)):
+            graph.replay()
+        torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(device) as clk, torch.cuda.stream(st):
+        e0.record(st)
+        for _ in range(args.steps):
+            graph.replay()
+        e1.record(st)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    finite = bool(all(torch.isfinite(o.float()).all().item() for o in outs.values()))
+    # end to end: host X in, the last window's output back to the host, every window through the API
+    xh = {K: v.cpu() for K, v in xs.items()}
+    yh = np.zeros((M, c["hidden"]), dtype=np.uint16)
+    t0 = time.perf_counter()
+    n_e2e = 1
+    for l in range(c["layers"]):
+        for kind, Ns, K in c4_windows(c):
+            ctx.compensated_linear(l, kind, xh[K], yh if kind in (1, 3) else outs[kind], out_dtype=hc.OUT_BF16)
+    e2e_s = time.perf_counter() - t0
+    ctx.close()
+    return dict(ms=ms, steps=args.steps, clocks=clk.summary, e2e_s=e2e_s, n_e2e=n_e2e, finite=finite, flops=flops,
+                launches=args.steps * c["layers"] * 4 * 3, h2d=c["layers"] * 4 * M * 4096 * 2, d2h=c["layers"] * 2 * M * 4096 * 2)
+
+
+def oracle_c4_sample(seconds: float = 15.0, c=C4, r=64):
+    """The float64 oracle on a bounded sample of C4: the O window (4096x4096, rank r) on 256 of the 2048
+    tokens, repeated; converted to tokens/s of the whole 32-layer prefill step by the flop ratio."""
+    import synth
+    from oracle import linear
+    case = synth.linear_case(41, N=4096, K=4096, bits=4, r_stored=max(r, 16), B=256)
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        linear.compensated_linear(case, r)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or n >= 20:
+            break
+    fl_sample = 2 * 256 * 4096 * 4096 + 2 * 256 * r * (8192)
+    fl_token = sum(2 * N * K + 2 * r * (N + K) for _, Ns, K in c4_windows(c) for N in Ns) * c["layers"]
+    return fl_sample * n / el / fl_token, n, el
+
+
 def cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -478,7 +577,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c5"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--mode", default="auto", choices=["auto", "tp", "replicas"],
                     help="N>1: tp = column-sharded stack with NCCL all-gather (strong scaling, default); "
                          "replicas = independent full-model replicas (weak scaling)")
@@ -494,7 +593,14 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", 0))
     hbm, tflops, peak_src = peaks()
     tp = world > 1 and args.mode in ("auto", "tp")
-    if args.workload == "c3":
+    if args.workload == "c4":
+        r4 = args.rank_override if args.rank_override is not None else 64
+        config = {"workload": f"c4: prefill of 2048 tokens through 32 Llama-3-8B-shaped layers (QKV 6144, O 4096, "
+                              f"UPGATE 2x14336, DOWN 4096x14336), 4-bit g128, rank {r4} on every matrix, tcgen05 GEMM",
+                  "hidden": 4096, "kv": 1024, "ffn": 14336, "layers": 32, "bits": 4, "group": 128, "tokens": 2048,
+                  "rank": r4, "parallelism": f"dp{world}",
+                  "l2": "per-window weights (<= 60 MB) may be L2-resident across replays; prefill is tensor-bound"}
+    elif args.workload == "c3":
         config = {"workload": f"c3: Qwen3-30B-A3B-shaped MoE expert linears (128 experts, top-8, 48 layers), 3-bit g128 + "
                               f"per-expert ranks in {{0, 8, 16}}, {args.batch} routed tokens per step, grouped launches",
                   "hidden": 2048, "expert_ffn": 768, "experts": 128, "topk": 8, "layers": 48, "bits": 3, "group": 128,
@@ -526,6 +632,11 @@ def main():
             val, unit = c1_bytes() * n / el / 1e9, "GB/s"
             sample = f"{n} whole C1 calls (numpy float64, unpack+dequant+matvec)"
             ms = 1e3 * el / n
+        elif args.workload == "c4":
+            val, n, el = oracle_c4_sample(seconds=20.0, r=config["rank"])
+            unit = "tokens/s"
+            sample = f"{n} O-window products (256 tokens, 4096x4096, float64), flop-scaled to the 32-layer step"
+            ms = 1e3 * 2048 / val
         elif args.workload == "c3":
             val, n, el = oracle_c3_sample(seconds=20.0, T=args.batch)
             unit = "tokens/s"
@@ -549,7 +660,11 @@ def main():
     if world > 1:
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
-    if args.workload == "c3":
+    if args.workload == "c4":
+        r = run_c4_ours(args, rank, world, local, config["rank"])
+        nbytes = 0
+        unit, kernel = "tokens/s", "hc::prefill_kernel (tcgen05, 128x256 tiles)"
+    elif args.workload == "c3":
         r = run_c3_ours(args, rank, world, local, args.batch)
         nbytes = r["bytes"]
         unit, kernel = "tokens/s", "hc::moe_gemv_kernel<3> (grouped UPGATE + DOWN per layer)"
@@ -566,7 +681,14 @@ def main():
         torch.distributed.all_reduce(per_rank, op=torch.distributed.ReduceOp.MAX)
     ms_max = float(per_rank.item())
     achieved = nbytes / (r["ms"] / r["steps"] * 1e-3) / 1e9
-    if args.workload == "c1":
+    if args.workload == "c4":
+        value = world * 2048 * r["steps"] / (ms_max * 1e-3)
+        tfl = r["flops"] / (r["ms"] / r["steps"] * 1e-3) / 1e12
+        e2e = {"value": round(2048 * r["n_e2e"] / r["e2e_s"], 2), "unit": "tokens/s",
+               "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]}
+        config["flops_per_step"] = r["flops"]
+        config["output_finite"] = r["finite"]
+    elif args.workload == "c1":
         value = world * nbytes * r["steps"] / (ms_max * 1e-3) / 1e9
         e2e = {"value": round(nbytes * r["n_e2e"] / r["e2e_s"] / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]}
@@ -584,9 +706,12 @@ def main():
                 "warmup": args.warmup, "ms_per_step": round(ms_max / r["steps"], 6), "higher_is_better": True,
                 "scaling": "strong" if tp else "weak", "vs_baseline": None, "dtype": f"bf16 x int{config.get('bits', 4)} (exact int dequant, fp32 accumulate)",
                 "data": "synthetic (seeded on device, random weights of the named shapes)", "config": config,
-                "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
-                             "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": peak_src,
-                             "kernel": kernel, "bytes_per_step": nbytes},
+                "roofline": ({"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
+                              "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": peak_src,
+                              "kernel": kernel, "bytes_per_step": nbytes} if args.workload != "c4" else
+                             {"bound": "tensor", "achieved": round(tfl, 1), "peak": tflops, "unit": "TFLOP/s",
+                              "frac": round(tfl / tflops, 4), "traffic": None, "peak_source": peak_src,
+                              "kernel": kernel, "flops_per_step": r["flops"]}),
                 "clocks": r["clocks"], "gpu_launches": r["launches"], "e2e": e2e}
         if args.workload == "c3" and args.sweep:
             sweep = {}
@@ -609,6 +734,10 @@ def main():
                 n, el = oracle_c1_sample(12.0)
                 line["cpu_baseline"] = {"value": round(nbytes * n / el / 1e9, 4), "unit": "GB/s", "cores": cores(),
                                         "kind": "oracle", "sample": f"{n} whole C1 calls, numpy float64"}
+            elif args.workload == "c4":
+                tps, n, el = oracle_c4_sample(15.0, r=config["rank"])
+                line["cpu_baseline"] = {"value": round(tps, 6), "unit": "tokens/s", "cores": cores(), "kind": "oracle",
+                                        "sample": f"{n} O-window products (256 tokens, float64), flop-scaled"}
             elif args.workload == "c3":
                 tps, n, el = oracle_c3_sample(15.0, T=args.batch)
                 line["cpu_baseline"] = {"value": round(tps, 6), "unit": "tokens/s", "cores": cores(), "kind": "oracle",
