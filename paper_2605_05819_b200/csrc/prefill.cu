@@ -7,9 +7,9 @@
 // same TMEM accumulator.  One CTA computes a 128 (tokens) x 256 (weight rows) tile:
 //   warp 0      TMA producer: X tiles (and T / U tiles for the rank slice, V tiles for T = X·Vᵀ)
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (kind::f16, M=128, N<=256, K=16)
-//   warps 2-5   dequant producers: 4-bit codes -> fp16 s·(q−z) written straight into the UMMA
+//   warps 2-9   dequant producers: 4-bit codes -> fp16 s·(q−z) written straight into the UMMA
 //               K-major 128-byte-swizzled smem layout (exact (q−z), one fp16 rounding of s·(q−z))
-//   warps 6-9   epilogue: tcgen05.ld TMEM -> registers -> fp32 / bf16 / fp16 global stores
+//   warps 10-13 epilogue: tcgen05.ld TMEM -> registers -> fp32 / bf16 / fp16 global stores
 // 4-stage smem ring (48 KB per stage) with full/empty mbarriers; tcgen05.commit releases stages.
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -29,7 +29,11 @@ constexpr int kBBytes = kPBN * kPBK * 2;   // 32 KB
 constexpr int kCBytes = kPBN * kPBK / 2;   // 8 KB of 4-bit codes per stage
 constexpr int kSBytes = kPBN * 2;          // bf16 scales of the stage's group
 constexpr int kZBytes = kPBN;              // zeros
-constexpr int kThreads = 320;
+#ifndef HC_PF_DQW
+#define HC_PF_DQW 8
+#endif
+constexpr int kDqWarps = HC_PF_DQW;        // dequant producer warps (4 or 8): rows per thread = 256 / (32·kDqWarps)
+constexpr int kThreads = (2 + kDqWarps + 4) * 32;
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -149,7 +153,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kPStages; ++s) {
       bar_init(&full_a[s], 1);
-      bar_init(&full_b[s], 128);
+      bar_init(&full_b[s], kDqWarps * 32);
       bar_init(&empty[s], 1);
     }
     bar_init(tmem_full, 1);
@@ -212,9 +216,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       umma_commit(tmem_full);
     }
-  } else if (warp < 6) {
+  } else if (warp < 2 + kDqWarps) {
     // ======================= dequant producers (smem -> smem) =======================
-    const int t = threadIdx.x - 64;            // 0..127: rows t and t + 128 of the B tile
+    const int t = threadIdx.x - 64;            // rows t, t + 32·kDqWarps, ... of the B tile
     for (int i = 0; i < nkb; ++i) {
       const int s = i % kPStages;
       bar_wait(&full_a[s], (i / kPStages) & 1);   // codes of this stage landed (and stage s is free)
@@ -222,8 +226,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* tile = sB + s * kBBytes;
         const uint8_t* codes = sC + s * kCBytes;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int row = t + 128 * h;
+        for (int h = 0; h < 256 / (32 * kDqWarps); ++h) {
+          const int row = t + 32 * kDqWarps * h;
           const uint4 c0 = *reinterpret_cast<const uint4*>(codes + row * 32);
           const uint4 c1 = *reinterpret_cast<const uint4*>(codes + row * 32 + 16);
           const uint32_t words[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
