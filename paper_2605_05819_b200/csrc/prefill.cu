@@ -10,7 +10,9 @@
 //   warps 2-9   dequant producers: 4-bit codes -> fp16 s·(q−z) written straight into the UMMA
 //               K-major 128-byte-swizzled smem layout (exact (q−z), one fp16 rounding of s·(q−z))
 //   warps 10-13 epilogue: tcgen05.ld TMEM -> registers -> fp32 / bf16 / fp16 global stores
-// 4-stage smem ring (48 KB per stage) with full/empty mbarriers; tcgen05.commit releases stages.
+// 3-stage smem ring (~57 KB per stage) with full/empty mbarriers; tcgen05.commit releases stages.
+// Persistent CTAs (one per SM) loop over tiles; the TMEM accumulator is double-buffered (2 x 256
+// columns) with tmem_full / tmem_empty barriers, so a tile's epilogue overlaps the next main loop.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -122,6 +124,28 @@ __device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t b, uint32_t
 
 }  // namespace
 
+// Work item w (persistent loop): tile = w % n_tiles (M-fastest, so the CTAs running concurrently
+// share weight tiles through L2), split-K slice ks = w / n_tiles.
+struct TileWork {
+  int m0, n0, ks, kb_lo, nkb1, nkb;
+};
+__device__ __forceinline__ TileWork tile_work(const PArgs& p, int w) {
+  TileWork t;
+  const int n_tiles = p.tiles_m * p.tiles_n;
+  const int tile = w % n_tiles;
+  t.ks = w / n_tiles;
+  t.m0 = (tile % p.tiles_m) * kPBM;
+  t.n0 = (tile / p.tiles_m) * kPBN;
+  const int nkb_all = p.K / kPBK;
+  t.kb_lo = t.ks * nkb_all / p.ksplit;
+  t.nkb1 = (t.ks + 1) * nkb_all / p.ksplit - t.kb_lo;
+  t.nkb = t.nkb1 + (p.K2 + kPBK - 1) / kPBK;
+  return t;
+}
+
+// Persistent: each CTA loops over work items; the producer / MMA / dequant roles run one continuous
+// stage sequence across tiles, and the accumulator is double-buffered in TMEM (2 x 256 columns) so
+// the epilogue of tile j overlaps the main loop of tile j + 1.
 __global__ void __launch_bounds__(kThreads, 1)
     prefill_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
@@ -136,19 +160,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* full_a = reinterpret_cast<uint64_t*>(sZ + kPStages * kZBytes);
   uint64_t* full_b = full_a + kPStages;
   uint64_t* empty = full_b + kPStages;
-  uint64_t* tmem_full = empty + kPStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tmem_full = empty + kPStages;      // [2]
+  uint64_t* tmem_empty = tmem_full + 2;        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_tiles = p.tiles_m * p.tiles_n;
-  const int tile = blockIdx.x % n_tiles, ks = blockIdx.x / n_tiles;
-  const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
-  const int m0 = tm * kPBM, n0 = tn * kPBN;
-  const int nkb_all = p.K / kPBK;
-  const int kb_lo = ks * nkb_all / p.ksplit, kb_hi = (ks + 1) * nkb_all / p.ksplit;
-  const int nkb1 = kb_hi - kb_lo;                        // main k-blocks of this CTA
-  const int nkb2 = (p.K2 + kPBK - 1) / kPBK;             // rank-slice k-blocks
-  const int nkb = nkb1 + nkb2;
+  const int n_work = p.tiles_m * p.tiles_n * p.ksplit;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kPStages; ++s) {
@@ -156,13 +173,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       bar_init(&full_b[s], kDqWarps * 32);
       bar_init(&empty[s], 1);
     }
-    bar_init(tmem_full, 1);
+    bar_init(&tmem_full[0], 1); bar_init(&tmem_full[1], 1);
+    bar_init(&tmem_empty[0], 4); bar_init(&tmem_empty[1], 4);   // one arrive per epilogue warp
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_u32(tmem_slot)),
-                 "r"(256)
+                 "r"(512)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -174,27 +192,31 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ======================= TMA producer =======================
     if (lane == 0) {
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % kPStages;
-        if (i >= kPStages) bar_wait(&empty[s], ((i / kPStages) + 1) & 1);
-        const bool main = i < nkb1;
-        const int kb = kb_lo + i;
-        if (main && p.b_mode == 0) {
-          // X tile + this k-block's codes (256 rows x 32 B) + the group's scales and zeros
-          bar_expect_tx(&full_a[s], (uint32_t)(kABytes + kCBytes + kSBytes + kZBytes));
-          tma_2d(sA + s * kABytes, &tmA, kb * kPBK, m0, &full_a[s]);
-          tma_2d(sC + s * kCBytes, &tmC, kb * (kPBK / 8), n0, &full_a[s]);
-          const int g = kb >> 1;
-          bulk_1d(sS + s * kSBytes, p.scales_t + (size_t)g * p.N + n0, kSBytes, &full_a[s]);
-          bulk_1d(sZ + s * kZBytes, p.zeros_t + (size_t)g * p.N + n0, kZBytes, &full_a[s]);
-        } else if (main) {
-          bar_expect_tx(&full_a[s], (uint32_t)(kABytes + kBBytes));
-          tma_2d(sA + s * kABytes, &tmA, kb * kPBK, m0, &full_a[s]);
-          tma_2d(sB + s * kBBytes, &tmB, kb * kPBK, n0, &full_a[s]);
-        } else {
-          bar_expect_tx(&full_a[s], (uint32_t)(kABytes + kBBytes));
-          tma_2d(sA + s * kABytes, &tmA2, (i - nkb1) * kPBK, m0, &full_a[s]);
-          tma_2d(sB + s * kBBytes, &tmB2, (i - nkb1) * kPBK, n0, &full_a[s]);
+      int ig = 0;                                   // global stage counter of this CTA
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+        const TileWork tw = tile_work(p, w);
+        for (int i = 0; i < tw.nkb; ++i, ++ig) {
+          const int s = ig % kPStages;
+          if (ig >= kPStages) bar_wait(&empty[s], ((ig / kPStages) + 1) & 1);
+          const bool main = i < tw.nkb1;
+          const int kb = tw.kb_lo + i;
+          if (main && p.b_mode == 0) {
+            // X tile + this k-block's codes (256 rows x 32 B) + the group's scales and zeros
+            bar_expect_tx(&full_a[s], (uint32_t)(kABytes + kCBytes + kSBytes + kZBytes));
+            tma_2d(sA + s * kABytes, &tmA, kb * kPBK, tw.m0, &full_a[s]);
+            tma_2d(sC + s * kCBytes, &tmC, kb * (kPBK / 8), tw.n0, &full_a[s]);
+            const int g = kb >> 1;
+            bulk_1d(sS + s * kSBytes, p.scales_t + (size_t)g * p.N + tw.n0, kSBytes, &full_a[s]);
+            bulk_1d(sZ + s * kZBytes, p.zeros_t + (size_t)g * p.N + tw.n0, kZBytes, &full_a[s]);
+          } else if (main) {
+            bar_expect_tx(&full_a[s], (uint32_t)(kABytes + kBBytes));
+            tma_2d(sA + s * kABytes, &tmA, kb * kPBK, tw.m0, &full_a[s]);
+            tma_2d(sB + s * kBBytes, &tmB, kb * kPBK, tw.n0, &full_a[s]);
+          } else {
+            bar_expect_tx(&full_a[s], (uint32_t)(kABytes + kBBytes));
+            tma_2d(sA + s * kABytes, &tmA2, (i - tw.nkb1) * kPBK, tw.m0, &full_a[s]);
+            tma_2d(sB + s * kBBytes, &tmB2, (i - tw.nkb1) * kPBK, tw.n0, &full_a[s]);
+          }
         }
       }
     }
@@ -202,112 +224,132 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ======================= MMA issuer (one thread) =======================
     if (lane == 0) {
       const uint32_t idesc = umma_idesc(p.n_dim);
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % kPStages;
-        const uint32_t ph = (i / kPStages) & 1;
-        bar_wait(&full_a[s], ph);
-        bar_wait(&full_b[s], ph);
+      int ig = 0, j = 0;
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++j) {
+        const TileWork tw = tile_work(p, w);
+        const int buf = j & 1;
+        if (j >= 2) bar_wait(&tmem_empty[buf], ((j >> 1) + 1) & 1);   // epilogue of tile j - 2 drained it
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int nk = i < nkb1 ? kPBK / 16 : min(kPBK, p.K2 - (i - nkb1) * kPBK) / 16;
-        const uint64_t ad = umma_desc(sA + s * kABytes), bd = umma_desc(sB + s * kBBytes);
-        for (int k = 0; k < nk; ++k)   // advance 16 fp16 = 32 bytes along K inside the swizzled rows
-          umma_f16(tmem_base, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc, (i | k) != 0);
-        umma_commit(&empty[s]);
+        const uint32_t acc = tmem_base + (uint32_t)(buf * kPBN);
+        for (int i = 0; i < tw.nkb; ++i, ++ig) {
+          const int s = ig % kPStages;
+          const uint32_t ph = (ig / kPStages) & 1;
+          bar_wait(&full_a[s], ph);
+          bar_wait(&full_b[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const int nk = i < tw.nkb1 ? kPBK / 16 : min(kPBK, p.K2 - (i - tw.nkb1) * kPBK) / 16;
+          const uint64_t ad = umma_desc(sA + s * kABytes), bd = umma_desc(sB + s * kBBytes);
+          for (int k = 0; k < nk; ++k)   // advance 16 fp16 = 32 bytes along K inside the swizzled rows
+            umma_f16(acc, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc, (i | k) != 0);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tmem_full[buf]);
       }
-      umma_commit(tmem_full);
     }
   } else if (warp < 2 + kDqWarps) {
     // ======================= dequant producers (smem -> smem) =======================
     const int t = threadIdx.x - 64;            // rows t, t + 32·kDqWarps, ... of the B tile
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % kPStages;
-      bar_wait(&full_a[s], (i / kPStages) & 1);   // codes of this stage landed (and stage s is free)
-      if (i < nkb1 && p.b_mode == 0) {
-        uint8_t* tile = sB + s * kBBytes;
-        const uint8_t* codes = sC + s * kCBytes;
+    int ig = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+      const TileWork tw = tile_work(p, w);
+      for (int i = 0; i < tw.nkb; ++i, ++ig) {
+        const int s = ig % kPStages;
+        bar_wait(&full_a[s], (ig / kPStages) & 1);   // codes of this stage landed (and stage s is free)
+        if (i < tw.nkb1 && p.b_mode == 0) {
+          uint8_t* tile = sB + s * kBBytes;
+          const uint8_t* codes = sC + s * kCBytes;
 #pragma unroll
-        for (int h = 0; h < 256 / (32 * kDqWarps); ++h) {
-          const int row = t + 32 * kDqWarps * h;
-          const uint4 c0 = *reinterpret_cast<const uint4*>(codes + row * 32);
-          const uint4 c1 = *reinterpret_cast<const uint4*>(codes + row * 32 + 16);
-          const uint32_t words[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-          const float sf = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(sS + s * kSBytes)[row] << 16);
-          const uint32_t sc = (uint32_t)__half_as_ushort(__float2half_rn(sf)) * 0x00010001u;      // half2(s, s)
-          const uint32_t zz = (0x6400u + (uint32_t)(sZ + s * kZBytes)[row]) * 0x00010001u;       // half2(1024+z)
+          for (int h = 0; h < 256 / (32 * kDqWarps); ++h) {
+            const int row = t + 32 * kDqWarps * h;
+            const uint4 c0 = *reinterpret_cast<const uint4*>(codes + row * 32);
+            const uint4 c1 = *reinterpret_cast<const uint4*>(codes + row * 32 + 16);
+            const uint32_t words[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+            const float sf = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(sS + s * kSBytes)[row] << 16);
+            const uint32_t sc = (uint32_t)__half_as_ushort(__float2half_rn(sf)) * 0x00010001u;      // half2(s, s)
+            const uint32_t zz = (0x6400u + (uint32_t)(sZ + s * kZBytes)[row]) * 0x00010001u;       // half2(1024+z)
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {        // word c = k 8c..8c+7 = 16-byte chunk c of the row
-            uint32_t v[4];
+            for (int c = 0; c < 8; ++c) {        // word c = k 8c..8c+7 = 16-byte chunk c of the row
+              uint32_t v[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              uint32_t hv = lop3_and_or(words[c] >> (4 * j), 0x000F000Fu, 0x64006400u);   // half2(1024 + q)
-              __half2 d = __hsub2(*reinterpret_cast<__half2*>(&hv), *reinterpret_cast<const __half2*>(&zz));
-              d = __hmul2(d, *reinterpret_cast<const __half2*>(&sc));                      // fp16(s·(q − z))
-              v[j] = *reinterpret_cast<uint32_t*>(&d);
+              for (int jj = 0; jj < 4; ++jj) {
+                uint32_t hv = lop3_and_or(words[c] >> (4 * jj), 0x000F000Fu, 0x64006400u);   // half2(1024 + q)
+                __half2 d = __hsub2(*reinterpret_cast<__half2*>(&hv), *reinterpret_cast<const __half2*>(&zz));
+                d = __hmul2(d, *reinterpret_cast<const __half2*>(&sc));                       // fp16(s·(q − z))
+                v[jj] = *reinterpret_cast<uint32_t*>(&d);
+              }
+              *reinterpret_cast<uint4*>(tile + sw128(row, c)) = make_uint4(v[0], v[1], v[2], v[3]);
             }
-            *reinterpret_cast<uint4*>(tile + sw128(row, c)) = make_uint4(v[0], v[1], v[2], v[3]);
           }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
+        bar_arrive(&full_b[s]);
       }
-      bar_arrive(&full_b[s]);
     }
   } else {
     // ======================= epilogue =======================
     const int q = warp & 3;                    // TMEM lane quadrant this warp may access
-    const int m = m0 + 32 * q + lane;
-    bar_wait(tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    void* outp = p.ksplit > 1 ? (void*)(reinterpret_cast<float*>(p.out) + (size_t)ks * p.M * p.ldo) : p.out;
-    for (int c0 = 0; c0 < p.n_dim; c0 += 32) {
-      uint32_t v[32];
-      const uint32_t addr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-            "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-            "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-          : "r"(addr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      const int n = n0 + c0;
-      if (m < p.M && n < p.N) {
-        if (p.out_type == 0) {
-          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(outp) + (size_t)m * p.ldo + n);
+    int j = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++j) {
+      const TileWork tw = tile_work(p, w);
+      const int buf = j & 1;
+      const int m = tw.m0 + 32 * q + lane;
+      bar_wait(&tmem_full[buf], (j >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      void* outp = p.ksplit > 1 ? (void*)(reinterpret_cast<float*>(p.out) + (size_t)tw.ks * p.M * p.ldo) : p.out;
+      for (int c0 = 0; c0 < p.n_dim; c0 += 32) {
+        uint32_t v[32];
+        const uint32_t addr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * kPBN + c0);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(addr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const int n = tw.n0 + c0;
+        if (m < p.M && n < p.N) {
+          if (p.out_type == 0) {
+            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(outp) + (size_t)m * p.ldo + n);
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
-                                 __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
-        } else {
-          uint32_t pk[16];
+            for (int i = 0; i < 8; ++i)
+              dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                   __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+          } else {
+            uint32_t pk[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float a = __uint_as_float(v[2 * i]), b = __uint_as_float(v[2 * i + 1]);
-            if (p.out_type == 1) {
-              __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
-              pk[i] = *reinterpret_cast<uint32_t*>(&h2);
-            } else {
-              __half2 h2 = __floats2half2_rn(a, b);
-              pk[i] = *reinterpret_cast<uint32_t*>(&h2);
+            for (int i = 0; i < 16; ++i) {
+              const float a = __uint_as_float(v[2 * i]), b = __uint_as_float(v[2 * i + 1]);
+              if (p.out_type == 1) {
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+                pk[i] = *reinterpret_cast<uint32_t*>(&h2);
+              } else {
+                __half2 h2 = __floats2half2_rn(a, b);
+                pk[i] = *reinterpret_cast<uint32_t*>(&h2);
+              }
             }
-          }
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(outp) + (size_t)m * p.ldo + n);
+            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(outp) + (size_t)m * p.ldo + n);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+            for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+          }
         }
       }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) bar_arrive(&tmem_empty[buf]);   // this warp's quadrant of buffer buf is drained
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512) : "memory");
   }
 }
 
 static size_t prefill_smem() {
-  return (size_t)kPStages * (kABytes + kBBytes + kCBytes + kSBytes + kZBytes) + (3 * kPStages + 2) * 8 + 1024;
+  return (size_t)kPStages * (kABytes + kBBytes + kCBytes + kSBytes + kZBytes) + (3 * kPStages + 5) * 8 + 1024;
 }
 
 cudaError_t launch_prefill(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmA2,
@@ -318,7 +360,15 @@ cudaError_t launch_prefill(const CUtensorMap& tmA, const CUtensorMap& tmB, const
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  prefill_kernel<<<p.tiles_m * p.tiles_n * p.ksplit, kThreads, prefill_smem(), st>>>(tmA, tmB, tmA2, tmB2, tmC, p);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int n_work = p.tiles_m * p.tiles_n * p.ksplit;
+  const int grid = n_work < sms ? n_work : sms;      // persistent: one CTA per SM (smem-limited)
+  prefill_kernel<<<grid, kThreads, prefill_smem(), st>>>(tmA, tmB, tmA2, tmB2, tmC, p);
   return cudaGetLastError();
 }
 
