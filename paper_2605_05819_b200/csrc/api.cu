@@ -49,8 +49,18 @@ struct Member {
   int cap() const { return std::min(std::min(r_stored, N), K); }
 };
 
+// Prefill copies of a multi-member window merged into one GEMM (rows concatenated, rank slices
+// stacked: T = X·[V_0[:r_0]; V_1[:r_1]; ...]ᵀ and a block-diagonal U), rebuilt when ranks change.
+struct PrefillMerged {
+  DevBuf codes, scales, zeros, V, U;
+  std::vector<int> ranks;      // r_alloc of each member the buffers were built for
+  int R = 0;                   // Σ ceil16(r_i)
+  bool valid = false;
+};
+
 struct Window {
   int layer = 0, kind = 0, expert = -1;
+  std::shared_ptr<PrefillMerged> pm = std::make_shared<PrefillMerged>();
   int glue = HC_GLUE_NONE;            // SILU_MUL: members[0] = up (interleaved records), [1] = gate
   std::vector<Member> members;        // sorted by slot
   DevBuf tacc, cnt;                   // launch workspace: fixed-point t, counters (self-resetting)
@@ -109,6 +119,7 @@ struct hc_ctx {
   DevBuf moe_ws, moe_idx, moe_gate;
   void invalidate_graphs() {
     graphs.clear();
+    for (auto& kv : windows) kv.second.pm->valid = false;
     for (auto& kv : moe) kv.second.valid = false;
   }
 };
@@ -554,6 +565,47 @@ static hc_status launch_window(hc_ctx* ctx, Window& w, const void* x, int ldx, i
 
 // Prefill / batched (B > 16) window: per member, T = X·V[:r]ᵀ (tcgen05, fp16 out) then
 // Y = X·deq(W)ᵀ + T·U[:, :r]ᵀ (tcgen05, dequant producers + rank slice in the same accumulator).
+static hc_status build_prefill_merged(Window& w, cudaStream_t st) {
+  PrefillMerged& P = *w.pm;
+  std::vector<int> rk;
+  for (const Member& m : w.members) rk.push_back(m.r_alloc);
+  if (P.valid && P.ranks == rk) return HC_OK;
+  const int K = w.members.front().K, G = K / kGroup;
+  int N = 0, R = 0;
+  for (const Member& m : w.members) { N += m.rows(); R += (m.r_alloc + 15) / 16 * 16; }
+  if (R > 256) return fail(HC_ERR_CONFIG, "merged prefill rank slice %d > 256", R);
+  CUDA_TRY(P.codes.alloc((size_t)N * (K / 8) * 4));
+  CUDA_TRY(P.scales.alloc((size_t)G * N * 2));
+  CUDA_TRY(P.zeros.alloc((size_t)G * N));
+  if (R > 0) {
+    CUDA_TRY(P.V.alloc((size_t)R * K * 2));
+    CUDA_TRY(P.U.alloc((size_t)N * R * 2));
+    CUDA_TRY(cudaMemsetAsync(P.V.p, 0, P.V.bytes, st));
+    CUDA_TRY(cudaMemsetAsync(P.U.p, 0, P.U.bytes, st));
+  }
+  int row = 0, roff = 0;
+  for (const Member& m : w.members) {
+    const int rows = m.rows(), r = m.r_alloc;
+    CUDA_TRY(cudaMemcpyAsync((uint32_t*)P.codes.p + (size_t)row * (K / 8), m.pcodes->p, (size_t)rows * (K / 8) * 4,
+                             cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaMemcpy2DAsync((uint16_t*)P.scales.p + row, (size_t)N * 2, m.pscales->p, (size_t)rows * 2, (size_t)rows * 2,
+                               G, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaMemcpy2DAsync((uint8_t*)P.zeros.p + row, (size_t)N, m.pzeros->p, (size_t)rows, (size_t)rows, G,
+                               cudaMemcpyDeviceToDevice, st));
+    if (r > 0) {
+      CUDA_TRY(cudaMemcpyAsync((uint16_t*)P.V.p + (size_t)roff * K, m.V16->p, (size_t)r * K * 2, cudaMemcpyDeviceToDevice, st));
+      CUDA_TRY(cudaMemcpy2DAsync((uint16_t*)P.U.p + (size_t)row * R + roff, (size_t)R * 2, m.U16->p, (size_t)m.r_stored * 2,
+                                 (size_t)r * 2, rows, cudaMemcpyDeviceToDevice, st));
+    }
+    row += rows;
+    roff += (r + 15) / 16 * 16;
+  }
+  P.R = R;
+  P.ranks = rk;
+  P.valid = true;
+  return HC_OK;
+}
+
 static hc_status launch_prefill_window(hc_ctx* ctx, Window& w, const void* x, int M, void* y, int y_dtype,
                                        cudaStream_t st) {
   if (w.glue != HC_GLUE_NONE) return fail(HC_ERR_CONFIG, "prefill of a fused SiLU window is not supported");
@@ -568,6 +620,40 @@ static hc_status launch_prefill_window(hc_ctx* ctx, Window& w, const void* x, in
   const int64_t ldy = w.out_rows();
   CUtensorMap tmX, tmV, tmT, tmU;
   if (!encode_tmap_f16(&tmX, ctx->p_x16.p, K, M, K, kPBM)) return fail(HC_ERR_RUNTIME, "tensor map (X) encoding failed");
+  int R_merged = 0;
+  for (const Member& m : w.members) R_merged += (m.r_alloc + 15) / 16 * 16;
+  const char* pe = getenv("HC_PREFILL_MERGE");                // "0": one GEMM per member (A/B testing)
+  if (w.members.size() > 1 && R_merged <= 256 && !(pe && pe[0] == '0')) {
+    // one GEMM over all members: concatenated rows, stacked rank slices, block-diagonal U
+    hc_status s = build_prefill_merged(w, st);
+    if (s != HC_OK) return s;
+    const PrefillMerged& P = *w.pm;
+    const int N = (int)ldy, R = P.R, tw = (R + 63) / 64 * 64;
+    CUtensorMap tmC;
+    if (!encode_tmap_codes(&tmC, P.codes.p, K / 8, N)) return fail(HC_ERR_RUNTIME, "tensor map (codes) encoding failed");
+    if (R > 0) {
+      const int tiles_m = (M + kPBM - 1) / kPBM;
+      const int ksplit = std::max(1, std::min(K / kPBK / 4, (ctx->sms + tiles_m - 1) / tiles_m));
+      if (ctx->p_t16.bytes < (size_t)M * tw * 2) CUDA_TRY(ctx->p_t16.alloc((size_t)M * tw * 2));
+      if (ctx->p_tpart.bytes < (size_t)ksplit * M * tw * 4) CUDA_TRY(ctx->p_tpart.alloc((size_t)ksplit * M * tw * 4));
+      if (!encode_tmap_f16(&tmV, P.V.p, K, R, K, kPBN)) return fail(HC_ERR_RUNTIME, "tensor map (V) encoding failed");
+      PArgs pt{};
+      pt.M = M; pt.N = tw; pt.K = K; pt.K2 = 0; pt.n_dim = R; pt.b_mode = 1; pt.ksplit = ksplit;
+      pt.out = ctx->p_tpart.p; pt.ldo = tw; pt.out_type = 0;
+      pt.tiles_m = tiles_m; pt.tiles_n = 1;
+      CUDA_TRY(launch_prefill(tmX, tmV, tmX, tmX, tmC, pt, st));
+      CUDA_TRY(launch_splitk_reduce_f16((const float*)ctx->p_tpart.p, ksplit, M, tw, (uint16_t*)ctx->p_t16.p, st));
+      if (!encode_tmap_f16(&tmT, ctx->p_t16.p, tw, M, tw, kPBM)) return fail(HC_ERR_RUNTIME, "tensor map (T) encoding failed");
+      if (!encode_tmap_f16(&tmU, P.U.p, R, N, R, kPBN)) return fail(HC_ERR_RUNTIME, "tensor map (U) encoding failed");
+    }
+    PArgs pm{};
+    pm.M = M; pm.N = N; pm.K = K; pm.K2 = R; pm.n_dim = kPBN; pm.b_mode = 0; pm.ksplit = 1;
+    pm.scales_t = (const uint16_t*)P.scales.p; pm.zeros_t = (const uint8_t*)P.zeros.p;
+    pm.out = y; pm.ldo = N; pm.out_type = y_dtype == HC_OUT_F32 ? 0 : 1;
+    pm.tiles_m = (M + kPBM - 1) / kPBM; pm.tiles_n = N / kPBN;
+    CUDA_TRY(launch_prefill(tmX, tmX, R > 0 ? tmT : tmX, R > 0 ? tmU : tmX, tmC, pm, st));
+    return HC_OK;
+  }
   int row_off = 0;
   for (const Member& m : w.members) {
     const int r = m.r_alloc, rpad = (r + 15) / 16 * 16, tw = (rpad + 63) / 64 * 64;

@@ -101,3 +101,33 @@ def test_prefill_c4_shape_sampled(hc, ctx):
     rows = synth.rng(1).choice(M, size=64, replace=False)
     ref = linear.compensated_linear(case, 64, x_bits=case["x"][rows])
     assert rel(y.cpu().numpy()[rows], ref) <= TOL
+
+
+def test_prefill_merged_window_matches_per_member(hc, ctx, monkeypatch):
+    """A multi-member window runs as ONE GEMM (rows concatenated, rank slices stacked, block-diagonal U);
+    it must agree with the oracle, with the per-member launches (HC_PREFILL_MERGE=0), and follow rank
+    changes (the merged copies are rebuilt)."""
+    M, K = 384, 1024
+    cases = [synth.linear_case(800 + i, N=n, K=K, bits=4, r_stored=32, B=M, zeros="asym")
+             for i, n in enumerate((512, 256, 256))]
+    L = nl()
+    for ranks in ((32, 8, 0), (0, 16, 32)):
+        for s, (c, r) in enumerate(zip(cases, ranks)):
+            ctx.load_layer([desc(c, L, 0, s, r)])
+        x = dev(cases[0]["x"])
+        y = torch.empty((M, 1024), dtype=torch.float32, device="cuda")
+        ctx.compensated_linear(L, 0, x, y)
+        monkeypatch.setenv("HC_PREFILL_MERGE", "0")
+        y2 = torch.empty_like(y)
+        ctx.compensated_linear(L, 0, x, y2)
+        monkeypatch.delenv("HC_PREFILL_MERGE")
+        torch.cuda.synchronize()
+        ref = linear.window_linear(cases, list(ranks), cases[0]["x"])
+        assert rel(y.cpu().numpy(), ref) <= TOL
+        assert rel(y.cpu().numpy(), y2.cpu().numpy()) <= 1e-6
+    # rank change through hc_set_rank rebuilds the merged rank slice
+    ctx.set_rank(L, 0, 0, 8)
+    y = torch.empty((M, 1024), dtype=torch.float32, device="cuda")
+    ctx.compensated_linear(L, 0, dev(cases[0]["x"]), y)
+    torch.cuda.synchronize()
+    assert rel(y.cpu().numpy(), linear.window_linear(cases, [8, 16, 32], cases[0]["x"])) <= TOL
