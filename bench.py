@@ -564,6 +564,19 @@ def oracle_c4_sample(seconds: float = 15.0, c=C4, r=64):
     return fl_sample * n / el / fl_token, n, el
 
 
+def traffic_of(args):
+    """DRAM bytes per step of the dominant kernel from one ncu --set full capture (profiles/r01/
+    ncu_c2_layer_dram.json: the 4 decode windows of one C2 layer, 111.3 MB, x 32 layers); the algorithmic
+    bytes of the same step are config.bytes_per_step.  Null where no capture exists."""
+    if args.workload == "c2" and args.batch == 1:
+        try:
+            with open(os.path.join(ROOT, "profiles", "r01", "ncu_c2_layer_dram.json")) as f:
+                return round(json.load(f)["layer_dram_MB"] * 1e6 * 32)
+        except Exception:
+            return None
+    return None
+
+
 def cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -707,7 +720,7 @@ def main():
                 "scaling": "strong" if tp else "weak", "vs_baseline": None, "dtype": f"bf16 x int{config.get('bits', 4)} (exact int dequant, fp32 accumulate)",
                 "data": "synthetic (seeded on device, random weights of the named shapes)", "config": config,
                 "roofline": ({"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
-                              "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": peak_src,
+                              "frac": round(achieved / hbm, 4), "traffic": traffic_of(args), "peak_source": peak_src,
                               "kernel": kernel, "bytes_per_step": nbytes} if args.workload != "c4" else
                              {"bound": "tensor", "achieved": round(tfl, 1), "peak": tflops, "unit": "TFLOP/s",
                               "frac": round(tfl / tflops, 4), "traffic": None, "peak_source": peak_src,
