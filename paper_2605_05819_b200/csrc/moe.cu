@@ -25,10 +25,12 @@ namespace {
 
 constexpr int kRouteThreads = 1024;
 
-// Single CTA: T <= 1024 tokens, E <= 256 experts, k <= 16.
+// Single CTA: T <= 1024 tokens, E <= 256 experts, k <= 16.  Per-expert token bitmaps (order-free
+// atomicOr), per-expert counts and entry counts by one thread per expert, exclusive scans over the
+// experts (one warp, fixed order), then every (token, slot) finds its row by popcount.
 __global__ void moe_route_kernel(const int32_t* __restrict__ idx, int T, int k, int E, MoERoute rt) {
   extern __shared__ unsigned bm[];                 // [E][W] token bitmaps, W = ceil(T/32)
-  __shared__ int off[257];
+  __shared__ int cnt[256], ecnt[256], off[257], eoff[257];
   const int W = (T + 31) / 32;
   for (int i = threadIdx.x; i < E * W; i += blockDim.x) bm[i] = 0u;
   __syncthreads();
@@ -37,25 +39,39 @@ __global__ void moe_route_kernel(const int32_t* __restrict__ idx, int T, int k, 
     if (e >= 0 && e < E) atomicOr(&bm[e * W + (t >> 5)], 1u << (t & 31));
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int o = 0, ne = 0;
-    for (int e = 0; e < E; ++e) {
-      int c = 0;
-      for (int w = 0; w < W; ++w) c += __popc(bm[e * W + w]);
-      off[e] = o;
-      for (int r = 0; r < c; r += 16) {
-        rt.ent_e[ne] = e;
-        rt.ent_row0[ne] = o + r;
-        rt.ent_ncol[ne] = min(16, c - r);
-        ++ne;
-      }
-      o += c;
-    }
-    off[E] = o;
-    *rt.n_rows = o;
-    *rt.n_ent = ne;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int c = 0;
+    for (int w = 0; w < W; ++w) c += __popc(bm[e * W + w]);
+    cnt[e] = c;
+    ecnt[e] = (c + 15) / 16;
   }
   __syncthreads();
+  if (threadIdx.x < 32) {                          // exclusive scans of cnt and ecnt (E <= 256)
+    const int lane = threadIdx.x;
+    int base_r = 0, base_e = 0;
+    for (int e0 = 0; e0 < E; e0 += 32) {
+      const int e = e0 + lane;
+      int vr = e < E ? cnt[e] : 0, ve = e < E ? ecnt[e] : 0;
+      int sr = vr, se = ve;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int tr = __shfl_up_sync(0xffffffffu, sr, o), te = __shfl_up_sync(0xffffffffu, se, o);
+        if (lane >= o) { sr += tr; se += te; }
+      }
+      if (e < E) { off[e] = base_r + sr - vr; eoff[e] = base_e + se - ve; }
+      base_r += __shfl_sync(0xffffffffu, sr, 31);
+      base_e += __shfl_sync(0xffffffffu, se, 31);
+    }
+    if (lane == 0) { off[E] = base_r; eoff[E] = base_e; *rt.n_rows = base_r; *rt.n_ent = base_e; }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    for (int j = 0; j < ecnt[e]; ++j) {
+      const int ne = eoff[e] + j;
+      rt.ent_e[ne] = e;
+      rt.ent_row0[ne] = off[e] + 16 * j;
+      rt.ent_ncol[ne] = min(16, cnt[e] - 16 * j);
+    }
   for (int i = threadIdx.x; i < T * k; i += blockDim.x) {
     const int e = idx[i], t = i / k;
     if (e < 0 || e >= E) { rt.tok_row[i] = -1; continue; }
@@ -103,26 +119,51 @@ __global__ void moe_rank_proj_kernel(MoEWin w, MoERoute rt, int max_ent, int max
   const int row0 = rt.ent_row0[ent], ncol = rt.ent_ncol[ent];
   const int cs = ex.rs[mb] / 16;
   const uint4* vn = ex.Vn[mb];
-  float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+  // 8 k-blocks in flight per iteration (independent loads, 4 accumulator chains), then a fixed-order sum
+  constexpr int U = 8;
+  float acc[4][2][4] = {};
   const int KB = w.K / 16;
-  for (int kb = 0; kb < KB; ++kb) {
-    const uint4 a4 = __ldg(vn + ((size_t)kb * cs + c) * 32 + lane);
-    const uint32_t af[4] = {a4.x, a4.y, a4.z, a4.w};
+  const uint16_t* xr0[2];
+  bool cv[2];
 #pragma unroll
-    for (int nb = 0; nb < 2; ++nb) {
-      const int col = gid + 8 * nb;
-      const uint16_t* xr = xg + (size_t)(row0 + (col < ncol ? col : 0)) * w.K + 16 * kb + 2 * tig;
-      const uint32_t b0 = col < ncol ? __ldg(reinterpret_cast<const uint32_t*>(xr)) : 0u;
-      const uint32_t b1 = col < ncol ? __ldg(reinterpret_cast<const uint32_t*>(xr + 8)) : 0u;
-      mma16816(acc[nb], af, b0, b1);
+  for (int nb = 0; nb < 2; ++nb) {
+    const int col = gid + 8 * nb;
+    cv[nb] = col < ncol;
+    xr0[nb] = xg + (size_t)(row0 + (cv[nb] ? col : 0)) * w.K + 2 * tig;
+  }
+  for (int kb0 = 0; kb0 < KB; kb0 += U) {
+    uint4 a4[U];
+    uint32_t b[U][2][2];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int kb = min(kb0 + u, KB - 1);
+      a4[u] = __ldg(vn + ((size_t)kb * cs + c) * 32 + lane);
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) {
+        b[u][nb][0] = cv[nb] ? __ldg(reinterpret_cast<const uint32_t*>(xr0[nb] + 16 * kb)) : 0u;
+        b[u][nb][1] = cv[nb] ? __ldg(reinterpret_cast<const uint32_t*>(xr0[nb] + 16 * kb + 8)) : 0u;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (kb0 + u >= KB) break;
+      const uint32_t af[4] = {a4[u].x, a4[u].y, a4[u].z, a4[u].w};
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) mma16816(acc[u & 3][nb], af, b[u][nb][0], b[u][nb][1]);
     }
   }
+#pragma unroll
+  for (int ch = 1; ch < 4; ++ch)
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[0][nb][e] += acc[ch][nb][e];
 #pragma unroll
   for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int col = 2 * tig + (e & 1) + 8 * nb, rank = 16 * c + gid + 8 * (e >> 1);
-      if (col < ncol && rank < ex.r[mb]) t[(size_t)(row0 + col) * w.t_ld + mb * (w.t_ld / 2) + rank] = acc[nb][e];
+      if (col < ncol && rank < ex.r[mb]) t[(size_t)(row0 + col) * w.t_ld + mb * (w.t_ld / 2) + rank] = acc[0][nb][e];
     }
 }
 
