@@ -8,8 +8,8 @@
 //   route     group the T·k (token, expert) pairs by expert (ascending), tokens ascending inside an
 //             expert; entries = chunks of <= 16 rows of one expert (the mma N dimension)
 //   prep      gather x rows per (token, expert) row: bf16 copy (for V·x) and x' = x·2^-fp (fp16)
-//   rank_proj t[row] = V_e·x_row with the natural-k V fragments (one warp per entry, member, 16 ranks;
-//             fixed k order: deterministic)
+//   rank_proj t[row] = V_e·x_row with the natural-k V fragments (one block per entry, member, 16 ranks;
+//             8 warps split K, fixed-order reduction: deterministic)
 //   gemv      one warp per (entry, row block) over all K groups: records decoded exactly as the
 //             decode kernel does (w_tile_regs; the next record's words load while one is decoded),
 //             U·t (bf16 hi + lo) and the SiLU glue in the same warp — no reduction, no barrier
@@ -105,24 +105,21 @@ __global__ void moe_prep_kernel(const uint16_t* __restrict__ x, int ldx, int K, 
   d[0] = out[0]; d[1] = out[1];
 }
 
-// one warp per (entry, member, 16-rank chunk)
-__global__ void moe_rank_proj_kernel(MoEWin w, MoERoute rt, int max_ent, int max_chunks,
-                                     const uint16_t* __restrict__ xg, float* __restrict__ t) {
-  const int lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
-  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int per_ent = 2 * max_chunks;
-  if (gw >= (long long)max_ent * per_ent) return;
-  const int ent = (int)(gw / per_ent), rem = (int)(gw % per_ent), mb = rem / max_chunks, c = rem % max_chunks;
-  if (ent >= *rt.n_ent || (mb == 1 && !w.glue)) return;
+// one block of 8 warps per (entry, member, 16-rank chunk); warp w takes k-blocks [w·KB/8, (w+1)·KB/8)
+// (4 in flight, independent loads), partials summed in a fixed order through shared memory
+__global__ void __launch_bounds__(256) moe_rank_proj_kernel(MoEWin w, MoERoute rt, int max_ent, int max_chunks,
+                                                            const uint16_t* __restrict__ xg, float* __restrict__ t) {
+  __shared__ float part[8][32][8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
+  const int job = blockIdx.x, per_ent = 2 * max_chunks;
+  const int ent = job / per_ent, rem = job % per_ent, mb = rem / max_chunks, c = rem % max_chunks;
+  if (ent >= *rt.n_ent || (mb == 1 && !w.glue)) return;      // uniform per block
   const MoEExpert& ex = w.ex[rt.ent_e[ent]];
   if (16 * c >= ex.r[mb]) return;
   const int row0 = rt.ent_row0[ent], ncol = rt.ent_ncol[ent];
   const int cs = ex.rs[mb] / 16;
   const uint4* vn = ex.Vn[mb];
-  // 8 k-blocks in flight per iteration (independent loads, 4 accumulator chains), then a fixed-order sum
-  constexpr int U = 8;
-  float acc[4][2][4] = {};
-  const int KB = w.K / 16;
+  const int KB = w.K / 16, kb_lo = warp * KB / 8, kb_hi = (warp + 1) * KB / 8;
   const uint16_t* xr0[2];
   bool cv[2];
 #pragma unroll
@@ -131,12 +128,14 @@ __global__ void moe_rank_proj_kernel(MoEWin w, MoERoute rt, int max_ent, int max
     cv[nb] = col < ncol;
     xr0[nb] = xg + (size_t)(row0 + (cv[nb] ? col : 0)) * w.K + 2 * tig;
   }
-  for (int kb0 = 0; kb0 < KB; kb0 += U) {
+  constexpr int U = 4;
+  float acc[U][2][4] = {};
+  for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += U) {
     uint4 a4[U];
     uint32_t b[U][2][2];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int kb = min(kb0 + u, KB - 1);
+      const int kb = min(kb0 + u, kb_hi - 1);
       a4[u] = __ldg(vn + ((size_t)kb * cs + c) * 32 + lane);
 #pragma unroll
       for (int nb = 0; nb < 2; ++nb) {
@@ -146,25 +145,29 @@ __global__ void moe_rank_proj_kernel(MoEWin w, MoERoute rt, int max_ent, int max
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      if (kb0 + u >= KB) break;
+      if (kb0 + u >= kb_hi) break;
       const uint32_t af[4] = {a4[u].x, a4[u].y, a4[u].z, a4[u].w};
 #pragma unroll
-      for (int nb = 0; nb < 2; ++nb) mma16816(acc[u & 3][nb], af, b[u][nb][0], b[u][nb][1]);
+      for (int nb = 0; nb < 2; ++nb) mma16816(acc[u][nb], af, b[u][nb][0], b[u][nb][1]);
     }
   }
 #pragma unroll
-  for (int ch = 1; ch < 4; ++ch)
+  for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      part[warp][lane][4 * nb + e] = ((acc[0][nb][e] + acc[1][nb][e]) + acc[2][nb][e]) + acc[3][nb][e];
+  __syncthreads();
+  if (warp == 0) {
 #pragma unroll
     for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) acc[0][nb][e] += acc[ch][nb][e];
-#pragma unroll
-  for (int nb = 0; nb < 2; ++nb)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int col = 2 * tig + (e & 1) + 8 * nb, rank = 16 * c + gid + 8 * (e >> 1);
-      if (col < ncol && rank < ex.r[mb]) t[(size_t)(row0 + col) * w.t_ld + mb * (w.t_ld / 2) + rank] = acc[0][nb][e];
-    }
+      for (int e = 0; e < 4; ++e) {
+        float v = 0.f;
+        for (int ww = 0; ww < 8; ++ww) v += part[ww][lane][4 * nb + e];   // fixed order
+        const int col = 2 * tig + (e & 1) + 8 * nb, rank = 16 * c + gid + 8 * (e >> 1);
+        if (col < ncol && rank < ex.r[mb]) t[(size_t)(row0 + col) * w.t_ld + mb * (w.t_ld / 2) + rank] = v;
+      }
+  }
 }
 
 // One warp per (entry, row block) over all K: no cross-warp reduction, no CTA barrier; the next
@@ -317,9 +320,9 @@ cudaError_t moe_prep(const uint16_t* x, int ldx, int K, int bits, int gather, co
 cudaError_t moe_rank_proj(const MoEWin& w, const MoERoute& rt, int max_ent, const uint16_t* xg, float* t,
                           cudaStream_t st) {
   const int max_chunks = w.t_ld / 32;
-  const long long warps = (long long)max_ent * 2 * max_chunks;
-  if (warps == 0) return cudaSuccess;
-  moe_rank_proj_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(w, rt, max_ent, max_chunks, xg, t);
+  const long long jobs = (long long)max_ent * 2 * max_chunks;
+  if (jobs == 0) return cudaSuccess;
+  moe_rank_proj_kernel<<<(unsigned)jobs, 256, 0, st>>>(w, rt, max_ent, max_chunks, xg, t);
   return cudaGetLastError();
 }
 
