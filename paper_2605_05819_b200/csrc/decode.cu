@@ -196,31 +196,9 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
                       evict_first_policy());
         }
       }
-      if (f_on) {                                        // zero the x tile (cols >= B and the other 8 k stay 0)
-        reinterpret_cast<uint4*>(xt)[lane] = make_uint4(0u, 0u, 0u, 0u);
-        __syncwarp();
-      }
-      asm volatile("bar.sync %0, %1;" ::"r"(1 + par), "n"(kDecodeThreads) : "memory");   // FULL[par]
-      if (lane == 0) { if (k == 0) dtrace(a, 2); if (item + (int)gridDim.x >= n_items) dtrace(a, 3); }
-      float fin[NB8][4];
-#pragma unroll
-      for (int nb = 0; nb < NB8; ++nb)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) fin[nb][e] = 0.f;
-#pragma unroll
-      for (int w = 0; w < kDecodeWarps; ++w) {            // fixed order: deterministic
-        const float* src = red + ((size_t)(par * kDecodeWarps + w) * 32 + lane) * 4 * NB8;
-#pragma unroll
-        for (int nb = 0; nb < NB8; ++nb) {
-          const float4 v = *reinterpret_cast<const float4*>(src + 4 * nb);
-          fin[nb][0] += v.x; fin[nb][1] += v.y; fin[nb][2] += v.z; fin[nb][3] += v.w;
-        }
-      }
-      if (item + 2 * (int)gridDim.x < n_items)
-        asm volatile("bar.arrive %0, %1;" ::"r"(3 + par), "n"(kDecodeThreads) : "memory");   // EMPTY[par]
-      prefetch_u(item + gridDim.x, par ^ 1);
-
-      // ---- row-block epilogue: + U[:, :r]·t, residual, output
+      // ---- independent of the tile warps (so done before waiting for their partial sums): U[:, :r]·t
+      // (U prefetched one item ahead) and the residual (its producer window is >= 2 windows back,
+      // complete once this window's dependency was met)
       const int rbl = item - m.rb_begin;
       // U·t: plain windows use the member's own chunks for all 16 rows; a fused SiLU window runs
       // the up chunks (rows 0-7 = up rows) and the gate chunks (rows 8-15 = gate rows) separately
@@ -253,6 +231,40 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
           }
         }
       }
+      float res[NB8][4];
+#pragma unroll
+      for (int nb = 0; nb < NB8; ++nb)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          res[nb][e] = 0.f;
+          const int b = 2 * tig + (e & 1) + 8 * nb;
+          if (a.resid && !a.glue && b < a.B)
+            res[nb][e] = bf16_bits_to_f32(__ldcg(a.resid + (size_t)b * a.ld_resid + m.row_off + rbl * kRows + gid + 8 * (e >> 1)));
+        }
+      if (f_on) {                                        // zero the x tile (cols >= B and the other 8 k stay 0)
+        reinterpret_cast<uint4*>(xt)[lane] = make_uint4(0u, 0u, 0u, 0u);
+        __syncwarp();
+      }
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + par), "n"(kDecodeThreads) : "memory");   // FULL[par]
+      if (lane == 0) { if (k == 0) dtrace(a, 2); if (item + (int)gridDim.x >= n_items) dtrace(a, 3); }
+      float fin[NB8][4];
+#pragma unroll
+      for (int nb = 0; nb < NB8; ++nb)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) fin[nb][e] = 0.f;
+#pragma unroll
+      for (int w = 0; w < kDecodeWarps; ++w) {            // fixed order: deterministic
+        const float* src = red + ((size_t)(par * kDecodeWarps + w) * 32 + lane) * 4 * NB8;
+#pragma unroll
+        for (int nb = 0; nb < NB8; ++nb) {
+          const float4 v = *reinterpret_cast<const float4*>(src + 4 * nb);
+          fin[nb][0] += v.x; fin[nb][1] += v.y; fin[nb][2] += v.z; fin[nb][3] += v.w;
+        }
+      }
+      if (item + 2 * (int)gridDim.x < n_items)
+        asm volatile("bar.arrive %0, %1;" ::"r"(3 + par), "n"(kDecodeThreads) : "memory");   // EMPTY[par]
+      prefetch_u(item + gridDim.x, par ^ 1);
+
       if (a.glue) {
         // m[b][8·rbl + gid] = silu(gate) · up, gate = row gid+8 (c2, c3), up = row gid (c0, c1)
 #pragma unroll
@@ -281,8 +293,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
             const int b = 2 * tig + (e & 1) + 8 * nb;
             if (b >= a.B) continue;
             const int n = m.row_off + rbl * kRows + gid + 8 * (e >> 1);
-            float v = fin[nb][e] + comp[0][nb][e];
-            if (a.resid) v += bf16_bits_to_f32(__ldcg(a.resid + (size_t)b * a.ld_resid + n));
+            const float v = fin[nb][e] + comp[0][nb][e] + res[nb][e];
             if (a.y_bf16) {
               const uint16_t bits = (uint16_t)f32_to_bf16_rn(v);
               reinterpret_cast<uint16_t*>(a.y)[(size_t)b * a.ldy + n] = bits;
@@ -305,6 +316,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
         }
         while (!mbar_try_wait(fbar, f_phase)) {}
         f_phase ^= 1u;
+#pragma unroll 4
         for (int cc = 0; cc < a.fwd_chunks; ++cc) {
           const uint4 v4 = fbuf[cc * 32 + lane];
           const uint32_t af[4] = {v4.x, v4.y, v4.z, v4.w};
