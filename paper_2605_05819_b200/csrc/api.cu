@@ -103,6 +103,7 @@ struct hc_ctx {
   // decode stack (hc_stack_forward)
   DevBuf s_h, s_h1, s_qkv, s_m;
   int trace_slot = 0;                  // dev tracing: slot of the next decode launch (HC_DEC_TRACE builds)
+  DevBuf s_x16[4];                     // x' hand-off buffers of the stack: q, h1, m, h (16 rows each)
   std::map<std::tuple<int, const void*, void*>, std::unique_ptr<StackGraph>> graphs;
   cudaStream_t cap_stream = nullptr;
   // column sharding (hc_set_comm): NCCL communicator, send / gather staging
@@ -442,10 +443,25 @@ static bool can_forward(const Window& next) {
 }
 
 // Launch arguments of one window (also used by the stack driver).
+// x' hand-off between stack windows (DArgs::x16_given / y16)
+struct X16Spec {
+  const uint16_t* in = nullptr;   // x' of this window written by its producer (or NULL)
+  uint16_t* out = nullptr;        // where this window writes the next window's x' (or NULL)
+  int lo = 0, hi = 0;             // output columns that are the next window's x
+};
+
 static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int B, void* y, int y_bf16,
                              const void* resid, int ld_resid, DArgs& a, int& grid, bool t_in = false,
-                             const FwdSpec* fw = nullptr, Window* dep = nullptr, bool keep_done = false) {
+                             const FwdSpec* fw = nullptr, Window* dep = nullptr, bool keep_done = false,
+                             const X16Spec* xs16 = nullptr) {
   std::memset(&a, 0, sizeof(a));
+  if (xs16) {
+    a.x16_given = xs16->in ? 1 : 0;
+    a.x16 = xs16->in;
+    a.y16 = xs16->out;
+    a.y16_lo = xs16->lo;
+    a.y16_hi = xs16->hi;
+  }
   a.t_in = t_in ? 1 : 0;
   a.keep_done = keep_done ? 1 : 0;
   if (dep) {
@@ -512,7 +528,7 @@ static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int
   }
   a.tacc = (long long*)w.tacc.p;
   a.cnt = (unsigned*)w.cnt.p;
-  if (!decode_stages_x(B, a.K)) {
+  if (!a.x16_given && !decode_stages_x(B, a.K)) {
     const size_t need = (size_t)16 * a.K * 2;
     if (w.xprep.bytes < need) CUDA_TRY(w.xprep.alloc(need));
     a.x16 = (const uint16_t*)w.xprep.p;
@@ -537,10 +553,11 @@ static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int
     a.fwd_cb[a.fwd_nm] = cb;
     a.fwd_tacc = (long long*)nx.tacc.p;
   }
-  const auto key = std::make_tuple(m0.bits, B, a.K, a.n_chunks, a.fwd ? a.fwd_chunks : 0);
+  const auto key = std::make_tuple(m0.bits, B, a.K, a.n_chunks, (a.fwd ? a.fwd_chunks : 0) + 1000 * a.x16_given);
   auto it = ctx->max_ctas.find(key);
   if (it == ctx->max_ctas.end())
-    it = ctx->max_ctas.emplace(key, decode_max_ctas(m0.bits, B, a.K, a.n_chunks, a.fwd ? a.fwd_chunks : 0)).first;
+    it = ctx->max_ctas.emplace(key, decode_max_ctas(m0.bits, B, a.K, a.n_chunks, a.fwd ? a.fwd_chunks : 0,
+                                                    a.x16_given != 0)).first;
   if (it->second <= 0) return fail(HC_ERR_RUNTIME, "decode kernel cannot be resident on this device");
   const int n_items = a.n_rb;
   static const int per_sm = [] { const char* e = getenv("HC_DECODE_CTAS_PER_SM"); return e ? atoi(e) : 0; }();
@@ -551,13 +568,14 @@ static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int
 
 static hc_status launch_window(hc_ctx* ctx, Window& w, const void* x, int ldx, int B, void* y, int y_bf16,
                                const void* resid, int ld_resid, cudaStream_t st, bool t_in = false,
-                               const FwdSpec* fw = nullptr, Window* dep = nullptr, bool keep_done = false) {
+                               const FwdSpec* fw = nullptr, Window* dep = nullptr, bool keep_done = false,
+                               const X16Spec* xs16 = nullptr) {
   DArgs a;
   int grid = 0;
-  hc_status s = window_args(ctx, w, x, ldx, B, y, y_bf16, resid, ld_resid, a, grid, t_in, fw, dep, keep_done);
+  hc_status s = window_args(ctx, w, x, ldx, B, y, y_bf16, resid, ld_resid, a, grid, t_in, fw, dep, keep_done, xs16);
   if (s != HC_OK) return s;
   a.trace_slot = ctx->trace_slot++;
-  if (a.x16)
+  if (a.x16 && !a.x16_given)
     CUDA_TRY(launch_xprep(a.x, a.ldx, B, a.K, w.members.front().bits, (uint16_t*)a.x16, st));
   CUDA_TRY(launch_decode(a, w.members.front().bits, grid, st));
   return HC_OK;
@@ -944,6 +962,11 @@ extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, voi
   }
   if (ctx->s_qkv.bytes < (size_t)16 * nqkv * 2) { ctx->invalidate_graphs(); CUDA_TRY(ctx->s_qkv.alloc((size_t)16 * nqkv * 2)); }
   if (ctx->s_m.bytes < (size_t)16 * f * 2) { ctx->invalidate_graphs(); CUDA_TRY(ctx->s_m.alloc((size_t)16 * f * 2)); }
+  {
+    const size_t xb[4] = {(size_t)16 * d * 2, (size_t)16 * d * 2, (size_t)16 * f * 2, (size_t)16 * d * 2};
+    for (int i = 0; i < 4; ++i)
+      if (ctx->s_x16[i].bytes < xb[i]) { ctx->invalidate_graphs(); CUDA_TRY(ctx->s_x16[i].alloc(xb[i])); }
+  }
   const bool tp = ctx->comm != nullptr;
   if (tp) {
     const size_t widest = (size_t)std::max(std::max(nqkv, f), d);   // full width of any window output
@@ -1066,18 +1089,31 @@ extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, voi
         // its producer's row-block counter instead of the kernel boundary (an unstaged window keeps the
         // grid dependency: its x-prep kernel sits in between)
         const bool dx_ok = getenv("HC_DEPWAIT") == nullptr || getenv("HC_DEPWAIT")[0] != '0';
+        const bool hx_ok = dx_ok && (getenv("HC_XHANDOFF") == nullptr || getenv("HC_XHANDOFF")[0] != '0');
         const bool sx_q = dx_ok && hc::decode_stages_x(B, d), sx_f = dx_ok && hc::decode_stages_x(B, f);
         Window* prev_dn = l > 0 ? plan[l - 1].down : nullptr;
         const bool next_q = l + 1 < plan.size() && sx_q;
         ctx->trace_slot = (int)(4 * l);
+        // x' hand-off: every window but layer 0's QKV reads the fp16 x' its producer's
+        // epilogue wrote (no staging, no x-prep kernel); it then waits for the producer's counter itself
+        const bool hx = hx_ok;
+        uint16_t* xq16 = (uint16_t*)ctx->s_x16[0].p, *xh1 = (uint16_t*)ctx->s_x16[1].p;
+        uint16_t* xm16 = (uint16_t*)ctx->s_x16[2].p, *xh16 = (uint16_t*)ctx->s_x16[3].p;
+        const hc::X16Spec x_q{hx && l > 0 ? xh16 : nullptr, hx ? xq16 : nullptr, 0, d};
+        const hc::X16Spec x_o{hx ? xq16 : nullptr, hx ? xh1 : nullptr, 0, d};
+        const hc::X16Spec x_ug{hx ? xh1 : nullptr, hx ? xm16 : nullptr, 0, f};
+        const hc::X16Spec x_dn{hx ? xm16 : nullptr, (hx && l + 1 < plan.size()) ? xh16 : nullptr, 0, d};
+        const bool dq = sx_q || (hx && l > 0), do_ = sx_q || hx, dug = sx_q || hx, ddn = sx_f || hx;
+        const bool kq = sx_q || hx, ko = sx_q || hx, kug = sx_f || hx;     // keep(producer) = dep(consumer)
+        const bool kdn = l + 1 < plan.size() && (sx_q || hx);
         cap = hc::launch_window(ctx, *p.qkv, hin, d, B, qkv, 1, nullptr, 0, cs, t_q, &s_o,
-                                (prev_dn && sx_q) ? prev_dn : nullptr, sx_q);                                 // q | k | v
+                                (prev_dn && dq) ? prev_dn : nullptr, kq, &x_q);                              // q | k | v
         if (cap == HC_OK) cap = hc::launch_window(ctx, *p.o, qkv, nqkv, B, h1, 1, hin, d, cs, f_o, &s_ug,
-                                                  sx_q ? p.qkv : nullptr, sx_q);                              // h1 = h + O(q)
+                                                  do_ ? p.qkv : nullptr, ko, &x_o);                           // h1 = h + O(q)
         if (cap == HC_OK) cap = hc::launch_window(ctx, *p.ug, h1, d, B, mm, 1, nullptr, 0, cs, f_ug, &s_dn,
-                                                  sx_q ? p.o : nullptr, sx_f);                                // m = silu(g)·u
+                                                  dug ? p.o : nullptr, kug, &x_ug);                           // m = silu(g)·u
         if (cap == HC_OK) cap = hc::launch_window(ctx, *p.down, mm, f, B, hout, 1, h1, d, cs, f_dn, &s_q,
-                                                  sx_f ? p.ug : nullptr, next_q);                             // h' = h1 + DOWN(m)
+                                                  ddn ? p.ug : nullptr, kdn, &x_dn);                          // h' = h1 + DOWN(m)
       } else {                                                   // column-sharded: gather every window
         cap = tp_window(ctx, *p.qkv, hin, d, B, qkv, nullptr, 0, cs);
         if (cap == HC_OK) cap = tp_window(ctx, *p.o, qkv, nqkv, B, h1, hin, d, cs);

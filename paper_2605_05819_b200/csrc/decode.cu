@@ -62,6 +62,16 @@ cudaError_t decode_set_trace(void* buf) { return cudaMemcpyToSymbol(g_dtrace, &b
 // window's t accumulators with 64-bit fixed-point atomics (exact integer adds: t is bit-identical
 // for any arrival order), then bumps v_done; each CTA's epilogue warp acquires v_done once and reads
 // t while its tile warps are still streaming.
+// The next window's x' (fp16, pre-scaled by the code-field exponent of its column pair, layout.h) of
+// one output element (bf16 bits) at output column n, batch row b.
+template <int BITS>
+__device__ __forceinline__ void write_xprime(const DArgs& a, int b, int n, uint16_t bits) {
+  const int k = n - a.y16_lo, kk = k & (kGroup - 1);
+  const int j = 2 * (kk >> 5) + ((kk >> 2) & 1), pr = (kk >> 1) & 1;
+  const float xv = bf16_bits_to_f32(bits) * __uint_as_float((uint32_t)(127 - step_fp(BITS, j, pr)) << 23);
+  a.y16[(size_t)b * (a.y16_hi - a.y16_lo) + k] = __half_as_ushort(__float2half_rn(xv));
+}
+
 // Wait for this window's inputs: the producer window's completion counter (acquire; every warp that
 // reads activations calls this), else the programmatic-dependent-launch grid dependency.
 __device__ __forceinline__ void dep_wait(const DArgs& a, int lane) {
@@ -133,6 +143,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
     };
     prefetch_u(blockIdx.x, 0);                           // weights: before the PDL wait
     dep_wait(a, lane);
+    if (!XS && a.dep_cnt) asm volatile("bar.sync 6, %0;" ::"n"(kDecodeThreads) : "memory");   // release the tile warps
     if (lane == 0) dtrace(a, 1);
     if constexpr (XS) {
       if (lane == 0) {
@@ -281,6 +292,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
               const uint16_t bits = (uint16_t)f32_to_bf16_rn(v);
               reinterpret_cast<uint16_t*>(a.y)[(size_t)b * a.ldy + n] = bits;
               if (f_on) xt[(((f_n0 - a.fwd_lo) & 15) + gid) * 16 + b] = bits;
+              if (a.y16 && n >= a.y16_lo && n < a.y16_hi) write_xprime<BITS>(a, b, n, bits);
             } else {
               reinterpret_cast<float*>(a.y)[(size_t)b * a.ldy + n] = v;
             }
@@ -298,6 +310,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
               const uint16_t bits = (uint16_t)f32_to_bf16_rn(v);
               reinterpret_cast<uint16_t*>(a.y)[(size_t)b * a.ldy + n] = bits;
               if (f_on) xt[(gid + 8 * (e >> 1)) * 16 + b] = bits;
+              if (a.y16 && n >= a.y16_lo && n < a.y16_hi) write_xprime<BITS>(a, b, n, bits);
             } else {
               reinterpret_cast<float*>(a.y)[(size_t)b * a.ldy + n] = v;
             }
@@ -405,7 +418,9 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
   for (int s = 0; s < kNBuf; ++s) issue_block();   // weights / V: before the PDL wait
   // tile warps read activations only through the x staged by the epilogue warp (XS, ordered by its
   // acquire and the x mbarrier), except for V pieces and unstaged x: only then do they wait themselves
-  if (!a.dep_cnt || !XS || n_vp > 0) dep_wait(a, lane);
+  if (!a.dep_cnt) dep_wait(a, lane);
+  else if (!XS) asm volatile("bar.sync 6, %0;" ::"n"(kDecodeThreads) : "memory");   // the epilogue warp waited
+  else if (n_vp > 0) dep_wait(a, lane);
   if constexpr (XS) {
     while (!mbar_try_wait(xbar, 0)) {}
     // in place: x (bf16) -> x' = x·2^-fp (fp16, the B operand of the W mma); 16 elements per thread
@@ -606,7 +621,7 @@ static int max_ctas_t(int B, int K, int n_chunks, int fwd_chunks) {
 
 #define HC_DISPATCH(FN, ...)                                                       \
   do {                                                                             \
-    const bool two = a_B > 8, xs = use_xs(a_B, a_K);                               \
+    const bool two = a_B > 8, xs = use_xs(a_B, a_K) && !a_noxs;                   \
     switch (bits) {                                                                \
       case 2: return two ? FN<2, 2, false>(__VA_ARGS__)                            \
                          : (xs ? FN<2, 1, true>(__VA_ARGS__) : FN<2, 1, false>(__VA_ARGS__)); \
@@ -620,12 +635,14 @@ static int max_ctas_t(int B, int K, int n_chunks, int fwd_chunks) {
 
 cudaError_t launch_decode(const DArgs& a, int bits, int grid, cudaStream_t st) {
   const int a_B = a.B, a_K = a.K;
+  const bool a_noxs = a.x16_given != 0;
   HC_DISPATCH(launch_t, a, grid, st);
   return cudaErrorInvalidValue;
 }
 
-int decode_max_ctas(int bits, int B, int K, int n_chunks, int fwd_chunks) {
+int decode_max_ctas(int bits, int B, int K, int n_chunks, int fwd_chunks, bool no_xs) {
   const int a_B = B, a_K = K;
+  const bool a_noxs = no_xs;
   HC_DISPATCH(max_ctas_t, B, K, n_chunks, fwd_chunks);
   return 0;
 }

@@ -73,6 +73,13 @@ struct DArgs {
   unsigned* dep_cnt;    // producer's cnt[1], or NULL (griddepcontrol.wait)
   unsigned dep_target;  // producer's n_rb
   int keep_done;        // 1: a consumer window resets this window's cnt[1] (do not self-reset it)
+  // x' hand-off (stack graphs): x16_given = 1 means x16 was written by the producer window's epilogue
+  // (no x-prep kernel, no shared-memory staging: the tile warps read x' fragments from L2 / L1);
+  // y16 (if set) receives this window's output columns [y16_lo, y16_hi) as the next window's x' =
+  // fp16(y·2^-fp), row stride y16_hi - y16_lo
+  int x16_given;
+  uint16_t* y16;
+  int y16_lo, y16_hi;
   long long* tacc;      // [n_chunks][16 batch][16 ranks] t = V·x in 2^-28 fixed point (self-resetting)
   unsigned* cnt;        // [0] v_done (tile warps done with their V share), [1] w_done (row blocks)
 };
@@ -85,6 +92,6 @@ bool decode_stages_x(int B, int K);
 cudaError_t launch_xprep(const uint16_t* x, int ldx, int B, int K, int bits, uint16_t* x16, cudaStream_t st);
 cudaError_t decode_set_trace(void* buf);   // dev: [slots][grid][8] globaltimer stamps (HC_DEC_TRACE builds)
 // Max co-resident CTAs of the decode kernel on this device (persistent grid size).
-int decode_max_ctas(int bits, int B, int K, int n_chunks, int fwd_chunks);
+int decode_max_ctas(int bits, int B, int K, int n_chunks, int fwd_chunks, bool no_xs = false);
 
 }  // namespace hc
