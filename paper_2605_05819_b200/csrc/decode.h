@@ -10,10 +10,10 @@ constexpr int kDecodeWarps = 8;          // tile (streaming + contraction) warps
 constexpr int kDecodeThreads = (kDecodeWarps + 1) * 32;   // + one epilogue warp
 constexpr int kMaxChunks = 32;           // Σ ceil(r_m/16) over a window's members
 #ifndef HC_DEC_TPB
-#define HC_DEC_TPB 4
+#define HC_DEC_TPB 2
 #endif
 #ifndef HC_DEC_NBUF
-#define HC_DEC_NBUF 2
+#define HC_DEC_NBUF 3
 #endif
 #ifndef HC_DEC_MINB
 #define HC_DEC_MINB 2
