@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import numpy as np
 
+from .allocate import align, cap_level
 from .packing import unpack_codes, bf16_to_f64
 from .quant import dequant_abi
 
@@ -135,4 +136,36 @@ def moe_forward(experts: list, ranks: list, x_bits, topk_idx, topk_gate) -> np.n
         de = _lin(experts[e]["down"], ranks[e]["down"], m)
         g = np.asarray(topk_gate, dtype=np.float32)[toks, slots].astype(np.float64)
         y[toks] += g[:, None] * de
+    return y
+
+
+def dynamic_rank(k: int, g, rtilde, cap: int, k0: int = 3) -> int:
+    """Per-(token, expert) rank of one matrix ("G_{i,e} = k·g_e"):
+    r̃_{i,e} = G_{i,e}·r̃_i with G = k·g_e, then Align (ties up R14) and the cap rule (R15).
+    The product that decides the integer is taken in fp32 — (k·g)·r̃ — the precision of the kernel
+    (task rule: both sides decide in the same precision); the Align comparisons are exact for it."""
+    rt = np.float32(np.float32(k) * np.float32(g)) * np.float32(rtilde)
+    return cap_level(align(float(rt), k0), int(cap), k0)
+
+
+def moe_forward_dynamic(experts: list, caps: list, x_bits, topk_idx, topk_gate, rtilde: list, k0: int = 3):
+    """Grouped MoE with per-(token, expert) dynamic ranks: for token t and slot j (expert e, gate g),
+    the up / gate / down products use r = dynamic_rank(k, g, rtilde[e][s], caps[e][s]), s = up, gate,
+    down; y[t] = Σ_j g · DOWN_e(bf16(silu(GATE_e(x_t)) ⊙ UP_e(x_t))).  caps[e] / rtilde[e] are dicts
+    with keys up, gate, down.  One token row at a time (plain, slow, test-sized)."""
+    x = bf16_to_f64(x_bits)
+    idx = np.asarray(topk_idx)
+    gates = np.asarray(topk_gate, dtype=np.float32)
+    T, k = idx.shape
+    d = experts[int(idx[0, 0])]["down"]["N"]
+    y = np.zeros((T, d), dtype=np.float64)
+    for t in range(T):
+        for j in range(k):
+            e, g = int(idx[t, j]), gates[t, j]
+            r = {s: dynamic_rank(k, g, rtilde[e][s], caps[e][s], k0) for s in ("up", "gate", "down")}
+            xt = x[t:t + 1]
+            up = _lin(experts[e]["up"], r["up"], xt)
+            gt = _lin(experts[e]["gate"], r["gate"], xt)
+            m = round_bf16(silu(gt) * up)
+            y[t] += float(g) * _lin(experts[e]["down"], r["down"], m)[0]
     return y

@@ -237,3 +237,30 @@ def test_moe_gate_linearity_two_identical_experts():
     assert np.allclose(two, one, rtol=1e-14, atol=0)
     half = linear.moe_forward([ex], [r], x, np.zeros((4, 1), np.int32), np.full((4, 1), g, np.float32))
     assert np.array_equal(half, one * float(g))
+
+
+def test_dynamic_rank_rule_worked_examples():
+    # G = k·g, r̃ = G·r̃_i, Align ties up (R14), cap to the largest level <= cap (R15)
+    assert linear.dynamic_rank(2, 0.75, 16.0, 64) == 32          # 24 is the 16/32 midpoint: ties up
+    assert linear.dynamic_rank(2, 0.75, 16.0, 16) == 16          # capped
+    assert linear.dynamic_rank(8, 0.125, 40.0, 64) == 32         # k·g = 1 leaves r̃ = 40 -> 32
+    assert linear.dynamic_rank(8, 0.01, 40.0, 64) == 0           # 3.2 < 4 -> 0
+    assert linear.dynamic_rank(4, 0.5, 3.0, 64) == 8             # 6 -> nearest of {0, 8}: 8
+    assert linear.dynamic_rank(1, 1.0, 300.0, 48) == 32          # 256 aligned, cap 48 -> 32
+
+
+def test_moe_dynamic_reduces_to_static_and_zero():
+    d, f = 128, 128
+    mk = lambda s: synth.linear_case(40 + s, 128, 128, 3, 128, 16, 1, "asym")
+    ex = [dict(up=mk(0), gate=mk(1), down=mk(2)), dict(up=mk(3), gate=mk(4), down=mk(5))]
+    caps = [dict(up=16, gate=8, down=16), dict(up=8, gate=16, down=0)]
+    x = synth.activations(46, 3, d)
+    idx = np.array([[0, 1], [1, 0], [0, 1]], np.int32)
+    gate = np.array([[0.5, 0.5], [0.75, 0.25], [0.625, 0.375]], np.float32)
+    big = [dict(up=1e6, gate=1e6, down=1e6)] * 2                 # every rank saturates at its cap
+    dyn = linear.moe_forward_dynamic(ex, caps, x, idx, gate, big)
+    stat = linear.moe_forward(ex, caps, x, idx, gate)
+    assert np.allclose(dyn, stat, rtol=1e-13, atol=1e-13)
+    zero = linear.moe_forward_dynamic(ex, caps, x, idx, gate, [dict(up=0.0, gate=0.0, down=0.0)] * 2)
+    z_stat = linear.moe_forward(ex, [dict(up=0, gate=0, down=0)] * 2, x, idx, gate)
+    assert np.allclose(zero, z_stat, rtol=1e-13, atol=1e-13)
