@@ -395,6 +395,10 @@ def run_c3_ours(args, rank, world, device, T, c=C3):
     idx = [torch.from_numpy(r[0]).cuda() for r in routes]
     gate = [torch.from_numpy(r[1]).cuda() for r in routes]
     ys = [torch.empty((T, d), dtype=torch.float32, device="cuda") for _ in range(c["layers"])]
+    if getattr(args, "moe_dynamic", False):
+        # per-(token, expert) ranks r = Cap(Align((k·g)·r̃)) (hc_moe_set_dynamic_ranks), r̃ ~ U[0, 24)
+        for l in range(c["layers"]):
+            ctx.moe_set_dynamic_ranks(l, (rng.random((E, 3)) * 24.0).astype(np.float32))
     nbytes = 0
     for l, (ri, _) in enumerate(routes):
         for e in sorted(set(int(v) for v in ri.reshape(-1))):
@@ -598,6 +602,7 @@ def main():
     ap.add_argument("--sweep", action="store_true", help="c2: also time B = 2, 4, 8, 16")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--rank-override", type=int, default=None, help="dev: use this rank for every matrix")
+    ap.add_argument("--moe-dynamic", action="store_true", help="c3: per-(token, expert) dynamic ranks (P:652-665)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -619,7 +624,8 @@ def main():
                   "hidden": 2048, "expert_ffn": 768, "experts": 128, "topk": 8, "layers": 48, "bits": 3, "group": 128,
                   "tokens": args.batch, "parallelism": f"dp{world}",
                   "l2": "inputs larger than L2 (11.4 GB of expert weights; each step touches every layer)",
-                  "routing": "softmax(N(0,1) logits) top-8, renormalised gates (synth.routing_case)"}
+                  "routing": "softmax(N(0,1) logits) top-8, renormalised gates (synth.routing_case)",
+                  "dynamic_ranks": bool(args.moe_dynamic)}
     elif args.workload == "c1":
         config = {"workload": "c1: single 4096x4096 linear, 4-bit g128, rank-64 compensation, batch-1 decode",
                   "N": 4096, "K": 4096, "bits": 4, "group": 128, "rank": 64, "batch": 1,

@@ -180,6 +180,17 @@ hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, void* y, void*
 hc_status hc_moe_forward(hc_ctx* ctx, int32_t layer, const void* x, int32_t T, const int32_t* topk_idx,
                          const float* topk_gate, int32_t topk, void* y, void* stream);
 
+/* Dynamic per-(token, expert) compensation ranks for the MoE layer `layer` (P:255-258, P:652-665:
+ * the expert activation score G = k·g_e scales the continuous rank): for a routed (token, slot) pair
+ * with expert e and gate g, matrix s in (up, gate, down) uses
+ *   r = Cap(Align((k·g)·rtilde[3e + s]))   (Align: nearest of {0} ∪ {2^j, j >= k0}, ties up; Cap: the
+ *                                            largest level <= the matrix's loaded r_alloc; fp32 product)
+ * instead of its static r_alloc (which stays the upper bound: U / V reads are sized by it).
+ * rtilde: host float [n_experts][3] (>= 0, finite), copied; NULL switches back to the static ranks.
+ * n_experts must match the layer's experts at the next hc_moe_forward (HC_ERR_CONFIG otherwise).
+ * HC_ERR_NUMERIC for a negative or non-finite r̃. */
+hc_status hc_moe_set_dynamic_ranks(hc_ctx* ctx, int32_t layer, const float* rtilde, int32_t n_experts, int32_t k0);
+
 /* Column sharding across GPUs.  Rank 0 calls hc_nccl_unique_id and shares the 128
  * bytes with every rank (e.g. through torch.distributed); each rank then calls hc_set_comm with its
  * rank and the world size (ncclCommInitRank on the context's device; NCCL is loaded at run time).

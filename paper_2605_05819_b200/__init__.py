@@ -188,6 +188,14 @@ class Context:
                                    _stream(stream)))
         return y
 
+    def moe_set_dynamic_ranks(self, layer, rtilde=None, k0=3):
+        """hc_moe_set_dynamic_ranks: rtilde float [E, 3] (up, gate, down) or None (static ranks)."""
+        if rtilde is None:
+            check(lib().hc_moe_set_dynamic_ranks(self._h, int(layer), None, 0, int(k0)))
+            return
+        r = np.ascontiguousarray(rtilde, dtype=np.float32)
+        check(lib().hc_moe_set_dynamic_ranks(self._h, int(layer), r.ctypes.data, int(r.shape[0]), int(k0)))
+
     def compensated_linear(self, layer, window, x, y, B=None, expert=-1, out_dtype=OUT_F32, stream=None):
         """y[b, :] = concat_m ( deq(W_m)·x_b + U_m[:, :r_m]·(V_m[:r_m, :]·x_b) ).
         x: bf16 [B, K] (torch bf16 / uint16 bits, device or host); y: [B, rows] fp32 or bf16."""

@@ -115,6 +115,10 @@ struct hc_ctx {
     DevBuf ex_ug, ex_dn;
     int E = 0, K = 0, F = 0, D = 0, bits = 0, t_ug = 32, t_dn = 32;
     bool valid = false;
+    // dynamic per-(token, expert) ranks (hc_moe_set_dynamic_ranks): host r̃ [E][3], device r̃ and caps
+    std::vector<float> rtilde;
+    int k0 = 3;
+    DevBuf d_rtilde, d_caps;
   };
   std::map<int, MoECache> moe;
   DevBuf moe_ws, moe_idx, moe_gate;
@@ -780,11 +784,42 @@ static hc_status moe_tables(hc_ctx* ctx, int layer, hc_ctx::MoECache*& out) {
   c.E = E;
   c.t_ug = 32 * cu;
   c.t_dn = 32 * cd;
+  if (!c.rtilde.empty()) {
+    if ((int)c.rtilde.size() != 3 * E)
+      return fail(HC_ERR_CONFIG, "hc_moe_forward: dynamic ranks were set for %d experts, layer %d has %d",
+                  (int)c.rtilde.size() / 3, layer, E);
+    std::vector<int> caps(3 * E);
+    for (int e = 0; e < E; ++e) { caps[3 * e] = ug[e].r[0]; caps[3 * e + 1] = ug[e].r[1]; caps[3 * e + 2] = dn[e].r[0]; }
+    CUDA_TRY(c.d_rtilde.alloc(c.rtilde.size() * sizeof(float)));
+    CUDA_TRY(c.d_caps.alloc(caps.size() * sizeof(int)));
+    CUDA_TRY(cudaMemcpy(c.d_rtilde.p, c.rtilde.data(), c.rtilde.size() * sizeof(float), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(c.d_caps.p, caps.data(), caps.size() * sizeof(int), cudaMemcpyHostToDevice));
+  }
   CUDA_TRY(c.ex_ug.alloc(ug.size() * sizeof(hc::MoEExpert)));
   CUDA_TRY(c.ex_dn.alloc(dn.size() * sizeof(hc::MoEExpert)));
   CUDA_TRY(cudaMemcpy(c.ex_ug.p, ug.data(), ug.size() * sizeof(hc::MoEExpert), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(c.ex_dn.p, dn.data(), dn.size() * sizeof(hc::MoEExpert), cudaMemcpyHostToDevice));
   c.valid = true;
+  return HC_OK;
+}
+
+extern "C" hc_status hc_moe_set_dynamic_ranks(hc_ctx* ctx, int32_t layer, const float* rtilde, int32_t n_experts,
+                                              int32_t k0) {
+  if (!ctx) return fail(HC_ERR_STATE, "hc_moe_set_dynamic_ranks: null context");
+  hc_ctx::MoECache& c = ctx->moe[layer];
+  if (!rtilde) {
+    c.rtilde.clear();
+    c.valid = false;
+    return HC_OK;
+  }
+  if (n_experts < 1 || n_experts > 256 || k0 < 0 || k0 > 7)
+    return fail(HC_ERR_CONFIG, "hc_moe_set_dynamic_ranks: n_experts %d / k0 %d", n_experts, k0);
+  for (int i = 0; i < 3 * n_experts; ++i)
+    if (!(rtilde[i] >= 0.f) || !(rtilde[i] < 1e30f))
+      return fail(HC_ERR_NUMERIC, "hc_moe_set_dynamic_ranks: r̃[%d] = %g is negative or not finite", i, (double)rtilde[i]);
+  c.rtilde.assign(rtilde, rtilde + 3 * n_experts);
+  c.k0 = k0;
+  c.valid = false;                                     // tables (and the device r̃ / caps) rebuilt on next use
   return HC_OK;
 }
 
@@ -807,7 +842,7 @@ extern "C" hc_status hc_moe_forward(hc_ctx* ctx, int32_t layer, const void* x, i
                o_er = take((size_t)maxe * 4), o_ec = take((size_t)maxe * 4), o_xg = take((size_t)R * c->K * 2),
                o_x16 = take((size_t)R * c->K * 2), o_tug = take((size_t)R * c->t_ug * 4), o_m = take((size_t)R * c->F * 2),
                o_md = take((size_t)R * c->F * 2), o_tdn = take((size_t)R * c->t_dn * 4), o_do = take((size_t)R * c->D * 4),
-               o_x = take((size_t)T * c->K * 2), o_y = take((size_t)T * c->D * 4);
+               o_x = take((size_t)T * c->K * 2), o_y = take((size_t)T * c->D * 4), o_rr = take((size_t)R * 3);
   if (ctx->moe_ws.bytes < off) CUDA_TRY(ctx->moe_ws.alloc(off));
   uint8_t* ws = (uint8_t*)ctx->moe_ws.p;
   hc::MoERoute rt;
@@ -834,8 +869,11 @@ extern "C" hc_status hc_moe_forward(hc_ctx* ctx, int32_t layer, const void* x, i
     dx = ws + o_x;
   }
   if (hy) dy = ws + o_y;
-  hc::MoEWin wu{(const hc::MoEExpert*)c->ex_ug.p, c->F / 8, c->K, c->K / hc::kGroup, 1, c->t_ug};
-  hc::MoEWin wd{(const hc::MoEExpert*)c->ex_dn.p, c->D / hc::kRows, c->F, c->F / hc::kGroup, 0, c->t_dn};
+  const bool dyn = !c->rtilde.empty();
+  uint8_t* row_rank = dyn ? ws + o_rr : nullptr;
+  hc::MoEWin wu{(const hc::MoEExpert*)c->ex_ug.p, c->F / 8, c->K, c->K / hc::kGroup, 1, c->t_ug, row_rank, 0};
+  hc::MoEWin wd{(const hc::MoEExpert*)c->ex_dn.p, c->D / hc::kRows, c->F, c->F / hc::kGroup, 0, c->t_dn, row_rank, 2};
+  hc::MoEDyn mdyn{(const float*)c->d_rtilde.p, (const int*)c->d_caps.p, c->k0, row_rank};
   uint16_t* xg = (uint16_t*)(ws + o_xg);
   uint16_t* x16 = (uint16_t*)(ws + o_x16);
   uint16_t* m = (uint16_t*)(ws + o_m);
@@ -843,7 +881,7 @@ extern "C" hc_status hc_moe_forward(hc_ctx* ctx, int32_t layer, const void* x, i
   float* tug = (float*)(ws + o_tug);
   float* tdn = (float*)(ws + o_tdn);
   float* dout = (float*)(ws + o_do);
-  CUDA_TRY(hc::moe_route(didx, T, topk, c->E, rt, st));
+  CUDA_TRY(hc::moe_route(didx, dgate, T, topk, c->E, rt, dyn ? &mdyn : nullptr, st));
   CUDA_TRY(hc::moe_prep((const uint16_t*)dx, c->K, c->K, c->bits, 1, rt, R, xg, x16, st));
   CUDA_TRY(hc::moe_rank_proj(wu, rt, maxe, xg, tug, st));
   const int max_cols = std::min(T, 16);                                             // rows of one expert <= T

@@ -28,7 +28,21 @@ constexpr int kRouteThreads = 1024;
 // Single CTA: T <= 1024 tokens, E <= 256 experts, k <= 16.  Per-expert token bitmaps (order-free
 // atomicOr), per-expert counts and entry counts by one thread per expert, exclusive scans over the
 // experts (one warp, fixed order), then every (token, slot) finds its row by popcount.
-__global__ void moe_route_kernel(const int32_t* __restrict__ idx, int T, int k, int E, MoERoute rt) {
+// Align (ties up) and the cap rule (R15) of the oracle, on an fp32 continuous rank
+__device__ __forceinline__ int dyn_rank(float rt, int cap, int k0) {
+  int lo = 0, hi = 1 << k0;
+  while (rt >= (float)hi) { lo = hi; hi *= 2; }
+  int r = (rt - (float)lo) < ((float)hi - rt) ? lo : hi;
+  if (r > cap) {
+    int lvl = 0;
+    for (int v = 1 << k0; v <= cap; v *= 2) lvl = v;
+    r = lvl;
+  }
+  return r;
+}
+
+__global__ void moe_route_kernel(const int32_t* __restrict__ idx, const float* __restrict__ gate, int T, int k, int E,
+                                 MoERoute rt, MoEDyn dyn) {
   extern __shared__ unsigned bm[];                 // [E][W] token bitmaps, W = ceil(T/32)
   __shared__ int cnt[256], ecnt[256], off[257], eoff[257];
   const int W = (T + 31) / 32;
@@ -81,6 +95,12 @@ __global__ void moe_route_kernel(const int32_t* __restrict__ idx, int T, int k, 
     const int row = off[e] + before;
     rt.row_tok[row] = t;
     rt.tok_row[i] = row;
+    if (dyn.row_rank) {
+      const float kg = (float)k * gate[i];                       // G = k·g (fp32, as the oracle)
+#pragma unroll
+      for (int sl = 0; sl < 3; ++sl)
+        dyn.row_rank[row * 3 + sl] = (uint8_t)min(255, dyn_rank(kg * dyn.rtilde[e * 3 + sl], dyn.caps[e * 3 + sl], dyn.k0));
+    }
   }
 }
 
@@ -238,13 +258,15 @@ __global__ void __launch_bounds__(128) moe_gemv_warp_kernel(MoEWin w, MoERoute r
 #pragma unroll
         for (int nb = 0; nb < NB8; ++nb) {
           const int col = gid + 8 * nb;
-          const float* tr = t + (size_t)(row0 + (col < ncol ? col : 0)) * w.t_ld + h * (w.t_ld / 2);
+          const int rowc = row0 + (col < ncol ? col : 0);
+          const float* tr = t + (size_t)rowc * w.t_ld + h * (w.t_ld / 2);
+          const int rlim = w.row_rank ? min(ex.r[h], (int)w.row_rank[rowc * 3 + w.rank_slot0 + h]) : ex.r[h];
           uint32_t hi[2], lo[2];
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             const int rk = 16 * c + 2 * tig + 8 * hh;
-            const float ta = (col < ncol && rk < ex.r[h]) ? tr[rk] : 0.f;
-            const float tb = (col < ncol && rk + 1 < ex.r[h]) ? tr[rk + 1] : 0.f;
+            const float ta = (col < ncol && rk < rlim) ? tr[rk] : 0.f;
+            const float tb = (col < ncol && rk + 1 < rlim) ? tr[rk + 1] : 0.f;
             const uint32_t ha = f32_to_bf16_rn(ta), hb = f32_to_bf16_rn(tb);
             hi[hh] = ha | (hb << 16);
             lo[hh] = f32_to_bf16_rn(ta - bf16_bits_to_f32(ha)) | (f32_to_bf16_rn(tb - bf16_bits_to_f32(hb)) << 16);
@@ -297,10 +319,13 @@ __global__ void moe_combine_kernel(const float* __restrict__ dout, int N, const 
 
 }  // namespace
 
-cudaError_t moe_route(const int32_t* topk_idx, int T, int k, int E, const MoERoute& rt, cudaStream_t st) {
+cudaError_t moe_route(const int32_t* topk_idx, const float* topk_gate, int T, int k, int E, const MoERoute& rt,
+                      const MoEDyn* dyn, cudaStream_t st) {
   if (T < 1 || T > 1024 || k < 1 || k > kMoEMaxK || E < 1 || E > 256) return cudaErrorInvalidValue;
   const size_t smem = (size_t)E * ((T + 31) / 32) * sizeof(unsigned);
-  moe_route_kernel<<<1, kRouteThreads, smem, st>>>(topk_idx, T, k, E, rt);
+  MoEDyn d{};
+  if (dyn) d = *dyn;
+  moe_route_kernel<<<1, kRouteThreads, smem, st>>>(topk_idx, topk_gate, T, k, E, rt, d);
   return cudaGetLastError();
 }
 

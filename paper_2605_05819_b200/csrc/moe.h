@@ -32,10 +32,22 @@ struct MoEWin {
   const MoEExpert* ex;      // [E] device
   int n_rb, K, G, glue;     // per expert: row blocks, input width; glue = fused SiLU(gate)·up (UPGATE)
   int t_ld;                 // floats per row of the t buffer (= 2 · max rank chunk · 16)
+  const uint8_t* row_rank;  // dynamic ranks [R][3] (up, gate, down) per routed row, or NULL (static ranks)
+  int rank_slot0;           // slot of member 0 in row_rank: 0 (UPGATE: up, gate), 2 (DOWN)
+};
+
+// Dynamic per-(token, expert) ranks: r = Cap(Align((k·g)·r̃[e][s])), decided in
+// fp32; rtilde / caps are [E][3] (up, gate, down), k0 the smallest nonzero level exponent.
+struct MoEDyn {
+  const float* rtilde;
+  const int* caps;
+  int k0;
+  uint8_t* row_rank;        // out: [R][3]
 };
 
 // Route: group (token, slot) pairs by expert (deterministic order), build entries of <= 16 rows.
-cudaError_t moe_route(const int32_t* topk_idx, int T, int k, int E, const MoERoute& rt, cudaStream_t st);
+cudaError_t moe_route(const int32_t* topk_idx, const float* topk_gate, int T, int k, int E, const MoERoute& rt,
+                      const MoEDyn* dyn, cudaStream_t st);
 // x rows of every routed (token, expert) row: xg = x[row_tok] (bf16) and x16 = x'(bits) (fp16).
 // gather == 0: the rows are x itself (row r = row r, used for the DOWN input m).
 cudaError_t moe_prep(const uint16_t* x, int ldx, int K, int bits, int gather, const MoERoute& rt, int R_max,

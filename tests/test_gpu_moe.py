@@ -99,3 +99,38 @@ def test_moe_rank_change_and_skipped_ids(hc):
     with pytest.raises(hc.HCError):
         ctx.moe_forward(7, dev(x), dev(idx), dev(gate), y)           # no experts on layer 7
     ctx.close()
+
+
+@pytest.mark.parametrize("T,topk", [(6, 2), (40, 4)])
+def test_moe_dynamic_ranks(hc, T, topk):
+    """Per-(token, expert) ranks r = Cap(Align((k·g)·r̃)) (hc_moe_set_dynamic_ranks) against the oracle
+    (oracle.linear.moe_forward_dynamic); huge r̃ reproduces the static path bit for bit; NULL restores it."""
+    E, d, f = 5, 256, 256
+    experts, _ = make_experts(E, d, f, 3, seed=123 + T)
+    caps = [dict(up=16, gate=16, down=16) for _ in range(E)]
+    ctx = hc.Context(0)
+    load(hc, ctx, 1, experts, caps)
+    x = synth.activations(T + 30, T, d)
+    idx, gate = synth.routing_case(T + 31, T, E, topk)
+    g = synth.rng(T)
+    rtilde = (g.random((E, 3)) * 24.0).astype(np.float32)          # mixes ranks 0 / 8 / 16 per token
+    ctx.moe_set_dynamic_ranks(1, rtilde)
+    y = torch.empty((T, d), dtype=torch.float32, device="cuda")
+    ctx.moe_forward(1, dev(x), dev(idx), dev(gate), y)
+    torch.cuda.synchronize()
+    rt = [dict(up=float(r[0]), gate=float(r[1]), down=float(r[2])) for r in rtilde]
+    ref = linear.moe_forward_dynamic(experts, caps, x, idx, gate, rt)
+    err = np.abs(y.cpu().numpy() - ref).max() / np.abs(ref).max()
+    assert err <= 2e-3, err
+    # the ranks really vary: the static-rank oracle differs from the dynamic one
+    assert np.abs(linear.moe_forward(experts, caps, x, idx, gate) - ref).max() > 1e-6
+    ctx.moe_set_dynamic_ranks(1, np.full((E, 3), 1e6, np.float32))  # saturate at the caps
+    ctx.moe_forward(1, dev(x), dev(idx), dev(gate), y)
+    ctx.moe_set_dynamic_ranks(1, None)
+    y_stat = torch.empty_like(y)
+    ctx.moe_forward(1, dev(x), dev(idx), dev(gate), y_stat)
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy(), y_stat.cpu().numpy())
+    with pytest.raises(hc.HCError):
+        ctx.moe_set_dynamic_ranks(1, np.full((E, 3), -1.0, np.float32))
+    ctx.close()
