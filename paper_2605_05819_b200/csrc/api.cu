@@ -966,8 +966,6 @@ static hc_status tp_window(hc_ctx* ctx, Window& w, const void* x, int ldx, int B
 }  // namespace
 
 // dev-only (not in hcinfer.h): point the stack kernel's trace stamps at a device buffer
-extern "C" int hc_dev_stack_trace(void* buf) { return (int)hc::stack_set_trace(buf); }
-extern "C" int hc_dev_stack_acct(void* buf) { return (int)hc::stack_set_acct(buf); }
 extern "C" int hc_dev_decode_trace(void* buf) { return (int)hc::decode_set_trace(buf); }
 
 extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, void* y, void* stream) {
@@ -1025,26 +1023,18 @@ extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, voi
         if (s != HC_OK) return s;
       }
     cudaStream_t cs = ctx->cap_stream;
-    // persistent stack kernel (one launch for all windows) when the plan qualifies
+    // persistent stack kernel (one launch for all windows) when the plan qualifies: one code width,
+    // B <= 8, every window after the first fed by t forwarding and the x' hand-off
     const char* stack_ev = getenv("HC_STACK_KERNEL");   // "1": persistent stack kernel (opt-in)
     const bool stack_env = stack_ev && stack_ev[0] == '1';
     const int bits0 = plan.front().qkv->members.front().bits;
     bool use_stack = stack_env && !tp && B <= 8;
-    int k_max = 0;
-    for (LayerPlan& p : plan)
-      for (Window* w : {p.qkv, p.o, p.ug, p.down}) {
-        k_max = std::max(k_max, w->members.front().K);
+    for (size_t l = 0; l < plan.size() && use_stack; ++l)
+      for (Window* w : {plan[l].qkv, plan[l].o, plan[l].ug, plan[l].down}) {
         if (w->members.front().bits != bits0) use_stack = false;
+        if ((l > 0 || w != plan[l].qkv) && !hc::can_forward(*w)) use_stack = false;
       }
-    int u_chunks = 1;                                    // largest U slice (16-rank chunks) of any row block
-    for (LayerPlan& p : plan)
-      for (Window* w : {p.qkv, p.o, p.ug, p.down}) {
-        if (w->glue == HC_GLUE_SILU_MUL) u_chunks = std::max(u_chunks, (std::max(w->members[0].r_alloc, w->members[1].r_alloc) + 15) / 16);
-        else for (const Member& m : w->members) u_chunks = std::max(u_chunks, (m.r_alloc + 15) / 16);
-      }
-    int n_us = hc::stack_uslots_max();
-    while (n_us > 2 && use_stack && hc::stack_smem_bytes(B, k_max, u_chunks, n_us) == 0) --n_us;
-    const size_t s_smem = use_stack ? hc::stack_smem_bytes(B, k_max, u_chunks, n_us) : 0;
+    const size_t s_smem = use_stack ? hc::stack_smem_bytes() : 0;
     const int s_grid = s_smem ? hc::stack_grid(bits0, s_smem) : 0;
     if (use_stack && s_grid > 0) {
       std::vector<hc::SWin> tab;
@@ -1053,30 +1043,38 @@ extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, voi
       uint16_t* h1 = (uint16_t*)ctx->s_h1.p;
       uint16_t* qkv = (uint16_t*)ctx->s_qkv.p;
       uint16_t* mm = (uint16_t*)ctx->s_m.p;
+      uint16_t* xq16 = (uint16_t*)ctx->s_x16[0].p, *xh1 = (uint16_t*)ctx->s_x16[1].p;
+      uint16_t* xm16 = (uint16_t*)ctx->s_x16[2].p, *xh16 = (uint16_t*)ctx->s_x16[3].p;
       int rot = 0;
-      auto add = [&](Window& w, const void* x, int ldx, void* y, const void* resid, int ld_resid) -> hc_status {
+      auto add = [&](Window& w, const void* x, int ldx, void* y, const void* resid, int ld_resid, bool t_in,
+                     const hc::FwdSpec& fw, const hc::X16Spec& xs) -> hc_status {
         hc::SWin sw;
         std::memset(&sw, 0, sizeof(sw));
         int grid_unused = 0;
-        hc_status st2 = hc::window_args(ctx, w, x, ldx, B, y, 1, resid, ld_resid, sw.a, grid_unused);
+        hc_status st2 = hc::window_args(ctx, w, x, ldx, B, y, 1, resid, ld_resid, sw.a, grid_unused, t_in,
+                                        fw.next ? &fw : nullptr, nullptr, false, &xs);
         if (st2 != HC_OK) return st2;
         sw.rot = rot;
-        sw.n_vwarps = hc::stack_vwarps(sw.a.n_chunks * 4 * sw.a.G, s_grid);
         rot = (rot + sw.a.n_rb) % s_grid;
         tab.push_back(sw);
         return HC_OK;
       };
       for (size_t l = 0; l < plan.size(); ++l) {
         LayerPlan& p = plan[l];
-        uint16_t* hout = (l + 1 == plan.size()) ? (uint16_t*)dy : h;
-        s = add(*p.qkv, hin, d, qkv, nullptr, 0);
-        if (s == HC_OK) s = add(*p.o, qkv, nqkv, h1, hin, d);
-        if (s == HC_OK) s = add(*p.ug, h1, d, mm, nullptr, 0);
-        if (s == HC_OK) s = add(*p.down, mm, f, hout, h1, d);
+        const bool last = l + 1 == plan.size();
+        uint16_t* hout = last ? (uint16_t*)dy : h;
+        const hc::FwdSpec s_o{p.o, 0, d}, s_ug{p.ug, 0, d}, s_dn{p.down, 0, f},
+            s_q{last ? nullptr : plan[l + 1].qkv, 0, d};
+        const hc::X16Spec x_q{xh16, xq16, 0, d}, x_o{xq16, xh1, 0, d}, x_ug{xh1, xm16, 0, f},
+            x_dn{xm16, last ? nullptr : xh16, 0, d};
+        s = add(*p.qkv, hin, d, qkv, nullptr, 0, l > 0, s_o, x_q);                 // q | k | v
+        if (s == HC_OK) s = add(*p.o, qkv, nqkv, h1, hin, d, true, s_ug, x_o);      // h1 = h + O(q)
+        if (s == HC_OK) s = add(*p.ug, h1, d, mm, nullptr, 0, true, s_dn, x_ug);    // m = silu(g)·u
+        if (s == HC_OK) s = add(*p.down, mm, f, hout, h1, d, true, s_q, x_dn);      // h' = h1 + DOWN(m)
         if (s != HC_OK) return s;
         hin = hout;
       }
-      const size_t tb = tab.size() * sizeof(hc::SWin), cb = 2 * tab.size() * sizeof(unsigned);
+      const size_t tb = tab.size() * sizeof(hc::SWin), cb = (tab.size() + 1) * sizeof(unsigned);
       std::unique_ptr<StackGraph> sg(new StackGraph());
       CUDA_TRY(sg->table.alloc(tb));
       CUDA_TRY(sg->cnt.alloc(cb));
@@ -1084,13 +1082,12 @@ extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, voi
       hc::StackArgs sa;
       sa.wins = (const hc::SWin*)sg->table.p;
       sa.n_win = (int)tab.size();
-      sa.xs_ld = k_max + 32;
-      sa.u_slot_chunks = u_chunks;
-      sa.n_uslots = n_us;
+      sa.n_vwarps0 = hc::stack_vwarps(tab[0].a.n_chunks * 4 * tab[0].a.G, s_grid);
       sa.done = (unsigned*)sg->cnt.p;
       sa.vdone = sa.done + tab.size();
       CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
       cudaError_t e1 = cudaMemsetAsync(sg->cnt.p, 0, cb, cs);
+      if (e1 == cudaSuccess) e1 = hc::launch_xprep((const uint16_t*)dx, d, B, d, bits0, xh16, cs);
       cudaError_t e2 = e1 == cudaSuccess ? hc::launch_stack(sa, bits0, s_grid, s_smem, cs) : e1;
       cudaGraph_t g = nullptr;
       cudaError_t e = cudaStreamEndCapture(cs, &g);

@@ -62,16 +62,6 @@ cudaError_t decode_set_trace(void* buf) { return cudaMemcpyToSymbol(g_dtrace, &b
 // window's t accumulators with 64-bit fixed-point atomics (exact integer adds: t is bit-identical
 // for any arrival order), then bumps v_done; each CTA's epilogue warp acquires v_done once and reads
 // t while its tile warps are still streaming.
-// The next window's x' (fp16, pre-scaled by the code-field exponent of its column pair, layout.h) of
-// one output element (bf16 bits) at output column n, batch row b.
-template <int BITS>
-__device__ __forceinline__ void write_xprime(const DArgs& a, int b, int n, uint16_t bits) {
-  const int k = n - a.y16_lo, kk = k & (kGroup - 1);
-  const int j = 2 * (kk >> 5) + ((kk >> 2) & 1), pr = (kk >> 1) & 1;
-  const float xv = bf16_bits_to_f32(bits) * __uint_as_float((uint32_t)(127 - step_fp(BITS, j, pr)) << 23);
-  a.y16[(size_t)b * (a.y16_hi - a.y16_lo) + k] = __half_as_ushort(__float2half_rn(xv));
-}
-
 // Wait for this window's inputs: the producer window's completion counter (acquire; every warp that
 // reads activations calls this), else the programmatic-dependent-launch grid dependency.
 __device__ __forceinline__ void dep_wait(const DArgs& a, int lane) {

@@ -186,7 +186,9 @@ __device__ __forceinline__ int xrow(const DArgs& a, int col) { return col < a.B 
 
 // x' fragments of group g from the window's fp16 x' buffer (global, L1-cached):
 // xr[nb][4q + e] = x'[b][g*128 + 32q + 8tig .. +7]
-template <int NB8>
+// NC: read-only path (x' written before the launch); !NC: coherent weak loads, for x' written by an
+// earlier window of the same launch (persistent stack kernel; ordered by an acquire + bar.sync)
+template <int NB8, bool NC = true>
 __device__ __forceinline__ void load_x_global(const DArgs& a, int g, int lane, uint32_t (&xr)[NB8][16]) {
 #pragma unroll
   for (int nb = 0; nb < NB8; ++nb) {
@@ -194,7 +196,9 @@ __device__ __forceinline__ void load_x_global(const DArgs& a, int g, int lane, u
                                                     g * kGroup + 8 * (lane & 3));
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const uint4 v = __ldg(p + 4 * q);
+      uint4 v;
+      if (NC) v = __ldg(p + 4 * q);
+      else asm volatile("ld.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p + 4 * q));
       xr[nb][4 * q + 0] = v.x; xr[nb][4 * q + 1] = v.y; xr[nb][4 * q + 2] = v.z; xr[nb][4 * q + 3] = v.w;
     }
   }
@@ -331,6 +335,16 @@ __device__ __forceinline__ void v_tile(const uint8_t* piece, int lane, const uin
       else        mma16816(tot[nb], af, xv[nb].z, xv[nb].w);
     }
   }
+}
+
+// The next window's x' (fp16, pre-scaled by the code-field exponent of its column pair, layout.h) of
+// one output element (bf16 bits) at output column n, batch row b.
+template <int BITS>
+__device__ __forceinline__ void write_xprime(const DArgs& a, int b, int n, uint16_t bits) {
+  const int k = n - a.y16_lo, kk = k & (kGroup - 1);
+  const int j = 2 * (kk >> 5) + ((kk >> 2) & 1), pr = (kk >> 1) & 1;
+  const float xv = bf16_bits_to_f32(bits) * __uint_as_float((uint32_t)(127 - step_fp(BITS, j, pr)) << 23);
+  a.y16[(size_t)b * (a.y16_hi - a.y16_lo) + k] = __half_as_ushort(__float2half_rn(xv));
 }
 
 }  // namespace
