@@ -39,7 +39,7 @@ namespace hc {
 #define HC_DEC_TRACE 0
 #endif
 // dev tracing: globaltimer stamps per (launch slot, CTA): [0] start, [1] after the PDL wait (epilogue),
-// [2] first FULL passed, [3] last FULL passed, [4] epilogue done
+// [2] first FULL passed, [3] last FULL passed, [4] epilogue done, [5] t ready
 __device__ unsigned long long* g_dtrace = nullptr;
 __device__ __forceinline__ void dtrace(const DArgs& a, int ev) {
 #if HC_DEC_TRACE
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
         // once per CTA, while the tile warps still stream: acquire t (all tile warps of the grid
         // have added their V·x shares) and keep its fragments in smem as fp32
         if (lane == 0) {
-          while (ld_relaxed(&a.cnt[0]) < (unsigned)n_vwarps) __nanosleep(32);
+          while (ld_relaxed(&a.cnt[0]) < (unsigned)n_vctas) __nanosleep(32);
           (void)ld_acquire(&a.cnt[0]);
         }
         __syncwarp();
@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
         }
         __syncwarp();
         t_ready = true;
+        if (lane == 0) dtrace(a, 5);
       }
       // t forwarding: this item's outputs are x of the next window at k = n0 - fwd_lo .. (16 or 8 of them);
       // fetch the next window's natural-k V fragments of that 16-k block while the tile warps work
@@ -411,6 +412,64 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
   if (!a.dep_cnt) dep_wait(a, lane);
   else if (!XS) asm volatile("bar.sync 6, %0;" ::"n"(kDecodeThreads) : "memory");   // the epilogue warp waited
   else if (n_vp > 0) dep_wait(a, lane);
+  const uint16_t* xs_row[NB8];
+#pragma unroll
+  for (int nb = 0; nb < NB8; ++nb) xs_row[nb] = xs + (size_t)xrow(a, gid + 8 * nb) * xs_ld + 8 * tig;
+
+  unsigned blk_done = 0;
+  // ---- rank projection share: t[cc][col][rank] += V pieces · x   (64-bit fixed point, exact adds).
+  // Runs before the x' staging below (it reads bf16 x from L2): t is on the critical path of every
+  // epilogue.  Partials of consecutive pieces of one chunk are summed in registers before the atomics.
+  {
+    float tp[NB8][4];
+    auto flush = [&](int cc) {
+#pragma unroll
+      for (int nb = 0; nb < NB8; ++nb)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int col = 2 * tig + (e & 1) + 8 * nb, rank = gid + 8 * (e >> 1);
+          if (col < a.B)
+            atomicAdd(reinterpret_cast<unsigned long long*>(a.tacc + ((size_t)cc * 16 + col) * 16 + rank),
+                      (unsigned long long)__float2ll_rn(tp[nb][e] * kTScale));
+          tp[nb][e] = 0.f;
+        }
+    };
+#pragma unroll
+    for (int nb = 0; nb < NB8; ++nb)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) tp[nb][e] = 0.f;
+    int cc_cur = -1;
+    for (int vp = vp0; vp < vp1; ++vp) {
+      const int s = blk_done % kNBuf;
+      const uint32_t ph = (blk_done / kNBuf) & 1u;
+      int g, part;
+      v_piece(a, vp, g, part);
+      const int cc = vp / (4 * a.G);
+      if (cc != cc_cur) {
+        if (cc_cur >= 0) flush(cc_cur);
+        cc_cur = cc;
+      }
+      uint4 xv[NB8];
+#pragma unroll
+      for (int nb = 0; nb < NB8; ++nb) {
+        const uint4* p = reinterpret_cast<const uint4*>(a.x + (size_t)xrow(a, gid + 8 * nb) * a.ldx + 8 * tig +
+                                                        g * kGroup + 32 * part);
+        xv[nb] = __ldcg(p);                              // bf16 x from L2 (written by the producer window)
+      }
+      while (!mbar_try_wait(&bars[s], ph)) {}
+      v_tile<NB8>(bufs + s * kBlk, lane, xv, tp);
+      __syncwarp();
+      ++blk_done;
+      issue_block();
+    }
+    if (cc_cur >= 0) flush(cc_cur);
+  }
+  if (v_warp) {
+    // v_done counts CTAs: the CTA's V warps meet at a named barrier, then one release add orders all
+    // of their t adds before it (cumulativity through the barrier)
+    asm volatile("bar.sync 7, %0;" ::"n"(kDecodeWarps * 32) : "memory");
+    if (warp == 0 && lane == 0) add_release(&a.cnt[0], 1u);
+  }
   if constexpr (XS) {
     while (!mbar_try_wait(xbar, 0)) {}
     // in place: x (bf16) -> x' = x·2^-fp (fp16, the B operand of the W mma); 16 elements per thread
@@ -425,50 +484,6 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
     }
     asm volatile("bar.sync 5, %0;" ::"n"(kDecodeWarps * 32) : "memory");   // tile warps only
   }
-  const uint16_t* xs_row[NB8];
-#pragma unroll
-  for (int nb = 0; nb < NB8; ++nb) xs_row[nb] = xs + (size_t)xrow(a, gid + 8 * nb) * xs_ld + 8 * tig;
-
-  unsigned blk_done = 0;
-  // ---- rank projection share: t[cc][col][rank] += V piece · x   (64-bit fixed point, exact adds)
-  for (int vp = vp0; vp < vp1; ++vp) {
-    const int s = blk_done % kNBuf;
-    const uint32_t ph = (blk_done / kNBuf) & 1u;
-    int g, part;
-    v_piece(a, vp, g, part);
-    const int cc = vp / (4 * a.G);
-    uint4 xv[NB8];
-#pragma unroll
-    for (int nb = 0; nb < NB8; ++nb) {
-      const uint4* p = reinterpret_cast<const uint4*>(a.x + (size_t)xrow(a, gid + 8 * nb) * a.ldx + 8 * tig +
-                                                      g * kGroup + 32 * part);
-      xv[nb] = __ldcg(p);                                // bf16 x from L2 (written by the producer window)
-    }
-    while (!mbar_try_wait(&bars[s], ph)) {}
-    float tp[NB8][4];
-#pragma unroll
-    for (int nb = 0; nb < NB8; ++nb)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) tp[nb][e] = 0.f;
-    v_tile<NB8>(bufs + s * kBlk, lane, xv, tp);
-    __syncwarp();
-    ++blk_done;
-    issue_block();
-#pragma unroll
-    for (int nb = 0; nb < NB8; ++nb)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int col = 2 * tig + (e & 1) + 8 * nb, rank = gid + 8 * (e >> 1);
-        if (col < a.B)
-          atomicAdd(reinterpret_cast<unsigned long long*>(a.tacc + ((size_t)cc * 16 + col) * 16 + rank),
-                    (unsigned long long)__float2ll_rn(tp[nb][e] * kTScale));
-      }
-  }
-  if (v_warp) {
-    __syncwarp();
-    if (lane == 0) add_release(&a.cnt[0], 1u);          // v_done: orders the warp's t adds before it
-  }
-
   int k = 0;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++k) {
     const int par = k & 1;

@@ -346,29 +346,41 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) stack_kernel(const __grid_c
   for (int s = 0; s < kNBuf; ++s) issue_block();
 
   unsigned blk_done = 0;
-  // ---- window 0 rank projection share (x from L2; t in 2^-28 fixed point, exact adds)
-  for (int vp = vp0; vp < vp1; ++vp) {
-    const int s = blk_done % kNBuf;
-    const uint32_t ph = (blk_done / kNBuf) & 1u;
-    int g, part;
-    v_piece(W0.a, vp, g, part);
-    const int cc = vp / (4 * W0.a.G);
-    uint4 xv[1];
-    xv[0] = __ldcg(reinterpret_cast<const uint4*>(W0.a.x + (size_t)xrow(W0.a, gid) * W0.a.ldx + 8 * tig + g * kGroup +
-                                                  32 * part));
-    while (!mbar_try_wait(&bars[s], ph)) {}
+  // ---- window 0 rank projection share (x from L2; t in 2^-28 fixed point, exact adds); partials of
+  // consecutive pieces of one chunk summed in registers first (same grouping as decode.cu)
+  {
     float tp[1][4] = {{0.f, 0.f, 0.f, 0.f}};
-    v_tile<1>(bufs + s * kSBlk, lane, xv, tp);
-    __syncwarp();
-    ++blk_done;
-    issue_block();
+    auto flush = [&](int cc) {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int col = 2 * tig + (e & 1), rk = gid + 8 * (e >> 1);
-      if (col < W0.a.B)
-        atomicAdd(reinterpret_cast<unsigned long long*>(W0.a.tacc + ((size_t)cc * 16 + col) * 16 + rk),
-                  (unsigned long long)__float2ll_rn(tp[0][e] * kTScale));
+      for (int e = 0; e < 4; ++e) {
+        const int col = 2 * tig + (e & 1), rk = gid + 8 * (e >> 1);
+        if (col < W0.a.B)
+          atomicAdd(reinterpret_cast<unsigned long long*>(W0.a.tacc + ((size_t)cc * 16 + col) * 16 + rk),
+                    (unsigned long long)__float2ll_rn(tp[0][e] * kTScale));
+        tp[0][e] = 0.f;
+      }
+    };
+    int cc_cur = -1;
+    for (int vp = vp0; vp < vp1; ++vp) {
+      const int s = blk_done % kNBuf;
+      const uint32_t ph = (blk_done / kNBuf) & 1u;
+      int g, part;
+      v_piece(W0.a, vp, g, part);
+      const int cc = vp / (4 * W0.a.G);
+      if (cc != cc_cur) {
+        if (cc_cur >= 0) flush(cc_cur);
+        cc_cur = cc;
+      }
+      uint4 xv[1];
+      xv[0] = __ldcg(reinterpret_cast<const uint4*>(W0.a.x + (size_t)xrow(W0.a, gid) * W0.a.ldx + 8 * tig + g * kGroup +
+                                                    32 * part));
+      while (!mbar_try_wait(&bars[s], ph)) {}
+      v_tile<1>(bufs + s * kSBlk, lane, xv, tp);
+      __syncwarp();
+      ++blk_done;
+      issue_block();
     }
+    if (cc_cur >= 0) flush(cc_cur);
   }
   if (v_warp) {
     __syncwarp();
