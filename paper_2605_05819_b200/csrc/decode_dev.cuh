@@ -250,7 +250,9 @@ __device__ __forceinline__ void w_tile_regs(const uint32_t (&w)[2 * BITS], uint3
       for (int nb = 0; nb < NB8; ++nb) mma16816_f16(acc[nb], af, xq[nb][2 * jj], xq[nb][2 * jj + 1]);
     }
   }
-  const float s0 = bf16_bits_to_f32(sw & 0xFFFFu), s1 = bf16_bits_to_f32(sw >> 16);
+  // row gid + 8 registers may carry 2^row_hi_shift (layout.h): exact power-of-two rescale
+  const float s0 = bf16_bits_to_f32(sw & 0xFFFFu),
+              s1 = bf16_bits_to_f32(sw >> 16) * (1.f / (float)(1 << row_hi_shift(BITS)));
 #pragma unroll
   for (int nb = 0; nb < NB8; ++nb) {
     tot[nb][0] = fmaf(s0, acc[nb][0], tot[nb][0]);

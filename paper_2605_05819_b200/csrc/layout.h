@@ -26,10 +26,13 @@
 // Register extraction ("slots"): register (j, i) = 0x64006400 | field bits, where a
 // field is up to 3 "parts" (word, shift, pos, nbits) taken from the lo 16-bit half
 // (and the same bits +16 from the hi half).  The register then holds
-// 1024 + q*2^fp in both halves (exact in fp16), fp = the field's bit position.  The two
-// registers of a column pair (i, i^1) share fp, so the B operand (x) of that pair is
-// pre-scaled by 2^-fp once (x' = x·2^-fp, exact in fp16 for normal-range x; R20).
-//   4-bit: word j, fields at bits [0,4) (fp 0) and [4,8) (fp 4) of w and of w >> 8;
+// 1024 + q*2^fp in both halves (exact in fp16), fp = the field's bit position.  The B operand
+// (x) of k pair p is pre-scaled by 2^-fp of the row-gid register (i = 2p): x' = x·2^-fp, exact in
+// fp16 for normal-range x (R20).  The row gid + 8 register of the pair may sit
+// row_hi_shift(bits) bits higher; its products are then 2^row_hi_shift too large and that row's
+// group scale is divided by the same power of two (exact).
+//   4-bit: word j, fields at bits [0,4) (fp 0, row gid) and [4,8) (fp 4, row gid + 8) of w and
+//          of w >> 8 (k pairs 0 and 1); x' = x;
 //   2-bit: word j/2, fields at bits 2p (fp 2p, p = (i>>1) + 2(j&1)) of w and of w >> 8;
 //   3-bit: fields at bits 0-2 and 3-5 (fp 3) of w >> {0, 6, 12}, plus two registers gathered
 //          from bit 15 of the six words.
@@ -67,8 +70,12 @@ struct Slot { int nparts; int fp; Part p[3]; };
 // Slot table for register (j, i) at a given bit width.  See the header comment.
 HC_HD constexpr Slot slot(int bits, int j, int i) {
   if (bits == 4) {
-    const int fp = 4 * (i >> 1);
-    return Slot{1, fp, {Part{j, 8 * (i & 1), fp, 4}, Part{0, 0, 0, 0}, Part{0, 0, 0, 0}}};
+    // row gid (i even) <- the low nibbles of word j's bytes, row gid + 8 (i odd) <- the high
+    // nibbles; k pair i>>1 <- bytes {0, 2} (shift 0) or {1, 3} (shift 8).  Each byte-wise half of
+    // a word is one row's 4 codes, so `w & 0x0F0F0F0F` / `w & 0xF0F0F0F0` are u8 A-fragments of
+    // the int8 mma path (decode_i8.cuh) and the fp16 path extracts with one lop3 per register.
+    const int fp = 4 * (i & 1);
+    return Slot{1, fp, {Part{j, 8 * (i >> 1), fp, 4}, Part{0, 0, 0, 0}, Part{0, 0, 0, 0}}};
   }
   if (bits == 2) {
     const int fp = 2 * (i >> 1) + 4 * (j & 1);
@@ -89,6 +96,9 @@ HC_HD constexpr Slot slot(int bits, int j, int i) {
   const int base = (w1 == 18) ? 0 : 3;   // gather bit 15 of words base..base+2
   return Slot{3, 0, {Part{base, 15, 0, 1}, Part{base + 1, 14, 1, 1}, Part{base + 2, 13, 2, 1}}};
 }
+
+// Extra exponent of the row gid + 8 registers over the row gid registers of the same k pair.
+HC_HD constexpr int row_hi_shift(int bits) { return bits == 4 ? 4 : 0; }
 
 // x pre-scale exponent for the B register of step j: pair 0 (b0, cols 2tig..) or pair 1 (b1).
 HC_HD constexpr int step_fp(int bits, int j, int pair) { return slot(bits, j, 2 * pair).fp; }
