@@ -1134,10 +1134,14 @@ extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, voi
         const bool hx = hx_ok;
         uint16_t* xq16 = (uint16_t*)ctx->s_x16[0].p, *xh1 = (uint16_t*)ctx->s_x16[1].p;
         uint16_t* xm16 = (uint16_t*)ctx->s_x16[2].p, *xh16 = (uint16_t*)ctx->s_x16[3].p;
-        const hc::X16Spec x_q{hx && l > 0 ? xh16 : nullptr, hx ? xq16 : nullptr, 0, d};
-        const hc::X16Spec x_o{hx ? xq16 : nullptr, hx ? xh1 : nullptr, 0, d};
-        const hc::X16Spec x_ug{hx ? xh1 : nullptr, hx ? xm16 : nullptr, 0, f};
-        const hc::X16Spec x_dn{hx ? xm16 : nullptr, (hx && l + 1 < plan.size()) ? xh16 : nullptr, 0, d};
+        // int8-path windows (decode_uses_i8) stage bf16 x themselves: no x' hand-off into them
+        auto i8w = [&](Window* w) { return hc::decode_uses_i8(w->members.front().bits, B, w->members.front().K); };
+        const bool i8q = i8w(p.qkv), i8o = i8w(p.o), i8ug = i8w(p.ug), i8dn = i8w(p.down);
+        const bool i8qn = l + 1 < plan.size() ? i8w(plan[l + 1].qkv) : true;
+        const hc::X16Spec x_q{hx && l > 0 && !i8q ? xh16 : nullptr, hx && !i8o ? xq16 : nullptr, 0, d};
+        const hc::X16Spec x_o{hx && !i8o ? xq16 : nullptr, hx && !i8ug ? xh1 : nullptr, 0, d};
+        const hc::X16Spec x_ug{hx && !i8ug ? xh1 : nullptr, hx && !i8dn ? xm16 : nullptr, 0, f};
+        const hc::X16Spec x_dn{hx && !i8dn ? xm16 : nullptr, (hx && !i8qn) ? xh16 : nullptr, 0, d};
         const bool dq = sx_q || (hx && l > 0), do_ = sx_q || hx, dug = sx_q || hx, ddn = sx_f || hx;
         const bool kq = sx_q || hx, ko = sx_q || hx, kug = sx_f || hx;     // keep(producer) = dep(consumer)
         const bool kdn = l + 1 < plan.size() && (sx_q || hx);

@@ -31,6 +31,7 @@
 
 #include "decode.h"
 #include "decode_dev.cuh"
+#include "decode_i8.cuh"
 #include "layout.h"
 
 namespace hc {
@@ -77,7 +78,8 @@ __device__ __forceinline__ void dep_wait(const DArgs& a, int lane) {
   }
 }
 
-template <int BITS, int NB8, bool XS>
+// I8: int8 tensor-core path (decode_i8.cuh; BITS = 4, NB8 = 1, B <= 2): x staged as x8 digits
+template <int BITS, int NB8, bool XS, bool I8>
 __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(const __grid_constant__ DArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -133,9 +135,9 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
     };
     prefetch_u(blockIdx.x, 0);                           // weights: before the PDL wait
     dep_wait(a, lane);
-    if (!XS && a.dep_cnt) asm volatile("bar.sync 6, %0;" ::"n"(kDecodeThreads) : "memory");   // release the tile warps
+    if ((!XS || I8) && a.dep_cnt) asm volatile("bar.sync 6, %0;" ::"n"(kDecodeThreads) : "memory");   // release the tile warps
     if (lane == 0) dtrace(a, 1);
-    if constexpr (XS) {
+    if constexpr (XS && !I8) {
       if (lane == 0) {
         mbar_expect_tx(xbar, (uint32_t)(a.B * a.K * 2));
         for (int b = 0; b < a.B; ++b)
@@ -410,7 +412,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
   // tile warps read activations only through the x staged by the epilogue warp (XS, ordered by its
   // acquire and the x mbarrier), except for V pieces and unstaged x: only then do they wait themselves
   if (!a.dep_cnt) dep_wait(a, lane);
-  else if (!XS) asm volatile("bar.sync 6, %0;" ::"n"(kDecodeThreads) : "memory");   // the epilogue warp waited
+  else if (!XS || I8) asm volatile("bar.sync 6, %0;" ::"n"(kDecodeThreads) : "memory");   // the epilogue warp waited
   else if (n_vp > 0) dep_wait(a, lane);
   const uint16_t* xs_row[NB8];
 #pragma unroll
@@ -470,7 +472,11 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
     asm volatile("bar.sync 7, %0;" ::"n"(kDecodeWarps * 32) : "memory");
     if (warp == 0 && lane == 0) add_release(&a.cnt[0], 1u);
   }
-  if constexpr (XS) {
+  if constexpr (I8) {
+    // x (L2) -> int8 digits (smem) of this warp's groups (the same for every item: warp_share)
+    x8_stage(a, reinterpret_cast<uint8_t*>(xs), warp * a.G / kDecodeWarps, (warp + 1) * a.G / kDecodeWarps, lane);
+    __syncwarp();
+  } else if constexpr (XS) {
     while (!mbar_try_wait(xbar, 0)) {}
     // in place: x (bf16) -> x' = x·2^-fp (fp16, the B operand of the W mma); 16 elements per thread
     const int tid = threadIdx.x;   // 0..255 (tile warps)
@@ -499,7 +505,18 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
       const int nt = min(kTPB, sh.n - t0);
       const uint8_t* blk = bufs + s * kBlk;
       while (!mbar_try_wait(&bars[s], ph)) {}
-      if (nt == kTPB) {
+      if constexpr (I8) {
+        const uint8_t* x8 = reinterpret_cast<const uint8_t*>(xs);
+        float (&t1)[1][4] = *reinterpret_cast<float(*)[1][4]>(&tot[0][0]);
+        if (nt == kTPB) {
+#pragma unroll
+          for (int t = 0; t < kTPB; ++t)
+            i8_tile(blk + t * rec_bytes(4), lane, x8 + (size_t)(sh.g0 + t0 + t) * kX8Group, t1);
+        } else {
+          for (int t = 0; t < nt; ++t)
+            i8_tile(blk + t * rec_bytes(4), lane, x8 + (size_t)(sh.g0 + t0 + t) * kX8Group, t1);
+        }
+      } else if (nt == kTPB) {
         // full block: the records are independent straight-line code, so their mma chains interleave
 #pragma unroll
         for (int t = 0; t < kTPB; ++t) {
@@ -526,6 +543,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
       ++blk_done;
       issue_block();
     }
+    if constexpr (I8) i8_finish(*reinterpret_cast<float(*)[1][4]>(&tot[0][0]), lane, a.B);
     // ---- hand the partial sums to the epilogue warp
     if (k >= 2) asm volatile("bar.sync %0, %1;" ::"r"(3 + par), "n"(kDecodeThreads) : "memory");   // EMPTY[par]
     float* rb_ = red + ((size_t)(par * kDecodeWarps + warp) * 32 + lane) * 4 * NB8;
@@ -536,12 +554,13 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
   }
 }
 
-static size_t decode_smem_bytes(bool xs, int B, int K, int n_chunks, int fwd_chunks) {
+static size_t decode_smem_bytes(bool xs, bool i8, int B, int K, int n_chunks, int fwd_chunks) {
   const int nb8 = B > 8 ? 2 : 1;
   size_t s = (size_t)kDecodeWarps * kNBuf * kTPB * kTileMax + 2 * kDecodeWarps * 32 * 4 * nb8 * sizeof(float) +
              2 * kUPre * 32 * 16 + (kDecodeWarps * kNBuf + 4) * sizeof(uint64_t) +
              (size_t)n_chunks * nb8 * 32 * 16 + 512 + (size_t)fwd_chunks * 512;
-  if (xs) s += (size_t)B * (K + 32) * 2;
+  if (i8) s += (size_t)(K / kGroup) * kX8Group;
+  else if (xs) s += (size_t)B * (K + 32) * 2;
   return s;
 }
 
@@ -550,6 +569,14 @@ constexpr size_t kSmemOptin = 227 * 1024;   // x staged in smem when B*(K+32)*2 
 
 static bool use_xs(int B, int K) { return B <= 8 && (size_t)B * (K + 32) * 2 <= kXsMax; }
 bool decode_stages_x(int B, int K) { return B <= 8 && use_xs(B, K); }
+
+// int8 path (decode_i8.cuh): 4-bit codes, B <= 2, x8 of all groups in shared memory
+constexpr size_t kX8Max = 40 * 1024;
+static bool use_i8(int bits, int B, int K) {
+  static const bool on = [] { const char* e = getenv("HC_I8"); return !(e && e[0] == '0'); }();
+  return on && bits == 4 && B <= 2 && (size_t)(K / kGroup) * kX8Group <= kX8Max;
+}
+bool decode_uses_i8(int bits, int B, int K) { return use_xs(B, K) && use_i8(bits, B, K); }
 
 // x -> x' (fp16, pre-scaled per the code layout) for the !XS decode launches.
 // One thread per (group, batch row, 16-element part).
@@ -588,13 +615,13 @@ cudaError_t launch_xprep(const uint16_t* x, int ldx, int B, int K, int bits, uin
   }
 }
 
-template <int BITS, int NB8, bool XS>
+template <int BITS, int NB8, bool XS, bool I8>
 static cudaError_t launch_t(const DArgs& a, int grid, cudaStream_t st) {
-  const size_t smem = decode_smem_bytes(XS, a.B, a.K, a.n_chunks, a.fwd ? a.fwd_chunks : 0);
+  const size_t smem = decode_smem_bytes(XS, I8, a.B, a.K, a.n_chunks, a.fwd ? a.fwd_chunks : 0);
   if (smem > kSmemOptin) return cudaErrorInvalidConfiguration;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(decode_kernel<BITS, NB8, XS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(decode_kernel<BITS, NB8, XS, I8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kSmemOptin);
     if (e != cudaSuccess) return e;
     attr = true;
@@ -609,16 +636,16 @@ static cudaError_t launch_t(const DArgs& a, int grid, cudaStream_t st) {
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, decode_kernel<BITS, NB8, XS>, a);
+  return cudaLaunchKernelEx(&cfg, decode_kernel<BITS, NB8, XS, I8>, a);
 }
 
-template <int BITS, int NB8, bool XS>
+template <int BITS, int NB8, bool XS, bool I8>
 static int max_ctas_t(int B, int K, int n_chunks, int fwd_chunks) {
-  const size_t smem = decode_smem_bytes(XS, B, K, n_chunks, fwd_chunks);
-  cudaFuncSetAttribute(decode_kernel<BITS, NB8, XS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t smem = decode_smem_bytes(XS, I8, B, K, n_chunks, fwd_chunks);
+  cudaFuncSetAttribute(decode_kernel<BITS, NB8, XS, I8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)kSmemOptin);
   int per_sm = 0, dev = 0, sms = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<BITS, NB8, XS>, kDecodeThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<BITS, NB8, XS, I8>, kDecodeThreads, smem);
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   return per_sm * sms;
@@ -628,12 +655,14 @@ static int max_ctas_t(int B, int K, int n_chunks, int fwd_chunks) {
   do {                                                                             \
     const bool two = a_B > 8, xs = use_xs(a_B, a_K) && !a_noxs;                   \
     switch (bits) {                                                                \
-      case 2: return two ? FN<2, 2, false>(__VA_ARGS__)                            \
-                         : (xs ? FN<2, 1, true>(__VA_ARGS__) : FN<2, 1, false>(__VA_ARGS__)); \
-      case 3: return two ? FN<3, 2, false>(__VA_ARGS__)                            \
-                         : (xs ? FN<3, 1, true>(__VA_ARGS__) : FN<3, 1, false>(__VA_ARGS__)); \
-      case 4: return two ? FN<4, 2, false>(__VA_ARGS__)                            \
-                         : (xs ? FN<4, 1, true>(__VA_ARGS__) : FN<4, 1, false>(__VA_ARGS__)); \
+      case 2: return two ? FN<2, 2, false, false>(__VA_ARGS__)                     \
+                         : (xs ? FN<2, 1, true, false>(__VA_ARGS__) : FN<2, 1, false, false>(__VA_ARGS__)); \
+      case 3: return two ? FN<3, 2, false, false>(__VA_ARGS__)                     \
+                         : (xs ? FN<3, 1, true, false>(__VA_ARGS__) : FN<3, 1, false, false>(__VA_ARGS__)); \
+      case 4: return two ? FN<4, 2, false, false>(__VA_ARGS__)                     \
+                         : (xs ? (use_i8(4, a_B, a_K) ? FN<4, 1, true, true>(__VA_ARGS__)                   \
+                                                      : FN<4, 1, true, false>(__VA_ARGS__))                 \
+                               : FN<4, 1, false, false>(__VA_ARGS__));                                     \
       default: break;                                                              \
     }                                                                              \
   } while (0)

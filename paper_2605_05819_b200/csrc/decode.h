@@ -88,6 +88,9 @@ struct DArgs {
 cudaError_t launch_decode(const DArgs& a, int bits, int grid, cudaStream_t st);
 // Whether a launch with this batch / K stages x in shared memory (else it needs launch_xprep first).
 bool decode_stages_x(int B, int K);
+// Whether an unstaged-x' launch (x16 not given) of this shape runs the int8 path (decode_i8.cuh); such
+// a window reads bf16 x itself, so its producer writes no x' hand-off for it.
+bool decode_uses_i8(int bits, int B, int K);
 // x' (fp16, pre-scaled per the code layout of `bits`) for a !XS decode launch.
 cudaError_t launch_xprep(const uint16_t* x, int ldx, int B, int K, int bits, uint16_t* x16, cudaStream_t st);
 cudaError_t decode_set_trace(void* buf);   // dev: [slots][grid][8] globaltimer stamps (HC_DEC_TRACE builds)
