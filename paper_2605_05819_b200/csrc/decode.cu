@@ -378,9 +378,9 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
   int vp_issue = vp0;
   int p_item = blockIdx.x, p_t = 0;
   Share p_sh = p_item < n_items ? warp_share<BITS>(a, p_item, warp) : Share{nullptr, 0, 1024, 0, 0, 0};
-  unsigned blk_issued = 0;
+  int p_slot = 0;               // ring slot of the next block issued (no div/mod on the hot path)
   auto issue_block = [&]() {   // issue the next block (a V piece or up to kTPB weight tiles), if any
-    const int s = blk_issued % kNBuf;
+    const int s = p_slot;
     if (vp_issue < vp1) {
       int g, part;
       const uint8_t* src = v_piece(a, vp_issue, g, part);
@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
         bulk_copy(bufs + s * kBlk, src, 1024u, &bars[s], pol_w);
       }
       ++vp_issue;
-      ++blk_issued;
+      p_slot = p_slot + 1 == kNBuf ? 0 : p_slot + 1;
       return;
     }
     while (p_item < n_items && p_t >= p_sh.n) {
@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
       bulk_copy(bufs + s * kBlk, p_sh.base + (size_t)p_t * p_sh.tb, bytes, &bars[s], pol_w);
     }
     p_t += nt;
-    ++blk_issued;
+    p_slot = p_slot + 1 == kNBuf ? 0 : p_slot + 1;
   };
 #pragma unroll
   for (int s = 0; s < kNBuf; ++s) issue_block();   // weights / V: before the PDL wait
@@ -418,7 +418,9 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
 #pragma unroll
   for (int nb = 0; nb < NB8; ++nb) xs_row[nb] = xs + (size_t)xrow(a, gid + 8 * nb) * xs_ld + 8 * tig;
 
-  unsigned blk_done = 0;
+  int c_slot = 0;          // consumer ring position: slot and mbarrier phase
+  uint32_t c_ph = 0;
+  auto advance = [&]() { if (++c_slot == kNBuf) { c_slot = 0; c_ph ^= 1u; } };
   // ---- rank projection share: t[cc][col][rank] += V pieces · x   (64-bit fixed point, exact adds).
   // Runs before the x' staging below (it reads bf16 x from L2): t is on the critical path of every
   // epilogue.  Partials of consecutive pieces of one chunk are summed in registers before the atomics.
@@ -442,8 +444,8 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
       for (int e = 0; e < 4; ++e) tp[nb][e] = 0.f;
     int cc_cur = -1;
     for (int vp = vp0; vp < vp1; ++vp) {
-      const int s = blk_done % kNBuf;
-      const uint32_t ph = (blk_done / kNBuf) & 1u;
+      const int s = c_slot;
+      const uint32_t ph = c_ph;
       int g, part;
       v_piece(a, vp, g, part);
       const int cc = vp / (4 * a.G);
@@ -461,7 +463,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
       while (!mbar_try_wait(&bars[s], ph)) {}
       v_tile<NB8>(bufs + s * kBlk, lane, xv, tp);
       __syncwarp();
-      ++blk_done;
+      advance();
       issue_block();
     }
     if (cc_cur >= 0) flush(cc_cur);
@@ -493,15 +495,16 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
   int k = 0;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++k) {
     const int par = k & 1;
-    const Share sh = warp_share<BITS>(a, item, warp);
+    // this warp's groups of every item: [g0, g0 + n) (warp_share; independent of the item)
+    const struct { int n, g0; } sh = {(warp + 1) * a.G / kDecodeWarps - warp * a.G / kDecodeWarps, warp * a.G / kDecodeWarps};
     float tot[NB8][4];
 #pragma unroll
     for (int nb = 0; nb < NB8; ++nb)
 #pragma unroll
       for (int e = 0; e < 4; ++e) tot[nb][e] = 0.f;
     for (int t0 = 0; t0 < sh.n; t0 += kTPB) {
-      const int s = blk_done % kNBuf;
-      const uint32_t ph = (blk_done / kNBuf) & 1u;
+      const int s = c_slot;
+      const uint32_t ph = c_ph;
       const int nt = min(kTPB, sh.n - t0);
       const uint8_t* blk = bufs + s * kBlk;
       while (!mbar_try_wait(&bars[s], ph)) {}
@@ -540,7 +543,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
         }
       }
       __syncwarp();
-      ++blk_done;
+      advance();
       issue_block();
     }
     if constexpr (I8) i8_finish(*reinterpret_cast<float(*)[1][4]>(&tot[0][0]), lane, a.B);
