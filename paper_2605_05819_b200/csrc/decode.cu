@@ -510,14 +510,15 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
       while (!mbar_try_wait(&bars[s], ph)) {}
       if constexpr (I8) {
         const uint8_t* x8 = reinterpret_cast<const uint8_t*>(xs);
+        const int xg = x8_stride(a.B), dd = 512 * a.B;
         float (&t1)[1][4] = *reinterpret_cast<float(*)[1][4]>(&tot[0][0]);
         if (nt == kTPB) {
 #pragma unroll
           for (int t = 0; t < kTPB; ++t)
-            i8_tile(blk + t * rec_bytes(4), lane, x8 + (size_t)(sh.g0 + t0 + t) * kX8Group, t1);
+            i8_tile<BITS>(blk + t * rec_bytes(BITS), lane, x8 + (size_t)(sh.g0 + t0 + t) * xg, dd, t1);
         } else {
           for (int t = 0; t < nt; ++t)
-            i8_tile(blk + t * rec_bytes(4), lane, x8 + (size_t)(sh.g0 + t0 + t) * kX8Group, t1);
+            i8_tile<BITS>(blk + t * rec_bytes(BITS), lane, x8 + (size_t)(sh.g0 + t0 + t) * xg, dd, t1);
         }
       } else if (nt == kTPB) {
         // full block: the records are independent straight-line code, so their mma chains interleave
@@ -562,7 +563,7 @@ static size_t decode_smem_bytes(bool xs, bool i8, int B, int K, int n_chunks, in
   size_t s = (size_t)kDecodeWarps * kNBuf * kTPB * kTileMax + 2 * kDecodeWarps * 32 * 4 * nb8 * sizeof(float) +
              2 * kUPre * 32 * 16 + (kDecodeWarps * kNBuf + 4) * sizeof(uint64_t) +
              (size_t)n_chunks * nb8 * 32 * 16 + 512 + (size_t)fwd_chunks * 512;
-  if (i8) s += (size_t)(K / kGroup) * kX8Group;
+  if (i8) s += (size_t)(K / kGroup) * x8_stride(B) + kX8Pad;
   else if (xs) s += (size_t)B * (K + 32) * 2;
   return s;
 }
@@ -577,7 +578,7 @@ bool decode_stages_x(int B, int K) { return B <= 8 && use_xs(B, K); }
 constexpr size_t kX8Max = 40 * 1024;
 static bool use_i8(int bits, int B, int K) {
   static const bool on = [] { const char* e = getenv("HC_I8"); return !(e && e[0] == '0'); }();
-  return on && bits == 4 && B <= 2 && (size_t)(K / kGroup) * kX8Group <= kX8Max;
+  return on && (bits == 4 || bits == 2) && B <= 2 && (size_t)(K / kGroup) * x8_stride(B) + kX8Pad <= kX8Max;
 }
 bool decode_uses_i8(int bits, int B, int K) { return use_xs(B, K) && use_i8(bits, B, K); }
 
@@ -659,7 +660,9 @@ static int max_ctas_t(int B, int K, int n_chunks, int fwd_chunks) {
     const bool two = a_B > 8, xs = use_xs(a_B, a_K) && !a_noxs;                   \
     switch (bits) {                                                                \
       case 2: return two ? FN<2, 2, false, false>(__VA_ARGS__)                     \
-                         : (xs ? FN<2, 1, true, false>(__VA_ARGS__) : FN<2, 1, false, false>(__VA_ARGS__)); \
+                         : (xs ? (use_i8(2, a_B, a_K) ? FN<2, 1, true, true>(__VA_ARGS__)                   \
+                                                      : FN<2, 1, true, false>(__VA_ARGS__))                 \
+                               : FN<2, 1, false, false>(__VA_ARGS__));                                     \
       case 3: return two ? FN<3, 2, false, false>(__VA_ARGS__)                     \
                          : (xs ? FN<3, 1, true, false>(__VA_ARGS__) : FN<3, 1, false, false>(__VA_ARGS__)); \
       case 4: return two ? FN<4, 2, false, false>(__VA_ARGS__)                     \

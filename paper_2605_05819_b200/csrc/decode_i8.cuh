@@ -1,11 +1,13 @@
-// Int8 tensor-core path of the decode kernel (4-bit codes, B <= 2; DESIGN.md §7.1 "I8").
+// Int8 tensor-core path of the decode kernel (2- and 4-bit codes, B <= 2; DESIGN.md §7.1 "I8").
 //
 // The fp16 path spends one lop3 + one hsub2 per two weights (plus shifts) turning codes into fp16
 // A-fragments, which makes the decode loop ALU-bound well below HBM speed.  Here:
 //  * A = the codes themselves as u8: with the 4-bit record layout of layout.h every byte of a code
 //    word holds one code of row gid (low nibble) and one of row gid + 8 (high nibble), so
 //    `w & 0x0F0F0F0F` is a row-gid u8 fragment and `w & 0xF0F0F0F0` a row-(gid + 8) fragment holding
-//    16·q — one lop3 per four weights, no shift, no zero subtraction;
+//    16·q — one lop3 per four weights, no shift, no zero subtraction.  2-bit: the four 2-bit fields
+//    of a byte are (row gid, row gid + 8) x (k block 8tig + 0..3, + 4..7) with weights 1, 4, 16, 64;
+//    the x16 fields run as separate mma steps and join as acc1 + (acc2 >> 4) (exact);
 //  * B = x in block fixed point: per (group, batch row) x_int = rint(x · 2^(29 − e)) with e the
 //    exponent of the group's largest |x| (exact for every x within 2^22 of it), split into four
 //    balanced base-256 digits (s8); mma column n = 4·b + d holds digit d of batch row b;
@@ -16,11 +18,13 @@
 //    like the fp16 path's per-group scale step);
 //  * after the last record of an item the digit partials of a batch row are summed across the two
 //    lanes holding them (fixed order: deterministic).
-// x8 (shared memory, per group: 1056 B):
-//   [n 0..7][tig 0..3][8 x u32]  B fragments: reg 2s + h = b_h of k32-step s, bytes = digit n&3 of
+// x8 (shared memory, per group: x8_stride(B) = 544 B at B = 1, 1056 B at B = 2):
+//   [n < 4B][tig 0..3][8 x u32]  B fragments: reg 2s + h = b_h of k32-step s, bytes = digit n&3 of
 //                                 batch n>>2 at k = 32s + 8tig + 4h + {0, 2, 1, 3}
-//   [tig 0..3] {int DD, float f}  DD = D_(2p) + 256·D_(2p+1) (D_d = Σ_k digit_d of batch b),
-//                                 f = 2^(16p + e_b − 29), for b = tig >> 1, p = tig & 1
+//   [tig < 2B] {int DD, float f} at 512·B: DD = D_(2p) + 256·D_(2p+1) (D_d = Σ_k digit_d of batch
+//                                 b), f = 2^(16p + e_b − 29), for b = tig >> 1, p = tig & 1
+// At B = 1 the lanes of batch-1 columns read whatever follows (their results are discarded); the
+// region carries kX8Pad bytes of slack after the last group for them.
 #pragma once
 #include <stdint.h>
 
@@ -28,7 +32,8 @@
 
 namespace hc {
 
-constexpr int kX8Group = 1056;   // bytes of x8 per group
+__host__ __device__ __forceinline__ int x8_stride(int B) { return B == 1 ? 544 : 1056; }
+constexpr int kX8Pad = 512;
 
 __device__ __forceinline__ void imma16832(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                           uint32_t b0, uint32_t b1) {
@@ -65,7 +70,7 @@ __device__ __forceinline__ void x8_stage(const DArgs& a, uint8_t* x8, int g0, in
 #pragma unroll
     for (int i = 0; i < 4; ++i)
       u[i] = (uint32_t)__float2int_rn(__uint_as_float(hb[i] << 16) * p1 * p2) + 0x80808080u;   // balanced digits + 128
-    uint8_t* blk = x8 + (size_t)g * kX8Group;
+    uint8_t* blk = x8 + (size_t)g * x8_stride(a.B);
     int dsum[4];
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
@@ -83,35 +88,54 @@ __device__ __forceinline__ void x8_stage(const DArgs& a, uint8_t* x8, int g0, in
       int2 v;
       v.x = pp ? dsum[2] + 256 * dsum[3] : dsum[0] + 256 * dsum[1];
       v.y = __float_as_int(pow2f(16 * pp + e - 29));
-      reinterpret_cast<int2*>(blk + 1024)[2 * b + pp] = v;
+      reinterpret_cast<int2*>(blk + 512 * a.B)[2 * b + pp] = v;
     }
   }
 }
 
 // One (row-block, group) record on the int8 path: tot[0] += row gid, tot[2] += row gid + 8 partial
-// of this lane's two digit columns (tot[1], tot[3] unused until i8_finish).
-__device__ __forceinline__ void i8_tile(const uint8_t* rec, int lane, const uint8_t* x8g, float (&tot)[1][4]) {
+// of this lane's two digit columns (tot[1], tot[3] unused until i8_finish).  dd_off = 512·B.
+template <int BITS>
+__device__ __forceinline__ void i8_tile(const uint8_t* rec, int lane, const uint8_t* x8g, int dd_off,
+                                        float (&tot)[1][4]) {
+  static_assert(BITS == 2 || BITS == 4, "int8 path: 2- or 4-bit codes");
   const int gid = lane >> 2, tig = lane & 3;
-  const uint4 w0 = *reinterpret_cast<const uint4*>(rec + lane * 16);
-  const uint4 w1 = *reinterpret_cast<const uint4*>(rec + 512 + lane * 16);
-  const uint32_t w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-  const uint32_t sw = *reinterpret_cast<const uint32_t*>(rec + scales_off(4) + 4 * gid);
-  const uint2 zz = *reinterpret_cast<const uint2*>(rec + zeros_off(4));
+  const uint32_t sw = *reinterpret_cast<const uint32_t*>(rec + scales_off(BITS) + 4 * gid);
+  const uint2 zz = *reinterpret_cast<const uint2*>(rec + zeros_off(BITS));
   const uint4* xb = reinterpret_cast<const uint4*>(x8g) + (gid * 4 + tig) * 2;
   const uint4 bv0 = xb[0], bv1 = xb[1];
   const uint32_t bb[8] = {bv0.x, bv0.y, bv0.z, bv0.w, bv1.x, bv1.y, bv1.z, bv1.w};
-  const int2 ddf = reinterpret_cast<const int2*>(x8g + 1024)[tig];
+  const int2 ddf = reinterpret_cast<const int2*>(x8g + dd_off)[tig];
   int c[4] = {0, 0, 0, 0};
+  if constexpr (BITS == 4) {
+    const uint4 w0 = *reinterpret_cast<const uint4*>(rec + lane * 16);
+    const uint4 w1 = *reinterpret_cast<const uint4*>(rec + 512 + lane * 16);
+    const uint32_t w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-  for (int s = 0; s < 4; ++s)
-    imma16832(c, w[2 * s] & 0x0F0F0F0Fu, w[2 * s] & 0xF0F0F0F0u, w[2 * s + 1] & 0x0F0F0F0Fu,
-              w[2 * s + 1] & 0xF0F0F0F0u, bb[2 * s], bb[2 * s + 1]);
+    for (int s = 0; s < 4; ++s)
+      imma16832(c, w[2 * s] & 0x0F0F0F0Fu, w[2 * s] & 0xF0F0F0F0u, w[2 * s + 1] & 0x0F0F0F0Fu,
+                w[2 * s + 1] & 0xF0F0F0F0u, bb[2 * s], bb[2 * s + 1]);
+  } else {
+    const uint4 wv = *reinterpret_cast<const uint4*>(rec + lane * 16);
+    const uint32_t w[4] = {wv.x, wv.y, wv.z, wv.w};
+    int c2[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int q = 0; q < 4; q += 2) {
+      imma16832(c, w[q] & 0x03030303u, w[q] & 0x0C0C0C0Cu, w[q + 1] & 0x03030303u, w[q + 1] & 0x0C0C0C0Cu,
+                bb[2 * q], bb[2 * q + 2]);
+      imma16832(c2, w[q] & 0x30303030u, w[q] & 0xC0C0C0C0u, w[q + 1] & 0x30303030u, w[q + 1] & 0xC0C0C0C0u,
+                bb[2 * q + 1], bb[2 * q + 3]);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) c[e] += c2[e] >> 4;    // the x16 fields: exact multiples of 16
+  }
+  constexpr int kHi = 1 << row_hi_shift(BITS);        // row gid + 8 weight: 16 (4-bit), 4 (2-bit)
   const int z0 = (int)((zz.x >> (4 * gid)) & 15u), z8 = (int)((zz.y >> (4 * gid)) & 15u);
   // modular int32 arithmetic: the results fit (|·| < 2^31), intermediates may wrap harmlessly
   const int v0 = (int)((uint32_t)c[0] + 256u * (uint32_t)c[1] - (uint32_t)(z0 * ddf.x));
-  const int v8 = (int)((uint32_t)c[2] + 256u * (uint32_t)c[3] - (uint32_t)(16 * z8 * ddf.x));
+  const int v8 = (int)((uint32_t)c[2] + 256u * (uint32_t)c[3] - (uint32_t)(kHi * z8 * ddf.x));
   const float f = __int_as_float(ddf.y);
-  const float s0 = bf16_bits_to_f32(sw & 0xFFFFu) * f, s1 = bf16_bits_to_f32(sw >> 16) * (f * 0.0625f);
+  const float s0 = bf16_bits_to_f32(sw & 0xFFFFu) * f, s1 = bf16_bits_to_f32(sw >> 16) * (f * (1.f / kHi));
   tot[0][0] = fmaf(s0, (float)v0, tot[0][0]);
   tot[0][2] = fmaf(s1, (float)v8, tot[0][2]);
 }

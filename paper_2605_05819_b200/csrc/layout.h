@@ -33,7 +33,8 @@
 // group scale is divided by the same power of two (exact).
 //   4-bit: word j, fields at bits [0,4) (fp 0, row gid) and [4,8) (fp 4, row gid + 8) of w and
 //          of w >> 8 (k pairs 0 and 1); x' = x;
-//   2-bit: word j/2, fields at bits 2p (fp 2p, p = (i>>1) + 2(j&1)) of w and of w >> 8;
+//   2-bit: word j/2, fields at bits 4(j&1) (fp 4(j&1), row gid) and 4(j&1) + 2 (row gid + 8) of w
+//          and of w >> 8 (k pairs 0 and 1);
 //   3-bit: fields at bits 0-2 and 3-5 (fp 3) of w >> {0, 6, 12}, plus two registers gathered
 //          from bit 15 of the six words.
 #pragma once
@@ -78,8 +79,11 @@ HC_HD constexpr Slot slot(int bits, int j, int i) {
     return Slot{1, fp, {Part{j, 8 * (i >> 1), fp, 4}, Part{0, 0, 0, 0}, Part{0, 0, 0, 0}}};
   }
   if (bits == 2) {
-    const int fp = 2 * (i >> 1) + 4 * (j & 1);
-    return Slot{1, fp, {Part{j / 2, 8 * (i & 1), fp, 2}, Part{0, 0, 0, 0}, Part{0, 0, 0, 0}}};
+    // word j/2; k pair i>>1 <- bytes {0, 2} (shift 0) or {1, 3} (shift 8); field 2·(j&1) + (i&1) of
+    // each byte: row gid in fields 0 / 2, row gid + 8 in fields 1 / 3 (4x higher), so each field
+    // mask (0x03030303 << 2f) of a word is a u8 A-fragment of the int8 path (decode_i8.cuh)
+    const int fp = 4 * (j & 1) + 2 * (i & 1);
+    return Slot{1, fp, {Part{j / 2, 8 * (i >> 1), fp, 2}, Part{0, 0, 0, 0}, Part{0, 0, 0, 0}}};
   }
   // bits == 3: 20 weight-1 slots (18 plain + 2 gathered from bit 15 of each word),
   // 12 weight-8 slots; steps 0..5 pair (w1, w8), steps 6..7 pair (w1, w1).
@@ -98,7 +102,7 @@ HC_HD constexpr Slot slot(int bits, int j, int i) {
 }
 
 // Extra exponent of the row gid + 8 registers over the row gid registers of the same k pair.
-HC_HD constexpr int row_hi_shift(int bits) { return bits == 4 ? 4 : 0; }
+HC_HD constexpr int row_hi_shift(int bits) { return bits == 4 ? 4 : (bits == 2 ? 2 : 0); }
 
 // x pre-scale exponent for the B register of step j: pair 0 (b0, cols 2tig..) or pair 1 (b1).
 HC_HD constexpr int step_fp(int bits, int j, int pair) { return slot(bits, j, 2 * pair).fp; }
