@@ -98,6 +98,17 @@ def c1_bytes(c=C1):
     return base + fac + io
 
 
+def dtype_of(args, config):
+    """The arithmetic the timed path computes in: int8 mma for 2/4-bit decode at
+    B <= 2 (codes x s8 digits of x, exact int32), else fp16 mma on exact dequantised integers."""
+    bits = config.get("bits", 4)
+    if args.workload == "c4":
+        return f"fp16 tcgen05 (s·(q−z) of int{bits}, bf16 X as fp16), fp32 accumulate"
+    if bits in (2, 4) and args.batch <= 2 and os.environ.get("HC_I8", "1") != "0" and args.workload != "c3":
+        return f"int8 mma (u{bits} codes x s8 digits of bf16 x, exact int32), fp32 per-group accumulate"
+    return f"fp16 mma (exact int{bits} dequant x fp16 x), fp32 accumulate"
+
+
 def run_c1_ours(args, rank, world, device):
     import torch
     import paper_2605_05819_b200 as hc
@@ -690,11 +701,11 @@ def main():
     elif args.workload == "c1":
         r = run_c1_ours(args, rank, world, local)
         nbytes = c1_bytes()
-        unit, kernel = "GB/s", "hc::decode_kernel<4,1,true>"
+        unit, kernel = "GB/s", "hc::decode_kernel<4,1,true,true> (int8 mma path)"
     else:
         r = run_c2_ours(args, rank, world, local, args.batch, STACKS[args.workload], tp)
         nbytes = r["bytes"]
-        unit, kernel = "tokens/s", "hc::decode_kernel (4 fused windows per layer)"
+        unit, kernel = "tokens/s", "hc::decode_kernel (4 fused windows per layer; int8 mma path where x8 fits)"
     per_rank = torch.tensor([r["ms"]], dtype=torch.float64, device="cuda")
     if world > 1:
         torch.distributed.all_reduce(per_rank, op=torch.distributed.ReduceOp.MAX)
@@ -723,7 +734,7 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 2), "unit": unit, "n_gpus": world, "steps": r["steps"],
                 "warmup": args.warmup, "ms_per_step": round(ms_max / r["steps"], 6), "higher_is_better": True,
-                "scaling": "strong" if tp else "weak", "vs_baseline": None, "dtype": f"bf16 x int{config.get('bits', 4)} (exact int dequant, fp32 accumulate)",
+                "scaling": "strong" if tp else "weak", "vs_baseline": None, "dtype": dtype_of(args, config),
                 "data": "synthetic (seeded on device, random weights of the named shapes)", "config": config,
                 "roofline": ({"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
                               "frac": round(achieved / hbm, 4), "traffic": traffic_of(args), "peak_source": peak_src,

@@ -125,7 +125,7 @@ def moe_forward(experts: list, ranks: list, x_bits, topk_idx, topk_gate) -> np.n
     """
     x = bf16_to_f64(x_bits)
     T = x.shape[0]
-    d = experts[0]["down"]["N"]
+    d = next(ex for ex in experts if ex is not None)["down"]["N"]   # inactive experts may be None
     y = np.zeros((T, d), dtype=np.float64)
     for e in sorted(set(int(v) for v in np.asarray(topk_idx).reshape(-1))):
         toks, slots = np.nonzero(np.asarray(topk_idx) == e)
