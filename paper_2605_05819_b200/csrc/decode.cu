@@ -85,6 +85,8 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
   constexpr int kBlk = kTPB * kTileMax;
+  // records per bulk-copy block: as many as the block holds (2-bit records are half the size)
+  constexpr int kRPB = (kBlk / rec_bytes(BITS)) < 1 ? 1 : (kBlk / rec_bytes(BITS));
   constexpr int kEpi = kDecodeWarps;          // epilogue warp index
   float* red = reinterpret_cast<float*>(smem + (size_t)kDecodeWarps * kNBuf * kBlk);        // [2][8][32][4·NB8]
   uint4* ubuf = reinterpret_cast<uint4*>(red + 2 * kDecodeWarps * 32 * 4 * NB8);             // [2][kUPre][32]
@@ -398,7 +400,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
       if (p_item < n_items) p_sh = warp_share<BITS>(a, p_item, warp);
     }
     if (p_item >= n_items) return;
-    const int nt = min(kTPB, p_sh.n - p_t);
+    const int nt = min(kRPB, p_sh.n - p_t);
     if (lane == 0) {
       const uint32_t bytes = (uint32_t)(nt * p_sh.tb);
       mbar_expect_tx(&bars[s], bytes);
@@ -502,28 +504,28 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
     for (int nb = 0; nb < NB8; ++nb)
 #pragma unroll
       for (int e = 0; e < 4; ++e) tot[nb][e] = 0.f;
-    for (int t0 = 0; t0 < sh.n; t0 += kTPB) {
+    for (int t0 = 0; t0 < sh.n; t0 += kRPB) {
       const int s = c_slot;
       const uint32_t ph = c_ph;
-      const int nt = min(kTPB, sh.n - t0);
+      const int nt = min(kRPB, sh.n - t0);
       const uint8_t* blk = bufs + s * kBlk;
       while (!mbar_try_wait(&bars[s], ph)) {}
       if constexpr (I8) {
         const uint8_t* x8 = reinterpret_cast<const uint8_t*>(xs);
         const int xg = x8_stride(a.B), dd = 512 * a.B;
         float (&t1)[1][4] = *reinterpret_cast<float(*)[1][4]>(&tot[0][0]);
-        if (nt == kTPB) {
+        if (nt == kRPB) {
 #pragma unroll
-          for (int t = 0; t < kTPB; ++t)
+          for (int t = 0; t < kRPB; ++t)
             i8_tile<BITS>(blk + t * rec_bytes(BITS), lane, x8 + (size_t)(sh.g0 + t0 + t) * xg, dd, t1);
         } else {
           for (int t = 0; t < nt; ++t)
             i8_tile<BITS>(blk + t * rec_bytes(BITS), lane, x8 + (size_t)(sh.g0 + t0 + t) * xg, dd, t1);
         }
-      } else if (nt == kTPB) {
+      } else if (nt == kRPB) {
         // full block: the records are independent straight-line code, so their mma chains interleave
 #pragma unroll
-        for (int t = 0; t < kTPB; ++t) {
+        for (int t = 0; t < kRPB; ++t) {
           const int g = sh.g0 + t0 + t;
           uint32_t xr[NB8][16];
           const uint4* xrs[NB8];
