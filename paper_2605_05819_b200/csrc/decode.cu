@@ -80,7 +80,7 @@ __device__ __forceinline__ void dep_wait(const DArgs& a, int lane) {
 
 // I8: int8 tensor-core path (decode_i8.cuh; BITS = 4, NB8 = 1, B <= 2): x staged as x8 digits
 template <int BITS, int NB8, bool XS, bool I8>
-__global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(const __grid_constant__ DArgs a) {
+__global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const __grid_constant__ DArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
@@ -94,7 +94,8 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
   uint64_t* ubar = bars_all + kDecodeWarps * kNBuf;       // [2]
   uint64_t* xbar = ubar + 2;
   uint64_t* fbar = xbar + 1;                              // t forwarding: Vn blocks landed
-  uint4* tsm = reinterpret_cast<uint4*>(xbar + 2);       // [n_chunks][NB8][32] t hi|lo fragments
+  uint64_t* ebars_all = xbar + 2;                         // [8 warps][kNBuf] ring slot consumed (empty)
+  uint4* tsm = reinterpret_cast<uint4*>(ebars_all + kDecodeWarps * kNBuf);   // [n_chunks][NB8][32] t hi|lo fragments
   uint16_t* xt = reinterpret_cast<uint16_t*>(tsm + (size_t)a.n_chunks * NB8 * 32);   // [16 k][16 cols] fwd x tile
   uint4* fbuf = reinterpret_cast<uint4*>(xt + 256);                                  // [fwd_chunks][32] Vn fragments
   uint16_t* xs = reinterpret_cast<uint16_t*>(fbuf + (size_t)(a.fwd ? a.fwd_chunks : 0) * 32);
@@ -103,8 +104,11 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
   if (lane == 0) {
     if (warp < kDecodeWarps) {
 #pragma unroll
-      for (int s = 0; s < kNBuf; ++s) mbar_init(&bars_all[warp * kNBuf + s], 1);
-    } else {
+      for (int s = 0; s < kNBuf; ++s) {
+        mbar_init(&bars_all[warp * kNBuf + s], 1);
+        mbar_init(&ebars_all[warp * kNBuf + s], 1);
+      }
+    } else if (warp == kDecodeWarps) {
       mbar_init(&ubar[0], 1); mbar_init(&ubar[1], 1); mbar_init(xbar, 1); mbar_init(fbar, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -118,6 +122,56 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
   const int n_vp = a.t_in ? 0 : a.n_chunks * 4 * a.G;   // t_in: t already accumulated by the producer of x
   const int n_vctas = n_vp == 0 ? 0 : min((int)gridDim.x, (n_vp + kDecodeWarps * kVPerWarp - 1) / (kDecodeWarps * kVPerWarp));
   const int n_vwarps = n_vctas * kDecodeWarps;            // v_done target
+
+  if (warp == kDecodeWarps + 1) {
+    // ======================= producer warp =======================
+    // Lane w issues tile warp w's ring: its V pieces, then blocks of up to kRPB consecutive records of
+    // each row-block share (warp_share), each into the next slot once the tile warp released it
+    // (empty mbarrier).  Nothing here reads activations, so it never waits on the producer window:
+    // a window's weight stream starts while the previous window is finishing.
+    if (lane < kDecodeWarps) {
+      const int w = lane;
+      uint8_t* wbufs = smem + (size_t)w * kNBuf * kBlk;
+      uint64_t* wfull = bars_all + w * kNBuf;
+      uint64_t* wempty = ebars_all + w * kNBuf;
+      const uint64_t pol_w = evict_first_policy();
+      const int gw = blockIdx.x * kDecodeWarps + w;
+      const bool v_w = gw < n_vwarps;
+      int vp = v_w ? (int)((long long)gw * n_vp / n_vwarps) : 0;
+      const int vp_end = v_w ? (int)((long long)(gw + 1) * n_vp / n_vwarps) : 0;
+      int p_item = blockIdx.x, p_t = 0;
+      Share sh = p_item < n_items ? warp_share<BITS>(a, p_item, w) : Share{nullptr, 0, 1024, 0, 0, 0};
+      int slot = 0;
+      uint32_t round = 0;
+      while (true) {
+        const uint8_t* src;
+        uint32_t bytes;
+        if (vp < vp_end) {
+          int g, part;
+          src = v_piece(a, vp, g, part);
+          bytes = 1024u;
+          ++vp;
+        } else {
+          while (p_item < n_items && p_t >= sh.n) {
+            p_item += gridDim.x;
+            p_t = 0;
+            if (p_item < n_items) sh = warp_share<BITS>(a, p_item, w);
+          }
+          if (p_item >= n_items) break;
+          const int nt = min(kRPB, sh.n - p_t);
+          src = sh.base + (size_t)p_t * sh.tb;
+          bytes = (uint32_t)(nt * sh.tb);
+          p_t += nt;
+        }
+        if (round > 0)
+          while (!mbar_try_wait(&wempty[slot], (round - 1) & 1u)) {}
+        mbar_expect_tx(&wfull[slot], bytes);
+        bulk_copy(wbufs + slot * kBlk, src, bytes, &wfull[slot], pol_w);
+        if (++slot == kNBuf) { slot = 0; ++round; }
+      }
+    }
+    return;
+  }
 
   if (warp == kEpi) {
     // ======================= epilogue warp =======================
@@ -367,50 +421,14 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
   }
 
   // ======================= tile warps =======================
-  uint8_t* bufs = smem + (size_t)warp * kNBuf * kBlk;    // [kNBuf][kBlk]
+  uint8_t* bufs = smem + (size_t)warp * kNBuf * kBlk;    // [kNBuf][kBlk], filled by the producer warp
   uint64_t* bars = bars_all + warp * kNBuf;
-  const uint64_t pol_w = evict_first_policy();
+  uint64_t* ebars = ebars_all + warp * kNBuf;
   // this warp's share of the window's V pieces (rank projection)
   const int gw = blockIdx.x * kDecodeWarps + warp;
   const bool v_warp = gw < n_vwarps;
   const int vp0 = v_warp ? (int)((long long)gw * n_vp / n_vwarps) : 0;
   const int vp1 = v_warp ? (int)((long long)(gw + 1) * n_vp / n_vwarps) : 0;
-  // producer: first the V pieces (one per slot), then blocks of up to kTPB consecutive tiles of each
-  // row-block share; double-buffered per warp.  State is warp-uniform; lane 0 issues.
-  int vp_issue = vp0;
-  int p_item = blockIdx.x, p_t = 0;
-  Share p_sh = p_item < n_items ? warp_share<BITS>(a, p_item, warp) : Share{nullptr, 0, 1024, 0, 0, 0};
-  int p_slot = 0;               // ring slot of the next block issued (no div/mod on the hot path)
-  auto issue_block = [&]() {   // issue the next block (a V piece or up to kTPB weight tiles), if any
-    const int s = p_slot;
-    if (vp_issue < vp1) {
-      int g, part;
-      const uint8_t* src = v_piece(a, vp_issue, g, part);
-      if (lane == 0) {
-        mbar_expect_tx(&bars[s], 1024u);
-        bulk_copy(bufs + s * kBlk, src, 1024u, &bars[s], pol_w);
-      }
-      ++vp_issue;
-      p_slot = p_slot + 1 == kNBuf ? 0 : p_slot + 1;
-      return;
-    }
-    while (p_item < n_items && p_t >= p_sh.n) {
-      p_item += gridDim.x;
-      p_t = 0;
-      if (p_item < n_items) p_sh = warp_share<BITS>(a, p_item, warp);
-    }
-    if (p_item >= n_items) return;
-    const int nt = min(kRPB, p_sh.n - p_t);
-    if (lane == 0) {
-      const uint32_t bytes = (uint32_t)(nt * p_sh.tb);
-      mbar_expect_tx(&bars[s], bytes);
-      bulk_copy(bufs + s * kBlk, p_sh.base + (size_t)p_t * p_sh.tb, bytes, &bars[s], pol_w);
-    }
-    p_t += nt;
-    p_slot = p_slot + 1 == kNBuf ? 0 : p_slot + 1;
-  };
-#pragma unroll
-  for (int s = 0; s < kNBuf; ++s) issue_block();   // weights / V: before the PDL wait
   // tile warps read activations only through the x staged by the epilogue warp (XS, ordered by its
   // acquire and the x mbarrier), except for V pieces and unstaged x: only then do they wait themselves
   if (!a.dep_cnt) dep_wait(a, lane);
@@ -422,7 +440,11 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
 
   int c_slot = 0;          // consumer ring position: slot and mbarrier phase
   uint32_t c_ph = 0;
-  auto advance = [&]() { if (++c_slot == kNBuf) { c_slot = 0; c_ph ^= 1u; } };
+  // release the consumed slot to the producer warp (the __syncwarp before it orders every lane's reads)
+  auto advance = [&]() {
+    if (lane == 0) mbar_arrive(&ebars[c_slot]);
+    if (++c_slot == kNBuf) { c_slot = 0; c_ph ^= 1u; }
+  };
   // ---- rank projection share: t[cc][col][rank] += V pieces · x   (64-bit fixed point, exact adds).
   // Runs before the x' staging below (it reads bf16 x from L2): t is on the critical path of every
   // epilogue.  Partials of consecutive pieces of one chunk are summed in registers before the atomics.
@@ -466,7 +488,6 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
       v_tile<NB8>(bufs + s * kBlk, lane, xv, tp);
       __syncwarp();
       advance();
-      issue_block();
     }
     if (cc_cur >= 0) flush(cc_cur);
   }
@@ -547,7 +568,6 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
       }
       __syncwarp();
       advance();
-      issue_block();
     }
     if constexpr (I8) i8_finish(*reinterpret_cast<float(*)[1][4]>(&tot[0][0]), lane, a.B);
     // ---- hand the partial sums to the epilogue warp
@@ -563,7 +583,7 @@ __global__ void __launch_bounds__(kDecodeThreads, HC_DEC_MINB) decode_kernel(con
 static size_t decode_smem_bytes(bool xs, bool i8, int B, int K, int n_chunks, int fwd_chunks) {
   const int nb8 = B > 8 ? 2 : 1;
   size_t s = (size_t)kDecodeWarps * kNBuf * kTPB * kTileMax + 2 * kDecodeWarps * 32 * 4 * nb8 * sizeof(float) +
-             2 * kUPre * 32 * 16 + (kDecodeWarps * kNBuf + 4) * sizeof(uint64_t) +
+             2 * kUPre * 32 * 16 + (2 * kDecodeWarps * kNBuf + 4) * sizeof(uint64_t) +
              (size_t)n_chunks * nb8 * 32 * 16 + 512 + (size_t)fwd_chunks * 512;
   if (i8) s += (size_t)(K / kGroup) * x8_stride(B) + kX8Pad;
   else if (xs) s += (size_t)B * (K + 32) * 2;
@@ -634,7 +654,7 @@ static cudaError_t launch_t(const DArgs& a, int grid, cudaStream_t st) {
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kDecodeThreads);
+  cfg.blockDim = dim3(kDecodeBlock);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
@@ -651,7 +671,7 @@ static int max_ctas_t(int B, int K, int n_chunks, int fwd_chunks) {
   cudaFuncSetAttribute(decode_kernel<BITS, NB8, XS, I8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)kSmemOptin);
   int per_sm = 0, dev = 0, sms = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<BITS, NB8, XS, I8>, kDecodeThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<BITS, NB8, XS, I8>, kDecodeBlock, smem);
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   return per_sm * sms;

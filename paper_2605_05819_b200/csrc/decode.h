@@ -7,7 +7,8 @@ namespace hc {
 
 constexpr int kMaxMembers = 4;
 constexpr int kDecodeWarps = 8;          // tile (streaming + contraction) warps per CTA
-constexpr int kDecodeThreads = (kDecodeWarps + 1) * 32;   // + one epilogue warp
+constexpr int kDecodeThreads = (kDecodeWarps + 1) * 32;   // + one epilogue warp (named-barrier count)
+constexpr int kDecodeBlock = kDecodeThreads + 32;         // decode kernel: + one producer (TMA issue) warp
 constexpr int kMaxChunks = 32;           // Σ ceil(r_m/16) over a window's members
 #ifndef HC_DEC_TPB
 #define HC_DEC_TPB 2
