@@ -834,7 +834,8 @@ extern "C" hc_status hc_moe_forward(hc_ctx* ctx, int32_t layer, const void* x, i
   hc_ctx::MoECache* c = nullptr;
   hc_status s = moe_tables(ctx, layer, c);
   if (s != HC_OK) return s;
-  const int R = T * topk, maxe = c->E + R;
+  // entries = Σ_e ceil(n_e / 16) <= min(E, R) + R / 16 (moe_route: chunks of <= 16 rows per expert)
+  const int R = T * topk, maxe = std::min(c->E, R) + (R + 15) / 16;
   // workspace carve (256-byte aligned pieces)
   size_t off = 0;
   auto take = [&](size_t bytes) { const size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };

@@ -192,13 +192,20 @@ __global__ void __launch_bounds__(256) moe_rank_proj_kernel(MoEWin w, MoERoute r
 
 // One warp per (entry, row block) over all K: no cross-warp reduction, no CTA barrier; the next
 // record's words are loaded while the current one is decoded (many warps per SM hide the rest).
-template <int BITS, int NB8>
+// KS: the item's K groups are split over the CTA's 4 warps (few items: routing of a handful of
+// tokens); else every warp owns whole items (many items).
+template <int BITS, int NB8, bool KS>
 __global__ void __launch_bounds__(128) moe_gemv_warp_kernel(MoEWin w, MoERoute rt, const uint16_t* __restrict__ x16,
                                                            const float* __restrict__ t, void* out) {
+  // one (entry, row block) item per CTA; its K groups split over the 4 warps (each warp keeps one
+  // record in flight ahead of the one it decodes), partials summed in a fixed order by warp 0
+  __shared__ float red[KS ? 4 : 1][32][4 * NB8];
+  const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
   const long long n_items = (long long)(*rt.n_ent) * w.n_rb;
-  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long it = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < n_items; it += warps) {
+  const long long it0 = KS ? (long long)blockIdx.x : (long long)blockIdx.x * 4 + warp;
+  const long long its = KS ? (long long)gridDim.x : (long long)gridDim.x * 4;
+  for (long long it = it0; it < n_items; it += its) {
     const int ent = (int)(it / w.n_rb), rb = (int)(it % w.n_rb);
     const MoEExpert& ex = w.ex[rt.ent_e[ent]];
     const int row0 = rt.ent_row0[ent], ncol = rt.ent_ncol[ent];
@@ -214,16 +221,17 @@ __global__ void __launch_bounds__(128) moe_gemv_warp_kernel(MoEWin w, MoERoute r
       const int col = gid + 8 * nb;
       xrow[nb] = x16 + (size_t)(row0 + (col < ncol ? col : 0)) * w.K + 8 * tig;
     }
+    const int g_lo = KS ? warp * w.G / 4 : 0, g_hi = KS ? (warp + 1) * w.G / 4 : w.G;
     uint32_t wn[2 * BITS], swn;
     uint2 zzn;
-    load_record<BITS>(rec0, lane, wn, swn, zzn);
-    for (int g = 0; g < w.G; ++g) {
+    if (g_lo < g_hi) load_record<BITS>(rec0 + (size_t)g_lo * rec_bytes(BITS), lane, wn, swn, zzn);
+    for (int g = g_lo; g < g_hi; ++g) {
       uint32_t wc[2 * BITS];
 #pragma unroll
       for (int i = 0; i < 2 * BITS; ++i) wc[i] = wn[i];
       const uint32_t swc = swn;
       const uint2 zzc = zzn;
-      if (g + 1 < w.G) load_record<BITS>(rec0 + (size_t)(g + 1) * rec_bytes(BITS), lane, wn, swn, zzn);
+      if (g + 1 < g_hi) load_record<BITS>(rec0 + (size_t)(g + 1) * rec_bytes(BITS), lane, wn, swn, zzn);
       uint32_t xr[NB8][16];
 #pragma unroll
       for (int nb = 0; nb < NB8; ++nb) {
@@ -236,6 +244,25 @@ __global__ void __launch_bounds__(128) moe_gemv_warp_kernel(MoEWin w, MoERoute r
       }
       const uint4* unused[NB8] = {};
       w_tile_regs<BITS, NB8, false>(wc, swc, zzc, lane, unused, xr, tot);
+    }
+    if constexpr (KS) {
+#pragma unroll
+      for (int nb = 0; nb < NB8; ++nb)
+        *reinterpret_cast<float4*>(&red[warp][lane][4 * nb]) = make_float4(tot[nb][0], tot[nb][1], tot[nb][2], tot[nb][3]);
+      __syncthreads();
+      if (warp != 0) {
+        __syncthreads();                               // red is reused by the next item
+        continue;
+      }
+#pragma unroll
+      for (int nb = 0; nb < NB8; ++nb)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float v = red[0][lane][4 * nb + e];
+#pragma unroll
+          for (int q = 1; q < 4; ++q) v += red[q][lane][4 * nb + e];   // fixed order: deterministic
+          tot[nb][e] = v;
+        }
     }
     // U·t (plain: member 0 on all 16 rows; SiLU window: up chunks on rows 0-7 with t of member 0,
     // gate chunks on rows 8-15 with t of member 1), then the glue and the output
@@ -301,6 +328,7 @@ __global__ void __launch_bounds__(128) moe_gemv_warp_kernel(MoEWin w, MoERoute r
           o[(size_t)(row0 + col) * ldo + rb * kRows + gid + 8 * (e >> 1)] = tot[nb][e] + comp[0][nb][e];
         }
     }
+    if constexpr (KS) __syncthreads();                 // pairs with the other warps' wait above
   }
 }
 
@@ -356,13 +384,20 @@ cudaError_t moe_gemv(const MoEWin& w, int bits, const MoERoute& rt, int max_ent,
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long items = (long long)max_ent * w.n_rb;           // warps needed at most
-  const long long blocks = (items + 3) / 4;
-  const unsigned grid = (unsigned)(blocks < 16LL * sms ? blocks : 16LL * sms);
+  const long long items = (long long)max_ent * w.n_rb;           // at most
+  // few items (a handful of routed tokens): one item per CTA with K split over its 4 warps
+  const bool ks = items <= 8LL * sms;
+  const long long need = ks ? items : (items + 3) / 4;
+  const unsigned grid = (unsigned)(need < 16LL * sms ? need : 16LL * sms);
   const bool one = max_cols <= 8;                                  // NB8 = 1: at most 8 rows per entry
 #define HC_MOE_LAUNCH(B_)                                                                                       \
-  if (one) moe_gemv_warp_kernel<B_, 1><<<grid, 128, 0, st>>>(w, rt, x16, t, out);                               \
-  else     moe_gemv_warp_kernel<B_, 2><<<grid, 128, 0, st>>>(w, rt, x16, t, out);
+  if (ks) {                                                                                                     \
+    if (one) moe_gemv_warp_kernel<B_, 1, true><<<grid, 128, 0, st>>>(w, rt, x16, t, out);                       \
+    else     moe_gemv_warp_kernel<B_, 2, true><<<grid, 128, 0, st>>>(w, rt, x16, t, out);                       \
+  } else {                                                                                                      \
+    if (one) moe_gemv_warp_kernel<B_, 1, false><<<grid, 128, 0, st>>>(w, rt, x16, t, out);                      \
+    else     moe_gemv_warp_kernel<B_, 2, false><<<grid, 128, 0, st>>>(w, rt, x16, t, out);                      \
+  }
   switch (bits) {
     case 2: HC_MOE_LAUNCH(2) break;
     case 3: HC_MOE_LAUNCH(3) break;
