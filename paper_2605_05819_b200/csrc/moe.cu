@@ -43,6 +43,8 @@ __device__ __forceinline__ int dyn_rank(float rt, int cap, int k0) {
 
 __global__ void moe_route_kernel(const int32_t* __restrict__ idx, const float* __restrict__ gate, int T, int k, int E,
                                  MoERoute rt, MoEDyn dyn) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");                 // PDL: the previous launch's outputs
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ unsigned bm[];                 // [E][W] token bitmaps, W = ceil(T/32)
   __shared__ int cnt[256], ecnt[256], off[257], eoff[257];
   const int W = (T + 31) / 32;
@@ -107,6 +109,8 @@ __global__ void moe_route_kernel(const int32_t* __restrict__ idx, const float* _
 template <int BITS>
 __global__ void moe_prep_kernel(const uint16_t* __restrict__ x, int ldx, int K, int gather, MoERoute rt, int R_max,
                                 uint16_t* __restrict__ xg, uint16_t* __restrict__ x16) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");                 // PDL: the previous launch's outputs
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int parts = K / 16;
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (long long)R_max * parts) return;
@@ -129,6 +133,8 @@ __global__ void moe_prep_kernel(const uint16_t* __restrict__ x, int ldx, int K, 
 // (4 in flight, independent loads), partials summed in a fixed order through shared memory
 __global__ void __launch_bounds__(256) moe_rank_proj_kernel(MoEWin w, MoERoute rt, int max_ent, int max_chunks,
                                                             const uint16_t* __restrict__ xg, float* __restrict__ t) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");                 // PDL: the previous launch's outputs
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __shared__ float part[8][32][8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
   const int job = blockIdx.x, per_ent = 2 * max_chunks;
@@ -197,6 +203,8 @@ __global__ void __launch_bounds__(256) moe_rank_proj_kernel(MoEWin w, MoERoute r
 template <int BITS, int NB8, bool KS>
 __global__ void __launch_bounds__(128) moe_gemv_warp_kernel(MoEWin w, MoERoute rt, const uint16_t* __restrict__ x16,
                                                            const float* __restrict__ t, void* out) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");                 // PDL: the previous launch's outputs
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // one (entry, row block) item per CTA; its K groups split over the 4 warps (each warp keeps one
   // record in flight ahead of the one it decodes), partials summed in a fixed order by warp 0
   __shared__ float red[KS ? 4 : 1][32][4 * NB8];
@@ -334,6 +342,8 @@ __global__ void __launch_bounds__(128) moe_gemv_warp_kernel(MoEWin w, MoERoute r
 
 __global__ void moe_combine_kernel(const float* __restrict__ dout, int N, const float* __restrict__ gate, int T, int k,
                                    MoERoute rt, float* __restrict__ y) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");                 // PDL: the previous launch's outputs
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (long long)T * N) return;
   const int tk = (int)(i / N), n = (int)(i % N);
@@ -347,13 +357,31 @@ __global__ void moe_combine_kernel(const float* __restrict__ dout, int N, const 
 
 }  // namespace
 
+// Programmatic dependent launch: every MoE kernel waits on the previous launch (griddepcontrol.wait)
+// before reading its outputs, so only the launch latency and prologue overlap.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 cudaError_t moe_route(const int32_t* topk_idx, const float* topk_gate, int T, int k, int E, const MoERoute& rt,
                       const MoEDyn* dyn, cudaStream_t st) {
   if (T < 1 || T > 1024 || k < 1 || k > kMoEMaxK || E < 1 || E > 256) return cudaErrorInvalidValue;
   const size_t smem = (size_t)E * ((T + 31) / 32) * sizeof(unsigned);
   MoEDyn d{};
   if (dyn) d = *dyn;
-  moe_route_kernel<<<1, kRouteThreads, smem, st>>>(topk_idx, topk_gate, T, k, E, rt, d);
+  if (cudaError_t e = launch_pdl(moe_route_kernel, 1, kRouteThreads, smem, st, topk_idx, topk_gate, T, k, E, rt, d)) return e;
   return cudaGetLastError();
 }
 
@@ -362,9 +390,9 @@ cudaError_t moe_prep(const uint16_t* x, int ldx, int K, int bits, int gather, co
   const long long n = (long long)R_max * (K / 16);
   const unsigned grid = (unsigned)((n + 255) / 256);
   switch (bits) {
-    case 2: moe_prep_kernel<2><<<grid, 256, 0, st>>>(x, ldx, K, gather, rt, R_max, xg, x16); break;
-    case 3: moe_prep_kernel<3><<<grid, 256, 0, st>>>(x, ldx, K, gather, rt, R_max, xg, x16); break;
-    case 4: moe_prep_kernel<4><<<grid, 256, 0, st>>>(x, ldx, K, gather, rt, R_max, xg, x16); break;
+    case 2: if (cudaError_t e = launch_pdl(moe_prep_kernel<2>, grid, 256, 0, st, x, ldx, K, gather, rt, R_max, xg, x16)) return e; break;
+    case 3: if (cudaError_t e = launch_pdl(moe_prep_kernel<3>, grid, 256, 0, st, x, ldx, K, gather, rt, R_max, xg, x16)) return e; break;
+    case 4: if (cudaError_t e = launch_pdl(moe_prep_kernel<4>, grid, 256, 0, st, x, ldx, K, gather, rt, R_max, xg, x16)) return e; break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -375,7 +403,7 @@ cudaError_t moe_rank_proj(const MoEWin& w, const MoERoute& rt, int max_ent, cons
   const int max_chunks = w.t_ld / 32;
   const long long jobs = (long long)max_ent * 2 * max_chunks;
   if (jobs == 0) return cudaSuccess;
-  moe_rank_proj_kernel<<<(unsigned)jobs, 256, 0, st>>>(w, rt, max_ent, max_chunks, xg, t);
+  if (cudaError_t e = launch_pdl(moe_rank_proj_kernel, (unsigned)jobs, 256, 0, st, w, rt, max_ent, max_chunks, xg, t)) return e;
   return cudaGetLastError();
 }
 
@@ -390,13 +418,14 @@ cudaError_t moe_gemv(const MoEWin& w, int bits, const MoERoute& rt, int max_ent,
   const long long need = ks ? items : (items + 3) / 4;
   const unsigned grid = (unsigned)(need < 16LL * sms ? need : 16LL * sms);
   const bool one = max_cols <= 8;                                  // NB8 = 1: at most 8 rows per entry
+  cudaError_t e = cudaSuccess;
 #define HC_MOE_LAUNCH(B_)                                                                                       \
   if (ks) {                                                                                                     \
-    if (one) moe_gemv_warp_kernel<B_, 1, true><<<grid, 128, 0, st>>>(w, rt, x16, t, out);                       \
-    else     moe_gemv_warp_kernel<B_, 2, true><<<grid, 128, 0, st>>>(w, rt, x16, t, out);                       \
+    if (one) e = launch_pdl(moe_gemv_warp_kernel<B_, 1, true>, grid, 128, 0, st, w, rt, x16, t, out);                       \
+    else     e = launch_pdl(moe_gemv_warp_kernel<B_, 2, true>, grid, 128, 0, st, w, rt, x16, t, out);                       \
   } else {                                                                                                      \
-    if (one) moe_gemv_warp_kernel<B_, 1, false><<<grid, 128, 0, st>>>(w, rt, x16, t, out);                      \
-    else     moe_gemv_warp_kernel<B_, 2, false><<<grid, 128, 0, st>>>(w, rt, x16, t, out);                      \
+    if (one) e = launch_pdl(moe_gemv_warp_kernel<B_, 1, false>, grid, 128, 0, st, w, rt, x16, t, out);                      \
+    else     e = launch_pdl(moe_gemv_warp_kernel<B_, 2, false>, grid, 128, 0, st, w, rt, x16, t, out);                      \
   }
   switch (bits) {
     case 2: HC_MOE_LAUNCH(2) break;
@@ -405,13 +434,13 @@ cudaError_t moe_gemv(const MoEWin& w, int bits, const MoERoute& rt, int max_ent,
     default: return cudaErrorInvalidValue;
   }
 #undef HC_MOE_LAUNCH
-  return cudaGetLastError();
+  return e;
 }
 
 cudaError_t moe_combine(const float* dout, int N, const float* topk_gate, int T, int k, const MoERoute& rt,
                         float* y, cudaStream_t st) {
   const long long n = (long long)T * N;
-  moe_combine_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(dout, N, topk_gate, T, k, rt, y);
+  if (cudaError_t e = launch_pdl(moe_combine_kernel, (unsigned)((n + 255) / 256), 256, 0, st, dout, N, topk_gate, T, k, rt, y)) return e;
   return cudaGetLastError();
 }
 
