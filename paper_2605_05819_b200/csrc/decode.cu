@@ -36,6 +36,9 @@
 
 namespace hc {
 
+#ifndef HC_DEP_SLEEP
+#define HC_DEP_SLEEP 64   // ns between polls of the producer window's counter
+#endif
 #ifndef HC_DEC_TRACE
 #define HC_DEC_TRACE 0
 #endif
@@ -68,7 +71,7 @@ cudaError_t decode_set_trace(void* buf) { return cudaMemcpyToSymbol(g_dtrace, &b
 __device__ __forceinline__ void dep_wait(const DArgs& a, int lane) {
   if (a.dep_cnt) {
     if (lane == 0) {
-      while (ld_relaxed(a.dep_cnt) < a.dep_target) __nanosleep(64);
+      while (ld_relaxed(a.dep_cnt) < a.dep_target) __nanosleep(HC_DEP_SLEEP);
       (void)ld_acquire(a.dep_cnt);
       asm volatile("fence.proxy.async.global;" ::: "memory");   // generic writes -> async-proxy (TMA) reads
     }
