@@ -63,7 +63,9 @@ __device__ __forceinline__ void x8_stage(const DArgs& a, uint8_t* x8, int g0, in
 #pragma unroll
     for (int i = 0; i < 4; ++i) m = max(m, hb[i] & 0x7FFFu);
     m = __reduce_max_sync(0xFFFFFFFFu, m);
-    const int e = m == 0 ? 0 : max((int)(m >> 7), 1) - 127;   // exponent of the group's largest |x|
+    // exponent of the group's largest |x|, clamped so that 2^(16p + e − 29) stays a normal float
+    // (groups below 2^-97 keep 29 bits of fixed point relative to 2^-97)
+    const int e = m == 0 ? 0 : max(max((int)(m >> 7), 1) - 127, -97);
     const int sh = 29 - e, sh1 = sh >> 1;
     const float p1 = pow2f(sh1), p2 = pow2f(sh - sh1);     // 2^(29 − e) in two exact steps
     uint32_t u[4];

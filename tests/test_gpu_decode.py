@@ -148,3 +148,35 @@ def test_errors(hc, ctx):
     with pytest.raises(hc.HCError) as ei:
         ctx.compensated_linear(12345, 0, dev(case["x"]), torch.empty(1, 128, device="cuda"))
     assert ei.value.code == hc.HC_ERR_STATE
+
+
+def _wide_range_x(seed, B, K):
+    """bf16 x spanning ~12 decades within each group, one all-zero group, one group of values near
+    the bf16 normal minimum, one group with a single large outlier (int8 path edge cases)."""
+    g = np.random.default_rng(seed)
+    x = g.standard_normal((B, K)) * 10.0 ** g.uniform(-9, 3, (B, K))
+    x[:, 128:256] = 0.0                                    # all-zero group
+    if K >= 512:
+        x[:, 256:384] = g.standard_normal((B, 128)) * 1e-37   # tiny group (exponent clamp)
+        x[:, 384:512] = g.standard_normal((B, 128)) * 1e-3
+        x[:, 400] = 3.0e4                                  # outlier: the rest sits 2^24 below it
+    return f64_to_bf16_bits_rne(x)
+
+
+@pytest.mark.parametrize("bits,zeros", [(4, "asym"), (4, "sym"), (2, "asym")])
+@pytest.mark.parametrize("B", [1, 2])
+@pytest.mark.parametrize("K", [640, 1408])
+def test_int8_path_edge_cases(hc, ctx, bits, zeros, B, K):
+    """The int8 mma path (4-/2-bit, B <= 2, x staged): x in per-group block fixed
+    point.  Wide-range, zero, tiny and outlier groups; K = 640 leaves three of the eight warps without
+    groups; every result within 1e-5 of the float64 oracle (relative to max|y*|) and deterministic."""
+    case = synth.linear_case(700 + 10 * bits + B, N=272, K=K, bits=bits, r_stored=32, B=B, zeros=zeros)
+    case["x"] = _wide_range_x(K + B, B, K)
+    L = next_layer()
+    for r in (0, 16):
+        load(ctx, case, L, r=r)
+        y = run(hc, ctx, L, case["x"], 272)
+        ref = linear.compensated_linear(case, r)
+        assert np.all(np.isfinite(y))
+        assert rel_err(y, ref) <= 1e-5, (r, rel_err(y, ref))
+        assert np.array_equal(y, run(hc, ctx, L, case["x"], 272))
