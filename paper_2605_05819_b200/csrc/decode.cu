@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
 #pragma unroll
       for (int s = 0; s < kNBuf; ++s) {
         mbar_init(&bars_all[warp * kNBuf + s], 1);
-        mbar_init(&ebars_all[warp * kNBuf + s], 1);
+        mbar_init(&ebars_all[warp * kNBuf + s], 32);
       }
     } else if (warp == kDecodeWarps) {
       mbar_init(&ubar[0], 1); mbar_init(&ubar[1], 1); mbar_init(xbar, 1); mbar_init(fbar, 1);
@@ -443,9 +443,10 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
 
   int c_slot = 0;          // consumer ring position: slot and mbarrier phase
   uint32_t c_ph = 0;
-  // release the consumed slot to the producer warp (the __syncwarp before it orders every lane's reads)
+  // release the consumed slot to the producer warp: every lane arrives after its own reads (the empty
+  // barrier counts 32), so no warp-wide sync is needed
   auto advance = [&]() {
-    if (lane == 0) mbar_arrive(&ebars[c_slot]);
+    mbar_arrive(&ebars[c_slot]);
     if (++c_slot == kNBuf) { c_slot = 0; c_ph ^= 1u; }
   };
   // ---- rank projection share: t[cc][col][rank] += V pieces · x   (64-bit fixed point, exact adds).
@@ -489,7 +490,6 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
       }
       while (!mbar_try_wait(&bars[s], ph)) {}
       v_tile<NB8>(bufs + s * kBlk, lane, xv, tp);
-      __syncwarp();
       advance();
     }
     if (cc_cur >= 0) flush(cc_cur);
@@ -569,7 +569,6 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
           w_tile<BITS, NB8, XS>(blk + t * rec_bytes(BITS), lane, xrs, xr, tot);
         }
       }
-      __syncwarp();
       advance();
     }
     if constexpr (I8) i8_finish(*reinterpret_cast<float(*)[1][4]>(&tot[0][0]), lane, a.B);
