@@ -180,7 +180,10 @@ __device__ __forceinline__ const uint8_t* v_piece(const DArgs& a, int vp, int& g
   return reinterpret_cast<const uint8_t*>(m.V + ((size_t)(cc - m.chunk_begin) * a.G * 256 + (size_t)rem * 64));
 }
 
-constexpr int kVPerWarp = 2;                    // V·x pieces per tile warp of the V CTAs
+#ifndef HC_VPW
+#define HC_VPW 1
+#endif
+constexpr int kVPerWarp = HC_VPW;                    // V·x pieces per tile warp of the V CTAs
 constexpr float kTScale = 268435456.f;          // 2^28: fixed-point scale of the t accumulators
 constexpr float kTInv = 1.f / 268435456.f;
 
