@@ -184,12 +184,19 @@ hc_status hc_moe_forward(hc_ctx* ctx, int32_t layer, const void* x, int32_t T, c
  * the expert activation score G = k·g_e scales the continuous rank): for a routed (token, slot) pair
  * with expert e and gate g, matrix s in (up, gate, down) uses
  *   r = Cap(Align((k·g)·rtilde[3e + s]))   (Align: nearest of {0} ∪ {2^j, j >= k0}, ties up; Cap: the
- *                                            largest level <= the matrix's loaded r_alloc; fp32 product)
+ *                                            largest level <= the matrix's loaded r_alloc; the product is
+ *                                            taken in float64, where it is exact for fp32 g and r̃)
  * instead of its static r_alloc (which stays the upper bound: U / V reads are sized by it).
  * rtilde: host float [n_experts][3] (>= 0, finite), copied; NULL switches back to the static ranks.
  * n_experts must match the layer's experts at the next hc_moe_forward (HC_ERR_CONFIG otherwise).
  * HC_ERR_NUMERIC for a negative or non-finite r̃. */
 hc_status hc_moe_set_dynamic_ranks(hc_ctx* ctx, int32_t layer, const float* rtilde, int32_t n_experts, int32_t k0);
+
+/* The per-(token, slot) ranks the device decided in the most recent hc_moe_forward that ran with dynamic
+ * ranks (test / inspection export; synchronises the device).  out: host int32 [T][topk][3] = the ranks
+ * used for (up, gate, down) of token t's slot j, or -1 for a slot whose expert id was skipped.  T and topk
+ * must equal the last call's.  HC_ERR_STATE if that call used static ranks. */
+hc_status hc_moe_last_ranks(hc_ctx* ctx, int32_t* out, int32_t T, int32_t topk);
 
 /* Column sharding across GPUs.  Rank 0 calls hc_nccl_unique_id and shares the 128
  * bytes with every rank (e.g. through torch.distributed); each rank then calls hc_set_comm with its

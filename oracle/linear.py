@@ -87,8 +87,11 @@ def round_bf16(a: np.ndarray) -> np.ndarray:
 
 
 def silu(v: np.ndarray) -> np.ndarray:
+    """SiLU(v) = v·σ(v) = v / (1 + e^-v) (σ = SiLU as SPEC); e^-v overflowing to inf for very
+    negative v gives the correct limit -0."""
     v = np.asarray(v, dtype=np.float64)
-    return v / (1.0 + np.exp(-v))
+    with np.errstate(over="ignore"):
+        return v / (1.0 + np.exp(-v))
 
 
 def stack_forward(layers: list, ranks: list, x_bits) -> np.ndarray:
@@ -142,10 +145,12 @@ def moe_forward(experts: list, ranks: list, x_bits, topk_idx, topk_gate) -> np.n
 def dynamic_rank(k: int, g, rtilde, cap: int, k0: int = 3) -> int:
     """Per-(token, expert) rank of one matrix ("G_{i,e} = k·g_e"):
     r̃_{i,e} = G_{i,e}·r̃_i with G = k·g_e, then Align (ties up R14) and the cap rule (R15).
-    The product that decides the integer is taken in fp32 — (k·g)·r̃ — the precision of the kernel
-    (task rule: both sides decide in the same precision); the Align comparisons are exact for it."""
-    rt = np.float32(np.float32(k) * np.float32(g)) * np.float32(rtilde)
-    return cap_level(align(float(rt), k0), int(cap), k0)
+
+    g (the routing weight) and r̃ arrive as fp32 values (the C-ABI's types) and are upcast exactly; the
+    product (k·g)·r̃ is then taken in float64, where it is EXACT (k <= 16 has <= 5 significant bits, g and
+    r̃ 24 each: <= 53 bits), so the integer decision is the exact-arithmetic one (R21)."""
+    rt = (float(k) * float(np.float32(g))) * float(np.float32(rtilde))
+    return cap_level(align(rt, k0), int(cap), k0)
 
 
 def moe_forward_dynamic(experts: list, caps: list, x_bits, topk_idx, topk_gate, rtilde: list, k0: int = 3):

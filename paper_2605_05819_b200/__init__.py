@@ -43,6 +43,28 @@ def _ptr(a):
     raise TypeError(type(a))
 
 
+def _itemsize(a) -> int:
+    return a.itemsize if isinstance(a, np.ndarray) else a.element_size()
+
+
+def _check_buf(name, a, n_elems, sizes, what):
+    """Argument check before a raw pointer crosses the ABI: element size in `sizes` and at least n_elems
+    elements (the C side trusts both)."""
+    if _itemsize(a) not in sizes:
+        raise TypeError(f"{name}: expected {what} (element size {sizes}), got element size {_itemsize(a)}")
+    n = a.size if isinstance(a, np.ndarray) else a.numel()
+    if n < n_elems:
+        raise ValueError(f"{name}: {n} elements < the {n_elems} the call reads / writes")
+
+
+def _is_int32(a) -> bool:
+    return (a.dtype == np.int32) if isinstance(a, np.ndarray) else str(a.dtype) == "torch.int32"
+
+
+def _is_f32(a) -> bool:
+    return (a.dtype == np.float32) if isinstance(a, np.ndarray) else str(a.dtype) == "torch.float32"
+
+
 def _stream(stream):
     if stream is None:
         try:
@@ -177,6 +199,9 @@ class Context:
         """hc_stack_forward: one decode step through all loaded layers (bf16 in, bf16 out)."""
         if B is None:
             B = x.shape[0]
+        d = int(x.shape[-1])
+        _check_buf("x", x, B * d, (2,), "bf16 [B, hidden]")
+        _check_buf("y", y, B * d, (2,), "bf16 [B, hidden]")
         check(lib().hc_stack_forward(self._h, _ptr(x), int(B), _ptr(y), _stream(stream)))
         return y
 
@@ -184,6 +209,13 @@ class Context:
         """hc_moe_forward: grouped MoE expert layer.  x bf16 [T, K]; topk_idx int32 [T, k];
         topk_gate fp32 [T, k]; y fp32 [T, D] (device tensors or host arrays)."""
         T, k = int(topk_idx.shape[0]), int(topk_idx.shape[1])
+        if not _is_int32(topk_idx):
+            raise TypeError(f"topk_idx must be int32 (got {topk_idx.dtype}; e.g. torch.topk returns int64)")
+        if not _is_f32(topk_gate):
+            raise TypeError(f"topk_gate must be float32 (got {topk_gate.dtype})")
+        _check_buf("topk_gate", topk_gate, T * k, (4,), "fp32 [T, k]")
+        _check_buf("x", x, T * int(x.shape[-1]), (2,), "bf16 [T, K]")
+        _check_buf("y", y, T, (4,), "fp32 [T, D]")
         check(lib().hc_moe_forward(self._h, int(layer), _ptr(x), T, _ptr(topk_idx), _ptr(topk_gate), k, _ptr(y),
                                    _stream(stream)))
         return y
@@ -196,11 +228,24 @@ class Context:
         r = np.ascontiguousarray(rtilde, dtype=np.float32)
         check(lib().hc_moe_set_dynamic_ranks(self._h, int(layer), r.ctypes.data, int(r.shape[0]), int(k0)))
 
+    def moe_last_ranks(self, T, topk):
+        """hc_moe_last_ranks: int32 [T, topk, 3] ranks (up, gate, down) the device decided in the last
+        hc_moe_forward with dynamic ranks (-1 for a skipped slot)."""
+        out = np.zeros((int(T), int(topk), 3), dtype=np.int32)
+        check(lib().hc_moe_last_ranks(self._h, out.ctypes.data, int(T), int(topk)))
+        return out
+
     def compensated_linear(self, layer, window, x, y, B=None, expert=-1, out_dtype=OUT_F32, stream=None):
         """y[b, :] = concat_m ( deq(W_m)·x_b + U_m[:, :r_m]·(V_m[:r_m, :]·x_b) ).
         x: bf16 [B, K] (torch bf16 / uint16 bits, device or host); y: [B, rows] fp32 or bf16."""
         if B is None:
             B = x.shape[0]
+        rows = self.window_rows(layer, window, expert)
+        if rows < 0:
+            raise HCError(HC_ERR_STATE, f"window ({layer},{window},{expert}) not loaded")
+        _check_buf("x", x, B * int(x.shape[-1]), (2,), "bf16 [B, K]")
+        _check_buf("y", y, B * rows, (4,) if out_dtype == OUT_F32 else (2,),
+                   "fp32 [B, rows]" if out_dtype == OUT_F32 else "bf16 [B, rows]")
         check(lib().hc_compensated_linear(self._h, layer, window, expert, _ptr(x), int(B), _ptr(y),
                                           int(out_dtype), _stream(stream)))
         return y

@@ -59,6 +59,7 @@ SIGNATURES = [
     ("hc_moe_forward", C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32,
                                  C.c_void_p, C.c_void_p]),
     ("hc_moe_set_dynamic_ranks", C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32]),
+    ("hc_moe_last_ranks", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32]),
     ("hc_nccl_unique_id", C.c_int, [C.c_void_p]),
     ("hc_set_comm", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32]),
     ("hc_repacked_bytes", C.c_size_t, [C.c_int32, C.c_int32, C.c_int32]),

@@ -45,14 +45,18 @@ std::vector<double> window_normalise(const std::vector<double>& v) {
   return out;
 }
 
-int align_rank(double rt, int k0) {
+// Nearest level, ties up.  Levels stop at 2^62: an rt >= 2^62 returns 2^62, which exceeds every int cap,
+// so cap_level maps it to the same level the oracle's unbounded align + cap gives (no overflow, no
+// endless loop for huge finite r̃ = 𝒫·r_std).
+long long align_rank(double rt, int k0) {
   long long lo = 0, hi = 1LL << k0;
-  while (rt >= (double)hi) { lo = hi; hi *= 2; }
-  return (rt - (double)lo) < ((double)hi - rt) ? (int)lo : (int)hi;
+  while (rt >= (double)hi && hi < (1LL << 62)) { lo = hi; hi *= 2; }
+  if (rt >= (double)hi) return hi;
+  return (rt - (double)lo) < ((double)hi - rt) ? lo : hi;
 }
 
-int cap_level(int r, int cap, int k0) {
-  if (r <= cap) return r;
+int cap_level(long long r, int cap, int k0) {
+  if (r <= cap) return (int)r;
   int lvl = 0;
   long long v = 1LL << k0;
   while (v <= cap) { lvl = (int)v; v *= 2; }

@@ -13,7 +13,6 @@
 #include "comm.h"
 #include "decode.h"
 #include "prefill.h"
-#include "stack.h"
 #include "moe.h"
 #include "hcinfer.h"
 #include "layout.h"
@@ -87,7 +86,6 @@ bool admissible_rank(int r) { return r == 0 || (r >= 8 && (r & (r - 1)) == 0); }
 
 struct StackGraph {
   cudaGraphExec_t exec = nullptr;
-  DevBuf table, cnt;                  // persistent stack kernel: this graph's window table and counters
   ~StackGraph() { if (exec) cudaGraphExecDestroy(exec); }
 };
 
@@ -99,11 +97,12 @@ struct hc_ctx {
   std::map<Key, Window> windows;
   std::map<std::tuple<int, int, int, int, int>, int> max_ctas;   // (bits, B, K, chunks, vks) -> co-resident CTAs
   DevBuf stage_x, stage_y;
-  DevBuf p_x16, p_t16, p_tpart;        // prefill scratch: fp16 activations, fp16 T = X·Vᵀ, split-K partials
+  DevBuf p_x16, p_t16, p_tpart, p_rsig;        // prefill scratch: fp16 activations, fp16 T = X·Vᵀ, split-K partials
   // decode stack (hc_stack_forward)
   DevBuf s_h, s_h1, s_qkv, s_m;
   int trace_slot = 0;                  // dev tracing: slot of the next decode launch (HC_DEC_TRACE builds)
   DevBuf s_x16[4];                     // x' hand-off buffers of the stack: q, h1, m, h (16 rows each)
+  DevBuf s_x16flag;                    // their exactness flags [4] (DArgs::y16_flag / x16_flag)
   std::map<std::tuple<int, const void*, void*>, std::unique_ptr<StackGraph>> graphs;
   cudaStream_t cap_stream = nullptr;
   // column sharding (hc_set_comm): NCCL communicator, send / gather staging
@@ -122,6 +121,8 @@ struct hc_ctx {
   };
   std::map<int, MoECache> moe;
   DevBuf moe_ws, moe_idx, moe_gate;
+  // the last hc_moe_forward with dynamic ranks (hc_moe_last_ranks): routing shape and device tables
+  struct { int T = 0, topk = 0; const int* tok_row = nullptr; const uint16_t* row_rank = nullptr; } moe_last;
   void invalidate_graphs() {
     graphs.clear();
     for (auto& kv : windows) kv.second.pm->valid = false;
@@ -284,19 +285,10 @@ static hc_status build_prefill(Member& m, const Staged& sd, cudaStream_t st) {
   return HC_OK;
 }
 
-extern "C" hc_status hc_load_layer(hc_ctx* ctx, const hc_matrix_desc* mats, int32_t n_mats, void* stream) {
-  if (!ctx) return fail(HC_ERR_STATE, "hc_load_layer: null context");
-  if (n_mats < 0 || (n_mats > 0 && !mats)) return fail(HC_ERR_CONFIG, "hc_load_layer: bad matrix list");
-  CUDA_TRY(cudaSetDevice(ctx->device));
-  cudaStream_t st = (cudaStream_t)stream;
-  for (int i = 0; i < n_mats; ++i) {
-    hc_status s = validate_desc(mats[i], i);
-    if (s != HC_OK) return s;
-  }
-  ctx->invalidate_graphs();
-  std::vector<char> done(n_mats, 0);
-  for (int i = 0; i < n_mats; ++i) {
-    if (done[i]) continue;
+// Load matrix i (and, for a fused SiLU pair, its partner) into its window.  On failure the caller drops a
+// window this call created and left empty.
+static hc_status load_one(hc_ctx* ctx, const hc_matrix_desc* mats, int32_t n_mats, int i, std::vector<char>& done,
+                          cudaStream_t st) {
     const hc_matrix_desc& d = mats[i];
     Key key{d.layer, d.window_kind, d.expert};
     Window& w = ctx->windows[key];
@@ -354,7 +346,7 @@ extern "C" hc_status hc_load_layer(hc_ctx* ctx, const hc_matrix_desc* mats, int3
       w.glue = HC_GLUE_SILU_MUL;
       w.ws_chunks = -1;
       done[i] = done[j] = 1;
-      continue;
+      return HC_OK;
     }
 
     // ---- plain member
@@ -362,6 +354,12 @@ extern "C" hc_status hc_load_layer(hc_ctx* ctx, const hc_matrix_desc* mats, int3
     for (const Member& o : w.members)
       if (o.slot != d.slot && (o.K != d.K || o.bits != d.bits))
         return fail(HC_ERR_CONFIG, "mat %d: window members must share K and bits", i);
+    {
+      const bool replaces = std::any_of(w.members.begin(), w.members.end(), [&](const Member& o) { return o.slot == d.slot; });
+      if (!replaces && (int)w.members.size() >= hc::kMaxMembers)   // checked before the window is touched
+        return fail(HC_ERR_CONFIG, "mat %d: window (%d,%d,%d) would have more than %d members", i, d.layer,
+                    d.window_kind, d.expert, hc::kMaxMembers);
+    }
     Member m = make_member(d);
     const int rows = m.rows();
     CUDA_TRY(m.rec->alloc((size_t)(rows / hc::kRows) * G * hc::rec_bytes(d.bits)));
@@ -393,9 +391,32 @@ extern "C" hc_status hc_load_layer(hc_ctx* ctx, const hc_matrix_desc* mats, int3
     auto it = std::find_if(w.members.begin(), w.members.end(), [&](const Member& o) { return o.slot == d.slot; });
     if (it != w.members.end()) *it = m; else w.members.push_back(m);
     std::sort(w.members.begin(), w.members.end(), [](const Member& a, const Member& b) { return a.slot < b.slot; });
-    if ((int)w.members.size() > hc::kMaxMembers) return fail(HC_ERR_CONFIG, "window has more than %d members", hc::kMaxMembers);
     w.ws_chunks = -1;
     done[i] = 1;
+    return HC_OK;
+}
+
+extern "C" hc_status hc_load_layer(hc_ctx* ctx, const hc_matrix_desc* mats, int32_t n_mats, void* stream) {
+  if (!ctx) return fail(HC_ERR_STATE, "hc_load_layer: null context");
+  if (n_mats < 0 || (n_mats > 0 && !mats)) return fail(HC_ERR_CONFIG, "hc_load_layer: bad matrix list");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int i = 0; i < n_mats; ++i) {
+    hc_status s = validate_desc(mats[i], i);
+    if (s != HC_OK) return s;
+  }
+  ctx->invalidate_graphs();
+  std::vector<char> done(n_mats, 0);
+  for (int i = 0; i < n_mats; ++i) {
+    if (done[i]) continue;
+    const Key key{mats[i].layer, mats[i].window_kind, mats[i].expert};
+    const bool created = ctx->windows.find(key) == ctx->windows.end();
+    const hc_status s = load_one(ctx, mats, n_mats, i, done, st);
+    if (s != HC_OK) {
+      auto it = ctx->windows.find(key);
+      if (created && it != ctx->windows.end() && it->second.members.empty()) ctx->windows.erase(it);
+      return s;
+    }
   }
   return HC_OK;
 }
@@ -452,19 +473,36 @@ struct X16Spec {
   const uint16_t* in = nullptr;   // x' of this window written by its producer (or NULL)
   uint16_t* out = nullptr;        // where this window writes the next window's x' (or NULL)
   int lo = 0, hi = 0;             // output columns that are the next window's x
+  unsigned* flag_in = nullptr;    // exactness flag of `in` (DArgs::x16_flag), of `out` (DArgs::y16_flag)
+  unsigned* flag_out = nullptr;
 };
 
 static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int B, void* y, int y_bf16,
                              const void* resid, int ld_resid, DArgs& a, int& grid, bool t_in = false,
                              const FwdSpec* fw = nullptr, Window* dep = nullptr, bool keep_done = false,
-                             const X16Spec* xs16 = nullptr) {
+                             const X16Spec* xs16 = nullptr, const Window* pf = nullptr) {
   std::memset(&a, 0, sizeof(a));
+  if (pf) {
+    // L2 prefetch of the next window's records (DArgs::pf_*): the first pf_mb MB of them
+    static const long long pf_cap = [] { const char* e = getenv("HC_PF_MB"); return (long long)(e ? atof(e) * 1e6 : 32e6); }();
+    long long tot = 0;
+    for (const Member& m : pf->members) {
+      if (!m.rec || !m.rec->p || a.pf_n >= kMaxMembers) continue;
+      a.pf_ptr[a.pf_n] = (const uint8_t*)m.rec->p;
+      a.pf_len[a.pf_n] = (long long)m.rec->bytes;
+      tot += (long long)m.rec->bytes;
+      ++a.pf_n;
+    }
+    a.pf_total = std::min(tot, pf_cap);
+  }
   if (xs16) {
     a.x16_given = xs16->in ? 1 : 0;
     a.x16 = xs16->in;
     a.y16 = xs16->out;
     a.y16_lo = xs16->lo;
     a.y16_hi = xs16->hi;
+    a.x16_flag = xs16->in ? xs16->flag_in : nullptr;
+    a.y16_flag = xs16->out ? xs16->flag_out : nullptr;
   }
   a.t_in = t_in ? 1 : 0;
   a.keep_done = keep_done ? 1 : 0;
@@ -476,6 +514,8 @@ static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int
     else for (const Member& m : dep->members) n += m.rows() / kRows;
     a.dep_target = (unsigned)n;
   }
+  if (w.members.empty() || (int)w.members.size() > kMaxMembers)
+    return fail(HC_ERR_STATE, "window has %d members (1..%d)", (int)w.members.size(), kMaxMembers);
   const Member& m0 = w.members.front();
   a.K = m0.K; a.G = m0.K / kGroup; a.B = B;
   a.x = (const uint16_t*)x; a.ldx = ldx; a.y = y; a.y_bf16 = y_bf16;
@@ -524,7 +564,7 @@ static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int
   if (a.n_chunks > kMaxChunks) return fail(HC_ERR_CONFIG, "window ranks need %d chunks > %d", a.n_chunks, kMaxChunks);
   if (w.ws_chunks < max_chunks) {
     const int mc = std::max(max_chunks, 1);
-    CUDA_TRY(w.tacc.alloc((size_t)mc * 256 * sizeof(long long)));
+    CUDA_TRY(w.tacc.alloc((size_t)mc * 512 * sizeof(long long)));
     CUDA_TRY(cudaMemset(w.tacc.p, 0, w.tacc.bytes));
     CUDA_TRY(w.cnt.alloc(2 * sizeof(unsigned)));
     CUDA_TRY(cudaMemset(w.cnt.p, 0, w.cnt.bytes));
@@ -533,9 +573,10 @@ static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int
   a.tacc = (long long*)w.tacc.p;
   a.cnt = (unsigned*)w.cnt.p;
   if (!a.x16_given && !decode_stages_x(B, a.K)) {
-    const size_t need = (size_t)16 * a.K * 2;
+    const size_t need = (size_t)16 * a.K * 2 + (size_t)16 * a.G * sizeof(float);   // x' [16][K] + 2^σ [G][16]
     if (w.xprep.bytes < need) CUDA_TRY(w.xprep.alloc(need));
     a.x16 = (const uint16_t*)w.xprep.p;
+    a.xsig = (float*)((uint16_t*)w.xprep.p + (size_t)16 * a.K);
   }
   if (fw && fw->next) {
     Window& nx = *fw->next;
@@ -573,14 +614,14 @@ static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int
 static hc_status launch_window(hc_ctx* ctx, Window& w, const void* x, int ldx, int B, void* y, int y_bf16,
                                const void* resid, int ld_resid, cudaStream_t st, bool t_in = false,
                                const FwdSpec* fw = nullptr, Window* dep = nullptr, bool keep_done = false,
-                               const X16Spec* xs16 = nullptr) {
+                               const X16Spec* xs16 = nullptr, const Window* pf = nullptr) {
   DArgs a;
   int grid = 0;
-  hc_status s = window_args(ctx, w, x, ldx, B, y, y_bf16, resid, ld_resid, a, grid, t_in, fw, dep, keep_done, xs16);
+  hc_status s = window_args(ctx, w, x, ldx, B, y, y_bf16, resid, ld_resid, a, grid, t_in, fw, dep, keep_done, xs16, pf);
   if (s != HC_OK) return s;
   a.trace_slot = ctx->trace_slot++;
   if (a.x16 && !a.x16_given)
-    CUDA_TRY(launch_xprep(a.x, a.ldx, B, a.K, w.members.front().bits, (uint16_t*)a.x16, st));
+    CUDA_TRY(launch_xprep(a.x, a.ldx, B, a.K, w.members.front().bits, (uint16_t*)a.x16, a.xsig, st));
   CUDA_TRY(launch_decode(a, w.members.front().bits, grid, st));
   return HC_OK;
 }
@@ -638,7 +679,9 @@ static hc_status launch_prefill_window(hc_ctx* ctx, Window& w, const void* x, in
   }
   const size_t xel = (size_t)M * K;
   if (ctx->p_x16.bytes < xel * 2) CUDA_TRY(ctx->p_x16.alloc(xel * 2));
-  CUDA_TRY(launch_bf16_to_f16((const uint16_t*)x, (uint16_t*)ctx->p_x16.p, xel, st));
+  if (ctx->p_rsig.bytes < (size_t)M * 4) CUDA_TRY(ctx->p_rsig.alloc((size_t)M * 4));
+  const float* rsig = (const float*)ctx->p_rsig.p;
+  CUDA_TRY(launch_x_rows_f16((const uint16_t*)x, M, K, (uint16_t*)ctx->p_x16.p, (float*)ctx->p_rsig.p, st));
   const int64_t ldy = w.out_rows();
   CUtensorMap tmX, tmV, tmT, tmU;
   if (!encode_tmap_f16(&tmX, ctx->p_x16.p, K, M, K, kPBM)) return fail(HC_ERR_RUNTIME, "tensor map (X) encoding failed");
@@ -673,6 +716,7 @@ static hc_status launch_prefill_window(hc_ctx* ctx, Window& w, const void* x, in
     pm.scales_t = (const uint16_t*)P.scales.p; pm.zeros_t = (const uint8_t*)P.zeros.p;
     pm.out = y; pm.ldo = N; pm.out_type = y_dtype == HC_OUT_F32 ? 0 : 1;
     pm.tiles_m = (M + kPBM - 1) / kPBM; pm.tiles_n = N / kPBN;
+    pm.rsig = rsig;
     CUDA_TRY(launch_prefill(tmX, tmX, R > 0 ? tmT : tmX, R > 0 ? tmU : tmX, tmC, pm, st));
     return HC_OK;
   }
@@ -703,6 +747,7 @@ static hc_status launch_prefill_window(hc_ctx* ctx, Window& w, const void* x, in
     pm.out = y_dtype == HC_OUT_F32 ? (void*)((float*)y + row_off) : (void*)((uint16_t*)y + row_off);
     pm.ldo = (int)ldy; pm.out_type = y_dtype == HC_OUT_F32 ? 0 : 1;
     pm.tiles_m = (M + kPBM - 1) / kPBM; pm.tiles_n = m.rows() / kPBN;
+    pm.rsig = rsig;
     CUDA_TRY(launch_prefill(tmX, tmX, r > 0 ? tmT : tmX, r > 0 ? tmU : tmX, tmC, pm, st));
     row_off += m.rows();
   }
@@ -843,7 +888,8 @@ extern "C" hc_status hc_moe_forward(hc_ctx* ctx, int32_t layer, const void* x, i
                o_er = take((size_t)maxe * 4), o_ec = take((size_t)maxe * 4), o_xg = take((size_t)R * c->K * 2),
                o_x16 = take((size_t)R * c->K * 2), o_tug = take((size_t)R * c->t_ug * 4), o_m = take((size_t)R * c->F * 2),
                o_md = take((size_t)R * c->F * 2), o_tdn = take((size_t)R * c->t_dn * 4), o_do = take((size_t)R * c->D * 4),
-               o_x = take((size_t)T * c->K * 2), o_y = take((size_t)T * c->D * 4), o_rr = take((size_t)R * 3);
+               o_x = take((size_t)T * c->K * 2), o_y = take((size_t)T * c->D * 4), o_rr = take((size_t)R * 3 * sizeof(uint16_t)),
+               o_fu = take((size_t)R * (c->K / hc::kGroup) * 4), o_fd = take((size_t)R * (c->F / hc::kGroup) * 4);
   if (ctx->moe_ws.bytes < off) CUDA_TRY(ctx->moe_ws.alloc(off));
   uint8_t* ws = (uint8_t*)ctx->moe_ws.p;
   hc::MoERoute rt;
@@ -871,7 +917,7 @@ extern "C" hc_status hc_moe_forward(hc_ctx* ctx, int32_t layer, const void* x, i
   }
   if (hy) dy = ws + o_y;
   const bool dyn = !c->rtilde.empty();
-  uint8_t* row_rank = dyn ? ws + o_rr : nullptr;
+  uint16_t* row_rank = dyn ? (uint16_t*)(ws + o_rr) : nullptr;
   hc::MoEWin wu{(const hc::MoEExpert*)c->ex_ug.p, c->F / 8, c->K, c->K / hc::kGroup, 1, c->t_ug, row_rank, 0};
   hc::MoEWin wd{(const hc::MoEExpert*)c->ex_dn.p, c->D / hc::kRows, c->F, c->F / hc::kGroup, 0, c->t_dn, row_rank, 2};
   hc::MoEDyn mdyn{(const float*)c->d_rtilde.p, (const int*)c->d_caps.p, c->k0, row_rank};
@@ -883,16 +929,37 @@ extern "C" hc_status hc_moe_forward(hc_ctx* ctx, int32_t layer, const void* x, i
   float* tdn = (float*)(ws + o_tdn);
   float* dout = (float*)(ws + o_do);
   CUDA_TRY(hc::moe_route(didx, dgate, T, topk, c->E, rt, dyn ? &mdyn : nullptr, st));
-  CUDA_TRY(hc::moe_prep((const uint16_t*)dx, c->K, c->K, c->bits, 1, rt, R, xg, x16, st));
+  ctx->moe_last.T = T; ctx->moe_last.topk = topk; ctx->moe_last.tok_row = rt.tok_row; ctx->moe_last.row_rank = row_rank;
+  float* fsu = (float*)(ws + o_fu);
+  float* fsd = (float*)(ws + o_fd);
+  CUDA_TRY(hc::moe_prep((const uint16_t*)dx, c->K, c->K, c->bits, 1, rt, R, xg, x16, fsu, st));
   CUDA_TRY(hc::moe_rank_proj(wu, rt, maxe, xg, tug, st));
   const int max_cols = std::min(T, 16);                                             // rows of one expert <= T
-  CUDA_TRY(hc::moe_gemv(wu, c->bits, rt, maxe, x16, tug, m, max_cols, st));        // m = bf16(silu(gate)·up)
-  CUDA_TRY(hc::moe_prep(m, c->F, c->F, c->bits, 0, rt, R, nullptr, md, st));
+  CUDA_TRY(hc::moe_gemv(wu, c->bits, rt, maxe, x16, fsu, tug, m, max_cols, st));   // m = bf16(silu(gate)·up)
+  CUDA_TRY(hc::moe_prep(m, c->F, c->F, c->bits, 0, rt, R, nullptr, md, fsd, st));
   CUDA_TRY(hc::moe_rank_proj(wd, rt, maxe, m, tdn, st));
-  CUDA_TRY(hc::moe_gemv(wd, c->bits, rt, maxe, md, tdn, dout, max_cols, st));      // DOWN_e(m) per row, fp32
+  CUDA_TRY(hc::moe_gemv(wd, c->bits, rt, maxe, md, fsd, tdn, dout, max_cols, st)); // DOWN_e(m) per row, fp32
   CUDA_TRY(hc::moe_combine(dout, c->D, dgate, T, topk, rt, (float*)dy, st));
   if (hy) CUDA_TRY(cudaMemcpyAsync(y, dy, (size_t)T * c->D * 4, cudaMemcpyDeviceToHost, st));
   if (hi || hg || hx || hy) CUDA_TRY(cudaStreamSynchronize(st));
+  return HC_OK;
+}
+
+extern "C" hc_status hc_moe_last_ranks(hc_ctx* ctx, int32_t* out, int32_t T, int32_t topk) {
+  if (!ctx) return fail(HC_ERR_STATE, "hc_moe_last_ranks: null context");
+  if (!out) return fail(HC_ERR_CONFIG, "hc_moe_last_ranks: null output");
+  const auto& L = ctx->moe_last;
+  if (!L.row_rank) return fail(HC_ERR_STATE, "hc_moe_last_ranks: the last hc_moe_forward ran without dynamic ranks");
+  if (T != L.T || topk != L.topk) return fail(HC_ERR_CONFIG, "hc_moe_last_ranks: T/topk %d/%d != last call's %d/%d", T, topk, L.T, L.topk);
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  const int R = T * topk;
+  std::vector<int> tok_row(R);
+  std::vector<uint16_t> rr((size_t)R * 3);
+  CUDA_TRY(cudaMemcpy(tok_row.data(), L.tok_row, (size_t)R * sizeof(int), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(rr.data(), L.row_rank, rr.size() * sizeof(uint16_t), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < R; ++i)
+    for (int sl = 0; sl < 3; ++sl) out[(size_t)i * 3 + sl] = tok_row[i] < 0 ? -1 : (int32_t)rr[(size_t)tok_row[i] * 3 + sl];
   return HC_OK;
 }
 
@@ -1003,6 +1070,10 @@ extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, voi
     const size_t xb[4] = {(size_t)16 * d * 2, (size_t)16 * d * 2, (size_t)16 * f * 2, (size_t)16 * d * 2};
     for (int i = 0; i < 4; ++i)
       if (ctx->s_x16[i].bytes < xb[i]) { ctx->invalidate_graphs(); CUDA_TRY(ctx->s_x16[i].alloc(xb[i])); }
+    if (!ctx->s_x16flag.p) {
+      CUDA_TRY(ctx->s_x16flag.alloc(4 * sizeof(unsigned)));
+      CUDA_TRY(cudaMemset(ctx->s_x16flag.p, 0, 4 * sizeof(unsigned)));
+    }
   }
   const bool tp = ctx->comm != nullptr;
   if (tp) {
@@ -1024,85 +1095,6 @@ extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, voi
         if (s != HC_OK) return s;
       }
     cudaStream_t cs = ctx->cap_stream;
-    // persistent stack kernel (one launch for all windows) when the plan qualifies: one code width,
-    // B <= 8, every window after the first fed by t forwarding and the x' hand-off
-    const char* stack_ev = getenv("HC_STACK_KERNEL");   // "1": persistent stack kernel (opt-in)
-    const bool stack_env = stack_ev && stack_ev[0] == '1';
-    const int bits0 = plan.front().qkv->members.front().bits;
-    bool use_stack = stack_env && !tp && B <= 8;
-    for (size_t l = 0; l < plan.size() && use_stack; ++l)
-      for (Window* w : {plan[l].qkv, plan[l].o, plan[l].ug, plan[l].down}) {
-        if (w->members.front().bits != bits0) use_stack = false;
-        if ((l > 0 || w != plan[l].qkv) && !hc::can_forward(*w)) use_stack = false;
-      }
-    const size_t s_smem = use_stack ? hc::stack_smem_bytes() : 0;
-    const int s_grid = s_smem ? hc::stack_grid(bits0, s_smem) : 0;
-    if (use_stack && s_grid > 0) {
-      std::vector<hc::SWin> tab;
-      const uint16_t* hin = (const uint16_t*)dx;
-      uint16_t* h = (uint16_t*)ctx->s_h.p;
-      uint16_t* h1 = (uint16_t*)ctx->s_h1.p;
-      uint16_t* qkv = (uint16_t*)ctx->s_qkv.p;
-      uint16_t* mm = (uint16_t*)ctx->s_m.p;
-      uint16_t* xq16 = (uint16_t*)ctx->s_x16[0].p, *xh1 = (uint16_t*)ctx->s_x16[1].p;
-      uint16_t* xm16 = (uint16_t*)ctx->s_x16[2].p, *xh16 = (uint16_t*)ctx->s_x16[3].p;
-      int rot = 0;
-      auto add = [&](Window& w, const void* x, int ldx, void* y, const void* resid, int ld_resid, bool t_in,
-                     const hc::FwdSpec& fw, const hc::X16Spec& xs) -> hc_status {
-        hc::SWin sw;
-        std::memset(&sw, 0, sizeof(sw));
-        int grid_unused = 0;
-        hc_status st2 = hc::window_args(ctx, w, x, ldx, B, y, 1, resid, ld_resid, sw.a, grid_unused, t_in,
-                                        fw.next ? &fw : nullptr, nullptr, false, &xs);
-        if (st2 != HC_OK) return st2;
-        sw.rot = rot;
-        rot = (rot + sw.a.n_rb) % s_grid;
-        tab.push_back(sw);
-        return HC_OK;
-      };
-      for (size_t l = 0; l < plan.size(); ++l) {
-        LayerPlan& p = plan[l];
-        const bool last = l + 1 == plan.size();
-        uint16_t* hout = last ? (uint16_t*)dy : h;
-        const hc::FwdSpec s_o{p.o, 0, d}, s_ug{p.ug, 0, d}, s_dn{p.down, 0, f},
-            s_q{last ? nullptr : plan[l + 1].qkv, 0, d};
-        const hc::X16Spec x_q{xh16, xq16, 0, d}, x_o{xq16, xh1, 0, d}, x_ug{xh1, xm16, 0, f},
-            x_dn{xm16, last ? nullptr : xh16, 0, d};
-        s = add(*p.qkv, hin, d, qkv, nullptr, 0, l > 0, s_o, x_q);                 // q | k | v
-        if (s == HC_OK) s = add(*p.o, qkv, nqkv, h1, hin, d, true, s_ug, x_o);      // h1 = h + O(q)
-        if (s == HC_OK) s = add(*p.ug, h1, d, mm, nullptr, 0, true, s_dn, x_ug);    // m = silu(g)·u
-        if (s == HC_OK) s = add(*p.down, mm, f, hout, h1, d, true, s_q, x_dn);      // h' = h1 + DOWN(m)
-        if (s != HC_OK) return s;
-        hin = hout;
-      }
-      const size_t tb = tab.size() * sizeof(hc::SWin), cb = (tab.size() + 1) * sizeof(unsigned);
-      std::unique_ptr<StackGraph> sg(new StackGraph());
-      CUDA_TRY(sg->table.alloc(tb));
-      CUDA_TRY(sg->cnt.alloc(cb));
-      CUDA_TRY(cudaMemcpy(sg->table.p, tab.data(), tb, cudaMemcpyHostToDevice));
-      hc::StackArgs sa;
-      sa.wins = (const hc::SWin*)sg->table.p;
-      sa.n_win = (int)tab.size();
-      sa.n_vwarps0 = hc::stack_vwarps(tab[0].a.n_chunks * 4 * tab[0].a.G, s_grid);
-      sa.done = (unsigned*)sg->cnt.p;
-      sa.vdone = sa.done + tab.size();
-      CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-      cudaError_t e1 = cudaMemsetAsync(sg->cnt.p, 0, cb, cs);
-      if (e1 == cudaSuccess) e1 = hc::launch_xprep((const uint16_t*)dx, d, B, d, bits0, xh16, cs);
-      cudaError_t e2 = e1 == cudaSuccess ? hc::launch_stack(sa, bits0, s_grid, s_smem, cs) : e1;
-      cudaGraph_t g = nullptr;
-      cudaError_t e = cudaStreamEndCapture(cs, &g);
-      if (e2 != cudaSuccess) { if (g) cudaGraphDestroy(g); return fail(HC_ERR_RUNTIME, "stack kernel capture: %s", cudaGetErrorString(e2)); }
-      CUDA_TRY(e);
-      e = cudaGraphInstantiate(&sg->exec, g, 0);
-      cudaGraphDestroy(g);
-      CUDA_TRY(e);
-      git = ctx->graphs.emplace(key, std::move(sg)).first;
-      CUDA_TRY(cudaGraphLaunch(git->second->exec, st));
-      if (hy) CUDA_TRY(cudaMemcpyAsync(y, dy, hb, cudaMemcpyDeviceToHost, st));
-      if (hx || hy) CUDA_TRY(cudaStreamSynchronize(st));
-      return HC_OK;
-    }
     CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
     hc_status cap = HC_OK;
     const uint16_t* hin = (const uint16_t*)dx;
@@ -1139,21 +1131,30 @@ extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, voi
         auto i8w = [&](Window* w) { return hc::decode_uses_i8(w->members.front().bits, B, w->members.front().K); };
         const bool i8q = i8w(p.qkv), i8o = i8w(p.o), i8ug = i8w(p.ug), i8dn = i8w(p.down);
         const bool i8qn = l + 1 < plan.size() ? i8w(plan[l + 1].qkv) : true;
-        const hc::X16Spec x_q{hx && l > 0 && !i8q ? xh16 : nullptr, hx && !i8o ? xq16 : nullptr, 0, d};
-        const hc::X16Spec x_o{hx && !i8o ? xq16 : nullptr, hx && !i8ug ? xh1 : nullptr, 0, d};
-        const hc::X16Spec x_ug{hx && !i8ug ? xh1 : nullptr, hx && !i8dn ? xm16 : nullptr, 0, f};
-        const hc::X16Spec x_dn{hx && !i8dn ? xm16 : nullptr, (hx && !i8qn) ? xh16 : nullptr, 0, d};
+        unsigned* xfl = (unsigned*)ctx->s_x16flag.p;     // flags of q, h1, m, h
+        const hc::X16Spec x_q{hx && l > 0 && !i8q ? xh16 : nullptr, hx && !i8o ? xq16 : nullptr, 0, d, xfl + 3, xfl + 0};
+        const hc::X16Spec x_o{hx && !i8o ? xq16 : nullptr, hx && !i8ug ? xh1 : nullptr, 0, d, xfl + 0, xfl + 1};
+        const hc::X16Spec x_ug{hx && !i8ug ? xh1 : nullptr, hx && !i8dn ? xm16 : nullptr, 0, f, xfl + 1, xfl + 2};
+        const hc::X16Spec x_dn{hx && !i8dn ? xm16 : nullptr, (hx && !i8qn) ? xh16 : nullptr, 0, d, xfl + 2, xfl + 3};
         const bool dq = sx_q || (hx && l > 0), do_ = sx_q || hx, dug = sx_q || hx, ddn = sx_f || hx;
         const bool kq = sx_q || hx, ko = sx_q || hx, kug = sx_f || hx;     // keep(producer) = dep(consumer)
         const bool kdn = l + 1 < plan.size() && (sx_q || hx);
+        // L2 prefetch of the next window's weights (DArgs::pf_*): opt-in (HC_PF=1); measured slower on C2
+        // (670 -> 668 / 651 / 640 tokens/s at 16 / 32 / 64 MB): the prefetch misses lengthen the L2 latency
+        // of the critical-path activation loads
+        const bool pf_on = getenv("HC_PF") != nullptr && getenv("HC_PF")[0] == '1';
+        const Window* pf_q = pf_on ? p.o : nullptr;
+        const Window* pf_o = pf_on ? p.ug : nullptr;
+        const Window* pf_ug = pf_on ? p.down : nullptr;
+        const Window* pf_dn = (pf_on && l + 1 < plan.size()) ? plan[l + 1].qkv : nullptr;
         cap = hc::launch_window(ctx, *p.qkv, hin, d, B, qkv, 1, nullptr, 0, cs, t_q, &s_o,
-                                (prev_dn && dq) ? prev_dn : nullptr, kq, &x_q);                              // q | k | v
+                                (prev_dn && dq) ? prev_dn : nullptr, kq, &x_q, pf_q);                        // q | k | v
         if (cap == HC_OK) cap = hc::launch_window(ctx, *p.o, qkv, nqkv, B, h1, 1, hin, d, cs, f_o, &s_ug,
-                                                  do_ ? p.qkv : nullptr, ko, &x_o);                           // h1 = h + O(q)
+                                                  do_ ? p.qkv : nullptr, ko, &x_o, pf_o);                     // h1 = h + O(q)
         if (cap == HC_OK) cap = hc::launch_window(ctx, *p.ug, h1, d, B, mm, 1, nullptr, 0, cs, f_ug, &s_dn,
-                                                  dug ? p.o : nullptr, kug, &x_ug);                           // m = silu(g)·u
+                                                  dug ? p.o : nullptr, kug, &x_ug, pf_ug);                    // m = silu(g)·u
         if (cap == HC_OK) cap = hc::launch_window(ctx, *p.down, mm, f, B, hout, 1, h1, d, cs, f_dn, &s_q,
-                                                  ddn ? p.ug : nullptr, kdn, &x_dn);                          // h' = h1 + DOWN(m)
+                                                  ddn ? p.ug : nullptr, kdn, &x_dn, pf_dn);                   // h' = h1 + DOWN(m)
       } else {                                                   // column-sharded: gather every window
         cap = tp_window(ctx, *p.qkv, hin, d, B, qkv, nullptr, 0, cs);
         if (cap == HC_OK) cap = tp_window(ctx, *p.o, qkv, nqkv, B, h1, hin, d, cs);

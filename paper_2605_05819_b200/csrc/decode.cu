@@ -22,17 +22,25 @@
 //  * the 8 warps' partial sums are reduced in shared memory in a fixed order; the CTA's epilogue
 //    warp adds U[:, :r]·t with t split into bf16 hi + lo (fp32-accurate) on the same mma and
 //    writes y once (fp32, or bf16 = RNE of the fp32 value), optionally adding a bf16 residual;
-//  * t is produced inside the launch with 64-bit fixed-point atomics (2^-28 resolution; integer adds
-//    are associative, so t is deterministic); epilogues acquire a release counter.  The accumulators
-//    and counters self-reset before the kernel exits.
+//  * t is produced inside the launch with two-word 64-bit fixed-point atomics (tacc_add: exact for
+//    fp32 partials down to 2^-78; integer adds are associative, so t is deterministic); epilogues
+//    acquire a release counter.  The accumulators and counters self-reset before the kernel exits.
+//  * fp16 path: the B operand carries a per-(group, batch row) power-of-two prescale when a group's
+//    range needs it (R20), so any bf16 x is accepted.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "decode.h"
 #include "decode_dev.cuh"
-#include "decode_i8.cuh"
 #include "layout.h"
+
+namespace hc {
+__device__ unsigned long long* g_dtrace = nullptr;   // dev tracing (HC_DEC_TRACE builds)
+}
+#include "decode_i8.cuh"
 
 namespace hc {
 
@@ -44,12 +52,11 @@ namespace hc {
 #endif
 // dev tracing: globaltimer stamps per (launch slot, CTA): [0] start, [1] after the PDL wait (epilogue),
 // [2] first FULL passed, [3] last FULL passed, [4] epilogue done, [5] t ready
-__device__ unsigned long long* g_dtrace = nullptr;
 __device__ __forceinline__ void dtrace(const DArgs& a, int ev) {
 #if HC_DEC_TRACE
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  if (g_dtrace) g_dtrace[((size_t)a.trace_slot * 512 + blockIdx.x) * 8 + ev] = t;
+  if (g_dtrace) g_dtrace[((size_t)a.trace_slot * 512 + blockIdx.x) * 16 + ev] = t;
 #endif
 }
 cudaError_t decode_set_trace(void* buf) { return cudaMemcpyToSymbol(g_dtrace, &buf, sizeof(buf)); }
@@ -101,7 +108,9 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
   uint4* tsm = reinterpret_cast<uint4*>(ebars_all + kDecodeWarps * kNBuf);   // [n_chunks][NB8][32] t hi|lo fragments
   uint16_t* xt = reinterpret_cast<uint16_t*>(tsm + (size_t)a.n_chunks * NB8 * 32);   // [16 k][16 cols] fwd x tile
   uint4* fbuf = reinterpret_cast<uint4*>(xt + 256);                                  // [fwd_chunks][32] Vn fragments
-  uint16_t* xs = reinterpret_cast<uint16_t*>(fbuf + (size_t)(a.fwd ? a.fwd_chunks : 0) * 32);
+  unsigned* misc = reinterpret_cast<unsigned*>(fbuf + (size_t)(a.fwd ? a.fwd_chunks : 0) * 32);   // [4]: [0] XS σ any, [1] x' slow path
+  float* fsg = reinterpret_cast<float*>(misc + 4);                                   // XS: 2^σ [G][B]
+  uint16_t* xs = reinterpret_cast<uint16_t*>(fsg + ((XS && !I8) ? ((a.G * a.B + 3) & ~3) : 0));
   const int xs_ld = a.K + 32;   // +64 B per row: consecutive batch rows fall in disjoint banks
 
   if (lane == 0) {
@@ -113,6 +122,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
       }
     } else if (warp == kDecodeWarps) {
       mbar_init(&ubar[0], 1); mbar_init(&ubar[1], 1); mbar_init(xbar, 1); mbar_init(fbar, 1);
+      misc[0] = 0u; misc[1] = 0u;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -173,6 +183,22 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
         if (++slot == kNBuf) { slot = 0; ++round; }
       }
     }
+    if (a.pf_total > 0) {
+      // every ring of this CTA is issued: prefetch this CTA's slice of the next window's records to L2
+      __syncwarp();
+      const long long lo = a.pf_total * blockIdx.x / gridDim.x, hi = a.pf_total * (blockIdx.x + 1) / gridDim.x;
+      constexpr long long kChunk = 16384;
+      long long base = 0;
+      for (int i = 0; i < a.pf_n; ++i) {
+        const long long s0 = max(lo, base), s1 = min(hi, base + a.pf_len[i]);
+        for (long long c = (s0 & ~15LL) + (long long)lane * kChunk; c < s1; c += 32 * kChunk) {
+          const long long e = min(c + kChunk, s1);
+          const uint32_t n = (uint32_t)((e - c + 15) & ~15LL);
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.pf_ptr[i] + (c - base)), "r"(n) : "memory");
+        }
+        base += a.pf_len[i];
+      }
+    }
     return;
   }
 
@@ -194,6 +220,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
     };
     prefetch_u(blockIdx.x, 0);                           // weights: before the PDL wait
     dep_wait(a, lane);
+    if (lane == 0 && a.x16_given && a.x16_flag) misc[1] = *reinterpret_cast<volatile unsigned*>(a.x16_flag);   // before bar 6
     if ((!XS || I8) && a.dep_cnt) asm volatile("bar.sync 6, %0;" ::"n"(kDecodeThreads) : "memory");   // release the tile warps
     if (lane == 0) dtrace(a, 1);
     if constexpr (XS && !I8) {
@@ -227,13 +254,13 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
           const int r0 = 16 * (cc - mt.chunk_begin) + 2 * tig;
 #pragma unroll
           for (int nb = 0; nb < NB8; ++nb) {
-            const long long* src = a.tacc + ((size_t)cc * 16 + ((gid + 8 * nb) & 15)) * 16 + 2 * tig;
-            const long long tr[4] = {__ldcg(src), __ldcg(src + 1), __ldcg(src + 8), __ldcg(src + 9)};
+            const long long* src = a.tacc + (((size_t)cc * 16 + ((gid + 8 * nb) & 15)) * 16 + 2 * tig) * 2;
+            const float tr[4] = {tacc_read(src), tacc_read(src + 2), tacc_read(src + 16), tacc_read(src + 18)};
             uint32_t hi[2], lo[2];
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
-              const float ta = (r0 + 8 * hh < mt.r) ? (float)tr[2 * hh] * kTInv : 0.f;
-              const float tb = (r0 + 8 * hh + 1 < mt.r) ? (float)tr[2 * hh + 1] * kTInv : 0.f;
+              const float ta = (r0 + 8 * hh < mt.r) ? tr[2 * hh] : 0.f;
+              const float tb = (r0 + 8 * hh + 1 < mt.r) ? tr[2 * hh + 1] : 0.f;
               const uint32_t ha = f32_to_bf16_rn(ta), hb = f32_to_bf16_rn(tb);
               hi[hh] = ha | (hb << 16);
               lo[hh] = f32_to_bf16_rn(ta - bf16_bits_to_f32(ha)) | (f32_to_bf16_rn(tb - bf16_bits_to_f32(hb)) << 16);
@@ -392,9 +419,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int col = 2 * tig + (e & 1) + 8 * nb, rank = gid + 8 * (e >> 1);
-              if (col < a.B)
-                atomicAdd(reinterpret_cast<unsigned long long*>(a.fwd_tacc + ((size_t)cc * 16 + col) * 16 + rank),
-                          (unsigned long long)__float2ll_rn(tp[e] * kTScale));
+              if (col < a.B) tacc_add(a.fwd_tacc + (((size_t)cc * 16 + col) * 16 + rank) * 2, tp[e]);
             }
           }
         }
@@ -408,16 +433,17 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
     __syncwarp();
     unsigned last = 0;
     if (lane == 0 && my_rb > 0) {
-      const unsigned old = add_release(&a.cnt[1], (unsigned)my_rb);
+      const unsigned old = add_acq_rel(&a.cnt[1], (unsigned)my_rb);
       last = (old + (unsigned)my_rb == (unsigned)a.n_rb);
     }
     last = __shfl_sync(0xffffffffu, last, 0);
     if (last) {
-      for (int i = lane; i < a.n_chunks * 256; i += 32) a.tacc[i] = 0;
+      for (int i = lane; i < a.n_chunks * 512; i += 32) a.tacc[i] = 0;
       if (lane == 0) {
         a.cnt[0] = 0u;
         if (!a.keep_done) a.cnt[1] = 0u;             // else the consumer window resets it
         if (a.dep_cnt) *a.dep_cnt = 0u;              // every CTA of this window passed its wait
+        if (a.x16_flag) *a.x16_flag = 0u;            // ... and read the producer's x' exactness flag
       }
     }
     return;
@@ -460,9 +486,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int col = 2 * tig + (e & 1) + 8 * nb, rank = gid + 8 * (e >> 1);
-          if (col < a.B)
-            atomicAdd(reinterpret_cast<unsigned long long*>(a.tacc + ((size_t)cc * 16 + col) * 16 + rank),
-                      (unsigned long long)__float2ll_rn(tp[nb][e] * kTScale));
+          if (col < a.B) tacc_add(a.tacc + (((size_t)cc * 16 + col) * 16 + rank) * 2, tp[nb][e]);
           tp[nb][e] = 0.f;
         }
     };
@@ -502,21 +526,43 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
   }
   if constexpr (I8) {
     // x (L2) -> int8 digits (smem) of this warp's groups (the same for every item: warp_share)
+    if (warp == 0 && lane == 0) dtrace(a, 6);
     x8_stage(a, reinterpret_cast<uint8_t*>(xs), warp * a.G / kDecodeWarps, (warp + 1) * a.G / kDecodeWarps, lane);
     __syncwarp();
+    if (warp == 0 && lane == 0) dtrace(a, 7);
   } else if constexpr (XS) {
     while (!mbar_try_wait(xbar, 0)) {}
-    // in place: x (bf16) -> x' = x·2^-fp (fp16, the B operand of the W mma); 16 elements per thread
+    // in place: x (bf16) -> x' = x·2^-(fp+σ) (fp16, the B operand of the W mma); 16 elements per thread,
+    // the 8 threads of one (group, batch row) are 8 consecutive lanes (they agree on σ, R20)
     const int tid = threadIdx.x;   // 0..255 (tile warps)
     for (int i = tid; i < a.G * a.B * 8; i += kDecodeWarps * 32) {
       const int part = i & 7, gb = i >> 3, b = gb % a.B, g = gb / a.B;
       uint4* src = reinterpret_cast<uint4*>(xs + (size_t)b * xs_ld + g * kGroup + part * 16);
       const uint4 in[2] = {src[0], src[1]};
+      const unsigned m8 = 0xFFu << (lane & 24);
+      uint32_t m = max(absmax8(in[0]), absmax8(in[1]));
+      m = max(m, __shfl_xor_sync(m8, m, 1));
+      m = max(m, __shfl_xor_sync(m8, m, 2));
+      m = max(m, __shfl_xor_sync(m8, m, 4));
+      const int sig = prescale_sigma(m);
       uint4 out[2];
-      xprime16<BITS>(in, part, out);
+      xprime16<BITS>(in, part, out, sig);
       src[0] = out[0]; src[1] = out[1];
+      if (part == 0) {
+        fsg[g * a.B + b] = pow2i(sig);
+        if (sig != 0) misc[0] = 1u;
+      }
     }
     asm volatile("bar.sync 5, %0;" ::"n"(kDecodeWarps * 32) : "memory");   // tile warps only
+  }
+  // fp16-path B-operand prescale (R20): factors 2^σ per (group, batch row) from the staging (XS), the
+  // x-prep kernel (global), or computed per record from bf16 x (hand-off slow path); else none
+  const float* fsig = nullptr;
+  bool slow = false;
+  if constexpr (!I8) {
+    if constexpr (XS) fsig = misc[0] ? fsg : nullptr;
+    else if (!a.x16_given) fsig = a.xsig;
+    else slow = misc[1] != 0u;
   }
   int k = 0;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++k) {
@@ -534,6 +580,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
       const int nt = min(kRPB, sh.n - t0);
       const uint8_t* blk = bufs + s * kBlk;
       while (!mbar_try_wait(&bars[s], ph)) {}
+      if (k == 0 && t0 == 0 && warp == 0 && lane == 0 && !I8) dtrace(a, 7);
       if constexpr (I8) {
         const uint8_t* x8 = reinterpret_cast<const uint8_t*>(xs);
         const int xg = x8_stride(a.B), dd = 512 * a.B;
@@ -546,27 +593,39 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
           for (int t = 0; t < nt; ++t)
             i8_tile<BITS>(blk + t * rec_bytes(BITS), lane, x8 + (size_t)(sh.g0 + t0 + t) * xg, dd, t1);
         }
-      } else if (nt == kRPB) {
-        // full block: the records are independent straight-line code, so their mma chains interleave
-#pragma unroll
-        for (int t = 0; t < kRPB; ++t) {
-          const int g = sh.g0 + t0 + t;
-          uint32_t xr[NB8][16];
-          const uint4* xrs[NB8];
-#pragma unroll
-          for (int nb = 0; nb < NB8; ++nb) xrs[nb] = reinterpret_cast<const uint4*>(xs_row[nb] + g * kGroup);
-          if constexpr (!XS) load_x_global<NB8>(a, g, lane, xr);
-          w_tile<BITS, NB8, XS>(blk + t * rec_bytes(BITS), lane, xrs, xr, tot);
-        }
       } else {
-        for (int t = 0; t < nt; ++t) {
+        // one record: x' fragments (smem, global, or the slow path's own conversion) and, with a
+        // prescale, the factors 2^σ of the lane's two output columns
+        auto rec = [&](auto sig_c, int t) {
+          constexpr bool SIG = decltype(sig_c)::value;
           const int g = sh.g0 + t0 + t;
           uint32_t xr[NB8][16];
+          float fs[NB8][2];
           const uint4* xrs[NB8];
 #pragma unroll
           for (int nb = 0; nb < NB8; ++nb) xrs[nb] = reinterpret_cast<const uint4*>(xs_row[nb] + g * kGroup);
-          if constexpr (!XS) load_x_global<NB8>(a, g, lane, xr);
-          w_tile<BITS, NB8, XS>(blk + t * rec_bytes(BITS), lane, xrs, xr, tot);
+          if constexpr (!XS) {
+            if (SIG && slow) load_x_bf16_sig<BITS, NB8>(a, g, lane, xr, fs);
+            else load_x_global<NB8>(a, g, lane, xr);
+          }
+          if (SIG && !slow) {
+#pragma unroll
+            for (int nb = 0; nb < NB8; ++nb)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) fs[nb][h] = fsig[g * a.B + min(2 * tig + h + 8 * nb, a.B - 1)];
+          }
+          w_tile<BITS, NB8, XS, SIG>(blk + t * rec_bytes(BITS), lane, xrs, xr, tot, fs);
+        };
+        if (fsig == nullptr && !slow) {
+          if (nt == kRPB) {
+            // full block: the records are independent straight-line code, so their mma chains interleave
+#pragma unroll
+            for (int t = 0; t < kRPB; ++t) rec(std::false_type{}, t);
+          } else {
+            for (int t = 0; t < nt; ++t) rec(std::false_type{}, t);
+          }
+        } else {
+          for (int t = 0; t < nt; ++t) rec(std::true_type{}, t);
         }
       }
       advance();
@@ -587,8 +646,9 @@ static size_t decode_smem_bytes(bool xs, bool i8, int B, int K, int n_chunks, in
   size_t s = (size_t)kDecodeWarps * kNBuf * kTPB * kTileMax + 2 * kDecodeWarps * 32 * 4 * nb8 * sizeof(float) +
              2 * kUPre * 32 * 16 + (2 * kDecodeWarps * kNBuf + 4) * sizeof(uint64_t) +
              (size_t)n_chunks * nb8 * 32 * 16 + 512 + (size_t)fwd_chunks * 512;
+  s += 16;                                                                 // misc
   if (i8) s += (size_t)(K / kGroup) * x8_stride(B) + kX8Pad;
-  else if (xs) s += (size_t)B * (K + 32) * 2;
+  else if (xs) s += (size_t)(((K / kGroup) * B + 3) & ~3) * 4 + (size_t)B * (K + 32) * 2;   // 2^σ [G][B] + x'
   return s;
 }
 
@@ -609,22 +669,33 @@ bool decode_uses_i8(int bits, int B, int K) { return use_xs(B, K) && use_i8(bits
 // x -> x' (fp16, pre-scaled per the code layout) for the !XS decode launches.
 // One thread per (group, batch row, 16-element part).
 template <int BITS>
-__global__ void xprep_kernel(const uint16_t* __restrict__ x, int ldx, int B, int K, uint16_t* __restrict__ x16) {
+__global__ void xprep_kernel(const uint16_t* __restrict__ x, int ldx, int B, int K, uint16_t* __restrict__ x16,
+                             float* __restrict__ xsig) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // one thread per (group, batch row, 16-element part): the 8 parts of a (group, row) are 8 consecutive
+  // lanes and agree on the group's prescale σ (R20); 2^σ -> xsig[g][b]
   const int i = blockIdx.x * blockDim.x + threadIdx.x;   // over G * B * 8
-  if (i < (K / kGroup) * B * 8) {
+  const int n = (K / kGroup) * B * 8;                    // a multiple of 8: 8-lane groups are all in or all out
+  if (i < n) {
     const int part = i & 7, gb = i >> 3, b = gb % B, g = gb / B;
     const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)b * ldx + g * kGroup + part * 16);
     const uint4 in[2] = {__ldg(src), __ldg(src + 1)};
+    const unsigned m8 = 0xFFu << (threadIdx.x & 24);
+    uint32_t m = max(absmax8(in[0]), absmax8(in[1]));
+    m = max(m, __shfl_xor_sync(m8, m, 1));
+    m = max(m, __shfl_xor_sync(m8, m, 2));
+    m = max(m, __shfl_xor_sync(m8, m, 4));
+    const int sig = prescale_sigma(m);
     uint4 out[2];
-    xprime16<BITS>(in, part, out);
+    xprime16<BITS>(in, part, out, sig);
     uint4* dst = reinterpret_cast<uint4*>(x16 + (size_t)b * K + g * kGroup + part * 16);
     dst[0] = out[0]; dst[1] = out[1];
+    if (part == 0) xsig[g * B + b] = pow2i(sig);
   }
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-cudaError_t launch_xprep(const uint16_t* x, int ldx, int B, int K, int bits, uint16_t* x16, cudaStream_t st) {
+cudaError_t launch_xprep(const uint16_t* x, int ldx, int B, int K, int bits, uint16_t* x16, float* xsig, cudaStream_t st) {
   const int n = (K / kGroup) * B * 8;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((n + 255) / 256);
@@ -636,9 +707,9 @@ cudaError_t launch_xprep(const uint16_t* x, int ldx, int B, int K, int bits, uin
   cfg.attrs = at;
   cfg.numAttrs = 1;
   switch (bits) {
-    case 2: return cudaLaunchKernelEx(&cfg, xprep_kernel<2>, x, ldx, B, K, x16);
-    case 3: return cudaLaunchKernelEx(&cfg, xprep_kernel<3>, x, ldx, B, K, x16);
-    case 4: return cudaLaunchKernelEx(&cfg, xprep_kernel<4>, x, ldx, B, K, x16);
+    case 2: return cudaLaunchKernelEx(&cfg, xprep_kernel<2>, x, ldx, B, K, x16, xsig);
+    case 3: return cudaLaunchKernelEx(&cfg, xprep_kernel<3>, x, ldx, B, K, x16, xsig);
+    case 4: return cudaLaunchKernelEx(&cfg, xprep_kernel<4>, x, ldx, B, K, x16, xsig);
     default: return cudaErrorInvalidValue;
   }
 }

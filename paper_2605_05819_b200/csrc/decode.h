@@ -81,8 +81,23 @@ struct DArgs {
   int x16_given;
   uint16_t* y16;
   int y16_lo, y16_hi;
+  // x' exactness (R20): the producer sets *y16_flag when some x' it wrote is not exact in fp16
+  // (|x| out of the fp16-exact band); the consumer reads *x16_flag after its dependency wait and then
+  // builds x' itself with a per-group prescale (slow path); its last CTA resets the flag
+  unsigned* y16_flag;
+  unsigned* x16_flag;
+  float* xsig;          // x-prep launches (x16 given by launch_xprep): 2^σ per (group, batch row) [G][B]
   long long* tacc;      // [n_chunks][16 batch][16 ranks] t = V·x in 2^-28 fixed point (self-resetting)
   unsigned* cnt;        // [0] v_done (tile warps done with their V share), [1] w_done (row blocks)
+  // L2 prefetch of the NEXT window's weight records (stack graphs): once a CTA's producer warp has issued
+  // its last bulk copy, it prefetches its share (by CTA index) of the first pf_total bytes of the
+  // concatenated record arrays pf_ptr[i] (pf_len[i] bytes each) into L2, so HBM keeps streaming through
+  // this window's tail, the dependency hand-off and the next window's ramp (weights do not depend on
+  // activations)
+  const uint8_t* pf_ptr[kMaxMembers];
+  long long pf_len[kMaxMembers];
+  int pf_n;
+  long long pf_total;
 };
 
 // Launch the fused window kernel; bits in {2,3,4}; 1 <= B <= 16.
@@ -93,7 +108,7 @@ bool decode_stages_x(int B, int K);
 // a window reads bf16 x itself, so its producer writes no x' hand-off for it.
 bool decode_uses_i8(int bits, int B, int K);
 // x' (fp16, pre-scaled per the code layout of `bits`) for a !XS decode launch.
-cudaError_t launch_xprep(const uint16_t* x, int ldx, int B, int K, int bits, uint16_t* x16, cudaStream_t st);
+cudaError_t launch_xprep(const uint16_t* x, int ldx, int B, int K, int bits, uint16_t* x16, float* xsig, cudaStream_t st);
 cudaError_t decode_set_trace(void* buf);   // dev: [slots][grid][8] globaltimer stamps (HC_DEC_TRACE builds)
 // Max co-resident CTAs of the decode kernel on this device (persistent grid size).
 int decode_max_ctas(int bits, int B, int K, int n_chunks, int fwd_chunks, bool no_xs = false);

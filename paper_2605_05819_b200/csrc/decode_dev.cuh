@@ -73,6 +73,14 @@ __device__ __forceinline__ unsigned add_release(unsigned* p, unsigned v) {
   return old;
 }
 
+// counter += v with acquire-release semantics: the CTA that completes a window (and then resets the
+// window's accumulators and counters) also observes every other CTA's released writes
+__device__ __forceinline__ unsigned add_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -187,9 +195,41 @@ constexpr int kVPerWarp = HC_VPW;                    // V·x pieces per tile war
 constexpr float kTScale = 268435456.f;          // 2^28: fixed-point scale of the t accumulators
 constexpr float kTInv = 1.f / 268435456.f;
 
+// t accumulators: two 64-bit integer words per element, hi = Σ rint(v·2^28) and lo = Σ rint(r·2^50) with
+// r = v·2^28 − rint(v·2^28) (exact in fp32), so every fp32 partial v with |v| < 2^35 is represented
+// EXACTLY down to 2^-78 and the sums are order-free integer adds (t is deterministic).  A second word
+// only when the first leaves a remainder (|v| < 2^-5 or non-integral v·2^28), so typical |t| ~ 1 partials
+// cost one atomic; activations down to ~1e-20 keep a full-precision rank projection (R22).
+__device__ __forceinline__ void tacc_add(long long* p, float v) {
+  const float s = v * kTScale;                               // exact (power of two)
+  const long long hi = __float2ll_rn(s);
+  if (hi != 0) atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)hi);
+  const float res = s - (float)hi;                           // exact: |s| < 2^23 -> hi fits 24 bits; else s integral
+  if (res != 0.f) atomicAdd(reinterpret_cast<unsigned long long*>(p + 1), (unsigned long long)__float2ll_rn(res * 0x1p50f));
+}
+__device__ __forceinline__ float tacc_read(const long long* p) {
+  return (float)((double)__ldcg(p) * 0x1p-28 + (double)__ldcg(p + 1) * 0x1p-78);
+}
+
 // Row of x used by mma column `col` (batch index).  Columns >= B read a valid row; their
 // outputs are never stored, so no zeroing is needed.
 __device__ __forceinline__ int xrow(const DArgs& a, int col) { return col < a.B ? col : a.B - 1; }
+
+// ---- per-(group, batch row) power-of-two prescale of the fp16 B operand (R20).
+// x' = x·2^-(fp + σ) is exact in fp16 for every bf16 x with |x|·2^-(fp+σ) in [2^-17, 2^15] (fp16's
+// 11-bit significand holds bf16's 8 bits down to the subnormal grid 2^-24).  σ = 0 whenever the group's
+// largest |x| has exponent E in [-2, 13] (the common case: no extra work, bit-identical to no prescale);
+// otherwise σ = E - 12 (the group's largest |x'| lands in [2^12, 2^13)), clamped to [-100, 115] so that
+// 2^±σ stay normal floats.  The group's fp32 partial sum is multiplied back by 2^σ (exact: a power of
+// two).  So the full bf16 range is accepted: outliers >= 65504 and tiny (< 2^-14) activations included.
+// Zero and non-finite groups keep σ = 0 (inf / NaN propagate through the products).
+__device__ __forceinline__ int prescale_sigma(uint32_t m) {   // m = the group's largest |x| (bf16 bits & 0x7FFF)
+  if (m == 0 || m >= 0x7F80u) return 0;
+  const int E = max((int)(m >> 7), 1) - 127;
+  if (E >= -2 && E <= 13) return 0;
+  return min(max(E - 12, -100), 115);
+}
+__device__ __forceinline__ float pow2i(int e) { return __uint_as_float((uint32_t)(127 + e) << 23); }   // e in [-126, 127]
 
 // x' fragments of group g from the window's fp16 x' buffer (global, L1-cached):
 // xr[nb][4q + e] = x'[b][g*128 + 32q + 8tig .. +7]
@@ -211,16 +251,62 @@ __device__ __forceinline__ void load_x_global(const DArgs& a, int g, int lane, u
   }
 }
 
+// Largest |x| (bf16 bits without the sign) of the 8 bf16 values in a uint4.
+__device__ __forceinline__ uint32_t absmax8(const uint4 v) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) m = max(m, max(w[i] & 0x7FFFu, (w[i] >> 16) & 0x7FFFu));
+  return m;
+}
+
+// Slow path of the x' hand-off (stack windows whose producer flagged an x' value fp16 cannot hold
+// exactly, R20): read bf16 x of group g from global memory, take the per-(group, column)
+// prescale from the group's largest |x| (the four tig lanes of a column hold its 128 k), and build the
+// same fragments as load_x_global plus the output-column factors fs.
+template <int BITS, int NB8>
+__device__ __forceinline__ void load_x_bf16_sig(const DArgs& a, int g, int lane, uint32_t (&xr)[NB8][16],
+                                                float (&fs)[NB8][2]) {
+  const int gid = lane >> 2, tig = lane & 3;
+#pragma unroll
+  for (int nb = 0; nb < NB8; ++nb) {
+    const uint4* p = reinterpret_cast<const uint4*>(a.x + (size_t)xrow(a, gid + 8 * nb) * a.ldx + g * kGroup + 8 * tig);
+    uint4 v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = __ldcg(p + 4 * q);          // k = 32q + 8tig .. +7
+    uint32_t m = max(max(absmax8(v[0]), absmax8(v[1])), max(absmax8(v[2]), absmax8(v[3])));
+    m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, 1));
+    m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, 2));
+    const int sig = prescale_sigma(m);                             // column gid + 8nb, group g
+    const float ps = pow2i(-sig);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t wv[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+#pragma unroll
+      for (int w2 = 0; w2 < 4; ++w2) {                             // k pair 32q + 8tig + 2w2 (+1)
+        const float c = __uint_as_float((uint32_t)(127 - step_fp(BITS, 2 * q + ((w2 >> 1) & 1), w2 & 1)) << 23);
+        const __half2 hv = __floats2half2_rn((bf16_bits_to_f32(wv[w2] & 0xFFFFu) * c) * ps,
+                                             (bf16_bits_to_f32(wv[w2] >> 16) * c) * ps);
+        xr[nb][4 * q + w2] = *reinterpret_cast<const uint32_t*>(&hv);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) fs[nb][h] = pow2i(__shfl_sync(0xFFFFFFFFu, sig, (2 * tig + h) * 4));
+  }
+}
+
 // One (row-block, group) record: tot[nb][e] += s_row · Σ_k (q − z)·x.
 // The A registers hold 2^fp·(q − z) (fp16, exact) and the B operand is x' = x·2^-fp (fp16), so every
 // product is exact and one mma chain accumulates Σ_k (q − z)·x_k in fp32.
 // XS: x' fragments come from shared memory (xrow_s[nb] = this lane's run start for the group).
 // The compute part of w_tile on a record already in registers (w = the lane's code words, sw = its
 // scales word, zz = the record's zeros).
-template <int BITS, int NB8, bool XS>
+// SIG: the B operand carries a per-(group, column) prescale 2^-σ; fs[nb][h] = 2^σ of output column
+// 2·tig + h + 8·nb multiplies the group's partial back (exact).
+template <int BITS, int NB8, bool XS, bool SIG = false>
 __device__ __forceinline__ void w_tile_regs(const uint32_t (&w)[2 * BITS], uint32_t sw, uint2 zz, int lane,
                                             const uint4* const (&xrow_s)[NB8], const uint32_t (&xr)[NB8][16],
-                                            float (&tot)[NB8][4]) {
+                                            float (&tot)[NB8][4], const float (&fs)[NB8][2]) {
   const int gid = lane >> 2;
   // fp16x2 (1024 + 2^fp·z) of rows gid / gid + 8 for each field exponent fp: subtracting it turns a
   // register into 2^fp·(q − z) exactly, so the mma accumulates Σ (q − z)·x with no large offset
@@ -262,16 +348,23 @@ __device__ __forceinline__ void w_tile_regs(const uint32_t (&w)[2 * BITS], uint3
               s1 = bf16_bits_to_f32(sw >> 16) * (1.f / (float)(1 << row_hi_shift(BITS)));
 #pragma unroll
   for (int nb = 0; nb < NB8; ++nb) {
-    tot[nb][0] = fmaf(s0, acc[nb][0], tot[nb][0]);
-    tot[nb][1] = fmaf(s0, acc[nb][1], tot[nb][1]);
-    tot[nb][2] = fmaf(s1, acc[nb][2], tot[nb][2]);
-    tot[nb][3] = fmaf(s1, acc[nb][3], tot[nb][3]);
+    if constexpr (SIG) {
+      tot[nb][0] = fmaf(s0 * fs[nb][0], acc[nb][0], tot[nb][0]);
+      tot[nb][1] = fmaf(s0 * fs[nb][1], acc[nb][1], tot[nb][1]);
+      tot[nb][2] = fmaf(s1 * fs[nb][0], acc[nb][2], tot[nb][2]);
+      tot[nb][3] = fmaf(s1 * fs[nb][1], acc[nb][3], tot[nb][3]);
+    } else {
+      tot[nb][0] = fmaf(s0, acc[nb][0], tot[nb][0]);
+      tot[nb][1] = fmaf(s0, acc[nb][1], tot[nb][1]);
+      tot[nb][2] = fmaf(s1, acc[nb][2], tot[nb][2]);
+      tot[nb][3] = fmaf(s1, acc[nb][3], tot[nb][3]);
+    }
   }
 }
 
-template <int BITS, int NB8, bool XS>
+template <int BITS, int NB8, bool XS, bool SIG = false>
 __device__ __forceinline__ void w_tile(const uint8_t* rec, int lane, const uint4* const (&xrow_s)[NB8],
-                                       const uint32_t (&xr)[NB8][16], float (&tot)[NB8][4]) {
+                                       const uint32_t (&xr)[NB8][16], float (&tot)[NB8][4], const float (&fs)[NB8][2]) {
   uint32_t w[2 * BITS];
 #pragma unroll
   for (int q = 0; q < (2 * BITS) / 4; ++q) {
@@ -285,7 +378,7 @@ __device__ __forceinline__ void w_tile(const uint8_t* rec, int lane, const uint4
   const int gid = lane >> 2;
   const uint32_t sw = *reinterpret_cast<const uint32_t*>(rec + scales_off(BITS) + 4 * gid);
   const uint2 zz = *reinterpret_cast<const uint2*>(rec + zeros_off(BITS));   // rows 0..7 | rows 8..15
-  w_tile_regs<BITS, NB8, XS>(w, sw, zz, lane, xrow_s, xr, tot);
+  w_tile_regs<BITS, NB8, XS, SIG>(w, sw, zz, lane, xrow_s, xr, tot, fs);
 }
 
 // Load the lane's part of one record (code words, scales word, zeros) from shared or global memory.
@@ -309,7 +402,8 @@ __device__ __forceinline__ void load_record(const uint8_t* rec, int lane, uint32
 // within the group; fp is the code-field exponent of that k's column pair (layout.h).  Shared by the
 // in-kernel staging pass (XS) and the x-prep kernel (global x').
 template <int BITS>
-__device__ __forceinline__ void xprime16(const uint4 (&in)[2], int part, uint4 (&out)[2]) {
+__device__ __forceinline__ void xprime16(const uint4 (&in)[2], int part, uint4 (&out)[2], int sig = 0) {
+  const float ps = pow2i(-sig);                                        // the group's prescale 2^-σ
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const uint32_t wv[4] = {in[h].x, in[h].y, in[h].z, in[h].w};
@@ -322,7 +416,7 @@ __device__ __forceinline__ void xprime16(const uint4 (&in)[2], int part, uint4 (
         const int k = part * 16 + h * 8 + 2 * e2 + hi;               // k within the group
         const int j = 2 * (k >> 5) + ((k >> 2) & 1), pr = (k >> 1) & 1;
         const float xv = bf16_bits_to_f32((wv[e2] >> (16 * hi)) & 0xFFFFu);
-        xp[hi] = xv * __uint_as_float((uint32_t)(127 - step_fp(BITS, j, pr)) << 23);
+        xp[hi] = (xv * __uint_as_float((uint32_t)(127 - step_fp(BITS, j, pr)) << 23)) * ps;
       }
       const __half2 hv = __floats2half2_rn(xp[0], xp[1]);
       ov[e2] = *reinterpret_cast<const uint32_t*>(&hv);
@@ -352,8 +446,12 @@ template <int BITS>
 __device__ __forceinline__ void write_xprime(const DArgs& a, int b, int n, uint16_t bits) {
   const int k = n - a.y16_lo, kk = k & (kGroup - 1);
   const int j = 2 * (kk >> 5) + ((kk >> 2) & 1), pr = (kk >> 1) & 1;
-  const float xv = bf16_bits_to_f32(bits) * __uint_as_float((uint32_t)(127 - step_fp(BITS, j, pr)) << 23);
+  const int fp = step_fp(BITS, j, pr);
+  const float xv = bf16_bits_to_f32(bits) * __uint_as_float((uint32_t)(127 - fp) << 23);
   a.y16[(size_t)b * (a.y16_hi - a.y16_lo) + k] = __half_as_ushort(__float2half_rn(xv));
+  // exact in fp16 iff zero or 2^-17 <= |x|·2^-fp < 2^16 (R20); otherwise flag the consumer's slow path
+  const int E = (int)((bits >> 7) & 0xFFu) - 127;
+  if ((bits & 0x7FFFu) != 0 && (E - fp < -17 || E - fp > 15) && a.y16_flag) *a.y16_flag = 1u;
 }
 
 }  // namespace

@@ -55,17 +55,40 @@ __device__ __forceinline__ float pow2f(int e) { return __uint_as_float((uint32_t
 // k = 4l .. 4l + 3 of one (group, batch row).
 __device__ __forceinline__ void x8_stage(const DArgs& a, uint8_t* x8, int g0, int g1, int lane) {
   const int tig = (lane >> 1) & 3, s = lane >> 3, h = lane & 1;
-  for (int p = g0 * a.B; p < g1 * a.B; ++p) {
+  constexpr int kPre = 8;                            // (group, batch row) pieces whose loads are in flight together
+  for (int p0 = g0 * a.B; p0 < g1 * a.B; p0 += kPre) {
+    // issue every load of the batch first: the staging is on the window's critical path and each load
+    // is an L2 round trip (the x of this window was just written by its producer)
+    uint2 rawv[kPre];
+#pragma unroll
+    for (int u = 0; u < kPre; ++u) {
+      const int p = min(p0 + u, g1 * a.B - 1), g = p / a.B, b = p - g * a.B;
+      rawv[u] = __ldcg(reinterpret_cast<const uint2*>(a.x + (size_t)b * a.ldx + g * kGroup + 4 * lane));
+    }
+#pragma unroll
+  for (int uu = 0; uu < kPre; ++uu) {
+    const int p = p0 + uu;
+    if (p >= g1 * a.B) break;
     const int g = p / a.B, b = p - g * a.B;
-    const uint2 raw = __ldcg(reinterpret_cast<const uint2*>(a.x + (size_t)b * a.ldx + g * kGroup + 4 * lane));
+    const uint2 raw = rawv[uu];
     const uint32_t hb[4] = {raw.x & 0xFFFFu, raw.x >> 16, raw.y & 0xFFFFu, raw.y >> 16};
     uint32_t m = 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) m = max(m, hb[i] & 0x7FFFu);
     m = __reduce_max_sync(0xFFFFFFFFu, m);
+#if HC_DEC_TRACE
+    if (uu == 0 && p0 == g0 * a.B && lane == 0 && (threadIdx.x >> 5) == 0) {
+      unsigned long long tt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+      if (g_dtrace) g_dtrace[((size_t)a.trace_slot * 512 + blockIdx.x) * 16 + 8] = tt;
+    }
+#endif
     // exponent of the group's largest |x|, clamped so that 2^(16p + e − 29) stays a normal float
-    // (groups below 2^-97 keep 29 bits of fixed point relative to 2^-97)
-    const int e = m == 0 ? 0 : max(max((int)(m >> 7), 1) - 127, -97);
+    // (groups below 2^-97 keep 29 bits of fixed point relative to 2^-97).  A non-finite x (inf / NaN
+    // bits, m >= 0x7F80) makes the group's scale NaN, so every output of the row is NaN (the float64
+    // product with an inf or NaN operand and a zero weight is NaN too).
+    const bool nonfinite = m >= 0x7F80u;
+    const int e = (m == 0 || nonfinite) ? 0 : max(max((int)(m >> 7), 1) - 127, -97);
     const int sh = 29 - e, sh1 = sh >> 1;
     const float p1 = pow2f(sh1), p2 = pow2f(sh - sh1);     // 2^(29 − e) in two exact steps
     uint32_t u[4];
@@ -89,9 +112,10 @@ __device__ __forceinline__ void x8_stage(const DArgs& a, uint8_t* x8, int g0, in
       const int pp = lane;
       int2 v;
       v.x = pp ? dsum[2] + 256 * dsum[3] : dsum[0] + 256 * dsum[1];
-      v.y = __float_as_int(pow2f(16 * pp + e - 29));
+      v.y = nonfinite ? 0x7FC00000 : __float_as_int(pow2f(16 * pp + e - 29));
       reinterpret_cast<int2*>(blk + 512 * a.B)[2 * b + pp] = v;
     }
+  }
   }
 }
 

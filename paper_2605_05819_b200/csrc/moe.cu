@@ -28,17 +28,17 @@ constexpr int kRouteThreads = 1024;
 // Single CTA: T <= 1024 tokens, E <= 256 experts, k <= 16.  Per-expert token bitmaps (order-free
 // atomicOr), per-expert counts and entry counts by one thread per expert, exclusive scans over the
 // experts (one warp, fixed order), then every (token, slot) finds its row by popcount.
-// Align (ties up) and the cap rule (R15) of the oracle, on an fp32 continuous rank
-__device__ __forceinline__ int dyn_rank(float rt, int cap, int k0) {
+// Align (ties up) and the cap rule (R15) of the oracle on the continuous rank
+// rt = (k·g)·r̃, which is EXACT in float64 (k <= 16: 5 bits, g and r̃ fp32: 24 bits each -> <= 53 bits), so
+// the integer decision is exact and equal to the oracle's.  Bounded for any finite or infinite rt: with
+// L = the largest level <= cap, an rt >= L aligns to a level >= L, which the cap maps to L.
+__device__ __forceinline__ int dyn_rank(double rt, int cap, int k0) {
+  int L = 0;
+  for (int v = 1 << k0; v <= cap && v <= (1 << 30); v *= 2) L = v;
+  if (!(rt < (double)L)) return L;                // rt >= L (also inf; NaN is rejected at the ABI)
   int lo = 0, hi = 1 << k0;
-  while (rt >= (float)hi) { lo = hi; hi *= 2; }
-  int r = (rt - (float)lo) < ((float)hi - rt) ? lo : hi;
-  if (r > cap) {
-    int lvl = 0;
-    for (int v = 1 << k0; v <= cap; v *= 2) lvl = v;
-    r = lvl;
-  }
-  return r;
+  while (rt >= (double)hi) { lo = hi; hi *= 2; }  // hi <= L <= 2^30: terminates
+  return (rt - (double)lo) < ((double)hi - rt) ? lo : hi;
 }
 
 __global__ void moe_route_kernel(const int32_t* __restrict__ idx, const float* __restrict__ gate, int T, int k, int E,
@@ -98,24 +98,26 @@ __global__ void moe_route_kernel(const int32_t* __restrict__ idx, const float* _
     rt.row_tok[row] = t;
     rt.tok_row[i] = row;
     if (dyn.row_rank) {
-      const float kg = (float)k * gate[i];                       // G = k·g (fp32, as the oracle)
+      const double kg = (double)k * (double)gate[i];             // G = k·g (exact in float64)
 #pragma unroll
       for (int sl = 0; sl < 3; ++sl)
-        dyn.row_rank[row * 3 + sl] = (uint8_t)min(255, dyn_rank(kg * dyn.rtilde[e * 3 + sl], dyn.caps[e * 3 + sl], dyn.k0));
+        dyn.row_rank[row * 3 + sl] = (uint16_t)dyn_rank(kg * (double)dyn.rtilde[e * 3 + sl], dyn.caps[e * 3 + sl], dyn.k0);
     }
   }
 }
 
 template <int BITS>
 __global__ void moe_prep_kernel(const uint16_t* __restrict__ x, int ldx, int K, int gather, MoERoute rt, int R_max,
-                                uint16_t* __restrict__ xg, uint16_t* __restrict__ x16) {
+                                uint16_t* __restrict__ xg, uint16_t* __restrict__ x16, float* __restrict__ xsig) {
   asm volatile("griddepcontrol.wait;" ::: "memory");                 // PDL: the previous launch's outputs
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // one thread per (row, 16-element part); the 8 parts of a (row, group) are 8 consecutive lanes (K/16 is
+  // a multiple of 8) and agree on the group's B-operand prescale σ (R20): 2^σ -> xsig[row][g]
   const int parts = K / 16;
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (long long)R_max * parts) return;
   const int r = (int)(i / parts), p = (int)(i % parts);
-  if (r >= *rt.n_rows) return;
+  if (r >= *rt.n_rows) return;                      // uniform per 8-lane group (a whole row)
   const int src = gather ? rt.row_tok[r] : r;
   const uint4* s = reinterpret_cast<const uint4*>(x + (size_t)src * ldx + p * 16);
   const uint4 in[2] = {s[0], s[1]};
@@ -123,10 +125,17 @@ __global__ void moe_prep_kernel(const uint16_t* __restrict__ x, int ldx, int K, 
     uint4* d = reinterpret_cast<uint4*>(xg + (size_t)r * K + p * 16);
     d[0] = in[0]; d[1] = in[1];
   }
+  const unsigned m8 = 0xFFu << (threadIdx.x & 24);
+  uint32_t m = max(absmax8(in[0]), absmax8(in[1]));
+  m = max(m, __shfl_xor_sync(m8, m, 1));
+  m = max(m, __shfl_xor_sync(m8, m, 2));
+  m = max(m, __shfl_xor_sync(m8, m, 4));
+  const int sig = prescale_sigma(m);
   uint4 out[2];
-  xprime16<BITS>(in, p & 7, out);                   // 16-element part p & 7 of group p / 8
+  xprime16<BITS>(in, p & 7, out, sig);              // 16-element part p & 7 of group p / 8
   uint4* d = reinterpret_cast<uint4*>(x16 + (size_t)r * K + p * 16);
   d[0] = out[0]; d[1] = out[1];
+  if ((p & 7) == 0) xsig[(size_t)r * (K / kGroup) + (p >> 3)] = pow2i(sig);
 }
 
 // one block of 8 warps per (entry, member, 16-rank chunk); warp w takes k-blocks [w·KB/8, (w+1)·KB/8)
@@ -202,7 +211,8 @@ __global__ void __launch_bounds__(256) moe_rank_proj_kernel(MoEWin w, MoERoute r
 // tokens); else every warp owns whole items (many items).
 template <int BITS, int NB8, bool KS>
 __global__ void __launch_bounds__(128) moe_gemv_warp_kernel(MoEWin w, MoERoute rt, const uint16_t* __restrict__ x16,
-                                                           const float* __restrict__ t, void* out) {
+                                                           const float* __restrict__ xsig, const float* __restrict__ t,
+                                                           void* out) {
   asm volatile("griddepcontrol.wait;" ::: "memory");                 // PDL: the previous launch's outputs
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // one (entry, row block) item per CTA; its K groups split over the 4 warps (each warp keeps one
@@ -251,7 +261,15 @@ __global__ void __launch_bounds__(128) moe_gemv_warp_kernel(MoEWin w, MoERoute r
         }
       }
       const uint4* unused[NB8] = {};
-      w_tile_regs<BITS, NB8, false>(wc, swc, zzc, lane, unused, xr, tot);
+      float fs[NB8][2];                               // 2^σ of the lane's output columns (rows of this entry)
+#pragma unroll
+      for (int nb = 0; nb < NB8; ++nb)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = 2 * tig + h + 8 * nb;
+          fs[nb][h] = __ldg(xsig + (size_t)(row0 + (col < ncol ? col : 0)) * w.G + g);
+        }
+      w_tile_regs<BITS, NB8, false, true>(wc, swc, zzc, lane, unused, xr, tot, fs);
     }
     if constexpr (KS) {
 #pragma unroll
@@ -386,13 +404,13 @@ cudaError_t moe_route(const int32_t* topk_idx, const float* topk_gate, int T, in
 }
 
 cudaError_t moe_prep(const uint16_t* x, int ldx, int K, int bits, int gather, const MoERoute& rt, int R_max,
-                     uint16_t* xg, uint16_t* x16, cudaStream_t st) {
+                     uint16_t* xg, uint16_t* x16, float* xsig, cudaStream_t st) {
   const long long n = (long long)R_max * (K / 16);
   const unsigned grid = (unsigned)((n + 255) / 256);
   switch (bits) {
-    case 2: if (cudaError_t e = launch_pdl(moe_prep_kernel<2>, grid, 256, 0, st, x, ldx, K, gather, rt, R_max, xg, x16)) return e; break;
-    case 3: if (cudaError_t e = launch_pdl(moe_prep_kernel<3>, grid, 256, 0, st, x, ldx, K, gather, rt, R_max, xg, x16)) return e; break;
-    case 4: if (cudaError_t e = launch_pdl(moe_prep_kernel<4>, grid, 256, 0, st, x, ldx, K, gather, rt, R_max, xg, x16)) return e; break;
+    case 2: if (cudaError_t e = launch_pdl(moe_prep_kernel<2>, grid, 256, 0, st, x, ldx, K, gather, rt, R_max, xg, x16, xsig)) return e; break;
+    case 3: if (cudaError_t e = launch_pdl(moe_prep_kernel<3>, grid, 256, 0, st, x, ldx, K, gather, rt, R_max, xg, x16, xsig)) return e; break;
+    case 4: if (cudaError_t e = launch_pdl(moe_prep_kernel<4>, grid, 256, 0, st, x, ldx, K, gather, rt, R_max, xg, x16, xsig)) return e; break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -408,7 +426,7 @@ cudaError_t moe_rank_proj(const MoEWin& w, const MoERoute& rt, int max_ent, cons
 }
 
 cudaError_t moe_gemv(const MoEWin& w, int bits, const MoERoute& rt, int max_ent, const uint16_t* x16,
-                     const float* t, void* out, int max_cols, cudaStream_t st) {
+                     const float* xsig, const float* t, void* out, int max_cols, cudaStream_t st) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -421,11 +439,11 @@ cudaError_t moe_gemv(const MoEWin& w, int bits, const MoERoute& rt, int max_ent,
   cudaError_t e = cudaSuccess;
 #define HC_MOE_LAUNCH(B_)                                                                                       \
   if (ks) {                                                                                                     \
-    if (one) e = launch_pdl(moe_gemv_warp_kernel<B_, 1, true>, grid, 128, 0, st, w, rt, x16, t, out);                       \
-    else     e = launch_pdl(moe_gemv_warp_kernel<B_, 2, true>, grid, 128, 0, st, w, rt, x16, t, out);                       \
+    if (one) e = launch_pdl(moe_gemv_warp_kernel<B_, 1, true>, grid, 128, 0, st, w, rt, x16, xsig, t, out);                       \
+    else     e = launch_pdl(moe_gemv_warp_kernel<B_, 2, true>, grid, 128, 0, st, w, rt, x16, xsig, t, out);                       \
   } else {                                                                                                      \
-    if (one) e = launch_pdl(moe_gemv_warp_kernel<B_, 1, false>, grid, 128, 0, st, w, rt, x16, t, out);                      \
-    else     e = launch_pdl(moe_gemv_warp_kernel<B_, 2, false>, grid, 128, 0, st, w, rt, x16, t, out);                      \
+    if (one) e = launch_pdl(moe_gemv_warp_kernel<B_, 1, false>, grid, 128, 0, st, w, rt, x16, xsig, t, out);                      \
+    else     e = launch_pdl(moe_gemv_warp_kernel<B_, 2, false>, grid, 128, 0, st, w, rt, x16, xsig, t, out);                      \
   }
   switch (bits) {
     case 2: HC_MOE_LAUNCH(2) break;

@@ -32,17 +32,18 @@ struct MoEWin {
   const MoEExpert* ex;      // [E] device
   int n_rb, K, G, glue;     // per expert: row blocks, input width; glue = fused SiLU(gate)·up (UPGATE)
   int t_ld;                 // floats per row of the t buffer (= 2 · max rank chunk · 16)
-  const uint8_t* row_rank;  // dynamic ranks [R][3] (up, gate, down) per routed row, or NULL (static ranks)
+  const uint16_t* row_rank; // dynamic ranks [R][3] (up, gate, down) per routed row, or NULL (static ranks)
   int rank_slot0;           // slot of member 0 in row_rank: 0 (UPGATE: up, gate), 2 (DOWN)
 };
 
 // Dynamic per-(token, expert) ranks: r = Cap(Align((k·g)·r̃[e][s])), decided in
-// fp32; rtilde / caps are [E][3] (up, gate, down), k0 the smallest nonzero level exponent.
+// float64 (exact for fp32 g and r̃); rtilde / caps are [E][3] (up, gate, down), k0 the smallest nonzero
+// level exponent.
 struct MoEDyn {
   const float* rtilde;
   const int* caps;
   int k0;
-  uint8_t* row_rank;        // out: [R][3]
+  uint16_t* row_rank;       // out: [R][3]
 };
 
 // Route: group (token, slot) pairs by expert (deterministic order), build entries of <= 16 rows.
@@ -50,8 +51,9 @@ cudaError_t moe_route(const int32_t* topk_idx, const float* topk_gate, int T, in
                       const MoEDyn* dyn, cudaStream_t st);
 // x rows of every routed (token, expert) row: xg = x[row_tok] (bf16) and x16 = x'(bits) (fp16).
 // gather == 0: the rows are x itself (row r = row r, used for the DOWN input m).
+// xsig: [R][K/128] the per-(row, group) factors 2^σ of the x' prescale (R20).
 cudaError_t moe_prep(const uint16_t* x, int ldx, int K, int bits, int gather, const MoERoute& rt, int R_max,
-                     uint16_t* xg, uint16_t* x16, cudaStream_t st);
+                     uint16_t* xg, uint16_t* x16, float* xsig, cudaStream_t st);
 // t[row][m][rank] = V_m·x_row for every row of every entry (members m < 1 + glue), fp32.
 cudaError_t moe_rank_proj(const MoEWin& w, const MoERoute& rt, int max_ent, const uint16_t* xg, float* t,
                           cudaStream_t st);
@@ -59,7 +61,7 @@ cudaError_t moe_rank_proj(const MoEWin& w, const MoERoute& rt, int max_ent, cons
 // else out = fp32 [R][n_rb·16].
 // max_cols: an upper bound on the rows of an entry (min(T, 16)): <= 8 selects the 8-column mma variant.
 cudaError_t moe_gemv(const MoEWin& w, int bits, const MoERoute& rt, int max_ent, const uint16_t* x16,
-                     const float* t, void* out, int max_cols, cudaStream_t st);
+                     const float* xsig, const float* t, void* out, int max_cols, cudaStream_t st);
 // y[t][n] = Σ_j g[t][j] · dout[tok_row[t][j]][n]   (fixed slot order)
 cudaError_t moe_combine(const float* dout, int N, const float* topk_gate, int T, int k, const MoERoute& rt,
                         float* y, cudaStream_t st);

@@ -310,6 +310,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         const int n = tw.n0 + c0;
         if (m < p.M && n < p.N) {
+          if (p.rsig) {                                // the row's X prescale (exact power of two, R20)
+            const float rs = __ldg(p.rsig + m);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * rs);
+          }
           if (p.out_type == 0) {
             float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(outp) + (size_t)m * p.ldo + n);
 #pragma unroll
@@ -437,6 +442,55 @@ __global__ void bf16_to_f16_kernel(const uint16_t* __restrict__ in, uint16_t* __
   } else {
     for (size_t j = i; j < n; ++j) out[j] = __half_as_ushort(__float2half_rn(__uint_as_float((uint32_t)in[j] << 16)));
   }
+}
+
+// X (bf16 [M][K]) -> X' = X·2^-σ_m (fp16), one CTA per token row m, and rsig[m] = 2^σ_m (R20,
+// prefill form: one power of two per row, because the tcgen05 accumulator spans all of K).  σ_m = 0 when
+// the row's largest |x| has exponent E in [-2, 13] (exactly the plain conversion), else E - 8 (clamped to
+// [-100, 115]): X' then holds every bf16 x within 2^25 of the row maximum exactly, for any bf16 range.
+// The T = X'·Vᵀ slice is in the same scaled units, so the epilogue's factor 2^σ_m restores the whole row.
+__global__ void __launch_bounds__(256) x_rows_f16_kernel(const uint16_t* __restrict__ in, int K, uint16_t* __restrict__ out,
+                                                         float* __restrict__ rsig) {
+  __shared__ uint32_t wmax[8];
+  const int m = blockIdx.x;
+  const uint16_t* row = in + (size_t)m * K;
+  uint32_t mx = 0;
+  for (int i = threadIdx.x * 8; i < K; i += 256 * 8) {
+    const uint4 v = *reinterpret_cast<const uint4*>(row + i);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) mx = max(mx, max(w[j] & 0x7FFFu, (w[j] >> 16) & 0x7FFFu));
+  }
+  mx = __reduce_max_sync(0xFFFFFFFFu, mx);
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) mx = max(mx, wmax[w]);
+  int sig = 0;
+  if (mx != 0 && mx < 0x7F80u) {
+    const int E = max((int)(mx >> 7), 1) - 127;
+    if (E < -2 || E > 13) sig = min(max(E - 8, -100), 115);
+  }
+  const float ps = __uint_as_float((uint32_t)(127 - sig) << 23);
+  for (int i = threadIdx.x * 8; i < K; i += 256 * 8) {
+    const uint4 v = *reinterpret_cast<const uint4*>(row + i);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      __half2 h = __floats2half2_rn(__uint_as_float(w[j] << 16) * ps, __uint_as_float(w[j] & 0xFFFF0000u) * ps);
+      o[j] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    *reinterpret_cast<uint4*>(out + (size_t)m * K + i) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+  if (threadIdx.x == 0) rsig[m] = __uint_as_float((uint32_t)(127 + sig) << 23);
+}
+
+cudaError_t launch_x_rows_f16(const uint16_t* in, int M, int K, uint16_t* out, float* rsig, cudaStream_t st) {
+  if (K % 8) return cudaErrorInvalidValue;
+  x_rows_f16_kernel<<<M, 256, 0, st>>>(in, K, out, rsig);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_bf16_to_f16(const uint16_t* in, uint16_t* out, size_t n, cudaStream_t st) {

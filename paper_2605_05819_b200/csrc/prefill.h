@@ -24,6 +24,7 @@ struct PArgs {
   int ldo;                  // row stride of out (elements)
   int out_type;             // 0 fp32, 1 bf16, 2 fp16
   int tiles_m, tiles_n;
+  const float* rsig;        // optional [M] per-row factors 2^σ_m of the X prescale (launch_x_rows_f16), else NULL
 };
 
 // tmC: 2-D u32 tensor map over the nibble-paired codes [N][K/8] (box 8 words x 256 rows), b_mode 0.
@@ -36,6 +37,8 @@ bool encode_tmap_codes(CUtensorMap* map, const void* base, uint64_t words_per_ro
 cudaError_t launch_transpose_groups(const uint16_t* s_in, const uint8_t* z_in, int rows, int G, uint16_t* s_out,
                                     uint8_t* z_out, cudaStream_t st);
 
+// X bf16 [M][K] -> fp16 X' = X·2^-σ_m with a per-row power-of-two prescale; rsig[m] = 2^σ_m
+cudaError_t launch_x_rows_f16(const uint16_t* in, int M, int K, uint16_t* out, float* rsig, cudaStream_t st);
 // bf16 [n] -> fp16 [n]
 cudaError_t launch_bf16_to_f16(const uint16_t* in, uint16_t* out, size_t n, cudaStream_t st);
 // canonical 4-bit codes [rows][K/8] -> prefill nibble order (word w: nibbles k0,k2,k4,k6,k1,k3,k5,k7)

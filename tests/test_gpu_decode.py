@@ -180,3 +180,86 @@ def test_int8_path_edge_cases(hc, ctx, bits, zeros, B, K):
         assert np.all(np.isfinite(y))
         assert rel_err(y, ref) <= 1e-5, (r, rel_err(y, ref))
         assert np.array_equal(y, run(hc, ctx, L, case["x"], 272))
+
+
+def _range_x(seed, B, K, kind):
+    """bf16 x outside fp16's exact band (R20): all-zero rows, tiny rows (~1e-12, far below
+    fp16's 2^-14), rows with outliers >= 65504 (up to 1e6), and a wide mix (each 128-group at its own
+    scale 1e-12 .. 1e7, elements spread a further 1e±3 inside the group)."""
+    g = np.random.default_rng(seed)
+    if kind == "zero":
+        x = np.zeros((B, K))
+    elif kind == "tiny":
+        x = g.standard_normal((B, K)) * 1e-12
+    elif kind == "outlier":
+        x = g.standard_normal((B, K))
+        x[:, 5] = 7.0e4
+        x[:, K // 3] = -2.5e5
+        x[:, K - 3] = 1.0e6
+    else:
+        gs = 10.0 ** g.uniform(-12, 7, (B, K // 128, 1))
+        x = (g.standard_normal((B, K // 128, 128)) * gs * 10.0 ** g.uniform(-3, 3, (B, K // 128, 128))).reshape(B, K)
+    return f64_to_bf16_bits_rne(x)
+
+
+def row_rel(y, ref):
+    """max over batch rows of max|y_b - y*_b| / max|y*_b| (each row judged at its own scale)."""
+    return max(np.abs(y[b] - ref[b]).max() / np.abs(ref[b]).max() for b in range(ref.shape[0]))
+
+
+@pytest.mark.parametrize("bits,B,K", [(3, 4, 1408), (3, 16, 1408), (4, 4, 11008), (4, 16, 11008), (2, 8, 1408),
+                                      (3, 1, 2560), (4, 1, 11008)])
+@pytest.mark.parametrize("kind", ["zero", "tiny", "outlier", "wide"])
+def test_fp16_path_full_bf16_range(hc, ctx, bits, B, K, kind):
+    """The fp16 mma path (3-bit; B > 2; K = 11008 DOWN-shaped at B = 1, 4, 16; both the shared-memory
+    staged x' and the x-prep kernel) accepts any bf16 x: per-(group, row) power-of-two prescale of x'
+    (R20) and the two-word t accumulators (R22).  Each batch row within 1e-5 of the float64 oracle at its
+    own scale; an all-zero x gives exactly zero."""
+    case = synth.linear_case(900 + 7 * bits + B, N=272, K=K, bits=bits, r_stored=32, B=B, zeros="asym")
+    case["x"] = _range_x(K + B + len(kind), B, K, kind)
+    L = next_layer()
+    for r in (0, 32):
+        load(ctx, case, L, r=r)
+        y = run(hc, ctx, L, case["x"], 272)
+        assert np.all(np.isfinite(y))
+        if kind == "zero":
+            assert np.all(y == 0.0)
+            continue
+        ref = linear.compensated_linear(case, r)
+        assert row_rel(y, ref) <= 1e-5, (r, row_rel(y, ref))
+        assert np.array_equal(y, run(hc, ctx, L, case["x"], 272))
+
+
+@pytest.mark.parametrize("bits,B", [(4, 1), (4, 2), (3, 4), (4, 16)])
+def test_nonfinite_x_propagates(hc, ctx, bits, B):
+    """A non-finite activation makes its batch row non-finite (as in float64, where inf·0 is NaN) on the
+    int8 path (B <= 2) and the fp16 path; the other rows are unaffected."""
+    case = synth.linear_case(950 + bits + B, N=144, K=1024, bits=bits, r_stored=16, B=B, zeros="asym")
+    xb = case["x"].copy()
+    xb[0, 300] = 0x7F80                      # +inf
+    if B > 1:
+        xb[B - 1, 17] = 0x7FC0               # NaN
+    L = next_layer()
+    load(ctx, case, L, r=16)
+    y = run(hc, ctx, L, xb, 144)
+    ref = linear.compensated_linear(case, 16, x_bits=xb)
+    assert np.all(~np.isfinite(y[0])) and np.all(~np.isfinite(ref[0]))
+    if B > 1:
+        assert np.all(~np.isfinite(y[B - 1]))
+    for b in range(1, B - 1):
+        assert np.abs(y[b] - ref[b]).max() <= 1e-5 * np.abs(ref[b]).max()
+
+
+@pytest.mark.parametrize("bits,B", [(4, 1), (2, 2), (4, 4), (3, 9)])
+@pytest.mark.parametrize("r", [128, 256])
+def test_high_rank_parity(hc, ctx, bits, B, r):
+    """Ranks 128 and 256 (the largest admissible level): U chunks beyond the shared-memory prefetch are
+    read from global memory; 16 rank chunks in the t accumulators."""
+    case = synth.linear_case(970 + bits * 3 + B, N=288, K=1280, bits=bits, r_stored=256, B=B, zeros="asym")
+    L = next_layer()
+    load(ctx, case, L, r=r)
+    y = run(hc, ctx, L, case["x"], 288)
+    ref = linear.compensated_linear(case, r)
+    assert rel_err(y, ref) <= 1e-5, rel_err(y, ref)
+    ref_low = linear.compensated_linear(case, r // 2)
+    assert rel_err(y, ref_low) > 10 * rel_err(y, ref)      # the top half of the ranks is really used

@@ -131,3 +131,53 @@ def test_prefill_merged_window_matches_per_member(hc, ctx, monkeypatch):
     ctx.compensated_linear(L, 0, dev(cases[0]["x"]), y)
     torch.cuda.synchronize()
     assert rel(y.cpu().numpy(), linear.window_linear(cases, [8, 16, 32], cases[0]["x"])) <= TOL
+
+
+@pytest.mark.parametrize("kind", ["zero", "tiny", "outlier", "wide"])
+def test_prefill_full_bf16_range(hc, ctx, kind):
+    """Prefill (tcgen05) with activations outside fp16's exact band: the per-token power-of-two prescale
+    of X (R20) keeps every row within the bar at its own scale; an all-zero X gives exactly zero."""
+    M, N, K = 200, 512, 1024
+    case = synth.linear_case(1200 + len(kind), N=N, K=K, bits=4, r_stored=64, B=M, zeros="asym")
+    g = np.random.default_rng(len(kind))
+    if kind == "zero":
+        x = np.zeros((M, K))
+    elif kind == "tiny":
+        x = g.standard_normal((M, K)) * 1e-12
+    elif kind == "outlier":
+        x = g.standard_normal((M, K))
+        x[:, 7] = 7.0e4
+        x[::3, 500] = -3.0e5
+        x[::5, 900] = 2.0e6
+    else:
+        x = g.standard_normal((M, K)) * 10.0 ** g.uniform(-12, 7, (M, 1)) * 10.0 ** g.uniform(-2, 2, (M, K))
+    case["x"] = f64_to_bf16_bits_rne(x)
+    L = nl()
+    for r in (0, 64):
+        ctx.load_layer([desc(case, L, 0, 0, r)])
+        y = torch.empty((M, N), dtype=torch.float32, device="cuda")
+        ctx.compensated_linear(L, 0, dev(case["x"]), y)
+        torch.cuda.synchronize()
+        y = y.cpu().numpy()
+        assert np.all(np.isfinite(y))
+        if kind == "zero":
+            assert np.all(y == 0.0)
+            continue
+        ref = linear.compensated_linear(case, r)
+        worst = max(np.abs(y[m] - ref[m]).max() / np.abs(ref[m]).max() for m in range(M))
+        assert worst <= TOL, (r, worst)
+
+
+@pytest.mark.parametrize("r", [128, 256])
+def test_prefill_high_rank(hc, ctx, r):
+    """Rank 128 and 256 (C4's rank sweep reaches 256): the rank slice is a 256-wide K extension."""
+    M, N, K = 160, 512, 1024
+    case = synth.linear_case(1300 + r, N=N, K=K, bits=4, r_stored=256, B=M, zeros="asym")
+    L = nl()
+    ctx.load_layer([desc(case, L, 0, 0, r)])
+    y = torch.empty((M, N), dtype=torch.float32, device="cuda")
+    ctx.compensated_linear(L, 0, dev(case["x"]), y)
+    torch.cuda.synchronize()
+    ref = linear.compensated_linear(case, r)
+    assert rel(y.cpu().numpy(), ref) <= TOL
+    assert rel(y.cpu().numpy(), linear.compensated_linear(case, r // 2)) > 3 * rel(y.cpu().numpy(), ref)

@@ -134,8 +134,6 @@ def test_stack_forward_parity(hc, bits, B):
         h = hl
     assert np.array_equal(h, yb)                                   # graph == chain of layers
     assert exact >= 0.98 * L * B * d                                # rounding flips are rare
-    ok, rel = stack_close(yb, linear.stack_forward(layers, ranks, x), n_layers=L)
-    assert ok, rel
     # host buffers through the public API
     yh = np.zeros((B, d), dtype=np.uint16)
     ctx.stack_forward(np.ascontiguousarray(x), yh)
@@ -198,27 +196,37 @@ def test_stack_nccl_path_single_rank_matches(hc):
     plain.close()
 
 
-@pytest.mark.parametrize("bits,B", [(4, 8), (3, 2), (4, 3)])
-def test_persistent_stack_matches_per_window_path(hc, bits, B, monkeypatch):
-    """The persistent stack kernel (default for B <= 8) and the per-window launch graph
-    (HC_STACK_KERNEL=0) both meet the per-layer oracle bound; they differ only in the fp32
-    summation order of the K-split partials (16 vs 8 warps)."""
-    L, d, kv, f = 2, 512, 256, 768
-    layers, ranks = make_stack(L, d, kv, f, bits, 32, seed=500 + bits * 10 + B)
-    x = synth.activations(11 + B, B, d)
-    out = {}
-    for mode in ("1", "0"):
-        monkeypatch.setenv("HC_STACK_KERNEL", mode)
-        ctx = hc.Context(0)
-        load_stack(hc, ctx, layers, ranks)
-        y = torch.empty((B, d), dtype=torch.int16, device="cuda")
-        for _ in range(3):                                          # replays: counters / t reset
-            ctx.stack_forward(dev(x), y)
+
+@pytest.mark.parametrize("bits,B,scale", [(3, 4, 1e5), (3, 4, 1e-9), (4, 16, 3e4), (4, 1, 2e5)])
+def test_stack_full_bf16_range(hc, bits, B, scale):
+    """Stack windows hand x' (fp16) to the next window; when an activation leaves fp16's exact band the
+    producer flags it and the consumer converts x itself with a per-group prescale (R20).  Each layer
+    against the oracle fed the kernel's own bf16 input; graph == chain of layers."""
+    # no normalisation layer is modelled, so large activations grow quadratically through SiLU(gate)·up:
+    # one layer at the large scales keeps t = V·x inside the accumulators' range (|t| < 2^35, R22)
+    L, d, kv, f = (1 if scale > 1 else 2), 256, 128, 512
+    layers, ranks = make_stack(L, d, kv, f, bits, 32, seed=bits * 7 + B)
+    ctx = hc.Context(0)
+    load_stack(hc, ctx, layers, ranks)
+    g = np.random.default_rng(B)
+    x = f64_to_bf16_bits_rne(g.standard_normal((B, d)) * scale)
+    y = torch.empty((B, d), dtype=torch.int16, device="cuda")
+    ctx.stack_forward(dev(x), y)
+    torch.cuda.synchronize()
+    yb = y.cpu().numpy().view(np.uint16)
+    h = x
+    for l in range(L):
+        c1 = one_layer_ctx(hc, layers, ranks, l)
+        yl = torch.empty((B, d), dtype=torch.int16, device="cuda")
+        c1.stack_forward(dev(h), yl)
         torch.cuda.synchronize()
-        out[mode] = y.cpu().numpy().view(np.uint16).copy()
-        ctx.close()
-    ref = linear.stack_forward(layers, ranks, x)
-    for mode, yb in out.items():
-        ok, rel = stack_close(yb, ref, n_layers=L)
-        assert ok, (mode, rel)
-    assert np.mean(out["1"] == out["0"]) >= 0.98
+        hl = yl.cpu().numpy().view(np.uint16).copy()
+        ref = linear.stack_forward([layers[l]], [ranks[l]], h)
+        assert np.all(np.isfinite(bf16_to_f64(hl)))
+        for b in range(B):
+            ok, rel = stack_close(hl[b:b + 1], ref[b:b + 1])
+            assert ok, (l, b, rel)
+        c1.close()
+        h = hl
+    assert np.array_equal(h, yb)
+    ctx.close()

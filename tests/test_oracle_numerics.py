@@ -206,8 +206,48 @@ def test_round_bf16_matches_fp32_route():
     assert linear.round_bf16(np.array([1.0 + 3 * 2.0 ** -8]))[0] == 1.0 + 2.0 ** -6
 
 
+def _silu_ref(v):
+    # independent SiLU: v·σ(v) with the library logistic (scipy.special.expit), not oracle.linear.silu
+    from scipy.special import expit
+    return np.asarray(v, np.float64) * expit(np.asarray(v, np.float64))
+
+
+def test_silu_closed_forms():
+    # SiLU(v) = v·σ(v) ("σ(W_gate X)", SPEC's σ = SiLU): closed forms that catch a dropped term,
+    # a sign flip or a wrong exponent.  σ(ln 3) = 3/4, σ(-ln 3) = 1/4; silu(v) - silu(-v) = v (σ(v) +
+    # σ(-v) = 1); silu(0) = 0, silu(h) = h/2 + h²/4 + O(h⁴); silu(v) -> v for large v and -> 0 for very negative v.
+    L3 = np.log(3.0)
+    assert linear.silu(np.array([0.0]))[0] == 0.0
+    assert abs(linear.silu(np.array([L3]))[0] - 0.75 * L3) <= 1e-15
+    assert abs(linear.silu(np.array([-L3]))[0] + 0.25 * L3) <= 1e-15
+    v = synth.rng(77).standard_normal(1000) * 6
+    assert np.abs(linear.silu(v) - linear.silu(-v) - v).max() <= 1e-13
+    assert abs(linear.silu(np.array([1e-8]))[0] - (0.5e-8 + 0.25e-16)) <= 1e-23     # h/2 + h²/4 + O(h⁴)
+    assert abs(linear.silu(np.array([40.0]))[0] - 40.0) <= 1e-14 * 40 and abs(linear.silu(np.array([-40.0]))[0]) < 1e-15
+    assert np.abs(linear.silu(v) - _silu_ref(v)).max() <= 1e-14
+
+
+def test_window_linear_member_order_and_widths():
+    # App. A.1.3: members sharing x run as one window; the output is the concatenation of the
+    # members' compensated products in member order, each at its own rank and width.  Checked column block
+    # by column block against the element-by-element brute force (_brute_linear, independent of oracle code).
+    cases = [synth.linear_case(60 + i, N=n, K=256, bits=b, r_stored=16, B=2, zeros="asym")
+             for i, (n, b) in enumerate(((6, 4), (2, 4), (4, 4)))]
+    x = cases[0]["x"]
+    for c in cases:
+        c["x"] = x
+    ranks = [8, 0, 16]
+    y = linear.window_linear(cases, ranks, x)
+    assert y.shape == (2, 12)
+    off = 0
+    for c, r in zip(cases, ranks):
+        yb = _brute_linear(c, r)
+        assert np.abs(y[:, off:off + c["N"]] - yb).max() <= 1e-12 * max(1.0, np.abs(yb).max())
+        off += c["N"]
+
+
 def test_moe_single_expert_equals_dense():
-    # SPEC toymodel example: MoE with one expert, g = 1 == dense FFN
+    # SPEC toymodel example: MoE with one expert, g = 1 == dense FFN (SiLU from the library logistic)
     d, f = 128, 128
     up = synth.linear_case(20, f, d, 3, 128, 16, 1, "asym")
     gate = synth.linear_case(21, f, d, 3, 128, 16, 1, "asym")
@@ -216,8 +256,8 @@ def test_moe_single_expert_equals_dense():
     y = linear.moe_forward([dict(up=up, gate=gate, down=down)], [dict(up=8, gate=0, down=16)],
                            x, np.zeros((5, 1), np.int32), np.ones((5, 1), np.float32))
     xf = packing.bf16_to_f64(x)
-    m = linear.round_bf16(linear.silu(linear._lin(gate, 0, xf)) * linear._lin(up, 8, xf))
-    assert np.array_equal(y, linear._lin(down, 16, m))
+    m = linear.round_bf16(_silu_ref(linear._lin(gate, 0, xf)) * linear._lin(up, 8, xf))
+    assert np.allclose(y, linear._lin(down, 16, m), rtol=0, atol=1e-12 * np.abs(y).max())
 
 
 def test_moe_gate_linearity_two_identical_experts():
@@ -247,6 +287,42 @@ def test_dynamic_rank_rule_worked_examples():
     assert linear.dynamic_rank(8, 0.01, 40.0, 64) == 0           # 3.2 < 4 -> 0
     assert linear.dynamic_rank(4, 0.5, 3.0, 64) == 8             # 6 -> nearest of {0, 8}: 8
     assert linear.dynamic_rank(1, 1.0, 300.0, 48) == 32          # 256 aligned, cap 48 -> 32
+
+
+# (k, g, r̃, exact rank, what an fp32 product would give): the exact product sits just below an Align
+# midpoint (48, 96, 12) while its fp32 rounding lands ON the midpoint and ties up (found by search)
+DYN_EXACT_CASES = [(9, 0.7322015762329102, 7.283968448638916, 32, 64),
+                   (5, 0.012711115181446075, 1510.489013671875, 64, 128),
+                   (2, 0.42846035957336426, 14.003628730773926, 8, 16)]
+
+
+def _align_exact(rt, k0=3):
+    from fractions import Fraction
+    lo, hi = Fraction(0), Fraction(1 << k0)
+    while rt >= hi:
+        lo, hi = hi, hi * 2
+    return int(lo) if (rt - lo) < (hi - rt) else int(hi)
+
+
+def test_dynamic_rank_is_exact_arithmetic():
+    # R21: (k·g)·r̃ is exact in float64 for fp32 g, r̃ and k <= 16, so the decision equals the one taken
+    # in exact rational arithmetic (fractions.Fraction); an fp32 product would flip these ties
+    from fractions import Fraction
+    for k, g, rt, exact, f32 in DYN_EXACT_CASES:
+        assert np.float32(g) == g and np.float32(rt) == rt
+        assert linear.dynamic_rank(k, np.float32(g), np.float32(rt), 256) == exact
+        assert _align_exact(Fraction(float(np.float32(np.float32(k) * np.float32(g)) * np.float32(rt)))) == f32
+    r = synth.rng(78)
+    for _ in range(3000):
+        k = int(r.integers(1, 17))
+        g = np.float32(r.uniform(0, 1))
+        rt = np.float32(r.uniform(0, 300))
+        ex = Fraction(k) * Fraction(float(g)) * Fraction(float(rt))
+        assert float(k) * float(g) * float(rt) == ex                       # no rounding in float64
+        cap = int(r.choice([0, 8, 16, 48, 64, 256]))
+        lv = _align_exact(ex)
+        want = lv if lv <= cap else max([0] + [v for v in (8, 16, 32, 64, 128, 256) if v <= cap])
+        assert linear.dynamic_rank(k, g, rt, cap) == want
 
 
 def test_moe_dynamic_reduces_to_static_and_zero():
