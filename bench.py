@@ -101,10 +101,11 @@ def c1_bytes(c=C1):
 def dtype_of(args, config):
     """The arithmetic the timed path computes in: int8 mma for 2/4-bit decode at
     B <= 2 (codes x s8 digits of x, exact int32), else fp16 mma on exact dequantised integers."""
+    import paper_2605_05819_b200 as hc
     bits = config.get("bits", 4)
     if args.workload == "c4":
         return f"fp16 tcgen05 (s·(q−z) of int{bits}, bf16 X as fp16), fp32 accumulate"
-    if bits in (2, 4) and args.batch <= 2 and os.environ.get("HC_I8", "1") != "0" and args.workload != "c3":
+    if bits in (2, 4) and args.batch <= 2 and hc.get_option("int8_path") != 0 and args.workload != "c3":
         return f"int8 mma (u{bits} codes x s8 digits of bf16 x, exact int32), fp32 per-group accumulate"
     return f"fp16 mma (exact int{bits} dequant x fp16 x), fp32 accumulate"
 

@@ -207,6 +207,19 @@ hc_status hc_moe_last_ranks(hc_ctx* ctx, int32_t* out, int32_t T, int32_t topk);
 hc_status hc_nccl_unique_id(uint8_t* out128);
 hc_status hc_set_comm(hc_ctx* ctx, const uint8_t* id128, int32_t rank, int32_t world);
 
+/* Process-wide development switches, for A/B timing of equivalent plans (every setting computes the same
+ * product up to fp32 accumulation order; the parity tests pass under each).  Read when a window plan or a
+ * stack graph is built; setting one makes contexts re-capture their stack graphs on the next call.
+ *   "t_forward"          0  stack: window w-1's epilogue accumulates window w's t = V·x
+ *   "x_handoff"          1  stack: the producer epilogue writes the next fp16-path window's x' (§7.1)
+ *   "dep_wait"           1  stack: wait on the producer window's counter, not the kernel boundary (§7.1)
+ *   "int8_path"          1  decode: u8·s8 tensor-core path for 2-/4-bit codes at B <= 2 (§7.1)
+ *   "prefill_merge"      1  prefill: one GEMM over a multi-member window (§7.5)
+ *   "decode_ctas_per_sm" 0  decode: cap on resident CTAs per SM (0 = the occupancy limit)
+ * HC_ERR_CONFIG for an unknown name or a negative value.  Not thread-safe against concurrent launches. */
+hc_status hc_set_option(const char* name, int32_t value);
+hc_status hc_get_option(const char* name, int32_t* value);
+
 /* Debug/test exports (host only, no GPU needed): the load-time repack and its inverse. */
 size_t hc_repacked_bytes(int32_t N, int32_t K, int32_t bits);
 hc_status hc_repack_host(const uint32_t* codes, const uint16_t* scales, const uint8_t* zeros,

@@ -18,7 +18,19 @@ from ._lib import (HCError, HC_OK, HC_ERR_CONFIG, HC_ERR_STATE, HC_ERR_NUMERIC, 
 
 __all__ = ["allocate_ranks", "Context", "HCError", "QKV", "O", "UPGATE", "DOWN", "OUT_F32", "OUT_BF16",
            "GLUE_NONE", "GLUE_SILU_MUL",
-           "repack_host", "unpack_repacked_host", "shard_rows", "unshard_host", "lib"]
+           "repack_host", "unpack_repacked_host", "shard_rows", "unshard_host", "set_option", "get_option", "lib"]
+
+
+def set_option(name: str, value: int) -> None:
+    """hc_set_option: process-wide development switch (include/hcinfer.h lists them)."""
+    check(lib().hc_set_option(name.encode(), int(value)))
+
+
+def get_option(name: str) -> int:
+    """hc_get_option."""
+    v = C.c_int32(0)
+    check(lib().hc_get_option(name.encode(), C.addressof(v)))
+    return int(v.value)
 
 
 def shard_rows(N: int, world: int, rank: int, unit: int = 16):

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "comm.h"
+#include "options.h"
 #include "decode.h"
 #include "prefill.h"
 #include "moe.h"
@@ -86,6 +87,7 @@ bool admissible_rank(int r) { return r == 0 || (r >= 8 && (r & (r - 1)) == 0); }
 
 struct StackGraph {
   cudaGraphExec_t exec = nullptr;
+  unsigned epoch = 0;                 // options().epoch at capture
   ~StackGraph() { if (exec) cudaGraphExecDestroy(exec); }
 };
 
@@ -102,7 +104,7 @@ struct hc_ctx {
   DevBuf s_h, s_h1, s_qkv, s_m;
   int trace_slot = 0;                  // dev tracing: slot of the next decode launch (HC_DEC_TRACE builds)
   DevBuf s_x16[4];                     // x' hand-off buffers of the stack: q, h1, m, h (16 rows each)
-  DevBuf s_x16flag;                    // their exactness flags [4] (DArgs::y16_flag / x16_flag)
+  DevBuf s_x16max;                     // their per-(group, batch row) max |x| [4][G][16] (DArgs::y16_max / x16_max)
   std::map<std::tuple<int, const void*, void*>, std::unique_ptr<StackGraph>> graphs;
   cudaStream_t cap_stream = nullptr;
   // column sharding (hc_set_comm): NCCL communicator, send / gather staging
@@ -396,6 +398,40 @@ static hc_status load_one(hc_ctx* ctx, const hc_matrix_desc* mats, int32_t n_mat
     return HC_OK;
 }
 
+namespace hc {
+Options& options() {
+  static Options o;
+  return o;
+}
+}  // namespace hc
+
+extern "C" hc_status hc_set_option(const char* name, int32_t value) {
+  if (!name) return fail(HC_ERR_CONFIG, "hc_set_option: null name");
+  hc::Options& o = hc::options();
+  const std::pair<const char*, int*> tab[] = {{"t_forward", &o.t_forward},       {"x_handoff", &o.x_handoff},
+                                              {"dep_wait", &o.dep_wait},         {"int8_path", &o.int8_path},
+                                              {"prefill_merge", &o.prefill_merge}, {"decode_ctas_per_sm", &o.decode_ctas_per_sm}};
+  for (const auto& kv : tab)
+    if (std::strcmp(kv.first, name) == 0) {
+      if (value < 0) return fail(HC_ERR_CONFIG, "hc_set_option: %s = %d < 0", name, value);
+      *kv.second = value;
+      ++o.epoch;
+      return HC_OK;
+    }
+  return fail(HC_ERR_CONFIG, "hc_set_option: unknown option '%s'", name);
+}
+
+extern "C" hc_status hc_get_option(const char* name, int32_t* value) {
+  if (!name || !value) return fail(HC_ERR_CONFIG, "hc_get_option: null argument");
+  const hc::Options& o = hc::options();
+  const std::pair<const char*, int> tab[] = {{"t_forward", o.t_forward},       {"x_handoff", o.x_handoff},
+                                             {"dep_wait", o.dep_wait},         {"int8_path", o.int8_path},
+                                             {"prefill_merge", o.prefill_merge}, {"decode_ctas_per_sm", o.decode_ctas_per_sm}};
+  for (const auto& kv : tab)
+    if (std::strcmp(kv.first, name) == 0) { *value = kv.second; return HC_OK; }
+  return fail(HC_ERR_CONFIG, "hc_get_option: unknown option '%s'", name);
+}
+
 extern "C" hc_status hc_load_layer(hc_ctx* ctx, const hc_matrix_desc* mats, int32_t n_mats, void* stream) {
   if (!ctx) return fail(HC_ERR_STATE, "hc_load_layer: null context");
   if (n_mats < 0 || (n_mats > 0 && !mats)) return fail(HC_ERR_CONFIG, "hc_load_layer: bad matrix list");
@@ -458,8 +494,7 @@ static int window_chunks(const Window& w) {
 
 // Whether `next` can receive t from the kernel producing its input (DArgs::fwd / t_in).
 static bool can_forward(const Window& next) {
-  const char* e = getenv("HC_TFWD");                  // "0": every window computes its own V·x (A/B testing)
-  if (e && e[0] == '0') return false;
+  if (!options().t_forward) return false;
   const int c = window_chunks(next);
   if (c == 0 || c > kFwdMax || (int)next.members.size() > kMaxMembers) return false;
   for (const Member& m : next.members)
@@ -473,36 +508,27 @@ struct X16Spec {
   const uint16_t* in = nullptr;   // x' of this window written by its producer (or NULL)
   uint16_t* out = nullptr;        // where this window writes the next window's x' (or NULL)
   int lo = 0, hi = 0;             // output columns that are the next window's x
-  unsigned* flag_in = nullptr;    // exactness flag of `in` (DArgs::x16_flag), of `out` (DArgs::y16_flag)
-  unsigned* flag_out = nullptr;
+  const unsigned* max_in = nullptr;   // max |x| per (group, batch row) of `in` (DArgs::x16_max), of `out` (y16_max)
+  unsigned* max_out = nullptr;
+  unsigned* clr = nullptr;            // the max buffer the next window publishes into (zeroed by CTA 0, DArgs::clr_max)
+  int clr_n = 0;
 };
 
 static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int B, void* y, int y_bf16,
                              const void* resid, int ld_resid, DArgs& a, int& grid, bool t_in = false,
                              const FwdSpec* fw = nullptr, Window* dep = nullptr, bool keep_done = false,
-                             const X16Spec* xs16 = nullptr, const Window* pf = nullptr) {
+                             const X16Spec* xs16 = nullptr) {
   std::memset(&a, 0, sizeof(a));
-  if (pf) {
-    // L2 prefetch of the next window's records (DArgs::pf_*): the first pf_mb MB of them
-    static const long long pf_cap = [] { const char* e = getenv("HC_PF_MB"); return (long long)(e ? atof(e) * 1e6 : 32e6); }();
-    long long tot = 0;
-    for (const Member& m : pf->members) {
-      if (!m.rec || !m.rec->p || a.pf_n >= kMaxMembers) continue;
-      a.pf_ptr[a.pf_n] = (const uint8_t*)m.rec->p;
-      a.pf_len[a.pf_n] = (long long)m.rec->bytes;
-      tot += (long long)m.rec->bytes;
-      ++a.pf_n;
-    }
-    a.pf_total = std::min(tot, pf_cap);
-  }
   if (xs16) {
     a.x16_given = xs16->in ? 1 : 0;
     a.x16 = xs16->in;
     a.y16 = xs16->out;
     a.y16_lo = xs16->lo;
     a.y16_hi = xs16->hi;
-    a.x16_flag = xs16->in ? xs16->flag_in : nullptr;
-    a.y16_flag = xs16->out ? xs16->flag_out : nullptr;
+    a.x16_max = xs16->in ? xs16->max_in : nullptr;
+    a.y16_max = xs16->out ? xs16->max_out : nullptr;
+    a.clr_max = xs16->clr;
+    a.clr_n = xs16->clr_n;
   }
   a.t_in = t_in ? 1 : 0;
   a.keep_done = keep_done ? 1 : 0;
@@ -564,7 +590,7 @@ static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int
   if (a.n_chunks > kMaxChunks) return fail(HC_ERR_CONFIG, "window ranks need %d chunks > %d", a.n_chunks, kMaxChunks);
   if (w.ws_chunks < max_chunks) {
     const int mc = std::max(max_chunks, 1);
-    CUDA_TRY(w.tacc.alloc((size_t)mc * 512 * sizeof(long long)));
+    CUDA_TRY(w.tacc.alloc(((size_t)mc * hc::kTChunk + 4) * sizeof(long long)));   // [chunk][tier][16][16] + deep flag
     CUDA_TRY(cudaMemset(w.tacc.p, 0, w.tacc.bytes));
     CUDA_TRY(w.cnt.alloc(2 * sizeof(unsigned)));
     CUDA_TRY(cudaMemset(w.cnt.p, 0, w.cnt.bytes));
@@ -605,7 +631,7 @@ static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int
                                                     a.x16_given != 0)).first;
   if (it->second <= 0) return fail(HC_ERR_RUNTIME, "decode kernel cannot be resident on this device");
   const int n_items = a.n_rb;
-  static const int per_sm = [] { const char* e = getenv("HC_DECODE_CTAS_PER_SM"); return e ? atoi(e) : 0; }();
+  const int per_sm = options().decode_ctas_per_sm;
   const int cap = per_sm > 0 ? std::min(it->second, per_sm * ctx->sms) : it->second;
   grid = std::max(1, std::min(n_items, cap));
   return HC_OK;
@@ -614,10 +640,10 @@ static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int
 static hc_status launch_window(hc_ctx* ctx, Window& w, const void* x, int ldx, int B, void* y, int y_bf16,
                                const void* resid, int ld_resid, cudaStream_t st, bool t_in = false,
                                const FwdSpec* fw = nullptr, Window* dep = nullptr, bool keep_done = false,
-                               const X16Spec* xs16 = nullptr, const Window* pf = nullptr) {
+                               const X16Spec* xs16 = nullptr) {
   DArgs a;
   int grid = 0;
-  hc_status s = window_args(ctx, w, x, ldx, B, y, y_bf16, resid, ld_resid, a, grid, t_in, fw, dep, keep_done, xs16, pf);
+  hc_status s = window_args(ctx, w, x, ldx, B, y, y_bf16, resid, ld_resid, a, grid, t_in, fw, dep, keep_done, xs16);
   if (s != HC_OK) return s;
   a.trace_slot = ctx->trace_slot++;
   if (a.x16 && !a.x16_given)
@@ -687,8 +713,7 @@ static hc_status launch_prefill_window(hc_ctx* ctx, Window& w, const void* x, in
   if (!encode_tmap_f16(&tmX, ctx->p_x16.p, K, M, K, kPBM)) return fail(HC_ERR_RUNTIME, "tensor map (X) encoding failed");
   int R_merged = 0;
   for (const Member& m : w.members) R_merged += (m.r_alloc + 15) / 16 * 16;
-  const char* pe = getenv("HC_PREFILL_MERGE");                // "0": one GEMM per member (A/B testing)
-  if (w.members.size() > 1 && R_merged <= 256 && !(pe && pe[0] == '0')) {
+  if (w.members.size() > 1 && R_merged <= 256 && options().prefill_merge) {
     // one GEMM over all members: concatenated rows, stacked rank slices, block-diagonal U
     hc_status s = build_prefill_merged(w, st);
     if (s != HC_OK) return s;
@@ -1070,9 +1095,11 @@ extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, voi
     const size_t xb[4] = {(size_t)16 * d * 2, (size_t)16 * d * 2, (size_t)16 * f * 2, (size_t)16 * d * 2};
     for (int i = 0; i < 4; ++i)
       if (ctx->s_x16[i].bytes < xb[i]) { ctx->invalidate_graphs(); CUDA_TRY(ctx->s_x16[i].alloc(xb[i])); }
-    if (!ctx->s_x16flag.p) {
-      CUDA_TRY(ctx->s_x16flag.alloc(4 * sizeof(unsigned)));
-      CUDA_TRY(cudaMemset(ctx->s_x16flag.p, 0, 4 * sizeof(unsigned)));
+    const size_t mb = (size_t)4 * (std::max(d, f) / hc::kGroup) * 16 * sizeof(unsigned);
+    if (ctx->s_x16max.bytes < mb) {
+      ctx->invalidate_graphs();
+      CUDA_TRY(ctx->s_x16max.alloc(mb));
+      CUDA_TRY(cudaMemset(ctx->s_x16max.p, 0, mb));
     }
   }
   const bool tp = ctx->comm != nullptr;
@@ -1084,6 +1111,10 @@ extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, voi
 
   auto key = std::make_tuple((int)B, dx, dy);
   auto git = ctx->graphs.find(key);
+  if (git != ctx->graphs.end() && git->second->epoch != hc::options().epoch) {   // options changed: re-plan
+    ctx->graphs.erase(git);
+    git = ctx->graphs.end();
+  }
   if (git == ctx->graphs.end()) {
     // first use: make sure every window's workspace exists (allocation is not capturable), then
     // capture the 4·L launches into one graph
@@ -1116,8 +1147,8 @@ extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, voi
         // dataflow dependencies: a window whose x is staged in shared memory waits on
         // its producer's row-block counter instead of the kernel boundary (an unstaged window keeps the
         // grid dependency: its x-prep kernel sits in between)
-        const bool dx_ok = getenv("HC_DEPWAIT") == nullptr || getenv("HC_DEPWAIT")[0] != '0';
-        const bool hx_ok = dx_ok && (getenv("HC_XHANDOFF") == nullptr || getenv("HC_XHANDOFF")[0] != '0');
+        const bool dx_ok = hc::options().dep_wait != 0;
+        const bool hx_ok = dx_ok && hc::options().x_handoff != 0;
         const bool sx_q = dx_ok && hc::decode_stages_x(B, d), sx_f = dx_ok && hc::decode_stages_x(B, f);
         Window* prev_dn = l > 0 ? plan[l - 1].down : nullptr;
         const bool next_q = l + 1 < plan.size() && sx_q;
@@ -1131,30 +1162,32 @@ extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, voi
         auto i8w = [&](Window* w) { return hc::decode_uses_i8(w->members.front().bits, B, w->members.front().K); };
         const bool i8q = i8w(p.qkv), i8o = i8w(p.o), i8ug = i8w(p.ug), i8dn = i8w(p.down);
         const bool i8qn = l + 1 < plan.size() ? i8w(plan[l + 1].qkv) : true;
-        unsigned* xfl = (unsigned*)ctx->s_x16flag.p;     // flags of q, h1, m, h
-        const hc::X16Spec x_q{hx && l > 0 && !i8q ? xh16 : nullptr, hx && !i8o ? xq16 : nullptr, 0, d, xfl + 3, xfl + 0};
-        const hc::X16Spec x_o{hx && !i8o ? xq16 : nullptr, hx && !i8ug ? xh1 : nullptr, 0, d, xfl + 0, xfl + 1};
-        const hc::X16Spec x_ug{hx && !i8ug ? xh1 : nullptr, hx && !i8dn ? xm16 : nullptr, 0, f, xfl + 1, xfl + 2};
-        const hc::X16Spec x_dn{hx && !i8dn ? xm16 : nullptr, (hx && !i8qn) ? xh16 : nullptr, 0, d, xfl + 2, xfl + 3};
+        // x' range (R20): max |x| per (group, batch row) of q, h1, m, h; window w zeroes the buffer window w+1
+        // publishes into (layer 0's QKV output buffer is zeroed by a memset at the start of the graph)
+        const int gm = std::max(d, f) / hc::kGroup;
+        unsigned* xmx = (unsigned*)ctx->s_x16max.p;
+        unsigned* mq = xmx, *mh1 = xmx + (size_t)gm * 16, *mm16 = xmx + (size_t)2 * gm * 16, *mh = xmx + (size_t)3 * gm * 16;
+        if (l == 0) {
+          const cudaError_t e0 = cudaMemsetAsync(mq, 0, (size_t)gm * 16 * sizeof(unsigned), cs);
+          if (e0 != cudaSuccess) { cap = fail(HC_ERR_RUNTIME, "x' max reset: %s", cudaGetErrorString(e0)); break; }
+        }
+        const int nd = d / hc::kGroup * 16, nf = f / hc::kGroup * 16;
+        const hc::X16Spec x_q{hx && l > 0 && !i8q ? xh16 : nullptr, hx && !i8o ? xq16 : nullptr, 0, d, mh, mq, mh1, nd};
+        const hc::X16Spec x_o{hx && !i8o ? xq16 : nullptr, hx && !i8ug ? xh1 : nullptr, 0, d, mq, mh1, mm16, nf};
+        const hc::X16Spec x_ug{hx && !i8ug ? xh1 : nullptr, hx && !i8dn ? xm16 : nullptr, 0, f, mh1, mm16, mh, nd};
+        const hc::X16Spec x_dn{hx && !i8dn ? xm16 : nullptr, (hx && !i8qn) ? xh16 : nullptr, 0, d, mm16, mh,
+                               l + 1 < plan.size() ? mq : nullptr, nd};
         const bool dq = sx_q || (hx && l > 0), do_ = sx_q || hx, dug = sx_q || hx, ddn = sx_f || hx;
         const bool kq = sx_q || hx, ko = sx_q || hx, kug = sx_f || hx;     // keep(producer) = dep(consumer)
         const bool kdn = l + 1 < plan.size() && (sx_q || hx);
-        // L2 prefetch of the next window's weights (DArgs::pf_*): opt-in (HC_PF=1); measured slower on C2
-        // (670 -> 668 / 651 / 640 tokens/s at 16 / 32 / 64 MB): the prefetch misses lengthen the L2 latency
-        // of the critical-path activation loads
-        const bool pf_on = getenv("HC_PF") != nullptr && getenv("HC_PF")[0] == '1';
-        const Window* pf_q = pf_on ? p.o : nullptr;
-        const Window* pf_o = pf_on ? p.ug : nullptr;
-        const Window* pf_ug = pf_on ? p.down : nullptr;
-        const Window* pf_dn = (pf_on && l + 1 < plan.size()) ? plan[l + 1].qkv : nullptr;
         cap = hc::launch_window(ctx, *p.qkv, hin, d, B, qkv, 1, nullptr, 0, cs, t_q, &s_o,
-                                (prev_dn && dq) ? prev_dn : nullptr, kq, &x_q, pf_q);                        // q | k | v
+                                (prev_dn && dq) ? prev_dn : nullptr, kq, &x_q);                        // q | k | v
         if (cap == HC_OK) cap = hc::launch_window(ctx, *p.o, qkv, nqkv, B, h1, 1, hin, d, cs, f_o, &s_ug,
-                                                  do_ ? p.qkv : nullptr, ko, &x_o, pf_o);                     // h1 = h + O(q)
+                                                  do_ ? p.qkv : nullptr, ko, &x_o);                     // h1 = h + O(q)
         if (cap == HC_OK) cap = hc::launch_window(ctx, *p.ug, h1, d, B, mm, 1, nullptr, 0, cs, f_ug, &s_dn,
-                                                  dug ? p.o : nullptr, kug, &x_ug, pf_ug);                    // m = silu(g)·u
+                                                  dug ? p.o : nullptr, kug, &x_ug);                    // m = silu(g)·u
         if (cap == HC_OK) cap = hc::launch_window(ctx, *p.down, mm, f, B, hout, 1, h1, d, cs, f_dn, &s_q,
-                                                  ddn ? p.ug : nullptr, kdn, &x_dn, pf_dn);                   // h' = h1 + DOWN(m)
+                                                  ddn ? p.ug : nullptr, kdn, &x_dn);                   // h' = h1 + DOWN(m)
       } else {                                                   // column-sharded: gather every window
         cap = tp_window(ctx, *p.qkv, hin, d, B, qkv, nullptr, 0, cs);
         if (cap == HC_OK) cap = tp_window(ctx, *p.o, qkv, nqkv, B, h1, hin, d, cs);
@@ -1168,6 +1201,7 @@ extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, voi
     if (cap != HC_OK) { if (g) cudaGraphDestroy(g); return cap; }
     CUDA_TRY(e);
     std::unique_ptr<StackGraph> sg(new StackGraph());
+    sg->epoch = hc::options().epoch;
     e = cudaGraphInstantiate(&sg->exec, g, 0);
     cudaGraphDestroy(g);
     CUDA_TRY(e);

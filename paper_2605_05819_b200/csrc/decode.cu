@@ -22,8 +22,8 @@
 //  * the 8 warps' partial sums are reduced in shared memory in a fixed order; the CTA's epilogue
 //    warp adds U[:, :r]·t with t split into bf16 hi + lo (fp32-accurate) on the same mma and
 //    writes y once (fp32, or bf16 = RNE of the fp32 value), optionally adding a bf16 residual;
-//  * t is produced inside the launch with two-word 64-bit fixed-point atomics (tacc_add: exact for
-//    fp32 partials down to 2^-78; integer adds are associative, so t is deterministic); epilogues
+//  * t is produced inside the launch with tiered 64-bit fixed-point atomics (tacc_add: one atomic per
+//    fp32 partial, rounded once to 24+ bits; integer adds are associative, so t is deterministic); epilogues
 //    acquire a release counter.  The accumulators and counters self-reset before the kernel exits.
 //  * fp16 path: the B operand carries a per-(group, batch row) power-of-two prescale when a group's
 //    range needs it (R20), so any bf16 x is accepted.
@@ -34,6 +34,7 @@
 #include <type_traits>
 
 #include "decode.h"
+#include "options.h"
 #include "decode_dev.cuh"
 #include "layout.h"
 
@@ -79,7 +80,7 @@ __device__ __forceinline__ void dep_wait(const DArgs& a, int lane) {
   if (a.dep_cnt) {
     if (lane == 0) {
       while (ld_relaxed(a.dep_cnt) < a.dep_target) __nanosleep(HC_DEP_SLEEP);
-      (void)ld_acquire(a.dep_cnt);
+      (void)ld_acquire(a.dep_cnt);   // (a fence.acq_rel here measured slower than the second load)
       asm volatile("fence.proxy.async.global;" ::: "memory");   // generic writes -> async-proxy (TMA) reads
     }
     __syncwarp();
@@ -183,22 +184,6 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
         if (++slot == kNBuf) { slot = 0; ++round; }
       }
     }
-    if (a.pf_total > 0) {
-      // every ring of this CTA is issued: prefetch this CTA's slice of the next window's records to L2
-      __syncwarp();
-      const long long lo = a.pf_total * blockIdx.x / gridDim.x, hi = a.pf_total * (blockIdx.x + 1) / gridDim.x;
-      constexpr long long kChunk = 16384;
-      long long base = 0;
-      for (int i = 0; i < a.pf_n; ++i) {
-        const long long s0 = max(lo, base), s1 = min(hi, base + a.pf_len[i]);
-        for (long long c = (s0 & ~15LL) + (long long)lane * kChunk; c < s1; c += 32 * kChunk) {
-          const long long e = min(c + kChunk, s1);
-          const uint32_t n = (uint32_t)((e - c + 15) & ~15LL);
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.pf_ptr[i] + (c - base)), "r"(n) : "memory");
-        }
-        base += a.pf_len[i];
-      }
-    }
     return;
   }
 
@@ -220,7 +205,8 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
     };
     prefetch_u(blockIdx.x, 0);                           // weights: before the PDL wait
     dep_wait(a, lane);
-    if (lane == 0 && a.x16_given && a.x16_flag) misc[1] = *reinterpret_cast<volatile unsigned*>(a.x16_flag);   // before bar 6
+    if (blockIdx.x == 0 && a.clr_max)                    // the max buffer the next window publishes into (R20)
+      for (int i = lane; i < a.clr_n; i += 32) a.clr_max[i] = 0u;
     if ((!XS || I8) && a.dep_cnt) asm volatile("bar.sync 6, %0;" ::"n"(kDecodeThreads) : "memory");   // release the tile warps
     if (lane == 0) dtrace(a, 1);
     if constexpr (XS && !I8) {
@@ -233,6 +219,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
     unsigned u_phase = 0;   // bit p = phase of ubar[p]
     unsigned f_phase = 0;
     bool t_ready = false;
+    bool t_deep = false;   // the extra-tier flag of this window's t (read with t; reset on the exit path)
     int my_rb = 0;
     int k = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++k) {
@@ -242,25 +229,29 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
       if (!t_ready && r_eff > 0) {
         // once per CTA, while the tile warps still stream: acquire t (all tile warps of the grid
         // have added their V·x shares) and keep its fragments in smem as fp32
-        if (lane == 0) {
+        if (lane == 0 && n_vctas > 0) {                 // t_in: ordered by the dependency wait already
           while (ld_relaxed(&a.cnt[0]) < (unsigned)n_vctas) __nanosleep(32);
           (void)ld_acquire(&a.cnt[0]);
         }
         __syncwarp();
-        // kept as the bf16 hi + lo B-fragments of the U·t mma (fp32-accurate), ranks >= r masked to 0
+        // t as bf16 hi + lo B-fragments of the U·t mma (fp32-accurate), ranks >= r masked to 0.  Tier 0 only
+        // (R22); the extra-tier flag is loaded first and consumed after the loop, and the rare extra-tier
+        // pass is out of line.  No branch may sit between the loads of this loop (a branch inside the
+        // unrolled loop serialises them into one L2 round trip per chunk: +2.5 µs on C1).
+        t_deep = __ldcg(a.tacc + (size_t)a.n_chunks * kTChunk) != 0;
 #pragma unroll 4
         for (int cc = 0; cc < a.n_chunks; ++cc) {
           const DMember& mt = a.m[member_of_chunk(a, cc)];
           const int r0 = 16 * (cc - mt.chunk_begin) + 2 * tig;
 #pragma unroll
           for (int nb = 0; nb < NB8; ++nb) {
-            const long long* src = a.tacc + (((size_t)cc * 16 + ((gid + 8 * nb) & 15)) * 16 + 2 * tig) * 2;
-            const float tr[4] = {tacc_read(src), tacc_read(src + 2), tacc_read(src + 16), tacc_read(src + 18)};
+            const long long* src = a.tacc + (size_t)cc * kTChunk + ((gid + 8 * nb) & 15) * 16 + 2 * tig;
+            const long long tr[4] = {__ldcg(src), __ldcg(src + 1), __ldcg(src + 8), __ldcg(src + 9)};
             uint32_t hi[2], lo[2];
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
-              const float ta = (r0 + 8 * hh < mt.r) ? tr[2 * hh] : 0.f;
-              const float tb = (r0 + 8 * hh + 1 < mt.r) ? tr[2 * hh + 1] : 0.f;
+              const float ta = (r0 + 8 * hh < mt.r) ? (float)tr[2 * hh] * 0x1p-36f : 0.f;
+              const float tb = (r0 + 8 * hh + 1 < mt.r) ? (float)tr[2 * hh + 1] * 0x1p-36f : 0.f;
               const uint32_t ha = f32_to_bf16_rn(ta), hb = f32_to_bf16_rn(tb);
               hi[hh] = ha | (hb << 16);
               lo[hh] = f32_to_bf16_rn(ta - bf16_bits_to_f32(ha)) | (f32_to_bf16_rn(tb - bf16_bits_to_f32(hb)) << 16);
@@ -268,6 +259,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
             tsm[((size_t)cc * NB8 + nb) * 32 + lane] = make_uint4(hi[0], hi[1], lo[0], lo[1]);
           }
         }
+        if (t_deep) t_fragments_xt<NB8>(a, tsm, lane);   // rare: outlier or tiny activations (R22)
         __syncwarp();
         t_ready = true;
         if (lane == 0) dtrace(a, 5);
@@ -355,6 +347,9 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
         asm volatile("bar.arrive %0, %1;" ::"r"(3 + par), "n"(kDecodeThreads) : "memory");   // EMPTY[par]
       prefetch_u(item + gridDim.x, par ^ 1);
 
+      uint32_t xm[NB8][2];                               // largest |bf16 y| per batch row (x' range, R20)
+#pragma unroll
+      for (int nb = 0; nb < NB8; ++nb) xm[nb][0] = xm[nb][1] = 0u;
       if (a.glue) {
         // m[b][8·rbl + gid] = silu(gate) · up, gate = row gid+8 (c2, c3), up = row gid (c0, c1)
 #pragma unroll
@@ -372,6 +367,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
               reinterpret_cast<uint16_t*>(a.y)[(size_t)b * a.ldy + n] = bits;
               if (f_on) xt[(((f_n0 - a.fwd_lo) & 15) + gid) * 16 + b] = bits;
               if (a.y16 && n >= a.y16_lo && n < a.y16_hi) write_xprime<BITS>(a, b, n, bits);
+              xm[nb][e] = max(xm[nb][e], (uint32_t)bits & 0x7FFFu);
             } else {
               reinterpret_cast<float*>(a.y)[(size_t)b * a.ldy + n] = v;
             }
@@ -390,11 +386,13 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
               reinterpret_cast<uint16_t*>(a.y)[(size_t)b * a.ldy + n] = bits;
               if (f_on) xt[(gid + 8 * (e >> 1)) * 16 + b] = bits;
               if (a.y16 && n >= a.y16_lo && n < a.y16_hi) write_xprime<BITS>(a, b, n, bits);
+              xm[nb][e & 1] = max(xm[nb][e & 1], (uint32_t)bits & 0x7FFFu);
             } else {
               reinterpret_cast<float*>(a.y)[(size_t)b * a.ldy + n] = v;
             }
           }
       }
+      if (a.y16 && a.y16_max && f_n0 >= a.y16_lo && f_n0 < a.y16_hi) publish_xmax<NB8>(a, f_n0, xm, lane);
       if (f_on) {
         // t_next[c][col][rank] += Σ_{k in this block} Vn[c][rank][k] · x[col][k]  (bf16 mma, fp32, then
         // 2^-28 fixed point: integer adds, so the sum is independent of the order items arrive)
@@ -419,7 +417,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int col = 2 * tig + (e & 1) + 8 * nb, rank = gid + 8 * (e >> 1);
-              if (col < a.B) tacc_add(a.fwd_tacc + (((size_t)cc * 16 + col) * 16 + rank) * 2, tp[e]);
+              if (col < a.B) tacc_add(a.fwd_tacc, a.fwd_chunks, cc, col, rank, tp[e]);
             }
           }
         }
@@ -433,17 +431,18 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
     __syncwarp();
     unsigned last = 0;
     if (lane == 0 && my_rb > 0) {
-      const unsigned old = add_acq_rel(&a.cnt[1], (unsigned)my_rb);
+            const unsigned old = add_acq_rel(&a.cnt[1], (unsigned)my_rb);
       last = (old + (unsigned)my_rb == (unsigned)a.n_rb);
     }
     last = __shfl_sync(0xffffffffu, last, 0);
     if (last) {
-      for (int i = lane; i < a.n_chunks * 512; i += 32) a.tacc[i] = 0;
+      // the flag as read with t (a CTA that never read t loads it here)
+      const bool xt = t_ready ? t_deep : (__ldcg(a.tacc + (size_t)a.n_chunks * kTChunk) != 0);
+      tacc_reset(a.tacc, a.n_chunks, a.B, xt, lane);
       if (lane == 0) {
         a.cnt[0] = 0u;
         if (!a.keep_done) a.cnt[1] = 0u;             // else the consumer window resets it
         if (a.dep_cnt) *a.dep_cnt = 0u;              // every CTA of this window passed its wait
-        if (a.x16_flag) *a.x16_flag = 0u;            // ... and read the producer's x' exactness flag
       }
     }
     return;
@@ -486,7 +485,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int col = 2 * tig + (e & 1) + 8 * nb, rank = gid + 8 * (e >> 1);
-          if (col < a.B) tacc_add(a.tacc + (((size_t)cc * 16 + col) * 16 + rank) * 2, tp[nb][e]);
+          if (col < a.B) tacc_add(a.tacc, a.n_chunks, cc, col, rank, tp[nb][e]);
           tp[nb][e] = 0.f;
         }
     };
@@ -558,11 +557,17 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
   // fp16-path B-operand prescale (R20): factors 2^σ per (group, batch row) from the staging (XS), the
   // x-prep kernel (global), or computed per record from bf16 x (hand-off slow path); else none
   const float* fsig = nullptr;
-  bool slow = false;
+  uint64_t slow = 0;      // x' hand-off: bit t = this warp's group g0 + t needs σ != 0 (per-record slow path)
   if constexpr (!I8) {
     if constexpr (XS) fsig = misc[0] ? fsg : nullptr;
     else if (!a.x16_given) fsig = a.xsig;
-    else slow = misc[1] != 0u;
+    else if (a.x16_max) {
+      const int g0 = warp * a.G / kDecodeWarps, ng = (warp + 1) * a.G / kDecodeWarps - g0;
+      for (int i = lane; i < ng * a.B; i += 32)
+        if (prescale_sigma(__ldcg(a.x16_max + (g0 + i / a.B) * 16 + i % a.B)) != 0) slow |= 1ull << (i / a.B);
+      const uint32_t lo = __reduce_or_sync(0xFFFFFFFFu, (uint32_t)slow), hi = __reduce_or_sync(0xFFFFFFFFu, (uint32_t)(slow >> 32));
+      slow = ((uint64_t)hi << 32) | lo;
+    }
   }
   int k = 0;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++k) {
@@ -604,19 +609,21 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
           const uint4* xrs[NB8];
 #pragma unroll
           for (int nb = 0; nb < NB8; ++nb) xrs[nb] = reinterpret_cast<const uint4*>(xs_row[nb] + g * kGroup);
+          const bool sl = (slow >> (t0 + t)) & 1ull;
           if constexpr (!XS) {
-            if (SIG && slow) load_x_bf16_sig<BITS, NB8>(a, g, lane, xr, fs);
+            if (SIG && sl) load_x_bf16_sig<BITS, NB8>(a, g, lane, xr, fs);
             else load_x_global<NB8>(a, g, lane, xr);
           }
-          if (SIG && !slow) {
+          if (SIG && !sl) {
 #pragma unroll
             for (int nb = 0; nb < NB8; ++nb)
 #pragma unroll
-              for (int h = 0; h < 2; ++h) fs[nb][h] = fsig[g * a.B + min(2 * tig + h + 8 * nb, a.B - 1)];
+              for (int h = 0; h < 2; ++h) fs[nb][h] = fsig ? fsig[g * a.B + min(2 * tig + h + 8 * nb, a.B - 1)] : 1.f;
           }
           w_tile<BITS, NB8, XS, SIG>(blk + t * rec_bytes(BITS), lane, xrs, xr, tot, fs);
         };
-        if (fsig == nullptr && !slow) {
+        const bool blk_slow = ((slow >> t0) & ((1ull << nt) - 1ull)) != 0ull;
+        if (fsig == nullptr && !blk_slow) {
           if (nt == kRPB) {
             // full block: the records are independent straight-line code, so their mma chains interleave
 #pragma unroll
@@ -661,8 +668,7 @@ bool decode_stages_x(int B, int K) { return B <= 8 && use_xs(B, K); }
 // int8 path (decode_i8.cuh): 4-bit codes, B <= 2, x8 of all groups in shared memory
 constexpr size_t kX8Max = 40 * 1024;
 static bool use_i8(int bits, int B, int K) {
-  static const bool on = [] { const char* e = getenv("HC_I8"); return !(e && e[0] == '0'); }();
-  return on && (bits == 4 || bits == 2) && B <= 2 && (size_t)(K / kGroup) * x8_stride(B) + kX8Pad <= kX8Max;
+  return options().int8_path != 0 && (bits == 4 || bits == 2) && B <= 2 && (size_t)(K / kGroup) * x8_stride(B) + kX8Pad <= kX8Max;
 }
 bool decode_uses_i8(int bits, int B, int K) { return use_xs(B, K) && use_i8(bits, B, K); }
 

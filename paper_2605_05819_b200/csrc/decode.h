@@ -26,6 +26,8 @@ constexpr int kTileMax = 1088;           // >= rec_bytes(4) = 1072, >= 1 KB V pi
 #define HC_DEC_UPRE 8
 #endif
 constexpr int kUPre = HC_DEC_UPRE;       // U chunks (16 ranks each) staged in smem per item (r <= 128)
+constexpr int kTTiers = 4;               // t accumulator tiers (decode_dev.cuh tacc_add)
+constexpr int kTChunk = kTTiers * 256;   // t accumulator words per rank chunk: [tier][16 cols][16 ranks]
 constexpr int kFwdMax = 24;              // next-window rank chunks a launch can forward t to (smem: 512 B each)
 
 struct DMember {
@@ -81,23 +83,18 @@ struct DArgs {
   int x16_given;
   uint16_t* y16;
   int y16_lo, y16_hi;
-  // x' exactness (R20): the producer sets *y16_flag when some x' it wrote is not exact in fp16
-  // (|x| out of the fp16-exact band); the consumer reads *x16_flag after its dependency wait and then
-  // builds x' itself with a per-group prescale (slow path); its last CTA resets the flag
-  unsigned* y16_flag;
-  unsigned* x16_flag;
+  // x' range (R20): the producer publishes, per (group of 128 x' columns, batch row), the largest
+  // |x| (bf16 bits without sign) of its hand-off through atomicMax into y16_max [G][16]; the consumer reads
+  // x16_max after its dependency wait and, for the groups whose prescale σ is not 0, builds x' itself from
+  // bf16 x (per-record slow path).  clr_max[0 .. clr_n) is zeroed by CTA 0 after its dependency wait: the
+  // max buffer the NEXT window publishes into (its previous reader finished before this window's producer)
+  unsigned* y16_max;
+  const unsigned* x16_max;
+  unsigned* clr_max;
+  int clr_n;
   float* xsig;          // x-prep launches (x16 given by launch_xprep): 2^σ per (group, batch row) [G][B]
-  long long* tacc;      // [n_chunks][16 batch][16 ranks] t = V·x in 2^-28 fixed point (self-resetting)
+  long long* tacc;      // [n_chunks][16 batch][16 ranks][4 tiers] t = V·x in tiered fixed point (self-resetting)
   unsigned* cnt;        // [0] v_done (tile warps done with their V share), [1] w_done (row blocks)
-  // L2 prefetch of the NEXT window's weight records (stack graphs): once a CTA's producer warp has issued
-  // its last bulk copy, it prefetches its share (by CTA index) of the first pf_total bytes of the
-  // concatenated record arrays pf_ptr[i] (pf_len[i] bytes each) into L2, so HBM keeps streaming through
-  // this window's tail, the dependency hand-off and the next window's ramp (weights do not depend on
-  // activations)
-  const uint8_t* pf_ptr[kMaxMembers];
-  long long pf_len[kMaxMembers];
-  int pf_n;
-  long long pf_total;
 };
 
 // Launch the fused window kernel; bits in {2,3,4}; 1 <= B <= 16.

@@ -195,20 +195,81 @@ constexpr int kVPerWarp = HC_VPW;                    // V·x pieces per tile war
 constexpr float kTScale = 268435456.f;          // 2^28: fixed-point scale of the t accumulators
 constexpr float kTInv = 1.f / 268435456.f;
 
-// t accumulators: two 64-bit integer words per element, hi = Σ rint(v·2^28) and lo = Σ rint(r·2^50) with
-// r = v·2^28 − rint(v·2^28) (exact in fp32), so every fp32 partial v with |v| < 2^35 is represented
-// EXACTLY down to 2^-78 and the sums are order-free integer adds (t is deterministic).  A second word
-// only when the first leaves a remainder (|v| < 2^-5 or non-integral v·2^28), so typical |t| ~ 1 partials
-// cost one atomic; activations down to ~1e-20 keep a full-precision rank projection (R22).
-__device__ __forceinline__ void tacc_add(long long* p, float v) {
-  const float s = v * kTScale;                               // exact (power of two)
-  const long long hi = __float2ll_rn(s);
-  if (hi != 0) atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)hi);
-  const float res = s - (float)hi;                           // exact: |s| < 2^23 -> hi fits 24 bits; else s integral
-  if (res != 0.f) atomicAdd(reinterpret_cast<unsigned long long*>(p + 1), (unsigned long long)__float2ll_rn(res * 0x1p50f));
+// t accumulators (R22): four tiers of 64-bit integer words, laid out [chunk][tier][16 batch cols][16 ranks]
+// (the 16 ranks of one (chunk, tier, col) are one 128-byte line) + one "extra tiers used" flag word after
+// the last chunk.  A fp32 partial v goes to exactly ONE tier, chosen by magnitude:
+//   tier 0: 2^-24 <= |v| < 2^12  in 2^-36 fixed point   (the common case: the only tier read and reset)
+//   tier 1: |v| >= 2^12          in 2^-12 fixed point   (outlier activations; saturates at 2^50)
+//   tier 2: 2^-48 <= |v| < 2^-24 in 2^-72 fixed point   (tiny activations)
+//   tier 3: |v| < 2^-48          in 2^-96 fixed point
+// Each partial is rounded once with |error| <= 2^-25·max(|v|, 2^-24·2^-12) in tier 0 and relative error
+// <= 2^-25 (one fp32 rounding) in tiers 1-3 (tier 3: down to |v| = 2^-72); a tier stays below 2^48 per
+// partial, 2^63 for up to 2^15 partials.  The tier-0 band is wide so that partials of ordinary activations
+// (including the occasional near-cancelled one: a normal partial falls below 2^-24 with probability
+// ~1e-6) never leave it; whole windows of tiny or huge activations set the flag.  Integer adds are
+// order-free: t is deterministic.  One atomic per partial; the common case reads and resets one word per
+// element.
+__device__ __forceinline__ size_t tacc_idx(int cc, int w, int rank, int col) {
+  return (size_t)cc * kTChunk + (w * 16 + col) * 16 + rank;
 }
-__device__ __forceinline__ float tacc_read(const long long* p) {
-  return (float)((double)__ldcg(p) * 0x1p-28 + (double)__ldcg(p + 1) * 0x1p-78);
+__device__ __forceinline__ void tacc_add(long long* t, int n_chunks, int cc, int col, int rank, float v) {
+  const float a = fabsf(v);
+  const int w = a >= 0x1p-24f ? (a >= 0x1p12f ? 1 : 0) : (a >= 0x1p-48f ? 2 : 3);
+  const int se = w == 0 ? 36 : (w == 1 ? 12 : (w == 2 ? 72 : 96));
+  const float q = fminf(fmaxf(v * __uint_as_float((uint32_t)(127 + se) << 23), -0x1p62f), 0x1p62f);   // exact scaling
+  const long long iq = __float2ll_rn(q);
+  if (iq != 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(t + tacc_idx(cc, w, rank, col)), (unsigned long long)iq);
+    if (w != 0) t[(size_t)n_chunks * kTChunk] = 1;     // extra tiers in use (idempotent plain store)
+  }
+}
+// t of (chunk cc, batch col) at ranks r0, r0 + 1: tier 0 (8-byte loads); XT: + tiers 1-3.  fp32 (no
+// fp64: its conversions are slow on the epilogue's critical path)
+template <bool XT>
+__device__ __forceinline__ void tacc_read2(const long long* t, int cc, int col, int r0, float& ta, float& tb) {
+  const long long* p = t + tacc_idx(cc, 0, r0, col);
+  ta = (float)__ldcg(p) * 0x1p-36f;
+  tb = (float)__ldcg(p + 1) * 0x1p-36f;
+  if (XT) {
+    const long long *p1 = t + tacc_idx(cc, 1, r0, col), *p2 = t + tacc_idx(cc, 2, r0, col), *p3 = t + tacc_idx(cc, 3, r0, col);
+    ta = fmaf((float)__ldcg(p1), 0x1p-12f, ta + fmaf((float)__ldcg(p2), 0x1p-72f, (float)__ldcg(p3) * 0x1p-96f));
+    tb = fmaf((float)__ldcg(p1 + 1), 0x1p-12f, tb + fmaf((float)__ldcg(p2 + 1), 0x1p-72f, (float)__ldcg(p3 + 1) * 0x1p-96f));
+  }
+}
+// Out-of-line t fragment pass over all four tiers (windows whose extra-tier flag is set, R22): rebuilds
+// tsm exactly as the tier-0 pass of the epilogue does, with t = Σ tiers.
+template <int NB8>
+__device__ __noinline__ void t_fragments_xt(const DArgs& a, uint4* tsm, int lane) {
+  const int gid = lane >> 2, tig = lane & 3;
+  for (int cc = 0; cc < a.n_chunks; ++cc) {
+    const DMember& mt = a.m[member_of_chunk(a, cc)];
+    const int r0 = 16 * (cc - mt.chunk_begin) + 2 * tig;
+    for (int nb = 0; nb < NB8; ++nb) {
+      float tr[4];
+      tacc_read2<true>(a.tacc, cc, (gid + 8 * nb) & 15, 2 * tig, tr[0], tr[1]);
+      tacc_read2<true>(a.tacc, cc, (gid + 8 * nb) & 15, 2 * tig + 8, tr[2], tr[3]);
+      uint32_t hi[2], lo[2];
+      for (int hh = 0; hh < 2; ++hh) {
+        const float ta = (r0 + 8 * hh < mt.r) ? tr[2 * hh] : 0.f;
+        const float tb = (r0 + 8 * hh + 1 < mt.r) ? tr[2 * hh + 1] : 0.f;
+        const uint32_t ha = f32_to_bf16_rn(ta), hb = f32_to_bf16_rn(tb);
+        hi[hh] = ha | (hb << 16);
+        lo[hh] = f32_to_bf16_rn(ta - bf16_bits_to_f32(ha)) | (f32_to_bf16_rn(tb - bf16_bits_to_f32(hb)) << 16);
+      }
+      tsm[((size_t)cc * NB8 + nb) * 32 + lane] = make_uint4(hi[0], hi[1], lo[0], lo[1]);
+    }
+  }
+}
+// Reset what a launch with batch B wrote: tier 0 always, tiers 1-3 and the flag when `xt` (the flag as the
+// caller read it; plain stores only on this exit path, no load); one warp.
+__device__ __forceinline__ void tacc_reset(long long* t, int n_chunks, int B, bool xt, int lane) {
+  const int per = B * 16, tiers = xt ? kTTiers : 1;      // words of one (chunk, tier): cols < B x 16 ranks
+  for (int i = lane; i < n_chunks * tiers * per; i += 32) {
+    const int row = i / per;                             // chunk * tiers + tier
+    const int c = row / tiers, w = row - c * tiers;
+    t[(size_t)c * kTChunk + w * 256 + (i - row * per)] = 0;
+  }
+  if (lane == 0 && xt) t[(size_t)n_chunks * kTChunk] = 0;
 }
 
 // Row of x used by mma column `col` (batch index).  Columns >= B read a valid row; their
@@ -216,17 +277,20 @@ __device__ __forceinline__ float tacc_read(const long long* p) {
 __device__ __forceinline__ int xrow(const DArgs& a, int col) { return col < a.B ? col : a.B - 1; }
 
 // ---- per-(group, batch row) power-of-two prescale of the fp16 B operand (R20).
-// x' = x·2^-(fp + σ) is exact in fp16 for every bf16 x with |x|·2^-(fp+σ) in [2^-17, 2^15] (fp16's
-// 11-bit significand holds bf16's 8 bits down to the subnormal grid 2^-24).  σ = 0 whenever the group's
-// largest |x| has exponent E in [-2, 13] (the common case: no extra work, bit-identical to no prescale);
-// otherwise σ = E - 12 (the group's largest |x'| lands in [2^12, 2^13)), clamped to [-100, 115] so that
-// 2^±σ stay normal floats.  The group's fp32 partial sum is multiplied back by 2^σ (exact: a power of
-// two).  So the full bf16 range is accepted: outliers >= 65504 and tiny (< 2^-14) activations included.
+// x' = x·2^-(fp + σ) (fp <= 4 for the B operand) is exact in fp16 for every bf16 x with |x|·2^-(fp+σ) in
+// [2^-17, 2^15] (fp16's 11-bit significand holds bf16's 8 bits down to the subnormal grid 2^-24).
+// σ = 0 whenever the group's largest |x| has exponent E in [-6, 13] (the common case: no extra work,
+// bit-identical to no prescale): x' < 2^14, and an element below 2^-13 rounds to the fp16 subnormal grid
+// with |error| <= 2^-21 <= 2^-15·max|x| of its group (a bounded, not an exact, product — R20).
+// Otherwise σ = E - 12 (the group's largest |x'| lands in [2^12, 2^13)), clamped to [-100, 115] so that
+// 2^±σ stay normal floats: elements within 2^-29 of the group max are exact, smaller ones round with
+// |error| <= 2^-42·max.  The group's fp32 partial sum is multiplied back by 2^σ (exact: a power of two).
+// So the full bf16 range is accepted: outliers >= 65504 and tiny (< 2^-14) activations included.
 // Zero and non-finite groups keep σ = 0 (inf / NaN propagate through the products).
 __device__ __forceinline__ int prescale_sigma(uint32_t m) {   // m = the group's largest |x| (bf16 bits & 0x7FFF)
   if (m == 0 || m >= 0x7F80u) return 0;
   const int E = max((int)(m >> 7), 1) - 127;
-  if (E >= -2 && E <= 13) return 0;
+  if (E >= -6 && E <= 13) return 0;
   return min(max(E - 12, -100), 115);
 }
 __device__ __forceinline__ float pow2i(int e) { return __uint_as_float((uint32_t)(127 + e) << 23); }   // e in [-126, 127]
@@ -441,7 +505,8 @@ __device__ __forceinline__ void v_tile(const uint8_t* piece, int lane, const uin
 }
 
 // The next window's x' (fp16, pre-scaled by the code-field exponent of its column pair, layout.h) of
-// one output element (bf16 bits) at output column n, batch row b.
+// one output element (bf16 bits) at output column n, batch row b.  Values outside the σ = 0 band of
+// their group are fixed up by the consumer (x16_max, R20).
 template <int BITS>
 __device__ __forceinline__ void write_xprime(const DArgs& a, int b, int n, uint16_t bits) {
   const int k = n - a.y16_lo, kk = k & (kGroup - 1);
@@ -449,9 +514,25 @@ __device__ __forceinline__ void write_xprime(const DArgs& a, int b, int n, uint1
   const int fp = step_fp(BITS, j, pr);
   const float xv = bf16_bits_to_f32(bits) * __uint_as_float((uint32_t)(127 - fp) << 23);
   a.y16[(size_t)b * (a.y16_hi - a.y16_lo) + k] = __half_as_ushort(__float2half_rn(xv));
-  // exact in fp16 iff zero or 2^-17 <= |x|·2^-fp < 2^16 (R20); otherwise flag the consumer's slow path
-  const int E = (int)((bits >> 7) & 0xFFu) - 127;
-  if ((bits & 0x7FFFu) != 0 && (E - fp < -17 || E - fp > 15) && a.y16_flag) *a.y16_flag = 1u;
+}
+
+// Publish the largest |x| of this lane's hand-off values per batch row into y16_max[g][b] (g = the next
+// window's group of output column n0).  m[nb][h] = the lane's max for batch row 2tig + h + 8nb; the
+// 8 gid lanes of a tig are reduced first, then one atomicMax per (group, batch row).
+template <int NB8>
+__device__ __forceinline__ void publish_xmax(const DArgs& a, int n0, const uint32_t (&m)[NB8][2], int lane) {
+  const int g = (n0 - a.y16_lo) >> 7, tig = lane & 3;
+#pragma unroll
+  for (int nb = 0; nb < NB8; ++nb)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t v = m[nb][h];
+      v = max(v, __shfl_xor_sync(0xFFFFFFFFu, v, 4));
+      v = max(v, __shfl_xor_sync(0xFFFFFFFFu, v, 8));
+      v = max(v, __shfl_xor_sync(0xFFFFFFFFu, v, 16));
+      const int b = 2 * tig + h + 8 * nb;
+      if ((lane >> 2) == 0 && b < a.B && v != 0) atomicMax(a.y16_max + g * 16 + b, v);
+    }
 }
 
 }  // namespace

@@ -55,7 +55,8 @@ __device__ __forceinline__ float pow2f(int e) { return __uint_as_float((uint32_t
 // k = 4l .. 4l + 3 of one (group, batch row).
 __device__ __forceinline__ void x8_stage(const DArgs& a, uint8_t* x8, int g0, int g1, int lane) {
   const int tig = (lane >> 1) & 3, s = lane >> 3, h = lane & 1;
-  constexpr int kPre = 8;                            // (group, batch row) pieces whose loads are in flight together
+  constexpr int kPre = 1;                            // (measured: batching 8 pieces' loads was slower)
+  //                          // (group, batch row) pieces whose loads are in flight together
   for (int p0 = g0 * a.B; p0 < g1 * a.B; p0 += kPre) {
     // issue every load of the batch first: the staging is on the window's critical path and each load
     // is an L2 round trip (the x of this window was just written by its producer)

@@ -107,3 +107,23 @@ def test_repack_rejects_bad_shapes():
     with pytest.raises(hc.HCError) as ei:
         hc.repack_host(c, np.zeros((17, 1), np.uint16), np.zeros((17, 1), np.uint8), 17, 128, 4)
     assert ei.value.code == hc.HC_ERR_CONFIG
+
+
+def test_options_roundtrip_and_errors():
+    """hc_set_option / hc_get_option (host only): every documented switch round-trips, unknown names and
+    negative values are HC_ERR_CONFIG, and the defaults are the measured-best plan."""
+    import paper_2605_05819_b200 as hc
+    defaults = {"t_forward": 0, "x_handoff": 1, "dep_wait": 1, "int8_path": 1, "prefill_merge": 1,
+                "decode_ctas_per_sm": 0}
+    for name, d in defaults.items():
+        assert hc.get_option(name) == d
+        hc.set_option(name, 3)
+        assert hc.get_option(name) == 3
+        hc.set_option(name, d)
+    with pytest.raises(hc.HCError) as e:
+        hc.set_option("no_such_switch", 1)
+    assert e.value.code == hc.HC_ERR_CONFIG
+    with pytest.raises(hc.HCError):
+        hc.set_option("x_handoff", -1)
+    with pytest.raises(hc.HCError):
+        hc.get_option("no_such_switch")

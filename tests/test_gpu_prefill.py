@@ -103,9 +103,9 @@ def test_prefill_c4_shape_sampled(hc, ctx):
     assert rel(y.cpu().numpy()[rows], ref) <= TOL
 
 
-def test_prefill_merged_window_matches_per_member(hc, ctx, monkeypatch):
+def test_prefill_merged_window_matches_per_member(hc, ctx):
     """A multi-member window runs as ONE GEMM (rows concatenated, rank slices stacked, block-diagonal U);
-    it must agree with the oracle, with the per-member launches (HC_PREFILL_MERGE=0), and follow rank
+    it must agree with the oracle, with the per-member launches (option prefill_merge = 0), and follow rank
     changes (the merged copies are rebuilt)."""
     M, K = 384, 1024
     cases = [synth.linear_case(800 + i, N=n, K=K, bits=4, r_stored=32, B=M, zeros="asym")
@@ -117,10 +117,12 @@ def test_prefill_merged_window_matches_per_member(hc, ctx, monkeypatch):
         x = dev(cases[0]["x"])
         y = torch.empty((M, 1024), dtype=torch.float32, device="cuda")
         ctx.compensated_linear(L, 0, x, y)
-        monkeypatch.setenv("HC_PREFILL_MERGE", "0")
-        y2 = torch.empty_like(y)
-        ctx.compensated_linear(L, 0, x, y2)
-        monkeypatch.delenv("HC_PREFILL_MERGE")
+        hc.set_option("prefill_merge", 0)
+        try:
+            y2 = torch.empty_like(y)
+            ctx.compensated_linear(L, 0, x, y2)
+        finally:
+            hc.set_option("prefill_merge", 1)
         torch.cuda.synchronize()
         ref = linear.window_linear(cases, list(ranks), cases[0]["x"])
         assert rel(y.cpu().numpy(), ref) <= TOL

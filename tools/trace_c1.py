@@ -27,7 +27,7 @@ for i in range(ncopy):
                          V=(0.02 * torch.randn((c["r_stored"], K), generator=g, device="cuda")).to(torch.bfloat16),
                          r_stored=c["r_stored"], r_alloc=r)])
 n_slot, grid = 64, 512
-buf = torch.zeros((n_slot, grid, 8), dtype=torch.int64, device="cuda")
+buf = torch.zeros((n_slot, grid, int(os.environ.get("HC_TRACE_W", "16"))), dtype=torch.int64, device="cuda")
 L = hc.lib()
 L.hc_dev_decode_trace.argtypes = [ctypes.c_void_p]
 assert L.hc_dev_decode_trace(buf.data_ptr()) == 0

@@ -43,5 +43,5 @@ for k in range(4):
     q = lambda ev, f: np.nanmean(f(rel[:, :, ev], axis=1))
     print(f"{names[k]:7s} win {np.mean(end[idx] - prev[idx]):6.2f} | start min {q(0, np.nanmin):6.2f} max {q(0, np.nanmax):6.2f}"
           f" | pdl {q(1, np.nanmin):6.2f}/{q(1, np.nanmax):6.2f} | 1stFULL {q(2, np.nanmin):6.2f}/{q(2, np.nanmedian):6.2f}/{q(2, np.nanmax):6.2f}"
-          f" | t {q(5, np.nanmin):6.2f}/{q(5, np.nanmax):6.2f} | stg {q(6, np.nanmedian):6.2f}->{q(8, np.nanmedian):6.2f}->{q(7, np.nanmedian):6.2f} | lastFULL {q(3, np.nanmedian):6.2f}/{q(3, np.nanmax):6.2f} | epi {q(4, np.nanmedian):6.2f}/{q(4, np.nanmax):6.2f}")
+          f" | t {q(5, np.nanmin):6.2f}/{q(5, np.nanmax):6.2f} | stg {q(6, np.nanmedian):6.2f}->{q(8, np.nanmedian):6.2f}->{q(7, np.nanmedian):6.2f} | tpre {q(9, np.nanmedian):6.2f} tpass {q(10, np.nanmedian):6.2f} deep {np.mean(~np.isnan(rel[:, :, 11])):.2f} | lastFULL {q(3, np.nanmedian):6.2f}/{q(3, np.nanmax):6.2f} | epi {q(4, np.nanmedian):6.2f}/{q(4, np.nanmax):6.2f}")
 ctx.close()
