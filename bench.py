@@ -88,10 +88,11 @@ class Clocks:
 C1 = dict(N=4096, K=4096, bits=4, group=128, r=64, r_stored=64, B=1)
 
 
-def c1_bytes(c=C1):
+def c1_bytes(c=C1, r=None):
     """Algorithmic bytes of one C1 call: codes b/8 per element, a bf16
     scale + a b-bit zero per group, the rank-r slices of U and V (bf16), x (bf16) and y (fp32)."""
-    N, K, b, g, r, B = c["N"], c["K"], c["bits"], c["group"], c["r"], c["B"]
+    N, K, b, g, B = c["N"], c["K"], c["bits"], c["group"], c["B"]
+    r = c["r"] if r is None else r
     base = N * K * b // 8 + N * (K // g) * (16 + b) // 8
     fac = 2 * r * (N + K)
     io = B * (2 * K + 4 * N)
@@ -161,6 +162,29 @@ def run_c1_ours(args, rank, world, device):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     steps = reps * ncopy
+    # the same copies at r = 0 (no U / V reads, the uncompensated body): the compensation overhead
+    for i in range(ncopy):
+        ctx.set_rank(i, 0, 0, 0)
+    with torch.cuda.stream(st):
+        for i in range(ncopy):
+            ctx.compensated_linear(i, 0, x, y)
+        torch.cuda.synchronize()
+        graph0 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph0, stream=st):
+            for i in range(ncopy):
+                ctx.compensated_linear(i, 0, x, y, stream=st)
+        for _ in range(warm):
+            graph0.replay()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(st)
+        for _ in range(reps):
+            graph0.replay()
+        f1.record(st)
+        torch.cuda.synchronize()
+    ms_r0 = f0.elapsed_time(f1)
+    for i in range(ncopy):
+        ctx.set_rank(i, 0, 0, c["r"])
     # end-to-end through the public API with HOST buffers (pinned x in, y out every step)
     xh = x.cpu().pin_memory()
     yh = torch.empty((c["B"], N), dtype=torch.float32).pin_memory()
@@ -173,7 +197,7 @@ def run_c1_ours(args, rank, world, device):
         ctx.compensated_linear(i % ncopy, 0, xh, yh, stream=st)   # syncs per call (host result)
     e2e_s = time.perf_counter() - t0
     ctx.close()
-    return dict(ms=ms, steps=steps, clocks=clk.summary, e2e_s=e2e_s, n_e2e=n_e2e,
+    return dict(ms=ms, steps=steps, clocks=clk.summary, e2e_s=e2e_s, n_e2e=n_e2e, ms_r0=ms_r0,
                 launches=steps, h2d=c["B"] * K * 2, d2h=c["B"] * N * 4)
 
 
@@ -241,6 +265,21 @@ def c2_ranks(c=C2, seed=0):
     return out
 
 
+def c2_ranks_oracle(c=C2, seed=0):
+    """The same plan as c2_ranks, computed by the float64 oracle allocator (oracle/allocate.py, bit-exact
+    with hc_allocate_ranks): the reference arm does not call the library."""
+    import synth
+    from oracle import allocate as oa
+    case = synth.sensitivity_case(seed, n_layers=c["layers"], members_per_window=(3, 1, 2, 1), n_sigma=256)
+    caps = []
+    for rec in case["records"]:
+        kind, Ns, K = c2_windows(c)[rec["window"]]
+        caps.append(min(c["r_stored"], Ns[rec["slot"]], K))
+    bud = oa.Budget(D_layer=list(case["D_layer"]), top_k_layers=(c["layers"] + 3) // 4, r_std=c2_r_std(c))
+    al = oa.allocate_ranks(oa.records_from_synth(case), bud, caps)
+    return {(rec["layer"], rec["window"], rec["slot"]): int(r) for rec, r in zip(case["records"], al.ranks)}
+
+
 def c2_bytes(ranks, B, c=C2, G=1):
     """Algorithmic bytes one GPU moves per decode step: its rows of every base weight (codes, bf16 scale,
     b-bit zero), its rows of the allocated U slices and ALL of the allocated V slices (V·x is replicated
@@ -288,7 +327,9 @@ def build_c2(ctx, ranks, c=C2, shard=None):
     torch.cuda.synchronize()
 
 
-def run_c2_ours(args, rank, world, device, B, c=C2, tp=False):
+def run_c2_ours(args, rank, world, device, B, c=C2, tp=False, sweep=()):
+    """Build the stack once; time B (the bench line), the same stack at r = 0 (compensation overhead,
+    SURVEY.md §8(d)), and the batch sweep `sweep`, all with device events on the launching stream."""
     import torch
     import paper_2605_05819_b200 as hc
     ranks = c2_ranks(c)
@@ -299,26 +340,34 @@ def run_c2_ours(args, rank, world, device, B, c=C2, tp=False):
     if tp:
         ctx.init_comm(rank, world)
     build_c2(ctx, ranks, c, shard=(rank, world) if tp else None)
-    gx = torch.Generator(device="cuda").manual_seed(7 + (0 if tp else rank))
-    x = torch.randn((B, c["hidden"]), generator=gx, device="cuda").to(torch.bfloat16)
-    y = torch.empty((B, c["hidden"]), dtype=torch.bfloat16, device="cuda")
     st = torch.cuda.Stream()
-    for _ in range(max(args.warmup, 3)):
-        ctx.stack_forward(x, y, stream=st)
-    torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(device) as clk:
+
+    def timed(Bt, clocks=False):
+        gx = torch.Generator(device="cuda").manual_seed(7 + (0 if tp else rank))
+        x = torch.randn((Bt, c["hidden"]), generator=gx, device="cuda").to(torch.bfloat16)
+        y = torch.empty((Bt, c["hidden"]), dtype=torch.bfloat16, device="cuda")
+        for _ in range(max(args.warmup, 3)):
+            ctx.stack_forward(x, y, stream=st)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clk = Clocks(device) if clocks else None
+        if clk:
+            clk.__enter__()
         e0.record(st)
         for _ in range(args.steps):
             ctx.stack_forward(x, y, stream=st)
         e1.record(st)
         torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    ms = e0.elapsed_time(e1)
+        if clk:
+            clk.__exit__(None, None, None)
+        if world > 1:
+            torch.distributed.barrier()
+        return e0.elapsed_time(e1), x, y, (clk.summary if clk else None)
+
+    ms, x, y, clocks = timed(B, clocks=True)
     finite = bool(torch.isfinite(y.float()).all().item())
     # end to end through the public API with pinned HOST buffers (H2D of x, D2H of y every step)
     xh = x.cpu().pin_memory()
@@ -331,30 +380,46 @@ def run_c2_ours(args, rank, world, device, B, c=C2, tp=False):
     for _ in range(n_e2e):
         ctx.stack_forward(xh, yh, stream=st)      # synchronises (host result)
     e2e_s = time.perf_counter() - t0
+    # the same weights at r = 0 everywhere (uncompensated body: no U / V bytes, no rank projection)
+    for (l, kind, sl) in ranks:
+        ctx.set_rank(l, kind, sl, 0)
+    ms_r0 = timed(B)[0]
+    for (l, kind, sl), r in ranks.items():
+        ctx.set_rank(l, kind, sl, r)
+    sw = {}
+    for Bs in sweep:
+        mss = timed(Bs)[0]
+        sw[str(Bs)] = {"tokens_per_s": round((1 if tp else world) * Bs * args.steps / (mss * 1e-3), 1),
+                       "ms_per_step": round(mss / args.steps, 4),
+                       "GBps": round(c2_bytes(ranks, Bs, c, G) / (mss / args.steps * 1e-3) / 1e9, 1)}
     ctx.close()
     mean_rank = sum(ranks.values()) / len(ranks)
     launches = args.steps * 4 * c["layers"] * (2 if tp else 1)   # decode kernel (+ unshard permute under TP)
-    return dict(ms=ms, steps=args.steps, clocks=clk.summary, e2e_s=e2e_s, n_e2e=n_e2e, finite=finite,
+    return dict(ms=ms, steps=args.steps, clocks=clocks, e2e_s=e2e_s, n_e2e=n_e2e, finite=finite,
                 launches=launches, h2d=B * c["hidden"] * 2, d2h=B * c["hidden"] * 2,
-                bytes=c2_bytes(ranks, B, c, G), mean_rank=mean_rank, ranks=ranks)
+                bytes=c2_bytes(ranks, B, c, G), bytes_r0=c2_bytes({k: 0 for k in ranks}, B, c, G), ms_r0=ms_r0,
+                mean_rank=mean_rank, ranks=ranks, sweep=sw)
 
 
 def oracle_c2_sample(seconds: float = 15.0, c=C2):
-    """The float64 oracle on a bounded sample of the C2 workload: whole layers (all 4 windows,
-    glue included) of the Llama-2-7B-shaped stack at B = 1; tokens/s extrapolated x32 layers."""
+    """The float64 oracle on a bounded sample of the C2 workload: whole layers (all 4 windows, glue
+    included) of the Llama-2-7B-shaped stack at B = 1, at the ranks hc_allocate_ranks gives layer 0 of the
+    bench's own plan (c2_ranks).  A sampled step is one layer; tokens/s = 1 / (32 x the time per layer)."""
     import synth
     from oracle import linear
     d, kv, f = c["hidden"], c["kv"], c["ffn"]
-    mk = lambda N, K, s: synth.linear_case(100 + s, N=N, K=K, bits=c["bits"], r_stored=16, zeros="asym",
+    ranks = c2_ranks_oracle(c)
+    rr = {w: [ranks[(0, k, sl)] for sl in range(n)] for w, k, n in (("qkv", 0, 3), ("o", 1, 1), ("upgate", 2, 2), ("down", 3, 1))}
+    rs = max(16, -(-max(max(v) for v in rr.values()) // 16) * 16)
+    mk = lambda N, K, s: synth.linear_case(100 + s, N=N, K=K, bits=c["bits"], r_stored=rs, zeros="asym",
                                            unit_gain=synth.STACK_GAINS[s])
     L = dict(qkv=[mk(d, d, 0), mk(kv, d, 1), mk(kv, d, 2)], o=[mk(d, d, 3)], upgate=[mk(f, d, 4), mk(f, d, 5)],
              down=[mk(d, f, 6)])
-    R = dict(qkv=[16, 16, 16], o=[16], upgate=[16, 16], down=[16])
     h = synth.activations(1, 1, d)
     t0 = time.perf_counter()
     n = 0
     while True:
-        linear.stack_forward([L], [R], h)
+        linear.stack_forward([L], [rr], h)
         n += 1
         el = time.perf_counter() - t0
         if el >= seconds or n >= 8:
@@ -547,6 +612,36 @@ def run_c4_ours(args, rank, world, device, r_all, c=C4):
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     finite = bool(all(torch.isfinite(o.float()).all().item() for o in outs.values()))
+    # the rank sweep of C4 on the same weights: r = 0 (the uncompensated GEMM) and r = 256 (the largest level)
+    rank_ms = {}
+    for rr in (0, 256):
+        if rr == r_all:
+            continue
+        for l in range(c["layers"]):
+            for kind, Ns, K in c4_windows(c):
+                for sl in range(len(Ns)):
+                    ctx.set_rank(l, kind, sl, rr)
+        with torch.cuda.stream(st):
+            step()
+            torch.cuda.synchronize()
+            g2 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g2, stream=st):
+                step()
+            g2.replay()
+            torch.cuda.synchronize()
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record(st)
+            for _ in range(args.steps):
+                g2.replay()
+            f1.record(st)
+            torch.cuda.synchronize()
+        fl = sum(2 * M * N * K + 2 * M * rr * (N + K) for _, Ns, K in c4_windows(c) for N in Ns) * c["layers"]
+        rank_ms[rr] = (f0.elapsed_time(f1), fl)
+        del g2
+    for l in range(c["layers"]):
+        for kind, Ns, K in c4_windows(c):
+            for sl in range(len(Ns)):
+                ctx.set_rank(l, kind, sl, r_all)
     # end to end: host X in, the last window's output back to the host, every window through the API
     xh = {K: v.cpu() for K, v in xs.items()}
     yh = np.zeros((M, c["hidden"]), dtype=np.uint16)
@@ -558,7 +653,7 @@ def run_c4_ours(args, rank, world, device, r_all, c=C4):
     e2e_s = time.perf_counter() - t0
     ctx.close()
     return dict(ms=ms, steps=args.steps, clocks=clk.summary, e2e_s=e2e_s, n_e2e=n_e2e, finite=finite, flops=flops,
-                launches=args.steps * c["layers"] * 4 * 3, h2d=c["layers"] * 4 * M * 4096 * 2, d2h=c["layers"] * 2 * M * 4096 * 2)
+                rank_ms=rank_ms, launches=args.steps * c["layers"] * 4 * 3, h2d=c["layers"] * 4 * M * 4096 * 2, d2h=c["layers"] * 2 * M * 4096 * 2)
 
 
 def oracle_c4_sample(seconds: float = 15.0, c=C4, r=64):
@@ -581,16 +676,16 @@ def oracle_c4_sample(seconds: float = 15.0, c=C4, r=64):
 
 
 def traffic_of(args):
-    """DRAM bytes per step of the dominant kernel from one ncu --set full capture (profiles/r01/
-    ncu_c2_layer_dram.json: the 4 decode windows of one C2 layer, 111.3 MB, x 32 layers); the algorithmic
-    bytes of the same step are config.bytes_per_step.  Null where no capture exists."""
-    if args.workload == "c2" and args.batch == 1:
-        try:
-            with open(os.path.join(ROOT, "profiles", "r01", "ncu_c2_layer_dram.json")) as f:
-                return round(json.load(f)["layer_dram_MB"] * 1e6 * 32)
-        except Exception:
-            return None
-    return None
+    """DRAM bytes per step of the timed kernels from one ncu capture of this code version
+    (profiles/r02/traffic.json: dram__bytes_read.sum + dram__bytes_write.sum over the decode launches of one
+    step, summed, written by tools/ncu_traffic.py); the algorithmic bytes of the same step are
+    roofline.bytes_per_step.  Null where no capture exists for the workload / batch."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02", "traffic.json")) as f:
+            t = json.load(f)
+        return t.get(f"{args.workload}_B{args.batch}")
+    except Exception:
+        return None
 
 
 def cores():
@@ -615,8 +710,19 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--rank-override", type=int, default=None, help="dev: use this rank for every matrix")
     ap.add_argument("--moe-dynamic", action="store_true", help="c3: per-(token, expert) dynamic ranks (P:652-665)")
+    ap.add_argument("--no-sweep", action="store_true", help="c2: skip the default B = 2/4/8/16 sweep")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        # one process per GPU: re-launch this command under torch.distributed.run (the driver's own launch
+        # sets WORLD_SIZE and skips this)
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
 
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -658,26 +764,28 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
+        # a sampled step is one unit of the workload the oracle ran in full (C1: one call; C2: one layer;
+        # C3: one MoE layer; C4: one O-window product on 256 tokens); ms_per_step is its measured time, so
+        # steps x ms_per_step is the wall time of the sample, and value converts it to the workload's metric
         if args.workload == "c1":
             n, el = oracle_c1_sample(seconds=max(5.0, min(60.0, 0.05 * (args.steps + args.warmup))))
             val, unit = c1_bytes() * n / el / 1e9, "GB/s"
-            sample = f"{n} whole C1 calls (numpy float64, unpack+dequant+matvec)"
-            ms = 1e3 * el / n
+            sample = f"{n} whole C1 calls (numpy float64, unpack+dequant+matvec); step = one call"
         elif args.workload == "c4":
             val, n, el = oracle_c4_sample(seconds=20.0, r=config["rank"])
             unit = "tokens/s"
-            sample = f"{n} O-window products (256 tokens, 4096x4096, float64), flop-scaled to the 32-layer step"
-            ms = 1e3 * 2048 / val
+            sample = (f"{n} O-window products (256 tokens, 4096x4096, rank {config['rank']}, float64), flop-scaled "
+                      f"to the 32-layer step; step = one product")
         elif args.workload == "c3":
             val, n, el = oracle_c3_sample(seconds=20.0, T=args.batch)
             unit = "tokens/s"
-            sample = f"{n} whole MoE layers ({args.batch} tokens, top-8 of 128 experts, float64), extrapolated x48 layers"
-            ms = 1e3 * args.batch / val
+            sample = f"{n} whole MoE layers ({args.batch} tokens, top-8 of 128 experts, float64), x48 layers; step = one layer"
         else:
             val, n, el = oracle_c2_sample(seconds=20.0)
             unit = "tokens/s"
-            sample = f"{n} whole Llama-2-7B layers at B=1 (float64, all 4 windows + glue), extrapolated x32 layers"
-            ms = 1e3 / val
+            sample = (f"{n} whole Llama-2-7B layers at B=1 (float64, all 4 windows + glue, allocator ranks of layer 0), "
+                      f"x32 layers; step = one layer")
+        ms = 1e3 * el / n
         line = {"impl": "reference", "metric": METRIC, "value": round(val, 6), "unit": unit, "n_gpus": args.gpus,
                 "steps": n, "warmup": 0, "ms_per_step": round(ms, 3), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
@@ -704,7 +812,10 @@ def main():
         nbytes = c1_bytes()
         unit, kernel = "GB/s", "hc::decode_kernel<4,1,true,true> (int8 mma path)"
     else:
-        r = run_c2_ours(args, rank, world, local, args.batch, STACKS[args.workload], tp)
+        sweep = () if (args.workload != "c2" or args.no_sweep) else tuple(b for b in (1, 2, 4, 8, 16) if b != args.batch)
+        if args.sweep and args.workload == "c5":
+            sweep = (2, 4, 8, 16)
+        r = run_c2_ours(args, rank, world, local, args.batch, STACKS[args.workload], tp, sweep=sweep)
         nbytes = r["bytes"]
         unit, kernel = "tokens/s", "hc::decode_kernel (4 fused windows per layer; int8 mma path where x8 fits)"
     per_rank = torch.tensor([r["ms"]], dtype=torch.float64, device="cuda")
@@ -752,14 +863,33 @@ def main():
                                   "ms_per_step": round(rs["ms"] / rs["steps"], 4),
                                   "GBps": round(rs["bytes"] / (rs["ms"] / rs["steps"] * 1e-3) / 1e9, 1)}
             line["token_sweep"] = sweep
-        elif args.workload not in ("c1", "c3") and args.sweep:
-            sweep = {}
-            for Bs in (2, 4, 8, 16):
-                rs = run_c2_ours(args, rank, world, local, Bs, STACKS[args.workload], tp)
-                sweep[str(Bs)] = {"tokens_per_s": round(Bs * rs["steps"] / (rs["ms"] * 1e-3), 1),
-                                  "ms_per_step": round(rs["ms"] / rs["steps"], 4),
-                                  "GBps": round(rs["bytes"] / (rs["ms"] / rs["steps"] * 1e-3) / 1e9, 1)}
-            line["batch_sweep"] = sweep
+        elif r.get("sweep"):
+            line["batch_sweep"] = r["sweep"]
+        # compensation overhead against the same weights at r = 0 (the paper's analogue is
+        # "≥85% of throughput"): time ratio - 1 beside the algorithmic byte / flop floor of the factors
+        if args.workload == "c1":
+            b0 = c1_bytes(r=0)
+            line["overhead_vs_r0"] = {"rank": C1["r"], "time": round(r["ms"] / r["ms_r0"] - 1, 4),
+                                      "bytes_floor": round(nbytes / b0 - 1, 4),
+                                      "r0_GBps_of_r0_bytes": round(b0 * r["steps"] / (r["ms_r0"] * 1e-3) / 1e9, 1)}
+        elif args.workload in ("c2", "c5"):
+            line["overhead_vs_r0"] = {"rank": "allocated" if args.workload == "c2" else STACKS[args.workload]["fixed_rank"],
+                                      "time": round(r["ms"] / r["ms_r0"] - 1, 4),
+                                      "bytes_floor": round(r["bytes"] / r["bytes_r0"] - 1, 4),
+                                      "r0_tokens_per_s": round(args.batch * r["steps"] / (r["ms_r0"] * 1e-3), 2)}
+        elif args.workload == "c4":
+            rs_ = {str(config["rank"]): {"TFLOPS": round(tfl, 1), "ms_per_step": round(r["ms"] / r["steps"], 4)}}
+            for rr, (mss, fl) in r["rank_ms"].items():
+                rs_[str(rr)] = {"TFLOPS": round(fl / (mss / r["steps"] * 1e-3) / 1e12, 1),
+                                "ms_per_step": round(mss / r["steps"], 4)}
+            line["rank_sweep"] = rs_
+            if 0 in r["rank_ms"]:
+                ms0, fl0 = r["rank_ms"][0]
+                ov = {str(config["rank"]): {"time": round(r["ms"] / ms0 - 1, 4), "flops_floor": round(r["flops"] / fl0 - 1, 4)}}
+                if 256 in r["rank_ms"]:
+                    ms2, fl2 = r["rank_ms"][256]
+                    ov["256"] = {"time": round(ms2 / ms0 - 1, 4), "flops_floor": round(fl2 / fl0 - 1, 4)}
+                line["overhead_vs_r0"] = ov
         if not args.no_cpu_baseline:
             if args.workload == "c1":
                 n, el = oracle_c1_sample(12.0)
