@@ -207,6 +207,41 @@ hc_status hc_moe_last_ranks(hc_ctx* ctx, int32_t* out, int32_t T, int32_t topk);
 hc_status hc_nccl_unique_id(uint8_t* out128);
 hc_status hc_set_comm(hc_ctx* ctx, const uint8_t* id128, int32_t rank, int32_t world);
 
+/* =====================================================================================
+ * Calibration (offline, on the GPU).  Produces the compensation factors and the
+ * allocator's spectrum input; not on the decode hot path.
+ * ===================================================================================== */
+
+/* Factors of the quantization error: ΔW = W − deq(codes, scales, zeros) in float64
+ * (deq as hcinfer.h's canonical formats, R1-R3), its SVD ΔW = P·diag(σ)·Qᵀ by one-sided Jacobi in
+ * float64 (the shorter side of ΔW is orthogonalised; fixed-order reductions, deterministic), and
+ *   U = P[:, :r]  (float64 [n_mats][N][r]),   V = diag(σ[:r])·Q[:, :r]ᵀ  (float64 [n_mats][r][K])   (R4)
+ * with the sign convention "first nonzero entry of each U column >= 0" (R5); sigma (float64 [n_mats][min(N,K)],
+ * non-increasing) if non-NULL.  Batched over n_mats matrices of one shape.  All pointers device memory;
+ * W float32 [n_mats][N][K] (the unquantized weights), codes / scales / zeros canonical [n_mats][N][...].
+ * N, K multiples of 32; group divides K; bits in {2, 3, 4, 8}; 0 <= r <= min(N, K).  sweeps_out (host,
+ * nullable): Jacobi sweeps run.  Synchronises the stream (the convergence test reads a device word per
+ * sweep).  Workspace: context-owned, about 16·N·K·n_mats bytes.  HC_ERR_CONFIG on bad shapes or
+ * pointers. */
+hc_status hc_calib_svd(hc_ctx* ctx, const float* W, const uint32_t* codes, const uint16_t* scales, const uint8_t* zeros,
+                       int32_t n_mats, int32_t N, int32_t K, int32_t bits, int32_t group, int32_t r,
+                       double* U_out, double* V_out, double* sigma_out, int32_t* sweeps_out, void* stream);
+
+/* Salience φ of each spectrum (App. B.1 eq. A8, R10) on the device: σ̂ = σ/σ₁,
+ * k_j = σ̂_{j−1} − 2σ̂_j + σ̂_{j+1} over interior j, cut = argmax (smallest index on ties), S = {1..cut} iff
+ * max k > tau, φ = mean_S σ / max(mean_R σ, 1e-300), else φ = 1 (n < 3 or σ₁ = 0: φ = 1).  sigma: device
+ * float64 [n_mats][n]; phi_out device float64 [n_mats]; n_salient_out device int32 [n_mats] (|S|, 0 if ∅).
+ * The float64 operations of oracle/allocate.py salience in its order (no contraction): bit-exact given σ. */
+hc_status hc_calib_salience(hc_ctx* ctx, const double* sigma, int32_t n_mats, int32_t n, double tau,
+                            double* phi_out, int32_t* n_salient_out, void* stream);
+
+/* B200 budget r_std of a compensation window (R17, the analogue of P:278-289's CPU-time budget):
+ * the largest rank whose factor bytes stay within eps of the window's base bytes,
+ *   r_std = floor(eps · bytes_base / (2·(N̄ + K))),  bytes_base = Σ_i N_i·K·bits/8 + N_i·(K/group)·(16 + bits)/8,
+ * N̄ = mean N_i (eps = 0.1 for the ≤10% target).  Host only, pure. */
+hc_status hc_calib_r_std(const int32_t* Ns, int32_t n_members, int32_t K, int32_t bits, int32_t group, double eps,
+                         double* r_std_out);
+
 /* Process-wide development switches, for A/B timing of equivalent plans (every setting computes the same
  * product up to fp32 accumulation order; the parity tests pass under each).  Read when a window plan or a
  * stack graph is built; setting one makes contexts re-capture their stack graphs on the next call.

@@ -283,3 +283,13 @@ def records_from_synth(case: dict) -> list:
     return [Record(layer=r["layer"], window=r["window"], slot=r["slot"], expert=r["expert"],
                    sigma=np.asarray(r["sigma"], dtype=np.float64), D=r["D"], gate=r["gate"])
             for r in case["records"]]
+
+
+# ---------------------------------------------------------------- r_std on B200 (R17)
+def r_std_bytes(Ns, K: int, bits: int, group: int = 128, eps: float = 0.1) -> float:
+    """B200 reading of the budget r_std (SURVEY.md §8(c) "Proposed B200 meaning", R17; the paper's
+    r_std is a CPU-time budget): the largest rank whose factor bytes 2·r·(N̄ + K) stay within eps
+    of the window's base bytes Σ_i N_i·K·b/8 + N_i·(K/g)·(16 + b)/8 (codes, bf16 scale, b-bit zero)."""
+    base = sum(N * K * bits // 8 + N * (K // group) * (16 + bits) // 8 for N in Ns)
+    nbar = sum(Ns) / len(Ns)
+    return float(math.floor(eps * base / (2 * (nbar + K))))

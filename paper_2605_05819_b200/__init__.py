@@ -18,7 +18,15 @@ from ._lib import (HCError, HC_OK, HC_ERR_CONFIG, HC_ERR_STATE, HC_ERR_NUMERIC, 
 
 __all__ = ["allocate_ranks", "Context", "HCError", "QKV", "O", "UPGATE", "DOWN", "OUT_F32", "OUT_BF16",
            "GLUE_NONE", "GLUE_SILU_MUL",
-           "repack_host", "unpack_repacked_host", "shard_rows", "unshard_host", "set_option", "get_option", "lib"]
+           "repack_host", "unpack_repacked_host", "shard_rows", "unshard_host", "set_option", "get_option", "calib_r_std", "lib"]
+
+
+def calib_r_std(Ns, K, bits, group=128, eps=0.1) -> float:
+    """hc_calib_r_std: B200 byte-budget r_std of a window (R17)."""
+    arr = np.ascontiguousarray(Ns, dtype=np.int32)
+    out = C.c_double(0.0)
+    check(lib().hc_calib_r_std(arr.ctypes.data, int(arr.size), int(K), int(bits), int(group), float(eps), C.addressof(out)))
+    return float(out.value)
 
 
 def set_option(name: str, value: int) -> None:
@@ -246,6 +254,23 @@ class Context:
         out = np.zeros((int(T), int(topk), 3), dtype=np.int32)
         check(lib().hc_moe_last_ranks(self._h, out.ctypes.data, int(T), int(topk)))
         return out
+
+    def calib_svd(self, W, codes, scales, zeros, bits, group, r, U, V, sigma=None, stream=None):
+        """hc_calib_svd: device tensors W fp32 [M, N, K], canonical codes int32 [M, N, K*bits/32], scales bf16
+        [M, N, K/g], zeros uint8 [M, N, K/g]; outputs float64 U [M, N, r], V [M, r, K], sigma [M, min(N, K)].
+        Returns the number of Jacobi sweeps."""
+        M, N, K = (int(v) for v in W.shape)
+        sw = C.c_int32(0)
+        check(lib().hc_calib_svd(self._h, _ptr(W), _ptr(codes), _ptr(scales), _ptr(zeros), M, N, K, int(bits),
+                                 int(group), int(r), _ptr(U) if U is not None else None,
+                                 _ptr(V) if V is not None else None, _ptr(sigma) if sigma is not None else None,
+                                 C.addressof(sw), _stream(stream)))
+        return int(sw.value)
+
+    def calib_salience(self, sigma, phi, n_salient, tau=0.01, stream=None):
+        """hc_calib_salience: device float64 sigma [M, n] -> phi float64 [M], n_salient int32 [M]."""
+        M, n = (int(v) for v in sigma.shape)
+        check(lib().hc_calib_salience(self._h, _ptr(sigma), M, n, float(tau), _ptr(phi), _ptr(n_salient), _stream(stream)))
 
     def compensated_linear(self, layer, window, x, y, B=None, expert=-1, out_dtype=OUT_F32, stream=None):
         """y[b, :] = concat_m ( deq(W_m)·x_b + U_m[:, :r_m]·(V_m[:r_m, :]·x_b) ).

@@ -46,6 +46,12 @@ class hc_matrix_desc(C.Structure):
 SIGNATURES = [
     ("hc_version", C.c_char_p, []),
     ("hc_set_option", C.c_int, [C.c_char_p, C.c_int32]),
+    ("hc_calib_svd", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
+                               C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                               C.c_void_p, C.c_void_p]),
+    ("hc_calib_salience", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_double, C.c_void_p, C.c_void_p,
+                                    C.c_void_p]),
+    ("hc_calib_r_std", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_void_p]),
     ("hc_get_option", C.c_int, [C.c_char_p, C.c_void_p]),
     ("hc_last_error", C.c_char_p, []),
     ("hc_allocate_ranks", C.c_int, [C.POINTER(hc_sens), C.c_int32, C.POINTER(hc_budget), C.POINTER(C.c_int32),

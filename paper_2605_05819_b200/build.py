@@ -18,7 +18,7 @@ BUILD = os.path.join(PKG, "_build")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["api.cu", "comm.cu", "decode.cu", "prefill.cu", "repack.cu", "moe.cu"]
+CU_SOURCES = ["api.cu", "comm.cu", "decode.cu", "prefill.cu", "repack.cu", "moe.cu", "calib.cu"]
 CPP_SOURCES = ["alloc.cpp"]
 
 

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -10,6 +11,7 @@
 #include <tuple>
 #include <vector>
 
+#include "calib.h"
 #include "comm.h"
 #include "options.h"
 #include "decode.h"
@@ -123,6 +125,7 @@ struct hc_ctx {
   };
   std::map<int, MoECache> moe;
   DevBuf moe_ws, moe_idx, moe_gate;
+  DevBuf calib_ws;                     // hc_calib_svd workspace
   // the last hc_moe_forward with dynamic ranks (hc_moe_last_ranks): routing shape and device tables
   struct { int T = 0, topk = 0; const int* tok_row = nullptr; const uint16_t* row_rank = nullptr; } moe_last;
   void invalidate_graphs() {
@@ -1210,5 +1213,57 @@ extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, voi
   CUDA_TRY(cudaGraphLaunch(git->second->exec, st));
   if (hy) CUDA_TRY(cudaMemcpyAsync(y, dy, hb, cudaMemcpyDeviceToHost, st));
   if (hx || hy) CUDA_TRY(cudaStreamSynchronize(st));
+  return HC_OK;
+}
+
+// ------------------------------------------------------------------ calibration
+extern "C" hc_status hc_calib_svd(hc_ctx* ctx, const float* W, const uint32_t* codes, const uint16_t* scales,
+                                  const uint8_t* zeros, int32_t n_mats, int32_t N, int32_t K, int32_t bits,
+                                  int32_t group, int32_t r, double* U_out, double* V_out, double* sigma_out,
+                                  int32_t* sweeps_out, void* stream) {
+  if (!ctx) return fail(HC_ERR_STATE, "hc_calib_svd: null context");
+  if (n_mats < 1 || N < 32 || K < 32 || N % 32 || K % 32)
+    return fail(HC_ERR_CONFIG, "hc_calib_svd: n_mats %d, N %d, K %d (N, K multiples of 32)", n_mats, N, K);
+  if (!(bits == 2 || bits == 3 || bits == 4 || bits == 8) || group < 1 || K % group || (K * bits) % 32)
+    return fail(HC_ERR_CONFIG, "hc_calib_svd: bits %d / group %d", bits, group);
+  if (r < 0 || r > std::min(N, K)) return fail(HC_ERR_CONFIG, "hc_calib_svd: rank %d outside [0, min(N, K)]", r);
+  if (!W || !codes || !scales || !zeros || (r > 0 && (!U_out || !V_out)))
+    return fail(HC_ERR_CONFIG, "hc_calib_svd: null input / output");
+  for (const void* p : {(const void*)W, (const void*)codes, (const void*)scales, (const void*)zeros})
+    if (!is_device_ptr(p)) return fail(HC_ERR_CONFIG, "hc_calib_svd: inputs must be device pointers");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  const size_t need = hc::calib_workspace_bytes(n_mats, N, K, r);
+  if (ctx->calib_ws.bytes < need) CUDA_TRY(ctx->calib_ws.alloc(need));
+  hc::CalibSvdArgs a{W, codes, scales, zeros, n_mats, N, K, bits, group, r, U_out, V_out, sigma_out, 40, 1e-15};
+  int sweeps = 0;
+  CUDA_TRY(hc::calib_svd(a, ctx->calib_ws.p, (cudaStream_t)stream, &sweeps));
+  if (sweeps_out) *sweeps_out = sweeps;
+  return HC_OK;
+}
+
+extern "C" hc_status hc_calib_salience(hc_ctx* ctx, const double* sigma, int32_t n_mats, int32_t n, double tau,
+                                       double* phi_out, int32_t* n_salient_out, void* stream) {
+  if (!ctx) return fail(HC_ERR_STATE, "hc_calib_salience: null context");
+  if (n_mats < 1 || n < 1 || !sigma || !phi_out || !n_salient_out || !std::isfinite(tau))
+    return fail(HC_ERR_CONFIG, "hc_calib_salience: bad arguments");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  CUDA_TRY(hc::calib_salience(sigma, n_mats, n, tau, phi_out, n_salient_out, (cudaStream_t)stream));
+  return HC_OK;
+}
+
+extern "C" hc_status hc_calib_r_std(const int32_t* Ns, int32_t n_members, int32_t K, int32_t bits, int32_t group,
+                                    double eps, double* r_std_out) {
+  if (!Ns || n_members < 1 || !r_std_out || K < 1 || group < 1 || K % group || !(eps > 0.0) || !std::isfinite(eps))
+    return fail(HC_ERR_CONFIG, "hc_calib_r_std: bad arguments");
+  if (!(bits == 2 || bits == 3 || bits == 4 || bits == 8)) return fail(HC_ERR_CONFIG, "hc_calib_r_std: bits %d", bits);
+  long long bytes = 0, nsum = 0;
+  for (int i = 0; i < n_members; ++i) {
+    if (Ns[i] < 1) return fail(HC_ERR_CONFIG, "hc_calib_r_std: N[%d] = %d", i, Ns[i]);
+    const long long N = Ns[i];
+    bytes += N * K * bits / 8 + N * (K / group) * (16 + bits) / 8;
+    nsum += N;
+  }
+  const double nbar = (double)nsum / (double)n_members;
+  *r_std_out = std::floor(eps * (double)bytes / (2.0 * (nbar + (double)K)));
   return HC_OK;
 }

@@ -217,3 +217,30 @@ def test_brute_force_examples():
     t2 = [brute.gain_table([5.0] * 20, 1.0, [0, 8, 16]), brute.gain_table([1.0] * 20, 1.0, [0, 8, 16])]
     assert brute.brute_force(t2, [0, 8, 16], 16)[0] == [16, 0]
     assert brute.brute_force(t2, [0, 8, 16], 0) == ([0, 0], 0.0)
+
+
+def test_r_std_bytes_hand_values():
+    """R17 pinned by hand: Llama-2-7B QKV (3 x 4096x4096, 4-bit g128) has base bytes 3·(8388608 + 327680) =
+    26148864, N̄ + K = 8192, so r_std = floor(0.1·26148864 / 16384) = floor(159.6) = 159 (SURVEY.md §8(c)
+    quotes ≈ 159); a single 4096² 2-bit matrix: 4194304 + 4096·32·18/8 = 4489216 -> floor(448921.6/16384) = 27."""
+    from oracle.allocate import r_std_bytes
+    assert r_std_bytes([4096, 4096, 4096], 4096, 4) == 159.0
+    assert r_std_bytes([4096], 4096, 2) == 27.0
+    # scale invariance of the rule: doubling every N and K doubles the bytes per unit rank and the base
+    # bytes by 4 -> r_std doubles (up to the floor)
+    assert abs(r_std_bytes([8192], 8192, 4) - 2 * r_std_bytes([4096], 4096, 4)) <= 1
+
+
+def test_r_std_library_bit_exact():
+    """hc_calib_r_std (host C++) equals the oracle's rule bit for bit on the bench windows and random ones."""
+    import paper_2605_05819_b200 as hc
+    from oracle.allocate import r_std_bytes
+    g = np.random.default_rng(5)
+    cases = [([4096, 4096, 4096], 4096, 4), ([4096], 4096, 4), ([11008, 11008], 4096, 4), ([4096], 11008, 4),
+             ([8192, 1024, 1024], 8192, 2), ([28672, 28672], 8192, 2), ([768, 768], 2048, 3), ([2048], 768, 3)]
+    for _ in range(50):
+        cases.append(([int(v) * 16 for v in g.integers(1, 800, size=int(g.integers(1, 5)))], int(g.integers(1, 100)) * 128,
+                      int(g.choice([2, 3, 4, 8]))))
+    for Ns, K, b in cases:
+        for eps in (0.1, 0.05, 0.25):
+            assert hc.calib_r_std(Ns, K, b, 128, eps) == r_std_bytes(Ns, K, b, 128, eps), (Ns, K, b, eps)
