@@ -337,9 +337,12 @@ def run_c2_ours(args, rank, world, device, B, c=C2, tp=False, sweep=()):
         ranks = {k: args.rank_override for k in ranks}
     ctx = hc.Context(device)
     G = world if tp else 1
-    if tp:
+    peer = tp and getattr(args, "tp_path", "peer") == "peer"
+    if tp and not peer:
         ctx.init_comm(rank, world)
     build_c2(ctx, ranks, c, shard=(rank, world) if tp else None)
+    if peer:
+        ctx.init_peers(rank, world)      # gather fused into the decode epilogue over peer memory
     st = torch.cuda.Stream()
 
     def timed(Bt, clocks=False):
@@ -394,7 +397,8 @@ def run_c2_ours(args, rank, world, device, B, c=C2, tp=False, sweep=()):
                        "GBps": round(c2_bytes(ranks, Bs, c, G) / (mss / args.steps * 1e-3) / 1e9, 1)}
     ctx.close()
     mean_rank = sum(ranks.values()) / len(ranks)
-    launches = args.steps * 4 * c["layers"] * (2 if tp else 1)   # decode kernel (+ unshard permute under TP)
+    # decode kernels (+ the NCCL path's unshard permute per window; + the peer path's final gather wait)
+    launches = args.steps * (4 * c["layers"] * (2 if (tp and not peer) else 1) + (1 if peer else 0))
     return dict(ms=ms, steps=args.steps, clocks=clocks, e2e_s=e2e_s, n_e2e=n_e2e, finite=finite,
                 launches=launches, h2d=B * c["hidden"] * 2, d2h=B * c["hidden"] * 2,
                 bytes=c2_bytes(ranks, B, c, G), bytes_r0=c2_bytes({k: 0 for k in ranks}, B, c, G), ms_r0=ms_r0,
@@ -711,6 +715,9 @@ def main():
     ap.add_argument("--rank-override", type=int, default=None, help="dev: use this rank for every matrix")
     ap.add_argument("--moe-dynamic", action="store_true", help="c3: per-(token, expert) dynamic ranks (P:652-665)")
     ap.add_argument("--no-sweep", action="store_true", help="c2: skip the default B = 2/4/8/16 sweep")
+    ap.add_argument("--tp-path", default="peer", choices=["peer", "nccl"],
+                    help="N>1 column sharding: peer = gather fused into the decode epilogue over NVLink peer "
+                         "memory with partial-t exchange (default); nccl = ncclAllGather + unshard per window")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
@@ -753,7 +760,9 @@ def main():
         desc = ("c2: Llama-2-7B-shaped 32-layer decode stack, 4-bit g128 + dynamic ranks (hc_allocate_ranks, "
                 "r_std = 10%-bytes rule)" if args.workload == "c2" else
                 "c5: Llama-3-70B-shaped 80-layer decode stack, 2-bit g128 + rank-64 compensation")
-        config = {"workload": desc + (f", column-sharded over {world} GPUs (NCCL all-gather per window)" if tp else
+        config = {"workload": desc + ((f", column-sharded over {world} GPUs (" + ("gather fused into the decode epilogue over "
+                                       "peer memory, partial-t exchange" if args.tp_path == "peer" else "NCCL all-gather per window")
+                                       + ")") if tp else
                                       (f", {world} independent replicas" if world > 1 else ", 1 GPU")),
                   "layers": c["layers"], "hidden": c["hidden"], "kv": c["kv"], "ffn": c["ffn"], "bits": c["bits"],
                   "group": 128, "r_stored": c["r_stored"], "batch": args.batch,

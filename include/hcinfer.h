@@ -251,9 +251,31 @@ hc_status hc_calib_r_std(const int32_t* Ns, int32_t n_members, int32_t K, int32_
  *   "int8_path"          1  decode: u8·s8 tensor-core path for 2-/4-bit codes at B <= 2 (§7.1)
  *   "prefill_merge"      1  prefill: one GEMM over a multi-member window (§7.5)
  *   "decode_ctas_per_sm" 0  decode: cap on resident CTAs per SM (0 = the occupancy limit)
+ *   "pdl"                1  decode: programmatic dependent launch between consecutive windows
  * HC_ERR_CONFIG for an unknown name or a negative value.  Not thread-safe against concurrent launches. */
 hc_status hc_set_option(const char* name, int32_t value);
 hc_status hc_get_option(const char* name, int32_t* value);
+
+/* Peer mode: the column-sharded stack with the gather FUSED into the decode epilogue.
+ * Every window's epilogue stores its output rows into the full-width activation buffer of every rank (peer
+ * memory over NVLink / NVSwitch), adds the next window's t partials of its own output slice
+ * (V_next[:, slice]·y_slice) into every rank's t accumulators — so no rank recomputes V·x over the full x —
+ * and bumps every rank's gather counter with a system-scope release; the next window waits for G times its
+ * producer's rows (system-scope acquire).  No NCCL call, no unshard kernel, one launch per window.  After the
+ * last layer one tiny kernel waits for the final gather and copies it to y.
+ * Setup, after every rank loaded its shard (rows [rank·N/G, (rank+1)·N/G) of every member):
+ *   hc_peer_region(ctx, G, &base, &bytes)   allocates this rank's region (gathered activations, per-window
+ *                                          counters and t accumulators; the same layout on every rank)
+ *   then EITHER hc_peer_ipc_handle + exchange (e.g. torch.distributed) + hc_peer_connect  (one process per GPU)
+ *   OR hc_peer_set with the bases already mapped in this process.
+ * Then hc_stack_forward runs the peer graph (priority over hc_set_comm's NCCL path).  Ranks must call
+ * hc_stack_forward with the same B and x, concurrently; a rank whose peers never arrive traps after ~20 s
+ * (HC_ERR_RUNTIME) instead of hanging.  2 <= G <= 8.  hc_peer_region again after hc_set_rank raises a
+ * window's rank beyond the region's t capacity. */
+hc_status hc_peer_region(hc_ctx* ctx, int32_t world, void** base_out, uint64_t* bytes_out);
+hc_status hc_peer_ipc_handle(hc_ctx* ctx, uint8_t* out64);
+hc_status hc_peer_connect(hc_ctx* ctx, int32_t rank, int32_t world, const uint8_t* handles /* [world][64] */);
+hc_status hc_peer_set(hc_ctx* ctx, int32_t rank, int32_t world, void* const* bases /* [world] */);
 
 /* Debug/test exports (host only, no GPU needed): the load-time repack and its inverse. */
 size_t hc_repacked_bytes(int32_t N, int32_t K, int32_t bits);

@@ -209,6 +209,29 @@ class Context:
         buf = np.frombuffer(obj[0], dtype=np.uint8).copy()
         check(lib().hc_set_comm(self._h, buf.ctypes.data, int(rank), int(world)))
 
+    def peer_region(self, world: int):
+        """hc_peer_region: allocate this rank's peer region for the loaded shard; returns (base, bytes)."""
+        base, nb = C.c_void_p(0), C.c_uint64(0)
+        check(lib().hc_peer_region(self._h, int(world), C.addressof(base), C.addressof(nb)))
+        return int(base.value), int(nb.value)
+
+    def peer_set(self, rank: int, world: int, bases):
+        """hc_peer_set: every rank's region base, already mapped in this process (in-process ranks)."""
+        arr = (C.c_void_p * len(bases))(*[int(b) for b in bases])
+        check(lib().hc_peer_set(self._h, int(rank), int(world), C.addressof(arr)))
+
+    def init_peers(self, rank: int, world: int, group=None):
+        """One process per GPU: allocate the peer region, exchange CUDA IPC handles through torch.distributed
+        (any backend), hc_peer_connect."""
+        import torch.distributed as dist
+        self.peer_region(world)
+        h = np.zeros(64, dtype=np.uint8)
+        check(lib().hc_peer_ipc_handle(self._h, h.ctypes.data))
+        allh = [None] * world
+        dist.all_gather_object(allh, h.tobytes(), group=group)
+        buf = np.frombuffer(b"".join(allh), dtype=np.uint8).copy()
+        check(lib().hc_peer_connect(self._h, int(rank), int(world), buf.ctypes.data))
+
     def set_rank(self, layer, window, slot, r, expert=-1):
         check(lib().hc_set_rank(self._h, layer, window, slot, expert, r))
 

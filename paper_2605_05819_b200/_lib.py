@@ -46,6 +46,10 @@ class hc_matrix_desc(C.Structure):
 SIGNATURES = [
     ("hc_version", C.c_char_p, []),
     ("hc_set_option", C.c_int, [C.c_char_p, C.c_int32]),
+    ("hc_peer_region", C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    ("hc_peer_ipc_handle", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("hc_peer_connect", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    ("hc_peer_set", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
     ("hc_calib_svd", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                C.c_void_p, C.c_void_p]),

@@ -126,6 +126,17 @@ struct hc_ctx {
   std::map<int, MoECache> moe;
   DevBuf moe_ws, moe_idx, moe_gate;
   DevBuf calib_ws;                     // hc_calib_svd workspace
+  // peer mode (hc_peer_region / hc_peer_set / hc_peer_connect): column-sharded stack with the gather fused
+  // into the decode epilogue over peer memory.  The region has the same layout on every
+  // rank: the four gathered activations, then per window a gather counter and the t accumulators.
+  struct Peer {
+    bool on = false;
+    DevBuf region;
+    void* base[hc::kMaxPeers] = {};    // every rank's region mapped in this process (own included)
+    std::vector<void*> opened;         // IPC mappings to close
+    size_t off_qkv = 0, off_h1 = 0, off_m = 0, off_h = 0, off_win = 0, win_stride = 0, bytes = 0;
+    int n_win = 0, G = 0, mc = 0;
+  } peer;
   // the last hc_moe_forward with dynamic ranks (hc_moe_last_ranks): routing shape and device tables
   struct { int T = 0, topk = 0; const int* tok_row = nullptr; const uint16_t* row_rank = nullptr; } moe_last;
   void invalidate_graphs() {
@@ -174,6 +185,7 @@ extern "C" hc_status hc_destroy(hc_ctx* ctx) {
   ctx->graphs.clear();
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   hc::comm_destroy(ctx->comm);
+  for (void* p : ctx->peer.opened) cudaIpcCloseMemHandle(p);
   delete ctx;
   return HC_OK;
 }
@@ -413,7 +425,8 @@ extern "C" hc_status hc_set_option(const char* name, int32_t value) {
   hc::Options& o = hc::options();
   const std::pair<const char*, int*> tab[] = {{"t_forward", &o.t_forward},       {"x_handoff", &o.x_handoff},
                                               {"dep_wait", &o.dep_wait},         {"int8_path", &o.int8_path},
-                                              {"prefill_merge", &o.prefill_merge}, {"decode_ctas_per_sm", &o.decode_ctas_per_sm}};
+                                              {"prefill_merge", &o.prefill_merge}, {"decode_ctas_per_sm", &o.decode_ctas_per_sm},
+                                              {"pdl", &o.pdl}};
   for (const auto& kv : tab)
     if (std::strcmp(kv.first, name) == 0) {
       if (value < 0) return fail(HC_ERR_CONFIG, "hc_set_option: %s = %d < 0", name, value);
@@ -429,7 +442,8 @@ extern "C" hc_status hc_get_option(const char* name, int32_t* value) {
   const hc::Options& o = hc::options();
   const std::pair<const char*, int> tab[] = {{"t_forward", o.t_forward},       {"x_handoff", o.x_handoff},
                                              {"dep_wait", o.dep_wait},         {"int8_path", o.int8_path},
-                                             {"prefill_merge", o.prefill_merge}, {"decode_ctas_per_sm", o.decode_ctas_per_sm}};
+                                             {"prefill_merge", o.prefill_merge}, {"decode_ctas_per_sm", o.decode_ctas_per_sm},
+                                             {"pdl", o.pdl}};
   for (const auto& kv : tab)
     if (std::strcmp(kv.first, name) == 0) { *value = kv.second; return HC_OK; }
   return fail(HC_ERR_CONFIG, "hc_get_option: unknown option '%s'", name);
@@ -496,14 +510,14 @@ static int window_chunks(const Window& w) {
 }
 
 // Whether `next` can receive t from the kernel producing its input (DArgs::fwd / t_in).
-static bool can_forward(const Window& next) {
-  if (!options().t_forward) return false;
+static bool forwardable(const Window& next) {
   const int c = window_chunks(next);
   if (c == 0 || c > kFwdMax || (int)next.members.size() > kMaxMembers) return false;
   for (const Member& m : next.members)
     if (m.r_alloc > 0 && !(m.Vn && m.Vn->p)) return false;
   return true;
 }
+static bool can_forward(const Window& next) { return options().t_forward && forwardable(next); }
 
 // Launch arguments of one window (also used by the stack driver).
 // x' hand-off between stack windows (DArgs::x16_given / y16)
@@ -538,6 +552,7 @@ static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int
   if (dep) {
     if (!dep->cnt.p) return fail(HC_ERR_STATE, "dataflow dependency: producer window workspace missing");
     a.dep_cnt = (unsigned*)dep->cnt.p + 1;
+    a.dep_reset = a.dep_cnt;
     int n = 0;
     if (dep->glue == HC_GLUE_SILU_MUL) n = dep->members.front().rows() / 8;
     else for (const Member& m : dep->members) n += m.rows() / kRows;
@@ -998,7 +1013,7 @@ struct LayerPlan {
   Window *qkv, *o, *ug, *down;
 };
 
-hc_status stack_plan(hc_ctx* ctx, std::vector<LayerPlan>& plan, int& d, int& nqkv, int& f) {
+hc_status stack_plan(hc_ctx* ctx, std::vector<LayerPlan>& plan, int& d, int& nqkv, int& f, bool check_shard = true) {
   plan.clear();
   for (int l = 0;; ++l) {
     auto f0 = ctx->windows.find(Key{l, HC_WIN_QKV, -1});
@@ -1026,12 +1041,111 @@ hc_status stack_plan(hc_ctx* ctx, std::vector<LayerPlan>& plan, int& d, int& nqk
         G * p.o->out_rows() != d || p.ug->members.front().K != d || G * p.ug->out_rows() != f ||
         p.down->members.front().K != f || G * p.down->out_rows() != d)
       return fail(HC_ERR_CONFIG, "hc_stack_forward: layer %zu shapes inconsistent (need q rows = hidden = O/DOWN rows)", l);
-    if (G > 1)
+    if (G > 1 && check_shard)
       for (Window* w : {p.qkv, p.o, p.ug, p.down})
         for (const Member& m : w->members)
           if (G * m.rows() != m.N || m.row_begin != ctx->rank * m.rows())
             return fail(HC_ERR_CONFIG, "hc_stack_forward: layer %zu member not column-sharded as rows [rank*N/G, (rank+1)*N/G)", l);
   }
+  return HC_OK;
+}
+
+// ---- peer mode: gather fused into the decode epilogue over peer memory
+static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+// Region layout for the loaded stack sharded over G ranks (identical on every rank).
+static hc_status peer_layout(hc_ctx* ctx, int G, hc_ctx::Peer& P) {
+  const int saved_w = ctx->world;
+  ctx->world = G;
+  std::vector<LayerPlan> plan;
+  int d = 0, nqkv = 0, f = 0;
+  hc_status s = stack_plan(ctx, plan, d, nqkv, f, false);   // the rank is checked by hc_peer_set / connect
+  ctx->world = saved_w;
+  if (s != HC_OK) return s;
+  int mc = 1;
+  for (const LayerPlan& p : plan)
+    for (Window* w : {p.qkv, p.o, p.ug, p.down}) {
+      int c = 0;
+      for (const Member& m : w->members) c += m.r_stored / 16;
+      mc = std::max(mc, c);
+    }
+  size_t off = 0;
+  P.off_qkv = off; off += align256((size_t)16 * nqkv * 2);
+  P.off_h1 = off;  off += align256((size_t)16 * d * 2);
+  P.off_m = off;   off += align256((size_t)16 * f * 2);
+  P.off_h = off;   off += align256((size_t)16 * d * 2);
+  P.off_win = off;
+  P.win_stride = align256(128 + ((size_t)mc * hc::kTChunk + 4) * sizeof(long long));
+  P.n_win = 4 * (int)plan.size();
+  P.mc = mc;
+  P.G = G;
+  P.bytes = off + (size_t)P.n_win * P.win_stride;
+  return HC_OK;
+}
+static unsigned* peer_cnt(const hc_ctx::Peer& P, int q, int wi) {
+  return (unsigned*)((uint8_t*)P.base[q] + P.off_win + (size_t)wi * P.win_stride);
+}
+static long long* peer_tacc(const hc_ctx::Peer& P, int q, int wi) {
+  return (long long*)((uint8_t*)P.base[q] + P.off_win + (size_t)wi * P.win_stride + 128);
+}
+static uint16_t* peer_act(const hc_ctx::Peer& P, int q, size_t off) { return (uint16_t*)((uint8_t*)P.base[q] + off); }
+
+// Rows of the gather one rank contributes for window w (the consumer waits for G times this).
+static unsigned local_row_blocks(const Window& w) {
+  if (w.glue == HC_GLUE_SILU_MUL) return (unsigned)(w.members.front().rows() / 8);
+  unsigned n = 0;
+  for (const Member& m : w.members) n += (unsigned)(m.rows() / hc::kRows);
+  return n;
+}
+
+// One peer-mode window: local rows, outputs to every rank's gathered buffer (act_off), t partials of this
+// rank's slice to every rank's next-window accumulators, and the gather counters.
+static hc_status peer_window(hc_ctx* ctx, Window& w, int wi, const void* x, int ldx, int B, size_t act_off, int ld_full,
+                             const void* resid, int ld_resid, const Window* dep, bool t_in, Window* next, int fwd_lo,
+                             int fwd_hi, cudaStream_t st) {
+  const hc_ctx::Peer& P = ctx->peer;
+  const int G = P.G, rank = ctx->rank;
+  const bool fwd = next && hc::forwardable(*next);
+  hc::FwdSpec fs{fwd ? next : nullptr, fwd_lo, fwd_hi};
+  hc::DArgs a;
+  int grid = 0;
+  hc_status s = hc::window_args(ctx, w, x, ldx, B, peer_act(P, rank, act_off), 1, resid, ld_resid, a, grid, t_in,
+                            fwd ? &fs : nullptr);
+  if (s != HC_OK) return s;
+  if (a.n_chunks > P.mc || (fwd && a.fwd_chunks > P.mc))
+    return fail(HC_ERR_STATE, "peer mode: ranks exceed the peer region's t accumulators (call hc_peer_region again)");
+  a.npeer = G;
+  a.ld_full = ld_full;
+  for (int q = 0; q < G; ++q) {
+    a.ypeer[q] = peer_act(P, q, act_off);
+    a.dpeer[q] = peer_cnt(P, q, wi);
+    if (fwd) a.fwdpeer[q] = peer_tacc(P, q, wi + 1);
+  }
+  a.tacc = peer_tacc(P, rank, wi);
+  if (fwd) a.fwd_tacc = peer_tacc(P, rank, wi + 1);
+  // output columns in the full gathered window output: member m's local rows start at F(m) + rank·rows(m)
+  if (a.glue) {
+    a.m[0].full_off = rank * (int)w.out_rows();
+  } else {
+    int F = 0;
+    for (int i = 0; i < a.n_members; ++i) {
+      a.m[i].full_off = F + rank * w.members[i].rows();
+      F += G * w.members[i].rows();
+    }
+  }
+  unsigned* dep_cnt = dep ? peer_cnt(P, rank, wi - 1) : nullptr;
+  const unsigned target = dep ? (unsigned)G * local_row_blocks(*dep) : 0u;
+  a.dep_reset = dep_cnt;
+  a.trace_slot = ctx->trace_slot++;
+  if (a.x16 && !a.x16_given) {
+    // unstaged x: the x-prep kernel waits for the gather; the decode launch follows it in stream order
+    a.dep_cnt = nullptr;
+    CUDA_TRY(hc::launch_xprep(a.x, a.ldx, B, a.K, w.members.front().bits, (uint16_t*)a.x16, a.xsig, st, dep_cnt, target));
+  } else {
+    a.dep_cnt = dep_cnt;
+    a.dep_target = target;
+  }
+  CUDA_TRY(hc::launch_decode(a, w.members.front().bits, grid, st));
   return HC_OK;
 }
 
@@ -1105,7 +1219,7 @@ extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, voi
       CUDA_TRY(cudaMemset(ctx->s_x16max.p, 0, mb));
     }
   }
-  const bool tp = ctx->comm != nullptr;
+  const bool tp = ctx->comm != nullptr && !ctx->peer.on;
   if (tp) {
     const size_t widest = (size_t)std::max(std::max(nqkv, f), d);   // full width of any window output
     if (ctx->t_send.bytes < (size_t)16 * widest * 2) { ctx->invalidate_graphs(); CUDA_TRY(ctx->t_send.alloc((size_t)16 * widest * 2)); }
@@ -1139,7 +1253,33 @@ extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, voi
     for (size_t l = 0; l < plan.size() && cap == HC_OK; ++l) {
       LayerPlan& p = plan[l];
       uint16_t* hout = (l + 1 == plan.size()) ? (uint16_t*)dy : h;
-      if (!tp) {
+      if (ctx->peer.on) {
+        // peer mode: every window gathers through peer memory; t of the next window is exchanged as partials
+        const hc_ctx::Peer& P = ctx->peer;
+        const int rk = ctx->rank;
+        const int wi = 4 * (int)l;
+        uint16_t* aq = peer_act(P, rk, P.off_qkv), *ah1 = peer_act(P, rk, P.off_h1), *am = peer_act(P, rk, P.off_m),
+                  *ah = peer_act(P, rk, P.off_h);
+        const uint16_t* hx_in = l == 0 ? (const uint16_t*)dx : ah;
+        Window* nq = l + 1 < plan.size() ? plan[l + 1].qkv : nullptr;
+        const bool tq = l > 0 && hc::forwardable(*p.qkv);
+        cap = peer_window(ctx, *p.qkv, wi, hx_in, d, B, P.off_qkv, nqkv, nullptr, 0, l > 0 ? plan[l - 1].down : nullptr,
+                          tq, p.o, 0, d, cs);                                                        // q | k | v
+        if (cap == HC_OK)
+          cap = peer_window(ctx, *p.o, wi + 1, aq, nqkv, B, P.off_h1, d, hx_in, d, p.qkv, hc::forwardable(*p.o), p.ug, 0, d,
+                            cs);                                                                     // h1 = h + O(q)
+        if (cap == HC_OK)
+          cap = peer_window(ctx, *p.ug, wi + 2, ah1, d, B, P.off_m, f, nullptr, 0, p.o, hc::forwardable(*p.ug), p.down, 0, f,
+                            cs);                                                                     // m = silu(g)·u
+        if (cap == HC_OK)
+          cap = peer_window(ctx, *p.down, wi + 3, am, f, B, P.off_h, d, ah1, d, p.ug, hc::forwardable(*p.down), nq, 0, d,
+                            cs);                                                                     // h' = h1 + DOWN(m)
+        if (cap == HC_OK && l + 1 == plan.size()) {
+          const cudaError_t e0 = hc::launch_peer_wait_copy(peer_cnt(P, rk, wi + 3), (unsigned)P.G * local_row_blocks(*p.down),
+                                                           peer_cnt(P, rk, wi + 3), ah, (uint16_t*)dy, (size_t)B * d, cs);
+          if (e0 != cudaSuccess) cap = fail(HC_ERR_RUNTIME, "peer gather wait: %s", cudaGetErrorString(e0));
+        }
+      } else if (!tp) {
         // t forwarding: each window's epilogue accumulates the next window's t = V·x from
         // the outputs it writes, so only layer 0's QKV computes its own V·x
         const bool f_o = hc::can_forward(*p.o), f_ug = hc::can_forward(*p.ug), f_dn = hc::can_forward(*p.down);
@@ -1266,4 +1406,77 @@ extern "C" hc_status hc_calib_r_std(const int32_t* Ns, int32_t n_members, int32_
   const double nbar = (double)nsum / (double)n_members;
   *r_std_out = std::floor(eps * (double)bytes / (2.0 * (nbar + (double)K)));
   return HC_OK;
+}
+
+// ------------------------------------------------------------------ peer mode
+extern "C" hc_status hc_peer_region(hc_ctx* ctx, int32_t world, void** base_out, uint64_t* bytes_out) {
+  if (!ctx) return fail(HC_ERR_STATE, "hc_peer_region: null context");
+  if (world < 2 || world > hc::kMaxPeers) return fail(HC_ERR_CONFIG, "hc_peer_region: world %d outside [2, %d]", world, hc::kMaxPeers);
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  hc_ctx::Peer& P = ctx->peer;
+  for (void* p : P.opened) cudaIpcCloseMemHandle(p);
+  P.opened.clear();
+  P.on = false;
+  hc_status s = peer_layout(ctx, world, P);
+  if (s != HC_OK) return s;
+  CUDA_TRY(P.region.alloc(P.bytes));
+  CUDA_TRY(cudaMemset(P.region.p, 0, P.bytes));
+  ctx->invalidate_graphs();
+  if (base_out) *base_out = ctx->peer.region.p;
+  if (bytes_out) *bytes_out = (uint64_t)ctx->peer.bytes;
+  return HC_OK;
+}
+
+static hc_status peer_enable(hc_ctx* ctx, int32_t rank, int32_t world) {
+  ctx->rank = rank;
+  ctx->world = world;
+  ctx->peer.on = true;
+  ctx->invalidate_graphs();
+  std::vector<LayerPlan> plan;
+  int d = 0, nqkv = 0, f = 0;
+  hc_status s = stack_plan(ctx, plan, d, nqkv, f);   // the loaded rows must be this rank's shard
+  if (s != HC_OK) { ctx->peer.on = false; ctx->world = 1; ctx->rank = 0; }
+  return s;
+}
+
+extern "C" hc_status hc_peer_set(hc_ctx* ctx, int32_t rank, int32_t world, void* const* bases) {
+  if (!ctx) return fail(HC_ERR_STATE, "hc_peer_set: null context");
+  if (!ctx->peer.region.p || ctx->peer.G != world) return fail(HC_ERR_STATE, "hc_peer_set: call hc_peer_region(world) first");
+  if (rank < 0 || rank >= world || !bases) return fail(HC_ERR_CONFIG, "hc_peer_set: rank %d / world %d", rank, world);
+  if (bases[rank] != ctx->peer.region.p) return fail(HC_ERR_CONFIG, "hc_peer_set: bases[rank] is not this context's region");
+  for (int q = 0; q < world; ++q) {
+    if (!bases[q]) return fail(HC_ERR_CONFIG, "hc_peer_set: null base of rank %d", q);
+    ctx->peer.base[q] = bases[q];
+  }
+  return peer_enable(ctx, rank, world);
+}
+
+extern "C" hc_status hc_peer_ipc_handle(hc_ctx* ctx, uint8_t* out64) {
+  if (!ctx || !out64) return fail(HC_ERR_CONFIG, "hc_peer_ipc_handle: null argument");
+  if (!ctx->peer.region.p) return fail(HC_ERR_STATE, "hc_peer_ipc_handle: no peer region");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, ctx->peer.region.p));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(out64, &h, 64);
+  return HC_OK;
+}
+
+extern "C" hc_status hc_peer_connect(hc_ctx* ctx, int32_t rank, int32_t world, const uint8_t* handles) {
+  if (!ctx || !handles) return fail(HC_ERR_CONFIG, "hc_peer_connect: null argument");
+  if (!ctx->peer.region.p || ctx->peer.G != world) return fail(HC_ERR_STATE, "hc_peer_connect: call hc_peer_region(world) first");
+  if (rank < 0 || rank >= world) return fail(HC_ERR_CONFIG, "hc_peer_connect: rank %d / world %d", rank, world);
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  for (void* p : ctx->peer.opened) cudaIpcCloseMemHandle(p);
+  ctx->peer.opened.clear();
+  for (int q = 0; q < world; ++q) {
+    if (q == rank) { ctx->peer.base[q] = ctx->peer.region.p; continue; }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handles + (size_t)q * 64, 64);
+    void* p = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    ctx->peer.opened.push_back(p);
+    ctx->peer.base[q] = p;
+  }
+  return peer_enable(ctx, rank, world);
 }

@@ -60,6 +60,23 @@ __device__ __forceinline__ void dtrace(const DArgs& a, int ev) {
   if (g_dtrace) g_dtrace[((size_t)a.trace_slot * 512 + blockIdx.x) * 16 + ev] = t;
 #endif
 }
+// Peer mode, end of the stack: wait for every rank's rows of the last window, copy them out, reset the counter.
+__global__ void peer_wait_copy_kernel(const unsigned* cnt, unsigned target, unsigned* reset, const uint16_t* src,
+                                      uint16_t* out, size_t n) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0) wait_sys(cnt, target);
+  __syncthreads();
+  for (size_t i = threadIdx.x; i < n; i += blockDim.x) out[i] = __ldcg(src + i);
+  __syncthreads();
+  if (threadIdx.x == 0 && reset) *reset = 0u;
+}
+
+cudaError_t launch_peer_wait_copy(const unsigned* cnt, unsigned target, unsigned* reset, const uint16_t* src, uint16_t* out,
+                                  size_t n_elems, cudaStream_t st) {
+  peer_wait_copy_kernel<<<1, 1024, 0, st>>>(cnt, target, reset, src, out, n_elems);
+  return cudaGetLastError();
+}
+
 cudaError_t decode_set_trace(void* buf) { return cudaMemcpyToSymbol(g_dtrace, &buf, sizeof(buf)); }
 
 
@@ -78,6 +95,14 @@ cudaError_t decode_set_trace(void* buf) { return cudaMemcpyToSymbol(g_dtrace, &b
 // reads activations calls this), else the programmatic-dependent-launch grid dependency.
 __device__ __forceinline__ void dep_wait(const DArgs& a, int lane) {
   if (a.dep_cnt) {
+    if (a.npeer > 1) {                                            // peer mode: every rank's producer adds into it
+      if (lane == 0) {
+        wait_sys(a.dep_cnt, a.dep_target);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
+      __syncwarp();
+      return;
+    }
     if (lane == 0) {
       while (ld_relaxed(a.dep_cnt) < a.dep_target) __nanosleep(HC_DEP_SLEEP);
       (void)ld_acquire(a.dep_cnt);   // (a fence.acq_rel here measured slower than the second load)
@@ -266,7 +291,10 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
       }
       // t forwarding: this item's outputs are x of the next window at k = n0 - fwd_lo .. (16 or 8 of them);
       // fetch the next window's natural-k V fragments of that 16-k block while the tile warps work
-      const int f_n0 = a.glue ? m.row_off + (item - m.rb_begin) * 8 : m.row_off + (item - m.rb_begin) * kRows;
+      // first output column of this item: in the window output (local), or in the full gathered output (peer
+      // mode: the column the other ranks and the next window see)
+      const int oc0 = (a.npeer > 1 ? m.full_off : m.row_off) + (item - m.rb_begin) * (a.glue ? 8 : kRows);
+      const int f_n0 = oc0;
       const bool f_on = a.fwd && f_n0 >= a.fwd_lo && f_n0 < a.fwd_hi;
       if (f_on && lane == 0) {
         const int kb = (f_n0 - a.fwd_lo) >> 4;
@@ -321,7 +349,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
           res[nb][e] = 0.f;
           const int b = 2 * tig + (e & 1) + 8 * nb;
           if (a.resid && !a.glue && b < a.B)
-            res[nb][e] = bf16_bits_to_f32(__ldcg(a.resid + (size_t)b * a.ld_resid + m.row_off + rbl * kRows + gid + 8 * (e >> 1)));
+            res[nb][e] = bf16_bits_to_f32(__ldcg(a.resid + (size_t)b * a.ld_resid + oc0 + gid + 8 * (e >> 1)));
         }
       if (f_on) {                                        // zero the x tile (cols >= B and the other 8 k stay 0)
         reinterpret_cast<uint4*>(xt)[lane] = make_uint4(0u, 0u, 0u, 0u);
@@ -364,7 +392,12 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
             const int n = m.row_off + rbl * 8 + gid;
             if (a.y_bf16) {
               const uint16_t bits = (uint16_t)f32_to_bf16_rn(v);
-              reinterpret_cast<uint16_t*>(a.y)[(size_t)b * a.ldy + n] = bits;
+              if (a.npeer > 1) {
+#pragma unroll 1
+                for (int q = 0; q < a.npeer; ++q) a.ypeer[q][(size_t)b * a.ld_full + oc0 + gid] = bits;
+              } else {
+                reinterpret_cast<uint16_t*>(a.y)[(size_t)b * a.ldy + n] = bits;
+              }
               if (f_on) xt[(((f_n0 - a.fwd_lo) & 15) + gid) * 16 + b] = bits;
               if (a.y16 && n >= a.y16_lo && n < a.y16_hi) write_xprime<BITS>(a, b, n, bits);
               xm[nb][e] = max(xm[nb][e], (uint32_t)bits & 0x7FFFu);
@@ -383,7 +416,12 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
             const float v = fin[nb][e] + comp[0][nb][e] + res[nb][e];
             if (a.y_bf16) {
               const uint16_t bits = (uint16_t)f32_to_bf16_rn(v);
-              reinterpret_cast<uint16_t*>(a.y)[(size_t)b * a.ldy + n] = bits;
+              if (a.npeer > 1) {
+#pragma unroll 1
+                for (int q = 0; q < a.npeer; ++q) a.ypeer[q][(size_t)b * a.ld_full + oc0 + gid + 8 * (e >> 1)] = bits;
+              } else {
+                reinterpret_cast<uint16_t*>(a.y)[(size_t)b * a.ldy + n] = bits;
+              }
               if (f_on) xt[(gid + 8 * (e >> 1)) * 16 + b] = bits;
               if (a.y16 && n >= a.y16_lo && n < a.y16_hi) write_xprime<BITS>(a, b, n, bits);
               xm[nb][e & 1] = max(xm[nb][e & 1], (uint32_t)bits & 0x7FFFu);
@@ -417,7 +455,14 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int col = 2 * tig + (e & 1) + 8 * nb, rank = gid + 8 * (e >> 1);
-              if (col < a.B) tacc_add(a.fwd_tacc, a.fwd_chunks, cc, col, rank, tp[e]);
+              if (col < a.B) {
+                if (a.npeer > 1) {                                 // partial-t exchange: this rank's slice, every rank
+#pragma unroll 1
+                  for (int q = 0; q < a.npeer; ++q) tacc_add(a.fwdpeer[q], a.fwd_chunks, cc, col, rank, tp[e]);
+                } else {
+                  tacc_add(a.fwd_tacc, a.fwd_chunks, cc, col, rank, tp[e]);
+                }
+              }
             }
           }
         }
@@ -431,8 +476,10 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
     __syncwarp();
     unsigned last = 0;
     if (lane == 0 && my_rb > 0) {
-            const unsigned old = add_acq_rel(&a.cnt[1], (unsigned)my_rb);
+      const unsigned old = add_acq_rel(&a.cnt[1], (unsigned)my_rb);
       last = (old + (unsigned)my_rb == (unsigned)a.n_rb);
+      if (a.npeer > 1)                                     // peer mode: this CTA's rows of the gather, on every rank
+        for (int q = 0; q < a.npeer; ++q) red_release_sys(a.dpeer[q], (unsigned)my_rb);
     }
     last = __shfl_sync(0xffffffffu, last, 0);
     if (last) {
@@ -442,7 +489,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
       if (lane == 0) {
         a.cnt[0] = 0u;
         if (!a.keep_done) a.cnt[1] = 0u;             // else the consumer window resets it
-        if (a.dep_cnt) *a.dep_cnt = 0u;              // every CTA of this window passed its wait
+        if (a.dep_reset) *a.dep_reset = 0u;          // every CTA of this window passed its wait
       }
     }
     return;
@@ -676,8 +723,12 @@ bool decode_uses_i8(int bits, int B, int K) { return use_xs(B, K) && use_i8(bits
 // One thread per (group, batch row, 16-element part).
 template <int BITS>
 __global__ void xprep_kernel(const uint16_t* __restrict__ x, int ldx, int B, int K, uint16_t* __restrict__ x16,
-                             float* __restrict__ xsig) {
+                             float* __restrict__ xsig, const unsigned* dep_cnt, unsigned dep_target) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (dep_cnt) {                                          // peer mode: x is gathered from every rank
+    if (threadIdx.x == 0) wait_sys(dep_cnt, dep_target);
+    __syncthreads();
+  }
   // one thread per (group, batch row, 16-element part): the 8 parts of a (group, row) are 8 consecutive
   // lanes and agree on the group's prescale σ (R20); 2^σ -> xsig[g][b]
   const int i = blockIdx.x * blockDim.x + threadIdx.x;   // over G * B * 8
@@ -701,7 +752,8 @@ __global__ void xprep_kernel(const uint16_t* __restrict__ x, int ldx, int B, int
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-cudaError_t launch_xprep(const uint16_t* x, int ldx, int B, int K, int bits, uint16_t* x16, float* xsig, cudaStream_t st) {
+cudaError_t launch_xprep(const uint16_t* x, int ldx, int B, int K, int bits, uint16_t* x16, float* xsig, cudaStream_t st,
+                         const unsigned* dep_cnt, unsigned dep_target) {
   const int n = (K / kGroup) * B * 8;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((n + 255) / 256);
@@ -709,13 +761,13 @@ cudaError_t launch_xprep(const uint16_t* x, int ldx, int B, int K, int bits, uin
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[0].val.programmaticStreamSerializationAllowed = options().pdl ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   switch (bits) {
-    case 2: return cudaLaunchKernelEx(&cfg, xprep_kernel<2>, x, ldx, B, K, x16, xsig);
-    case 3: return cudaLaunchKernelEx(&cfg, xprep_kernel<3>, x, ldx, B, K, x16, xsig);
-    case 4: return cudaLaunchKernelEx(&cfg, xprep_kernel<4>, x, ldx, B, K, x16, xsig);
+    case 2: return cudaLaunchKernelEx(&cfg, xprep_kernel<2>, x, ldx, B, K, x16, xsig, dep_cnt, dep_target);
+    case 3: return cudaLaunchKernelEx(&cfg, xprep_kernel<3>, x, ldx, B, K, x16, xsig, dep_cnt, dep_target);
+    case 4: return cudaLaunchKernelEx(&cfg, xprep_kernel<4>, x, ldx, B, K, x16, xsig, dep_cnt, dep_target);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -738,7 +790,7 @@ static cudaError_t launch_t(const DArgs& a, int grid, cudaStream_t st) {
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[0].val.programmaticStreamSerializationAllowed = options().pdl ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, decode_kernel<BITS, NB8, XS, I8>, a);

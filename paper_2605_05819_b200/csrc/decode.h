@@ -40,7 +40,10 @@ struct DMember {
   int r;                // allocated rank (0 = no compensation, no U/V reads)
   int r_stored;
   int chunk_begin;      // first window-global rank chunk (16 ranks) of this member
+  int full_off;         // peer mode: output column (in the full, gathered window output) of local row 0
 };
+
+constexpr int kMaxPeers = 8;
 
 struct DArgs {
   DMember m[kMaxMembers];
@@ -73,7 +76,7 @@ struct DArgs {
   // dataflow dependency on the producer window (stack graphs): instead of griddepcontrol.wait (the
   // kernel-boundary release, ~2 µs), wait until the producer's row-block counter reaches its n_rb
   // (release / acquire), and reset that counter when this window completes
-  unsigned* dep_cnt;    // producer's cnt[1], or NULL (griddepcontrol.wait)
+  unsigned* dep_cnt;    // producer's cnt[1] (peer mode: this rank's gather counter), or NULL (griddepcontrol.wait)
   unsigned dep_target;  // producer's n_rb
   int keep_done;        // 1: a consumer window resets this window's cnt[1] (do not self-reset it)
   // x' hand-off (stack graphs): x16_given = 1 means x16 was written by the producer window's epilogue
@@ -88,6 +91,17 @@ struct DArgs {
   // x16_max after its dependency wait and, for the groups whose prescale σ is not 0, builds x' itself from
   // bf16 x (per-record slow path).  clr_max[0 .. clr_n) is zeroed by CTA 0 after its dependency wait: the
   // max buffer the NEXT window publishes into (its previous reader finished before this window's producer)
+  // peer mode (column sharding over G GPUs with the gather fused into the epilogue):
+  // every output element is stored into each of the npeer ranks' full-width window output ypeer[q] (peer memory over
+  // NVLink), the next window's t partials of this rank's output slice are added into each rank's t
+  // accumulators fwdpeer[q], and each CTA adds its row-block count to each rank's dependency counter
+  // dpeer[q] (system-scope release); the consumer waits for npeer x n_rb.  npeer <= 1: off.
+  int npeer;
+  uint16_t* ypeer[kMaxPeers];
+  int ld_full;          // row stride of ypeer (the full window output width)
+  unsigned* dpeer[kMaxPeers];
+  long long* fwdpeer[kMaxPeers];
+  unsigned* dep_reset;  // the producer's dependency counter this window resets when it completes (NULL: none)
   unsigned* y16_max;
   const unsigned* x16_max;
   unsigned* clr_max;
@@ -105,7 +119,12 @@ bool decode_stages_x(int B, int K);
 // a window reads bf16 x itself, so its producer writes no x' hand-off for it.
 bool decode_uses_i8(int bits, int B, int K);
 // x' (fp16, pre-scaled per the code layout of `bits`) for a !XS decode launch.
-cudaError_t launch_xprep(const uint16_t* x, int ldx, int B, int K, int bits, uint16_t* x16, float* xsig, cudaStream_t st);
+cudaError_t launch_xprep(const uint16_t* x, int ldx, int B, int K, int bits, uint16_t* x16, float* xsig, cudaStream_t st,
+                         const unsigned* dep_cnt = nullptr, unsigned dep_target = 0);
+// Peer mode: wait until this rank's gather counter reaches `target` (system scope), then copy the gathered
+// [B][n] bf16 activations to `out` (the stack's final output).
+cudaError_t launch_peer_wait_copy(const unsigned* cnt, unsigned target, unsigned* reset, const uint16_t* src, uint16_t* out,
+                                  size_t n_elems, cudaStream_t st);
 cudaError_t decode_set_trace(void* buf);   // dev: [slots][grid][8] globaltimer stamps (HC_DEC_TRACE builds)
 // Max co-resident CTAs of the decode kernel on this device (persistent grid size).
 int decode_max_ctas(int bits, int B, int K, int n_chunks, int fwd_chunks, bool no_xs = false);

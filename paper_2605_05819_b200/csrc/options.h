@@ -13,6 +13,7 @@ struct Options {
   int int8_path = 1;           // decode: u8·s8 tensor-core path for 2/4-bit at B <= 2 (decode_i8.cuh)
   int prefill_merge = 1;       // prefill: one GEMM over a multi-member window
   int decode_ctas_per_sm = 0;  // decode: cap on resident CTAs per SM (0 = occupancy limit)
+  int pdl = 1;                 // decode: programmatic dependent launch between windows
   unsigned epoch = 0;
 };
 
