@@ -729,6 +729,9 @@ def main():
             port = so.getsockname()[1]
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
                "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        if os.environ.get("HC_BENCH_DRYRUN") == "1":     # test hook: show the launch instead of running it
+            print(json.dumps({"spawn": cmd}))
+            sys.exit(0)
         sys.exit(subprocess.call(cmd))
 
     rank = int(os.environ.get("RANK", 0))

@@ -123,3 +123,22 @@ def test_shard_rows_and_unshard_layout():
     # member 0 full rows = rank0 (0,1) | rank1 (6,7); member 1 = rank0 (2) | rank1 (8)
     assert out[0].tolist() == [0, 1, 6, 7, 2, 8]
     assert out[1].tolist() == [3, 4, 9, 10, 5, 11]
+
+
+def test_bench_spawns_one_rank_per_gpu():
+    """bench.py --gpus N without WORLD_SIZE re-launches itself under torch.distributed.run with N ranks on
+    127.0.0.1 (dry run: the command is printed, nothing runs); with WORLD_SIZE set (the driver's own
+    torchrun launch) it does not re-spawn."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, HC_BENCH_DRYRUN="1")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "4", "--steps", "5", "--warmup", "3"],
+                         env=env, capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    cmd = json.loads(out.stdout.strip().splitlines()[-1])["spawn"]
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=4" in cmd and cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[-6:] == ["--gpus", "4", "--steps", "5", "--warmup", "3"]
