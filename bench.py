@@ -88,13 +88,21 @@ class Clocks:
 C1 = dict(N=4096, K=4096, bits=4, group=128, r=64, r_stored=64, B=1)
 
 
-def c1_bytes(c=C1, r=None):
+FACTOR_BYTES = {"bf16": 2, "fp8": 1}   # bytes per factor element (fp8: e4m3 + 2 fp32 scales per rank)
+
+
+def factor_bytes(r, N, K, kind="bf16"):
+    return FACTOR_BYTES[kind] * r * (N + K) + (8 * r if kind == "fp8" else 0)
+
+
+def c1_bytes(c=C1, r=None, kind="bf16"):
     """Algorithmic bytes of one C1 call: codes b/8 per element, a bf16
-    scale + a b-bit zero per group, the rank-r slices of U and V (bf16), x (bf16) and y (fp32)."""
+    scale + a b-bit zero per group, the rank-r slices of U and V (bf16, or e4m3 + per-rank scales), x (bf16)
+    and y (fp32)."""
     N, K, b, g, B = c["N"], c["K"], c["bits"], c["group"], c["B"]
     r = c["r"] if r is None else r
     base = N * K * b // 8 + N * (K // g) * (16 + b) // 8
-    fac = 2 * r * (N + K)
+    fac = factor_bytes(r, N, K, kind)
     io = B * (2 * K + 4 * N)
     return base + fac + io
 
@@ -109,6 +117,31 @@ def dtype_of(args, config):
     if bits in (2, 4) and args.batch <= 2 and hc.get_option("int8_path") != 0 and args.workload != "c3":
         return f"int8 mma (u{bits} codes x s8 digits of bf16 x, exact int32), fp32 per-group accumulate"
     return f"fp16 mma (exact int{bits} dequant x fp16 x), fp32 accumulate"
+
+
+def e4m3_random(shape, g):
+    """Random e4m3 bytes on the device (random BYTES: sign, exponent field in [4, 10], mantissa; 1/16 of them
+    subnormal / zero codes) -- the synth.fp8_factors recipe."""
+    import torch
+    sign = torch.randint(0, 2, shape, generator=g, device="cuda", dtype=torch.int32) << 7
+    e = torch.randint(4, 11, shape, generator=g, device="cuda", dtype=torch.int32)
+    e = torch.where(torch.rand(shape, generator=g, device="cuda") < 1.0 / 16.0, torch.zeros_like(e), e)
+    m = torch.randint(0, 8, shape, generator=g, device="cuda", dtype=torch.int32)
+    return (sign | (e << 3) | m).to(torch.uint8)
+
+
+def factor_fields(U, V, N, K, rs, g, kind):
+    """Matrix-descriptor fields of the factors: bf16 U / V as given, or e4m3 bytes + per-rank scales with the
+    same RMS as the bf16 factors (|e4m3| RMS of the recipe ~ 4.9)."""
+    import torch
+    import paper_2605_05819_b200 as hc
+    if kind != "fp8":
+        return dict(U=U, V=V)
+    su = float(U.float().pow(2).mean().sqrt()) / 4.9
+    sv = float(V.float().pow(2).mean().sqrt()) / 4.9
+    return dict(U=e4m3_random((N, rs), g), V=e4m3_random((rs, K), g), factor_dtype=hc.FACTORS_FP8,
+                u_scale=(su * (0.5 + torch.rand(rs, generator=g, device="cuda"))).contiguous(),
+                v_scale=(sv * (0.5 + torch.rand(rs, generator=g, device="cuda"))).contiguous())
 
 
 def run_c1_ours(args, rank, world, device):
@@ -127,7 +160,8 @@ def run_c1_ours(args, rank, world, device):
         U = (torch.randn((N, c["r_stored"]), generator=g, device="cuda") / N ** 0.5).to(torch.bfloat16)
         V = (0.02 * torch.randn((c["r_stored"], K), generator=g, device="cuda")).to(torch.bfloat16)
         ctx.load_layer([dict(layer=i, window=0, slot=0, N=N, K=K, bits=b, codes=codes, scales=scales, zeros=zeros,
-                             U=U, V=V, r_stored=c["r_stored"], r_alloc=c["r"])])
+                             r_stored=c["r_stored"], r_alloc=c["r"],
+                             **factor_fields(U, V, N, K, c["r_stored"], g, getattr(args, "factors", "bf16")))])
         del codes, scales, zeros, U, V
     x = torch.randn((c["B"], K), generator=g, device="cuda").to(torch.bfloat16)
     y = torch.empty((c["B"], N), dtype=torch.float32, device="cuda")
@@ -280,21 +314,21 @@ def c2_ranks_oracle(c=C2, seed=0):
     return {(rec["layer"], rec["window"], rec["slot"]): int(r) for rec, r in zip(case["records"], al.ranks)}
 
 
-def c2_bytes(ranks, B, c=C2, G=1):
+def c2_bytes(ranks, B, c=C2, G=1, kind="bf16"):
     """Algorithmic bytes one GPU moves per decode step: its rows of every base weight (codes, bf16 scale,
     b-bit zero), its rows of the allocated U slices and ALL of the allocated V slices (V·x is replicated
     under column sharding), and the activations in/out of each window."""
     tot = 0
     for l in range(c["layers"]):
-        for kind, Ns, K in c2_windows(c):
+        for wk, Ns, K in c2_windows(c):
             tot += window_bytes_base([N // G for N in Ns], K, c["bits"])
             for s, N in enumerate(Ns):
-                tot += 2 * ranks[(l, kind, s)] * (N // G + K)
-            tot += B * 2 * K + B * 2 * ((sum(Ns) if kind != 2 else Ns[0]) // G)
+                tot += factor_bytes(ranks[(l, wk, s)], N // G, K, kind)
+            tot += B * 2 * K + B * 2 * ((sum(Ns) if wk != 2 else Ns[0]) // G)
     return tot
 
 
-def build_c2(ctx, ranks, c=C2, shard=None):
+def build_c2(ctx, ranks, c=C2, shard=None, factors="bf16"):
     """Random-init weights of the named shapes, generated on the device; every matrix has its own seed so
     all ranks of a column-sharded run see the same model and load rows [rank·N/G, (rank+1)·N/G)."""
     import torch
@@ -319,9 +353,10 @@ def build_c2(ctx, ranks, c=C2, shard=None):
                     codes=torch.randint(-2**31, 2**31, (N, K * b // 32), generator=g, device="cuda", dtype=torch.int32),
                     scales=(gain * (0.5 + torch.rand((N, G), generator=g, device="cuda")) / (e2 * K) ** 0.5).to(torch.bfloat16),
                     zeros=torch.randint(0, 1 << b, (N, G), generator=g, device="cuda", dtype=torch.uint8),
-                    U=(torch.randn((N, rs), generator=g, device="cuda") / N ** 0.5).to(torch.bfloat16),
-                    V=(0.05 * (N / (rs * K)) ** 0.5 * torch.randn((rs, K), generator=g, device="cuda")).to(torch.bfloat16),
-                    r_stored=rs, r_alloc=ranks[(l, kind, s)], glue=1 if kind == 2 else 0))
+                    r_stored=rs, r_alloc=ranks[(l, kind, s)], glue=1 if kind == 2 else 0,
+                    **factor_fields((torch.randn((N, rs), generator=g, device="cuda") / N ** 0.5).to(torch.bfloat16),
+                                    (0.05 * (N / (rs * K)) ** 0.5 * torch.randn((rs, K), generator=g, device="cuda")).to(torch.bfloat16),
+                                    N, K, rs, g, factors)))
         ctx.load_layer(mats)
         del mats
     torch.cuda.synchronize()
@@ -340,7 +375,8 @@ def run_c2_ours(args, rank, world, device, B, c=C2, tp=False, sweep=()):
     peer = tp and getattr(args, "tp_path", "peer") == "peer"
     if tp and not peer:
         ctx.init_comm(rank, world)
-    build_c2(ctx, ranks, c, shard=(rank, world) if tp else None)
+    fk = getattr(args, "factors", "bf16")
+    build_c2(ctx, ranks, c, shard=(rank, world) if tp else None, factors=fk)
     if peer:
         ctx.init_peers(rank, world)      # gather fused into the decode epilogue over peer memory
     st = torch.cuda.Stream()
@@ -394,14 +430,14 @@ def run_c2_ours(args, rank, world, device, B, c=C2, tp=False, sweep=()):
         mss = timed(Bs)[0]
         sw[str(Bs)] = {"tokens_per_s": round((1 if tp else world) * Bs * args.steps / (mss * 1e-3), 1),
                        "ms_per_step": round(mss / args.steps, 4),
-                       "GBps": round(c2_bytes(ranks, Bs, c, G) / (mss / args.steps * 1e-3) / 1e9, 1)}
+                       "GBps": round(c2_bytes(ranks, Bs, c, G, fk) / (mss / args.steps * 1e-3) / 1e9, 1)}
     ctx.close()
     mean_rank = sum(ranks.values()) / len(ranks)
     # decode kernels (+ the NCCL path's unshard permute per window; + the peer path's final gather wait)
     launches = args.steps * (4 * c["layers"] * (2 if (tp and not peer) else 1) + (1 if peer else 0))
     return dict(ms=ms, steps=args.steps, clocks=clocks, e2e_s=e2e_s, n_e2e=n_e2e, finite=finite,
                 launches=launches, h2d=B * c["hidden"] * 2, d2h=B * c["hidden"] * 2,
-                bytes=c2_bytes(ranks, B, c, G), bytes_r0=c2_bytes({k: 0 for k in ranks}, B, c, G), ms_r0=ms_r0,
+                bytes=c2_bytes(ranks, B, c, G, fk), bytes_r0=c2_bytes({k: 0 for k in ranks}, B, c, G), ms_r0=ms_r0,
                 mean_rank=mean_rank, ranks=ranks, sweep=sw)
 
 
@@ -715,6 +751,8 @@ def main():
     ap.add_argument("--rank-override", type=int, default=None, help="dev: use this rank for every matrix")
     ap.add_argument("--moe-dynamic", action="store_true", help="c3: per-(token, expert) dynamic ranks (P:652-665)")
     ap.add_argument("--no-sweep", action="store_true", help="c2: skip the default B = 2/4/8/16 sweep")
+    ap.add_argument("--factors", default="bf16", choices=["bf16", "fp8"],
+                    help="compensation factor storage (fp8: e4m3 + per-rank fp32 scales, SURVEY 8(f)4)")
     ap.add_argument("--tp-path", default="peer", choices=["peer", "nccl"],
                     help="N>1 column sharding: peer = gather fused into the decode epilogue over NVLink peer "
                          "memory with partial-t exchange (default); nccl = ncclAllGather + unshard per window")
@@ -756,7 +794,7 @@ def main():
                   "dynamic_ranks": bool(args.moe_dynamic)}
     elif args.workload == "c1":
         config = {"workload": "c1: single 4096x4096 linear, 4-bit g128, rank-64 compensation, batch-1 decode",
-                  "N": 4096, "K": 4096, "bits": 4, "group": 128, "rank": 64, "batch": 1,
+                  "N": 4096, "K": 4096, "bits": 4, "group": 128, "rank": 64, "batch": 1, "factors": args.factors,
                   "l2": "defeated: 128 distinct weight copies (1.25 GB) rotated per step"}
     else:
         c = STACKS[args.workload]
@@ -768,7 +806,7 @@ def main():
                                        + ")") if tp else
                                       (f", {world} independent replicas" if world > 1 else ", 1 GPU")),
                   "layers": c["layers"], "hidden": c["hidden"], "kv": c["kv"], "ffn": c["ffn"], "bits": c["bits"],
-                  "group": 128, "r_stored": c["r_stored"], "batch": args.batch,
+                  "group": 128, "r_stored": c["r_stored"], "batch": args.batch, "factors": args.factors,
                   "parallelism": f"tp{world}" if tp else f"dp{world}",
                   "l2": "inputs larger than L2 (all weights streamed per step)",
                   "attention": "identity stand-in on the q-part (out of scope, DESIGN.md R9)"}
@@ -821,7 +859,7 @@ def main():
         unit, kernel = "tokens/s", "hc::moe_gemv_kernel<3> (grouped UPGATE + DOWN per layer)"
     elif args.workload == "c1":
         r = run_c1_ours(args, rank, world, local)
-        nbytes = c1_bytes()
+        nbytes = c1_bytes(kind=args.factors)
         unit, kernel = "GB/s", "hc::decode_kernel<4,1,true,true> (int8 mma path)"
     else:
         sweep = () if (args.workload != "c2" or args.no_sweep) else tuple(b for b in (1, 2, 4, 8, 16) if b != args.batch)

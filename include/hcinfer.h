@@ -40,6 +40,7 @@ typedef enum {
 typedef enum { HC_WIN_QKV = 0, HC_WIN_O = 1, HC_WIN_UPGATE = 2, HC_WIN_DOWN = 3 } hc_window_kind;
 typedef enum { HC_OUT_F32 = 0, HC_OUT_BF16 = 1 } hc_out_dtype;
 typedef enum { HC_GLUE_NONE = 0, HC_GLUE_SILU_MUL = 1 } hc_glue;
+typedef enum { HC_FACTORS_BF16 = 0, HC_FACTORS_FP8 = 1 } hc_factor_dtype;
 
 const char* hc_version(void);
 const char* hc_last_error(void);
@@ -108,6 +109,14 @@ hc_status hc_destroy(hc_ctx* ctx);
  * row_begin/row_end: the rows [row_begin, row_end) this context keeps (column sharding of
  * the output across GPUs); use 0 / N for an unsharded matrix.
  * (row_end - row_begin) % 16 == 0.
+ * factor_dtype: HC_FACTORS_BF16 (U, V as above) or HC_FACTORS_FP8: U and V are e4m3 bytes
+ * (uint8 [N][r_stored] and [r_stored][K]; NaN encodings 0x7F / 0xFF rejected with HC_ERR_NUMERIC) with fp32
+ * per-rank scales u_scale [r_stored], v_scale [r_stored] (host or device):
+ *   U_eff[n][j] = e4m3(U[n][j])·u_scale[j],   V_eff[j][k] = e4m3(V[j][k])·v_scale[j]
+ * and the window computes y = deq(W)·x + U_eff[:, :r]·(V_eff[:r, :]·x): half the factor bytes of bf16.  Decode
+ * windows read the e4m3 bytes (converted exactly in registers); the prefill path uses fp16 copies of
+ * U_eff / V_eff (one fp16 rounding).  Members of a window share the factor dtype; MoE expert windows and
+ * t forwarding take bf16 factors only (HC_ERR_CONFIG for fp8 experts).  u_scale / v_scale ignored for bf16.
  * glue: HC_GLUE_SILU_MUL fuses the FFN gate (App. A.1.3, "h = σ(W_gate X) ⊙ W_up X", σ = SiLU)
  * into an UPGATE window: slot 0 = up and slot 1 = gate, same shape, loaded in the SAME call, both
  * flagged; their rows are interleaved at load time (8 up + 8 gate rows per row block) so the
@@ -124,6 +133,9 @@ typedef struct {
   int32_t r_stored, r_alloc;
   int32_t row_begin, row_end;
   int32_t glue;
+  int32_t factor_dtype;     /* hc_factor_dtype */
+  const float* u_scale;     /* HC_FACTORS_FP8: [r_stored] */
+  const float* v_scale;     /* HC_FACTORS_FP8: [r_stored] */
 } hc_matrix_desc;
 
 /* Copy + repack matrices into context-owned device memory (synchronous w.r.t. its inputs:

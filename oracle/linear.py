@@ -24,7 +24,7 @@ from __future__ import annotations
 import numpy as np
 
 from .allocate import align, cap_level
-from .packing import unpack_codes, bf16_to_f64
+from .packing import unpack_codes, bf16_to_f64, e4m3_to_f64
 from .quant import dequant_abi
 
 
@@ -45,18 +45,32 @@ def compensated_product(W_hat: np.ndarray, U: np.ndarray, V: np.ndarray, r: int,
     return y
 
 
+def factors_f64(case: dict, rows=None):
+    """(U, V) in float64 from the ABI formats: bf16 bits, or (factor_dtype "fp8") e4m3 bytes
+    U8 [N, r_stored] / V8 [r_stored, K] with fp32 per-rank scales us / vs:
+    U_eff = e4m3(U8)·us[j] (column j), V_eff = e4m3(V8)·vs[j] (row j), exact in float64."""
+    if case.get("factor_dtype", "bf16") == "fp8":
+        U8 = case["U8"] if rows is None else case["U8"][rows]
+        us = np.asarray(case["us"], dtype=np.float32).astype(np.float64)
+        vs = np.asarray(case["vs"], dtype=np.float32).astype(np.float64)
+        return e4m3_to_f64(U8) * us[None, :], e4m3_to_f64(case["V8"]) * vs[:, None]
+    U = case["U"] if rows is None else case["U"][rows]
+    return bf16_to_f64(U), bf16_to_f64(case["V"])
+
+
 def compensated_linear(case: dict, r: int, x_bits=None, rows=None) -> np.ndarray:
     """Oracle for one matrix given a synth.linear_case-style dict (ABI formats).
 
     ``rows`` (optional index array) restricts the output rows (sampled checks at full size).
     """
     K, bits, group = case["K"], case["bits"], case["group"]
-    codes, scales, zeros, U = case["codes"], case["scales"], case["zeros"], case["U"]
+    codes, scales, zeros = case["codes"], case["scales"], case["zeros"]
     if rows is not None:
-        codes, scales, zeros, U = codes[rows], scales[rows], zeros[rows], U[rows]
+        codes, scales, zeros = codes[rows], scales[rows], zeros[rows]
     W_hat = deq_weight(codes, scales, zeros, K, bits, group)
     x = bf16_to_f64(case["x"] if x_bits is None else x_bits)
-    return compensated_product(W_hat, bf16_to_f64(U), bf16_to_f64(case["V"]), r, x)
+    U, V = factors_f64(case, rows)
+    return compensated_product(W_hat, U, V, r, x)
 
 
 def window_linear(members: list, ranks: list, x_bits) -> np.ndarray:
@@ -116,7 +130,8 @@ def stack_forward(layers: list, ranks: list, x_bits) -> np.ndarray:
 
 def _lin(case: dict, r: int, x_f64: np.ndarray) -> np.ndarray:
     W_hat = deq_weight(case["codes"], case["scales"], case["zeros"], case["K"], case["bits"], case["group"])
-    return compensated_product(W_hat, bf16_to_f64(case["U"]), bf16_to_f64(case["V"]), r, x_f64)
+    U, V = factors_f64(case)
+    return compensated_product(W_hat, U, V, r, x_f64)
 
 
 def moe_forward(experts: list, ranks: list, x_bits, topk_idx, topk_gate) -> np.ndarray:

@@ -45,3 +45,16 @@ def f64_to_bf16_bits_rne(a: np.ndarray) -> np.ndarray:
     u = f.view(np.uint32).astype(np.uint64)
     u = (u + (((u >> 16) & 1) + 0x7FFF)) >> 16
     return u.astype(np.uint16)
+
+
+def e4m3_to_f64(b: np.ndarray) -> np.ndarray:
+    """OCP FP8 E4M3 (e4m3fn) bytes -> float64 by the format's definition: sign bit 7,
+    exponent bits 6-3 (bias 7), mantissa bits 2-0; e > 0: (-1)^s·2^(e-7)·(1 + m/8); e = 0: (-1)^s·2^-6·m/8;
+    0x7F / 0xFF (e = 15, m = 7) are NaN (no infinities)."""
+    b = np.asarray(b, dtype=np.uint8).astype(np.int64)
+    s = np.where(b & 0x80, -1.0, 1.0)
+    e = (b >> 3) & 0xF
+    m = (b & 0x7).astype(np.float64)
+    v = np.where(e > 0, np.ldexp(1.0 + m / 8.0, (e - 7).astype(np.int64)), np.ldexp(m / 8.0, -6))
+    v = s * v
+    return np.where((e == 15) & ((b & 0x7) == 7), np.nan, v)

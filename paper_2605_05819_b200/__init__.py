@@ -14,10 +14,11 @@ import numpy as np
 
 from . import _lib
 from ._lib import (HCError, HC_OK, HC_ERR_CONFIG, HC_ERR_STATE, HC_ERR_NUMERIC, HC_ERR_RUNTIME,
-                   QKV, O, UPGATE, DOWN, OUT_F32, OUT_BF16, GLUE_NONE, GLUE_SILU_MUL, check, lib)
+                   QKV, O, UPGATE, DOWN, OUT_F32, OUT_BF16, GLUE_NONE, GLUE_SILU_MUL, FACTORS_BF16, FACTORS_FP8,
+                   check, lib)
 
 __all__ = ["allocate_ranks", "Context", "HCError", "QKV", "O", "UPGATE", "DOWN", "OUT_F32", "OUT_BF16",
-           "GLUE_NONE", "GLUE_SILU_MUL",
+           "GLUE_NONE", "GLUE_SILU_MUL", "FACTORS_BF16", "FACTORS_FP8",
            "repack_host", "unpack_repacked_host", "shard_rows", "unshard_host", "set_option", "get_option", "calib_r_std", "lib"]
 
 
@@ -182,7 +183,8 @@ class Context:
 
     def load_layer(self, mats, stream=None):
         """mats: list of dicts with layer, window, slot, expert(-1), N, K, bits, group(128),
-        codes, scales, zeros, U, V (numpy or torch), r_stored, r_alloc, row_begin(0), row_end(N)."""
+        codes, scales, zeros, U, V (numpy or torch), r_stored, r_alloc, row_begin(0), row_end(N), glue(0),
+        factor_dtype(FACTORS_BF16; FACTORS_FP8: U / V e4m3 bytes + fp32 u_scale / v_scale [r_stored])."""
         arr = (_lib.hc_matrix_desc * len(mats))()
         for i, m in enumerate(mats):
             d = arr[i]
@@ -194,6 +196,8 @@ class Context:
             d.r_stored, d.r_alloc = int(m.get("r_stored", 0)), int(m.get("r_alloc", 0))
             d.row_begin, d.row_end = int(m.get("row_begin", 0)), int(m.get("row_end", m["N"]))
             d.glue = int(m.get("glue", 0))
+            d.factor_dtype = int(m.get("factor_dtype", 0))
+            d.u_scale, d.v_scale = _ptr(m.get("u_scale")), _ptr(m.get("v_scale"))
         check(lib().hc_load_layer(self._h, arr, len(mats), _stream(stream)))
 
     def init_comm(self, rank: int, world: int, group=None):

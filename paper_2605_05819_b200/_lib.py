@@ -13,6 +13,7 @@ HC_OK, HC_ERR_CONFIG, HC_ERR_STATE, HC_ERR_NUMERIC, HC_ERR_RUNTIME = 0, 2, 3, 4,
 QKV, O, UPGATE, DOWN = 0, 1, 2, 3
 OUT_F32, OUT_BF16 = 0, 1
 GLUE_NONE, GLUE_SILU_MUL = 0, 1
+FACTORS_BF16, FACTORS_FP8 = 0, 1
 
 
 class HCError(RuntimeError):
@@ -39,7 +40,7 @@ class hc_matrix_desc(C.Structure):
                 ("codes", C.c_void_p), ("scales", C.c_void_p), ("zeros", C.c_void_p),
                 ("U", C.c_void_p), ("V", C.c_void_p),
                 ("r_stored", C.c_int32), ("r_alloc", C.c_int32), ("row_begin", C.c_int32), ("row_end", C.c_int32),
-                ("glue", C.c_int32)]
+                ("glue", C.c_int32), ("factor_dtype", C.c_int32), ("u_scale", C.c_void_p), ("v_scale", C.c_void_p)]
 
 
 # (name, restype, argtypes) — every symbol include/hcinfer.h declares

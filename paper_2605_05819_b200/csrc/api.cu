@@ -47,6 +47,8 @@ struct Member {
   // prefill (tcgen05) copies, 4-bit plain members only: nibble-paired codes, canonical scales /
   // zeros of the shard rows, fp16 U [rows][r_stored] and V [r_stored][K]
   std::shared_ptr<DevBuf> pcodes, pscales, pzeros, U16, V16;
+  bool fp8 = false;                    // e4m3 factors (U / V hold U8 / V8 fragments) with per-rank scales us / vs
+  std::shared_ptr<DevBuf> us, vs;      // fp32 [r_stored]
   int rows() const { return row_end - row_begin; }
   int cap() const { return std::min(std::min(r_stored, N), K); }
 };
@@ -226,6 +228,12 @@ static hc_status validate_desc(const hc_matrix_desc& d, int i) {
   if (!d.codes || !d.scales || !d.zeros) return fail(HC_ERR_CONFIG, "mat %d: null codes/scales/zeros", i);
   if (d.r_stored > 0 && (!d.U || !d.V)) return fail(HC_ERR_CONFIG, "mat %d: r_stored > 0 needs U and V", i);
   if (d.glue != HC_GLUE_NONE && d.glue != HC_GLUE_SILU_MUL) return fail(HC_ERR_CONFIG, "mat %d: glue %d", i, d.glue);
+  if (d.factor_dtype != HC_FACTORS_BF16 && d.factor_dtype != HC_FACTORS_FP8)
+    return fail(HC_ERR_CONFIG, "mat %d: factor_dtype %d", i, d.factor_dtype);
+  if (d.factor_dtype == HC_FACTORS_FP8 && d.expert >= 0)
+    return fail(HC_ERR_CONFIG, "mat %d: fp8 factors are for dense windows (MoE experts take bf16 factors)", i);
+  if (d.factor_dtype == HC_FACTORS_FP8 && d.r_stored > 0 && (!d.u_scale || !d.v_scale))
+    return fail(HC_ERR_CONFIG, "mat %d: fp8 factors need u_scale and v_scale", i);
   if (d.glue == HC_GLUE_SILU_MUL && (d.window_kind != HC_WIN_UPGATE || (d.slot != 0 && d.slot != 1)))
     return fail(HC_ERR_CONFIG, "mat %d: SiLU glue needs an UPGATE window with slots 0 (up) and 1 (gate)", i);
   return HC_OK;
@@ -237,7 +245,9 @@ struct Staged {
   const uint32_t* codes = nullptr;
   const uint16_t* scales = nullptr;
   const uint8_t* zeros = nullptr;
-  const uint16_t *U = nullptr, *V = nullptr;
+  const uint16_t *U = nullptr, *V = nullptr;     // bf16, or the e4m3 bytes (fp8 factors)
+  DevBuf tus, tvs;
+  const float *us = nullptr, *vs = nullptr;      // fp8 per-rank scales
 };
 
 static const void* to_device(const void* src, size_t bytes, DevBuf& tmp, cudaStream_t st, cudaError_t& err) {
@@ -259,10 +269,17 @@ static hc_status stage(const hc_matrix_desc& d, Staged& s, cudaStream_t st) {
   s.zeros = (const uint8_t*)to_device(d.zeros, (size_t)d.N * G, s.tz, st, e);
   CUDA_TRY(e);
   if (d.r_stored > 0) {
-    s.U = (const uint16_t*)to_device(d.U, (size_t)d.N * d.r_stored * 2, s.tu, st, e);
+    const size_t es = d.factor_dtype == HC_FACTORS_FP8 ? 1 : 2;
+    s.U = (const uint16_t*)to_device(d.U, (size_t)d.N * d.r_stored * es, s.tu, st, e);
     CUDA_TRY(e);
-    s.V = (const uint16_t*)to_device(d.V, (size_t)d.r_stored * d.K * 2, s.tv, st, e);
+    s.V = (const uint16_t*)to_device(d.V, (size_t)d.r_stored * d.K * es, s.tv, st, e);
     CUDA_TRY(e);
+    if (d.factor_dtype == HC_FACTORS_FP8) {
+      s.us = (const float*)to_device(d.u_scale, (size_t)d.r_stored * 4, s.tus, st, e);
+      CUDA_TRY(e);
+      s.vs = (const float*)to_device(d.v_scale, (size_t)d.r_stored * 4, s.tvs, st, e);
+      CUDA_TRY(e);
+    }
   }
   return HC_OK;
 }
@@ -280,6 +297,9 @@ static Member make_member(const hc_matrix_desc& d) {
   m.pzeros = std::make_shared<DevBuf>();
   m.U16 = std::make_shared<DevBuf>();
   m.V16 = std::make_shared<DevBuf>();
+  m.fp8 = d.factor_dtype == HC_FACTORS_FP8;
+  m.us = std::make_shared<DevBuf>();
+  m.vs = std::make_shared<DevBuf>();
   return m;
 }
 
@@ -295,10 +315,45 @@ static hc_status build_prefill(Member& m, const Staged& sd, cudaStream_t st) {
                                        (uint16_t*)m.pscales->p, (uint8_t*)m.pzeros->p, st));
   if (m.r_stored > 0) {
     CUDA_TRY(m.U16->alloc((size_t)rows * m.r_stored * 2));
-    CUDA_TRY(hc::launch_bf16_to_f16(sd.U + (size_t)m.row_begin * m.r_stored, (uint16_t*)m.U16->p, (size_t)rows * m.r_stored, st));
     CUDA_TRY(m.V16->alloc((size_t)m.r_stored * m.K * 2));
-    CUDA_TRY(hc::launch_bf16_to_f16(sd.V, (uint16_t*)m.V16->p, (size_t)m.r_stored * m.K, st));
+    if (m.fp8) {   // fp16(e4m3 · scale): one rounding of U_eff / V_eff
+      CUDA_TRY(hc::launch_fp8_to_f16((const uint8_t*)sd.U + (size_t)m.row_begin * m.r_stored, sd.us, (size_t)rows * m.r_stored,
+                                     m.r_stored, false, m.K, (uint16_t*)m.U16->p, st));
+      CUDA_TRY(hc::launch_fp8_to_f16((const uint8_t*)sd.V, sd.vs, (size_t)m.r_stored * m.K, m.r_stored, true, m.K,
+                                     (uint16_t*)m.V16->p, st));
+    } else {
+      CUDA_TRY(hc::launch_bf16_to_f16(sd.U + (size_t)m.row_begin * m.r_stored, (uint16_t*)m.U16->p, (size_t)rows * m.r_stored, st));
+      CUDA_TRY(hc::launch_bf16_to_f16(sd.V, (uint16_t*)m.V16->p, (size_t)m.r_stored * m.K, st));
+    }
   }
+  return HC_OK;
+}
+
+// fp8 factors of one member (or the fused pair): U8 fragments from rows U0 / U1 (rstride as RepackSrc), V8
+// pieces, the per-rank scales copied to member-owned buffers; HC_ERR_NUMERIC on a NaN encoding.
+static hc_status load_fp8(Member& m, const uint8_t* U0, const uint8_t* U1, int rstride, int n_rb, const Staged& sd,
+                          bool with_u, cudaStream_t st) {
+  if (m.r_stored == 0) return HC_OK;
+  DevBuf flag;
+  CUDA_TRY(flag.alloc(sizeof(unsigned)));
+  CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(unsigned), st));
+  if (with_u) CUDA_TRY(m.U->alloc((size_t)n_rb * hc::kRows * m.r_stored));
+  CUDA_TRY(m.V->alloc((size_t)m.r_stored * m.K));
+  CUDA_TRY(hc::launch_repack_fp8(U0, U1, rstride, with_u ? n_rb : 0, (const uint8_t*)sd.V, m.K, m.r_stored,
+                                 with_u ? (uint8_t*)m.U->p : nullptr, (uint8_t*)m.V->p, (unsigned*)flag.p, st));
+  CUDA_TRY(m.us->alloc((size_t)m.r_stored * 4));
+  CUDA_TRY(m.vs->alloc((size_t)m.r_stored * 4));
+  CUDA_TRY(cudaMemcpyAsync(m.us->p, sd.us, (size_t)m.r_stored * 4, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(m.vs->p, sd.vs, (size_t)m.r_stored * 4, cudaMemcpyDeviceToDevice, st));
+  unsigned h = 0;
+  CUDA_TRY(cudaMemcpyAsync(&h, flag.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (h) return fail(HC_ERR_NUMERIC, "fp8 factors: NaN encoding (0x7F / 0xFF) in U or V");
+  std::vector<float> sc(2 * m.r_stored);
+  CUDA_TRY(cudaMemcpy(sc.data(), m.us->p, (size_t)m.r_stored * 4, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(sc.data() + m.r_stored, m.vs->p, (size_t)m.r_stored * 4, cudaMemcpyDeviceToHost));
+  for (float v : sc)
+    if (!std::isfinite(v)) return fail(HC_ERR_NUMERIC, "fp8 factors: non-finite scale");
   return HC_OK;
 }
 
@@ -323,8 +378,9 @@ static hc_status load_one(hc_ctx* ctx, const hc_matrix_desc* mats, int32_t n_mat
       const hc_matrix_desc& up = d.slot == 0 ? d : mats[j];
       const hc_matrix_desc& gate = d.slot == 0 ? mats[j] : d;
       if (up.N != gate.N || up.K != gate.K || up.bits != gate.bits || up.r_stored != gate.r_stored ||
-          up.row_begin != gate.row_begin || up.row_end != gate.row_end)
-        return fail(HC_ERR_CONFIG, "SiLU glue: up and gate must have identical shape, bits, r_stored and shard");
+          up.row_begin != gate.row_begin || up.row_end != gate.row_end || up.factor_dtype != gate.factor_dtype)
+        return fail(HC_ERR_CONFIG, "SiLU glue: up and gate must have identical shape, bits, r_stored, shard and factor dtype");
+      const bool f8 = up.factor_dtype == HC_FACTORS_FP8;
       Member mu = make_member(up), mg = make_member(gate);
       const int rows = mu.rows();
       Staged su, sg;
@@ -333,7 +389,7 @@ static hc_status load_one(hc_ctx* ctx, const hc_matrix_desc* mats, int32_t n_mat
       s = stage(gate, sg, st);
       if (s != HC_OK) return s;
       CUDA_TRY(mu.rec->alloc((size_t)(rows / 8) * G * hc::rec_bytes(up.bits)));
-      if (up.r_stored > 0) {
+      if (up.r_stored > 0 && !f8) {
         CUDA_TRY(mu.U->alloc((size_t)2 * rows * up.r_stored * 2));
         CUDA_TRY(mu.V->alloc((size_t)up.r_stored * up.K * 2));
         CUDA_TRY(mg.V->alloc((size_t)gate.r_stored * gate.K * 2));
@@ -343,14 +399,21 @@ static hc_status load_one(hc_ctx* ctx, const hc_matrix_desc* mats, int32_t n_mat
       src.codes[0] = su.codes + (size_t)up.row_begin * wpr;  src.codes[1] = sg.codes + (size_t)up.row_begin * wpr;
       src.scales[0] = su.scales + (size_t)up.row_begin * G;  src.scales[1] = sg.scales + (size_t)up.row_begin * G;
       src.zeros[0] = su.zeros + (size_t)up.row_begin * G;    src.zeros[1] = sg.zeros + (size_t)up.row_begin * G;
-      src.U[0] = su.U ? su.U + (size_t)up.row_begin * up.r_stored : nullptr;
-      src.U[1] = sg.U ? sg.U + (size_t)up.row_begin * up.r_stored : nullptr;
+      src.U[0] = (su.U && !f8) ? su.U + (size_t)up.row_begin * up.r_stored : nullptr;
+      src.U[1] = (sg.U && !f8) ? sg.U + (size_t)up.row_begin * up.r_stored : nullptr;
       src.rstride = 8;
-      CUDA_TRY(hc::launch_repack_records(src, up.K, up.bits, up.r_stored, rows / 8, (uint8_t*)mu.rec->p,
+      CUDA_TRY(hc::launch_repack_records(src, up.K, up.bits, f8 ? 0 : up.r_stored, rows / 8, (uint8_t*)mu.rec->p,
                                          (uint32_t*)mu.U->p, st));
-      CUDA_TRY(hc::launch_repack_v(su.V, up.K, up.r_stored, (uint32_t*)mu.V->p, st));
-      CUDA_TRY(hc::launch_repack_v(sg.V, gate.K, gate.r_stored, (uint32_t*)mg.V->p, st));
-      if (up.r_stored > 0) {
+      if (f8) {
+        hc_status s8 = load_fp8(mu, (const uint8_t*)su.U + (size_t)up.row_begin * up.r_stored,
+                                (const uint8_t*)sg.U + (size_t)up.row_begin * up.r_stored, 8, rows / 8, su, true, st);
+        if (s8 == HC_OK) s8 = load_fp8(mg, nullptr, nullptr, 8, rows / 8, sg, false, st);
+        if (s8 != HC_OK) return s8;
+      } else {
+        CUDA_TRY(hc::launch_repack_v(su.V, up.K, up.r_stored, (uint32_t*)mu.V->p, st));
+        CUDA_TRY(hc::launch_repack_v(sg.V, gate.K, gate.r_stored, (uint32_t*)mg.V->p, st));
+      }
+      if (up.r_stored > 0 && !f8) {
         CUDA_TRY(mu.Vn->alloc((size_t)up.r_stored * up.K * 2));
         CUDA_TRY(mg.Vn->alloc((size_t)gate.r_stored * gate.K * 2));
         CUDA_TRY(hc::launch_repack_vn(su.V, up.K, up.r_stored, (uint32_t*)mu.Vn->p, st));
@@ -368,9 +431,10 @@ static hc_status load_one(hc_ctx* ctx, const hc_matrix_desc* mats, int32_t n_mat
 
     // ---- plain member
     if (w.glue != HC_GLUE_NONE) { w.members.clear(); w.glue = HC_GLUE_NONE; }
+    const bool f8 = d.factor_dtype == HC_FACTORS_FP8;
     for (const Member& o : w.members)
-      if (o.slot != d.slot && (o.K != d.K || o.bits != d.bits))
-        return fail(HC_ERR_CONFIG, "mat %d: window members must share K and bits", i);
+      if (o.slot != d.slot && (o.K != d.K || o.bits != d.bits || o.fp8 != f8))
+        return fail(HC_ERR_CONFIG, "mat %d: window members must share K, bits and the factor dtype", i);
     {
       const bool replaces = std::any_of(w.members.begin(), w.members.end(), [&](const Member& o) { return o.slot == d.slot; });
       if (!replaces && (int)w.members.size() >= hc::kMaxMembers)   // checked before the window is touched
@@ -380,7 +444,7 @@ static hc_status load_one(hc_ctx* ctx, const hc_matrix_desc* mats, int32_t n_mat
     Member m = make_member(d);
     const int rows = m.rows();
     CUDA_TRY(m.rec->alloc((size_t)(rows / hc::kRows) * G * hc::rec_bytes(d.bits)));
-    if (d.r_stored > 0) {
+    if (d.r_stored > 0 && !f8) {
       CUDA_TRY(m.U->alloc((size_t)rows * d.r_stored * 2));
       CUDA_TRY(m.V->alloc((size_t)d.r_stored * d.K * 2));
     }
@@ -392,13 +456,19 @@ static hc_status load_one(hc_ctx* ctx, const hc_matrix_desc* mats, int32_t n_mat
     src.codes[0] = sd.codes + (size_t)d.row_begin * wpr;  src.codes[1] = src.codes[0] + (size_t)8 * wpr;
     src.scales[0] = sd.scales + (size_t)d.row_begin * G;  src.scales[1] = src.scales[0] + (size_t)8 * G;
     src.zeros[0] = sd.zeros + (size_t)d.row_begin * G;    src.zeros[1] = src.zeros[0] + (size_t)8 * G;
-    src.U[0] = sd.U ? sd.U + (size_t)d.row_begin * d.r_stored : nullptr;
-    src.U[1] = sd.U ? src.U[0] + (size_t)8 * d.r_stored : nullptr;
+    src.U[0] = (sd.U && !f8) ? sd.U + (size_t)d.row_begin * d.r_stored : nullptr;
+    src.U[1] = (sd.U && !f8) ? src.U[0] + (size_t)8 * d.r_stored : nullptr;
     src.rstride = hc::kRows;
-    CUDA_TRY(hc::launch_repack_records(src, d.K, d.bits, d.r_stored, rows / hc::kRows, (uint8_t*)m.rec->p,
+    CUDA_TRY(hc::launch_repack_records(src, d.K, d.bits, f8 ? 0 : d.r_stored, rows / hc::kRows, (uint8_t*)m.rec->p,
                                        (uint32_t*)m.U->p, st));
-    CUDA_TRY(hc::launch_repack_v(sd.V, d.K, d.r_stored, (uint32_t*)m.V->p, st));
-    if (d.r_stored > 0) {
+    if (f8) {
+      const uint8_t* u8 = (const uint8_t*)sd.U + (size_t)d.row_begin * d.r_stored;
+      hc_status s8 = load_fp8(m, u8, u8 + (size_t)8 * d.r_stored, hc::kRows, rows / hc::kRows, sd, true, st);
+      if (s8 != HC_OK) return s8;
+    } else {
+      CUDA_TRY(hc::launch_repack_v(sd.V, d.K, d.r_stored, (uint32_t*)m.V->p, st));
+    }
+    if (d.r_stored > 0 && !f8) {
       CUDA_TRY(m.Vn->alloc((size_t)d.r_stored * d.K * 2));
       CUDA_TRY(hc::launch_repack_vn(sd.V, d.K, d.r_stored, (uint32_t*)m.Vn->p, st));
     }
@@ -514,7 +584,7 @@ static bool forwardable(const Window& next) {
   const int c = window_chunks(next);
   if (c == 0 || c > kFwdMax || (int)next.members.size() > kMaxMembers) return false;
   for (const Member& m : next.members)
-    if (m.r_alloc > 0 && !(m.Vn && m.Vn->p)) return false;
+    if (m.fp8 || (m.r_alloc > 0 && !(m.Vn && m.Vn->p))) return false;
   return true;
 }
 static bool can_forward(const Window& next) { return options().t_forward && forwardable(next); }
@@ -574,10 +644,13 @@ static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int
     d0.rec = (const uint8_t*)up.rec->p; d0.U = (const uint4*)up.U->p; d0.V = (const uint4*)up.V->p;
     d0.n_rb = up.rows() / 8; d0.rb_begin = 0; d0.row_off = 0; d0.r = up.r_alloc; d0.r_stored = up.r_stored;
     d0.chunk_begin = 0;
+    d0.us = up.fp8 ? (const float*)up.us->p : nullptr; d0.vs = up.fp8 ? (const float*)up.vs->p : nullptr;
     DMember& d1 = a.m[1];
     d1.rec = nullptr; d1.U = nullptr; d1.V = (const uint4*)gate.V->p;
     d1.n_rb = 0; d1.rb_begin = INT_MAX; d1.row_off = 0; d1.r = gate.r_alloc; d1.r_stored = gate.r_stored;
     d1.chunk_begin = (up.r_alloc + 15) / 16;
+    d1.us = gate.fp8 ? (const float*)gate.us->p : nullptr; d1.vs = gate.fp8 ? (const float*)gate.vs->p : nullptr;
+    a.fp8 = up.fp8 ? 1 : 0;
     a.n_rb = d0.n_rb;
     a.ldy = up.rows();
     a.n_chunks = d1.chunk_begin + (gate.r_alloc + 15) / 16;
@@ -596,6 +669,9 @@ static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int
       d.r = m.r_alloc;
       d.r_stored = m.r_stored;
       d.chunk_begin = chunks;
+      d.us = m.fp8 ? (const float*)m.us->p : nullptr;
+      d.vs = m.fp8 ? (const float*)m.vs->p : nullptr;
+      a.fp8 = m.fp8 ? 1 : 0;
       rb += d.n_rb;
       row += m.rows();
       chunks += (m.r_alloc + 15) / 16;

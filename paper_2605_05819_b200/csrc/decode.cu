@@ -115,7 +115,7 @@ __device__ __forceinline__ void dep_wait(const DArgs& a, int lane) {
 }
 
 // I8: int8 tensor-core path (decode_i8.cuh; BITS = 4, NB8 = 1, B <= 2): x staged as x8 digits
-template <int BITS, int NB8, bool XS, bool I8>
+template <int BITS, int NB8, bool XS, bool I8, bool F8>
 __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const __grid_constant__ DArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
 
   const int n_items = a.n_rb;
   // the V·x share lives on the first CTAs (started first), ~kVPerWarp 1 KB pieces per tile warp
-  const int n_vp = a.t_in ? 0 : a.n_chunks * 4 * a.G;   // t_in: t already accumulated by the producer of x
+  const int n_vp = a.t_in ? 0 : a.n_chunks * (F8 ? 2 : 4) * a.G;   // t_in: t accumulated by the producer of x
   const int n_vctas = n_vp == 0 ? 0 : min((int)gridDim.x, (n_vp + kDecodeWarps * kVPerWarp - 1) / (kDecodeWarps * kVPerWarp));
   const int n_vwarps = n_vctas * kDecodeWarps;            // v_done target
 
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
         uint32_t bytes;
         if (vp < vp_end) {
           int g, part;
-          src = v_piece(a, vp, g, part);
+          src = F8 ? v_piece8(a, vp, g, part) : v_piece(a, vp, g, part);
           bytes = 1024u;
           ++vp;
         } else {
@@ -222,9 +222,11 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
       const int nck = min((r_eff + 15) >> 4, kUPre);
       if (nck == 0) return;
       if (lane == 0) {
-        const uint32_t bytes = (uint32_t)nck * 512u;
+        const uint32_t cb = F8 ? 256u : 512u;          // bytes of one rank chunk of a row block's U fragments
+        const uint32_t bytes = (uint32_t)nck * cb;
         mbar_expect_tx(&ubar[par], bytes);
-        bulk_copy(ubuf + par * kUPre * 32, m.U + (size_t)(rb - m.rb_begin) * (m.r_stored >> 4) * 32, bytes,
+        bulk_copy(ubuf + par * kUPre * 32,
+                  reinterpret_cast<const uint8_t*>(m.U) + (size_t)(rb - m.rb_begin) * (m.r_stored >> 4) * cb, bytes,
                   &ubar[par], evict_first_policy());
       }
     };
@@ -275,8 +277,12 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
             uint32_t hi[2], lo[2];
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
-              const float ta = (r0 + 8 * hh < mt.r) ? (float)tr[2 * hh] * 0x1p-36f : 0.f;
-              const float tb = (r0 + 8 * hh + 1 < mt.r) ? (float)tr[2 * hh + 1] * 0x1p-36f : 0.f;
+              float ta = (r0 + 8 * hh < mt.r) ? (float)tr[2 * hh] * 0x1p-36f : 0.f;
+              float tb = (r0 + 8 * hh + 1 < mt.r) ? (float)tr[2 * hh + 1] * 0x1p-36f : 0.f;
+              if constexpr (F8) {                        // t'_j = u_scale_j·t_j (unconditional, in-range loads)
+                ta *= mt.us[min(r0 + 8 * hh, mt.r_stored - 1)];
+                tb *= mt.us[min(r0 + 8 * hh + 1, mt.r_stored - 1)];
+              }
               const uint32_t ha = f32_to_bf16_rn(ta), hb = f32_to_bf16_rn(tb);
               hi[hh] = ha | (hb << 16);
               lo[hh] = f32_to_bf16_rn(ta - bf16_bits_to_f32(ha)) | (f32_to_bf16_rn(tb - bf16_bits_to_f32(hb)) << 16);
@@ -284,7 +290,8 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
             tsm[((size_t)cc * NB8 + nb) * 32 + lane] = make_uint4(hi[0], hi[1], lo[0], lo[1]);
           }
         }
-        if (t_deep) t_fragments_xt<NB8>(a, tsm, lane);   // rare: outlier or tiny activations (R22)
+        // rare: outlier or tiny activations (R22); fp8 factors (u_scale folded into t)
+        if (t_deep) t_fragments_full<NB8>(a, tsm, lane, true);
         __syncwarp();
         t_ready = true;
         if (lane == 0) dtrace(a, 5);
@@ -324,9 +331,16 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
         while (!mbar_try_wait(&ubar[par], (u_phase >> par) & 1u)) {}
         u_phase ^= 1u << par;
         for (int c = 0; c < nck; ++c) {
-          const uint4 u = (c < kUPre) ? ubuf[(par * kUPre + c) * 32 + lane]
-                                      : __ldg(m.U + ((size_t)rbl * (m.r_stored >> 4) + c) * 32 + lane);
-          const uint32_t af[4] = {u.x, u.y, u.z, u.w};
+          uint32_t af[4];
+          if constexpr (F8) {                            // e4m3 fragments, converted exactly (t carries u_scale)
+            const uint2 u8 = (c < kUPre) ? reinterpret_cast<const uint2*>(ubuf + par * kUPre * 32)[c * 32 + lane]
+                                         : __ldg(reinterpret_cast<const uint2*>(m.U) + ((size_t)rbl * (m.r_stored >> 4) + c) * 32 + lane);
+            e4m3x8_frag(u8, af);
+          } else {
+            const uint4 u = (c < kUPre) ? ubuf[(par * kUPre + c) * 32 + lane]
+                                        : __ldg(m.U + ((size_t)rbl * (m.r_stored >> 4) + c) * 32 + lane);
+            af[0] = u.x; af[1] = u.y; af[2] = u.z; af[3] = u.w;
+          }
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             if (h == 1 && !a.glue) break;
@@ -526,13 +540,23 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
   // epilogue.  Partials of consecutive pieces of one chunk are summed in registers before the atomics.
   {
     float tp[NB8][4];
+    // fp8 factors: t_j = v_scale_j · Σ_k e4m3(V[j][k])·x_k; the scales of the current chunk's ranks gid and
+    // gid + 8 are loaded when the chunk starts (off the atomics' critical path)
+    float vsc[2] = {1.f, 1.f};
+    auto load_vsc = [&](int cc) {
+      if constexpr (F8) {
+        const DMember& mv = a.m[member_of_chunk(a, cc)];
+        vsc[0] = mv.vs[16 * (cc - mv.chunk_begin) + gid];
+        vsc[1] = mv.vs[16 * (cc - mv.chunk_begin) + gid + 8];
+      }
+    };
     auto flush = [&](int cc) {
 #pragma unroll
       for (int nb = 0; nb < NB8; ++nb)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int col = 2 * tig + (e & 1) + 8 * nb, rank = gid + 8 * (e >> 1);
-          if (col < a.B) tacc_add(a.tacc, a.n_chunks, cc, col, rank, tp[nb][e]);
+          if (col < a.B) tacc_add(a.tacc, a.n_chunks, cc, col, rank, F8 ? tp[nb][e] * vsc[e >> 1] : tp[nb][e]);
           tp[nb][e] = 0.f;
         }
     };
@@ -545,21 +569,35 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
       const int s = c_slot;
       const uint32_t ph = c_ph;
       int g, part;
-      v_piece(a, vp, g, part);
-      const int cc = vp / (4 * a.G);
+      if constexpr (F8) v_piece8(a, vp, g, part); else v_piece(a, vp, g, part);
+      const int cc = vp / ((F8 ? 2 : 4) * a.G);
       if (cc != cc_cur) {
         if (cc_cur >= 0) flush(cc_cur);
         cc_cur = cc;
+        load_vsc(cc);
       }
-      uint4 xv[NB8];
+      if constexpr (F8) {                                // 16 ranks x 64 k: two 32-k x runs per lane
+        uint4 xa[NB8], xb[NB8];
 #pragma unroll
-      for (int nb = 0; nb < NB8; ++nb) {
-        const uint4* p = reinterpret_cast<const uint4*>(a.x + (size_t)xrow(a, gid + 8 * nb) * a.ldx + 8 * tig +
-                                                        g * kGroup + 32 * part);
-        xv[nb] = __ldcg(p);                              // bf16 x from L2 (written by the producer window)
+        for (int nb = 0; nb < NB8; ++nb) {
+          const uint4* p = reinterpret_cast<const uint4*>(a.x + (size_t)xrow(a, gid + 8 * nb) * a.ldx + 8 * tig +
+                                                          g * kGroup + 64 * part);
+          xa[nb] = __ldcg(p);
+          xb[nb] = __ldcg(p + 4);
+        }
+        while (!mbar_try_wait(&bars[s], ph)) {}
+        v_tile8<NB8>(bufs + s * kBlk, lane, xa, xb, tp);
+      } else {
+        uint4 xv[NB8];
+#pragma unroll
+        for (int nb = 0; nb < NB8; ++nb) {
+          const uint4* p = reinterpret_cast<const uint4*>(a.x + (size_t)xrow(a, gid + 8 * nb) * a.ldx + 8 * tig +
+                                                          g * kGroup + 32 * part);
+          xv[nb] = __ldcg(p);                            // bf16 x from L2 (written by the producer window)
+        }
+        while (!mbar_try_wait(&bars[s], ph)) {}
+        v_tile<NB8>(bufs + s * kBlk, lane, xv, tp);
       }
-      while (!mbar_try_wait(&bars[s], ph)) {}
-      v_tile<NB8>(bufs + s * kBlk, lane, xv, tp);
       advance();
     }
     if (cc_cur >= 0) flush(cc_cur);
@@ -772,13 +810,13 @@ cudaError_t launch_xprep(const uint16_t* x, int ldx, int B, int K, int bits, uin
   }
 }
 
-template <int BITS, int NB8, bool XS, bool I8>
-static cudaError_t launch_t(const DArgs& a, int grid, cudaStream_t st) {
+template <int BITS, int NB8, bool XS, bool I8, bool F8>
+static cudaError_t launch_tf(const DArgs& a, int grid, cudaStream_t st) {
   const size_t smem = decode_smem_bytes(XS, I8, a.B, a.K, a.n_chunks, a.fwd ? a.fwd_chunks : 0);
   if (smem > kSmemOptin) return cudaErrorInvalidConfiguration;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(decode_kernel<BITS, NB8, XS, I8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(decode_kernel<BITS, NB8, XS, I8, F8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kSmemOptin);
     if (e != cudaSuccess) return e;
     attr = true;
@@ -793,16 +831,25 @@ static cudaError_t launch_t(const DArgs& a, int grid, cudaStream_t st) {
   at[0].val.programmaticStreamSerializationAllowed = options().pdl ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, decode_kernel<BITS, NB8, XS, I8>, a);
+  return cudaLaunchKernelEx(&cfg, decode_kernel<BITS, NB8, XS, I8, F8>, a);
+}
+// fp8 factors select their own instantiation (no run-time branch in the bf16 kernels)
+template <int BITS, int NB8, bool XS, bool I8>
+static cudaError_t launch_t(const DArgs& a, int grid, cudaStream_t st) {
+  return a.fp8 ? launch_tf<BITS, NB8, XS, I8, true>(a, grid, st) : launch_tf<BITS, NB8, XS, I8, false>(a, grid, st);
 }
 
 template <int BITS, int NB8, bool XS, bool I8>
 static int max_ctas_t(int B, int K, int n_chunks, int fwd_chunks) {
   const size_t smem = decode_smem_bytes(XS, I8, B, K, n_chunks, fwd_chunks);
-  cudaFuncSetAttribute(decode_kernel<BITS, NB8, XS, I8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(decode_kernel<BITS, NB8, XS, I8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)kSmemOptin);
-  int per_sm = 0, dev = 0, sms = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<BITS, NB8, XS, I8>, kDecodeBlock, smem);
+  cudaFuncSetAttribute(decode_kernel<BITS, NB8, XS, I8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kSmemOptin);
+  int per_sm = 0, per_sm8 = 0, dev = 0, sms = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<BITS, NB8, XS, I8, false>, kDecodeBlock, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm8, decode_kernel<BITS, NB8, XS, I8, true>, kDecodeBlock, smem);
+  per_sm = per_sm < per_sm8 ? per_sm : per_sm8;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   return per_sm * sms;

@@ -41,6 +41,8 @@ struct DMember {
   int r_stored;
   int chunk_begin;      // first window-global rank chunk (16 ranks) of this member
   int full_off;         // peer mode: output column (in the full, gathered window output) of local row 0
+  const float* us;      // fp8 factors (DArgs::fp8): per-rank scales of U and V [r_stored]
+  const float* vs;
 };
 
 constexpr int kMaxPeers = 8;
@@ -57,6 +59,8 @@ struct DArgs {
   int ld_resid;
   int glue;             // 0 none; 1 fused SiLU(gate)*up: m[0] = up (holds the interleaved records and U),
                         //   m[1] = gate (V / rank only); row block = 8 up rows + 8 gate rows
+  int fp8;              // 1: U / V are e4m3 fragments (U: [rb][c][lane][8 B], V: 1 KB pieces of 16 ranks x 64 k)
+                        //    with per-rank scales DMember::us / vs
   int n_rb;             // Σ members
   int n_chunks;         // Σ ceil(r_m / 16)
   const uint16_t* x16;  // !XS launches: fp16 x' = x·2^-fp [B][K] written by launch_xprep (else unused)

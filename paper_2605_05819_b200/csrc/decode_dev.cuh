@@ -216,6 +216,35 @@ __device__ __forceinline__ const uint8_t* v_piece(const DArgs& a, int vp, int& g
   return reinterpret_cast<const uint8_t*>(m.V + ((size_t)(cc - m.chunk_begin) * a.G * 256 + (size_t)rem * 64));
 }
 
+// fp8 (e4m3) factors: V piece vp of a window = (chunk cc, group g, half p2): steps 4·p2 .. 4·p2 + 3 of the
+// (chunk, group), 16 ranks x 64 k in 1 KB (repack.cu repack_v8_kernel).
+__device__ __forceinline__ const uint8_t* v_piece8(const DArgs& a, int vp, int& g, int& p2) {
+  const int per_chunk = 2 * a.G;
+  const int cc = vp / per_chunk, rem = vp - cc * per_chunk;
+  g = rem >> 1;
+  p2 = rem & 1;
+  const DMember& m = a.m[member_of_chunk(a, cc)];
+  return reinterpret_cast<const uint8_t*>(m.V) + ((size_t)(cc - m.chunk_begin) * a.G * 2 + rem) * 1024;
+}
+
+// Two e4m3 bytes (bytes 0 and 1 of w) -> bf16x2, exactly: the byte's magnitude bits placed in a bf16 as
+// exponent field e and mantissa m << 4 give value·2^-120 for normals and subnormals alike (a bf16
+// subnormal for e = 0), and x 2^120 in bf16 is exact.
+__device__ __forceinline__ uint32_t e4m3x2_bf16x2(uint32_t w) {
+  const uint32_t t = __byte_perm(w, 0u, 0x4140);                 // byte 0 -> bits 0-7, byte 1 -> bits 16-23
+  const uint32_t r = ((t & 0x007F007Fu) << 4) | ((t & 0x00800080u) << 8);
+  __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(&r);
+  v = __hmul2(v, __floats2bfloat162_rn(0x1p120f, 0x1p120f));
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+// 8 e4m3 bytes of an A fragment (byte 2i + h = register i, half h) -> the 4 bf16x2 registers.
+__device__ __forceinline__ void e4m3x8_frag(const uint2 v, uint32_t (&af)[4]) {
+  af[0] = e4m3x2_bf16x2(v.x);
+  af[1] = e4m3x2_bf16x2(v.x >> 16);
+  af[2] = e4m3x2_bf16x2(v.y);
+  af[3] = e4m3x2_bf16x2(v.y >> 16);
+}
+
 #ifndef HC_VPW
 #define HC_VPW 1
 #endif
@@ -264,22 +293,33 @@ __device__ __forceinline__ void tacc_read2(const long long* t, int cc, int col, 
     tb = fmaf((float)__ldcg(p1 + 1), 0x1p-12f, tb + fmaf((float)__ldcg(p2 + 1), 0x1p-72f, (float)__ldcg(p3 + 1) * 0x1p-96f));
   }
 }
-// Out-of-line t fragment pass over all four tiers (windows whose extra-tier flag is set, R22): rebuilds
-// tsm exactly as the tier-0 pass of the epilogue does, with t = Σ tiers.
+// Out-of-line t fragment pass (DArgs::fp8 windows, and windows whose extra-tier flag is set, R22): rebuilds
+// tsm as the tier-0 pass of the epilogue does, with t = Σ tiers when xt, and t'_j = u_scale_j·t_j for fp8
+// factors (the U mma then multiplies the exact e4m3 values).
 template <int NB8>
-__device__ __noinline__ void t_fragments_xt(const DArgs& a, uint4* tsm, int lane) {
+__device__ __noinline__ void t_fragments_full(const DArgs& a, uint4* tsm, int lane, bool xt) {
   const int gid = lane >> 2, tig = lane & 3;
   for (int cc = 0; cc < a.n_chunks; ++cc) {
     const DMember& mt = a.m[member_of_chunk(a, cc)];
     const int r0 = 16 * (cc - mt.chunk_begin) + 2 * tig;
     for (int nb = 0; nb < NB8; ++nb) {
       float tr[4];
-      tacc_read2<true>(a.tacc, cc, (gid + 8 * nb) & 15, 2 * tig, tr[0], tr[1]);
-      tacc_read2<true>(a.tacc, cc, (gid + 8 * nb) & 15, 2 * tig + 8, tr[2], tr[3]);
+      if (xt) {
+        tacc_read2<true>(a.tacc, cc, (gid + 8 * nb) & 15, 2 * tig, tr[0], tr[1]);
+        tacc_read2<true>(a.tacc, cc, (gid + 8 * nb) & 15, 2 * tig + 8, tr[2], tr[3]);
+      } else {
+        tacc_read2<false>(a.tacc, cc, (gid + 8 * nb) & 15, 2 * tig, tr[0], tr[1]);
+        tacc_read2<false>(a.tacc, cc, (gid + 8 * nb) & 15, 2 * tig + 8, tr[2], tr[3]);
+      }
       uint32_t hi[2], lo[2];
       for (int hh = 0; hh < 2; ++hh) {
-        const float ta = (r0 + 8 * hh < mt.r) ? tr[2 * hh] : 0.f;
-        const float tb = (r0 + 8 * hh + 1 < mt.r) ? tr[2 * hh + 1] : 0.f;
+        const int ra = r0 + 8 * hh, rb = ra + 1;
+        float ta = ra < mt.r ? tr[2 * hh] : 0.f;
+        float tb = rb < mt.r ? tr[2 * hh + 1] : 0.f;
+        if (a.fp8) {
+          ta *= ra < mt.r ? mt.us[ra] : 0.f;
+          tb *= rb < mt.r ? mt.us[rb] : 0.f;
+        }
         const uint32_t ha = f32_to_bf16_rn(ta), hb = f32_to_bf16_rn(tb);
         hi[hh] = ha | (hb << 16);
         lo[hh] = f32_to_bf16_rn(ta - bf16_bits_to_f32(ha)) | (f32_to_bf16_rn(tb - bf16_bits_to_f32(hb)) << 16);
@@ -528,6 +568,22 @@ __device__ __forceinline__ void v_tile(const uint8_t* piece, int lane, const uin
     for (int nb = 0; nb < NB8; ++nb) {
       if (s == 0) mma16816(tot[nb], af, xv[nb].x, xv[nb].y);
       else        mma16816(tot[nb], af, xv[nb].z, xv[nb].w);
+    }
+  }
+}
+
+// fp8 V piece (4 steps, 16 ranks x 64 k): xa / xb = the lane's x runs of the piece's two 32-k halves.
+template <int NB8>
+__device__ __forceinline__ void v_tile8(const uint8_t* piece, int lane, const uint4 (&xa)[NB8], const uint4 (&xb)[NB8],
+                                        float (&tot)[NB8][4]) {
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    uint32_t af[4];
+    e4m3x8_frag(*reinterpret_cast<const uint2*>(piece + s * 256 + lane * 8), af);
+#pragma unroll
+    for (int nb = 0; nb < NB8; ++nb) {
+      const uint4& xx = s < 2 ? xa[nb] : xb[nb];
+      mma16816(tot[nb], af, (s & 1) ? xx.z : xx.x, (s & 1) ? xx.w : xx.y);
     }
   }
 }

@@ -1,4 +1,5 @@
 // Load-time repack (hc_load_layer) and its host test exports.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstring>
@@ -103,6 +104,88 @@ cudaError_t launch_repack_records(const RepackSrc& src, int K, int bits, int r_s
     n = (long long)n_rb * (r_stored / 16) * 32;
     repack_u_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, n_rb, r_stored, u_out);
   }
+  return cudaGetLastError();
+}
+
+// ---- fp8 (e4m3) compensation factors: the same fragment orders, one byte per value.
+// NaN encodings (|b| = 0x7F) raise *nan_flag.
+// U8: [rb][c][lane][8 bytes], byte 2i + h = U[row frag_row(lane, i)][16c + u_rank(lane, i, h)]
+__global__ void repack_u8_kernel(const uint8_t* __restrict__ U0, const uint8_t* __restrict__ U1, int rstride, int n_rb,
+                                 int r_stored, uint8_t* __restrict__ out, unsigned* nan_flag) {
+  const int nc = r_stored / 16;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= (long long)n_rb * nc * 32) return;
+  const int lane = (int)(tid & 31);
+  const int c = (int)((tid >> 5) % nc), rb = (int)((tid >> 5) / nc);
+  unsigned bad = 0;
+  for (int i = 0; i < 4; ++i) {
+    const uint8_t* row = row_ptr(U0, U1, rstride, (size_t)r_stored, rb, frag_row(lane, i));
+    for (int h = 0; h < 2; ++h) {
+      const uint8_t b = row[16 * c + u_rank(lane, i, h)];
+      bad |= (b & 0x7Fu) == 0x7Fu;
+      out[tid * 8 + 2 * i + h] = b;
+    }
+  }
+  if (bad) atomicOr(nan_flag, 1u);
+}
+// V8 pieces: [c][g][j][lane][8 bytes] (j = step), byte 2i + h = V[rank 16c + frag_row(lane, i)][g·128 + frag_k(lane, j, i, h)];
+// one 1 KB piece = steps 4p .. 4p + 3 of a (chunk, group) = 16 ranks x 64 k
+__global__ void repack_v8_kernel(const uint8_t* __restrict__ V, int K, int r_stored, uint8_t* __restrict__ out,
+                                 unsigned* nan_flag) {
+  const int G = K / kGroup, nc = r_stored / 16;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= (long long)nc * G * 8 * 32) return;
+  const int lane = (int)(tid & 31);
+  const int j = (int)((tid >> 5) & 7);
+  const long long cg = tid >> 8;
+  const int g = (int)(cg % G), c = (int)(cg / G);
+  unsigned bad = 0;
+  for (int i = 0; i < 4; ++i) {
+    const size_t rank = (size_t)(16 * c + frag_row(lane, i));
+    for (int h = 0; h < 2; ++h) {
+      const uint8_t b = V[rank * K + g * kGroup + frag_k(lane, j, i, h)];
+      bad |= (b & 0x7Fu) == 0x7Fu;
+      out[tid * 8 + 2 * i + h] = b;
+    }
+  }
+  if (bad) atomicOr(nan_flag, 1u);
+}
+
+// e4m3 -> float: the byte's magnitude bits placed as a bf16 (exponent field e, mantissa m << 4) is the value
+// times 2^-120 for normals and subnormals alike; x 2^120 is exact.
+__device__ __forceinline__ float e4m3_to_f32(uint8_t b) {
+  const uint32_t bits = ((uint32_t)(b & 0x7Fu) << 20) | ((uint32_t)(b & 0x80u) << 24);
+  return __uint_as_float(bits) * 0x1p120f;
+}
+
+// Prefill copies of fp8 factors: out[i] = fp16(e4m3(in[i]) · scale[rank of i]); rank = i / per_rank (V rows) or
+// i % r_stored (U rows).
+__global__ void fp8_to_f16_kernel(const uint8_t* __restrict__ in, const float* __restrict__ scale, size_t n, int r_stored,
+                                  int rank_major, int K, uint16_t* __restrict__ out) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int rank = rank_major ? (int)(i / (size_t)K) : (int)(i % (size_t)r_stored);
+  out[i] = __half_as_ushort(__float2half_rn(e4m3_to_f32(in[i]) * scale[rank]));
+}
+
+cudaError_t launch_repack_fp8(const uint8_t* U0, const uint8_t* U1, int rstride, int n_rb, const uint8_t* V, int K,
+                              int r_stored, uint8_t* u_out, uint8_t* v_out, unsigned* nan_flag, cudaStream_t st) {
+  if (r_stored <= 0) return cudaSuccess;
+  if (u_out && n_rb > 0) {
+    const long long nu = (long long)n_rb * (r_stored / 16) * 32;
+    repack_u8_kernel<<<(unsigned)((nu + 255) / 256), 256, 0, st>>>(U0, U1, rstride, n_rb, r_stored, u_out, nan_flag);
+  }
+  if (v_out) {
+    const long long nv = (long long)(r_stored / 16) * (K / kGroup) * 8 * 32;
+    repack_v8_kernel<<<(unsigned)((nv + 255) / 256), 256, 0, st>>>(V, K, r_stored, v_out, nan_flag);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fp8_to_f16(const uint8_t* in, const float* scale, size_t n, int r_stored, bool rank_major, int K,
+                              uint16_t* out, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  fp8_to_f16_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(in, scale, n, r_stored, rank_major ? 1 : 0, K, out);
   return cudaGetLastError();
 }
 

@@ -20,4 +20,11 @@ cudaError_t launch_repack_v(const uint16_t* V, int K, int r_stored, uint32_t* v_
 // Natural-k V fragments [K/16][c][lane][4] (standard m16n8k16 A layout: ranks = rows, 16 consecutive k)
 // for t forwarding (DArgs::fwd_vn).
 cudaError_t launch_repack_vn(const uint16_t* V, int K, int r_stored, uint32_t* out, cudaStream_t st);
+// fp8 (e4m3) factors: U8 fragments [rb][c][lane][8 B] of n_rb row blocks (rows from U0 / U1
+// as RepackSrc) and V8 pieces [c][g][j][lane][8 B]; *nan_flag |= 1 on a NaN encoding.
+cudaError_t launch_repack_fp8(const uint8_t* U0, const uint8_t* U1, int rstride, int n_rb, const uint8_t* V, int K,
+                              int r_stored, uint8_t* u_out, uint8_t* v_out, unsigned* nan_flag, cudaStream_t st);
+// fp16(e4m3 · per-rank scale) copies for the prefill path; rank_major: [r_stored][K] (V), else [rows][r_stored] (U).
+cudaError_t launch_fp8_to_f16(const uint8_t* in, const float* scale, size_t n, int r_stored, bool rank_major, int K,
+                              uint16_t* out, cudaStream_t st);
 }  // namespace hc

@@ -94,6 +94,34 @@ def linear_case(seed: int, N: int, K: int, bits: int = 4, group: int = 128,
                 N=N, K=K, bits=bits, group=group, r_stored=r_stored, B=B)
 
 
+def fp8_factors(case: dict, seed: int, all_codes: bool = False) -> dict:
+    """Replace a linear_case's factors by e4m3 bytes + fp32 per-rank scales (SURVEY.md §8(f)4 inputs).
+    Random BYTES, no arithmetic: sign uniform, exponent field uniform in [4, 10] (|v| in [2^-3, 15]) with
+    1/16 of the bytes drawn from the subnormal / zero codes; all_codes cycles through every non-NaN code.
+    Scales fp32: us ~ U(0.5, 1.5)/(4·sqrt(N)), vs ~ U(0.5, 1.5)·σ_V/4 (σ_V of linear_case's bf16 V)."""
+    g = rng(seed)
+    N, K, rs = case["N"], case["K"], case["r_stored"]
+
+    def draw(shape):
+        if all_codes:
+            valid = np.array([c for c in range(256) if (c & 0x7F) != 0x7F], dtype=np.uint8)
+            return valid[np.arange(int(np.prod(shape))) % valid.size].reshape(shape)
+        sign = g.integers(0, 2, size=shape, dtype=np.uint8) << 7
+        e = g.integers(4, 11, size=shape, dtype=np.uint8)
+        sub = g.random(shape) < 1.0 / 16.0
+        e = np.where(sub, 0, e).astype(np.uint8)
+        m = g.integers(0, 8, size=shape, dtype=np.uint8)
+        return (sign | (e << 3) | m).astype(np.uint8)
+    out = dict(case)
+    out["factor_dtype"] = "fp8"
+    out["U8"] = draw((N, rs))
+    out["V8"] = draw((rs, K))
+    sv = 0.05 * np.sqrt(N / (max(rs, 1) * K)) if K else 0.02
+    out["us"] = ((0.5 + g.random(rs, dtype=np.float32)) / np.float32(4.0 * np.sqrt(N))).astype(np.float32)
+    out["vs"] = ((0.5 + g.random(rs, dtype=np.float32)) * np.float32(sv / 4.0)).astype(np.float32)
+    return out
+
+
 def activations(seed: int, B: int, K: int) -> np.ndarray:
     """bf16 bits of x ~ N(0, 1), shape [B, K]."""
     return f32_to_bf16_bits(rng(seed).standard_normal((B, K), dtype=np.float32))

@@ -340,3 +340,37 @@ def test_moe_dynamic_reduces_to_static_and_zero():
     zero = linear.moe_forward_dynamic(ex, caps, x, idx, gate, [dict(up=0.0, gate=0.0, down=0.0)] * 2)
     z_stat = linear.moe_forward(ex, [dict(up=0, gate=0, down=0)] * 2, x, idx, gate)
     assert np.allclose(zero, z_stat, rtol=1e-13, atol=1e-13)
+
+
+def test_e4m3_decode_pins():
+    """OCP E4M3 by hand: zero, the smallest subnormal 2^-9, the largest subnormal 7·2^-9,
+    the smallest normal 2^-6, 1.0, 1.875, 2.0, the largest finite 448, signed zero, -1, NaN; the codes
+    0x00..0x7E increase strictly and within a binade step by 2^(e-10)."""
+    from oracle.packing import e4m3_to_f64
+    vals = e4m3_to_f64(np.array([0x00, 0x01, 0x07, 0x08, 0x38, 0x3F, 0x40, 0x7E, 0x80, 0xB8], dtype=np.uint8))
+    assert list(vals) == [0.0, 2.0 ** -9, 7 * 2.0 ** -9, 2.0 ** -6, 1.0, 1.875, 2.0, 448.0, 0.0, -1.0]
+    assert np.signbit(vals[8])
+    assert np.isnan(e4m3_to_f64(np.array([0x7F, 0xFF], dtype=np.uint8))).all()
+    pos = e4m3_to_f64(np.arange(0x7F, dtype=np.uint8))
+    assert np.all(np.diff(pos) > 0)
+    for c in range(8, 0x7E):
+        e = c >> 3
+        if (c & 7) != 7:
+            assert pos[c + 1] - pos[c] == 2.0 ** (e - 10)
+    assert np.array_equal(e4m3_to_f64(np.arange(0x80, 0xFF, dtype=np.uint8)), -pos)
+
+
+def test_fp8_factor_product_definition():
+    """The fp8 compensated product is the bf16 one with U_eff = e4m3(U8)·us, V_eff = e4m3(V8)·vs: when every
+    byte is a power-of-two code and the scales are 1, U_eff / V_eff equal bf16 factors holding the same values,
+    so both oracle paths agree exactly."""
+    from oracle import linear
+    from oracle.packing import e4m3_to_f64, f64_to_bf16_bits_rne
+    case = synth.linear_case(5, N=32, K=128, bits=4, r_stored=16)
+    g = np.random.default_rng(1)
+    U8 = (g.integers(0, 2, (32, 16)) << 7 | g.integers(3, 12, (32, 16)) << 3).astype(np.uint8)
+    V8 = (g.integers(0, 2, (16, 128)) << 7 | g.integers(3, 12, (16, 128)) << 3).astype(np.uint8)
+    f8 = dict(case, factor_dtype="fp8", U8=U8, V8=V8, us=np.ones(16, np.float32), vs=np.ones(16, np.float32))
+    bf = dict(case, U=f64_to_bf16_bits_rne(e4m3_to_f64(U8)), V=f64_to_bf16_bits_rne(e4m3_to_f64(V8)))
+    for r in (0, 8, 16):
+        assert np.array_equal(linear.compensated_linear(f8, r), linear.compensated_linear(bf, r))
