@@ -130,7 +130,8 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
   uint64_t* ubar = bars_all + kDecodeWarps * kNBuf;       // [2]
   uint64_t* xbar = ubar + 2;
   uint64_t* fbar = xbar + 1;                              // t forwarding: Vn blocks landed
-  uint64_t* ebars_all = xbar + 2;                         // [8 warps][kNBuf] ring slot consumed (empty)
+  uint64_t* dbar = xbar + 2;                              // dataflow dependency met (epilogue -> tile warps)
+  uint64_t* ebars_all = xbar + 4;                         // [8 warps][kNBuf] ring slot consumed (empty; +1 pad: tsm 16-B aligned)
   uint4* tsm = reinterpret_cast<uint4*>(ebars_all + kDecodeWarps * kNBuf);   // [n_chunks][NB8][32] t hi|lo fragments
   uint16_t* xt = reinterpret_cast<uint16_t*>(tsm + (size_t)a.n_chunks * NB8 * 32);   // [16 k][16 cols] fwd x tile
   uint4* fbuf = reinterpret_cast<uint4*>(xt + 256);                                  // [fwd_chunks][32] Vn fragments
@@ -147,7 +148,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
         mbar_init(&ebars_all[warp * kNBuf + s], 32);
       }
     } else if (warp == kDecodeWarps) {
-      mbar_init(&ubar[0], 1); mbar_init(&ubar[1], 1); mbar_init(xbar, 1); mbar_init(fbar, 1);
+      mbar_init(&ubar[0], 1); mbar_init(&ubar[1], 1); mbar_init(xbar, 1); mbar_init(fbar, 1); mbar_init(dbar, 1);
       misc[0] = 0u; misc[1] = 0u;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -234,7 +235,9 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
     dep_wait(a, lane);
     if (blockIdx.x == 0 && a.clr_max)                    // the max buffer the next window publishes into (R20)
       for (int i = lane; i < a.clr_n; i += 32) a.clr_max[i] = 0u;
-    if ((!XS || I8) && a.dep_cnt) asm volatile("bar.sync 6, %0;" ::"n"(kDecodeThreads) : "memory");   // release the tile warps
+    // release the tile warps: one mbarrier arrive after the acquire (cumulative through the mbarrier's
+    // release / acquire); the tile warps read activations only after their wait on it
+    if ((!XS || I8) && a.dep_cnt && lane == 0) mbar_arrive(dbar);
     if (lane == 0) dtrace(a, 1);
     if constexpr (XS && !I8) {
       if (lane == 0) {
@@ -521,7 +524,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
   // tile warps read activations only through the x staged by the epilogue warp (XS, ordered by its
   // acquire and the x mbarrier), except for V pieces and unstaged x: only then do they wait themselves
   if (!a.dep_cnt) dep_wait(a, lane);
-  else if (!XS || I8) asm volatile("bar.sync 6, %0;" ::"n"(kDecodeThreads) : "memory");   // the epilogue warp waited
+  else if (!XS || I8) { while (!mbar_try_wait(dbar, 0)) {} }                 // the epilogue warp waited
   else if (n_vp > 0) dep_wait(a, lane);
   const uint16_t* xs_row[NB8];
 #pragma unroll
@@ -736,7 +739,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
 static size_t decode_smem_bytes(bool xs, bool i8, int B, int K, int n_chunks, int fwd_chunks) {
   const int nb8 = B > 8 ? 2 : 1;
   size_t s = (size_t)kDecodeWarps * kNBuf * kTPB * kTileMax + 2 * kDecodeWarps * 32 * 4 * nb8 * sizeof(float) +
-             2 * kUPre * 32 * 16 + (2 * kDecodeWarps * kNBuf + 4) * sizeof(uint64_t) +
+             2 * kUPre * 32 * 16 + (2 * kDecodeWarps * kNBuf + 6) * sizeof(uint64_t) +
              (size_t)n_chunks * nb8 * 32 * 16 + 512 + (size_t)fwd_chunks * 512;
   s += 16;                                                                 // misc
   if (i8) s += (size_t)(K / kGroup) * x8_stride(B) + kX8Pad;

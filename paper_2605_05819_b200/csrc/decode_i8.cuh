@@ -129,7 +129,10 @@ __device__ __forceinline__ void i8_tile(const uint8_t* rec, int lane, const uint
   const int gid = lane >> 2, tig = lane & 3;
   const uint32_t sw = *reinterpret_cast<const uint32_t*>(rec + scales_off(BITS) + 4 * gid);
   const uint2 zz = *reinterpret_cast<const uint2*>(rec + zeros_off(BITS));
-  const uint4* xb = reinterpret_cast<const uint4*>(x8g) + (gid * 4 + tig) * 2;
+  // digit rows 4b + d exist for b < B only (dd_off = 512·B): the columns of lanes beyond them are discarded,
+  // so those lanes read row 0 of the same group instead of the next group's bytes (no cross-warp read)
+  const int gid_r = min(gid, (dd_off >> 7) - 1);
+  const uint4* xb = reinterpret_cast<const uint4*>(x8g) + (gid_r * 4 + tig) * 2;
   const uint4 bv0 = xb[0], bv1 = xb[1];
   const uint32_t bb[8] = {bv0.x, bv0.y, bv0.z, bv0.w, bv1.x, bv1.y, bv1.z, bv1.w};
   const int2 ddf = reinterpret_cast<const int2*>(x8g + dd_off)[tig];

@@ -276,20 +276,20 @@ __global__ void __launch_bounds__(128) moe_gemv_warp_kernel(MoEWin w, MoERoute r
       for (int nb = 0; nb < NB8; ++nb)
         *reinterpret_cast<float4*>(&red[warp][lane][4 * nb]) = make_float4(tot[nb][0], tot[nb][1], tot[nb][2], tot[nb][3]);
       __syncthreads();
-      if (warp != 0) {
-        __syncthreads();                               // red is reused by the next item
-        continue;
+      if (warp == 0) {
+#pragma unroll
+        for (int nb = 0; nb < NB8; ++nb)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float v = red[0][lane][4 * nb + e];
+#pragma unroll
+            for (int q = 1; q < 4; ++q) v += red[q][lane][4 * nb + e];   // fixed order: deterministic
+            tot[nb][e] = v;
+          }
       }
-#pragma unroll
-      for (int nb = 0; nb < NB8; ++nb)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          float v = red[0][lane][4 * nb + e];
-#pragma unroll
-          for (int q = 1; q < 4; ++q) v += red[q][lane][4 * nb + e];   // fixed order: deterministic
-          tot[nb][e] = v;
-        }
     }
+    // K-split items: warp 0 finishes the item; every warp meets the same barrier below (red is reused)
+    if (!KS || warp == 0) {
     // U·t (plain: member 0 on all 16 rows; SiLU window: up chunks on rows 0-7 with t of member 0,
     // gate chunks on rows 8-15 with t of member 1), then the glue and the output
     float comp[2][NB8][4];
@@ -354,7 +354,8 @@ __global__ void __launch_bounds__(128) moe_gemv_warp_kernel(MoEWin w, MoERoute r
           o[(size_t)(row0 + col) * ldo + rb * kRows + gid + 8 * (e >> 1)] = tot[nb][e] + comp[0][nb][e];
         }
     }
-    if constexpr (KS) __syncthreads();                 // pairs with the other warps' wait above
+    }
+    if constexpr (KS) __syncthreads();                 // every warp, the same barrier: red is free again
   }
 }
 
