@@ -751,6 +751,8 @@ def main():
     ap.add_argument("--rank-override", type=int, default=None, help="dev: use this rank for every matrix")
     ap.add_argument("--moe-dynamic", action="store_true", help="c3: per-(token, expert) dynamic ranks (P:652-665)")
     ap.add_argument("--no-sweep", action="store_true", help="c2: skip the default B = 2/4/8/16 sweep")
+    ap.add_argument("--set-option", action="append", default=[], metavar="NAME=VALUE",
+                    help="dev A/B: hc_set_option before the run (e.g. t_forward=1)")
     ap.add_argument("--factors", default="bf16", choices=["bf16", "fp8"],
                     help="compensation factor storage (fp8: e4m3 + per-rank fp32 scales, SURVEY 8(f)4)")
     ap.add_argument("--tp-path", default="peer", choices=["peer", "nccl"],
@@ -846,6 +848,12 @@ def main():
         return
 
     import torch
+    import paper_2605_05819_b200 as hc
+    for kv in args.set_option:
+        k, v = kv.split("=")
+        hc.set_option(k, int(v))
+    if args.set_option:
+        config["options"] = {kv.split("=")[0]: int(kv.split("=")[1]) for kv in args.set_option}
     if world > 1:
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)

@@ -45,6 +45,9 @@ __device__ unsigned long long* g_dtrace = nullptr;   // dev tracing (HC_DEC_TRAC
 
 namespace hc {
 
+#ifndef HC_POLL_RELAXED
+#define HC_POLL_RELAXED 0
+#endif
 #ifndef HC_DEP_SLEEP
 #define HC_DEP_SLEEP 64   // ns between polls of the producer window's counter
 #endif
@@ -104,8 +107,14 @@ __device__ __forceinline__ void dep_wait(const DArgs& a, int lane) {
       return;
     }
     if (lane == 0) {
+#if HC_POLL_RELAXED
       while (ld_relaxed(a.dep_cnt) < a.dep_target) __nanosleep(HC_DEP_SLEEP);
       (void)ld_acquire(a.dep_cnt);   // (a fence.acq_rel here measured slower than the second load)
+#else
+      // acquire loads in the poll: the load that sees the target is the acquire (one L2 round trip less
+      // than relaxed polling + a separate acquire; ~1-2 µs under a full weight stream)
+      while (ld_acquire(a.dep_cnt) < a.dep_target) __nanosleep(HC_DEP_SLEEP);
+#endif
       asm volatile("fence.proxy.async.global;" ::: "memory");   // generic writes -> async-proxy (TMA) reads
     }
     __syncwarp();
@@ -260,8 +269,12 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
         // once per CTA, while the tile warps still stream: acquire t (all tile warps of the grid
         // have added their V·x shares) and keep its fragments in smem as fp32
         if (lane == 0 && n_vctas > 0) {                 // t_in: ordered by the dependency wait already
+#if HC_POLL_RELAXED
           while (ld_relaxed(&a.cnt[0]) < (unsigned)n_vctas) __nanosleep(32);
           (void)ld_acquire(&a.cnt[0]);
+#else
+          while (ld_acquire(&a.cnt[0]) < (unsigned)n_vctas) __nanosleep(32);
+#endif
         }
         __syncwarp();
         // t as bf16 hi + lo B-fragments of the U·t mma (fp32-accurate), ranks >= r masked to 0.  Tier 0 only
@@ -469,6 +482,24 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
           for (int nb = 0; nb < NB8; ++nb) {
             float tp[4] = {0.f, 0.f, 0.f, 0.f};
             mma16816(tp, af, b0[nb], b1[nb]);
+            if (NB8 == 1 && a.B <= 2) {
+              // B <= 2: the 16·B valid partials sit in the tig = 0 lanes; gather them one per lane so the
+              // fixed-point adds run as one warp-wide sequence instead of four predicated ones
+              const int rk = lane & 15, cl = lane >> 4;                  // lane -> (rank, batch column)
+              const int src = 4 * (rk & 7), e0 = 2 * (rk >> 3);
+              const float v0 = __shfl_sync(0xFFFFFFFFu, tp[0], src), v1 = __shfl_sync(0xFFFFFFFFu, tp[1], src);
+              const float v2 = __shfl_sync(0xFFFFFFFFu, tp[2], src), v3 = __shfl_sync(0xFFFFFFFFu, tp[3], src);
+              const float v = e0 == 0 ? (cl ? v1 : v0) : (cl ? v3 : v2);
+              if (cl < a.B) {
+                if (a.npeer > 1) {
+#pragma unroll 1
+                  for (int q = 0; q < a.npeer; ++q) tacc_add(a.fwdpeer[q], a.fwd_chunks, cc, cl, rk, v);
+                } else {
+                  tacc_add(a.fwd_tacc, a.fwd_chunks, cc, cl, rk, v);
+                }
+              }
+              continue;
+            }
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int col = 2 * tig + (e & 1) + 8 * nb, rank = gid + 8 * (e >> 1);
