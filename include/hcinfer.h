@@ -154,6 +154,12 @@ int64_t hc_window_rows(hc_ctx* ctx, int32_t layer, int32_t window_kind, int32_t 
 
 /* =====================================================================================
  * Execution (asynchronous on `stream`; caller keeps x / y alive until the stream is done)
+ *
+ * Concurrency: a context owns per-window workspaces (t accumulators, completion counters, x' hand-off and
+ * staging buffers, stack graphs) that every launch resets before it completes.  Launches that use the same
+ * window — directly or through hc_stack_forward / hc_moe_forward — must therefore be stream-ordered: calling
+ * them concurrently on different streams (or from different host threads) races on those workspaces.  Use
+ * one context per concurrent stream.  Different contexts are independent.
  * ===================================================================================== */
 
 /* y[b, :] = concat over the window's members of  deq(W_m)·x_b + U_m[:, :r_m]·(V_m[:r_m, :]·x_b)
