@@ -303,29 +303,33 @@ static Member make_member(const hc_matrix_desc& d) {
   return m;
 }
 
-// Prefill copies of a plain 4-bit member (rows [row_begin, row_end) of the staged canonical inputs).
-static hc_status build_prefill(Member& m, const Staged& sd, cudaStream_t st) {
-  if (m.bits != 4) return HC_OK;
+// Prefill copies of a plain 4-bit member, built on the device from its decode records and factor fragments the
+// first time a B > 16 launch needs them (a decode-only stack never pays their memory): nibble-paired codes,
+// scales / zeros transposed to [G][rows], fp16 U [rows][r_stored] and V [r_stored][K] (fp8 factors: fp16 of
+// e4m3 · scale).
+static hc_status ensure_prefill(Member& m, cudaStream_t st) {
+  if (m.bits != 4 || (m.pcodes && m.pcodes->p)) return HC_OK;
   const int rows = m.rows(), G = m.K / hc::kGroup, wpr = m.K / 8;
-  CUDA_TRY(m.pcodes->alloc((size_t)rows * wpr * 4));
-  CUDA_TRY(hc::launch_prefill_codes(sd.codes + (size_t)m.row_begin * wpr, (uint32_t*)m.pcodes->p, (size_t)rows * wpr, st));
-  CUDA_TRY(m.pscales->alloc((size_t)rows * G * 2));   // transposed [G][rows]
-  CUDA_TRY(m.pzeros->alloc((size_t)rows * G));
-  CUDA_TRY(hc::launch_transpose_groups(sd.scales + (size_t)m.row_begin * G, sd.zeros + (size_t)m.row_begin * G, rows, G,
-                                       (uint16_t*)m.pscales->p, (uint8_t*)m.pzeros->p, st));
+  DevBuf q, codes, sc, zr;
+  CUDA_TRY(q.alloc((size_t)rows * m.K));
+  CUDA_TRY(codes.alloc((size_t)rows * wpr * 4));
+  CUDA_TRY(sc.alloc((size_t)rows * G * 2));
+  CUDA_TRY(zr.alloc((size_t)rows * G));
   if (m.r_stored > 0) {
     CUDA_TRY(m.U16->alloc((size_t)rows * m.r_stored * 2));
     CUDA_TRY(m.V16->alloc((size_t)m.r_stored * m.K * 2));
-    if (m.fp8) {   // fp16(e4m3 · scale): one rounding of U_eff / V_eff
-      CUDA_TRY(hc::launch_fp8_to_f16((const uint8_t*)sd.U + (size_t)m.row_begin * m.r_stored, sd.us, (size_t)rows * m.r_stored,
-                                     m.r_stored, false, m.K, (uint16_t*)m.U16->p, st));
-      CUDA_TRY(hc::launch_fp8_to_f16((const uint8_t*)sd.V, sd.vs, (size_t)m.r_stored * m.K, m.r_stored, true, m.K,
-                                     (uint16_t*)m.V16->p, st));
-    } else {
-      CUDA_TRY(hc::launch_bf16_to_f16(sd.U + (size_t)m.row_begin * m.r_stored, (uint16_t*)m.U16->p, (size_t)rows * m.r_stored, st));
-      CUDA_TRY(hc::launch_bf16_to_f16(sd.V, (uint16_t*)m.V16->p, (size_t)m.r_stored * m.K, st));
-    }
   }
+  CUDA_TRY(hc::launch_unrepack_prefill((const uint8_t*)m.rec->p, rows / hc::kRows, m.K, m.bits, (uint8_t*)q.p,
+                                       (uint32_t*)codes.p, (uint16_t*)sc.p, (uint8_t*)zr.p, (const uint8_t*)m.U->p,
+                                       (const uint8_t*)m.V->p, m.r_stored, m.fp8 ? (const float*)m.us->p : nullptr,
+                                       m.fp8 ? (const float*)m.vs->p : nullptr, (uint16_t*)m.U16->p, (uint16_t*)m.V16->p, st));
+  CUDA_TRY(m.pcodes->alloc((size_t)rows * wpr * 4));
+  CUDA_TRY(hc::launch_prefill_codes((const uint32_t*)codes.p, (uint32_t*)m.pcodes->p, (size_t)rows * wpr, st));
+  CUDA_TRY(m.pscales->alloc((size_t)rows * G * 2));   // transposed [G][rows]
+  CUDA_TRY(m.pzeros->alloc((size_t)rows * G));
+  CUDA_TRY(hc::launch_transpose_groups((const uint16_t*)sc.p, (const uint8_t*)zr.p, rows, G, (uint16_t*)m.pscales->p,
+                                       (uint8_t*)m.pzeros->p, st));
+  CUDA_TRY(cudaStreamSynchronize(st));                // the temporaries die at scope end
   return HC_OK;
 }
 
@@ -472,8 +476,7 @@ static hc_status load_one(hc_ctx* ctx, const hc_matrix_desc* mats, int32_t n_mat
       CUDA_TRY(m.Vn->alloc((size_t)d.r_stored * d.K * 2));
       CUDA_TRY(hc::launch_repack_vn(sd.V, d.K, d.r_stored, (uint32_t*)m.Vn->p, st));
     }
-    s = build_prefill(m, sd, st);
-    if (s != HC_OK) return s;
+    // prefill copies are built lazily from the decode records on the first B > 16 call (ensure_prefill)
     CUDA_TRY(cudaStreamSynchronize(st));   // staged temporaries die at scope end
     auto it = std::find_if(w.members.begin(), w.members.end(), [&](const Member& o) { return o.slot == d.slot; });
     if (it != w.members.end()) *it = m; else w.members.push_back(m);
@@ -684,7 +687,7 @@ static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int
   if (a.n_chunks > kMaxChunks) return fail(HC_ERR_CONFIG, "window ranks need %d chunks > %d", a.n_chunks, kMaxChunks);
   if (w.ws_chunks < max_chunks) {
     const int mc = std::max(max_chunks, 1);
-    CUDA_TRY(w.tacc.alloc(((size_t)mc * hc::kTChunk + 4) * sizeof(long long)));   // [chunk][tier][16][16] + deep flag
+    CUDA_TRY(w.tacc.alloc(((size_t)hc::kTCopies * mc * hc::kTChunk + 4) * sizeof(long long)));   // [chunk][tier][16][16] + deep flag
     CUDA_TRY(cudaMemset(w.tacc.p, 0, w.tacc.bytes));
     CUDA_TRY(w.cnt.alloc(2 * sizeof(unsigned)));
     CUDA_TRY(cudaMemset(w.cnt.p, 0, w.cnt.bytes));
@@ -796,6 +799,10 @@ static hc_status launch_prefill_window(hc_ctx* ctx, Window& w, const void* x, in
   for (const Member& m : w.members) {
     if (m.bits != 4) return fail(HC_ERR_CONFIG, "prefill (B > 16) supports 4-bit windows only (got %d-bit)", m.bits);
     if (m.rows() % kPBN) return fail(HC_ERR_CONFIG, "prefill needs member rows %% 256 == 0 (got %d)", m.rows());
+  }
+  for (Member& m : w.members) {
+    hc_status s = ensure_prefill(m, st);
+    if (s != HC_OK) return s;
   }
   const size_t xel = (size_t)M * K;
   if (ctx->p_x16.bytes < xel * 2) CUDA_TRY(ctx->p_x16.alloc(xel * 2));
@@ -1151,7 +1158,7 @@ static hc_status peer_layout(hc_ctx* ctx, int G, hc_ctx::Peer& P) {
   P.off_m = off;   off += align256((size_t)16 * f * 2);
   P.off_h = off;   off += align256((size_t)16 * d * 2);
   P.off_win = off;
-  P.win_stride = align256(128 + ((size_t)mc * hc::kTChunk + 4) * sizeof(long long));
+  P.win_stride = align256(128 + ((size_t)hc::kTCopies * mc * hc::kTChunk + 4) * sizeof(long long));
   P.n_win = 4 * (int)plan.size();
   P.mc = mc;
   P.G = G;

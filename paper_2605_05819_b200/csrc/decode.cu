@@ -138,13 +138,14 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
   uint64_t* bars_all = reinterpret_cast<uint64_t*>(ubuf + 2 * kUPre * 32);
   uint64_t* ubar = bars_all + kDecodeWarps * kNBuf;       // [2]
   uint64_t* xbar = ubar + 2;
-  uint64_t* fbar = xbar + 1;                              // t forwarding: Vn blocks landed
+  uint64_t* fbar = xbar + 1;                              // t forwarding: Vn blocks landed, buffer 0
+  uint64_t* fbar1 = xbar + 3;                             //   ... buffer 1 (the Vn blocks are double-buffered)
   uint64_t* dbar = xbar + 2;                              // dataflow dependency met (epilogue -> tile warps)
   uint64_t* ebars_all = xbar + 4;                         // [8 warps][kNBuf] ring slot consumed (empty; +1 pad: tsm 16-B aligned)
   uint4* tsm = reinterpret_cast<uint4*>(ebars_all + kDecodeWarps * kNBuf);   // [n_chunks][NB8][32] t hi|lo fragments
   uint16_t* xt = reinterpret_cast<uint16_t*>(tsm + (size_t)a.n_chunks * NB8 * 32);   // [16 k][16 cols] fwd x tile
-  uint4* fbuf = reinterpret_cast<uint4*>(xt + 256);                                  // [fwd_chunks][32] Vn fragments
-  unsigned* misc = reinterpret_cast<unsigned*>(fbuf + (size_t)(a.fwd ? a.fwd_chunks : 0) * 32);   // [4]: [0] XS σ any, [1] x' slow path
+  uint4* fbuf = reinterpret_cast<uint4*>(xt + 256);                                  // [2][fwd_chunks][32] Vn fragments
+  unsigned* misc = reinterpret_cast<unsigned*>(fbuf + (size_t)(a.fwd ? a.fwd_chunks : 0) * 64);   // [4]: [0] XS σ any, [1] x' slow path
   float* fsg = reinterpret_cast<float*>(misc + 4);                                   // XS: 2^σ [G][B]
   uint16_t* xs = reinterpret_cast<uint16_t*>(fsg + ((XS && !I8) ? ((a.G * a.B + 3) & ~3) : 0));
   const int xs_ld = a.K + 32;   // +64 B per row: consecutive batch rows fall in disjoint banks
@@ -158,6 +159,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
       }
     } else if (warp == kDecodeWarps) {
       mbar_init(&ubar[0], 1); mbar_init(&ubar[1], 1); mbar_init(xbar, 1); mbar_init(fbar, 1); mbar_init(dbar, 1);
+      mbar_init(fbar1, 1);
       misc[0] = 0u; misc[1] = 0u;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -240,7 +242,25 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
                   &ubar[par], evict_first_policy());
       }
     };
+    // t forwarding: the next window's natural-k V fragments of an item's 16-k output block -> fbuf[buf]
+    // (double-buffered: the first item's before the dependency wait, then one item ahead; weights only)
+    auto prefetch_fwd = [&](int it, int buf) {
+      if (!a.fwd || it >= n_items || lane != 0) return;
+      const DMember& mm = a.m[member_of_rb(a, it)];
+      const int n0 = (a.npeer > 1 ? mm.full_off : mm.row_off) + (it - mm.rb_begin) * (a.glue ? 8 : kRows);
+      if (n0 < a.fwd_lo || n0 >= a.fwd_hi) return;
+      const int kb = (n0 - a.fwd_lo) >> 4;
+      uint64_t* fb = buf ? fbar1 : fbar;
+      mbar_expect_tx(fb, (uint32_t)a.fwd_chunks * 512u);
+      for (int i = 0; i < a.fwd_nm; ++i) {
+        const int nc = a.fwd_cb[i + 1] - a.fwd_cb[i];
+        if (nc > 0)
+          bulk_copy(fbuf + ((size_t)buf * a.fwd_chunks + a.fwd_cb[i]) * 32, a.fwd_vn[i] + (size_t)kb * a.fwd_rs[i] * 32,
+                    (uint32_t)nc * 512u, fb, evict_first_policy());
+      }
+    };
     prefetch_u(blockIdx.x, 0);                           // weights: before the PDL wait
+    prefetch_fwd(blockIdx.x, 0);
     dep_wait(a, lane);
     if (blockIdx.x == 0 && a.clr_max)                    // the max buffer the next window publishes into (R20)
       for (int i = lane; i < a.clr_n; i += 32) a.clr_max[i] = 0u;
@@ -281,7 +301,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
         // (R22); the extra-tier flag is loaded first and consumed after the loop, and the rare extra-tier
         // pass is out of line.  No branch may sit between the loads of this loop (a branch inside the
         // unrolled loop serialises them into one L2 round trip per chunk: +2.5 µs on C1).
-        t_deep = __ldcg(a.tacc + (size_t)a.n_chunks * kTChunk) != 0;
+        t_deep = __ldcg(a.tacc + (size_t)kTCopies * a.n_chunks * kTChunk) != 0;
 #pragma unroll 4
         for (int cc = 0; cc < a.n_chunks; ++cc) {
           const DMember& mt = a.m[member_of_chunk(a, cc)];
@@ -289,7 +309,14 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
 #pragma unroll
           for (int nb = 0; nb < NB8; ++nb) {
             const long long* src = a.tacc + (size_t)cc * kTChunk + ((gid + 8 * nb) & 15) * 16 + 2 * tig;
-            const long long tr[4] = {__ldcg(src), __ldcg(src + 1), __ldcg(src + 8), __ldcg(src + 9)};
+            // only the lanes of batch columns < B load (the others' words are zero): predicated, not branched
+            const bool on = gid + 8 * nb < a.B;
+            long long tr[4] = {ldcg_if(src, on), ldcg_if(src + 1, on), ldcg_if(src + 8, on), ldcg_if(src + 9, on)};
+#pragma unroll
+            for (int c = 1; c < kTCopies; ++c) {           // the copies (integer sums: exact, order-free)
+              const long long* sc = src + (size_t)c * a.n_chunks * kTChunk;
+              tr[0] += ldcg_if(sc, on); tr[1] += ldcg_if(sc + 1, on); tr[2] += ldcg_if(sc + 8, on); tr[3] += ldcg_if(sc + 9, on);
+            }
             uint32_t hi[2], lo[2];
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
@@ -319,16 +346,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
       const int oc0 = (a.npeer > 1 ? m.full_off : m.row_off) + (item - m.rb_begin) * (a.glue ? 8 : kRows);
       const int f_n0 = oc0;
       const bool f_on = a.fwd && f_n0 >= a.fwd_lo && f_n0 < a.fwd_hi;
-      if (f_on && lane == 0) {
-        const int kb = (f_n0 - a.fwd_lo) >> 4;
-        mbar_expect_tx(fbar, (uint32_t)a.fwd_chunks * 512u);
-        for (int i = 0; i < a.fwd_nm; ++i) {
-          const int nc = a.fwd_cb[i + 1] - a.fwd_cb[i];
-          if (nc > 0)
-            bulk_copy(fbuf + a.fwd_cb[i] * 32, a.fwd_vn[i] + (size_t)kb * a.fwd_rs[i] * 32, (uint32_t)nc * 512u, fbar,
-                      evict_first_policy());
-        }
-      }
+      prefetch_fwd(item + (int)gridDim.x, (k + 1) & 1);     // the next item's Vn block (this one's is in flight)
       // ---- independent of the tile warps (so done before waiting for their partial sums): U[:, :r]·t
       // (U prefetched one item ahead) and the residual (its producer window is >= 2 windows back,
       // complete once this window's dependency was met)
@@ -472,11 +490,13 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
           b0[nb] = (uint32_t)xt[(2 * tig) * 16 + col] | ((uint32_t)xt[(2 * tig + 1) * 16 + col] << 16);
           b1[nb] = (uint32_t)xt[(2 * tig + 8) * 16 + col] | ((uint32_t)xt[(2 * tig + 9) * 16 + col] << 16);
         }
-        while (!mbar_try_wait(fbar, f_phase)) {}
-        f_phase ^= 1u;
+        const int fb = k & 1;
+        while (!mbar_try_wait(fb ? fbar1 : fbar, (f_phase >> fb) & 1u)) {}
+        f_phase ^= 1u << fb;
+        const uint4* fbk = fbuf + (size_t)fb * a.fwd_chunks * 32;
 #pragma unroll 4
         for (int cc = 0; cc < a.fwd_chunks; ++cc) {
-          const uint4 v4 = fbuf[cc * 32 + lane];
+          const uint4 v4 = fbk[cc * 32 + lane];
           const uint32_t af[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
           for (int nb = 0; nb < NB8; ++nb) {
@@ -532,7 +552,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
     last = __shfl_sync(0xffffffffu, last, 0);
     if (last) {
       // the flag as read with t (a CTA that never read t loads it here)
-      const bool xt = t_ready ? t_deep : (__ldcg(a.tacc + (size_t)a.n_chunks * kTChunk) != 0);
+      const bool xt = t_ready ? t_deep : (__ldcg(a.tacc + (size_t)kTCopies * a.n_chunks * kTChunk) != 0);
       tacc_reset(a.tacc, a.n_chunks, a.B, xt, lane);
       if (lane == 0) {
         a.cnt[0] = 0u;
@@ -771,7 +791,7 @@ static size_t decode_smem_bytes(bool xs, bool i8, int B, int K, int n_chunks, in
   const int nb8 = B > 8 ? 2 : 1;
   size_t s = (size_t)kDecodeWarps * kNBuf * kTPB * kTileMax + 2 * kDecodeWarps * 32 * 4 * nb8 * sizeof(float) +
              2 * kUPre * 32 * 16 + (2 * kDecodeWarps * kNBuf + 6) * sizeof(uint64_t) +
-             (size_t)n_chunks * nb8 * 32 * 16 + 512 + (size_t)fwd_chunks * 512;
+             (size_t)n_chunks * nb8 * 32 * 16 + 512 + (size_t)fwd_chunks * 1024;
   s += 16;                                                                 // misc
   if (i8) s += (size_t)(K / kGroup) * x8_stride(B) + kX8Pad;
   else if (xs) s += (size_t)(((K / kGroup) * B + 3) & ~3) * 4 + (size_t)B * (K + 32) * 2;   // 2^σ [G][B] + x'

@@ -28,6 +28,12 @@ constexpr int kTileMax = 1088;           // >= rec_bytes(4) = 1072, >= 1 KB V pi
 constexpr int kUPre = HC_DEC_UPRE;       // U chunks (16 ranks each) staged in smem per item (r <= 128)
 constexpr int kTTiers = 4;               // t accumulator tiers (decode_dev.cuh tacc_add)
 constexpr int kTChunk = kTTiers * 256;   // t accumulator words per rank chunk: [tier][16 cols][16 ranks]
+#ifndef HC_TCOPIES
+#define HC_TCOPIES 1   // measured: 4 copies C1 891 vs 1189 GB/s, 8 copies 585 (the epilogue's extra loads cost more than the queue)
+#endif
+// t accumulator copies: a CTA adds into copy blockIdx % kTCopies and readers sum the copies, which divides the
+// same-address atomic queue at L2 (every item of a window adds into the same t elements)
+constexpr int kTCopies = HC_TCOPIES;
 constexpr int kFwdMax = 24;              // next-window rank chunks a launch can forward t to (smem: 512 B each)
 
 struct DMember {

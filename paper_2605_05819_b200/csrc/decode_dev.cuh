@@ -266,6 +266,13 @@ constexpr float kTInv = 1.f / 268435456.f;
 // ~1e-6) never leave it; whole windows of tiny or huge activations set the flag.  Integer adds are
 // order-free: t is deterministic.  One atomic per partial; the common case reads and resets one word per
 // element.
+// Predicated L2 load (no branch: the predicate goes on the load, so a batch of these stays one round trip).
+__device__ __forceinline__ long long ldcg_if(const long long* p, bool on) {
+  long long v;
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n mov.b64 %0, 0;\n @q ld.global.cg.b64 %0, [%1];\n}"
+               : "=l"(v) : "l"(p), "r"((int)on) : "memory");
+  return v;
+}
 __device__ __forceinline__ size_t tacc_idx(int cc, int w, int rank, int col) {
   return (size_t)cc * kTChunk + (w * 16 + col) * 16 + rank;
 }
@@ -276,21 +283,27 @@ __device__ __forceinline__ void tacc_add(long long* t, int n_chunks, int cc, int
   const float q = fminf(fmaxf(v * __uint_as_float((uint32_t)(127 + se) << 23), -0x1p62f), 0x1p62f);   // exact scaling
   const long long iq = __float2ll_rn(q);
   if (iq != 0) {
-    atomicAdd(reinterpret_cast<unsigned long long*>(t + tacc_idx(cc, w, rank, col)), (unsigned long long)iq);
-    if (w != 0) t[(size_t)n_chunks * kTChunk] = 1;     // extra tiers in use (idempotent plain store)
+    const size_t cp = (size_t)(blockIdx.x % kTCopies) * n_chunks * kTChunk;   // this CTA's copy
+    atomicAdd(reinterpret_cast<unsigned long long*>(t + cp + tacc_idx(cc, w, rank, col)), (unsigned long long)iq);
+    if (w != 0) t[(size_t)kTCopies * n_chunks * kTChunk] = 1;   // extra tiers in use (idempotent plain store)
   }
 }
 // t of (chunk cc, batch col) at ranks r0, r0 + 1: tier 0 (8-byte loads); XT: + tiers 1-3.  fp32 (no
 // fp64: its conversions are slow on the epilogue's critical path)
 template <bool XT>
-__device__ __forceinline__ void tacc_read2(const long long* t, int cc, int col, int r0, float& ta, float& tb) {
-  const long long* p = t + tacc_idx(cc, 0, r0, col);
-  ta = (float)__ldcg(p) * 0x1p-36f;
-  tb = (float)__ldcg(p + 1) * 0x1p-36f;
-  if (XT) {
-    const long long *p1 = t + tacc_idx(cc, 1, r0, col), *p2 = t + tacc_idx(cc, 2, r0, col), *p3 = t + tacc_idx(cc, 3, r0, col);
-    ta = fmaf((float)__ldcg(p1), 0x1p-12f, ta + fmaf((float)__ldcg(p2), 0x1p-72f, (float)__ldcg(p3) * 0x1p-96f));
-    tb = fmaf((float)__ldcg(p1 + 1), 0x1p-12f, tb + fmaf((float)__ldcg(p2 + 1), 0x1p-72f, (float)__ldcg(p3 + 1) * 0x1p-96f));
+__device__ __forceinline__ void tacc_read2(const long long* t, int n_chunks, int cc, int col, int r0, float& ta, float& tb) {
+  ta = 0.f;
+  tb = 0.f;
+  for (int c = 0; c < kTCopies; ++c) {
+    const long long* tc = t + (size_t)c * n_chunks * kTChunk;
+    const long long* p = tc + tacc_idx(cc, 0, r0, col);
+    ta += (float)__ldcg(p) * 0x1p-36f;
+    tb += (float)__ldcg(p + 1) * 0x1p-36f;
+    if (XT) {
+      const long long *p1 = tc + tacc_idx(cc, 1, r0, col), *p2 = tc + tacc_idx(cc, 2, r0, col), *p3 = tc + tacc_idx(cc, 3, r0, col);
+      ta += fmaf((float)__ldcg(p1), 0x1p-12f, fmaf((float)__ldcg(p2), 0x1p-72f, (float)__ldcg(p3) * 0x1p-96f));
+      tb += fmaf((float)__ldcg(p1 + 1), 0x1p-12f, fmaf((float)__ldcg(p2 + 1), 0x1p-72f, (float)__ldcg(p3 + 1) * 0x1p-96f));
+    }
   }
 }
 // Out-of-line t fragment pass (DArgs::fp8 windows, and windows whose extra-tier flag is set, R22): rebuilds
@@ -305,11 +318,11 @@ __device__ __noinline__ void t_fragments_full(const DArgs& a, uint4* tsm, int la
     for (int nb = 0; nb < NB8; ++nb) {
       float tr[4];
       if (xt) {
-        tacc_read2<true>(a.tacc, cc, (gid + 8 * nb) & 15, 2 * tig, tr[0], tr[1]);
-        tacc_read2<true>(a.tacc, cc, (gid + 8 * nb) & 15, 2 * tig + 8, tr[2], tr[3]);
+        tacc_read2<true>(a.tacc, a.n_chunks, cc, (gid + 8 * nb) & 15, 2 * tig, tr[0], tr[1]);
+        tacc_read2<true>(a.tacc, a.n_chunks, cc, (gid + 8 * nb) & 15, 2 * tig + 8, tr[2], tr[3]);
       } else {
-        tacc_read2<false>(a.tacc, cc, (gid + 8 * nb) & 15, 2 * tig, tr[0], tr[1]);
-        tacc_read2<false>(a.tacc, cc, (gid + 8 * nb) & 15, 2 * tig + 8, tr[2], tr[3]);
+        tacc_read2<false>(a.tacc, a.n_chunks, cc, (gid + 8 * nb) & 15, 2 * tig, tr[0], tr[1]);
+        tacc_read2<false>(a.tacc, a.n_chunks, cc, (gid + 8 * nb) & 15, 2 * tig + 8, tr[2], tr[3]);
       }
       uint32_t hi[2], lo[2];
       for (int hh = 0; hh < 2; ++hh) {
@@ -331,13 +344,13 @@ __device__ __noinline__ void t_fragments_full(const DArgs& a, uint4* tsm, int la
 // Reset what a launch with batch B wrote: tier 0 always, tiers 1-3 and the flag when `xt` (the flag as the
 // caller read it; plain stores only on this exit path, no load); one warp.
 __device__ __forceinline__ void tacc_reset(long long* t, int n_chunks, int B, bool xt, int lane) {
-  const int per = B * 16, tiers = xt ? kTTiers : 1;      // words of one (chunk, tier): cols < B x 16 ranks
-  for (int i = lane; i < n_chunks * tiers * per; i += 32) {
-    const int row = i / per;                             // chunk * tiers + tier
+  const int per = B * 16, tiers = xt ? kTTiers : 1;      // words of one (copy, chunk, tier): cols < B x 16 ranks
+  for (int i = lane; i < kTCopies * n_chunks * tiers * per; i += 32) {
+    const int row = i / per;                             // (copy · n_chunks + chunk) · tiers + tier
     const int c = row / tiers, w = row - c * tiers;
     t[(size_t)c * kTChunk + w * 256 + (i - row * per)] = 0;
   }
-  if (lane == 0 && xt) t[(size_t)n_chunks * kTChunk] = 0;
+  if (lane == 0 && xt) t[(size_t)kTCopies * n_chunks * kTChunk] = 0;
 }
 
 // Row of x used by mma column `col` (batch index).  Columns >= B read a valid row; their

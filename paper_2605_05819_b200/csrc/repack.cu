@@ -189,6 +189,98 @@ cudaError_t launch_fp8_to_f16(const uint8_t* in, const float* scale, size_t n, i
   return cudaGetLastError();
 }
 
+// ---- inverse repack on the device (lazy prefill copies, built on the first B > 16 call from the decode
+// records and factor fragments instead of being kept from load time)
+// records [n_rb][G][rec] -> q bytes [rows][K], scales bf16 [rows][G], zeros [rows][G]; one thread per (rb, g, lane)
+__global__ void unrepack_records_kernel(const uint8_t* __restrict__ rec, int n_rb, int K, int bits, uint8_t* __restrict__ q,
+                                        uint16_t* __restrict__ scales, uint8_t* __restrict__ zeros) {
+  const int G = K / kGroup;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= (long long)n_rb * G * 32) return;
+  const int lane = (int)(tid & 31);
+  const long long rg = tid >> 5;
+  const int g = (int)(rg % G), rb = (int)(rg / G);
+  const uint8_t* r = rec + (size_t)rg * rec_bytes(bits);
+  uint32_t words[8];
+  for (int w = 0; w < 2 * bits; ++w) words[w] = *reinterpret_cast<const uint32_t*>(r + word_offset(bits, w, lane));
+  unpack_lane_words(words, lane, bits, g, rb, q, K);
+  if (lane < 8) {
+    const uint32_t sw = *reinterpret_cast<const uint32_t*>(r + scales_off(bits) + 4 * lane);
+    scales[((size_t)rb * kRows + lane) * G + g] = (uint16_t)(sw & 0xFFFFu);
+    scales[((size_t)rb * kRows + lane + 8) * G + g] = (uint16_t)(sw >> 16);
+  }
+  if (lane == 8) {
+    const uint64_t zw = *reinterpret_cast<const uint64_t*>(r + zeros_off(bits));
+    for (int rr = 0; rr < kRows; ++rr) zeros[((size_t)rb * kRows + rr) * G + g] = (uint8_t)((zw >> (4 * rr)) & 0xF);
+  }
+}
+// q bytes [n][K] -> canonical 4-bit code words [n][K/8] (element k at bits 4k)
+__global__ void pack4_kernel(const uint8_t* __restrict__ q, size_t n_words, uint32_t* __restrict__ out) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_words) return;
+  const uint2 v = *reinterpret_cast<const uint2*>(q + 8 * i);
+  uint32_t w = 0;
+  for (int j = 0; j < 4; ++j) w |= ((v.x >> (8 * j)) & 0xFu) << (4 * j);
+  for (int j = 0; j < 4; ++j) w |= ((v.y >> (8 * j)) & 0xFu) << (16 + 4 * j);
+  out[i] = w;
+}
+__device__ __forceinline__ float frag_val(const uint8_t* base, size_t reg, int h, const float* scale, int rank) {
+  if (scale) {                                           // fp8: e4m3 byte 2i + h, times the rank's scale
+    const uint8_t b = base[reg * 2 + h];
+    return e4m3_to_f32(b) * scale[rank];
+  }
+  const uint32_t v = reinterpret_cast<const uint32_t*>(base)[reg];
+  return __uint_as_float((h ? (v >> 16) : (v & 0xFFFFu)) << 16);
+}
+// U fragments [rb][c][lane][4 regs] -> fp16 U [rows][r_stored]; fp8: the e4m3 bytes x u_scale
+__global__ void unrepack_u_f16_kernel(const uint8_t* __restrict__ U, int n_rb, int r_stored, const float* __restrict__ us,
+                                      uint16_t* __restrict__ out) {
+  const int nc = r_stored / 16;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= (long long)n_rb * nc * 32) return;
+  const int lane = (int)(tid & 31);
+  const int c = (int)((tid >> 5) % nc), rb = (int)((tid >> 5) / nc);
+  for (int i = 0; i < 4; ++i)
+    for (int h = 0; h < 2; ++h) {
+      const int row = rb * kRows + frag_row(lane, i), rank = 16 * c + u_rank(lane, i, h);
+      out[(size_t)row * r_stored + rank] = __half_as_ushort(__float2half_rn(frag_val(U, (size_t)tid * 4 + i, h, us, rank)));
+    }
+}
+// V fragments [c][g][j][lane][4 regs] -> fp16 V [r_stored][K]; fp8: x v_scale
+__global__ void unrepack_v_f16_kernel(const uint8_t* __restrict__ V, int K, int r_stored, const float* __restrict__ vs,
+                                      uint16_t* __restrict__ out) {
+  const int G = K / kGroup, nc = r_stored / 16;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= (long long)nc * G * 8 * 32) return;
+  const int lane = (int)(tid & 31);
+  const int j = (int)((tid >> 5) & 7);
+  const long long cg = tid >> 8;
+  const int g = (int)(cg % G), c = (int)(cg / G);
+  for (int i = 0; i < 4; ++i)
+    for (int h = 0; h < 2; ++h) {
+      const int rank = 16 * c + frag_row(lane, i);
+      const int k = g * kGroup + frag_k(lane, j, i, h);
+      out[(size_t)rank * K + k] = __half_as_ushort(__float2half_rn(frag_val(V, (size_t)tid * 4 + i, h, vs, rank)));
+    }
+}
+
+cudaError_t launch_unrepack_prefill(const uint8_t* rec, int n_rb, int K, int bits, uint8_t* q_tmp, uint32_t* codes_out,
+                                    uint16_t* scales_out, uint8_t* zeros_out, const uint8_t* Ufrag, const uint8_t* Vfrag,
+                                    int r_stored, const float* us, const float* vs, uint16_t* U16, uint16_t* V16,
+                                    cudaStream_t st) {
+  const long long n = (long long)n_rb * (K / kGroup) * 32;
+  unrepack_records_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(rec, n_rb, K, bits, q_tmp, scales_out, zeros_out);
+  const size_t nw = (size_t)n_rb * kRows * K / 8;
+  pack4_kernel<<<(unsigned)((nw + 255) / 256), 256, 0, st>>>(q_tmp, nw, codes_out);
+  if (r_stored > 0) {
+    const long long nu = (long long)n_rb * (r_stored / 16) * 32;
+    unrepack_u_f16_kernel<<<(unsigned)((nu + 255) / 256), 256, 0, st>>>(Ufrag, n_rb, r_stored, us, U16);
+    const long long nv = (long long)(r_stored / 16) * (K / kGroup) * 8 * 32;
+    unrepack_v_f16_kernel<<<(unsigned)((nv + 255) / 256), 256, 0, st>>>(Vfrag, K, r_stored, vs, V16);
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_repack_v(const uint16_t* V, int K, int r_stored, uint32_t* v_out, cudaStream_t st) {
   if (r_stored <= 0) return cudaSuccess;
   const long long n = (long long)(r_stored / 16) * (K / kGroup) * 8 * 32;

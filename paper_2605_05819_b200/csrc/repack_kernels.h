@@ -27,4 +27,11 @@ cudaError_t launch_repack_fp8(const uint8_t* U0, const uint8_t* U1, int rstride,
 // fp16(e4m3 · per-rank scale) copies for the prefill path; rank_major: [r_stored][K] (V), else [rows][r_stored] (U).
 cudaError_t launch_fp8_to_f16(const uint8_t* in, const float* scale, size_t n, int r_stored, bool rank_major, int K,
                               uint16_t* out, cudaStream_t st);
+// Lazy prefill copies (4-bit plain members): decode records -> canonical 4-bit codes [rows][K/8] (via q bytes
+// [rows][K] in q_tmp), scales / zeros [rows][G]; U / V fragments (bf16, or fp8 with scales us / vs) -> fp16
+// U [rows][r_stored] and V [r_stored][K].
+cudaError_t launch_unrepack_prefill(const uint8_t* rec, int n_rb, int K, int bits, uint8_t* q_tmp, uint32_t* codes_out,
+                                    uint16_t* scales_out, uint8_t* zeros_out, const uint8_t* Ufrag, const uint8_t* Vfrag,
+                                    int r_stored, const float* us, const float* vs, uint16_t* U16, uint16_t* V16,
+                                    cudaStream_t st);
 }  // namespace hc

@@ -15,6 +15,8 @@ import paper_2605_05819_b200 as hc  # noqa: E402
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 c = bench.C2
 ranks = bench.c2_ranks(c)
+for kv in os.environ.get("HC_TRACE_OPTS", "").split():   # e.g. t_forward=1
+    hc.set_option(kv.split("=")[0], int(kv.split("=")[1]))
 ctx = hc.Context(0)
 bench.build_c2(ctx, ranks, c)
 n_win, grid = 4 * c["layers"], 512
