@@ -8,6 +8,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -46,22 +47,25 @@ def build(verbose: bool = False, force: bool = False, defines=(), lib_out: str =
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(INC, "hcinfer.h"))
     objs = []
-    log = []
+    jobs = []
     for src in CU_SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(build_dir, src + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            log.append(_run([NVCC, "-c", s, "-o", o, "-std=c++17", "-O3", "-lineinfo", *ARCH,
-                             "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
-                             "-I", INC, "-I", CSRC, *dflags]))
+            jobs.append([NVCC, "-c", s, "-o", o, "-std=c++17", "-O3", "-lineinfo", *ARCH,
+                         "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
+                         "-I", INC, "-I", CSRC, *dflags])
     for src in CPP_SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(build_dir, src + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            log.append(_run(["g++", "-c", s, "-o", o, "-std=c++17", "-O2", "-fPIC", "-ffp-contract=off",
-                             "-fno-fast-math", "-I", INC, "-I", CSRC]))
+            jobs.append(["g++", "-c", s, "-o", o, "-std=c++17", "-O2", "-fPIC", "-ffp-contract=off",
+                         "-fno-fast-math", "-I", INC, "-I", CSRC])
+    # independent translation units: compile them concurrently
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        log = list(ex.map(_run, jobs))
     if force or _stale(lib_path, objs):
         log.append(_run([NVCC, "-shared", "-o", lib_path, *objs, *ARCH, "-lcudart", "-ldl"]))
     out = "\n".join(x for x in log if x)

@@ -499,7 +499,7 @@ extern "C" hc_status hc_set_option(const char* name, int32_t value) {
   const std::pair<const char*, int*> tab[] = {{"t_forward", &o.t_forward},       {"x_handoff", &o.x_handoff},
                                               {"dep_wait", &o.dep_wait},         {"int8_path", &o.int8_path},
                                               {"prefill_merge", &o.prefill_merge}, {"decode_ctas_per_sm", &o.decode_ctas_per_sm},
-                                              {"pdl", &o.pdl}};
+                                              {"pdl", &o.pdl}, {"l2_prefetch", &o.l2_prefetch}, {"l2_prefetch_at_start", &o.l2_prefetch_at_start}};
   for (const auto& kv : tab)
     if (std::strcmp(kv.first, name) == 0) {
       if (value < 0) return fail(HC_ERR_CONFIG, "hc_set_option: %s = %d < 0", name, value);
@@ -516,7 +516,7 @@ extern "C" hc_status hc_get_option(const char* name, int32_t* value) {
   const std::pair<const char*, int> tab[] = {{"t_forward", o.t_forward},       {"x_handoff", o.x_handoff},
                                              {"dep_wait", o.dep_wait},         {"int8_path", o.int8_path},
                                              {"prefill_merge", o.prefill_merge}, {"decode_ctas_per_sm", o.decode_ctas_per_sm},
-                                             {"pdl", o.pdl}};
+                                             {"pdl", o.pdl}, {"l2_prefetch", o.l2_prefetch}, {"l2_prefetch_at_start", o.l2_prefetch_at_start}};
   for (const auto& kv : tab)
     if (std::strcmp(kv.first, name) == 0) { *value = kv.second; return HC_OK; }
   return fail(HC_ERR_CONFIG, "hc_get_option: unknown option '%s'", name);
@@ -734,14 +734,38 @@ static hc_status window_args(hc_ctx* ctx, Window& w, const void* x, int ldx, int
   return HC_OK;
 }
 
+// L2 prefetch of the next window's records by this launch (DArgs::pf_*; options().l2_prefetch items per CTA).
+static void set_prefetch(DArgs& a, const Window* next) {
+  const int per_cta = options().l2_prefetch;
+  if (!next || per_cta <= 0 || next->members.empty()) return;
+  const Member& n0 = next->members.front();
+  a.pf_items = per_cta;
+  a.pf_at_start = options().l2_prefetch_at_start ? 1 : 0;
+  a.pf_item_bytes = (unsigned)((n0.K / kGroup) * rec_bytes(n0.bits));
+  if (next->glue == HC_GLUE_SILU_MUL) {   // one record array: 8 up + 8 gate rows per row block
+    a.pf_nm = 1;
+    a.pf_rec[0] = (const uint8_t*)n0.rec->p;
+    a.pf_rb_end[0] = n0.rows() / 8;
+    return;
+  }
+  int cum = 0;
+  a.pf_nm = (int)next->members.size();
+  for (int i = 0; i < a.pf_nm; ++i) {
+    a.pf_rec[i] = (const uint8_t*)next->members[i].rec->p;
+    cum += next->members[i].rows() / kRows;
+    a.pf_rb_end[i] = cum;
+  }
+}
+
 static hc_status launch_window(hc_ctx* ctx, Window& w, const void* x, int ldx, int B, void* y, int y_bf16,
                                const void* resid, int ld_resid, cudaStream_t st, bool t_in = false,
                                const FwdSpec* fw = nullptr, Window* dep = nullptr, bool keep_done = false,
-                               const X16Spec* xs16 = nullptr) {
+                               const X16Spec* xs16 = nullptr, const Window* pf = nullptr) {
   DArgs a;
   int grid = 0;
   hc_status s = window_args(ctx, w, x, ldx, B, y, y_bf16, resid, ld_resid, a, grid, t_in, fw, dep, keep_done, xs16);
   if (s != HC_OK) return s;
+  set_prefetch(a, pf);
   a.trace_slot = ctx->trace_slot++;
   if (a.x16 && !a.x16_given)
     CUDA_TRY(launch_xprep(a.x, a.ldx, B, a.K, w.members.front().bits, (uint16_t*)a.x16, a.xsig, st));
@@ -1195,6 +1219,7 @@ static hc_status peer_window(hc_ctx* ctx, Window& w, int wi, const void* x, int 
   hc_status s = hc::window_args(ctx, w, x, ldx, B, peer_act(P, rank, act_off), 1, resid, ld_resid, a, grid, t_in,
                             fwd ? &fs : nullptr);
   if (s != HC_OK) return s;
+  hc::set_prefetch(a, next);
   if (a.n_chunks > P.mc || (fwd && a.fwd_chunks > P.mc))
     return fail(HC_ERR_STATE, "peer mode: ranks exceed the peer region's t accumulators (call hc_peer_region again)");
   a.npeer = G;
@@ -1406,14 +1431,15 @@ extern "C" hc_status hc_stack_forward(hc_ctx* ctx, const void* x, int32_t B, voi
         const bool dq = sx_q || (hx && l > 0), do_ = sx_q || hx, dug = sx_q || hx, ddn = sx_f || hx;
         const bool kq = sx_q || hx, ko = sx_q || hx, kug = sx_f || hx;     // keep(producer) = dep(consumer)
         const bool kdn = l + 1 < plan.size() && (sx_q || hx);
+        const Window* nqw = l + 1 < plan.size() ? plan[l + 1].qkv : nullptr;
         cap = hc::launch_window(ctx, *p.qkv, hin, d, B, qkv, 1, nullptr, 0, cs, t_q, &s_o,
-                                (prev_dn && dq) ? prev_dn : nullptr, kq, &x_q);                        // q | k | v
+                                (prev_dn && dq) ? prev_dn : nullptr, kq, &x_q, p.o);                   // q | k | v
         if (cap == HC_OK) cap = hc::launch_window(ctx, *p.o, qkv, nqkv, B, h1, 1, hin, d, cs, f_o, &s_ug,
-                                                  do_ ? p.qkv : nullptr, ko, &x_o);                     // h1 = h + O(q)
+                                                  do_ ? p.qkv : nullptr, ko, &x_o, p.ug);              // h1 = h + O(q)
         if (cap == HC_OK) cap = hc::launch_window(ctx, *p.ug, h1, d, B, mm, 1, nullptr, 0, cs, f_ug, &s_dn,
-                                                  dug ? p.o : nullptr, kug, &x_ug);                    // m = silu(g)·u
+                                                  dug ? p.o : nullptr, kug, &x_ug, p.down);            // m = silu(g)·u
         if (cap == HC_OK) cap = hc::launch_window(ctx, *p.down, mm, f, B, hout, 1, h1, d, cs, f_dn, &s_q,
-                                                  ddn ? p.ug : nullptr, kdn, &x_dn);                   // h' = h1 + DOWN(m)
+                                                  ddn ? p.ug : nullptr, kdn, &x_dn, nqw);              // h' = h1 + DOWN(m)
       } else {                                                   // column-sharded: gather every window
         cap = tp_window(ctx, *p.qkv, hin, d, B, qkv, nullptr, 0, cs);
         if (cap == HC_OK) cap = tp_window(ctx, *p.o, qkv, nqkv, B, h1, hin, d, cs);

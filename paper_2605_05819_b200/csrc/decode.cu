@@ -83,12 +83,12 @@ cudaError_t launch_peer_wait_copy(const unsigned* cnt, unsigned target, unsigned
 cudaError_t decode_set_trace(void* buf) { return cudaMemcpyToSymbol(g_dtrace, &buf, sizeof(buf)); }
 
 
-// Warp roles: warps 0..7 stream and contract tiles; warp 8 is the epilogue warp (reduction of the
-// 8 partial sums, U·t, output).  Named barriers hand the shared reduction buffer red[p] (p = item
-// parity) between them:
-//   FULL[p]  (id 1+p): 256 tile threads arrive, the epilogue warp syncs
-//   EMPTY[p] (id 3+p): the epilogue warp arrives after reading red[p], the tile warps sync before
-//                      writing red[p] again two items later.
+// Warp roles: warps 0..7 stream and contract tiles; warps 8 (.. 8 + epi - 1) are the epilogue warps (reduction of
+// the 8 partial sums, U·t, output; item k of a CTA -> epilogue warp k % epi, dec_epi_warps); the last warp issues
+// the TMA ring.  Named barriers hand the shared reduction buffer red[s] (s = k % kRedSlots) between them:
+//   FULL[s]  (red_full_id): 256 tile threads arrive, the item's epilogue warp syncs
+//   EMPTY[s] (red_empty_id): that epilogue warp arrives after reading red[s], the tile warps sync before
+//                            writing red[s] again kRedSlots items later.
 // Rank projection t = V·x: every tile warp of the grid first contracts an equal share of the
 // window's 1 KB V pieces (requested before its weight tiles) and adds its partial into the
 // window's t accumulators with 64-bit fixed-point atomics (exact integer adds: t is bit-identical
@@ -123,18 +123,35 @@ __device__ __forceinline__ void dep_wait(const DArgs& a, int lane) {
   }
 }
 
+// L2 prefetch of this CTA's share of the next window's records (DArgs::pf_items); lane j of nl lanes takes
+// the CTA's next-window items j, j + nl, ...
+__device__ __forceinline__ void prefetch_next_window(const DArgs& a, int j, int nl) {
+  if (a.pf_items <= 0) return;
+  const int total = a.pf_rb_end[a.pf_nm - 1];
+  for (; j < a.pf_items; j += nl) {
+    const int it = blockIdx.x + j * gridDim.x;
+    if (it >= total) return;
+    int i = 0, b0 = 0;
+#pragma unroll
+    for (int q = 0; q < kMaxMembers - 1; ++q)
+      if (q + 1 < a.pf_nm && it >= a.pf_rb_end[q]) { i = q + 1; b0 = a.pf_rb_end[q]; }
+    prefetch_l2(a.pf_rec[i] + (size_t)(it - b0) * a.pf_item_bytes, a.pf_item_bytes);
+  }
+}
+
 // I8: int8 tensor-core path (decode_i8.cuh; BITS = 4, NB8 = 1, B <= 2): x staged as x8 digits
 template <int BITS, int NB8, bool XS, bool I8, bool F8>
-__global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const __grid_constant__ DArgs a) {
+__global__ void __launch_bounds__(dec_block(I8), HC_DEC_MINB) decode_kernel(const __grid_constant__ DArgs a) {
+  constexpr int kEpiWarps = dec_epi_warps(I8);
+  constexpr int kProdWarp = kDecodeWarps + kEpiWarps;       // the producer (TMA issue) warp
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
   constexpr int kBlk = kTPB * kTileMax;
   // records per bulk-copy block: as many as the block holds (2-bit records are half the size)
   constexpr int kRPB = (kBlk / rec_bytes(BITS)) < 1 ? 1 : (kBlk / rec_bytes(BITS));
-  constexpr int kEpi = kDecodeWarps;          // epilogue warp index
-  float* red = reinterpret_cast<float*>(smem + (size_t)kDecodeWarps * kNBuf * kBlk);        // [2][8][32][4·NB8]
-  uint4* ubuf = reinterpret_cast<uint4*>(red + 2 * kDecodeWarps * 32 * 4 * NB8);             // [2][kUPre][32]
+  float* red = reinterpret_cast<float*>(smem + (size_t)kDecodeWarps * kNBuf * kBlk);        // [kRedSlots][8][32][4·NB8]
+  uint4* ubuf = reinterpret_cast<uint4*>(red + kRedSlots * kDecodeWarps * 32 * 4 * NB8);     // [2][kUPre][32]
   uint64_t* bars_all = reinterpret_cast<uint64_t*>(ubuf + 2 * kUPre * 32);
   uint64_t* ubar = bars_all + kDecodeWarps * kNBuf;       // [2]
   uint64_t* xbar = ubar + 2;
@@ -142,10 +159,13 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
   uint64_t* fbar1 = xbar + 3;                             //   ... buffer 1 (the Vn blocks are double-buffered)
   uint64_t* dbar = xbar + 2;                              // dataflow dependency met (epilogue -> tile warps)
   uint64_t* ebars_all = xbar + 4;                         // [8 warps][kNBuf] ring slot consumed (empty; +1 pad: tsm 16-B aligned)
-  uint4* tsm = reinterpret_cast<uint4*>(ebars_all + kDecodeWarps * kNBuf);   // [n_chunks][NB8][32] t hi|lo fragments
-  uint16_t* xt = reinterpret_cast<uint16_t*>(tsm + (size_t)a.n_chunks * NB8 * 32);   // [16 k][16 cols] fwd x tile
-  uint4* fbuf = reinterpret_cast<uint4*>(xt + 256);                                  // [2][fwd_chunks][32] Vn fragments
-  unsigned* misc = reinterpret_cast<unsigned*>(fbuf + (size_t)(a.fwd ? a.fwd_chunks : 0) * 64);   // [4]: [0] XS σ any, [1] x' slow path
+  uint64_t* e2bar = ebars_all + kDecodeWarps * kNBuf;    // [2]: [0] epilogue warp 0 passed the dependency wait (+1 pad)
+  // t fragments: one copy per epilogue warp, each loads t itself (measured: sharing one copy, the first warp to
+  // need t loading it for both, C2 635 -> 578 tokens/s, C1 1127 -> 846 GB/s)
+  uint4* tsm_all = reinterpret_cast<uint4*>(e2bar + 2);  // [epi warp][n_chunks][NB8][32] t hi|lo fragments
+  uint16_t* xt_all = reinterpret_cast<uint16_t*>(tsm_all + (size_t)kEpiWarps * a.n_chunks * NB8 * 32);   // [epi warp][16 k][16 cols]
+  uint4* fbuf = reinterpret_cast<uint4*>(xt_all + 256 * kEpiWarps);                  // [2][fwd_chunks][32] Vn fragments
+  unsigned* misc = reinterpret_cast<unsigned*>(fbuf + (size_t)(a.fwd ? a.fwd_chunks : 0) * 64);   // [4]: [0] XS σ any, [1] x' slow path, [2] epilogue warp 1 row blocks
   float* fsg = reinterpret_cast<float*>(misc + 4);                                   // XS: 2^σ [G][B]
   uint16_t* xs = reinterpret_cast<uint16_t*>(fsg + ((XS && !I8) ? ((a.G * a.B + 3) & ~3) : 0));
   const int xs_ld = a.K + 32;   // +64 B per row: consecutive batch rows fall in disjoint banks
@@ -157,10 +177,11 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
         mbar_init(&bars_all[warp * kNBuf + s], 1);
         mbar_init(&ebars_all[warp * kNBuf + s], 32);
       }
-    } else if (warp == kDecodeWarps) {
+    } else if (warp == kDecodeWarps) {   // epilogue warp 0
       mbar_init(&ubar[0], 1); mbar_init(&ubar[1], 1); mbar_init(xbar, 1); mbar_init(fbar, 1); mbar_init(dbar, 1);
       mbar_init(fbar1, 1);
-      misc[0] = 0u; misc[1] = 0u;
+      mbar_init(e2bar, 1);
+      misc[0] = 0u; misc[1] = 0u; misc[2] = 0u;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -174,7 +195,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
   const int n_vctas = n_vp == 0 ? 0 : min((int)gridDim.x, (n_vp + kDecodeWarps * kVPerWarp - 1) / (kDecodeWarps * kVPerWarp));
   const int n_vwarps = n_vctas * kDecodeWarps;            // v_done target
 
-  if (warp == kDecodeWarps + 1) {
+  if (warp == kProdWarp) {
     // ======================= producer warp =======================
     // Lane w issues tile warp w's ring: its V pieces, then blocks of up to kRPB consecutive records of
     // each row-block share (warp_share), each into the next slot once the tile warp released it
@@ -220,13 +241,20 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
         bulk_copy(wbufs + slot * kBlk, src, bytes, &wfull[slot], pol_w);
         if (++slot == kNBuf) { slot = 0; ++round; }
       }
+      if (!a.pf_at_start) prefetch_next_window(a, lane, kDecodeWarps);
+    } else if (a.pf_at_start) {
+      prefetch_next_window(a, lane - kDecodeWarps, 32 - kDecodeWarps);
     }
     return;
   }
 
-  if (warp == kEpi) {
-    // ======================= epilogue warp =======================
-    if (lane == 0) dtrace(a, 0);
+  if (warp >= kDecodeWarps) {
+    // ======================= epilogue warps =======================
+    // warp e takes the CTA's items k = e, e + kEpiWarps, ... (item parity = reduction buffer = e when 2 warps)
+    const int e_w = warp - kDecodeWarps;
+    uint4* tsm = tsm_all + (size_t)e_w * a.n_chunks * NB8 * 32;
+    uint16_t* xt = xt_all + 256 * e_w;
+    if (lane == 0 && e_w == 0) dtrace(a, 0);
     auto prefetch_u = [&](int rb, int par) {   // U fragments of a row-block item -> ubuf[par]
       if (rb >= n_items) return;
       const DMember& m = a.m[member_of_rb(a, rb)];
@@ -259,17 +287,35 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
                     (uint32_t)nc * 512u, fb, evict_first_policy());
       }
     };
-    prefetch_u(blockIdx.x, 0);                           // weights: before the PDL wait
-    prefetch_fwd(blockIdx.x, 0);
-    dep_wait(a, lane);
-    if (blockIdx.x == 0 && a.clr_max)                    // the max buffer the next window publishes into (R20)
+    // warm the SM's constant cache with every line of the kernel parameters (the member table is indexed
+    // dynamically on the t / epilogue critical path; a constant-cache miss there costs an L2 round trip under
+    // the weight stream), while the window still waits for its producer
+    if (lane * 64 < (int)sizeof(DArgs)) {
+      const uint32_t v = reinterpret_cast<const uint32_t*>(&a)[lane * 16];
+      asm volatile("" ::"r"(v));
+    }
+    const int item0 = blockIdx.x + e_w * (int)gridDim.x;
+    prefetch_u(item0, e_w);                              // weights: before the PDL wait
+    prefetch_fwd(item0, e_w);
+    // dependency: warp 0 acquires the producer's counter (or waits on the grid dependency); the other epilogue
+    // warp waits on warp 0's mbarrier arrive (cumulative, like the tile warps' dbar) instead of polling the
+    // producer's counter a second time
+    if (e_w == 0) {
+      dep_wait(a, lane);
+      if (kEpiWarps > 1 && a.dep_cnt && lane == 0) mbar_arrive(e2bar);
+    } else if (!a.dep_cnt) {
+      dep_wait(a, lane);
+    } else {
+      while (!mbar_try_wait(e2bar, 0)) {}
+    }
+    if (e_w == 0 && blockIdx.x == 0 && a.clr_max)        // the max buffer the next window publishes into (R20)
       for (int i = lane; i < a.clr_n; i += 32) a.clr_max[i] = 0u;
     // release the tile warps: one mbarrier arrive after the acquire (cumulative through the mbarrier's
     // release / acquire); the tile warps read activations only after their wait on it
-    if ((!XS || I8) && a.dep_cnt && lane == 0) mbar_arrive(dbar);
-    if (lane == 0) dtrace(a, 1);
+    if ((!XS || I8) && a.dep_cnt && lane == 0 && e_w == 0) mbar_arrive(dbar);
+    if (lane == 0 && e_w == 0) dtrace(a, 1);
     if constexpr (XS && !I8) {
-      if (lane == 0) {
+      if (lane == 0 && e_w == 0) {
         mbar_expect_tx(xbar, (uint32_t)(a.B * a.K * 2));
         for (int b = 0; b < a.B; ++b)
           bulk_copy(xs + (size_t)b * xs_ld, a.x + (size_t)b * a.ldx, (uint32_t)(a.K * 2), xbar, evict_last_policy());
@@ -280,27 +326,32 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
     bool t_ready = false;
     bool t_deep = false;   // the extra-tier flag of this window's t (read with t; reset on the exit path)
     int my_rb = 0;
-    int k = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++k) {
+    int k = e_w;
+    for (int item = item0; item < n_items; item += kEpiWarps * (int)gridDim.x, k += kEpiWarps) {
       const int par = k & 1;
       const DMember& m = a.m[member_of_rb(a, item)];
       const int r_eff = a.glue ? max(a.m[0].r, a.m[1].r) : m.r;
       if (!t_ready && r_eff > 0) {
         // once per CTA, while the tile warps still stream: acquire t (all tile warps of the grid
-        // have added their V·x shares) and keep its fragments in smem as fp32
+        // have added their V·x shares) and keep its fragments in smem (each epilogue warp its own copy)
+        unsigned seen = 0;
         if (lane == 0 && n_vctas > 0) {                 // t_in: ordered by the dependency wait already
 #if HC_POLL_RELAXED
           while (ld_relaxed(&a.cnt[0]) < (unsigned)n_vctas) __nanosleep(32);
-          (void)ld_acquire(&a.cnt[0]);
+          seen = ld_acquire(&a.cnt[0]);
 #else
-          while (ld_acquire(&a.cnt[0]) < (unsigned)n_vctas) __nanosleep(32);
+          while ((seen = ld_acquire(&a.cnt[0])) < (unsigned)n_vctas) __nanosleep(32);
 #endif
+          if (e_w == 0) dtrace(a, 11);                   // v_done observed
         }
-        __syncwarp();
-        // t as bf16 hi + lo B-fragments of the U·t mma (fp32-accurate), ranks >= r masked to 0.  Tier 0 only
-        // (R22); the extra-tier flag is loaded first and consumed after the loop, and the rare extra-tier
-        // pass is out of line.  No branch may sit between the loads of this loop (a branch inside the
-        // unrolled loop serialises them into one L2 round trip per chunk: +2.5 µs on C1).
+        // the t loads below are plain (non-volatile) asm so that they batch: their addresses carry a data
+        // dependency on the acquired counter value so the compiler cannot move them above the acquire
+        __syncwarp();                                    // orders every lane's t loads after lane 0's acquire
+        const long long* tq = a.tacc + zero_dep(__shfl_sync(0xFFFFFFFFu, seen, 0));
+        // t as bf16 hi + lo B-fragments of the U·t mma (fp32-accurate), ranks >= r masked to 0.  Tier 0 here, each
+        // lane loading the words of its own fragments (R22); the extra-tier flag is loaded first and consumed after
+        // the loop.  No branch may sit between the loads of this loop (a branch inside the unrolled loop
+        // serialises them into one L2 round trip per chunk: +2.5 µs on C1).
         t_deep = __ldcg(a.tacc + (size_t)kTCopies * a.n_chunks * kTChunk) != 0;
 #pragma unroll 4
         for (int cc = 0; cc < a.n_chunks; ++cc) {
@@ -311,12 +362,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
             const long long* src = a.tacc + (size_t)cc * kTChunk + ((gid + 8 * nb) & 15) * 16 + 2 * tig;
             // only the lanes of batch columns < B load (the others' words are zero): predicated, not branched
             const bool on = gid + 8 * nb < a.B;
-            long long tr[4] = {ldcg_if(src, on), ldcg_if(src + 1, on), ldcg_if(src + 8, on), ldcg_if(src + 9, on)};
-#pragma unroll
-            for (int c = 1; c < kTCopies; ++c) {           // the copies (integer sums: exact, order-free)
-              const long long* sc = src + (size_t)c * a.n_chunks * kTChunk;
-              tr[0] += ldcg_if(sc, on); tr[1] += ldcg_if(sc + 1, on); tr[2] += ldcg_if(sc + 8, on); tr[3] += ldcg_if(sc + 9, on);
-            }
+            const long long tr[4] = {ldcg_if(src, on), ldcg_if(src + 1, on), ldcg_if(src + 8, on), ldcg_if(src + 9, on)};
             uint32_t hi[2], lo[2];
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
@@ -333,11 +379,16 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
             tsm[((size_t)cc * NB8 + nb) * 32 + lane] = make_uint4(hi[0], hi[1], lo[0], lo[1]);
           }
         }
-        // rare: outlier or tiny activations (R22); fp8 factors (u_scale folded into t)
-        if (t_deep) t_fragments_full<NB8>(a, tsm, lane, true);
+        if (lane == 0 && e_w == 0) dtrace(a, 13);
+        // rare (outlier or tiny activations, R22): every tier, all loads of the pass in flight together
+        if (t_deep) {
+          t_fragments_deep_load<NB8>(a, tq, tsm, lane);
+          t_fragments_build<NB8>(a, tsm, lane);
+        }
+        if (lane == 0 && e_w == 0) dtrace(a, 14);
         __syncwarp();
         t_ready = true;
-        if (lane == 0) dtrace(a, 5);
+        if (lane == 0 && e_w == 0) dtrace(a, 5);
       }
       // t forwarding: this item's outputs are x of the next window at k = n0 - fwd_lo .. (16 or 8 of them);
       // fetch the next window's natural-k V fragments of that 16-k block while the tile warps work
@@ -346,7 +397,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
       const int oc0 = (a.npeer > 1 ? m.full_off : m.row_off) + (item - m.rb_begin) * (a.glue ? 8 : kRows);
       const int f_n0 = oc0;
       const bool f_on = a.fwd && f_n0 >= a.fwd_lo && f_n0 < a.fwd_hi;
-      prefetch_fwd(item + (int)gridDim.x, (k + 1) & 1);     // the next item's Vn block (this one's is in flight)
+      if (kEpiWarps == 1) prefetch_fwd(item + (int)gridDim.x, (k + 1) & 1);   // the next item's Vn block (this one's is in flight)
       // ---- independent of the tile warps (so done before waiting for their partial sums): U[:, :r]·t
       // (U prefetched one item ahead) and the residual (its producer window is >= 2 windows back,
       // complete once this window's dependency was met)
@@ -403,7 +454,8 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
         reinterpret_cast<uint4*>(xt)[lane] = make_uint4(0u, 0u, 0u, 0u);
         __syncwarp();
       }
-      asm volatile("bar.sync %0, %1;" ::"r"(1 + par), "n"(kDecodeThreads) : "memory");   // FULL[par]
+      const int rs = k % kRedSlots;                      // reduction slot of this item
+      asm volatile("bar.sync %0, %1;" ::"r"(red_full_id(rs)), "n"(kDecodeThreads) : "memory");   // FULL[rs]
       if (lane == 0) { if (k == 0) dtrace(a, 2); if (item + (int)gridDim.x >= n_items) dtrace(a, 3); }
       float fin[NB8][4];
 #pragma unroll
@@ -412,16 +464,17 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
         for (int e = 0; e < 4; ++e) fin[nb][e] = 0.f;
 #pragma unroll
       for (int w = 0; w < kDecodeWarps; ++w) {            // fixed order: deterministic
-        const float* src = red + ((size_t)(par * kDecodeWarps + w) * 32 + lane) * 4 * NB8;
+        const float* src = red + ((size_t)(rs * kDecodeWarps + w) * 32 + lane) * 4 * NB8;
 #pragma unroll
         for (int nb = 0; nb < NB8; ++nb) {
           const float4 v = *reinterpret_cast<const float4*>(src + 4 * nb);
           fin[nb][0] += v.x; fin[nb][1] += v.y; fin[nb][2] += v.z; fin[nb][3] += v.w;
         }
       }
-      if (item + 2 * (int)gridDim.x < n_items)
-        asm volatile("bar.arrive %0, %1;" ::"r"(3 + par), "n"(kDecodeThreads) : "memory");   // EMPTY[par]
-      prefetch_u(item + gridDim.x, par ^ 1);
+      if (item + kRedSlots * (int)gridDim.x < n_items)
+        asm volatile("bar.arrive %0, %1;" ::"r"(red_empty_id(rs)), "n"(kDecodeThreads) : "memory");   // EMPTY[rs]
+      if (kEpiWarps == 1) prefetch_u(item + gridDim.x, par ^ 1);
+      else prefetch_u(item + kEpiWarps * (int)gridDim.x, par);   // this warp's next item (its U·t is done)
 
       uint32_t xm[NB8][2];                               // largest |bf16 y| per batch row (x' range, R20)
 #pragma unroll
@@ -536,12 +589,21 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
         }
         __syncwarp();                                    // fbuf / xt reused by the next item
       }
+      if (kEpiWarps > 1) prefetch_fwd(item + kEpiWarps * (int)gridDim.x, par);   // this warp's buffer is free again
       ++my_rb;
     }
-    if (lane == 0) dtrace(a, 4);
+    if (lane == 0 && e_w == 0) dtrace(a, 4);
     // one counter update per CTA: the CTA completing the last row block resets t and the counters
     // (every t reader is a row-block epilogue, all of which have finished by then)
     __syncwarp();
+    if constexpr (kEpiWarps > 1) {
+      // the epilogue warps meet (named barrier 6); warp 0 publishes the CTA's row blocks (cumulativity through
+      // the barrier orders warp 1's output stores before warp 0's release)
+      if (e_w == 1 && lane == 0) misc[2] = (unsigned)my_rb;
+      asm volatile("bar.sync 6, %0;" ::"n"(kEpiWarps * 32) : "memory");
+      if (e_w != 0) return;
+      my_rb += (int)misc[2];
+    }
     unsigned last = 0;
     if (lane == 0 && my_rb > 0) {
       const unsigned old = add_acq_rel(&a.cnt[1], (unsigned)my_rb);
@@ -652,6 +714,7 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
         while (!mbar_try_wait(&bars[s], ph)) {}
         v_tile<NB8>(bufs + s * kBlk, lane, xv, tp);
       }
+      if (vp == vp0 && warp == 0 && lane == 0) dtrace(a, 9);     // first V piece contracted (x loaded)
       advance();
     }
     if (cc_cur >= 0) flush(cc_cur);
@@ -660,7 +723,11 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
     // v_done counts CTAs: the CTA's V warps meet at a named barrier, then one release add orders all
     // of their t adds before it (cumulativity through the barrier)
     asm volatile("bar.sync 7, %0;" ::"n"(kDecodeWarps * 32) : "memory");
-    if (warp == 0 && lane == 0) add_release(&a.cnt[0], 1u);
+    if (warp == 0 && lane == 0) {
+      dtrace(a, 10);                                     // the CTA's V warps flushed their t atomics
+      add_release(&a.cnt[0], 1u);
+      dtrace(a, 12);
+    }
   }
   if constexpr (I8) {
     // x (L2) -> int8 digits (smem) of this warp's groups (the same for every item: warp_share)
@@ -778,20 +845,21 @@ __global__ void __launch_bounds__(kDecodeBlock, HC_DEC_MINB) decode_kernel(const
     }
     if constexpr (I8) i8_finish(*reinterpret_cast<float(*)[1][4]>(&tot[0][0]), lane, a.B);
     // ---- hand the partial sums to the epilogue warp
-    if (k >= 2) asm volatile("bar.sync %0, %1;" ::"r"(3 + par), "n"(kDecodeThreads) : "memory");   // EMPTY[par]
-    float* rb_ = red + ((size_t)(par * kDecodeWarps + warp) * 32 + lane) * 4 * NB8;
+    const int rs = k % kRedSlots;
+    if (k >= kRedSlots) asm volatile("bar.sync %0, %1;" ::"r"(red_empty_id(rs)), "n"(kDecodeThreads) : "memory");   // EMPTY[rs]
+    float* rb_ = red + ((size_t)(rs * kDecodeWarps + warp) * 32 + lane) * 4 * NB8;
 #pragma unroll
     for (int nb = 0; nb < NB8; ++nb)
       *reinterpret_cast<float4*>(rb_ + 4 * nb) = make_float4(tot[nb][0], tot[nb][1], tot[nb][2], tot[nb][3]);
-    asm volatile("bar.arrive %0, %1;" ::"r"(1 + par), "n"(kDecodeThreads) : "memory");            // FULL[par]
+    asm volatile("bar.arrive %0, %1;" ::"r"(red_full_id(rs)), "n"(kDecodeThreads) : "memory");    // FULL[rs]
   }
 }
 
 static size_t decode_smem_bytes(bool xs, bool i8, int B, int K, int n_chunks, int fwd_chunks) {
   const int nb8 = B > 8 ? 2 : 1;
-  size_t s = (size_t)kDecodeWarps * kNBuf * kTPB * kTileMax + 2 * kDecodeWarps * 32 * 4 * nb8 * sizeof(float) +
-             2 * kUPre * 32 * 16 + (2 * kDecodeWarps * kNBuf + 6) * sizeof(uint64_t) +
-             (size_t)n_chunks * nb8 * 32 * 16 + 512 + (size_t)fwd_chunks * 1024;
+  size_t s = (size_t)kDecodeWarps * kNBuf * kTPB * kTileMax + kRedSlots * kDecodeWarps * 32 * 4 * nb8 * sizeof(float) +
+             2 * kUPre * 32 * 16 + (2 * kDecodeWarps * kNBuf + 8) * sizeof(uint64_t) +
+             (size_t)dec_epi_warps(i8) * (n_chunks * nb8 * 32 * 16 + 512) + (size_t)fwd_chunks * 1024;
   s += 16;                                                                 // misc
   if (i8) s += (size_t)(K / kGroup) * x8_stride(B) + kX8Pad;
   else if (xs) s += (size_t)(((K / kGroup) * B + 3) & ~3) * 4 + (size_t)B * (K + 32) * 2;   // 2^σ [G][B] + x'
@@ -877,7 +945,7 @@ static cudaError_t launch_tf(const DArgs& a, int grid, cudaStream_t st) {
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kDecodeBlock);
+  cfg.blockDim = dim3(dec_block(I8));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
@@ -901,8 +969,8 @@ static int max_ctas_t(int B, int K, int n_chunks, int fwd_chunks) {
   cudaFuncSetAttribute(decode_kernel<BITS, NB8, XS, I8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)kSmemOptin);
   int per_sm = 0, per_sm8 = 0, dev = 0, sms = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<BITS, NB8, XS, I8, false>, kDecodeBlock, smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm8, decode_kernel<BITS, NB8, XS, I8, true>, kDecodeBlock, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<BITS, NB8, XS, I8, false>, dec_block(I8), smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm8, decode_kernel<BITS, NB8, XS, I8, true>, dec_block(I8), smem);
   per_sm = per_sm < per_sm8 ? per_sm : per_sm8;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

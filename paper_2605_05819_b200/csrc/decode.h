@@ -7,8 +7,27 @@ namespace hc {
 
 constexpr int kMaxMembers = 4;
 constexpr int kDecodeWarps = 8;          // tile (streaming + contraction) warps per CTA
-constexpr int kDecodeThreads = (kDecodeWarps + 1) * 32;   // + one epilogue warp (named-barrier count)
-constexpr int kDecodeBlock = kDecodeThreads + 32;         // decode kernel: + one producer (TMA issue) warp
+#ifndef HC_DEC_EPI
+#define HC_DEC_EPI 3
+#endif
+// epilogue warps per CTA: item k of a CTA goes to epilogue warp k % epi (its own reduction buffer, U buffer, named
+// barriers FULL / EMPTY[k % 2] and t fragments), so the per-item epilogue work (reduction of the 8 partial sums,
+// U·t, output, t forwarding) of consecutive items runs in parallel.  HC_DEC_EPI = 1 or 2 everywhere; 3 (default):
+// two on the int8 path, one on the fp16 path (whose tile loop needs > 88 registers: a 12th warp would cap it there)
+constexpr int dec_epi_warps(bool i8) { return HC_DEC_EPI == 3 ? (i8 ? 2 : 1) : HC_DEC_EPI; }
+static_assert(HC_DEC_EPI >= 1 && HC_DEC_EPI <= 3, "HC_DEC_EPI: 1, 2 or 3");
+constexpr int kDecodeThreads = (kDecodeWarps + 1) * 32;   // tile warps + one epilogue warp (named-barrier count)
+#ifndef HC_DEC_RED
+#define HC_DEC_RED 2   // (4 measured neutral on C2 and it costs the 2-bit C5 windows their second CTA per SM)
+#endif
+// reduction slots: the tile warps run up to kRedSlots items ahead of the epilogue warps (item k -> slot k % kRedSlots),
+// so a window's weight stream continues while its first epilogues wait for t = V·x
+constexpr int kRedSlots = HC_DEC_RED;
+static_assert(kRedSlots == 2 || kRedSlots == 4, "2 or 4 reduction slots");
+// named barrier ids of slot s: FULL (tile warps arrive, the epilogue warp syncs), EMPTY (the reverse)
+__host__ __device__ constexpr int red_full_id(int s) { return s < 2 ? 1 + s : 6 + s; }    // 1, 2, 8, 9
+__host__ __device__ constexpr int red_empty_id(int s) { return s < 2 ? 3 + s : 8 + s; }   // 3, 4, 10, 11
+constexpr int dec_block(bool i8) { return (kDecodeWarps + dec_epi_warps(i8) + 1) * 32; }   // + the producer warp
 constexpr int kMaxChunks = 32;           // Σ ceil(r_m/16) over a window's members
 #ifndef HC_DEC_TPB
 #define HC_DEC_TPB 2
@@ -117,6 +136,17 @@ struct DArgs {
   unsigned* clr_max;
   int clr_n;
   float* xsig;          // x-prep launches (x16 given by launch_xprep): 2^σ per (group, batch row) [G][B]
+  // L2 prefetch of the next window's weight records (stack graphs, options().l2_prefetch): weights do not depend
+  // on activations, so while this window finishes (its tail, the next window's dependency wait and x staging)
+  // HBM keeps streaming the next window's records into L2.  CTA c prefetches next-window items c, c + grid, ...
+  // (at most pf_items of them; item = one row block's records, contiguous), issued by the producer warp once
+  // its own ring is fully issued (pf_at_start = 0) or by its spare lanes at kernel start (1).
+  int pf_items;
+  int pf_at_start;
+  int pf_nm;
+  const uint8_t* pf_rec[kMaxMembers];
+  int pf_rb_end[kMaxMembers];   // cumulative item counts of the next window's members
+  unsigned pf_item_bytes;       // G_next · rec_bytes(bits_next)
   long long* tacc;      // [n_chunks][16 batch][16 ranks][4 tiers] t = V·x in tiered fixed point (self-resetting)
   unsigned* cnt;        // [0] v_done (tile warps done with their V share), [1] w_done (row blocks)
 };

@@ -48,6 +48,9 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -288,47 +291,70 @@ __device__ __forceinline__ void tacc_add(long long* t, int n_chunks, int cc, int
     if (w != 0) t[(size_t)kTCopies * n_chunks * kTChunk] = 1;   // extra tiers in use (idempotent plain store)
   }
 }
-// t of (chunk cc, batch col) at ranks r0, r0 + 1: tier 0 (8-byte loads); XT: + tiers 1-3.  fp32 (no
-// fp64: its conversions are slow on the epilogue's critical path)
-template <bool XT>
-__device__ __forceinline__ void tacc_read2(const long long* t, int n_chunks, int cc, int col, int r0, float& ta, float& tb) {
-  ta = 0.f;
-  tb = 0.f;
-  for (int c = 0; c < kTCopies; ++c) {
-    const long long* tc = t + (size_t)c * n_chunks * kTChunk;
-    const long long* p = tc + tacc_idx(cc, 0, r0, col);
-    ta += (float)__ldcg(p) * 0x1p-36f;
-    tb += (float)__ldcg(p + 1) * 0x1p-36f;
-    if (XT) {
-      const long long *p1 = tc + tacc_idx(cc, 1, r0, col), *p2 = tc + tacc_idx(cc, 2, r0, col), *p3 = tc + tacc_idx(cc, 3, r0, col);
-      ta += fmaf((float)__ldcg(p1), 0x1p-12f, fmaf((float)__ldcg(p2), 0x1p-72f, (float)__ldcg(p3) * 0x1p-96f));
-      tb += fmaf((float)__ldcg(p1 + 1), 0x1p-12f, fmaf((float)__ldcg(p2 + 1), 0x1p-72f, (float)__ldcg(p3 + 1) * 0x1p-96f));
-    }
-  }
+// 0, computed from v by an opaque instruction: a data dependency on v that the compiler cannot fold
+__device__ __forceinline__ unsigned zero_dep(unsigned v) {
+  unsigned z;
+  asm("and.b32 %0, %1, 0;" : "=r"(z) : "r"(v));
+  return z;
 }
-// Out-of-line t fragment pass (DArgs::fp8 windows, and windows whose extra-tier flag is set, R22): rebuilds
-// tsm as the tier-0 pass of the epilogue does, with t = Σ tiers when xt, and t'_j = u_scale_j·t_j for fp8
-// factors (the U mma then multiplies the exact e4m3 values).
+// Predicated L2 load without a compiler barrier (the deep t pass: loads of several elements stay in flight together;
+// the data was ordered by the caller's acquire)
+__device__ __forceinline__ long long ldcg_if_nb(const long long* p, bool on) {
+  long long v;
+  asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n mov.b64 %0, 0;\n @q ld.global.cg.b64 %0, [%1];\n}"
+      : "=l"(v) : "l"(p), "r"((int)on));
+  return v;
+}
+// Extra-tier t pass (R22: the window's flag is set, outlier or tiny activations): the t fragments of the epilogue's
+// U·t mma are rebuilt from all four tiers.  Load: the 32 lanes convert distinct (chunk, live column, rank) elements
+// into fp32 scratch laid over the chunk's own fragment slots ([cc][col < 8·NB8][rank], exactly NB8 x 512 B), every
+// load in flight together (one L2 round trip for any chunk count); per element t = t0·2^-36 + (t1·2^-12 +
+// (t2·2^-72 + t3·2^-96)) in fp32.  Build (t_fragments_build), chunk by chunk: each lane reads its four values per
+// batch-column block, then the chunk's slots are overwritten with the fragments (ranks >= r masked; fp8 factors:
+// t'_j = u_scale_j·t_j).  tq = the accumulators, carrying a data dependency on the acquire (the loads are
+// non-volatile so that they batch).
 template <int NB8>
-__device__ __noinline__ void t_fragments_full(const DArgs& a, uint4* tsm, int lane, bool xt) {
+__device__ __forceinline__ void t_fragments_deep_load(const DArgs& a, const long long* tq, uint4* tsm, int lane) {
+  constexpr int kCol = 8 * NB8;
+  static_assert(kTCopies == 1, "extra-tier pass: one accumulator copy");
+  float* scr = reinterpret_cast<float*>(tsm);
+  __syncwarp();                                          // the tier-0 fragments are overwritten below
+  const int per = a.B * 16, n_el = a.n_chunks * per;     // only the B live columns (build reads zero for the others)
+#pragma unroll 4
+  for (int e = lane; e < n_el; e += 32) {
+    const int cc = e / per, rem = e - cc * per;          // rem = col · 16 + rank
+    const long long* p = tq + (size_t)cc * kTChunk + rem;
+    scr[cc * kCol * 16 + rem] = (float)ldcg_if_nb(p, true) * 0x1p-36f +
+                                fmaf((float)ldcg_if_nb(p + 256, true), 0x1p-12f,
+                                     fmaf((float)ldcg_if_nb(p + 512, true), 0x1p-72f,
+                                          (float)ldcg_if_nb(p + 768, true) * 0x1p-96f));
+  }
+  __syncwarp();
+}
+template <int NB8>
+__device__ __forceinline__ void t_fragments_build(const DArgs& a, uint4* tsm, int lane) {
   const int gid = lane >> 2, tig = lane & 3;
+  constexpr int kCol = 8 * NB8;
+  const float* scr = reinterpret_cast<const float*>(tsm);
   for (int cc = 0; cc < a.n_chunks; ++cc) {
     const DMember& mt = a.m[member_of_chunk(a, cc)];
     const int r0 = 16 * (cc - mt.chunk_begin) + 2 * tig;
+    float tr[NB8][4];
+#pragma unroll
     for (int nb = 0; nb < NB8; ++nb) {
-      float tr[4];
-      if (xt) {
-        tacc_read2<true>(a.tacc, a.n_chunks, cc, (gid + 8 * nb) & 15, 2 * tig, tr[0], tr[1]);
-        tacc_read2<true>(a.tacc, a.n_chunks, cc, (gid + 8 * nb) & 15, 2 * tig + 8, tr[2], tr[3]);
-      } else {
-        tacc_read2<false>(a.tacc, a.n_chunks, cc, (gid + 8 * nb) & 15, 2 * tig, tr[0], tr[1]);
-        tacc_read2<false>(a.tacc, a.n_chunks, cc, (gid + 8 * nb) & 15, 2 * tig + 8, tr[2], tr[3]);
-      }
+      const float* src = scr + (size_t)cc * kCol * 16 + (gid + 8 * nb) * 16 + 2 * tig;
+      const bool on = gid + 8 * nb < a.B;
+      tr[nb][0] = on ? src[0] : 0.f; tr[nb][1] = on ? src[1] : 0.f; tr[nb][2] = on ? src[8] : 0.f; tr[nb][3] = on ? src[9] : 0.f;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int nb = 0; nb < NB8; ++nb) {
       uint32_t hi[2], lo[2];
+#pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         const int ra = r0 + 8 * hh, rb = ra + 1;
-        float ta = ra < mt.r ? tr[2 * hh] : 0.f;
-        float tb = rb < mt.r ? tr[2 * hh + 1] : 0.f;
+        float ta = ra < mt.r ? tr[nb][2 * hh] : 0.f;
+        float tb = rb < mt.r ? tr[nb][2 * hh + 1] : 0.f;
         if (a.fp8) {
           ta *= ra < mt.r ? mt.us[ra] : 0.f;
           tb *= rb < mt.r ? mt.us[rb] : 0.f;
@@ -339,6 +365,7 @@ __device__ __noinline__ void t_fragments_full(const DArgs& a, uint4* tsm, int la
       }
       tsm[((size_t)cc * NB8 + nb) * 32 + lane] = make_uint4(hi[0], hi[1], lo[0], lo[1]);
     }
+    __syncwarp();
   }
 }
 // Reset what a launch with batch B wrote: tier 0 always, tiers 1-3 and the flag when `xt` (the flag as the
@@ -348,7 +375,8 @@ __device__ __forceinline__ void tacc_reset(long long* t, int n_chunks, int B, bo
   for (int i = lane; i < kTCopies * n_chunks * tiers * per; i += 32) {
     const int row = i / per;                             // (copy · n_chunks + chunk) · tiers + tier
     const int c = row / tiers, w = row - c * tiers;
-    t[(size_t)c * kTChunk + w * 256 + (i - row * per)] = 0;
+    const int j = i - row * per;                         // col · 16 + rank
+    t[(size_t)c * kTChunk + tacc_idx(0, w, j & 15, j >> 4)] = 0;
   }
   if (lane == 0 && xt) t[(size_t)kTCopies * n_chunks * kTChunk] = 0;
 }

@@ -55,7 +55,10 @@ __device__ __forceinline__ float pow2f(int e) { return __uint_as_float((uint32_t
 // k = 4l .. 4l + 3 of one (group, batch row).
 __device__ __forceinline__ void x8_stage(const DArgs& a, uint8_t* x8, int g0, int g1, int lane) {
   const int tig = (lane >> 1) & 3, s = lane >> 3, h = lane & 1;
-  constexpr int kPre = 1;                            // (measured: batching 8 pieces' loads was slower)
+#ifndef HC_X8PRE
+#define HC_X8PRE 1
+#endif
+  constexpr int kPre = HC_X8PRE;                     // (measured: batching 8 pieces' loads was slower)
   //                          // (group, batch row) pieces whose loads are in flight together
   for (int p0 = g0 * a.B; p0 < g1 * a.B; p0 += kPre) {
     // issue every load of the batch first: the staging is on the window's critical path and each load
@@ -63,14 +66,14 @@ __device__ __forceinline__ void x8_stage(const DArgs& a, uint8_t* x8, int g0, in
     uint2 rawv[kPre];
 #pragma unroll
     for (int u = 0; u < kPre; ++u) {
-      const int p = min(p0 + u, g1 * a.B - 1), g = p / a.B, b = p - g * a.B;
+      const int p = min(p0 + u, g1 * a.B - 1), g = a.B == 1 ? p : p >> 1, b = p - g * a.B;
       rawv[u] = __ldcg(reinterpret_cast<const uint2*>(a.x + (size_t)b * a.ldx + g * kGroup + 4 * lane));
     }
 #pragma unroll
   for (int uu = 0; uu < kPre; ++uu) {
     const int p = p0 + uu;
     if (p >= g1 * a.B) break;
-    const int g = p / a.B, b = p - g * a.B;
+    const int g = a.B == 1 ? p : p >> 1, b = p - g * a.B;   // the int8 path runs B <= 2
     const uint2 raw = rawv[uu];
     const uint32_t hb[4] = {raw.x & 0xFFFFu, raw.x >> 16, raw.y & 0xFFFFu, raw.y >> 16};
     uint32_t m = 0;
@@ -104,10 +107,8 @@ __device__ __forceinline__ void x8_stage(const DArgs& a, uint8_t* x8, int g0, in
       const uint32_t t = prmt(u[0], u[1], sel), v = prmt(u[2], u[3], sel);
       const uint32_t reg = prmt(t, v, 0x5140u) ^ 0x80808080u;   // [u0.d, u2.d, u1.d, u3.d] − 128 each
       reinterpret_cast<uint32_t*>(blk)[((4 * b + d) * 4 + tig) * 8 + 2 * s + h] = reg;
-      int sum = 0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) sum += (int)((u[i] >> (8 * d)) & 0xFFu) - 128;
-      dsum[d] = __reduce_add_sync(0xFFFFFFFFu, sum);
+      // Σ of this lane's four digits d: the s8 bytes of reg (one dp4a with ones instead of 4 extract-adds)
+      dsum[d] = __reduce_add_sync(0xFFFFFFFFu, __dp4a((int)reg, 0x01010101, 0));
     }
     if (lane < 2) {
       const int pp = lane;

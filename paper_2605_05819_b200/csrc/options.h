@@ -14,6 +14,8 @@ struct Options {
   int prefill_merge = 1;       // prefill: one GEMM over a multi-member window
   int decode_ctas_per_sm = 0;  // decode: cap on resident CTAs per SM (0 = occupancy limit)
   int pdl = 1;                 // decode: programmatic dependent launch between windows
+  int l2_prefetch = 0;         // stack: next-window record items each CTA prefetches into L2 (0 = off)
+  int l2_prefetch_at_start = 0;   // stack: issue them at kernel start (spare producer lanes) instead of after the ring
   unsigned epoch = 0;
 };
 

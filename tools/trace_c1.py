@@ -64,5 +64,6 @@ for i in range(1, len(used)):
     f = lambda ev, fn: fn(rel[:, ev])
     print(f"launch {i:2d} dur {end[i] - prev[i]:6.2f} | start {f(0, np.nanmin):6.2f}/{f(0, np.nanmax):6.2f}"
           f" | pdl {f(1, np.nanmin):6.2f}/{f(1, np.nanmax):6.2f} | 1stFULL {f(2, np.nanmin):6.2f}/{f(2, np.nanmedian):6.2f}/{f(2, np.nanmax):6.2f}"
+          f" | Vx {f(9, np.nanmax):6.2f} Vflush {f(10, np.nanmax):6.2f} rel {f(12, np.nanmax):6.2f} vdone {f(11, np.nanmin):6.2f}/{f(11, np.nanmax):6.2f} t0 {f(13, np.nanmin):6.2f}/{f(13, np.nanmax):6.2f} tb {f(14, np.nanmin):6.2f}/{f(14, np.nanmax):6.2f}"
           f" | t {f(5, np.nanmin):6.2f}/{f(5, np.nanmax):6.2f} | lastFULL {f(3, np.nanmedian):6.2f}/{f(3, np.nanmax):6.2f} | epi {f(4, np.nanmedian):6.2f}/{f(4, np.nanmax):6.2f}")
 ctx.close()

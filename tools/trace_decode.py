@@ -15,6 +15,8 @@ import paper_2605_05819_b200 as hc  # noqa: E402
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 c = bench.C2
 ranks = bench.c2_ranks(c)
+if os.environ.get("HC_TRACE_R0"):
+    ranks = {key: 0 for key in ranks}
 for kv in os.environ.get("HC_TRACE_OPTS", "").split():   # e.g. t_forward=1
     hc.set_option(kv.split("=")[0], int(kv.split("=")[1]))
 ctx = hc.Context(0)
@@ -45,5 +47,5 @@ for k in range(4):
     q = lambda ev, f: np.nanmean(f(rel[:, :, ev], axis=1))
     print(f"{names[k]:7s} win {np.mean(end[idx] - prev[idx]):6.2f} | start min {q(0, np.nanmin):6.2f} max {q(0, np.nanmax):6.2f}"
           f" | pdl {q(1, np.nanmin):6.2f}/{q(1, np.nanmax):6.2f} | 1stFULL {q(2, np.nanmin):6.2f}/{q(2, np.nanmedian):6.2f}/{q(2, np.nanmax):6.2f}"
-          f" | t {q(5, np.nanmin):6.2f}/{q(5, np.nanmax):6.2f} | stg {q(6, np.nanmedian):6.2f}->{q(8, np.nanmedian):6.2f}->{q(7, np.nanmedian):6.2f} | tpre {q(9, np.nanmedian):6.2f} tpass {q(10, np.nanmedian):6.2f} deep {np.mean(~np.isnan(rel[:, :, 11])):.2f} | lastFULL {q(3, np.nanmedian):6.2f}/{q(3, np.nanmax):6.2f} | epi {q(4, np.nanmedian):6.2f}/{q(4, np.nanmax):6.2f}")
+          f" | t {q(5, np.nanmin):6.2f}/{q(5, np.nanmax):6.2f} | stg {q(6, np.nanmedian):6.2f}->{q(8, np.nanmedian):6.2f}->{q(7, np.nanmedian):6.2f} | Vx {q(9, np.nanmedian):6.2f}/{q(9, np.nanmax):6.2f} Vflush {q(10, np.nanmedian):6.2f}/{q(10, np.nanmax):6.2f} rel {q(12, np.nanmax):6.2f} vdone {q(11, np.nanmin):6.2f}/{q(11, np.nanmedian):6.2f} t0 {q(13, np.nanmedian):6.2f} tdeep {q(14, np.nanmedian):6.2f} | lastFULL {q(3, np.nanmedian):6.2f}/{q(3, np.nanmax):6.2f} | epi {q(4, np.nanmedian):6.2f}/{q(4, np.nanmax):6.2f}")
 ctx.close()
