@@ -138,13 +138,18 @@ __global__ void moe_prep_kernel(const uint16_t* __restrict__ x, int ldx, int K, 
   if ((p & 7) == 0) xsig[(size_t)r * (K / kGroup) + (p >> 3)] = pow2i(sig);
 }
 
-// one block of 8 warps per (entry, member, 16-rank chunk); warp w takes k-blocks [w·KB/8, (w+1)·KB/8)
-// (4 in flight, independent loads), partials summed in a fixed order through shared memory
-__global__ void __launch_bounds__(256) moe_rank_proj_kernel(MoEWin w, MoERoute rt, int max_ent, int max_chunks,
+// one block of kRPW warps per (entry, member, 16-rank chunk); warp w takes k-blocks [w·KB/kRPW, (w+1)·KB/kRPW)
+// (up to 8 in flight, independent loads: the whole V slice of a job is requested in about one round trip),
+// partials summed in a fixed order through shared memory.  (8 warps with 4 loads in flight: 12.6 µs for the C3
+// UPGATE projection at T = 1, latency-bound on 18 CTAs.)
+// warps per rank-projection job: 16 when the jobs are few (T = 1: 18 CTAs, latency-bound; measured C3 T = 1
+// 545 -> 583 tokens/s), 8 when they fill the GPU (T = 256: 16 warps measured -3%)
+template <int kRPW>
+__global__ void __launch_bounds__(kRPW * 32) moe_rank_proj_kernel(MoEWin w, MoERoute rt, int max_ent, int max_chunks,
                                                             const uint16_t* __restrict__ xg, float* __restrict__ t) {
   asm volatile("griddepcontrol.wait;" ::: "memory");                 // PDL: the previous launch's outputs
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  __shared__ float part[8][32][8];
+  __shared__ float part[kRPW][32][8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
   const int job = blockIdx.x, per_ent = 2 * max_chunks;
   const int ent = job / per_ent, rem = job % per_ent, mb = rem / max_chunks, c = rem % max_chunks;
@@ -154,7 +159,7 @@ __global__ void __launch_bounds__(256) moe_rank_proj_kernel(MoEWin w, MoERoute r
   const int row0 = rt.ent_row0[ent], ncol = rt.ent_ncol[ent];
   const int cs = ex.rs[mb] / 16;
   const uint4* vn = ex.Vn[mb];
-  const int KB = w.K / 16, kb_lo = warp * KB / 8, kb_hi = (warp + 1) * KB / 8;
+  const int KB = w.K / 16, kb_lo = warp * KB / kRPW, kb_hi = (warp + 1) * KB / kRPW;
   const uint16_t* xr0[2];
   bool cv[2];
 #pragma unroll
@@ -163,8 +168,8 @@ __global__ void __launch_bounds__(256) moe_rank_proj_kernel(MoEWin w, MoERoute r
     cv[nb] = col < ncol;
     xr0[nb] = xg + (size_t)(row0 + (cv[nb] ? col : 0)) * w.K + 2 * tig;
   }
-  constexpr int U = 4;
-  float acc[U][2][4] = {};
+  constexpr int U = 4, NCH = 4;                          // loads in flight per warp, independent mma chains
+  float acc[NCH][2][4] = {};
   for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += U) {
     uint4 a4[U];
     uint32_t b[U][2][2];
@@ -183,14 +188,19 @@ __global__ void __launch_bounds__(256) moe_rank_proj_kernel(MoEWin w, MoERoute r
       if (kb0 + u >= kb_hi) break;
       const uint32_t af[4] = {a4[u].x, a4[u].y, a4[u].z, a4[u].w};
 #pragma unroll
-      for (int nb = 0; nb < 2; ++nb) mma16816(acc[u][nb], af, b[u][nb][0], b[u][nb][1]);
+      for (int nb = 0; nb < 2; ++nb) mma16816(acc[u % NCH][nb], af, b[u][nb][0], b[u][nb][1]);
     }
   }
 #pragma unroll
   for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
     for (int e = 0; e < 4; ++e)
-      part[warp][lane][4 * nb + e] = ((acc[0][nb][e] + acc[1][nb][e]) + acc[2][nb][e]) + acc[3][nb][e];
+      {
+        float v = acc[0][nb][e];
+#pragma unroll
+        for (int q = 1; q < NCH; ++q) v += acc[q][nb][e];
+        part[warp][lane][4 * nb + e] = v;
+      }
   __syncthreads();
   if (warp == 0) {
 #pragma unroll
@@ -198,7 +208,7 @@ __global__ void __launch_bounds__(256) moe_rank_proj_kernel(MoEWin w, MoERoute r
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         float v = 0.f;
-        for (int ww = 0; ww < 8; ++ww) v += part[ww][lane][4 * nb + e];   // fixed order
+        for (int ww = 0; ww < kRPW; ++ww) v += part[ww][lane][4 * nb + e];   // fixed order
         const int col = 2 * tig + (e & 1) + 8 * nb, rank = 16 * c + gid + 8 * (e >> 1);
         if (col < ncol && rank < ex.r[mb]) t[(size_t)(row0 + col) * w.t_ld + mb * (w.t_ld / 2) + rank] = v;
       }
@@ -209,15 +219,16 @@ __global__ void __launch_bounds__(256) moe_rank_proj_kernel(MoEWin w, MoERoute r
 // record's words are loaded while the current one is decoded (many warps per SM hide the rest).
 // KS: the item's K groups are split over the CTA's 4 warps (few items: routing of a handful of
 // tokens); else every warp owns whole items (many items).
+constexpr int kKSW = 4;   // K-split items: warps per CTA (8 measured slower: C3 T = 1 579 -> 463 tokens/s)
 template <int BITS, int NB8, bool KS>
-__global__ void __launch_bounds__(128) moe_gemv_warp_kernel(MoEWin w, MoERoute rt, const uint16_t* __restrict__ x16,
+__global__ void __launch_bounds__(KS ? kKSW * 32 : 128) moe_gemv_warp_kernel(MoEWin w, MoERoute rt, const uint16_t* __restrict__ x16,
                                                            const float* __restrict__ xsig, const float* __restrict__ t,
                                                            void* out) {
   asm volatile("griddepcontrol.wait;" ::: "memory");                 // PDL: the previous launch's outputs
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  // one (entry, row block) item per CTA; its K groups split over the 4 warps (each warp keeps one
+  // one (entry, row block) item per CTA; its K groups split over the kKSW warps (each warp keeps one
   // record in flight ahead of the one it decodes), partials summed in a fixed order by warp 0
-  __shared__ float red[KS ? 4 : 1][32][4 * NB8];
+  __shared__ float red[KS ? kKSW : 1][32][4 * NB8];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
   const long long n_items = (long long)(*rt.n_ent) * w.n_rb;
@@ -239,7 +250,7 @@ __global__ void __launch_bounds__(128) moe_gemv_warp_kernel(MoEWin w, MoERoute r
       const int col = gid + 8 * nb;
       xrow[nb] = x16 + (size_t)(row0 + (col < ncol ? col : 0)) * w.K + 8 * tig;
     }
-    const int g_lo = KS ? warp * w.G / 4 : 0, g_hi = KS ? (warp + 1) * w.G / 4 : w.G;
+    const int g_lo = KS ? warp * w.G / kKSW : 0, g_hi = KS ? (warp + 1) * w.G / kKSW : w.G;
     uint32_t wn[2 * BITS], swn;
     uint2 zzn;
     if (g_lo < g_hi) load_record<BITS>(rec0 + (size_t)g_lo * rec_bytes(BITS), lane, wn, swn, zzn);
@@ -283,7 +294,7 @@ __global__ void __launch_bounds__(128) moe_gemv_warp_kernel(MoEWin w, MoERoute r
           for (int e = 0; e < 4; ++e) {
             float v = red[0][lane][4 * nb + e];
 #pragma unroll
-            for (int q = 1; q < 4; ++q) v += red[q][lane][4 * nb + e];   // fixed order: deterministic
+            for (int q = 1; q < kKSW; ++q) v += red[q][lane][4 * nb + e];   // fixed order: deterministic
             tot[nb][e] = v;
           }
       }
@@ -422,7 +433,15 @@ cudaError_t moe_rank_proj(const MoEWin& w, const MoERoute& rt, int max_ent, cons
   const int max_chunks = w.t_ld / 32;
   const long long jobs = (long long)max_ent * 2 * max_chunks;
   if (jobs == 0) return cudaSuccess;
-  if (cudaError_t e = launch_pdl(moe_rank_proj_kernel, (unsigned)jobs, 256, 0, st, w, rt, max_ent, max_chunks, xg, t)) return e;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (jobs < 2LL * sms) {
+    if (cudaError_t e = launch_pdl(moe_rank_proj_kernel<16>, (unsigned)jobs, 16 * 32, 0, st, w, rt, max_ent, max_chunks, xg, t))
+      return e;
+  } else if (cudaError_t e = launch_pdl(moe_rank_proj_kernel<8>, (unsigned)jobs, 8 * 32, 0, st, w, rt, max_ent, max_chunks, xg, t)) {
+    return e;
+  }
   return cudaGetLastError();
 }
 
@@ -432,7 +451,7 @@ cudaError_t moe_gemv(const MoEWin& w, int bits, const MoERoute& rt, int max_ent,
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long items = (long long)max_ent * w.n_rb;           // at most
-  // few items (a handful of routed tokens): one item per CTA with K split over its 4 warps
+  // few items (a handful of routed tokens): one item per CTA with K split over its kKSW warps
   const bool ks = items <= 8LL * sms;
   const long long need = ks ? items : (items + 3) / 4;
   const unsigned grid = (unsigned)(need < 16LL * sms ? need : 16LL * sms);
@@ -440,8 +459,8 @@ cudaError_t moe_gemv(const MoEWin& w, int bits, const MoERoute& rt, int max_ent,
   cudaError_t e = cudaSuccess;
 #define HC_MOE_LAUNCH(B_)                                                                                       \
   if (ks) {                                                                                                     \
-    if (one) e = launch_pdl(moe_gemv_warp_kernel<B_, 1, true>, grid, 128, 0, st, w, rt, x16, xsig, t, out);                       \
-    else     e = launch_pdl(moe_gemv_warp_kernel<B_, 2, true>, grid, 128, 0, st, w, rt, x16, xsig, t, out);                       \
+    if (one) e = launch_pdl(moe_gemv_warp_kernel<B_, 1, true>, grid, kKSW * 32, 0, st, w, rt, x16, xsig, t, out);                \
+    else     e = launch_pdl(moe_gemv_warp_kernel<B_, 2, true>, grid, kKSW * 32, 0, st, w, rt, x16, xsig, t, out);                \
   } else {                                                                                                      \
     if (one) e = launch_pdl(moe_gemv_warp_kernel<B_, 1, false>, grid, 128, 0, st, w, rt, x16, xsig, t, out);                      \
     else     e = launch_pdl(moe_gemv_warp_kernel<B_, 2, false>, grid, 128, 0, st, w, rt, x16, xsig, t, out);                      \
