@@ -270,6 +270,8 @@ hc_status hc_calib_r_std(const int32_t* Ns, int32_t n_members, int32_t K, int32_
  *   "prefill_merge"      1  prefill: one GEMM over a multi-member window (§7.5)
  *   "decode_ctas_per_sm" 0  decode: cap on resident CTAs per SM (0 = the occupancy limit)
  *   "pdl"                1  decode: programmatic dependent launch between consecutive windows
+ *   "l2_prefetch"        0  stack: next-window record items each CTA prefetches into L2 (0 = off)
+ *   "l2_prefetch_at_start" 0  stack: issue those prefetches at kernel start instead of after the CTA's own ring
  * HC_ERR_CONFIG for an unknown name or a negative value.  Not thread-safe against concurrent launches. */
 hc_status hc_set_option(const char* name, int32_t value);
 hc_status hc_get_option(const char* name, int32_t* value);

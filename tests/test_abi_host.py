@@ -114,7 +114,7 @@ def test_options_roundtrip_and_errors():
     negative values are HC_ERR_CONFIG, and the defaults are the measured-best plan."""
     import paper_2605_05819_b200 as hc
     defaults = {"t_forward": 0, "x_handoff": 1, "dep_wait": 1, "int8_path": 1, "prefill_merge": 1,
-                "decode_ctas_per_sm": 0}
+                "decode_ctas_per_sm": 0, "pdl": 1, "l2_prefetch": 0, "l2_prefetch_at_start": 0}
     for name, d in defaults.items():
         assert hc.get_option(name) == d
         hc.set_option(name, 3)
