@@ -263,3 +263,26 @@ def test_high_rank_parity(hc, ctx, bits, B, r):
     assert rel_err(y, ref) <= 1e-5, rel_err(y, ref)
     ref_low = linear.compensated_linear(case, r // 2)
     assert rel_err(y, ref_low) > 10 * rel_err(y, ref)      # the top half of the ranks is really used
+
+
+@pytest.mark.parametrize("scale", [1.0, 1e-9, 1e9])
+@pytest.mark.parametrize("B", [1, 2])
+def test_int8_two_epilogue_warps_multi_item(hc, ctx, scale, B):
+    """Int8 path with several row-block items per CTA (decode grid capped at one CTA per SM): consecutive items
+    alternate between the two epilogue warps (own reduction slot, U buffer and t fragments).
+    Tiny / huge activations move the V·x partials out of tier 0 (below 2^-24 / above 2^12), so the lane-distributed
+    extra-tier t pass runs (R22; tier 1 holds partials up to 2^50).  Within the oracle bound, and bit-identical to the full-grid launch (items on other CTAs / warps)."""
+    case = synth.linear_case(70 + B, N=4096, K=512, bits=4, r_stored=32, B=B, zeros="asym")
+    xf = bf16_to_f64(case["x"]) * scale
+    case["x"] = f64_to_bf16_bits_rne(xf)
+    L = next_layer()
+    load(ctx, case, L, r=32)
+    ref = linear.compensated_linear(case, 32)
+    y_full = run(hc, ctx, L, case["x"], 4096)
+    hc.set_option("decode_ctas_per_sm", 1)
+    try:
+        y_one = run(hc, ctx, L, case["x"], 4096)
+    finally:
+        hc.set_option("decode_ctas_per_sm", 0)
+    assert row_rel(y_one, ref) <= 1e-5, row_rel(y_one, ref)
+    assert np.array_equal(y_one, y_full)

@@ -39,6 +39,20 @@ for bits, B, K in ((4, 1, 512), (3, 4, 512), (4, 16, 384), (2, 2, 1280)):
     torch.cuda.synchronize()
     check(y.cpu().numpy(), linear.compensated_linear(c, 32), 1e-5, f"decode bits {bits} B {B} K {K}")
     L += 1
+# int8 path with several items per CTA (both epilogue warps: items alternate between them) and the extra-tier t
+# pass (tiny activations put the V·x partials below 2^-24): decode grid capped at one CTA per SM
+hc.set_option("decode_ctas_per_sm", 1)
+for scale, tag in ((1.0, "int8 multi-item"), (1e-9, "int8 multi-item, extra-tier t")):
+    c = synth.linear_case(30, N=4096, K=512, bits=4, r_stored=32, B=1, zeros="asym")
+    xb = (c["x"].astype(np.uint32) << 16).view(np.float32) * np.float32(scale)
+    c["x"] = (xb.view(np.uint32) >> 16).astype(np.uint16)          # exact: a power-of-ten scale of bf16 values, truncated
+    ctx.load_layer([desc(c, L, 0, 0, 32)])
+    y = torch.empty((1, 4096), dtype=torch.float32, device="cuda")
+    ctx.compensated_linear(L, 0, dev(c["x"]), y)
+    torch.cuda.synchronize()
+    check(y.cpu().numpy(), linear.compensated_linear(c, 32), 1e-5, tag)
+    L += 1
+hc.set_option("decode_ctas_per_sm", 0)
 # fused SiLU + fp8 factors
 up = synth.linear_case(40, N=128, K=256, bits=4, r_stored=16, B=2, zeros="asym", unit_gain=True)
 gate = synth.linear_case(41, N=128, K=256, bits=4, r_stored=16, B=2, zeros="asym", unit_gain=True)
