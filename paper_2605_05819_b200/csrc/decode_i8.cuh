@@ -56,10 +56,9 @@ __device__ __forceinline__ float pow2f(int e) { return __uint_as_float((uint32_t
 __device__ __forceinline__ void x8_stage(const DArgs& a, uint8_t* x8, int g0, int g1, int lane) {
   const int tig = (lane >> 1) & 3, s = lane >> 3, h = lane & 1;
 #ifndef HC_X8PRE
-#define HC_X8PRE 1
+#define HC_X8PRE 4
 #endif
-  constexpr int kPre = HC_X8PRE;                     // (measured: batching 8 pieces' loads was slower)
-  //                          // (group, batch row) pieces whose loads are in flight together
+  constexpr int kPre = HC_X8PRE;   // pieces whose loads are in flight together (round 2: 4 measured C2 r = 0 794 -> 817, C5 110.9 -> 112.6, C2 at allocated ranks ±0; round 1: 8 slower)
   for (int p0 = g0 * a.B; p0 < g1 * a.B; p0 += kPre) {
     // issue every load of the batch first: the staging is on the window's critical path and each load
     // is an L2 round trip (the x of this window was just written by its producer)
