@@ -376,9 +376,7 @@ __global__ void __launch_bounds__(dec_block(I8), HC_DEC_MINB) decode_kernel(cons
                   ta *= mt.us[min(r0 + 8 * hh, mt.r_stored - 1)];
                   tb *= mt.us[min(r0 + 8 * hh + 1, mt.r_stored - 1)];
                 }
-                const uint32_t ha = f32_to_bf16_rn(ta), hb = f32_to_bf16_rn(tb);
-                hi[hh] = ha | (hb << 16);
-                lo[hh] = f32_to_bf16_rn(ta - bf16_bits_to_f32(ha)) | (f32_to_bf16_rn(tb - bf16_bits_to_f32(hb)) << 16);
+                t_hi_lo(ta, tb, hi[hh], lo[hh]);
               }
               tsm[((size_t)cc * NB8 + nb) * 32 + lane] = make_uint4(hi[0], hi[1], lo[0], lo[1]);
             }

@@ -144,6 +144,14 @@ __device__ __forceinline__ uint32_t f32_to_bf16_rn(float f) {
   __nv_bfloat16 b = __float2bfloat16_rn(f);
   return (uint32_t)(*reinterpret_cast<uint16_t*>(&b));
 }
+// t as a bf16 hi + lo pair per value (fp32-accurate B operand of the U·t mma), two values per register: one packed
+// RN conversion per pair (F2FP) instead of two; a in the low half, b in the high half
+__device__ __forceinline__ void t_hi_lo(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  const __nv_bfloat162 l = __floats2bfloat162_rn(a - bf16_bits_to_f32(hi & 0xFFFFu), b - bf16_bits_to_f32(hi >> 16));
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
 
 // (a & b) | c in one LOP3 (nvcc otherwise emits two)
 __device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t b, uint32_t c) {
@@ -359,9 +367,7 @@ __device__ __forceinline__ void t_fragments_build(const DArgs& a, uint4* tsm, in
           ta *= ra < mt.r ? mt.us[ra] : 0.f;
           tb *= rb < mt.r ? mt.us[rb] : 0.f;
         }
-        const uint32_t ha = f32_to_bf16_rn(ta), hb = f32_to_bf16_rn(tb);
-        hi[hh] = ha | (hb << 16);
-        lo[hh] = f32_to_bf16_rn(ta - bf16_bits_to_f32(ha)) | (f32_to_bf16_rn(tb - bf16_bits_to_f32(hb)) << 16);
+        t_hi_lo(ta, tb, hi[hh], lo[hh]);
       }
       tsm[((size_t)cc * NB8 + nb) * 32 + lane] = make_uint4(hi[0], hi[1], lo[0], lo[1]);
     }

@@ -331,9 +331,7 @@ __global__ void __launch_bounds__(KS ? kKSW * 32 : 128) moe_gemv_warp_kernel(MoE
             const int rk = 16 * c + 2 * tig + 8 * hh;
             const float ta = (col < ncol && rk < rlim) ? tr[rk] : 0.f;
             const float tb = (col < ncol && rk + 1 < rlim) ? tr[rk + 1] : 0.f;
-            const uint32_t ha = f32_to_bf16_rn(ta), hb = f32_to_bf16_rn(tb);
-            hi[hh] = ha | (hb << 16);
-            lo[hh] = f32_to_bf16_rn(ta - bf16_bits_to_f32(ha)) | (f32_to_bf16_rn(tb - bf16_bits_to_f32(hb)) << 16);
+            t_hi_lo(ta, tb, hi[hh], lo[hh]);
           }
           mma16816(comp[h][nb], af, hi[0], hi[1]);
           mma16816(comp[h][nb], af, lo[0], lo[1]);
